@@ -1,0 +1,219 @@
+/*
+ * caffe_b200.h -- C ABI of the B200-native Caffe convolution hot path.
+ *
+ * The paper (arXiv 1408.5093, /root/reference/PAPER.md = P:n) defines a layer
+ * as "a forward pass that takes the inputs and produces the outputs, and a
+ * backward pass that takes the gradient with respect to the output, and
+ * computes the gradients with respect to the parameters and to the inputs"
+ * (Sec. 3.2) over 4-D blobs (num, channels, height, width) (P:141-147,
+ * Sec. 3.1).  The layer formulas follow SPEC.md (S:n) lines cited per call;
+ * the readings R1..R20 are listed in DESIGN.md.
+ *
+ * General conventions (apply to every call):
+ *  - Pointers inside caffe_blob and the float/int scalars marked "device" are
+ *    DEVICE pointers (cudaMalloc / torch allocations on the current device).
+ *    Pointers marked "host" are host pointers.  The caller owns every buffer;
+ *    the library never allocates device memory and never synchronizes
+ *    ("reserves exactly as much memory as needed").
+ *  - Blobs are contiguous row-major NCHW: index ((n*C+c)*H+h)*W+w.
+ *  - Asynchrony: CAFFE_OK means the work was ENQUEUED on `stream`.  Kernel
+ *    launch failures return CAFFE_E_CUDA.  A NULL stream is the legacy
+ *    default stream.
+ *  - Errors: all validation is host-only and happens before any launch; on
+ *    any error nothing is written.  caffe_last_error() returns a thread-local
+ *    message naming the offending argument.
+ *  - n == 0 is a no-op returning CAFFE_OK; any other zero axis is
+ *    CAFFE_E_SHAPE.
+ *  - In-place (aliasing input and output) is allowed only where stated
+ *    (ReLU); other overlaps return CAFFE_E_ALIAS.
+ *  - Determinism: for fixed inputs, configuration and device the outputs are
+ *    bitwise reproducible run to run.  No floating-point atomics.
+ *  - Math modes: CAFFE_MATH_FP32 = CUDA-core FP32 FMA reference kernels;
+ *    CAFFE_MATH_BF16 / CAFFE_MATH_TF32 = sm_100a tcgen05 tensor-core
+ *    implicit GEMM with FP32 accumulation in TMEM.  Operands are rounded
+ *    (RNE) to bf16 / tf32 before the MMA (reading R12).  TF32 with BF16
+ *    storage is CAFFE_E_DTYPE.
+ */
+#ifndef CAFFE_B200_H_
+#define CAFFE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* caffe_stream_t; /* == cudaStream_t */
+
+#define CAFFE_ABI_VERSION 1
+
+typedef enum {
+    CAFFE_OK = 0,
+    CAFFE_E_INVALID = 1,   /* NULL pointer, bad enum, missing required argument */
+    CAFFE_E_SHAPE = 2,     /* inconsistent or zero (non-batch) dimensions */
+    CAFFE_E_PARAM = 3,     /* bad layer parameter (kernel > padded input, even LRN size, C%group...) */
+    CAFFE_E_DTYPE = 4,     /* unsupported dtype combination */
+    CAFFE_E_ALIGN = 5,     /* pointer not 16-byte aligned (tensor-core paths) */
+    CAFFE_E_WORKSPACE = 6, /* workspace missing or smaller than caffe_*_workspace_size */
+    CAFFE_E_ALIAS = 7,     /* forbidden overlap between input and output buffers */
+    CAFFE_E_CUDA = 8,      /* CUDA runtime/driver error (launch failure, no device) */
+    CAFFE_E_ARCH = 9       /* device is not sm_100 */
+} caffe_status;
+
+typedef enum { CAFFE_F32 = 0, CAFFE_BF16 = 1, CAFFE_I32 = 2 } caffe_dtype;
+
+typedef enum { CAFFE_MATH_FP32 = 0, CAFFE_MATH_TF32 = 1, CAFFE_MATH_BF16 = 2 } caffe_math;
+
+typedef struct { int32_t n, c, h, w; } caffe_shape4;
+
+typedef struct {
+    void* ptr;          /* device pointer, contiguous NCHW */
+    caffe_shape4 shape;
+    caffe_dtype dtype;
+} caffe_blob;
+
+#define CAFFE_FUSE_RELU 1u /* conv/ip forward: apply max(0, .) in the epilogue */
+
+typedef struct {
+    int32_t kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w, group;
+    caffe_math math;
+    uint32_t flags; /* CAFFE_FUSE_RELU */
+} caffe_conv_desc;
+
+typedef enum { CAFFE_POOL_MAX = 0, CAFFE_POOL_AVE = 1 } caffe_pool_method;
+
+typedef struct {
+    int32_t method; /* caffe_pool_method */
+    int32_t kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w;
+} caffe_pool_desc;
+
+typedef struct {
+    int32_t local_size; /* odd, >= 1 */
+    float alpha, beta, k;
+} caffe_lrn_desc;
+
+typedef enum { CAFFE_PASS_FORWARD = 0, CAFFE_PASS_BACKWARD_DATA = 1, CAFFE_PASS_BACKWARD_WEIGHT = 2 } caffe_pass;
+
+/* ------------------------------------------------------------------ library */
+int32_t caffe_abi_version(void);
+/* Thread-local text of the last error returned on this thread ("" if none). */
+const char* caffe_last_error(void);
+/* Checks that a CUDA device of compute capability 10.0 is current. */
+caffe_status caffe_device_check(void);
+
+/* ------------------------------------------------------------------ convolution
+ * Convolution with groups, stride and zero padding (S:145 + reading R3):
+ *   top[n,o,y,x] = bias[o] + sum_{c'<C/g,i<kh,j<kw} W[o,c',i,j] *
+ *                  bottom[n, (o/(O/g))*(C/g)+c', y*sh-ph+i, x*sw-pw+j]
+ * Output size floor((H+2p-k)/s)+1.  Weight blob shape (O, C/g, kh, kw).
+ */
+
+/* top shape (host out) for a bottom shape and num_output.  E_PARAM if the kernel
+   exceeds the padded input or C % group != 0 or num_output % group != 0. */
+caffe_status caffe_conv_output_shape(const caffe_conv_desc* desc, caffe_shape4 bottom, int32_t num_output,
+                                     caffe_shape4* top /* host */);
+
+/* Bytes of device workspace the given pass needs (host out).  0 for CAFFE_MATH_FP32
+   forward/backward-data.  `weight` is the weight blob shape. */
+caffe_status caffe_conv_workspace_size(const caffe_conv_desc* desc, caffe_shape4 bottom, caffe_shape4 weight,
+                                       int32_t pass /* caffe_pass */, size_t* bytes /* host */);
+
+/* Forward.  bottom F32|BF16, weight F32|BF16, bias F32 (nullable), top
+   F32|BF16 (overwritten).  Fused ReLU with CAFFE_FUSE_RELU. */
+caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
+                                const caffe_blob* bias, caffe_blob* top, void* workspace, size_t workspace_bytes,
+                                caffe_stream_t stream);
+
+/* Data gradient: bottom_diff = beta*bottom_diff + conv^T(top_diff) (R4:
+   beta = 0 overwrites, Caffe default for data). */
+caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_blob* top_diff,
+                                      const caffe_blob* weight, caffe_blob* bottom_diff, float beta,
+                                      void* workspace, size_t workspace_bytes, caffe_stream_t stream);
+
+/* Weight/bias gradient (accumulate S:154 via beta, R4):
+     weight_diff[o,c',i,j] = beta*weight_diff + sum_{n,y,x} top_diff[n,o,y,x]*bottom[n,g(o)C/g+c',y*sh-ph+i,x*sw-pw+j]
+     bias_diff[o]          = beta*bias_diff   + sum_{n,y,x} top_diff[n,o,y,x]
+   weight_diff and bias_diff are F32; bias_diff nullable.  Deterministic split
+   reduction (no atomics). */
+caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe_blob* bottom,
+                                        const caffe_blob* top_diff, caffe_blob* weight_diff, caffe_blob* bias_diff,
+                                        float beta, void* workspace, size_t workspace_bytes, caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ ReLU
+   forward: top = bottom > 0 ? bottom : +0 (R10); top may equal bottom (in place).
+   backward: bottom_diff = top_diff where x > 0 else 0, x = the forward input or output
+   (same sign test); bottom_diff may equal top_diff. */
+caffe_status caffe_relu_forward(const caffe_blob* bottom, caffe_blob* top, caffe_stream_t stream);
+caffe_status caffe_relu_backward(const caffe_blob* bottom_or_top, const caffe_blob* top_diff, caffe_blob* bottom_diff,
+                                 caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ pooling
+   Output size: ceil((H+2p-k)/s)+1, minus 1 if (OH-1)*s >= H+p (reading R5).
+   MAX: strict '>' row-major scan seeded by the first in-image element; mask =
+   int32 h*W+w in the (n,c) plane (R7), mask nullable in forward.
+   AVE: divisor (min(hs+k,H+p)-hs)*(min(ws+k,W+p)-ws) (R6).
+   backward overwrites bottom_diff; MAX sums top_diff in ascending (py,px) order
+   in FP32 (R8, bit-exact); MAX backward without mask is CAFFE_E_INVALID. */
+caffe_status caffe_pool_output_shape(const caffe_pool_desc* desc, caffe_shape4 bottom, caffe_shape4* top /* host */);
+caffe_status caffe_pool_forward(const caffe_pool_desc* desc, const caffe_blob* bottom, caffe_blob* top,
+                                caffe_blob* mask, caffe_stream_t stream);
+caffe_status caffe_pool_backward(const caffe_pool_desc* desc, const caffe_blob* top_diff, const caffe_blob* mask,
+                                 caffe_blob* bottom_diff, caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ LRN (R9)
+   S = k + alpha/n * sum_{c' in [c-r, c+r] clipped} x^2, r=(n-1)/2;  top = bottom * S^-beta.
+   scale (F32, nullable) receives S.  Backward is the exact derivative:
+   bottom_diff = top_diff*S^-beta - (2 alpha beta/n) * x * sum_{c' in win(c)} top_diff*top/S.
+   Even local_size is CAFFE_E_PARAM. */
+caffe_status caffe_lrn_forward(const caffe_lrn_desc* desc, const caffe_blob* bottom, caffe_blob* top,
+                               caffe_blob* scale, caffe_stream_t stream);
+caffe_status caffe_lrn_backward(const caffe_lrn_desc* desc, const caffe_blob* bottom, const caffe_blob* top,
+                                const caffe_blob* top_diff, const caffe_blob* scale, caffe_blob* bottom_diff,
+                                caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ inner product
+   bottom (N,C,H,W) is flattened to (N, K=C*H*W); weight (O,K,1,1); bias (O) F32
+   nullable; top (N,O,1,1).  forward top = bottom * W^T + b, CAFFE_FUSE_RELU
+   honoured via `flags`; backward_data bottom_diff = beta*bottom_diff + top_diff*W;
+   backward_weight weight_diff = beta*weight_diff + top_diff^T*bottom,
+   bias_diff = beta*bias_diff + sum_n top_diff. */
+caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32_t num_output, int32_t pass,
+                                     size_t* bytes /* host */);
+caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob* bottom, const caffe_blob* weight,
+                              const caffe_blob* bias, caffe_blob* top, void* workspace, size_t workspace_bytes,
+                              caffe_stream_t stream);
+caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
+                                    caffe_blob* bottom_diff, float beta, void* workspace, size_t workspace_bytes,
+                                    caffe_stream_t stream);
+caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom, const caffe_blob* top_diff,
+                                      caffe_blob* weight_diff, caffe_blob* bias_diff, float beta, void* workspace,
+                                      size_t workspace_bytes, caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ im2col / col2im (test entry points)
+   S:297 / S:806 lowering of image n: col[(c*kh+i)*kw+j][y*OW+x] = bottom[n,c,y*sh-ph+i,x*sw-pw+j]
+   (0 outside), col is an F32 blob of shape (1,1,C*kh*kw,OH*OW).  col2im is its
+   adjoint, written as a gather summing in ascending (y, x) order in FP32 into image n
+   of bottom_diff (overwritten).  Bit-exact vs the oracle.  group/math ignored. */
+caffe_status caffe_im2col(const caffe_conv_desc* desc, const caffe_blob* bottom, int32_t n, caffe_blob* col,
+                          caffe_stream_t stream);
+caffe_status caffe_col2im(const caffe_conv_desc* desc, const caffe_blob* col, int32_t n, caffe_blob* bottom_diff,
+                          caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ glue for the training step
+   Softmax with loss: loss (device F32 scalar) = -(1/N) sum_n log softmax(s_n)[l_n];
+   score_diff = (softmax - onehot)/N (nullable).  labels: device int32[N] in [0,K). */
+caffe_status caffe_softmax_loss(const caffe_blob* scores, const int32_t* labels /* device */,
+                                float* loss /* device */, caffe_blob* score_diff, caffe_stream_t stream);
+
+/* SGD with momentum and weight decay (reading R18):
+   g' = g*grad_scale + decay*w;  v = momentum*v - lr*g';  w = w + v.
+   All device F32 of `count` elements; w_bf16 (device, nullable) receives RNE(w) for
+   the next step's BF16 operands. */
+caffe_status caffe_sgd_update(float* w, const float* g, float* v, void* w_bf16, int64_t count, float lr,
+                              float momentum, float decay, float grad_scale, caffe_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAFFE_B200_H_ */

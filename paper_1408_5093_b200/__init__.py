@@ -1,0 +1,351 @@
+"""B200-native Caffe convolution hot path (arXiv 1408.5093) -- thin Python binding.
+
+Every function here only marshals torch CUDA tensors into the C ABI declared in
+include/caffe_b200.h (``caffe_*`` entry points of libcaffe_b200.so) and passes the
+current CUDA stream; every step of the computation runs in the library's kernels.
+PyTorch provides device memory, streams and process groups only.
+
+Layer semantics (P:n = PAPER.md, S:n = SPEC.md lines):
+  conv_forward / conv_backward_data / conv_backward_weight
+  relu_*  S:196-213   pool_*  S:160-177   lrn_*  S:214-231   ip_*  S:178-195
+  softmax_loss  S:250-267   sgd_update
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence, Tuple, Union
+
+from . import _abi
+from ._abi import (CAFFE_BF16, CAFFE_F32, CAFFE_I32, CAFFE_MATH_BF16, CAFFE_MATH_FP32, CAFFE_MATH_TF32,
+                   CaffeError, call, load)
+
+__all__ = ["load", "CaffeError", "conv_forward", "conv_backward_data", "conv_backward_weight", "conv_output_shape",
+           "relu_forward", "relu_backward", "pool_forward", "pool_backward", "pool_output_shape", "lrn_forward",
+           "lrn_backward", "ip_forward", "ip_backward_data", "ip_backward_weight", "im2col", "col2im",
+           "softmax_loss", "sgd_update", "MATH"]
+
+MATH = {"fp32": CAFFE_MATH_FP32, "tf32": CAFFE_MATH_TF32, "bf16": CAFFE_MATH_BF16}
+
+_torch = None
+
+
+def _t():
+    global _torch
+    if _torch is None:
+        import torch
+        _torch = torch
+    return _torch
+
+
+def _pair(v) -> Tuple[int, int]:
+    return (int(v), int(v)) if isinstance(v, int) else (int(v[0]), int(v[1]))
+
+
+def _dtype_code(t) -> int:
+    torch = _t()
+    if t.dtype == torch.float32:
+        return CAFFE_F32
+    if t.dtype == torch.bfloat16:
+        return CAFFE_BF16
+    if t.dtype == torch.int32:
+        return CAFFE_I32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _shape4(shape) -> Tuple[int, int, int, int]:
+    s = tuple(int(x) for x in shape)
+    if len(s) == 4:
+        return s
+    if len(s) == 2:
+        return (s[0], s[1], 1, 1)
+    if len(s) == 1:
+        return (1, s[0], 1, 1)
+    raise ValueError(f"blob shape must have 1, 2 or 4 axes, got {s}")
+
+
+def blob(t, shape=None) -> _abi.Blob:
+    """Describe a contiguous CUDA tensor as a caffe_blob (NCHW)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("caffe_b200 blobs must live on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError("caffe_b200 blobs must be contiguous (NCHW)")
+    n, c, h, w = _shape4(t.shape if shape is None else shape)
+    return _abi.Blob(ctypes.c_void_p(t.data_ptr()), _abi.Shape4(n, c, h, w), _dtype_code(t))
+
+
+def _bp(b):
+    return ctypes.byref(b) if b is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(_t().cuda.current_stream().cuda_stream)
+
+
+# ------------------------------------------------------------------ workspace (caller-owned device memory)
+_ws = {}
+
+
+def workspace(nbytes: int, device=None):
+    """Return (ptr, size) of a 1024-byte-aligned scratch buffer of >= nbytes on `device` (cached, grows)."""
+    torch = _t()
+    if nbytes == 0:
+        return None, 0
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    buf = _ws.get(dev)
+    if buf is None or buf.numel() < nbytes + 1024:
+        buf = torch.empty(int(nbytes * 1.1) + 2048, dtype=torch.uint8, device=dev)
+        _ws[dev] = buf
+    p = buf.data_ptr()
+    off = (-p) % 1024
+    return ctypes.c_void_p(p + off), buf.numel() - off
+
+
+def _conv_desc(kernel, stride, pad, group, math, relu=False):
+    kh, kw = _pair(kernel)
+    sh, sw = _pair(stride)
+    ph, pw = _pair(pad)
+    return _abi.ConvDesc(kh, kw, sh, sw, ph, pw, int(group), MATH[math] if isinstance(math, str) else int(math),
+                         _abi.CAFFE_FUSE_RELU if relu else 0)
+
+
+def conv_output_shape(in_shape, num_output, kernel, stride=1, pad=0, group=1):
+    d = _conv_desc(kernel, stride, pad, group, "fp32")
+    out = _abi.Shape4()
+    call("caffe_conv_output_shape", ctypes.byref(d), _abi.Shape4(*_shape4(in_shape)), int(num_output), ctypes.byref(out))
+    return (out.n, out.c, out.h, out.w)
+
+
+def _conv_ws(d, in_shape, w_shape, pass_):
+    n = ctypes.c_size_t()
+    call("caffe_conv_workspace_size", ctypes.byref(d), _abi.Shape4(*_shape4(in_shape)), _abi.Shape4(*_shape4(w_shape)),
+         int(pass_), ctypes.byref(n))
+    return workspace(n.value)
+
+
+def conv_forward(x, w, b=None, stride=1, pad=0, group=1, math="bf16", relu=False, out=None, out_dtype=None):
+    """Y = W (*) X + b with groups/stride/zero-pad; optional fused ReLU."""
+    torch = _t()
+    kh, kw = w.shape[2], w.shape[3]
+    d = _conv_desc((kh, kw), stride, pad, group, math, relu)
+    oshape = conv_output_shape(x.shape, w.shape[0], (kh, kw), stride, pad, group)
+    if out is None:
+        out = torch.empty(oshape, dtype=out_dtype or x.dtype, device=x.device)
+    ws, wsz = _conv_ws(d, x.shape, w.shape, _abi.CAFFE_PASS_FORWARD)
+    bx, bw, bb, by = blob(x), blob(w), blob(b), blob(out)
+    call("caffe_conv_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(bw), _bp(bb), ctypes.byref(by), ws, wsz,
+         _stream())
+    return out
+
+
+def conv_backward_data(dy, w, in_shape, stride=1, pad=0, group=1, math="bf16", beta=0.0, out=None, out_dtype=None):
+    """dX = beta*dX + W^T (*) dY."""
+    torch = _t()
+    kh, kw = w.shape[2], w.shape[3]
+    d = _conv_desc((kh, kw), stride, pad, group, math)
+    if out is None:
+        out = torch.zeros(tuple(in_shape), dtype=out_dtype or dy.dtype, device=dy.device)
+    ws, wsz = _conv_ws(d, in_shape, w.shape, _abi.CAFFE_PASS_BACKWARD_DATA)
+    bdy, bw, bdx = blob(dy), blob(w), blob(out)
+    call("caffe_conv_backward_data", ctypes.byref(d), ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(bdx),
+         float(beta), ws, wsz, _stream())
+    return out
+
+
+def conv_backward_weight(x, dy, w_shape, stride=1, pad=0, group=1, math="bf16", beta=0.0, dw=None, db=None,
+                         bias=True):
+    """dW = beta*dW + dY (*) X, db = beta*db + sum dY.  Returns (dW, db)."""
+    torch = _t()
+    kh, kw = w_shape[2], w_shape[3]
+    d = _conv_desc((kh, kw), stride, pad, group, math)
+    if dw is None:
+        dw = torch.zeros(tuple(w_shape), dtype=torch.float32, device=x.device)
+    if bias and db is None:
+        db = torch.zeros((w_shape[0],), dtype=torch.float32, device=x.device)
+    ws, wsz = _conv_ws(d, x.shape, w_shape, _abi.CAFFE_PASS_BACKWARD_WEIGHT)
+    bx, bdy, bdw, bdb = blob(x), blob(dy), blob(dw), blob(db) if bias else None
+    call("caffe_conv_backward_weight", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(bdy), ctypes.byref(bdw),
+         _bp(bdb), float(beta), ws, wsz, _stream())
+    return dw, (db if bias else None)
+
+
+# ------------------------------------------------------------------ ReLU
+def relu_forward(x, out=None, inplace=False):
+    torch = _t()
+    if inplace:
+        out = x
+    elif out is None:
+        out = torch.empty_like(x)
+    bx, by = blob(x), blob(out)
+    call("caffe_relu_forward", ctypes.byref(bx), ctypes.byref(by), _stream())
+    return out
+
+
+def relu_backward(x, dy, out=None, inplace=False):
+    torch = _t()
+    if inplace:
+        out = dy
+    elif out is None:
+        out = torch.empty_like(dy)
+    bx, bdy, bdx = blob(x), blob(dy), blob(out)
+    call("caffe_relu_backward", ctypes.byref(bx), ctypes.byref(bdy), ctypes.byref(bdx), _stream())
+    return out
+
+
+# ------------------------------------------------------------------ pooling
+def _pool_desc(method, kernel, stride, pad):
+    kh, kw = _pair(kernel)
+    sh, sw = _pair(stride)
+    ph, pw = _pair(pad)
+    m = {"max": _abi.CAFFE_POOL_MAX, "ave": _abi.CAFFE_POOL_AVE}[method] if isinstance(method, str) else int(method)
+    return _abi.PoolDesc(m, kh, kw, sh, sw, ph, pw)
+
+
+def pool_output_shape(in_shape, method, kernel, stride, pad=0):
+    d = _pool_desc(method, kernel, stride, pad)
+    out = _abi.Shape4()
+    call("caffe_pool_output_shape", ctypes.byref(d), _abi.Shape4(*_shape4(in_shape)), ctypes.byref(out))
+    return (out.n, out.c, out.h, out.w)
+
+
+def pool_forward(x, method, kernel, stride, pad=0, out=None, mask=None, want_mask=True):
+    torch = _t()
+    d = _pool_desc(method, kernel, stride, pad)
+    oshape = pool_output_shape(x.shape, method, kernel, stride, pad)
+    if out is None:
+        out = torch.empty(oshape, dtype=x.dtype, device=x.device)
+    if d.method == _abi.CAFFE_POOL_MAX and want_mask and mask is None:
+        mask = torch.empty(oshape, dtype=torch.int32, device=x.device)
+    bx, by, bm = blob(x), blob(out), blob(mask) if d.method == _abi.CAFFE_POOL_MAX else None
+    call("caffe_pool_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(by), _bp(bm), _stream())
+    return out, (mask if d.method == _abi.CAFFE_POOL_MAX else None)
+
+
+def pool_backward(dy, mask, in_shape, method, kernel, stride, pad=0, out=None):
+    torch = _t()
+    d = _pool_desc(method, kernel, stride, pad)
+    if out is None:
+        out = torch.empty(tuple(in_shape), dtype=dy.dtype, device=dy.device)
+    bdy, bm, bdx = blob(dy), blob(mask), blob(out)
+    call("caffe_pool_backward", ctypes.byref(d), ctypes.byref(bdy), _bp(bm), ctypes.byref(bdx), _stream())
+    return out
+
+
+# ------------------------------------------------------------------ LRN
+def lrn_forward(x, local_size=5, alpha=1e-4, beta=0.75, k=1.0, out=None, scale=None, want_scale=False):
+    torch = _t()
+    d = _abi.LrnDesc(int(local_size), float(alpha), float(beta), float(k))
+    if out is None:
+        out = torch.empty_like(x)
+    if want_scale and scale is None:
+        scale = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    bx, by, bs = blob(x), blob(out), blob(scale)
+    call("caffe_lrn_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(by), _bp(bs), _stream())
+    return (out, scale) if want_scale else out
+
+
+def lrn_backward(x, y, dy, local_size=5, alpha=1e-4, beta=0.75, k=1.0, scale=None, out=None):
+    torch = _t()
+    d = _abi.LrnDesc(int(local_size), float(alpha), float(beta), float(k))
+    if out is None:
+        out = torch.empty_like(dy)
+    bx, by, bdy, bs, bdx = blob(x), blob(y), blob(dy), blob(scale), blob(out)
+    call("caffe_lrn_backward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(by), ctypes.byref(bdy), _bp(bs),
+         ctypes.byref(bdx), _stream())
+    return out
+
+
+# ------------------------------------------------------------------ inner product
+def _ip_ws(math, in_shape, O, pass_):
+    n = ctypes.c_size_t()
+    call("caffe_ip_workspace_size", MATH[math], _abi.Shape4(*_shape4(in_shape)), int(O), int(pass_), ctypes.byref(n))
+    return workspace(n.value)
+
+
+def _wblob(w):
+    # weight (O, K) or (O, K, 1, 1) -> (O, K, 1, 1)
+    return blob(w, (w.shape[0], w.numel() // w.shape[0], 1, 1))
+
+
+def ip_forward(x, w, b=None, math="bf16", relu=False, out=None, out_dtype=None):
+    """Y = X W^T + b over X flattened to (N, C*H*W)."""
+    torch = _t()
+    O = w.shape[0]
+    if out is None:
+        out = torch.empty((x.shape[0], O), dtype=out_dtype or x.dtype, device=x.device)
+    ws, wsz = _ip_ws(math, x.shape, O, 0)
+    bx, bw, bb, by = blob(x), _wblob(w), blob(b), blob(out, (x.shape[0], O, 1, 1))
+    call("caffe_ip_forward", MATH[math], _abi.CAFFE_FUSE_RELU if relu else 0, ctypes.byref(bx), ctypes.byref(bw),
+         _bp(bb), ctypes.byref(by), ws, wsz, _stream())
+    return out
+
+
+def ip_backward_data(dy, w, in_shape, math="bf16", beta=0.0, out=None, out_dtype=None):
+    torch = _t()
+    if out is None:
+        out = torch.zeros(tuple(in_shape), dtype=out_dtype or dy.dtype, device=dy.device)
+    ws, wsz = _ip_ws(math, in_shape, w.shape[0], 1)
+    bdy, bw, bdx = blob(dy, (dy.shape[0], w.shape[0], 1, 1)), _wblob(w), blob(out)
+    call("caffe_ip_backward_data", MATH[math], ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(bdx), float(beta), ws,
+         wsz, _stream())
+    return out
+
+
+def ip_backward_weight(x, dy, w_shape, math="bf16", beta=0.0, dw=None, db=None, bias=True):
+    torch = _t()
+    O = w_shape[0]
+    if dw is None:
+        dw = torch.zeros(tuple(w_shape), dtype=torch.float32, device=x.device)
+    if bias and db is None:
+        db = torch.zeros((O,), dtype=torch.float32, device=x.device)
+    ws, wsz = _ip_ws(math, x.shape, O, 2)
+    bx, bdy, bdw = blob(x), blob(dy, (dy.shape[0], O, 1, 1)), _wblob(dw)
+    bdb = blob(db) if bias else None
+    call("caffe_ip_backward_weight", MATH[math], ctypes.byref(bx), ctypes.byref(bdy), ctypes.byref(bdw), _bp(bdb),
+         float(beta), ws, wsz, _stream())
+    return dw, (db if bias else None)
+
+
+# ------------------------------------------------------------------ im2col / col2im (test entry points)
+def im2col(x, n, kernel, stride=1, pad=0):
+    torch = _t()
+    d = _conv_desc(kernel, stride, pad, 1, "fp32")
+    C = x.shape[1]
+    _, _, OH, OW = conv_output_shape(x.shape, 1, kernel, stride, pad)
+    kh, kw = _pair(kernel)
+    col = torch.empty((C * kh * kw, OH * OW), dtype=torch.float32, device=x.device)
+    bx, bc = blob(x), blob(col, (1, 1, C * kh * kw, OH * OW))
+    call("caffe_im2col", ctypes.byref(d), ctypes.byref(bx), int(n), ctypes.byref(bc), _stream())
+    return col
+
+
+def col2im(col, in_shape, n, kernel, stride=1, pad=0, out=None):
+    torch = _t()
+    d = _conv_desc(kernel, stride, pad, 1, "fp32")
+    if out is None:
+        out = torch.zeros(tuple(in_shape), dtype=torch.float32, device=col.device)
+    bc, bx = blob(col, (1, 1, col.shape[0], col.shape[1])), blob(out)
+    call("caffe_col2im", ctypes.byref(d), ctypes.byref(bc), int(n), ctypes.byref(bx), _stream())
+    return out
+
+
+# ------------------------------------------------------------------ loss / solver glue
+def softmax_loss(scores, labels, loss=None, diff=None, want_diff=True):
+    torch = _t()
+    if loss is None:
+        loss = torch.empty((), dtype=torch.float32, device=scores.device)
+    if want_diff and diff is None:
+        diff = torch.empty_like(scores)
+    bs, bd = blob(scores, (scores.shape[0], scores.numel() // scores.shape[0], 1, 1)), \
+        (blob(diff, (scores.shape[0], scores.numel() // scores.shape[0], 1, 1)) if want_diff else None)
+    call("caffe_softmax_loss", ctypes.byref(bs), ctypes.c_void_p(labels.data_ptr()), ctypes.c_void_p(loss.data_ptr()),
+         _bp(bd), _stream())
+    return loss, diff
+
+
+def sgd_update(w, g, v, lr, momentum=0.0, decay=0.0, grad_scale=1.0, w_bf16=None):
+    call("caffe_sgd_update", ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(v.data_ptr()),
+         ctypes.c_void_p(w_bf16.data_ptr()) if w_bf16 is not None else None, int(w.numel()), float(lr),
+         float(momentum), float(decay), float(grad_scale), _stream())
+    return w

@@ -1,0 +1,111 @@
+"""ctypes declarations of include/caffe_b200.h (argument marshalling only).
+
+Loading fails loudly if libcaffe_b200.so is missing: there is no fallback path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcaffe_b200.so")
+
+# enums (include/caffe_b200.h)
+CAFFE_OK, CAFFE_E_INVALID, CAFFE_E_SHAPE, CAFFE_E_PARAM, CAFFE_E_DTYPE = 0, 1, 2, 3, 4
+CAFFE_E_ALIGN, CAFFE_E_WORKSPACE, CAFFE_E_ALIAS, CAFFE_E_CUDA, CAFFE_E_ARCH = 5, 6, 7, 8, 9
+STATUS_NAMES = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_PARAM", 4: "E_DTYPE", 5: "E_ALIGN",
+                6: "E_WORKSPACE", 7: "E_ALIAS", 8: "E_CUDA", 9: "E_ARCH"}
+CAFFE_F32, CAFFE_BF16, CAFFE_I32 = 0, 1, 2
+CAFFE_MATH_FP32, CAFFE_MATH_TF32, CAFFE_MATH_BF16 = 0, 1, 2
+CAFFE_FUSE_RELU = 1
+CAFFE_POOL_MAX, CAFFE_POOL_AVE = 0, 1
+CAFFE_PASS_FORWARD, CAFFE_PASS_BACKWARD_DATA, CAFFE_PASS_BACKWARD_WEIGHT = 0, 1, 2
+
+
+class Shape4(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("c", ctypes.c_int32), ("h", ctypes.c_int32), ("w", ctypes.c_int32)]
+
+
+class Blob(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("shape", Shape4), ("dtype", ctypes.c_int)]
+
+
+class ConvDesc(ctypes.Structure):
+    _fields_ = [("kernel_h", ctypes.c_int32), ("kernel_w", ctypes.c_int32), ("stride_h", ctypes.c_int32),
+                ("stride_w", ctypes.c_int32), ("pad_h", ctypes.c_int32), ("pad_w", ctypes.c_int32),
+                ("group", ctypes.c_int32), ("math", ctypes.c_int), ("flags", ctypes.c_uint32)]
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int32), ("kernel_h", ctypes.c_int32), ("kernel_w", ctypes.c_int32),
+                ("stride_h", ctypes.c_int32), ("stride_w", ctypes.c_int32), ("pad_h", ctypes.c_int32),
+                ("pad_w", ctypes.c_int32)]
+
+
+class LrnDesc(ctypes.Structure):
+    _fields_ = [("local_size", ctypes.c_int32), ("alpha", ctypes.c_float), ("beta", ctypes.c_float),
+                ("k", ctypes.c_float)]
+
+
+P = ctypes.POINTER
+vp, i32, f32, sz, i64, u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float, ctypes.c_size_t, ctypes.c_int64, ctypes.c_uint32
+B, CD, PD, LD = P(Blob), P(ConvDesc), P(PoolDesc), P(LrnDesc)
+
+# name -> argtypes (every function returns caffe_status unless listed in _RESTYPES)
+SIGNATURES = {
+    "caffe_abi_version": [],
+    "caffe_last_error": [],
+    "caffe_device_check": [],
+    "caffe_conv_output_shape": [CD, Shape4, i32, P(Shape4)],
+    "caffe_conv_workspace_size": [CD, Shape4, Shape4, i32, P(sz)],
+    "caffe_conv_forward": [CD, B, B, B, B, vp, sz, vp],
+    "caffe_conv_backward_data": [CD, B, B, B, f32, vp, sz, vp],
+    "caffe_conv_backward_weight": [CD, B, B, B, B, f32, vp, sz, vp],
+    "caffe_relu_forward": [B, B, vp],
+    "caffe_relu_backward": [B, B, B, vp],
+    "caffe_pool_output_shape": [PD, Shape4, P(Shape4)],
+    "caffe_pool_forward": [PD, B, B, B, vp],
+    "caffe_pool_backward": [PD, B, B, B, vp],
+    "caffe_lrn_forward": [LD, B, B, B, vp],
+    "caffe_lrn_backward": [LD, B, B, B, B, B, vp],
+    "caffe_ip_workspace_size": [ctypes.c_int, Shape4, i32, i32, P(sz)],
+    "caffe_ip_forward": [ctypes.c_int, u32, B, B, B, B, vp, sz, vp],
+    "caffe_ip_backward_data": [ctypes.c_int, B, B, B, f32, vp, sz, vp],
+    "caffe_ip_backward_weight": [ctypes.c_int, B, B, B, B, f32, vp, sz, vp],
+    "caffe_im2col": [CD, B, i32, B, vp],
+    "caffe_col2im": [CD, B, i32, B, vp],
+    "caffe_softmax_loss": [B, vp, vp, B, vp],
+    "caffe_sgd_update": [vp, vp, vp, vp, i64, f32, f32, f32, f32, vp],
+}
+_RESTYPES = {"caffe_abi_version": ctypes.c_int32, "caffe_last_error": ctypes.c_char_p}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libcaffe_b200.so (build it first with `python -m paper_1408_5093_b200.build`)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: the CUDA library must be built "
+                              "(python -m paper_1408_5093_b200.build); there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        _lib = lib
+    return _lib
+
+
+class CaffeError(RuntimeError):
+    def __init__(self, status: int, fn: str, msg: str):
+        super().__init__(f"{fn} -> {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    st = getattr(lib, name)(*args)
+    if st != CAFFE_OK:
+        raise CaffeError(st, name, lib.caffe_last_error().decode())

@@ -1,0 +1,843 @@
+// abi.cu -- the extern "C" boundary (include/caffe_b200.h): host-side validation, workspace
+// planning and launch sequencing.  Every numerical step runs in the kernels of tc_gemm.cu,
+// pack.cu and simple.cu; nothing here touches device data.
+#include "../../include/caffe_b200.h"
+#include "internal.h"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+using namespace cb;
+
+namespace {
+
+thread_local std::string g_err;
+
+caffe_status fail(caffe_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+caffe_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(CAFFE_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(expr, what)                                  \
+    do {                                                \
+        cudaError_t _e = (expr);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+inline long long cnt(const caffe_shape4& s) { return (long long)s.n * s.c * s.h * s.w; }
+inline size_t esize(caffe_dtype d) { return d == CAFFE_BF16 ? 2 : 4; }
+inline size_t bytes_of(const caffe_blob* b) { return (size_t)cnt(b->shape) * esize(b->dtype); }
+inline long long rup(long long a, long long b) { return (a + b - 1) / b * b; }
+inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+inline size_t align1k(size_t x) { return (x + 1023) & ~size_t(1023); }
+
+caffe_status check_blob(const caffe_blob* b, const char* name, bool float_only = true) {
+    if (!b) return fail(CAFFE_E_INVALID, "%s is NULL", name);
+    if (!b->ptr && cnt(b->shape) != 0) return fail(CAFFE_E_INVALID, "%s->ptr is NULL", name);
+    const caffe_shape4& s = b->shape;
+    if (s.n < 0 || s.c < 0 || s.h < 0 || s.w < 0) return fail(CAFFE_E_SHAPE, "%s has a negative axis", name);
+    if (s.n > 0 && (s.c == 0 || s.h == 0 || s.w == 0))
+        return fail(CAFFE_E_SHAPE, "%s has a zero axis (%d,%d,%d,%d)", name, s.n, s.c, s.h, s.w);
+    if (float_only && b->dtype != CAFFE_F32 && b->dtype != CAFFE_BF16)
+        return fail(CAFFE_E_DTYPE, "%s dtype must be F32 or BF16", name);
+    if (!float_only && b->dtype != CAFFE_I32) return fail(CAFFE_E_DTYPE, "%s dtype must be I32", name);
+    return CAFFE_OK;
+}
+bool overlap(const caffe_blob* a, const caffe_blob* b) {
+    if (!a || !b || !a->ptr || !b->ptr) return false;
+    const char* x = (const char*)a->ptr;
+    const char* y = (const char*)b->ptr;
+    return x < y + bytes_of(b) && y < x + bytes_of(a);
+}
+bool same_shape(const caffe_shape4& a, const caffe_shape4& b) {
+    return a.n == b.n && a.c == b.c && a.h == b.h && a.w == b.w;
+}
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ------------------------------------------------------------------ conv planning
+struct Plan {
+    int N, C, H, W, O, G, Cg, Og, kh, kw, sh, sw, ph, pw, OH, OW;
+    int E, CH;             // operand element size, elements per 128-byte row
+    bool s2d;
+    int bh, bw, khp, kwp, php, pwp, Hp, Wp, Cge, Cgp, Ogp, taps;
+};
+
+caffe_status conv_validate(const caffe_conv_desc* d, caffe_shape4 bottom, int32_t O, Plan* p) {
+    if (!d) return fail(CAFFE_E_INVALID, "desc is NULL");
+    if (d->kernel_h < 1 || d->kernel_w < 1 || d->stride_h < 1 || d->stride_w < 1 || d->pad_h < 0 || d->pad_w < 0 ||
+        d->group < 1)
+        return fail(CAFFE_E_PARAM, "bad conv parameter (kernel %dx%d stride %dx%d pad %dx%d group %d)", d->kernel_h,
+                    d->kernel_w, d->stride_h, d->stride_w, d->pad_h, d->pad_w, d->group);
+    if (d->math != CAFFE_MATH_FP32 && d->math != CAFFE_MATH_TF32 && d->math != CAFFE_MATH_BF16)
+        return fail(CAFFE_E_INVALID, "bad math mode %d", (int)d->math);
+    if (bottom.c % d->group) return fail(CAFFE_E_PARAM, "channels %d not divisible by group %d", bottom.c, d->group);
+    if (O < 1 || O % d->group) return fail(CAFFE_E_PARAM, "num_output %d not divisible by group %d", O, d->group);
+    if (d->kernel_h > bottom.h + 2 * d->pad_h || d->kernel_w > bottom.w + 2 * d->pad_w)
+        return fail(CAFFE_E_PARAM, "kernel %dx%d larger than padded input %dx%d (S:146)", d->kernel_h, d->kernel_w,
+                    bottom.h + 2 * d->pad_h, bottom.w + 2 * d->pad_w);
+    Plan& q = *p;
+    q.N = bottom.n; q.C = bottom.c; q.H = bottom.h; q.W = bottom.w; q.O = O; q.G = d->group;
+    q.Cg = q.C / q.G; q.Og = O / q.G; q.kh = d->kernel_h; q.kw = d->kernel_w; q.sh = d->stride_h; q.sw = d->stride_w;
+    q.ph = d->pad_h; q.pw = d->pad_w;
+    q.OH = (q.H + 2 * q.ph - q.kh) / q.sh + 1;
+    q.OW = (q.W + 2 * q.pw - q.kw) / q.sw + 1;
+    q.E = d->math == CAFFE_MATH_TF32 ? 4 : 2;
+    q.CH = 128 / q.E;
+    q.s2d = q.sh > 1 || q.sw > 1;
+    q.bh = q.s2d ? q.sh : 1; q.bw = q.s2d ? q.sw : 1;
+    q.khp = (int)cdiv(q.kh, q.bh); q.kwp = (int)cdiv(q.kw, q.bw);
+    q.php = q.s2d ? 0 : q.ph; q.pwp = q.s2d ? 0 : q.pw;
+    q.Hp = q.s2d ? q.OH + q.khp - 1 : q.H;
+    q.Wp = q.s2d ? q.OW + q.kwp - 1 : q.W;
+    q.Cge = q.Cg * q.bh * q.bw;
+    q.Cgp = (int)rup(q.Cge, q.CH);
+    q.Ogp = (int)rup(q.Og, q.CH);
+    q.taps = q.khp * q.kwp;
+    return CAFFE_OK;
+}
+
+ConvGeom cgeom(const Plan& p) {
+    return ConvGeom{p.N, p.C, p.H, p.W, p.O, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, p.G, p.OH, p.OW};
+}
+PackGeom xpack(const Plan& p) {
+    return PackGeom{p.N, p.C, p.H, p.W, p.G, p.Cg, p.bh, p.bw, p.s2d ? p.ph : 0, p.s2d ? p.pw : 0, p.Hp, p.Wp, p.Cgp};
+}
+PackGeom dypack(const Plan& p) {
+    return PackGeom{p.N, p.O, p.OH, p.OW, p.G, p.Og, 1, 1, 0, 0, p.OH, p.OW, p.Ogp};
+}
+WGeom wgeom(const Plan& p) {
+    return WGeom{p.O, p.G, p.Cg, p.Og, p.kh, p.kw, p.bh, p.bw, p.khp, p.kwp, p.Cgp, p.Ogp};
+}
+
+int choose_bn(int n) {
+    if (n <= 256) return (int)rup(n, 16);
+    const int t = (int)cdiv(n, 256);
+    return (int)rup(cdiv(n, t), 16);
+}
+int pow2ceil(int x) {
+    int p = 32;
+    while (p < x) p <<= 1;
+    return p;
+}
+void finish_args(TcArgs& a, int bstage) {
+    a.b_stage_bytes = bstage;
+    const int stage = 16384 + bstage;
+    a.stages = (200 * 1024) / stage;
+    if (a.stages > 8) a.stages = 8;
+    a.acc_stride = pow2ceil(a.BN);
+    a.tmem_cols = 2 * a.acc_stride;
+    a.units = a.m_tiles * a.n_tiles * a.groups * a.splits;
+}
+
+// workspace sub-buffer sizes
+size_t ws_xa(const Plan& p) { return align1k((size_t)p.N * p.Hp * p.Wp * p.G * p.Cgp * p.E); }
+size_t ws_dya(const Plan& p) { return align1k((size_t)p.N * p.OH * p.OW * p.G * p.Ogp * p.E); }
+size_t ws_wb(const Plan& p) { return align1k((size_t)p.O * p.taps * p.Cgp * p.E); }
+size_t ws_wd(const Plan& p) { return align1k((size_t)p.G * p.Cge * p.taps * p.Ogp * p.E); }
+size_t ws_t(const Plan& p) { return p.s2d ? align1k((size_t)p.N * p.Hp * p.Wp * p.G * p.Cgp * 4) : 0; }
+
+struct WgradSplit {
+    int m_tiles, n_tiles, BN, splits, kb_per, kblocks;
+};
+WgradSplit wgrad_split(const Plan& p) {
+    WgradSplit w;
+    const int nchunks = p.taps * (p.Cgp / p.CH);
+    const int chunks_per_tile = 128 / p.CH;
+    w.m_tiles = (int)cdiv(nchunks, chunks_per_tile);
+    w.BN = choose_bn(p.Og);
+    w.n_tiles = (int)cdiv(p.Og, w.BN);
+    w.kblocks = (int)cdiv((long long)p.N * p.OH * p.OW, p.CH);
+    const int tiles = w.m_tiles * w.n_tiles * p.G;
+    const int sms = 148;
+    int s = (int)cdiv(2 * sms, tiles);
+    if (s < 1) s = 1;
+    int kb_per = (int)cdiv(w.kblocks, s);
+    if (kb_per < 4) kb_per = 4;
+    w.kb_per = kb_per;
+    w.splits = (int)cdiv(w.kblocks, kb_per);
+    return w;
+}
+size_t ws_partial(const Plan& p) {
+    WgradSplit w = wgrad_split(p);
+    return align1k((size_t)w.m_tiles * w.n_tiles * p.G * w.splits * w.BN * 128 * 4);
+}
+
+size_t conv_ws(const Plan& p, int pass, caffe_math m) {
+    if (m == CAFFE_MATH_FP32) return 0;
+    if (pass == CAFFE_PASS_FORWARD) return ws_xa(p) + ws_wb(p);
+    if (pass == CAFFE_PASS_BACKWARD_DATA) return ws_dya(p) + ws_wd(p) + ws_t(p);
+    return ws_xa(p) + ws_dya(p) + ws_partial(p);
+}
+
+caffe_status check_ws(void* ws, size_t have, size_t need) {
+    if (need == 0) return CAFFE_OK;
+    if (!ws || have < need)
+        return fail(CAFFE_E_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws ? have : (size_t)0);
+    if ((reinterpret_cast<uintptr_t>(ws) & 1023) != 0) return fail(CAFFE_E_ALIGN, "workspace must be 1024-byte aligned");
+    return CAFFE_OK;
+}
+
+caffe_status run_tc(TcLaunch& L, cudaStream_t s) {
+    L.grid = L.args.units < num_sms() ? L.args.units : num_sms();
+    cudaError_t e = tc_launch(L, s);
+    if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
+    return CAFFE_OK;
+}
+
+}  // namespace
+
+// ====================================================================== exported
+extern "C" {
+
+int32_t caffe_abi_version(void) { return CAFFE_ABI_VERSION; }
+const char* caffe_last_error(void) { return g_err.c_str(); }
+
+caffe_status caffe_device_check(void) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0) return fail(CAFFE_E_ARCH, "device is sm_%d%d, this library is built for sm_100a", major, minor);
+    return CAFFE_OK;
+}
+
+caffe_status caffe_conv_output_shape(const caffe_conv_desc* desc, caffe_shape4 bottom, int32_t num_output,
+                                     caffe_shape4* top) {
+    if (!top) return fail(CAFFE_E_INVALID, "top is NULL");
+    Plan p;
+    caffe_status st = conv_validate(desc, bottom, num_output, &p);
+    if (st) return st;
+    *top = caffe_shape4{bottom.n, num_output, p.OH, p.OW};
+    return CAFFE_OK;
+}
+
+caffe_status caffe_conv_workspace_size(const caffe_conv_desc* desc, caffe_shape4 bottom, caffe_shape4 weight,
+                                       int32_t pass, size_t* bytes) {
+    if (!bytes) return fail(CAFFE_E_INVALID, "bytes is NULL");
+    if (pass < 0 || pass > 2) return fail(CAFFE_E_INVALID, "bad pass %d", pass);
+    Plan p;
+    caffe_status st = conv_validate(desc, bottom, weight.n, &p);
+    if (st) return st;
+    *bytes = bottom.n == 0 ? 0 : conv_ws(p, pass, desc->math);
+    return CAFFE_OK;
+}
+
+static caffe_status conv_common(const caffe_conv_desc* desc, const caffe_blob* bottom_like, const caffe_blob* weight,
+                                Plan* p) {
+    caffe_status st;
+    if ((st = check_blob(bottom_like, "bottom"))) return st;
+    if ((st = check_blob(weight, "weight"))) return st;
+    if ((st = conv_validate(desc, bottom_like->shape, weight->shape.n, p))) return st;
+    if (weight->shape.c != p->Cg || weight->shape.h != p->kh || weight->shape.w != p->kw)
+        return fail(CAFFE_E_SHAPE, "weight shape (%d,%d,%d,%d) != (O,C/g,kh,kw) = (%d,%d,%d,%d)", weight->shape.n,
+                    weight->shape.c, weight->shape.h, weight->shape.w, p->O, p->Cg, p->kh, p->kw);
+    if (desc->math == CAFFE_MATH_TF32 && (bottom_like->dtype == CAFFE_BF16 || weight->dtype == CAFFE_BF16))
+        return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
+                                const caffe_blob* bias, caffe_blob* top, void* ws, size_t ws_bytes,
+                                caffe_stream_t stream) {
+    Plan p;
+    caffe_status st = conv_common(desc, bottom, weight, &p);
+    if (st) return st;
+    if ((st = check_blob(top, "top"))) return st;
+    if (bias) {
+        if ((st = check_blob(bias, "bias"))) return st;
+        if (bias->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "bias must be F32");
+        if (cnt(bias->shape) != p.O) return fail(CAFFE_E_SHAPE, "bias has %lld elements, num_output %d", cnt(bias->shape), p.O);
+    }
+    caffe_shape4 want{p.N, p.O, p.OH, p.OW};
+    if (!same_shape(top->shape, want))
+        return fail(CAFFE_E_SHAPE, "top shape (%d,%d,%d,%d) != (%d,%d,%d,%d)", top->shape.n, top->shape.c, top->shape.h,
+                    top->shape.w, want.n, want.c, want.h, want.w);
+    if (overlap(top, bottom) || overlap(top, weight) || overlap(top, bias)) return fail(CAFFE_E_ALIAS, "top overlaps an input");
+    if (desc->math == CAFFE_MATH_TF32 && top->dtype == CAFFE_BF16) return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
+    if (p.N == 0) return CAFFE_OK;
+    const size_t need = conv_ws(p, CAFFE_PASS_FORWARD, desc->math);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int xb = bottom->dtype == CAFFE_BF16, wb = weight->dtype == CAFFE_BF16, yb = top->dtype == CAFFE_BF16;
+    const int relu = (desc->flags & CAFFE_FUSE_RELU) ? 1 : 0;
+    const float* bptr = bias ? (const float*)bias->ptr : nullptr;
+    if (desc->math == CAFFE_MATH_FP32) {
+        CK(fp32_conv_fwd(bottom->ptr, xb, weight->ptr, wb, bptr, top->ptr, yb, relu, cgeom(p), s), "conv fwd fp32");
+        return CAFFE_OK;
+    }
+    char* w8 = (char*)ws;
+    void* XA = w8;
+    void* WB = w8 + ws_xa(p);
+    CK(pack_nhwc(bottom->ptr, xb, XA, p.E, xpack(p), s), "pack activations");
+    CK(repack_w_fwd(weight->ptr, wb, WB, p.E, wgeom(p), s), "repack weights");
+    TcLaunch L;
+    memset(&L, 0, sizeof L);
+    L.esz = p.E; L.amode = A_IM2COL_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
+    if (!encode_im2col_4d(&L.mapA, p.E, XA, p.G * p.Cgp, p.Wp, p.Hp, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
+                          p.php - (p.khp - 1), p.CH, 128))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (activation)");
+    TcArgs& a = L.args;
+    a.BN = choose_bn(p.Og);
+    if (!encode_tiled_2d(&L.mapB, p.E, WB, (uint64_t)p.taps * p.Cgp, (uint64_t)p.O, (uint64_t)p.taps * p.Cgp * p.E,
+                         p.CH, a.BN))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (weights)");
+    a.M = p.N * p.OH * p.OW; a.N = p.Og;
+    a.m_tiles = (int)cdiv(a.M, 128); a.n_tiles = (int)cdiv(p.Og, a.BN); a.groups = p.G; a.splits = 1;
+    a.kblocks = p.taps * (p.Cgp / p.CH); a.kb_per_split = a.kblocks;
+    a.a_P = p.OH * p.OW; a.a_OW = p.OW; a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_kw = p.kwp;
+    a.a_cblocks = p.Cgp / p.CH; a.a_cpg = p.Cgp; a.b_row_g = p.Og;
+    a.out = top->ptr; a.out_bf16 = yb; a.s_n = (long long)p.O * p.OH * p.OW; a.s_c = (long long)p.OH * p.OW; a.s_p = 1;
+    a.P = p.OH * p.OW; a.col_g = p.Og; a.bias = bptr; a.relu = relu; a.beta = 0.f;
+    finish_args(a, a.BN * 128);
+    return run_tc(L, s);
+}
+
+caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_blob* top_diff, const caffe_blob* weight,
+                                      caffe_blob* bottom_diff, float beta, void* ws, size_t ws_bytes,
+                                      caffe_stream_t stream) {
+    Plan p;
+    caffe_status st;
+    if ((st = check_blob(bottom_diff, "bottom_diff"))) return st;
+    if ((st = conv_common(desc, bottom_diff, weight, &p))) return st;
+    if ((st = check_blob(top_diff, "top_diff"))) return st;
+    caffe_shape4 want{p.N, p.O, p.OH, p.OW};
+    if (!same_shape(top_diff->shape, want))
+        return fail(CAFFE_E_SHAPE, "top_diff shape (%d,%d,%d,%d) != (%d,%d,%d,%d)", top_diff->shape.n, top_diff->shape.c,
+                    top_diff->shape.h, top_diff->shape.w, want.n, want.c, want.h, want.w);
+    if (overlap(bottom_diff, top_diff) || overlap(bottom_diff, weight)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
+    if (desc->math == CAFFE_MATH_TF32 && top_diff->dtype == CAFFE_BF16) return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
+    if (p.N == 0) return CAFFE_OK;
+    const size_t need = conv_ws(p, CAFFE_PASS_BACKWARD_DATA, desc->math);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int db = top_diff->dtype == CAFFE_BF16, wb = weight->dtype == CAFFE_BF16, xb = bottom_diff->dtype == CAFFE_BF16;
+    if (desc->math == CAFFE_MATH_FP32) {
+        CK(fp32_conv_dgrad(top_diff->ptr, db, weight->ptr, wb, bottom_diff->ptr, xb, beta, cgeom(p), s), "conv dgrad fp32");
+        return CAFFE_OK;
+    }
+    char* w8 = (char*)ws;
+    void* DYA = w8;
+    void* WD = w8 + ws_dya(p);
+    float* T = (float*)(w8 + ws_dya(p) + ws_wd(p));
+    CK(pack_nhwc(top_diff->ptr, db, DYA, p.E, dypack(p), s), "pack top_diff");
+    CK(repack_w_dgrad(weight->ptr, wb, WD, p.E, wgeom(p), p.Cge, s), "repack weights (dgrad)");
+    const int Hd = p.s2d ? p.Hp : p.H, Wd = p.s2d ? p.Wp : p.W;
+    const int lo_h = p.khp - 1 - p.php, lo_w = p.kwp - 1 - p.pwp;
+    TcLaunch L;
+    memset(&L, 0, sizeof L);
+    L.esz = p.E; L.amode = A_IM2COL_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
+    if (!encode_im2col_4d(&L.mapA, p.E, DYA, p.G * p.Ogp, p.OW, p.OH, p.N, lo_w, lo_h, lo_w - (p.kwp - 1),
+                          lo_h - (p.khp - 1), p.CH, 128))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (top_diff)");
+    TcArgs& a = L.args;
+    a.BN = choose_bn(p.Cge);
+    if (!encode_tiled_2d(&L.mapB, p.E, WD, (uint64_t)p.taps * p.Ogp, (uint64_t)p.G * p.Cge,
+                         (uint64_t)p.taps * p.Ogp * p.E, p.CH, a.BN))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (dgrad weights)");
+    a.M = p.N * Hd * Wd; a.N = p.Cge;
+    a.m_tiles = (int)cdiv(a.M, 128); a.n_tiles = (int)cdiv(p.Cge, a.BN); a.groups = p.G; a.splits = 1;
+    a.kblocks = p.taps * (p.Ogp / p.CH); a.kb_per_split = a.kblocks;
+    a.a_P = Hd * Wd; a.a_OW = Wd; a.a_pad_h = lo_h; a.a_pad_w = lo_w; a.a_kw = p.kwp;
+    a.a_cblocks = p.Ogp / p.CH; a.a_cpg = p.Ogp; a.b_row_g = p.Cge;
+    a.P = Hd * Wd;
+    if (!p.s2d) {
+        a.out = bottom_diff->ptr; a.out_bf16 = xb; a.s_n = (long long)p.C * p.H * p.W; a.s_c = (long long)p.H * p.W;
+        a.s_p = 1; a.col_g = p.Cg; a.beta = beta;
+    } else {
+        a.out = T; a.out_bf16 = 0; a.s_n = (long long)p.Hp * p.Wp * p.G * p.Cgp; a.s_c = 1; a.s_p = (long long)p.G * p.Cgp;
+        a.col_g = p.Cgp; a.beta = 0.f;
+    }
+    finish_args(a, a.BN * 128);
+    if ((st = run_tc(L, s))) return st;
+    if (p.s2d) CK(unpack_s2d_grad(T, bottom_diff->ptr, xb, beta, xpack(p), s), "unpack s2d gradient");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe_blob* bottom,
+                                        const caffe_blob* top_diff, caffe_blob* weight_diff, caffe_blob* bias_diff,
+                                        float beta, void* ws, size_t ws_bytes, caffe_stream_t stream) {
+    Plan p;
+    caffe_status st;
+    if ((st = conv_common(desc, bottom, weight_diff, &p))) return st;
+    if ((st = check_blob(top_diff, "top_diff"))) return st;
+    if (weight_diff->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "weight_diff must be F32");
+    caffe_shape4 want{p.N, p.O, p.OH, p.OW};
+    if (!same_shape(top_diff->shape, want))
+        return fail(CAFFE_E_SHAPE, "top_diff shape (%d,%d,%d,%d) != (%d,%d,%d,%d)", top_diff->shape.n, top_diff->shape.c,
+                    top_diff->shape.h, top_diff->shape.w, want.n, want.c, want.h, want.w);
+    if (bias_diff) {
+        if ((st = check_blob(bias_diff, "bias_diff"))) return st;
+        if (bias_diff->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "bias_diff must be F32");
+        if (cnt(bias_diff->shape) != p.O) return fail(CAFFE_E_SHAPE, "bias_diff has %lld elements, num_output %d", cnt(bias_diff->shape), p.O);
+    }
+    if (overlap(weight_diff, bottom) || overlap(weight_diff, top_diff) || overlap(bias_diff, bottom) ||
+        overlap(bias_diff, top_diff) || overlap(bias_diff, weight_diff))
+        return fail(CAFFE_E_ALIAS, "weight_diff/bias_diff overlaps an input");
+    if (desc->math == CAFFE_MATH_TF32 && top_diff->dtype == CAFFE_BF16) return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
+    if (desc->math == CAFFE_MATH_TF32) return fail(CAFFE_E_DTYPE, "TF32 weight gradient not built yet (use BF16 or FP32 math)");
+    if (p.N == 0) return CAFFE_OK;
+    const size_t need = conv_ws(p, CAFFE_PASS_BACKWARD_WEIGHT, desc->math);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int xb = bottom->dtype == CAFFE_BF16, db = top_diff->dtype == CAFFE_BF16;
+    if (bias_diff)
+        CK(bias_grad(top_diff->ptr, db, (float*)bias_diff->ptr, beta, p.N, p.O, (long long)p.OH * p.OW, s), "bias grad");
+    if (desc->math == CAFFE_MATH_FP32) {
+        CK(fp32_conv_wgrad(bottom->ptr, xb, top_diff->ptr, db, (float*)weight_diff->ptr, beta, cgeom(p), s), "conv wgrad fp32");
+        return CAFFE_OK;
+    }
+    char* w8 = (char*)ws;
+    void* XA = w8;
+    void* DYA = w8 + ws_xa(p);
+    float* PART = (float*)(w8 + ws_xa(p) + ws_dya(p));
+    CK(pack_nhwc(bottom->ptr, xb, XA, p.E, xpack(p), s), "pack activations");
+    CK(pack_nhwc(top_diff->ptr, db, DYA, p.E, dypack(p), s), "pack top_diff");
+    WgradSplit w = wgrad_split(p);
+    TcLaunch L;
+    memset(&L, 0, sizeof L);
+    L.esz = p.E; L.amode = A_IM2COL_MN; L.bmode = B_TILED_MN; L.epi = EPI_PARTIAL;
+    if (!encode_im2col_4d(&L.mapA, p.E, XA, p.G * p.Cgp, p.Wp, p.Hp, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
+                          p.php - (p.khp - 1), p.CH, p.CH))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (wgrad activation)");
+    if (!encode_tiled_2d(&L.mapB, p.E, DYA, (uint64_t)p.G * p.Ogp, (uint64_t)p.N * p.OH * p.OW,
+                         (uint64_t)p.G * p.Ogp * p.E, p.CH, p.CH))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (wgrad top_diff)");
+    TcArgs& a = L.args;
+    a.BN = w.BN; a.M = 128 * w.m_tiles; a.N = p.Og;
+    a.m_tiles = w.m_tiles; a.n_tiles = w.n_tiles; a.groups = p.G; a.splits = w.splits;
+    a.kblocks = w.kblocks; a.kb_per_split = w.kb_per;
+    a.a_P = p.OH * p.OW; a.a_OW = p.OW; a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_kw = p.kwp;
+    a.a_cblocks = p.Cgp / p.CH; a.a_cpg = p.Cgp; a.a_nchunks_total = p.taps * (p.Cgp / p.CH);
+    a.b_col_g = p.Ogp; a.b_nchunks = (int)cdiv(w.BN, p.CH);
+    a.partial = PART;
+    finish_args(a, a.b_nchunks * p.CH * 128);
+    if ((st = run_tc(L, s))) return st;
+    CK(wgrad_reduce(PART, (float*)weight_diff->ptr, beta, wgeom(p), w.m_tiles, w.n_tiles, w.splits, w.BN, p.CH,
+                    p.Cgp / p.CH, s),
+       "wgrad reduce");
+    return CAFFE_OK;
+}
+
+// ------------------------------------------------------------------ ReLU
+caffe_status caffe_relu_forward(const caffe_blob* bottom, caffe_blob* top, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom, "bottom")) || (st = check_blob(top, "top"))) return st;
+    if (!same_shape(bottom->shape, top->shape) || bottom->dtype != top->dtype)
+        return fail(CAFFE_E_SHAPE, "top must match bottom in shape and dtype");
+    if (bottom->ptr != top->ptr && overlap(bottom, top)) return fail(CAFFE_E_ALIAS, "partial overlap of top and bottom");
+    if (cnt(bottom->shape) == 0) return CAFFE_OK;
+    if (!aligned16(bottom->ptr) || !aligned16(top->ptr)) return fail(CAFFE_E_ALIGN, "ReLU buffers must be 16-byte aligned");
+    CK(relu_fwd(bottom->ptr, top->ptr, bottom->dtype == CAFFE_BF16, cnt(bottom->shape), (cudaStream_t)stream), "relu fwd");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_relu_backward(const caffe_blob* x, const caffe_blob* top_diff, caffe_blob* bottom_diff,
+                                 caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(x, "bottom_or_top")) || (st = check_blob(top_diff, "top_diff")) ||
+        (st = check_blob(bottom_diff, "bottom_diff")))
+        return st;
+    if (!same_shape(x->shape, top_diff->shape) || !same_shape(x->shape, bottom_diff->shape) ||
+        top_diff->dtype != bottom_diff->dtype)
+        return fail(CAFFE_E_SHAPE, "ReLU backward blobs must share shape (and diff dtype)");
+    if ((bottom_diff->ptr != top_diff->ptr && overlap(bottom_diff, top_diff)) || overlap(bottom_diff, x))
+        return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
+    if (cnt(x->shape) == 0) return CAFFE_OK;
+    CK(relu_bwd(x->ptr, top_diff->ptr, bottom_diff->ptr, x->dtype == CAFFE_BF16, top_diff->dtype == CAFFE_BF16,
+                cnt(x->shape), (cudaStream_t)stream),
+       "relu bwd");
+    return CAFFE_OK;
+}
+
+// ------------------------------------------------------------------ pooling
+static caffe_status pool_validate(const caffe_pool_desc* d, caffe_shape4 b, PoolGeom* g) {
+    if (!d) return fail(CAFFE_E_INVALID, "desc is NULL");
+    if (d->method != CAFFE_POOL_MAX && d->method != CAFFE_POOL_AVE) return fail(CAFFE_E_INVALID, "bad pool method %d", d->method);
+    if (d->kernel_h < 1 || d->kernel_w < 1) return fail(CAFFE_E_PARAM, "zero-sized pooling window (S:164)");
+    if (d->stride_h < 1 || d->stride_w < 1 || d->pad_h < 0 || d->pad_w < 0)
+        return fail(CAFFE_E_PARAM, "bad pool stride/pad");
+    if (d->pad_h >= d->kernel_h || d->pad_w >= d->kernel_w) return fail(CAFFE_E_PARAM, "pad must be smaller than the window");
+    if (d->kernel_h > b.h + 2 * d->pad_h || d->kernel_w > b.w + 2 * d->pad_w)
+        return fail(CAFFE_E_PARAM, "pool window larger than padded input");
+    auto od = [](int in, int k, int s, int p) {
+        int o = (in + 2 * p - k + s - 1) / s + 1;
+        if ((o - 1) * s >= in + p) o -= 1;
+        return o;
+    };
+    *g = PoolGeom{b.n, b.c, b.h, b.w, d->kernel_h, d->kernel_w, d->stride_h, d->stride_w, d->pad_h, d->pad_w,
+                  od(b.h, d->kernel_h, d->stride_h, d->pad_h), od(b.w, d->kernel_w, d->stride_w, d->pad_w)};
+    return CAFFE_OK;
+}
+
+caffe_status caffe_pool_output_shape(const caffe_pool_desc* desc, caffe_shape4 bottom, caffe_shape4* top) {
+    if (!top) return fail(CAFFE_E_INVALID, "top is NULL");
+    PoolGeom g;
+    caffe_status st = pool_validate(desc, bottom, &g);
+    if (st) return st;
+    *top = caffe_shape4{bottom.n, bottom.c, g.OH, g.OW};
+    return CAFFE_OK;
+}
+
+caffe_status caffe_pool_forward(const caffe_pool_desc* desc, const caffe_blob* bottom, caffe_blob* top, caffe_blob* mask,
+                                caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom, "bottom")) || (st = check_blob(top, "top"))) return st;
+    PoolGeom g;
+    if ((st = pool_validate(desc, bottom->shape, &g))) return st;
+    caffe_shape4 want{g.N, g.C, g.OH, g.OW};
+    if (!same_shape(top->shape, want) || top->dtype != bottom->dtype)
+        return fail(CAFFE_E_SHAPE, "top shape/dtype mismatch (want %d,%d,%d,%d)", want.n, want.c, want.h, want.w);
+    if (mask) {
+        if ((st = check_blob(mask, "mask", false))) return st;
+        if (!same_shape(mask->shape, want)) return fail(CAFFE_E_SHAPE, "mask shape must equal top shape");
+        if (desc->method != CAFFE_POOL_MAX) return fail(CAFFE_E_INVALID, "mask is only produced by MAX pooling");
+    }
+    if (overlap(top, bottom) || overlap(mask, bottom) || overlap(mask, top)) return fail(CAFFE_E_ALIAS, "pool outputs overlap");
+    if (g.N == 0) return CAFFE_OK;
+    const int bf = bottom->dtype == CAFFE_BF16;
+    if (desc->method == CAFFE_POOL_MAX)
+        CK(maxpool_fwd(bottom->ptr, top->ptr, mask ? (int32_t*)mask->ptr : nullptr, bf, g, (cudaStream_t)stream), "maxpool fwd");
+    else
+        CK(avepool_fwd(bottom->ptr, top->ptr, bf, g, (cudaStream_t)stream), "avepool fwd");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_pool_backward(const caffe_pool_desc* desc, const caffe_blob* top_diff, const caffe_blob* mask,
+                                 caffe_blob* bottom_diff, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(top_diff, "top_diff")) || (st = check_blob(bottom_diff, "bottom_diff"))) return st;
+    PoolGeom g;
+    if ((st = pool_validate(desc, bottom_diff->shape, &g))) return st;
+    caffe_shape4 want{g.N, g.C, g.OH, g.OW};
+    if (!same_shape(top_diff->shape, want) || top_diff->dtype != bottom_diff->dtype)
+        return fail(CAFFE_E_SHAPE, "top_diff shape/dtype mismatch");
+    if (desc->method == CAFFE_POOL_MAX) {
+        if (!mask) return fail(CAFFE_E_INVALID, "MAX pool backward needs the argmax mask (S:173)");
+        if ((st = check_blob(mask, "mask", false))) return st;
+        if (!same_shape(mask->shape, want)) return fail(CAFFE_E_SHAPE, "mask shape must equal top shape");
+    }
+    if (overlap(bottom_diff, top_diff) || overlap(bottom_diff, mask)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
+    if (g.N == 0) return CAFFE_OK;
+    const int bf = top_diff->dtype == CAFFE_BF16;
+    if (desc->method == CAFFE_POOL_MAX)
+        CK(maxpool_bwd(top_diff->ptr, (const int32_t*)mask->ptr, bottom_diff->ptr, bf, g, (cudaStream_t)stream), "maxpool bwd");
+    else
+        CK(avepool_bwd(top_diff->ptr, bottom_diff->ptr, bf, g, (cudaStream_t)stream), "avepool bwd");
+    return CAFFE_OK;
+}
+
+// ------------------------------------------------------------------ LRN
+static caffe_status lrn_validate(const caffe_lrn_desc* d) {
+    if (!d) return fail(CAFFE_E_INVALID, "desc is NULL");
+    if (d->local_size < 1 || d->local_size % 2 == 0) return fail(CAFFE_E_PARAM, "LRN local_size %d must be odd (S:216)", d->local_size);
+    if (!(d->k > 0.f) || !(d->beta > 0.f) || d->alpha < 0.f) return fail(CAFFE_E_PARAM, "LRN needs k > 0, beta > 0, alpha >= 0");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_lrn_forward(const caffe_lrn_desc* desc, const caffe_blob* bottom, caffe_blob* top, caffe_blob* scale,
+                               caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = lrn_validate(desc)) || (st = check_blob(bottom, "bottom")) || (st = check_blob(top, "top"))) return st;
+    if (!same_shape(bottom->shape, top->shape) || bottom->dtype != top->dtype) return fail(CAFFE_E_SHAPE, "top must match bottom");
+    if (scale) {
+        if ((st = check_blob(scale, "scale"))) return st;
+        if (scale->dtype != CAFFE_F32 || !same_shape(scale->shape, bottom->shape)) return fail(CAFFE_E_SHAPE, "scale must be F32 of bottom's shape");
+    }
+    if (overlap(top, bottom) || overlap(scale, bottom) || overlap(scale, top)) return fail(CAFFE_E_ALIAS, "LRN outputs overlap");
+    if (bottom->shape.n == 0) return CAFFE_OK;
+    const caffe_shape4& s = bottom->shape;
+    CK(lrn_fwd(bottom->ptr, top->ptr, scale ? (float*)scale->ptr : nullptr, bottom->dtype == CAFFE_BF16, s.n, s.c,
+               (long long)s.h * s.w, desc->local_size, desc->alpha, desc->beta, desc->k, (cudaStream_t)stream),
+       "lrn fwd");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_lrn_backward(const caffe_lrn_desc* desc, const caffe_blob* bottom, const caffe_blob* top,
+                                const caffe_blob* top_diff, const caffe_blob* scale, caffe_blob* bottom_diff,
+                                caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = lrn_validate(desc)) || (st = check_blob(bottom, "bottom")) || (st = check_blob(top, "top")) ||
+        (st = check_blob(top_diff, "top_diff")) || (st = check_blob(bottom_diff, "bottom_diff")))
+        return st;
+    const caffe_shape4& s = bottom->shape;
+    if (!same_shape(s, top->shape) || !same_shape(s, top_diff->shape) || !same_shape(s, bottom_diff->shape))
+        return fail(CAFFE_E_SHAPE, "LRN backward blobs must share bottom's shape");
+    const caffe_dtype dt = bottom->dtype;
+    if (top->dtype != dt || top_diff->dtype != dt || bottom_diff->dtype != dt) return fail(CAFFE_E_DTYPE, "LRN blobs must share one dtype");
+    if (scale) {
+        if ((st = check_blob(scale, "scale"))) return st;
+        if (scale->dtype != CAFFE_F32 || !same_shape(scale->shape, s)) return fail(CAFFE_E_SHAPE, "scale must be F32 of bottom's shape");
+    }
+    if (overlap(bottom_diff, bottom) || overlap(bottom_diff, top) || overlap(bottom_diff, top_diff) || overlap(bottom_diff, scale))
+        return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
+    if (s.n == 0) return CAFFE_OK;
+    CK(lrn_bwd(bottom->ptr, top->ptr, top_diff->ptr, scale ? (const float*)scale->ptr : nullptr, bottom_diff->ptr,
+               dt == CAFFE_BF16, s.n, s.c, (long long)s.h * s.w, desc->local_size, desc->alpha, desc->beta, desc->k,
+               (cudaStream_t)stream),
+       "lrn bwd");
+    return CAFFE_OK;
+}
+
+// ------------------------------------------------------------------ inner product
+static caffe_status ip_shapes(const caffe_blob* bottom, const caffe_blob* weight, long long* K, int* O) {
+    *K = (long long)bottom->shape.c * bottom->shape.h * bottom->shape.w;
+    *O = weight->shape.n;
+    if ((long long)weight->shape.c * weight->shape.h * weight->shape.w != *K)
+        return fail(CAFFE_E_SHAPE, "weight fan-in %lld != bottom C*H*W %lld (S:183)",
+                    (long long)weight->shape.c * weight->shape.h * weight->shape.w, *K);
+    return CAFFE_OK;
+}
+
+caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32_t O, int32_t pass, size_t* bytes) {
+    if (!bytes) return fail(CAFFE_E_INVALID, "bytes is NULL");
+    if (math == CAFFE_MATH_FP32) { *bytes = 0; return CAFFE_OK; }
+    if (math != CAFFE_MATH_BF16 && math != CAFFE_MATH_TF32) return fail(CAFFE_E_INVALID, "bad math mode");
+    const int E = math == CAFFE_MATH_TF32 ? 4 : 2, CHh = 128 / E;
+    const long long N = bottom.n, K = (long long)bottom.c * bottom.h * bottom.w;
+    // worst case: every operand staged
+    size_t s = align1k((size_t)N * rup(K, CHh) * E) + align1k((size_t)O * rup(K, CHh) * E) + align1k((size_t)N * rup(O, CHh) * E);
+    (void)pass;
+    *bytes = s;
+    return CAFFE_OK;
+}
+
+// stage src (rows x cols, ld = cols) into dst with padded ld, return pointer to use and its ld
+static cudaError_t stage(const caffe_blob* b, long long rows, long long cols, int E, char*& cursor, const void** out,
+                         long long* ld, cudaStream_t s) {
+    const bool ok = (E == 2 ? b->dtype == CAFFE_BF16 : false) && aligned16(b->ptr) && (cols * E) % 16 == 0;
+    if (ok) { *out = b->ptr; *ld = cols; return cudaSuccess; }
+    const long long ldp = rup(cols, 128 / E);
+    cudaError_t e = convert_pad_2d(b->ptr, b->dtype == CAFFE_BF16, cols, cursor, E, ldp, rows, cols, s);
+    *out = cursor;
+    *ld = ldp;
+    cursor += align1k((size_t)rows * ldp * E);
+    return e;
+}
+
+caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob* bottom, const caffe_blob* weight,
+                              const caffe_blob* bias, caffe_blob* top, void* ws, size_t ws_bytes, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom, "bottom")) || (st = check_blob(weight, "weight")) || (st = check_blob(top, "top"))) return st;
+    long long K; int O;
+    if ((st = ip_shapes(bottom, weight, &K, &O))) return st;
+    const int N = bottom->shape.n;
+    if (top->shape.n != N || top->shape.c != O || top->shape.h != 1 || top->shape.w != 1)
+        return fail(CAFFE_E_SHAPE, "top must be (%d,%d,1,1)", N, O);
+    if (bias) {
+        if ((st = check_blob(bias, "bias"))) return st;
+        if (bias->dtype != CAFFE_F32 || cnt(bias->shape) != O) return fail(CAFFE_E_SHAPE, "bias must be F32 with %d elements", O);
+    }
+    if (overlap(top, bottom) || overlap(top, weight) || overlap(top, bias)) return fail(CAFFE_E_ALIAS, "top overlaps an input");
+    if (math == CAFFE_MATH_TF32 && (bottom->dtype == CAFFE_BF16 || weight->dtype == CAFFE_BF16 || top->dtype == CAFFE_BF16))
+        return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
+    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16 && math != CAFFE_MATH_TF32) return fail(CAFFE_E_INVALID, "bad math");
+    if (N == 0) return CAFFE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int relu = (flags & CAFFE_FUSE_RELU) ? 1 : 0;
+    const float* bptr = bias ? (const float*)bias->ptr : nullptr;
+    if (math == CAFFE_MATH_FP32) {
+        ConvGeom g{N, bottom->shape.c, bottom->shape.h, bottom->shape.w, O, bottom->shape.h, bottom->shape.w, 1, 1, 0, 0, 1, 1, 1};
+        CK(fp32_conv_fwd(bottom->ptr, bottom->dtype == CAFFE_BF16, weight->ptr, weight->dtype == CAFFE_BF16, bptr, top->ptr,
+                         top->dtype == CAFFE_BF16, relu, g, s), "ip fwd fp32");
+        return CAFFE_OK;
+    }
+    size_t need;
+    caffe_ip_workspace_size(math, bottom->shape, O, 0, &need);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    const int E = math == CAFFE_MATH_TF32 ? 4 : 2;
+    char* cur = (char*)ws;
+    const void *A, *B;
+    long long lda, ldb;
+    CK(stage(bottom, N, K, E, cur, &A, &lda, s), "stage bottom");
+    CK(stage(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
+    TcLaunch L;
+    memset(&L, 0, sizeof L);
+    L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
+    TcArgs& a = L.args;
+    a.BN = choose_bn(O);
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 128 / E, 128) ||
+        !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 128 / E, a.BN))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip fwd)");
+    a.M = N; a.N = O; a.m_tiles = (int)cdiv(N, 128); a.n_tiles = (int)cdiv(O, a.BN); a.groups = 1; a.splits = 1;
+    a.kblocks = (int)cdiv(K, 128 / E); a.kb_per_split = a.kblocks;
+    a.out = top->ptr; a.out_bf16 = top->dtype == CAFFE_BF16; a.s_n = O; a.s_c = 1; a.s_p = 0; a.P = 1; a.col_g = 0;
+    a.bias = bptr; a.relu = relu; a.beta = 0.f;
+    finish_args(a, a.BN * 128);
+    return run_tc(L, s);
+}
+
+caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
+                                    caffe_blob* bottom_diff, float beta, void* ws, size_t ws_bytes, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(top_diff, "top_diff")) || (st = check_blob(weight, "weight")) ||
+        (st = check_blob(bottom_diff, "bottom_diff")))
+        return st;
+    long long K; int O;
+    if ((st = ip_shapes(bottom_diff, weight, &K, &O))) return st;
+    const int N = bottom_diff->shape.n;
+    if (top_diff->shape.n != N || top_diff->shape.c != O || top_diff->shape.h != 1 || top_diff->shape.w != 1)
+        return fail(CAFFE_E_SHAPE, "top_diff must be (%d,%d,1,1)", N, O);
+    if (overlap(bottom_diff, top_diff) || overlap(bottom_diff, weight)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
+    if (math == CAFFE_MATH_TF32) return fail(CAFFE_E_DTYPE, "TF32 inner-product backward not built yet");
+    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16) return fail(CAFFE_E_INVALID, "bad math");
+    if (N == 0) return CAFFE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (math == CAFFE_MATH_FP32) {
+        ConvGeom g{N, bottom_diff->shape.c, bottom_diff->shape.h, bottom_diff->shape.w, O, bottom_diff->shape.h,
+                   bottom_diff->shape.w, 1, 1, 0, 0, 1, 1, 1};
+        CK(fp32_conv_dgrad(top_diff->ptr, top_diff->dtype == CAFFE_BF16, weight->ptr, weight->dtype == CAFFE_BF16,
+                           bottom_diff->ptr, bottom_diff->dtype == CAFFE_BF16, beta, g, s), "ip dgrad fp32");
+        return CAFFE_OK;
+    }
+    size_t need;
+    caffe_ip_workspace_size(math, bottom_diff->shape, O, 1, &need);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    const int E = 2;
+    char* cur = (char*)ws;
+    const void *A, *B;
+    long long lda, ldb;
+    CK(stage(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
+    CK(stage(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
+    TcLaunch L;
+    memset(&L, 0, sizeof L);
+    L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
+    TcArgs& a = L.args;
+    a.BN = choose_bn((int)(K < 256 ? K : 256));
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 128) || !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 64, 64))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip dgrad)");
+    a.M = N; a.N = (int)K; a.m_tiles = (int)cdiv(N, 128); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1; a.splits = 1;
+    a.kblocks = (int)cdiv(O, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
+    a.out = bottom_diff->ptr; a.out_bf16 = bottom_diff->dtype == CAFFE_BF16; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1;
+    a.beta = beta;
+    finish_args(a, a.b_nchunks * 64 * 128);
+    return run_tc(L, s);
+}
+
+caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom, const caffe_blob* top_diff,
+                                      caffe_blob* weight_diff, caffe_blob* bias_diff, float beta, void* ws, size_t ws_bytes,
+                                      caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom, "bottom")) || (st = check_blob(top_diff, "top_diff")) ||
+        (st = check_blob(weight_diff, "weight_diff")))
+        return st;
+    long long K; int O;
+    if ((st = ip_shapes(bottom, weight_diff, &K, &O))) return st;
+    const int N = bottom->shape.n;
+    if (top_diff->shape.n != N || top_diff->shape.c != O || top_diff->shape.h != 1 || top_diff->shape.w != 1)
+        return fail(CAFFE_E_SHAPE, "top_diff must be (%d,%d,1,1)", N, O);
+    if (weight_diff->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "weight_diff must be F32");
+    if (bias_diff) {
+        if ((st = check_blob(bias_diff, "bias_diff"))) return st;
+        if (bias_diff->dtype != CAFFE_F32 || cnt(bias_diff->shape) != O) return fail(CAFFE_E_SHAPE, "bias_diff must be F32 with %d elements", O);
+    }
+    if (overlap(weight_diff, bottom) || overlap(weight_diff, top_diff) || overlap(bias_diff, bottom) ||
+        overlap(bias_diff, top_diff) || overlap(bias_diff, weight_diff))
+        return fail(CAFFE_E_ALIAS, "weight_diff/bias_diff overlaps an input");
+    if (math == CAFFE_MATH_TF32) return fail(CAFFE_E_DTYPE, "TF32 inner-product backward not built yet");
+    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16) return fail(CAFFE_E_INVALID, "bad math");
+    if (N == 0) return CAFFE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (bias_diff) CK(bias_grad(top_diff->ptr, top_diff->dtype == CAFFE_BF16, (float*)bias_diff->ptr, beta, N, O, 1, s), "ip bias grad");
+    if (math == CAFFE_MATH_FP32) {
+        ConvGeom g{N, bottom->shape.c, bottom->shape.h, bottom->shape.w, O, bottom->shape.h, bottom->shape.w, 1, 1, 0, 0, 1, 1, 1};
+        CK(fp32_conv_wgrad(bottom->ptr, bottom->dtype == CAFFE_BF16, top_diff->ptr, top_diff->dtype == CAFFE_BF16,
+                           (float*)weight_diff->ptr, beta, g, s), "ip wgrad fp32");
+        return CAFFE_OK;
+    }
+    size_t need;
+    caffe_ip_workspace_size(math, bottom->shape, O, 2, &need);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    const int E = 2;
+    char* cur = (char*)ws;
+    const void *A, *B;
+    long long lda, ldb;
+    CK(stage(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
+    CK(stage(bottom, N, K, E, cur, &B, &ldb, s), "stage bottom");
+    TcLaunch L;
+    memset(&L, 0, sizeof L);
+    L.esz = E; L.amode = A_TILED_MN; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
+    TcArgs& a = L.args;
+    a.BN = choose_bn((int)(K < 256 ? K : 256));
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, 64, 64))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip wgrad)");
+    a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1; a.splits = 1;
+    a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
+    a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
+    finish_args(a, a.b_nchunks * 64 * 128);
+    return run_tc(L, s);
+}
+
+// ------------------------------------------------------------------ im2col / col2im
+caffe_status caffe_im2col(const caffe_conv_desc* desc, const caffe_blob* bottom, int32_t n, caffe_blob* col,
+                          caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom, "bottom")) || (st = check_blob(col, "col"))) return st;
+    if (bottom->dtype != CAFFE_F32 || col->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "im2col is F32 only");
+    caffe_conv_desc d = *desc;
+    d.group = 1;
+    Plan p;
+    if ((st = conv_validate(&d, bottom->shape, 1, &p))) return st;
+    if (n < 0 || n >= bottom->shape.n) return fail(CAFFE_E_PARAM, "image index %d out of range", n);
+    if (cnt(col->shape) != (long long)p.C * p.kh * p.kw * p.OH * p.OW) return fail(CAFFE_E_SHAPE, "col must hold C*kh*kw*OH*OW elements");
+    if (overlap(col, bottom)) return fail(CAFFE_E_ALIAS, "col overlaps bottom");
+    CK(im2col_k((const float*)bottom->ptr, n, cgeom(p), (float*)col->ptr, (cudaStream_t)stream), "im2col");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_col2im(const caffe_conv_desc* desc, const caffe_blob* col, int32_t n, caffe_blob* bottom_diff,
+                          caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom_diff, "bottom_diff")) || (st = check_blob(col, "col"))) return st;
+    if (bottom_diff->dtype != CAFFE_F32 || col->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "col2im is F32 only");
+    caffe_conv_desc d = *desc;
+    d.group = 1;
+    Plan p;
+    if ((st = conv_validate(&d, bottom_diff->shape, 1, &p))) return st;
+    if (n < 0 || n >= bottom_diff->shape.n) return fail(CAFFE_E_PARAM, "image index %d out of range", n);
+    if (cnt(col->shape) != (long long)p.C * p.kh * p.kw * p.OH * p.OW) return fail(CAFFE_E_SHAPE, "col must hold C*kh*kw*OH*OW elements");
+    if (overlap(col, bottom_diff)) return fail(CAFFE_E_ALIAS, "col overlaps bottom_diff");
+    CK(col2im_k((const float*)col->ptr, n, cgeom(p), (float*)bottom_diff->ptr, (cudaStream_t)stream), "col2im");
+    return CAFFE_OK;
+}
+
+// ------------------------------------------------------------------ glue
+caffe_status caffe_softmax_loss(const caffe_blob* scores, const int32_t* labels, float* loss, caffe_blob* score_diff,
+                                caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(scores, "scores"))) return st;
+    if (!labels || !loss) return fail(CAFFE_E_INVALID, "labels and loss are required");
+    const int N = scores->shape.n;
+    const long long K = (long long)scores->shape.c * scores->shape.h * scores->shape.w;
+    if (score_diff) {
+        if ((st = check_blob(score_diff, "score_diff"))) return st;
+        if (!same_shape(score_diff->shape, scores->shape)) return fail(CAFFE_E_SHAPE, "score_diff must match scores");
+        if (overlap(score_diff, scores)) return fail(CAFFE_E_ALIAS, "score_diff overlaps scores");
+    }
+    if (N == 0) return CAFFE_OK;
+    CK(softmax_loss_k(scores->ptr, scores->dtype == CAFFE_BF16, labels, loss, score_diff ? score_diff->ptr : nullptr,
+                      score_diff ? score_diff->dtype == CAFFE_BF16 : 0, N, (int)K, (cudaStream_t)stream),
+       "softmax loss");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_sgd_update(float* w, const float* g, float* v, void* w_bf16, int64_t count, float lr, float momentum,
+                              float decay, float grad_scale, caffe_stream_t stream) {
+    if (count < 0) return fail(CAFFE_E_SHAPE, "negative count");
+    if (count == 0) return CAFFE_OK;
+    if (!w || !g || !v) return fail(CAFFE_E_INVALID, "w, g and v are required");
+    CK(sgd_k(w, g, v, w_bf16, count, lr, momentum, decay, grad_scale, (cudaStream_t)stream), "sgd update");
+    return CAFFE_OK;
+}
+
+}  // extern "C"

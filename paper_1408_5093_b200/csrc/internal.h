@@ -1,0 +1,123 @@
+// internal.h -- declarations shared by the C-ABI host code and the kernel files.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda.h>
+
+namespace cb {
+
+// ------------------------------------------------------------------ tensor-core GEMM (tc_gemm.cu)
+// D[m, n] = sum_k A[m, k] * B[n, k], A/B staged by TMA in 128-byte-swizzled shared memory,
+// tcgen05.mma (M=128, N=BN, K=16 bf16 / 8 tf32) accumulating FP32 in TMEM.
+enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3 };
+enum BMode { B_TILED_K = 0, B_TILED_MN = 1 };
+enum EpiMode { EPI_STRIDED = 0, EPI_PARTIAL = 1 };
+
+struct TcArgs {
+    int M, N, BN;                       // valid rows, valid cols (per group), N tile
+    int m_tiles, n_tiles, groups, splits, units;
+    int kblocks, kb_per_split;          // reduction blocks (of 128 bytes of K per row)
+    int stages, b_stage_bytes, acc_stride, tmem_cols;
+    // A geometry
+    int a_P, a_OW;                      // im2col: pixels per image / output width (m -> n, y, x)
+    int a_pad_h, a_pad_w, a_kw, a_cblocks, a_cpg;
+    int a_nchunks_total;                // A_IM2COL_MN: number of (tap, channel-block) chunks
+    int a_row_g;                        // tiled A: row offset per group
+    // B geometry
+    int b_row_g;                        // B_TILED_K: row offset per group
+    int b_col_g;                        // B_TILED_MN: column offset per group
+    int b_nchunks;                      // B_TILED_MN: chunks per tile
+    // epilogue
+    void* out;
+    int out_bf16;
+    long long s_n, s_c, s_p;            // element strides of (image, column, pixel)
+    int P;                              // pixels per image (m -> image, pixel)
+    int col_g;                          // output column offset per group
+    const float* bias;
+    int relu;
+    float beta;
+    float* partial;                     // EPI_PARTIAL: [unit][BN][128] fp32
+};
+
+struct TcLaunch {
+    CUtensorMap mapA, mapB;
+    TcArgs args;
+    int esz;                            // 2 = bf16 (kind::f16), 4 = fp32 (kind::tf32)
+    int amode, bmode, epi;
+    int grid;
+};
+
+size_t tc_smem_bytes(const TcArgs& a);
+cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s);
+int num_sms();
+
+// TMA descriptor encoders (driver entry points resolved at runtime; no -lcuda needed).
+bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                     uint32_t box_inner, uint32_t box_outer);
+bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
+                      int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels);
+
+// ------------------------------------------------------------------ packing kernels (pack.cu)
+// Activation NCHW -> packed NHWC [N][Hp][Wp][G*Cgp] in bf16 (esz 2) or tf32-rounded fp32 (esz 4).
+// Space-to-depth for stride s>1: channel (dy*sw+dx)*Cg+c of packed pixel (Y,X) is
+// X[n][g*Cg+c][Y*sh+dy-ph][X*sw+dx-pw] (0 outside); for s=1 (no s2d) the padding is left to TMA.
+struct PackGeom {
+    int N, C, H, W, G, Cg;              // source (NCHW) geometry
+    int sh, sw, ph, pw;                 // s2d block (1,1 = plain transpose) and the pad folded into s2d
+    int Hp, Wp, Cgp;                    // packed geometry
+};
+cudaError_t pack_nhwc(const void* src, int src_bf16, void* dst, int dst_esz, const PackGeom& g, cudaStream_t s);
+// Inverse for the s2d data gradient: dX[n][c][h][w] = beta*dX + T[n][(h+ph)/sh][(w+pw)/sw][g*Cgp+((h+ph)%sh*sw+(w+pw)%sw)*Cg+c]
+cudaError_t unpack_s2d_grad(const float* T, void* dX, int dx_bf16, float beta, const PackGeom& g, cudaStream_t s);
+// Weights (O, Cg, kh, kw) -> forward B operand [G*Og rows][taps'*Cgp] (s2d-aware).
+struct WGeom {
+    int O, G, Cg, Og, kh, kw, sh, sw;   // original filter geometry (sh,sw = s2d block)
+    int khp, kwp, Cgp, Ogp;             // effective (s2d) kernel, padded channels
+};
+cudaError_t repack_w_fwd(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, cudaStream_t s);
+// dgrad B operand [G*Cge rows][taps'*Ogp]: row (g, c''), k = (i',j', o), value = fwd-packed W at
+// (g*Og+o, kh'-1-i', kw'-1-j', c'')  (flip + transpose); Cge = Cg*sh*sw.
+cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, int Cge,
+                           cudaStream_t s);
+// Deterministic fixed-order reduction of wgrad partials into dW (O, Cg, kh, kw) fp32 with beta.
+cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
+                         int splits, int BN, int chunk, int cblocks, cudaStream_t s);
+// Generic 2-D convert/pad: dst[r][c] (ld_dst, esz) = src[r][c] (ld_src, f32|bf16) for c < cols, 0 up to ld_dst.
+cudaError_t convert_pad_2d(const void* src, int src_bf16, long long ld_src, void* dst, int dst_esz,
+                           long long ld_dst, long long rows, long long cols, cudaStream_t s);
+
+// ------------------------------------------------------------------ CUDA-core kernels (simple.cu)
+struct ConvGeom {
+    int N, C, H, W, O, kh, kw, sh, sw, ph, pw, G, OH, OW;
+};
+cudaError_t fp32_conv_fwd(const void* x, int x_bf16, const void* w, int w_bf16, const float* b, void* y, int y_bf16,
+                          int relu, const ConvGeom& g, cudaStream_t s);
+cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, const void* w, int w_bf16, void* dx, int dx_bf16,
+                            float beta, const ConvGeom& g, cudaStream_t s);
+cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, const void* dy, int dy_bf16, float* dw, float beta,
+                            const ConvGeom& g, cudaStream_t s);
+cudaError_t bias_grad(const void* dy, int dy_bf16, float* db, float beta, int N, int O, long long P,
+                      cudaStream_t s);
+cudaError_t im2col_k(const float* x, int n, const ConvGeom& g, float* col, cudaStream_t s);
+cudaError_t col2im_k(const float* col, int n, const ConvGeom& g, float* dx, cudaStream_t s);
+cudaError_t relu_fwd(const void* x, void* y, int bf16, long long count, cudaStream_t s);
+cudaError_t relu_bwd(const void* x, const void* dy, void* dx, int x_bf16, int d_bf16, long long count,
+                     cudaStream_t s);
+struct PoolGeom {
+    int N, C, H, W, kh, kw, sh, sw, ph, pw, OH, OW;
+};
+cudaError_t maxpool_fwd(const void* x, void* y, int32_t* mask, int bf16, const PoolGeom& g, cudaStream_t s);
+cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, void* dx, int bf16, const PoolGeom& g, cudaStream_t s);
+cudaError_t avepool_fwd(const void* x, void* y, int bf16, const PoolGeom& g, cudaStream_t s);
+cudaError_t avepool_bwd(const void* dy, void* dx, int bf16, const PoolGeom& g, cudaStream_t s);
+cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int N, int C, long long P, int size,
+                    float alpha, float beta, float k, cudaStream_t s);
+cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* scale, void* dx, int bf16, int N,
+                    int C, long long P, int size, float alpha, float beta, float k, cudaStream_t s);
+cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff,
+                           int diff_bf16, int N, int K, cudaStream_t s);
+cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,
+                  float decay, float gscale, cudaStream_t s);
+
+}  // namespace cb

@@ -1,0 +1,343 @@
+// tc_gemm.cu -- the tensor-core core of the hot path: one persistent, warp-specialised
+// tcgen05 GEMM whose operand loaders understand convolution (TMA im2col mode over packed
+// NHWC activations) as well as plain 2-D tiles.  The same kernel serves
+//   conv forward            (A = im2col(X) K-major, B = repacked W K-major, NCHW epilogue, bias+ReLU)
+//   conv backward-data s=1  (A = im2col(dY) with pad k-1-p K-major, B = flipped W^T K-major)
+//   conv backward-weight    (A = im2col(X) MN-major, B = dY NHWC MN-major, split-K partials)
+//   inner product f/d/w     (plain 2-D tiles, K- or MN-major)
+// Paper: the conv layer's forward/backward contract P:156 (Sec. 3.2); formulas S:145.
+//
+// Roles (256 threads, 1 CTA per SM, persistent over work units):
+//   warp 0 lane 0 : TMA producer          (smem ring: full/empty mbarriers)
+//   warp 1 lane 0 : tcgen05.mma issuer    (accumulator double buffer in TMEM)
+//   warp 2        : TMEM allocator
+//   warps 4..7    : epilogue (tcgen05.ld -> bias/ReLU/beta -> global), TMEM lanes 32*(w-4)..
+#include "internal.h"
+#include "ptx.cuh"
+
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <mutex>
+
+namespace cb {
+
+constexpr int BM = 128;
+constexpr int A_STAGE_BYTES = 16384;   // 128 rows x 128 B
+constexpr int SMEM_ALIGN = 1024;
+
+size_t tc_smem_bytes(const TcArgs& a) {
+    return (size_t)a.stages * (A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + SMEM_ALIGN;
+}
+
+template <int ESZ, int AMODE, int BMODE, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const TcArgs args) {
+    constexpr int CH = 128 / ESZ;          // elements per 128-byte row (= K per stage, = MN per chunk)
+    constexpr int UMMA_K = 32 / ESZ;       // K per tcgen05.mma
+    constexpr int KSTEPS = CH / UMMA_K;    // MMAs per stage (4)
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + SMEM_ALIGN - 1) &
+                                               ~uintptr_t(SMEM_ALIGN - 1));
+    const int stages = args.stages;
+    const int stage_bytes = A_STAGE_BYTES + args.b_stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+    uint64_t* empty = full + stages;
+    uint64_t* tfull = empty + stages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&mapA);
+        tma_prefetch(&mapB);
+        for (int i = 0; i < stages; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_holder, args.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0 && lane == 0) {
+        // ===================== TMA producer =====================
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t tx = A_STAGE_BYTES + (BMODE == B_TILED_K ? args.BN * 128 : args.b_nchunks * CH * 128);
+        for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+            int t = u;
+            const int n_tile = t % args.n_tiles; t /= args.n_tiles;
+            const int m_tile = t % args.m_tiles; t /= args.m_tiles;
+            const int g = t % args.groups;
+            const int split = t / args.groups;
+            const int kb0 = split * args.kb_per_split;
+            const int kb1 = min(args.kblocks, kb0 + args.kb_per_split);
+            // per-tile A base for K-major im2col
+            int an = 0, ay = 0, ax = 0;
+            if (AMODE == A_IM2COL_K) {
+                const int m0 = m_tile * BM;
+                an = m0 / args.a_P;
+                const int r = m0 - an * args.a_P;
+                ay = r / args.a_OW;
+                ax = r - ay * args.a_OW;
+            }
+            for (int kb = kb0; kb < kb1; kb++) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * stage_bytes;
+                uint8_t* sb = sa + A_STAGE_BYTES;
+                mbar_arrive_expect_tx(&full[stage], tx);
+                // ---- A
+                if (AMODE == A_TILED_K) {
+                    tma_load_2d(sa, &mapA, &full[stage], kb * CH, g * args.a_row_g + m_tile * BM);
+                } else if (AMODE == A_IM2COL_K) {
+                    const int tap = kb / args.a_cblocks, cbk = kb - tap * args.a_cblocks;
+                    const int i = tap / args.a_kw, j = tap - i * args.a_kw;
+                    tma_load_im2col_4d(sa, &mapA, &full[stage], g * args.a_cpg + cbk * CH, ax - args.a_pad_w,
+                                       ay - args.a_pad_h, an, (uint16_t)j, (uint16_t)i);
+                } else if (AMODE == A_IM2COL_MN) {
+                    const int m0 = kb * CH;   // first pixel of this reduction block
+                    const int n0 = m0 / args.a_P;
+                    const int r = m0 - n0 * args.a_P;
+                    const int y0 = r / args.a_OW, x0 = r - (r / args.a_OW) * args.a_OW;
+#pragma unroll
+                    for (int q = 0; q < ESZ; q++) {   // 128 rows of M = ESZ chunks of CH
+                        int chunk = m_tile * ESZ + q;
+                        if (chunk >= args.a_nchunks_total) chunk = args.a_nchunks_total - 1;  // rows discarded
+                        const int tap = chunk / args.a_cblocks, cbk = chunk - tap * args.a_cblocks;
+                        const int i = tap / args.a_kw, j = tap - i * args.a_kw;
+                        tma_load_im2col_4d(sa + q * CH * 128, &mapA, &full[stage], g * args.a_cpg + cbk * CH,
+                                           x0 - args.a_pad_w, y0 - args.a_pad_h, n0, (uint16_t)j, (uint16_t)i);
+                    }
+                } else {  // A_TILED_MN
+#pragma unroll
+                    for (int q = 0; q < ESZ; q++)
+                        tma_load_2d(sa + q * CH * 128, &mapA, &full[stage], g * args.a_row_g + m_tile * BM + q * CH,
+                                    kb * CH);
+                }
+                // ---- B
+                if (BMODE == B_TILED_K) {
+                    tma_load_2d(sb, &mapB, &full[stage], kb * CH, g * args.b_row_g + n_tile * args.BN);
+                } else {
+                    for (int q = 0; q < args.b_nchunks; q++)
+                        tma_load_2d(sb + q * CH * 128, &mapB, &full[stage],
+                                    g * args.b_col_g + n_tile * args.BN + q * CH, kb * CH);
+                }
+                if (++stage == stages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ===================== MMA issuer =====================
+        // instruction descriptor: D=f32, A/B format (bf16=1, tf32=2), majors, N>>3, M>>4
+        const uint32_t fmt = (ESZ == 2) ? 1u : 2u;
+        const uint32_t a_mn = (AMODE == A_IM2COL_MN || AMODE == A_TILED_MN) ? 1u : 0u;
+        const uint32_t b_mn = (BMODE == B_TILED_MN) ? 1u : 0u;
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn << 15) | (b_mn << 16) |
+                               ((uint32_t)(args.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+            int t = u / (args.n_tiles * args.m_tiles);
+            const int split = t / args.groups;
+            const int kb0 = split * args.kb_per_split;
+            const int kb1 = min(args.kblocks, kb0 + args.kb_per_split);
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * args.acc_stride;
+            for (int kb = kb0; kb < kb1; kb++) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+                const uint32_t sb = sa + A_STAGE_BYTES;
+#pragma unroll
+                for (int k = 0; k < KSTEPS; k++) {
+                    uint64_t ad, bd;
+                    if (a_mn) ad = smem_desc_sw128(sa + k * UMMA_K * 128, CH * 128, 1024);
+                    else      ad = smem_desc_sw128(sa + k * 32, 16, 1024);
+                    if (b_mn) bd = smem_desc_sw128(sb + k * UMMA_K * 128, CH * 128, 1024);
+                    else      bd = smem_desc_sw128(sb + k * 32, 16, 1024);
+                    umma<ESZ>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                }
+                umma_commit(&empty[stage]);
+                if (++stage == stages) { stage = 0; phase ^= 1; }
+            }
+            umma_commit(&tfull[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue =====================
+        const int q = warp - 4;
+        const int row = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+            int t = u;
+            const int n_tile = t % args.n_tiles; t /= args.n_tiles;
+            const int m_tile = t % args.m_tiles; t /= args.m_tiles;
+            const int g = t % args.groups;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * args.acc_stride;
+            if (EPI == EPI_PARTIAL) {
+                float* dst = args.partial + (size_t)u * args.BN * BM + row;
+                for (int c0 = 0; c0 < args.BN; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(taddr + c0, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; j++) dst[(size_t)(c0 + j) * BM] = __uint_as_float(v[j]);
+                }
+            } else {
+                const long long m = (long long)m_tile * BM + row;
+                const bool row_ok = m < args.M;
+                const long long img = m / args.P, pix = m - img * args.P;
+                const long long rbase = img * args.s_n + pix * args.s_p;
+                const int col0 = n_tile * args.BN;
+                for (int c0 = 0; c0 < args.BN; c0 += 16) {
+                    if (col0 + c0 >= args.N) break;  // warp-uniform
+                    uint32_t v[16];
+                    tmem_ld16(taddr + c0, v);
+                    tmem_wait_ld();
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 16; j++) {
+                            const int col = col0 + c0 + j;
+                            if (col < args.N) {
+                                const int oc = g * args.col_g + col;
+                                float x = __uint_as_float(v[j]);
+                                if (args.bias) x += args.bias[oc];
+                                const long long off = rbase + (long long)oc * args.s_c;
+                                if (args.out_bf16) {
+                                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + off;
+                                    if (args.beta != 0.f) x += args.beta * __bfloat162float(*o);
+                                    if (args.relu) x = x > 0.f ? x : 0.f;
+                                    *o = __float2bfloat16_rn(x);
+                                } else {
+                                    float* o = reinterpret_cast<float*>(args.out) + off;
+                                    if (args.beta != 0.f) x += args.beta * *o;
+                                    if (args.relu) x = x > 0.f ? x : 0.f;
+                                    *o = x;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, args.tmem_cols);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int ESZ, int AM, int BMd, int EP>
+static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
+    auto kern = tc_gemm_kernel<ESZ, AM, BMd, EP>;
+    const size_t smem = tc_smem_bytes(L.args);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+    return cudaGetLastError();
+}
+
+#define TC_CASE(E, A, B, P)                                                          \
+    if (L.esz == E && L.amode == A && L.bmode == B && L.epi == P) return launch_one<E, A, B, P>(L, s);
+
+cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s) {
+    TC_CASE(2, A_IM2COL_K, B_TILED_K, EPI_STRIDED)
+    TC_CASE(2, A_IM2COL_MN, B_TILED_MN, EPI_PARTIAL)
+    TC_CASE(2, A_TILED_K, B_TILED_K, EPI_STRIDED)
+    TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_STRIDED)
+    TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED)
+    TC_CASE(4, A_IM2COL_K, B_TILED_K, EPI_STRIDED)
+    TC_CASE(4, A_TILED_K, B_TILED_K, EPI_STRIDED)
+    return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ TMA descriptor encoding
+typedef CUresult (*PFN_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_im2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_tiled g_tiled = nullptr;
+static PFN_im2col g_im2col = nullptr;
+
+static bool resolve() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_tiled = reinterpret_cast<PFN_tiled>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_im2col = reinterpret_cast<PFN_im2col>(p);
+    });
+    return g_tiled && g_im2col;
+}
+
+bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                     uint32_t box_inner, uint32_t box_outer) {
+    if (!resolve()) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
+                      int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels) {
+    if (!resolve()) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)C * esz, (cuuint64_t)C * W * esz, (cuuint64_t)C * W * H * esz};
+    int lower[2] = {-pad_lo_w, -pad_lo_h};
+    int upper[2] = {up_w, up_h};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = g_im2col(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                          const_cast<void*>(base), dims, strides, lower, upper, channels, pixels, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace cb

@@ -1,0 +1,221 @@
+"""Straight-line CaffeNet / LeNet training steps over the C ABI (host orchestration only).
+
+The paper's nets (Fig. 1 LeNet; P:117-119 reference "AlexNet with variations",
+i.e. CaffeNet) are linear chains, so the DAG bookkeeping of P:162-165 reduces to a fixed
+call list.  Every layer call goes to libcaffe_b200.so; this module only allocates blobs,
+wires them and orders the calls.
+
+Layout: activations and their diffs in BF16 (or F32), parameters as one flat FP32 master
+buffer (weights and biases), one flat FP32 gradient buffer (the data-parallel allreduce unit),
+one flat FP32 momentum buffer and one flat BF16 copy of the weights consumed by the BF16
+tensor-core operands.  The SGD update writes the BF16 copy as a side output.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+import paper_1408_5093_b200 as cb
+
+
+@dataclass
+class Layer:
+    kind: str                 # conv | pool | lrn | ip | loss
+    name: str
+    num_output: int = 0
+    kernel: int = 0
+    stride: int = 1
+    pad: int = 0
+    group: int = 1
+    relu: bool = False
+    method: str = "max"
+    w_std: float = 0.0        # gaussian std (0 -> xavier)
+    b_init: float = 0.0
+
+
+# CaffeNet (bvlc_reference_caffenet topology; SURVEY Sec. 8 shapes): conv1 -> relu1 -> pool1 -> norm1 ...
+CAFFENET: List[Layer] = [
+    Layer("conv", "conv1", 96, 11, 4, 0, 1, True, w_std=0.01, b_init=0.0),
+    Layer("pool", "pool1", kernel=3, stride=2),
+    Layer("lrn", "norm1"),
+    Layer("conv", "conv2", 256, 5, 1, 2, 2, True, w_std=0.01, b_init=1.0),
+    Layer("pool", "pool2", kernel=3, stride=2),
+    Layer("lrn", "norm2"),
+    Layer("conv", "conv3", 384, 3, 1, 1, 1, True, w_std=0.01, b_init=0.0),
+    Layer("conv", "conv4", 384, 3, 1, 1, 2, True, w_std=0.01, b_init=1.0),
+    Layer("conv", "conv5", 256, 3, 1, 1, 2, True, w_std=0.01, b_init=1.0),
+    Layer("pool", "pool5", kernel=3, stride=2),
+    Layer("ip", "fc6", 4096, relu=True, w_std=0.005, b_init=1.0),
+    Layer("ip", "fc7", 4096, relu=True, w_std=0.005, b_init=1.0),
+    Layer("ip", "fc8", 1000, w_std=0.01, b_init=0.0),
+    Layer("loss", "loss"),
+]
+CAFFENET_INPUT = (3, 227, 227)
+
+# LeNet (Fig. 1): conv1 20@5x5 -> pool 2x2/2 -> conv2 50@5x5 -> pool -> ip1 500 -> relu -> ip2 10
+LENET: List[Layer] = [
+    Layer("conv", "conv1", 20, 5, 1, 0, 1, False),
+    Layer("pool", "pool1", kernel=2, stride=2),
+    Layer("conv", "conv2", 50, 5, 1, 0, 1, False),
+    Layer("pool", "pool2", kernel=2, stride=2),
+    Layer("ip", "ip1", 500, relu=True),
+    Layer("ip", "ip2", 10),
+    Layer("loss", "loss"),
+]
+LENET_INPUT = (1, 28, 28)
+
+LRN = dict(local_size=5, alpha=1e-4, beta=0.75, k=1.0)
+
+
+def conv_flops(in_shape, L: Layer) -> Tuple[int, Tuple[int, int, int, int]]:
+    """Algorithmic FLOPs of one conv pass (2 * MACs) and the output shape."""
+    N, C, H, W = in_shape
+    OH = (H + 2 * L.pad - L.kernel) // L.stride + 1
+    OW = (W + 2 * L.pad - L.kernel) // L.stride + 1
+    macs = N * L.num_output * OH * OW * (C // L.group) * L.kernel * L.kernel
+    return 2 * macs, (N, L.num_output, OH, OW)
+
+
+class Net:
+    def __init__(self, layers: List[Layer], batch: int, input_shape, device, act_dtype=None, math="bf16", seed=0):
+        import torch
+        import synth
+        self.torch = torch
+        self.layers = layers
+        self.batch = batch
+        self.device = device
+        self.math = math
+        self.act_dtype = act_dtype or (torch.bfloat16 if math == "bf16" else torch.float32)
+        self.shapes = []            # input shape of each layer
+        shape = (batch,) + tuple(input_shape)
+        pspecs = []                 # (layer idx, w_shape, b_shape)
+        self.conv_flops_fwd = 0
+        self.conv_flops_step = 0    # fwd + wgrad + dgrad (no dgrad for the first layer)
+        for i, L in enumerate(layers):
+            self.shapes.append(shape)
+            if L.kind == "conv":
+                f, out = conv_flops(shape, L)
+                self.conv_flops_fwd += f
+                self.conv_flops_step += 2 * f + (f if i > 0 else 0)
+                pspecs.append((i, (L.num_output, shape[1] // L.group, L.kernel, L.kernel), (L.num_output,)))
+                shape = out
+            elif L.kind == "pool":
+                shape = cb.pool_output_shape(shape, L.method, L.kernel, L.stride, L.pad)
+            elif L.kind == "ip":
+                K = int(np.prod(shape[1:]))
+                pspecs.append((i, (L.num_output, K), (L.num_output,)))
+                shape = (batch, L.num_output)
+            elif L.kind == "lrn":
+                pass
+        self.out_shape = shape
+        # flat parameter storage: [w0, b0, w1, b1, ...]
+        offs, total = [], 0
+        for (_, ws, bs) in pspecs:
+            nw, nb = int(np.prod(ws)), int(np.prod(bs))
+            offs.append((total, nw, total + nw, nb))
+            total += nw + nb
+            total = (total + 63) // 64 * 64  # 256-byte alignment of every tensor
+        self.nparams = total
+        f32 = torch.float32
+        self.params = torch.zeros(total, dtype=f32, device=device)
+        self.grads = torch.zeros(total, dtype=f32, device=device)
+        self.mom = torch.zeros(total, dtype=f32, device=device)
+        self.params_bf16 = torch.zeros(total, dtype=torch.bfloat16, device=device)
+        self.W, self.B, self.dW, self.dB, self.Wq = {}, {}, {}, {}, {}
+        host = np.zeros(total, np.float32)
+        for k, ((i, ws, bs), (ow, nw, ob, nb)) in enumerate(zip(pspecs, offs)):
+            L = layers[i]
+            w = synth.gaussian(ws, L.w_std, seed, synth.S_W, k) if L.w_std > 0 else synth.xavier(ws, seed, synth.S_W, k)
+            host[ow:ow + nw] = w.ravel()
+            host[ob:ob + nb] = L.b_init
+            self.W[i] = self.params[ow:ow + nw].view(ws)
+            self.B[i] = self.params[ob:ob + nb]
+            self.dW[i] = self.grads[ow:ow + nw].view(ws)
+            self.dB[i] = self.grads[ob:ob + nb]
+            self.Wq[i] = self.params_bf16[ow:ow + nw].view(ws)
+        self.params.copy_(torch.from_numpy(host))
+        self.params_bf16.copy_(self.params.to(torch.bfloat16))
+        self.pspecs = pspecs
+        # activations: a[i] = input of layer i; d[i] = diff w.r.t. a[i]
+        self.a, self.d, self.mask = [], [], {}
+        ad = self.act_dtype
+        for i, L in enumerate(layers):
+            s = self.shapes[i]
+            self.a.append(torch.empty(s, dtype=ad, device=device))
+            self.d.append(torch.empty(s, dtype=ad, device=device) if i > 0 else None)
+        self.scores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
+        self.dscores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
+        for i, L in enumerate(layers):
+            if L.kind == "pool":
+                out = self.shapes[i + 1]
+                self.mask[i] = torch.empty(out, dtype=torch.int32, device=device)
+        self.labels = torch.zeros(batch, dtype=torch.int32, device=device)
+        self.loss = torch.zeros((), dtype=torch.float32, device=device)
+
+    # --------------------------------------------------------------- one training iteration
+    def _wop(self, i):
+        return self.Wq[i] if self.math == "bf16" else self.W[i]
+
+    def forward(self):
+        a, n = self.a, len(self.layers)
+        for i, L in enumerate(self.layers):
+            x = a[i]
+            nxt = a[i + 1] if i + 1 < n - 1 else None
+            if L.kind == "conv":
+                cb.conv_forward(x, self._wop(i), self.B[i], L.stride, L.pad, L.group, self.math, relu=L.relu, out=nxt)
+            elif L.kind == "pool":
+                cb.pool_forward(x, L.method, L.kernel, L.stride, L.pad, out=nxt, mask=self.mask[i])
+            elif L.kind == "lrn":
+                cb.lrn_forward(x, **LRN, out=nxt)
+            elif L.kind == "ip":
+                out = nxt if nxt is not None else self.scores
+                cb.ip_forward(x.view(x.shape[0], -1), self._wop(i), self.B[i], self.math, relu=L.relu,
+                              out=out.view(out.shape[0], -1))
+            elif L.kind == "loss":
+                cb.softmax_loss(self.scores, self.labels, loss=self.loss, diff=self.dscores)
+
+    def backward(self, hook=None):
+        """Backward in reverse; `hook(i)` is called after layer i's parameter gradients are enqueued
+        (data-parallel bucketing point)."""
+        a, d, n = self.a, self.d, len(self.layers)
+        for i in range(n - 2, -1, -1):
+            L = self.layers[i]
+            dy = d[i + 1] if i + 1 < n - 1 else self.dscores
+            y = a[i + 1] if i + 1 < n - 1 else self.scores
+            if L.kind in ("conv", "ip") and L.relu:
+                cb.relu_backward(y, dy, inplace=True)  # sign of the ReLU output == sign test on its input
+            if L.kind == "conv":
+                cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math, beta=0.0,
+                                        dw=self.dW[i], db=self.dB[i])
+                if hook:
+                    hook(i)
+                if i > 0:
+                    cb.conv_backward_data(dy, self._wop(i), a[i].shape, L.stride, L.pad, L.group, self.math,
+                                          beta=0.0, out=d[i])
+            elif L.kind == "ip":
+                x2 = a[i].view(a[i].shape[0], -1)
+                dy2 = dy.view(dy.shape[0], -1)
+                cb.ip_backward_weight(x2, dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i], db=self.dB[i])
+                if hook:
+                    hook(i)
+                if i > 0:
+                    cb.ip_backward_data(dy2, self._wop(i), x2.shape, self.math, beta=0.0, out=d[i].view(x2.shape))
+            elif L.kind == "pool":
+                cb.pool_backward(dy, self.mask[i], a[i].shape, L.method, L.kernel, L.stride, L.pad, out=d[i])
+            elif L.kind == "lrn":
+                cb.lrn_backward(a[i], y, dy, **LRN, out=d[i])
+
+    def update(self, lr=0.01, momentum=0.9, decay=5e-4, grad_scale=1.0):
+        cb.sgd_update(self.params, self.grads, self.mom, lr, momentum, decay, grad_scale,
+                      w_bf16=self.params_bf16 if self.math == "bf16" else None)
+
+    def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4):
+        self.forward()
+        self.backward(hook=allreduce.on_grad if allreduce else None)
+        scale = 1.0
+        if allreduce:
+            allreduce.finish()
+            scale = 1.0 / allreduce.world
+        self.update(lr, momentum, decay, grad_scale=scale)

@@ -1,0 +1,140 @@
+"""GPU parity of the convolution ABI calls against the CPU oracle (-m gpu).
+
+FP32 math: per-element |err| <= 1e-5(|ref|+1).  BF16/TF32 math: relative L2 <= 1e-3 against the
+oracle fed the same RNE-quantized operands (reading R12); results are FP32.
+"""
+import numpy as np
+import pytest
+
+import synth
+from _helpers import assert_fp32_close, assert_tc_close, cuda, host
+
+pytestmark = pytest.mark.gpu
+
+# N, C, H, W, O, k, s, p, g  -- spans several M tiles, ragged tails, groups, stride (s2d path)
+CASES = [
+    (2, 3, 9, 9, 8, (3, 3), (1, 1), (1, 1), 1),
+    (3, 8, 13, 13, 12, (3, 3), (1, 1), (1, 1), 2),        # conv4/5-like, 2 groups, ragged M
+    (2, 6, 27, 27, 32, (5, 5), (1, 1), (2, 2), 2),        # conv2-like, Cg=3 (K padding)
+    (2, 3, 35, 35, 16, (11, 11), (4, 4), (0, 0), 1),      # conv1-like, stride 4 (s2d path)
+    (2, 1, 28, 28, 20, (5, 5), (1, 1), (0, 0), 1),        # LeNet conv1
+    (2, 20, 12, 12, 50, (5, 5), (1, 1), (0, 0), 1),       # LeNet conv2
+    (1, 4, 10, 9, 6, (3, 2), (2, 1), (1, 0), 2),          # asymmetric stride/kernel/pad
+    (2, 128, 13, 13, 96, (3, 3), (1, 1), (1, 1), 1),      # several channel blocks (Cg=128)
+    (1, 72, 8, 8, 300, (1, 1), (1, 1), (0, 0), 1),        # 1x1, 2 N tiles
+]
+IDS = [f"N{c[0]}C{c[1]}H{c[2]}O{c[4]}k{c[5][0]}s{c[6][0]}p{c[7][0]}g{c[8]}" for c in CASES]
+
+
+def _inputs(case, seed=0):
+    N, C, H, W, O, k, s, p, g = case
+    X = synth.uniform((N, C, H, W), seed, synth.S_X)
+    Wt = synth.xavier((O, C // g) + k, seed)
+    b = synth.uniform((O,), seed, synth.S_B)
+    OH = (H + 2 * p[0] - k[0]) // s[0] + 1
+    OW = (W + 2 * p[1] - k[1]) // s[1] + 1
+    dY = synth.uniform((N, O, OH, OW), seed, synth.S_DY)
+    return X, Wt, b, dY
+
+
+def _quant(oracle, math, a):
+    return {"fp32": lambda v: v, "bf16": oracle.quant_bf16, "tf32": oracle.quant_tf32_rn}[math](a)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16", "tf32"])
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_conv_forward(oracle, case, math):
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, _ = _inputs(case)
+    for relu in (False, True):
+        Y = cb.conv_forward(cuda(X), cuda(Wt), cuda(b), stride=s, pad=p, group=g, math=math, relu=relu)
+        ref = oracle.conv_forward(_quant(oracle, math, X), _quant(oracle, math, Wt), b, stride=s, pad=p, group=g,
+                                  relu=relu)
+        if math == "fp32":
+            assert_fp32_close(host(Y), ref, f"conv fwd relu={relu}")
+        else:
+            assert_tc_close(host(Y), ref, f"conv fwd {math} relu={relu}")
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16", "tf32"])
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_conv_backward_data(oracle, case, math):
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, _, dY = _inputs(case, 1)
+    dX = cb.conv_backward_data(cuda(dY), cuda(Wt), X.shape, stride=s, pad=p, group=g, math=math)
+    ref = oracle.conv_backward_data(_quant(oracle, math, dY), _quant(oracle, math, Wt), X.shape, stride=s, pad=p,
+                                    group=g)
+    if math == "fp32":
+        assert_fp32_close(host(dX), ref, "conv dgrad")
+    else:
+        assert_tc_close(host(dX), ref, f"conv dgrad {math}")
+    # beta = 1 accumulates (S:292 2x rule up to rounding)
+    dX0 = synth.uniform(X.shape, 1, synth.S_AUX)
+    dX2 = cb.conv_backward_data(cuda(dY), cuda(Wt), X.shape, stride=s, pad=p, group=g, math=math, beta=1.0,
+                                out=cuda(dX0))
+    if math == "fp32":
+        assert_fp32_close(host(dX2), ref + dX0, "conv dgrad beta=1")
+    else:
+        assert_tc_close(host(dX2), ref + dX0, "conv dgrad beta=1")
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_conv_backward_weight(oracle, case, math):
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, _, dY = _inputs(case, 2)
+    dW, db = cb.conv_backward_weight(cuda(X), cuda(dY), Wt.shape, stride=s, pad=p, group=g, math=math)
+    rW, rb = oracle.conv_backward_weight(_quant(oracle, math, X), _quant(oracle, math, dY), Wt.shape, stride=s, pad=p,
+                                         group=g)
+    _, rb_exact = oracle.conv_backward_weight(X, dY, Wt.shape, stride=s, pad=p, group=g)
+    assert_fp32_close(host(db), rb_exact, "bias grad (fp32 sum of dY)")
+    if math == "fp32":
+        assert_fp32_close(host(dW), rW, "conv wgrad")
+    else:
+        assert_tc_close(host(dW), rW, f"conv wgrad {math}")
+    # accumulate: beta=1 on top of the previous result gives 2x
+    dW2, db2 = cb.conv_backward_weight(cuda(X), cuda(dY), Wt.shape, stride=s, pad=p, group=g, math=math, beta=1.0,
+                                       dw=dW.clone(), db=db.clone())
+    np.testing.assert_array_equal(host(dW2), 2 * host(dW))
+    np.testing.assert_array_equal(host(db2), 2 * host(db))
+
+
+@pytest.mark.parametrize("math", ["bf16", "fp32"])
+def test_conv_deterministic(math):
+    """bitwise reproducible run to run."""
+    import paper_1408_5093_b200 as cb
+    case = CASES[2]
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 3)
+    outs = []
+    for _ in range(2):
+        Y = cb.conv_forward(cuda(X), cuda(Wt), cuda(b), stride=s, pad=p, group=g, math=math)
+        dX = cb.conv_backward_data(cuda(dY), cuda(Wt), X.shape, stride=s, pad=p, group=g, math=math)
+        dW, db = cb.conv_backward_weight(cuda(X), cuda(dY), Wt.shape, stride=s, pad=p, group=g, math=math)
+        outs.append([host(t) for t in (Y, dX, dW, db)])
+    for a, b_ in zip(*outs):
+        np.testing.assert_array_equal(a, b_)
+
+
+def test_conv_bf16_storage_output_is_rne_of_fp32(oracle):
+    """BF16-output epilogue: bf16 result == RNE(fp32 result), bit-exact."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    case = CASES[1]
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, _ = _inputs(case, 4)
+    Y32 = cb.conv_forward(cuda(X), cuda(Wt), cuda(b), stride=s, pad=p, group=g, math="bf16")
+    Y16 = cb.conv_forward(cuda(X), cuda(Wt), cuda(b), stride=s, pad=p, group=g, math="bf16", out_dtype=torch.bfloat16)
+    np.testing.assert_array_equal(host(Y16), oracle.quant_bf16(host(Y32)))
+
+
+def test_conv_empty_batch_is_noop():
+    import torch
+    import paper_1408_5093_b200 as cb
+    X = torch.zeros((0, 3, 8, 8), device="cuda")
+    Wt = torch.zeros((4, 3, 3, 3), device="cuda")
+    Y = cb.conv_forward(X, Wt, None, pad=1, math="bf16")
+    assert Y.shape == (0, 4, 8, 8)

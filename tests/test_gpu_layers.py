@@ -1,0 +1,159 @@
+"""GPU parity of the neighbour layers (ReLU, pooling, LRN, inner product), im2col/col2im,
+softmax-with-loss and the SGD update against the CPU oracle (-m gpu)."""
+import numpy as np
+import pytest
+
+import synth
+from _helpers import assert_fp32_close, assert_tc_close, cuda, host
+
+pytestmark = pytest.mark.gpu
+
+
+def test_im2col_col2im_bit_exact(oracle):
+    import paper_1408_5093_b200 as cb
+    for (shape, k, s, p) in [((2, 3, 9, 8), (3, 3), (2, 1), (1, 1)), ((1, 3, 23, 23), (11, 11), (4, 4), (0, 0)),
+                             ((2, 5, 7, 7), (5, 5), (1, 1), (2, 2))]:
+        X = synth.uniform(shape, 1, synth.S_X)
+        for n in range(shape[0]):
+            col = cb.im2col(cuda(X), n, k, s, p)
+            np.testing.assert_array_equal(host(col), oracle.im2col(X, n, k, s, p))
+            dcol = synth.uniform(tuple(col.shape), 1, synth.S_DY, n)
+            dX = cb.col2im(cuda(dcol), shape, n, k, s, p)
+            ref = oracle.col2im(dcol, shape, n, k, s, p)
+            np.testing.assert_array_equal(host(dX)[n], ref[n])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_relu(oracle, dtype):
+    import torch
+    import paper_1408_5093_b200 as cb
+    X = synth.uniform((3, 5, 7, 9), 2, synth.S_X)
+    X[0, 0, 0, :3] = [0.0, -0.0, 1e-30]
+    dY = synth.uniform(X.shape, 2, synth.S_DY)
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    xt = cuda(X).to(td)
+    Xq = host(xt)
+    Y = cb.relu_forward(xt)
+    np.testing.assert_array_equal(host(Y), oracle.relu_forward(Xq))
+    assert not np.signbit(host(Y)).any()
+    dX = cb.relu_backward(xt, cuda(dY).to(td))
+    np.testing.assert_array_equal(host(dX), oracle.relu_backward(Xq, host(cuda(dY).to(td))))
+    y2 = xt.clone()
+    cb.relu_forward(y2, inplace=True)
+    np.testing.assert_array_equal(host(y2), host(Y))
+
+
+POOLS = [((2, 3, 11, 11), (3, 3), (2, 2), (0, 0)), ((2, 4, 8, 8), (2, 2), (2, 2), (0, 0)),
+         ((1, 2, 7, 6), (3, 3), (2, 2), (1, 1)), ((2, 96, 55, 55), (3, 3), (2, 2), (0, 0))]
+
+
+@pytest.mark.parametrize("case", POOLS)
+def test_maxpool_bit_exact(oracle, case):
+    import paper_1408_5093_b200 as cb
+    shape, k, s, p = case
+    X = synth.uniform(shape, 3, synth.S_X)
+    X[0, 0] = np.round(X[0, 0] * 2)  # plenty of ties in one plane (R7)
+    Y, M = cb.pool_forward(cuda(X), "max", k, s, p)
+    rY, rM = oracle.maxpool_forward(X, k, s, p)
+    np.testing.assert_array_equal(host(Y), rY)
+    np.testing.assert_array_equal(host(M), rM)
+    dY = synth.uniform(rY.shape, 3, synth.S_DY)
+    dX = cb.pool_backward(cuda(dY), M, shape, "max", k, s, p)
+    np.testing.assert_array_equal(host(dX), oracle.maxpool_backward(dY, rM, shape, k, s, p))
+
+
+@pytest.mark.parametrize("case", POOLS[:3])
+def test_avepool(oracle, case):
+    import paper_1408_5093_b200 as cb
+    shape, k, s, p = case
+    X = synth.uniform(shape, 4, synth.S_X)
+    Y, _ = cb.pool_forward(cuda(X), "ave", k, s, p)
+    assert_fp32_close(host(Y), oracle.avepool_forward(X, k, s, p), "avepool fwd")
+    dY = synth.uniform(tuple(Y.shape), 4, synth.S_DY)
+    dX = cb.pool_backward(cuda(dY), None, shape, "ave", k, s, p)
+    assert_fp32_close(host(dX), oracle.avepool_backward(dY, shape, k, s, p), "avepool bwd")
+
+
+def test_pool_bf16_maxpool_bit_exact(oracle):
+    import torch
+    import paper_1408_5093_b200 as cb
+    shape, k, s, p = POOLS[0]
+    X = oracle.quant_bf16(synth.uniform(shape, 5, synth.S_X))
+    Y, M = cb.pool_forward(cuda(X).to(torch.bfloat16), "max", k, s, p)
+    rY, rM = oracle.maxpool_forward(X, k, s, p)
+    np.testing.assert_array_equal(host(Y), rY)
+    np.testing.assert_array_equal(host(M), rM)
+
+
+@pytest.mark.parametrize("params", [(5, 1e-4, 0.75, 1.0), (3, 0.5, 0.75, 2.0), (5, 2.0, 1.3, 1.0)])
+def test_lrn(oracle, params):
+    import paper_1408_5093_b200 as cb
+    n, a, b, k = params
+    X = synth.uniform((2, 9, 5, 6), 6, synth.S_X) * 3
+    Y, S = cb.lrn_forward(cuda(X), n, a, b, k, want_scale=True)
+    rY, rS = oracle.lrn_forward(X, n, a, b, k, want_scale=True)
+    assert_fp32_close(host(Y), rY, "lrn fwd")
+    assert_fp32_close(host(S), rS, "lrn scale")
+    dY = synth.uniform(X.shape, 6, synth.S_DY)
+    ref = oracle.lrn_backward(X, dY, n, a, b, k)
+    for sc in (S, None):
+        dX = cb.lrn_backward(cuda(X), Y, cuda(dY), n, a, b, k, scale=sc)
+        assert_fp32_close(host(dX), ref, "lrn bwd")
+
+
+IPS = [(4, (3, 2, 5), 7), (64, (50, 4, 4), 500), (64, (500, 1, 1), 10), (256, (256, 6, 6), 300)]
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("case", IPS)
+def test_inner_product(oracle, case, math):
+    import paper_1408_5093_b200 as cb
+    N, chw, O = case
+    X = synth.uniform((N,) + chw, 7, synth.S_X)
+    K = int(np.prod(chw))
+    Wt = synth.xavier((O, K), 7)
+    b = synth.uniform((O,), 7, synth.S_B)
+    dY = synth.uniform((N, O), 7, synth.S_DY)
+    q = (lambda v: v) if math == "fp32" else oracle.quant_bf16
+    chk = assert_fp32_close if math == "fp32" else assert_tc_close
+    Y = cb.ip_forward(cuda(X), cuda(Wt), cuda(b), math=math)
+    chk(host(Y), oracle.ip_forward(q(X), q(Wt), b), "ip fwd")
+    Yr = cb.ip_forward(cuda(X), cuda(Wt), cuda(b), math=math, relu=True)
+    chk(host(Yr), np.maximum(oracle.ip_forward(q(X), q(Wt), b), 0), "ip fwd relu")
+    dX = cb.ip_backward_data(cuda(dY), cuda(Wt), X.shape, math=math)
+    rdX, rdW, rdb = oracle.ip_backward(q(X), q(Wt), q(dY))
+    chk(host(dX), rdX, "ip dgrad")
+    dW, db = cb.ip_backward_weight(cuda(X), cuda(dY), (O, K), math=math)
+    chk(host(dW), rdW, "ip wgrad")
+    assert_fp32_close(host(db), oracle.ip_backward(X, Wt, dY)[2], "ip bias grad")
+
+
+def test_softmax_loss(oracle):
+    import torch
+    import paper_1408_5093_b200 as cb
+    s = synth.uniform((256, 1000), 8, synth.S_X) * 5
+    lab = synth.labels(256, 1000, 8)
+    loss, d = cb.softmax_loss(cuda(s), cuda(lab))
+    rl, rd = oracle.softmax_loss(s, lab)
+    assert abs(float(loss) - rl) <= 1e-5 * (abs(rl) + 1)
+    assert_fp32_close(host(d), rd, "softmax diff")
+    loss, _ = cb.softmax_loss(torch.zeros((3, 10), device="cuda"), cuda(np.array([0, 4, 9], np.int32)))
+    assert abs(float(loss) - np.log(10)) < 1e-6
+
+
+def test_sgd(oracle):
+    import torch
+    import paper_1408_5093_b200 as cb
+    w = synth.uniform((1000,), 9, synth.S_W)
+    g = synth.uniform((1000,), 9, synth.S_DY)
+    v = synth.uniform((1000,), 9, synth.S_AUX) * 0.1
+    wt, gt, vt = cuda(w), cuda(g), cuda(v)
+    wb = torch.empty(1000, dtype=torch.bfloat16, device="cuda")
+    cb.sgd_update(wt, gt, vt, 0.01, 0.9, 5e-4, 0.5, w_bf16=wb)
+    rw, rv = oracle.sgd_update(w, g, v, 0.01, 0.9, 5e-4, 0.5)
+    assert_fp32_close(host(wt), rw, "sgd w")
+    assert_fp32_close(host(vt), rv, "sgd v")
+    np.testing.assert_array_equal(host(wb), oracle.quant_bf16(host(wt)))
+    w0 = wt.clone()
+    cb.sgd_update(wt, gt, torch.zeros_like(vt), 0.0, 0.0, 0.0)  # S:558 zero-LR fixed point
+    np.testing.assert_array_equal(host(wt), host(w0))
