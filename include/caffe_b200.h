@@ -15,7 +15,10 @@
  *    Pointers marked "host" are host pointers.  The caller owns every buffer;
  *    the library never allocates device memory and never synchronizes
  *    ("reserves exactly as much memory as needed").
- *  - Blobs are contiguous row-major NCHW: index ((n*C+c)*H+h)*W+w.
+ *  - Blobs are contiguous, NCHW (index ((n*C+c)*H+h)*W+w) or channels-last NHWC
+ *    (caffe_layout).  Every call accepts either layout for every activation/diff blob and
+ *    the input and output layouts may differ; weights are always (O, C/g, kh, kw) NCHW-order;
+ *    pooling masks follow their top's layout.  Blobs hold < 2^31 elements.
  *  - Asynchrony: CAFFE_OK means the work was ENQUEUED on `stream`.  Kernel
  *    launch failures return CAFFE_E_CUDA.  A NULL stream is the legacy
  *    default stream.
@@ -46,7 +49,7 @@ extern "C" {
 
 typedef struct CUstream_st* caffe_stream_t; /* == cudaStream_t */
 
-#define CAFFE_ABI_VERSION 1
+#define CAFFE_ABI_VERSION 2
 
 typedef enum {
     CAFFE_OK = 0,
@@ -67,10 +70,18 @@ typedef enum { CAFFE_MATH_FP32 = 0, CAFFE_MATH_TF32 = 1, CAFFE_MATH_BF16 = 2 } c
 
 typedef struct { int32_t n, c, h, w; } caffe_shape4;
 
+/* Memory order of a blob.  The shape is always the logical (num, channels, height, width)
+   of P:142 / S:27; the layout only says how it is stored:
+     CAFFE_NCHW: index ((n*C+c)*H+h)*W+w   (the paper's blob; default)
+     CAFFE_NHWC: index ((n*H+h)*W+w)*C+c   (channels-last: what the tensor-core convolution
+                 reads and writes without a transpose; same values, same semantics). */
+typedef enum { CAFFE_NCHW = 0, CAFFE_NHWC = 1 } caffe_layout;
+
 typedef struct {
-    void* ptr;          /* device pointer, contiguous NCHW */
+    void* ptr;          /* device pointer, contiguous in `layout` order */
     caffe_shape4 shape;
     caffe_dtype dtype;
+    int32_t layout;     /* caffe_layout */
 } caffe_blob;
 
 #define CAFFE_FUSE_RELU 1u /* conv/ip forward: apply max(0, .) in the epilogue */
@@ -101,6 +112,21 @@ int32_t caffe_abi_version(void);
 const char* caffe_last_error(void);
 /* Checks that a CUDA device of compute capability 10.0 is current. */
 caffe_status caffe_device_check(void);
+
+/* ------------------------------------------------------------------ instrumentation
+   (for benchmarks; never changes results)
+   caffe_launch_count: cumulative number of kernels this library launched in the process.
+   caffe_profiler_enable(on): on != 0 clears the record list and starts recording a CUDA event
+     pair on the call's stream around every tcgen05 GEMM launch, tagged with the call's
+     algorithmic FLOPs (2*MACs of the layer pass) and kind (0 = convolution, 1 = inner product);
+     on == 0 stops recording.
+   caffe_profiler_read(kind, ...): synchronises the recorded events and returns the summed
+     duration (ms), summed algorithmic FLOPs and launch count of the records of `kind`
+     (-1 = all).  Host pointers. */
+int64_t caffe_launch_count(void);
+caffe_status caffe_profiler_enable(int32_t on);
+caffe_status caffe_profiler_read(int32_t kind, double* ms /* host */, double* flops /* host */,
+                                 int64_t* launches /* host */);
 
 /* ------------------------------------------------------------------ convolution
  * Convolution with groups, stride and zero padding (S:145 + reading R3):

@@ -63,16 +63,35 @@ def _shape4(shape) -> Tuple[int, int, int, int]:
     raise ValueError(f"blob shape must have 1, 2 or 4 axes, got {s}")
 
 
+def layout_of(t) -> int:
+    """CAFFE_NHWC for a 4-D torch.channels_last tensor, CAFFE_NCHW for a contiguous one."""
+    torch = _t()
+    if t.dim() == 4 and t.is_contiguous(memory_format=torch.channels_last) and not t.is_contiguous():
+        return _abi.CAFFE_NHWC
+    if t.is_contiguous():
+        return _abi.CAFFE_NCHW
+    raise ValueError("caffe_b200 blobs must be contiguous (NCHW) or channels_last (NHWC)")
+
+
 def blob(t, shape=None) -> _abi.Blob:
-    """Describe a contiguous CUDA tensor as a caffe_blob (NCHW)."""
+    """Describe a CUDA tensor as a caffe_blob: contiguous -> NCHW, channels_last -> NHWC."""
     if t is None:
         return None
     if not t.is_cuda:
         raise ValueError("caffe_b200 blobs must live on a CUDA device")
-    if not t.is_contiguous():
-        raise ValueError("caffe_b200 blobs must be contiguous (NCHW)")
+    lay = layout_of(t)
     n, c, h, w = _shape4(t.shape if shape is None else shape)
-    return _abi.Blob(ctypes.c_void_p(t.data_ptr()), _abi.Shape4(n, c, h, w), _dtype_code(t))
+    return _abi.Blob(ctypes.c_void_p(t.data_ptr()), _abi.Shape4(n, c, h, w), _dtype_code(t), lay)
+
+
+def empty_like_layout(shape, dtype, device, like=None, nhwc=None):
+    """Allocate a 4-D blob in the layout of `like` (or NHWC if nhwc=True)."""
+    torch = _t()
+    if nhwc is None:
+        nhwc = like is not None and layout_of(like) == _abi.CAFFE_NHWC
+    if nhwc and len(shape) == 4:
+        return torch.empty(tuple(shape), dtype=dtype, device=device, memory_format=torch.channels_last)
+    return torch.empty(tuple(shape), dtype=dtype, device=device)
 
 
 def _bp(b):
@@ -131,7 +150,7 @@ def conv_forward(x, w, b=None, stride=1, pad=0, group=1, math="bf16", relu=False
     d = _conv_desc((kh, kw), stride, pad, group, math, relu)
     oshape = conv_output_shape(x.shape, w.shape[0], (kh, kw), stride, pad, group)
     if out is None:
-        out = torch.empty(oshape, dtype=out_dtype or x.dtype, device=x.device)
+        out = empty_like_layout(oshape, out_dtype or x.dtype, x.device, like=x)
     ws, wsz = _conv_ws(d, x.shape, w.shape, _abi.CAFFE_PASS_FORWARD)
     bx, bw, bb, by = blob(x), blob(w), blob(b), blob(out)
     call("caffe_conv_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(bw), _bp(bb), ctypes.byref(by), ws, wsz,
@@ -145,7 +164,8 @@ def conv_backward_data(dy, w, in_shape, stride=1, pad=0, group=1, math="bf16", b
     kh, kw = w.shape[2], w.shape[3]
     d = _conv_desc((kh, kw), stride, pad, group, math)
     if out is None:
-        out = torch.zeros(tuple(in_shape), dtype=out_dtype or dy.dtype, device=dy.device)
+        out = empty_like_layout(in_shape, out_dtype or dy.dtype, dy.device, like=dy)
+        out.zero_()
     ws, wsz = _conv_ws(d, in_shape, w.shape, _abi.CAFFE_PASS_BACKWARD_DATA)
     bdy, bw, bdx = blob(dy), blob(w), blob(out)
     call("caffe_conv_backward_data", ctypes.byref(d), ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(bdx),
@@ -214,9 +234,9 @@ def pool_forward(x, method, kernel, stride, pad=0, out=None, mask=None, want_mas
     d = _pool_desc(method, kernel, stride, pad)
     oshape = pool_output_shape(x.shape, method, kernel, stride, pad)
     if out is None:
-        out = torch.empty(oshape, dtype=x.dtype, device=x.device)
+        out = empty_like_layout(oshape, x.dtype, x.device, like=x)
     if d.method == _abi.CAFFE_POOL_MAX and want_mask and mask is None:
-        mask = torch.empty(oshape, dtype=torch.int32, device=x.device)
+        mask = empty_like_layout(oshape, torch.int32, x.device, like=out)
     bx, by, bm = blob(x), blob(out), blob(mask) if d.method == _abi.CAFFE_POOL_MAX else None
     call("caffe_pool_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(by), _bp(bm), _stream())
     return out, (mask if d.method == _abi.CAFFE_POOL_MAX else None)
@@ -226,7 +246,7 @@ def pool_backward(dy, mask, in_shape, method, kernel, stride, pad=0, out=None):
     torch = _t()
     d = _pool_desc(method, kernel, stride, pad)
     if out is None:
-        out = torch.empty(tuple(in_shape), dtype=dy.dtype, device=dy.device)
+        out = empty_like_layout(in_shape, dy.dtype, dy.device, like=dy)
     bdy, bm, bdx = blob(dy), blob(mask), blob(out)
     call("caffe_pool_backward", ctypes.byref(d), ctypes.byref(bdy), _bp(bm), ctypes.byref(bdx), _stream())
     return out
@@ -239,7 +259,7 @@ def lrn_forward(x, local_size=5, alpha=1e-4, beta=0.75, k=1.0, out=None, scale=N
     if out is None:
         out = torch.empty_like(x)
     if want_scale and scale is None:
-        scale = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+        scale = empty_like_layout(x.shape, torch.float32, x.device, like=x)
     bx, by, bs = blob(x), blob(out), blob(scale)
     call("caffe_lrn_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(by), _bp(bs), _stream())
     return (out, scale) if want_scale else out

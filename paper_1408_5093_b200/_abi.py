@@ -16,6 +16,7 @@ CAFFE_E_ALIGN, CAFFE_E_WORKSPACE, CAFFE_E_ALIAS, CAFFE_E_CUDA, CAFFE_E_ARCH = 5,
 STATUS_NAMES = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_PARAM", 4: "E_DTYPE", 5: "E_ALIGN",
                 6: "E_WORKSPACE", 7: "E_ALIAS", 8: "E_CUDA", 9: "E_ARCH"}
 CAFFE_F32, CAFFE_BF16, CAFFE_I32 = 0, 1, 2
+CAFFE_NCHW, CAFFE_NHWC = 0, 1
 CAFFE_MATH_FP32, CAFFE_MATH_TF32, CAFFE_MATH_BF16 = 0, 1, 2
 CAFFE_FUSE_RELU = 1
 CAFFE_POOL_MAX, CAFFE_POOL_AVE = 0, 1
@@ -27,7 +28,7 @@ class Shape4(ctypes.Structure):
 
 
 class Blob(ctypes.Structure):
-    _fields_ = [("ptr", ctypes.c_void_p), ("shape", Shape4), ("dtype", ctypes.c_int)]
+    _fields_ = [("ptr", ctypes.c_void_p), ("shape", Shape4), ("dtype", ctypes.c_int), ("layout", ctypes.c_int32)]
 
 
 class ConvDesc(ctypes.Structure):
@@ -56,6 +57,9 @@ SIGNATURES = {
     "caffe_abi_version": [],
     "caffe_last_error": [],
     "caffe_device_check": [],
+    "caffe_launch_count": [],
+    "caffe_profiler_enable": [i32],
+    "caffe_profiler_read": [i32, P(ctypes.c_double), P(ctypes.c_double), P(i64)],
     "caffe_conv_output_shape": [CD, Shape4, i32, P(Shape4)],
     "caffe_conv_workspace_size": [CD, Shape4, Shape4, i32, P(sz)],
     "caffe_conv_forward": [CD, B, B, B, B, vp, sz, vp],
@@ -77,7 +81,8 @@ SIGNATURES = {
     "caffe_softmax_loss": [B, vp, vp, B, vp],
     "caffe_sgd_update": [vp, vp, vp, vp, i64, f32, f32, f32, f32, vp],
 }
-_RESTYPES = {"caffe_abi_version": ctypes.c_int32, "caffe_last_error": ctypes.c_char_p}
+_RESTYPES = {"caffe_abi_version": ctypes.c_int32, "caffe_last_error": ctypes.c_char_p,
+             "caffe_launch_count": ctypes.c_int64}
 
 _lib = None
 

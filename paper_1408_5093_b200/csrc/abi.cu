@@ -4,12 +4,39 @@
 #include "../../include/caffe_b200.h"
 #include "internal.h"
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 using namespace cb;
+
+// ------------------------------------------------------------------ instrumentation
+namespace {
+std::atomic<long long> g_launches{0};
+struct ProfRec {
+    cudaEvent_t a, b;
+    double flops;
+    int kind;
+};
+std::mutex g_pmu;
+bool g_prof = false;
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_evpool;
+size_t g_evused = 0;
+cudaEvent_t prof_event() {
+    if (g_evused == g_evpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        g_evpool.push_back(e);
+    }
+    return g_evpool[g_evused++];
+}
+}  // namespace
+void cb::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
@@ -27,9 +54,9 @@ caffe_status fail(caffe_status st, const char* fmt, ...) {
 caffe_status cuda_fail(cudaError_t e, const char* what) {
     return fail(CAFFE_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
-#define CK(expr, what)                                  \
-    do {                                                \
-        cudaError_t _e = (expr);                        \
+#define CK(expr, what)                                     \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
         if (_e != cudaSuccess) return cuda_fail(_e, what); \
     } while (0)
 
@@ -39,6 +66,15 @@ inline size_t bytes_of(const caffe_blob* b) { return (size_t)cnt(b->shape) * esi
 inline long long rup(long long a, long long b) { return (a + b - 1) / b * b; }
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 inline size_t align1k(size_t x) { return (x + 1023) & ~size_t(1023); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+inline bool nhwc(const caffe_blob* b) { return b->layout == CAFFE_NHWC; }
+inline int isbf(const caffe_blob* b) { return b->dtype == CAFFE_BF16; }
+
+L4 strides(const caffe_blob* b) {
+    const caffe_shape4& s = b->shape;
+    if (nhwc(b)) return L4{s.h * s.w * s.c, 1, s.w * s.c, s.c};
+    return L4{s.c * s.h * s.w, s.h * s.w, s.w, 1};
+}
 
 caffe_status check_blob(const caffe_blob* b, const char* name, bool float_only = true) {
     if (!b) return fail(CAFFE_E_INVALID, "%s is NULL", name);
@@ -47,6 +83,8 @@ caffe_status check_blob(const caffe_blob* b, const char* name, bool float_only =
     if (s.n < 0 || s.c < 0 || s.h < 0 || s.w < 0) return fail(CAFFE_E_SHAPE, "%s has a negative axis", name);
     if (s.n > 0 && (s.c == 0 || s.h == 0 || s.w == 0))
         return fail(CAFFE_E_SHAPE, "%s has a zero axis (%d,%d,%d,%d)", name, s.n, s.c, s.h, s.w);
+    if (cnt(s) >= (1LL << 31)) return fail(CAFFE_E_SHAPE, "%s has >= 2^31 elements", name);
+    if (b->layout != CAFFE_NCHW && b->layout != CAFFE_NHWC) return fail(CAFFE_E_INVALID, "%s has a bad layout %d", name, b->layout);
     if (float_only && b->dtype != CAFFE_F32 && b->dtype != CAFFE_BF16)
         return fail(CAFFE_E_DTYPE, "%s dtype must be F32 or BF16", name);
     if (!float_only && b->dtype != CAFFE_I32) return fail(CAFFE_E_DTYPE, "%s dtype must be I32", name);
@@ -61,7 +99,6 @@ bool overlap(const caffe_blob* a, const caffe_blob* b) {
 bool same_shape(const caffe_shape4& a, const caffe_shape4& b) {
     return a.n == b.n && a.c == b.c && a.h == b.h && a.w == b.w;
 }
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ------------------------------------------------------------------ conv planning
 struct Plan {
@@ -84,6 +121,8 @@ caffe_status conv_validate(const caffe_conv_desc* d, caffe_shape4 bottom, int32_
     if (d->kernel_h > bottom.h + 2 * d->pad_h || d->kernel_w > bottom.w + 2 * d->pad_w)
         return fail(CAFFE_E_PARAM, "kernel %dx%d larger than padded input %dx%d (S:146)", d->kernel_h, d->kernel_w,
                     bottom.h + 2 * d->pad_h, bottom.w + 2 * d->pad_w);
+    if (d->pad_h > 100 || d->pad_w > 100 || d->kernel_h > 100 || d->kernel_w > 100)
+        return fail(CAFFE_E_PARAM, "kernel/pad larger than 100 not supported");
     Plan& q = *p;
     q.N = bottom.n; q.C = bottom.c; q.H = bottom.h; q.W = bottom.w; q.O = O; q.G = d->group;
     q.Cg = q.C / q.G; q.Og = O / q.G; q.kh = d->kernel_h; q.kw = d->kernel_w; q.sh = d->stride_h; q.sw = d->stride_w;
@@ -108,14 +147,52 @@ caffe_status conv_validate(const caffe_conv_desc* d, caffe_shape4 bottom, int32_
 ConvGeom cgeom(const Plan& p) {
     return ConvGeom{p.N, p.C, p.H, p.W, p.O, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, p.G, p.OH, p.OW};
 }
-PackGeom xpack(const Plan& p) {
-    return PackGeom{p.N, p.C, p.H, p.W, p.G, p.Cg, p.bh, p.bw, p.s2d ? p.ph : 0, p.s2d ? p.pw : 0, p.Hp, p.Wp, p.Cgp};
-}
-PackGeom dypack(const Plan& p) {
-    return PackGeom{p.N, p.O, p.OH, p.OW, p.G, p.Og, 1, 1, 0, 0, p.OH, p.OW, p.Ogp};
-}
 WGeom wgeom(const Plan& p) {
     return WGeom{p.O, p.G, p.Cg, p.Og, p.kh, p.kw, p.bh, p.bw, p.khp, p.kwp, p.Cgp, p.Ogp};
+}
+
+// An activation consumed by a TMA operand: either the caller's NHWC BF16 blob as-is, or a packed
+// channels-last copy in workspace.  Group g's channels start at g*cpg; Ctot channels per pixel.
+// A 64-channel operand block may run past its group's channels: those K positions meet zero
+// weights (forward/data gradient) or produce discarded rows (weight gradient).
+struct Operand {
+    const void* ptr;
+    int Ctot, cpg, H, W;
+    bool packed;
+    PackGeom pg;
+};
+int round_ch(int c, int E) { return (int)rup(c, 16 / E); }
+bool can_use_direct(const caffe_blob* b, int Cg, int E, bool s2d) {
+    return !s2d && E == 2 && b->dtype == CAFFE_BF16 && nhwc(b) && (b->shape.c * 2) % 16 == 0 && (Cg * 2) % 16 == 0 &&
+           aligned16(b->ptr);
+}
+// X-like operand (conv forward input, wgrad input)
+Operand plan_x(const caffe_blob* b, const Plan& p) {
+    if (can_use_direct(b, p.Cg, p.E, p.s2d)) return Operand{b->ptr, p.C, p.Cg, p.H, p.W, false, {}};
+    const int cpg = round_ch(p.Cge, p.E);
+    return Operand{nullptr, p.G * cpg, cpg, p.Hp, p.Wp, true,
+                   PackGeom{p.N, p.C, p.H, p.W, p.G, p.Cg, p.bh, p.bw, p.s2d ? p.ph : 0, p.s2d ? p.pw : 0, p.Hp, p.Wp,
+                            cpg, p.G * cpg}};
+}
+// dY-like operand (conv backward inputs): O channels on the OH x OW grid, never s2d
+Operand plan_dy(const caffe_blob* b, const Plan& p) {
+    if (can_use_direct(b, p.Og, p.E, false)) return Operand{b->ptr, p.O, p.Og, p.OH, p.OW, false, {}};
+    const int cpg = round_ch(p.Og, p.E);
+    return Operand{nullptr, p.G * cpg, cpg, p.OH, p.OW, true,
+                   PackGeom{p.N, p.O, p.OH, p.OW, p.G, p.Og, 1, 1, 0, 0, p.OH, p.OW, cpg, p.G * cpg}};
+}
+// conservative (always-packed) sizes used for workspace queries
+size_t ws_x_max(const Plan& p) { return align1k((size_t)p.N * p.Hp * p.Wp * p.G * round_ch(p.Cge, p.E) * p.E); }
+size_t ws_dy_max(const Plan& p) { return align1k((size_t)p.N * p.OH * p.OW * p.G * round_ch(p.Og, p.E) * p.E); }
+size_t ws_wb(const Plan& p) { return align1k((size_t)p.O * p.taps * p.Cgp * p.E); }
+size_t ws_wd(const Plan& p) { return align1k((size_t)p.G * p.Cge * p.taps * p.Ogp * p.E); }
+size_t ws_t(const Plan& p) { return p.s2d ? align1k((size_t)p.N * p.Hp * p.Wp * p.G * p.Cge * 4) : 0; }
+size_t ws_bias(const Plan& p) { return align1k((size_t)bias_grad_splits(p.N, p.O, p.OH * p.OW) * p.O * 4); }
+
+caffe_status pack_if(const Operand& o, const caffe_blob* src, void* dst, int E, cudaStream_t s) {
+    if (!o.packed) return CAFFE_OK;
+    CK(pack_act(src->ptr, isbf(src), strides(src), nhwc(src), dst, E, o.pg, s), "pack activations");
+    return CAFFE_OK;
 }
 
 int choose_bn(int n) {
@@ -137,13 +214,15 @@ void finish_args(TcArgs& a, int bstage) {
     a.tmem_cols = 2 * a.acc_stride;
     a.units = a.m_tiles * a.n_tiles * a.groups * a.splits;
 }
-
-// workspace sub-buffer sizes
-size_t ws_xa(const Plan& p) { return align1k((size_t)p.N * p.Hp * p.Wp * p.G * p.Cgp * p.E); }
-size_t ws_dya(const Plan& p) { return align1k((size_t)p.N * p.OH * p.OW * p.G * p.Ogp * p.E); }
-size_t ws_wb(const Plan& p) { return align1k((size_t)p.O * p.taps * p.Cgp * p.E); }
-size_t ws_wd(const Plan& p) { return align1k((size_t)p.G * p.Cge * p.taps * p.Ogp * p.E); }
-size_t ws_t(const Plan& p) { return p.s2d ? align1k((size_t)p.N * p.Hp * p.Wp * p.G * p.Cgp * 4) : 0; }
+void set_out(TcArgs& a, const caffe_blob* b) {
+    // m = image * P + pixel;  column = output channel
+    const caffe_shape4& s = b->shape;
+    if (nhwc(b)) { a.s_n = (long long)s.h * s.w * s.c; a.s_c = 1; a.s_p = s.c; }
+    else { a.s_n = (long long)s.c * s.h * s.w; a.s_c = (long long)s.h * s.w; a.s_p = 1; }
+    a.P = s.h * s.w;
+    a.out = b->ptr;
+    a.out_bf16 = isbf(b);
+}
 
 struct WgradSplit {
     int m_tiles, n_tiles, BN, splits, kb_per, kblocks;
@@ -172,10 +251,13 @@ size_t ws_partial(const Plan& p) {
 }
 
 size_t conv_ws(const Plan& p, int pass, caffe_math m) {
+    if (pass == CAFFE_PASS_BACKWARD_WEIGHT) {
+        if (m == CAFFE_MATH_FP32) return ws_bias(p);
+        return ws_x_max(p) + ws_dy_max(p) + ws_partial(p) + ws_bias(p);
+    }
     if (m == CAFFE_MATH_FP32) return 0;
-    if (pass == CAFFE_PASS_FORWARD) return ws_xa(p) + ws_wb(p);
-    if (pass == CAFFE_PASS_BACKWARD_DATA) return ws_dya(p) + ws_wd(p) + ws_t(p);
-    return ws_xa(p) + ws_dya(p) + ws_partial(p);
+    if (pass == CAFFE_PASS_FORWARD) return ws_x_max(p) + ws_wb(p);
+    return ws_dy_max(p) + ws_wd(p) + ws_t(p);
 }
 
 caffe_status check_ws(void* ws, size_t have, size_t need) {
@@ -186,12 +268,26 @@ caffe_status check_ws(void* ws, size_t have, size_t need) {
     return CAFFE_OK;
 }
 
-caffe_status run_tc(TcLaunch& L, cudaStream_t s) {
+// kind: 0 = convolution pass, 1 = inner product; flops = algorithmic FLOPs of the call
+caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     L.grid = L.args.units < num_sms() ? L.args.units : num_sms();
+    ProfRec rec{nullptr, nullptr, flops, kind};
+    if (g_prof) {
+        std::lock_guard<std::mutex> lk(g_pmu);
+        rec.a = prof_event();
+        rec.b = prof_event();
+        cudaEventRecord(rec.a, s);
+    }
     cudaError_t e = tc_launch(L, s);
+    if (g_prof) {
+        cudaEventRecord(rec.b, s);
+        std::lock_guard<std::mutex> lk(g_pmu);
+        g_recs.push_back(rec);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
     return CAFFE_OK;
 }
+double conv_flops(const Plan& p) { return 2.0 * p.N * p.O * p.OH * p.OW * (double)p.Cg * p.kh * p.kw; }
 
 }  // namespace
 
@@ -200,6 +296,39 @@ extern "C" {
 
 int32_t caffe_abi_version(void) { return CAFFE_ABI_VERSION; }
 const char* caffe_last_error(void) { return g_err.c_str(); }
+int64_t caffe_launch_count(void) { return g_launches.load(); }
+
+caffe_status caffe_profiler_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    if (on) {
+        g_recs.clear();
+        g_evused = 0;
+    }
+    g_prof = on != 0;
+    return CAFFE_OK;
+}
+
+caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_t* launches) {
+    if (!ms || !flops || !launches) return fail(CAFFE_E_INVALID, "NULL output pointer");
+    std::lock_guard<std::mutex> lk(g_pmu);
+    double t = 0.0, f = 0.0;
+    int64_t n = 0;
+    for (const ProfRec& r : g_recs) {
+        if (kind >= 0 && r.kind != kind) continue;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "profiler event sync");
+        float x = 0.f;
+        e = cudaEventElapsedTime(&x, r.a, r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "profiler elapsed time");
+        t += x;
+        f += r.flops;
+        n++;
+    }
+    *ms = t;
+    *flops = f;
+    *launches = n;
+    return CAFFE_OK;
+}
 
 caffe_status caffe_device_check(void) {
     int dev = 0;
@@ -269,22 +398,25 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     const size_t need = conv_ws(p, CAFFE_PASS_FORWARD, desc->math);
     if ((st = check_ws(ws, ws_bytes, need))) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    const int xb = bottom->dtype == CAFFE_BF16, wb = weight->dtype == CAFFE_BF16, yb = top->dtype == CAFFE_BF16;
     const int relu = (desc->flags & CAFFE_FUSE_RELU) ? 1 : 0;
     const float* bptr = bias ? (const float*)bias->ptr : nullptr;
     if (desc->math == CAFFE_MATH_FP32) {
-        CK(fp32_conv_fwd(bottom->ptr, xb, weight->ptr, wb, bptr, top->ptr, yb, relu, cgeom(p), s), "conv fwd fp32");
+        CK(fp32_conv_fwd(bottom->ptr, isbf(bottom), strides(bottom), weight->ptr, isbf(weight), bptr, top->ptr, isbf(top),
+                         strides(top), nhwc(top), relu, cgeom(p), s),
+           "conv fwd fp32");
         return CAFFE_OK;
     }
     char* w8 = (char*)ws;
+    Operand A = plan_x(bottom, p);
     void* XA = w8;
-    void* WB = w8 + ws_xa(p);
-    CK(pack_nhwc(bottom->ptr, xb, XA, p.E, xpack(p), s), "pack activations");
-    CK(repack_w_fwd(weight->ptr, wb, WB, p.E, wgeom(p), s), "repack weights");
+    void* WB = w8 + ws_x_max(p);
+    if ((st = pack_if(A, bottom, XA, p.E, s))) return st;
+    const void* aptr = A.packed ? XA : A.ptr;
+    CK(repack_w_fwd(weight->ptr, isbf(weight), WB, p.E, wgeom(p), s), "repack weights");
     TcLaunch L;
     memset(&L, 0, sizeof L);
     L.esz = p.E; L.amode = A_IM2COL_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
-    if (!encode_im2col_4d(&L.mapA, p.E, XA, p.G * p.Cgp, p.Wp, p.Hp, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
+    if (!encode_im2col_4d(&L.mapA, p.E, aptr, A.Ctot, A.W, A.H, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
                           p.php - (p.khp - 1), p.CH, 128))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (activation)");
     TcArgs& a = L.args;
@@ -296,11 +428,11 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     a.m_tiles = (int)cdiv(a.M, 128); a.n_tiles = (int)cdiv(p.Og, a.BN); a.groups = p.G; a.splits = 1;
     a.kblocks = p.taps * (p.Cgp / p.CH); a.kb_per_split = a.kblocks;
     a.a_P = p.OH * p.OW; a.a_OW = p.OW; a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_kw = p.kwp;
-    a.a_cblocks = p.Cgp / p.CH; a.a_cpg = p.Cgp; a.b_row_g = p.Og;
-    a.out = top->ptr; a.out_bf16 = yb; a.s_n = (long long)p.O * p.OH * p.OW; a.s_c = (long long)p.OH * p.OW; a.s_p = 1;
-    a.P = p.OH * p.OW; a.col_g = p.Og; a.bias = bptr; a.relu = relu; a.beta = 0.f;
+    a.a_cblocks = p.Cgp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Og;
+    set_out(a, top);
+    a.col_g = p.Og; a.bias = bptr; a.relu = relu; a.beta = 0.f;
     finish_args(a, a.BN * 128);
-    return run_tc(L, s);
+    return run_tc(L, s, conv_flops(p), 0);
 }
 
 caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_blob* top_diff, const caffe_blob* weight,
@@ -321,23 +453,26 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
     const size_t need = conv_ws(p, CAFFE_PASS_BACKWARD_DATA, desc->math);
     if ((st = check_ws(ws, ws_bytes, need))) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    const int db = top_diff->dtype == CAFFE_BF16, wb = weight->dtype == CAFFE_BF16, xb = bottom_diff->dtype == CAFFE_BF16;
     if (desc->math == CAFFE_MATH_FP32) {
-        CK(fp32_conv_dgrad(top_diff->ptr, db, weight->ptr, wb, bottom_diff->ptr, xb, beta, cgeom(p), s), "conv dgrad fp32");
+        CK(fp32_conv_dgrad(top_diff->ptr, isbf(top_diff), strides(top_diff), weight->ptr, isbf(weight), bottom_diff->ptr,
+                           isbf(bottom_diff), nhwc(bottom_diff), beta, cgeom(p), s),
+           "conv dgrad fp32");
         return CAFFE_OK;
     }
     char* w8 = (char*)ws;
+    Operand A = plan_dy(top_diff, p);
     void* DYA = w8;
-    void* WD = w8 + ws_dya(p);
-    float* T = (float*)(w8 + ws_dya(p) + ws_wd(p));
-    CK(pack_nhwc(top_diff->ptr, db, DYA, p.E, dypack(p), s), "pack top_diff");
-    CK(repack_w_dgrad(weight->ptr, wb, WD, p.E, wgeom(p), p.Cge, s), "repack weights (dgrad)");
+    void* WD = w8 + ws_dy_max(p);
+    float* T = (float*)(w8 + ws_dy_max(p) + ws_wd(p));
+    if ((st = pack_if(A, top_diff, DYA, p.E, s))) return st;
+    const void* aptr = A.packed ? DYA : A.ptr;
+    CK(repack_w_dgrad(weight->ptr, isbf(weight), WD, p.E, wgeom(p), p.Cge, s), "repack weights (dgrad)");
     const int Hd = p.s2d ? p.Hp : p.H, Wd = p.s2d ? p.Wp : p.W;
     const int lo_h = p.khp - 1 - p.php, lo_w = p.kwp - 1 - p.pwp;
     TcLaunch L;
     memset(&L, 0, sizeof L);
     L.esz = p.E; L.amode = A_IM2COL_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
-    if (!encode_im2col_4d(&L.mapA, p.E, DYA, p.G * p.Ogp, p.OW, p.OH, p.N, lo_w, lo_h, lo_w - (p.kwp - 1),
+    if (!encode_im2col_4d(&L.mapA, p.E, aptr, A.Ctot, p.OW, p.OH, p.N, lo_w, lo_h, lo_w - (p.kwp - 1),
                           lo_h - (p.khp - 1), p.CH, 128))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (top_diff)");
     TcArgs& a = L.args;
@@ -349,18 +484,19 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
     a.m_tiles = (int)cdiv(a.M, 128); a.n_tiles = (int)cdiv(p.Cge, a.BN); a.groups = p.G; a.splits = 1;
     a.kblocks = p.taps * (p.Ogp / p.CH); a.kb_per_split = a.kblocks;
     a.a_P = Hd * Wd; a.a_OW = Wd; a.a_pad_h = lo_h; a.a_pad_w = lo_w; a.a_kw = p.kwp;
-    a.a_cblocks = p.Ogp / p.CH; a.a_cpg = p.Ogp; a.b_row_g = p.Cge;
-    a.P = Hd * Wd;
+    a.a_cblocks = p.Ogp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Cge;
+    PackGeom tg{p.N, p.C, p.H, p.W, p.G, p.Cg, p.bh, p.bw, p.ph, p.pw, p.Hp, p.Wp, p.Cge, p.G * p.Cge};
     if (!p.s2d) {
-        a.out = bottom_diff->ptr; a.out_bf16 = xb; a.s_n = (long long)p.C * p.H * p.W; a.s_c = (long long)p.H * p.W;
-        a.s_p = 1; a.col_g = p.Cg; a.beta = beta;
+        set_out(a, bottom_diff);
+        a.col_g = p.Cg; a.beta = beta;
     } else {
-        a.out = T; a.out_bf16 = 0; a.s_n = (long long)p.Hp * p.Wp * p.G * p.Cgp; a.s_c = 1; a.s_p = (long long)p.G * p.Cgp;
-        a.col_g = p.Cgp; a.beta = 0.f;
+        a.out = T; a.out_bf16 = 0; a.P = p.Hp * p.Wp;
+        a.s_n = (long long)p.Hp * p.Wp * tg.Ctot; a.s_c = 1; a.s_p = tg.Ctot;
+        a.col_g = p.Cge; a.beta = 0.f;
     }
     finish_args(a, a.BN * 128);
-    if ((st = run_tc(L, s))) return st;
-    if (p.s2d) CK(unpack_s2d_grad(T, bottom_diff->ptr, xb, beta, xpack(p), s), "unpack s2d gradient");
+    if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
+    if (p.s2d) CK(unpack_s2d_grad(T, bottom_diff->ptr, isbf(bottom_diff), nhwc(bottom_diff), beta, tg, s), "unpack s2d gradient");
     return CAFFE_OK;
 }
 
@@ -390,39 +526,51 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
     const size_t need = conv_ws(p, CAFFE_PASS_BACKWARD_WEIGHT, desc->math);
     if ((st = check_ws(ws, ws_bytes, need))) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    const int xb = bottom->dtype == CAFFE_BF16, db = top_diff->dtype == CAFFE_BF16;
-    if (bias_diff)
-        CK(bias_grad(top_diff->ptr, db, (float*)bias_diff->ptr, beta, p.N, p.O, (long long)p.OH * p.OW, s), "bias grad");
+    char* w8 = (char*)ws;
     if (desc->math == CAFFE_MATH_FP32) {
-        CK(fp32_conv_wgrad(bottom->ptr, xb, top_diff->ptr, db, (float*)weight_diff->ptr, beta, cgeom(p), s), "conv wgrad fp32");
+        if (bias_diff)
+            CK(bias_grad(top_diff->ptr, isbf(top_diff), nhwc(top_diff), (float*)bias_diff->ptr, beta, p.N, p.O,
+                         p.OH * p.OW, (float*)w8, s),
+               "bias grad");
+        CK(fp32_conv_wgrad(bottom->ptr, isbf(bottom), strides(bottom), top_diff->ptr, isbf(top_diff), strides(top_diff),
+                           (float*)weight_diff->ptr, beta, cgeom(p), s),
+           "conv wgrad fp32");
         return CAFFE_OK;
     }
-    char* w8 = (char*)ws;
+    Operand A = plan_x(bottom, p);
+    Operand B = plan_dy(top_diff, p);
     void* XA = w8;
-    void* DYA = w8 + ws_xa(p);
-    float* PART = (float*)(w8 + ws_xa(p) + ws_dya(p));
-    CK(pack_nhwc(bottom->ptr, xb, XA, p.E, xpack(p), s), "pack activations");
-    CK(pack_nhwc(top_diff->ptr, db, DYA, p.E, dypack(p), s), "pack top_diff");
+    void* DYA = w8 + ws_x_max(p);
+    float* PART = (float*)(w8 + ws_x_max(p) + ws_dy_max(p));
+    float* BPART = (float*)(w8 + ws_x_max(p) + ws_dy_max(p) + ws_partial(p));
+    if (bias_diff)
+        CK(bias_grad(top_diff->ptr, isbf(top_diff), nhwc(top_diff), (float*)bias_diff->ptr, beta, p.N, p.O,
+                     p.OH * p.OW, BPART, s),
+           "bias grad");
+    if ((st = pack_if(A, bottom, XA, p.E, s))) return st;
+    if ((st = pack_if(B, top_diff, DYA, p.E, s))) return st;
+    const void* aptr = A.packed ? XA : A.ptr;
+    const void* bptr = B.packed ? DYA : B.ptr;
     WgradSplit w = wgrad_split(p);
     TcLaunch L;
     memset(&L, 0, sizeof L);
     L.esz = p.E; L.amode = A_IM2COL_MN; L.bmode = B_TILED_MN; L.epi = EPI_PARTIAL;
-    if (!encode_im2col_4d(&L.mapA, p.E, XA, p.G * p.Cgp, p.Wp, p.Hp, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
+    if (!encode_im2col_4d(&L.mapA, p.E, aptr, A.Ctot, A.W, A.H, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
                           p.php - (p.khp - 1), p.CH, p.CH))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (wgrad activation)");
-    if (!encode_tiled_2d(&L.mapB, p.E, DYA, (uint64_t)p.G * p.Ogp, (uint64_t)p.N * p.OH * p.OW,
-                         (uint64_t)p.G * p.Ogp * p.E, p.CH, p.CH))
+    if (!encode_tiled_2d(&L.mapB, p.E, bptr, (uint64_t)B.Ctot, (uint64_t)p.N * p.OH * p.OW, (uint64_t)B.Ctot * p.E,
+                         p.CH, p.CH))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (wgrad top_diff)");
     TcArgs& a = L.args;
     a.BN = w.BN; a.M = 128 * w.m_tiles; a.N = p.Og;
     a.m_tiles = w.m_tiles; a.n_tiles = w.n_tiles; a.groups = p.G; a.splits = w.splits;
     a.kblocks = w.kblocks; a.kb_per_split = w.kb_per;
     a.a_P = p.OH * p.OW; a.a_OW = p.OW; a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_kw = p.kwp;
-    a.a_cblocks = p.Cgp / p.CH; a.a_cpg = p.Cgp; a.a_nchunks_total = p.taps * (p.Cgp / p.CH);
-    a.b_col_g = p.Ogp; a.b_nchunks = (int)cdiv(w.BN, p.CH);
+    a.a_cblocks = p.Cgp / p.CH; a.a_cpg = A.cpg; a.a_nchunks_total = p.taps * (p.Cgp / p.CH);
+    a.b_col_g = B.cpg; a.b_nchunks = (int)cdiv(w.BN, p.CH);
     a.partial = PART;
     finish_args(a, a.b_nchunks * p.CH * 128);
-    if ((st = run_tc(L, s))) return st;
+    if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
     CK(wgrad_reduce(PART, (float*)weight_diff->ptr, beta, wgeom(p), w.m_tiles, w.n_tiles, w.splits, w.BN, p.CH,
                     p.Cgp / p.CH, s),
        "wgrad reduce");
@@ -433,12 +581,12 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
 caffe_status caffe_relu_forward(const caffe_blob* bottom, caffe_blob* top, caffe_stream_t stream) {
     caffe_status st;
     if ((st = check_blob(bottom, "bottom")) || (st = check_blob(top, "top"))) return st;
-    if (!same_shape(bottom->shape, top->shape) || bottom->dtype != top->dtype)
-        return fail(CAFFE_E_SHAPE, "top must match bottom in shape and dtype");
+    if (!same_shape(bottom->shape, top->shape) || bottom->dtype != top->dtype || bottom->layout != top->layout)
+        return fail(CAFFE_E_SHAPE, "top must match bottom in shape, dtype and layout");
     if (bottom->ptr != top->ptr && overlap(bottom, top)) return fail(CAFFE_E_ALIAS, "partial overlap of top and bottom");
     if (cnt(bottom->shape) == 0) return CAFFE_OK;
     if (!aligned16(bottom->ptr) || !aligned16(top->ptr)) return fail(CAFFE_E_ALIGN, "ReLU buffers must be 16-byte aligned");
-    CK(relu_fwd(bottom->ptr, top->ptr, bottom->dtype == CAFFE_BF16, cnt(bottom->shape), (cudaStream_t)stream), "relu fwd");
+    CK(relu_fwd(bottom->ptr, top->ptr, isbf(bottom), (int)cnt(bottom->shape), (cudaStream_t)stream), "relu fwd");
     return CAFFE_OK;
 }
 
@@ -449,13 +597,12 @@ caffe_status caffe_relu_backward(const caffe_blob* x, const caffe_blob* top_diff
         (st = check_blob(bottom_diff, "bottom_diff")))
         return st;
     if (!same_shape(x->shape, top_diff->shape) || !same_shape(x->shape, bottom_diff->shape) ||
-        top_diff->dtype != bottom_diff->dtype)
-        return fail(CAFFE_E_SHAPE, "ReLU backward blobs must share shape (and diff dtype)");
+        top_diff->dtype != bottom_diff->dtype || x->layout != top_diff->layout || x->layout != bottom_diff->layout)
+        return fail(CAFFE_E_SHAPE, "ReLU backward blobs must share shape and layout (and diff dtype)");
     if ((bottom_diff->ptr != top_diff->ptr && overlap(bottom_diff, top_diff)) || overlap(bottom_diff, x))
         return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
     if (cnt(x->shape) == 0) return CAFFE_OK;
-    CK(relu_bwd(x->ptr, top_diff->ptr, bottom_diff->ptr, x->dtype == CAFFE_BF16, top_diff->dtype == CAFFE_BF16,
-                cnt(x->shape), (cudaStream_t)stream),
+    CK(relu_bwd(x->ptr, top_diff->ptr, bottom_diff->ptr, isbf(x), isbf(top_diff), (int)cnt(x->shape), (cudaStream_t)stream),
        "relu bwd");
     return CAFFE_OK;
 }
@@ -500,16 +647,19 @@ caffe_status caffe_pool_forward(const caffe_pool_desc* desc, const caffe_blob* b
         return fail(CAFFE_E_SHAPE, "top shape/dtype mismatch (want %d,%d,%d,%d)", want.n, want.c, want.h, want.w);
     if (mask) {
         if ((st = check_blob(mask, "mask", false))) return st;
-        if (!same_shape(mask->shape, want)) return fail(CAFFE_E_SHAPE, "mask shape must equal top shape");
+        if (!same_shape(mask->shape, want) || mask->layout != top->layout)
+            return fail(CAFFE_E_SHAPE, "mask shape/layout must equal top's");
         if (desc->method != CAFFE_POOL_MAX) return fail(CAFFE_E_INVALID, "mask is only produced by MAX pooling");
     }
     if (overlap(top, bottom) || overlap(mask, bottom) || overlap(mask, top)) return fail(CAFFE_E_ALIAS, "pool outputs overlap");
     if (g.N == 0) return CAFFE_OK;
-    const int bf = bottom->dtype == CAFFE_BF16;
     if (desc->method == CAFFE_POOL_MAX)
-        CK(maxpool_fwd(bottom->ptr, top->ptr, mask ? (int32_t*)mask->ptr : nullptr, bf, g, (cudaStream_t)stream), "maxpool fwd");
+        CK(maxpool_fwd(bottom->ptr, strides(bottom), top->ptr, nhwc(top), mask ? (int32_t*)mask->ptr : nullptr,
+                       isbf(bottom), g, (cudaStream_t)stream),
+           "maxpool fwd");
     else
-        CK(avepool_fwd(bottom->ptr, top->ptr, bf, g, (cudaStream_t)stream), "avepool fwd");
+        CK(avepool_fwd(bottom->ptr, strides(bottom), top->ptr, nhwc(top), isbf(bottom), g, (cudaStream_t)stream),
+           "avepool fwd");
     return CAFFE_OK;
 }
 
@@ -525,15 +675,19 @@ caffe_status caffe_pool_backward(const caffe_pool_desc* desc, const caffe_blob* 
     if (desc->method == CAFFE_POOL_MAX) {
         if (!mask) return fail(CAFFE_E_INVALID, "MAX pool backward needs the argmax mask (S:173)");
         if ((st = check_blob(mask, "mask", false))) return st;
-        if (!same_shape(mask->shape, want)) return fail(CAFFE_E_SHAPE, "mask shape must equal top shape");
+        if (!same_shape(mask->shape, want) || mask->layout != top_diff->layout)
+            return fail(CAFFE_E_SHAPE, "mask shape/layout must equal top_diff's");
     }
     if (overlap(bottom_diff, top_diff) || overlap(bottom_diff, mask)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
     if (g.N == 0) return CAFFE_OK;
-    const int bf = top_diff->dtype == CAFFE_BF16;
     if (desc->method == CAFFE_POOL_MAX)
-        CK(maxpool_bwd(top_diff->ptr, (const int32_t*)mask->ptr, bottom_diff->ptr, bf, g, (cudaStream_t)stream), "maxpool bwd");
+        CK(maxpool_bwd(top_diff->ptr, (const int32_t*)mask->ptr, strides(top_diff), bottom_diff->ptr, nhwc(bottom_diff),
+                       isbf(top_diff), g, (cudaStream_t)stream),
+           "maxpool bwd");
     else
-        CK(avepool_bwd(top_diff->ptr, bottom_diff->ptr, bf, g, (cudaStream_t)stream), "avepool bwd");
+        CK(avepool_bwd(top_diff->ptr, strides(top_diff), bottom_diff->ptr, nhwc(bottom_diff), isbf(top_diff), g,
+                       (cudaStream_t)stream),
+           "avepool bwd");
     return CAFFE_OK;
 }
 
@@ -549,16 +703,18 @@ caffe_status caffe_lrn_forward(const caffe_lrn_desc* desc, const caffe_blob* bot
                                caffe_stream_t stream) {
     caffe_status st;
     if ((st = lrn_validate(desc)) || (st = check_blob(bottom, "bottom")) || (st = check_blob(top, "top"))) return st;
-    if (!same_shape(bottom->shape, top->shape) || bottom->dtype != top->dtype) return fail(CAFFE_E_SHAPE, "top must match bottom");
+    if (!same_shape(bottom->shape, top->shape) || bottom->dtype != top->dtype || bottom->layout != top->layout)
+        return fail(CAFFE_E_SHAPE, "top must match bottom (shape, dtype, layout)");
     if (scale) {
         if ((st = check_blob(scale, "scale"))) return st;
-        if (scale->dtype != CAFFE_F32 || !same_shape(scale->shape, bottom->shape)) return fail(CAFFE_E_SHAPE, "scale must be F32 of bottom's shape");
+        if (scale->dtype != CAFFE_F32 || !same_shape(scale->shape, bottom->shape) || scale->layout != bottom->layout)
+            return fail(CAFFE_E_SHAPE, "scale must be F32 with bottom's shape and layout");
     }
     if (overlap(top, bottom) || overlap(scale, bottom) || overlap(scale, top)) return fail(CAFFE_E_ALIAS, "LRN outputs overlap");
     if (bottom->shape.n == 0) return CAFFE_OK;
     const caffe_shape4& s = bottom->shape;
-    CK(lrn_fwd(bottom->ptr, top->ptr, scale ? (float*)scale->ptr : nullptr, bottom->dtype == CAFFE_BF16, s.n, s.c,
-               (long long)s.h * s.w, desc->local_size, desc->alpha, desc->beta, desc->k, (cudaStream_t)stream),
+    CK(lrn_fwd(bottom->ptr, top->ptr, scale ? (float*)scale->ptr : nullptr, isbf(bottom), nhwc(bottom), s.n, s.c, s.h, s.w,
+               desc->local_size, desc->alpha, desc->beta, desc->k, (cudaStream_t)stream),
        "lrn fwd");
     return CAFFE_OK;
 }
@@ -575,21 +731,31 @@ caffe_status caffe_lrn_backward(const caffe_lrn_desc* desc, const caffe_blob* bo
         return fail(CAFFE_E_SHAPE, "LRN backward blobs must share bottom's shape");
     const caffe_dtype dt = bottom->dtype;
     if (top->dtype != dt || top_diff->dtype != dt || bottom_diff->dtype != dt) return fail(CAFFE_E_DTYPE, "LRN blobs must share one dtype");
+    if (top->layout != bottom->layout || top_diff->layout != bottom->layout || bottom_diff->layout != bottom->layout)
+        return fail(CAFFE_E_SHAPE, "LRN blobs must share one layout");
     if (scale) {
         if ((st = check_blob(scale, "scale"))) return st;
-        if (scale->dtype != CAFFE_F32 || !same_shape(scale->shape, s)) return fail(CAFFE_E_SHAPE, "scale must be F32 of bottom's shape");
+        if (scale->dtype != CAFFE_F32 || !same_shape(scale->shape, s) || scale->layout != bottom->layout)
+            return fail(CAFFE_E_SHAPE, "scale must be F32 with bottom's shape and layout");
     }
     if (overlap(bottom_diff, bottom) || overlap(bottom_diff, top) || overlap(bottom_diff, top_diff) || overlap(bottom_diff, scale))
         return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
     if (s.n == 0) return CAFFE_OK;
     CK(lrn_bwd(bottom->ptr, top->ptr, top_diff->ptr, scale ? (const float*)scale->ptr : nullptr, bottom_diff->ptr,
-               dt == CAFFE_BF16, s.n, s.c, (long long)s.h * s.w, desc->local_size, desc->alpha, desc->beta, desc->k,
+               dt == CAFFE_BF16, nhwc(bottom), s.n, s.c, s.h, s.w, desc->local_size, desc->alpha, desc->beta, desc->k,
                (cudaStream_t)stream),
        "lrn bwd");
     return CAFFE_OK;
 }
 
 // ------------------------------------------------------------------ inner product
+// bottom (N,C,H,W) is flattened to rows of K = C*H*W in the (c,h,w) order of S:130; an NHWC bottom
+// with H*W > 1 and C > 1 is staged into that order.
+static bool rows_direct(const caffe_blob* b, int E) {
+    const bool order_ok = !nhwc(b) || (b->shape.h == 1 && b->shape.w == 1) || b->shape.c == 1;
+    const long long K = (long long)b->shape.c * b->shape.h * b->shape.w;
+    return order_ok && E == 2 && b->dtype == CAFFE_BF16 && aligned16(b->ptr) && (K * 2) % 16 == 0;
+}
 static caffe_status ip_shapes(const caffe_blob* bottom, const caffe_blob* weight, long long* K, int* O) {
     *K = (long long)bottom->shape.c * bottom->shape.h * bottom->shape.w;
     *O = weight->shape.n;
@@ -601,24 +767,31 @@ static caffe_status ip_shapes(const caffe_blob* bottom, const caffe_blob* weight
 
 caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32_t O, int32_t pass, size_t* bytes) {
     if (!bytes) return fail(CAFFE_E_INVALID, "bytes is NULL");
-    if (math == CAFFE_MATH_FP32) { *bytes = 0; return CAFFE_OK; }
-    if (math != CAFFE_MATH_BF16 && math != CAFFE_MATH_TF32) return fail(CAFFE_E_INVALID, "bad math mode");
-    const int E = math == CAFFE_MATH_TF32 ? 4 : 2, CHh = 128 / E;
+    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16 && math != CAFFE_MATH_TF32) return fail(CAFFE_E_INVALID, "bad math mode");
     const long long N = bottom.n, K = (long long)bottom.c * bottom.h * bottom.w;
-    // worst case: every operand staged
-    size_t s = align1k((size_t)N * rup(K, CHh) * E) + align1k((size_t)O * rup(K, CHh) * E) + align1k((size_t)N * rup(O, CHh) * E);
-    (void)pass;
-    *bytes = s;
+    size_t bias = align1k((size_t)bias_grad_splits((int)N, O, 1) * O * 4);
+    if (math == CAFFE_MATH_FP32) { *bytes = pass == CAFFE_PASS_BACKWARD_WEIGHT ? bias : 0; return CAFFE_OK; }
+    const int E = math == CAFFE_MATH_TF32 ? 4 : 2, CHh = 128 / E;
+    // worst case: every operand staged (+ fp32 rows for an NHWC data gradient) + bias partials
+    *bytes = align1k((size_t)N * rup(K, CHh) * E) + align1k((size_t)O * rup(K, CHh) * E) +
+             align1k((size_t)N * rup(O, CHh) * E) + align1k((size_t)N * K * 4) + bias;
     return CAFFE_OK;
 }
 
-// stage src (rows x cols, ld = cols) into dst with padded ld, return pointer to use and its ld
-static cudaError_t stage(const caffe_blob* b, long long rows, long long cols, int E, char*& cursor, const void** out,
-                         long long* ld, cudaStream_t s) {
-    const bool ok = (E == 2 ? b->dtype == CAFFE_BF16 : false) && aligned16(b->ptr) && (cols * E) % 16 == 0;
-    if (ok) { *out = b->ptr; *ld = cols; return cudaSuccess; }
+// stage a blob as (rows x cols) TMA-able rows (bf16 or tf32) into `cursor`, return pointer and ld
+static cudaError_t stage_rows(const caffe_blob* b, long long rows, long long cols, int E, char*& cursor, const void** out,
+                              long long* ld, cudaStream_t s) {
+    if (rows_direct(b, E)) {
+        *out = b->ptr;
+        *ld = cols;
+        return cudaSuccess;
+    }
     const long long ldp = rup(cols, 128 / E);
-    cudaError_t e = convert_pad_2d(b->ptr, b->dtype == CAFFE_BF16, cols, cursor, E, ldp, rows, cols, s);
+    cudaError_t e;
+    if (nhwc(b) && b->shape.h * b->shape.w > 1 && b->shape.c > 1)
+        e = nhwc_to_rows(b->ptr, isbf(b), cursor, E, b->shape.n, b->shape.c, b->shape.h * b->shape.w, ldp, s);
+    else
+        e = convert_pad_2d(b->ptr, isbf(b), cols, cursor, E, ldp, rows, cols, s);
     *out = cursor;
     *ld = ldp;
     cursor += align1k((size_t)rows * ldp * E);
@@ -647,9 +820,12 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
     const int relu = (flags & CAFFE_FUSE_RELU) ? 1 : 0;
     const float* bptr = bias ? (const float*)bias->ptr : nullptr;
     if (math == CAFFE_MATH_FP32) {
-        ConvGeom g{N, bottom->shape.c, bottom->shape.h, bottom->shape.w, O, bottom->shape.h, bottom->shape.w, 1, 1, 0, 0, 1, 1, 1};
-        CK(fp32_conv_fwd(bottom->ptr, bottom->dtype == CAFFE_BF16, weight->ptr, weight->dtype == CAFFE_BF16, bptr, top->ptr,
-                         top->dtype == CAFFE_BF16, relu, g, s), "ip fwd fp32");
+        const caffe_shape4& b = bottom->shape;
+        ConvGeom g{N, b.c, b.h, b.w, O, b.h, b.w, 1, 1, 0, 0, 1, 1, 1};
+        L4 ly{O, 1, 1, 1};
+        CK(fp32_conv_fwd(bottom->ptr, isbf(bottom), strides(bottom), weight->ptr, isbf(weight), bptr, top->ptr, isbf(top), ly,
+                         1, relu, g, s),
+           "ip fwd fp32");
         return CAFFE_OK;
     }
     size_t need;
@@ -659,8 +835,8 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
     char* cur = (char*)ws;
     const void *A, *B;
     long long lda, ldb;
-    CK(stage(bottom, N, K, E, cur, &A, &lda, s), "stage bottom");
-    CK(stage(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
+    CK(stage_rows(bottom, N, K, E, cur, &A, &lda, s), "stage bottom");
+    CK(stage_rows(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
     TcLaunch L;
     memset(&L, 0, sizeof L);
     L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
@@ -671,10 +847,10 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip fwd)");
     a.M = N; a.N = O; a.m_tiles = (int)cdiv(N, 128); a.n_tiles = (int)cdiv(O, a.BN); a.groups = 1; a.splits = 1;
     a.kblocks = (int)cdiv(K, 128 / E); a.kb_per_split = a.kblocks;
-    a.out = top->ptr; a.out_bf16 = top->dtype == CAFFE_BF16; a.s_n = O; a.s_c = 1; a.s_p = 0; a.P = 1; a.col_g = 0;
+    a.out = top->ptr; a.out_bf16 = isbf(top); a.s_n = O; a.s_c = 1; a.s_p = 0; a.P = 1; a.col_g = 0;
     a.bias = bptr; a.relu = relu; a.beta = 0.f;
     finish_args(a, a.BN * 128);
-    return run_tc(L, s);
+    return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }
 
 caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
@@ -693,11 +869,13 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
     if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16) return fail(CAFFE_E_INVALID, "bad math");
     if (N == 0) return CAFFE_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    const caffe_shape4& xs = bottom_diff->shape;
     if (math == CAFFE_MATH_FP32) {
-        ConvGeom g{N, bottom_diff->shape.c, bottom_diff->shape.h, bottom_diff->shape.w, O, bottom_diff->shape.h,
-                   bottom_diff->shape.w, 1, 1, 0, 0, 1, 1, 1};
-        CK(fp32_conv_dgrad(top_diff->ptr, top_diff->dtype == CAFFE_BF16, weight->ptr, weight->dtype == CAFFE_BF16,
-                           bottom_diff->ptr, bottom_diff->dtype == CAFFE_BF16, beta, g, s), "ip dgrad fp32");
+        ConvGeom g{N, xs.c, xs.h, xs.w, O, xs.h, xs.w, 1, 1, 0, 0, 1, 1, 1};
+        L4 ly{O, 1, 1, 1};
+        CK(fp32_conv_dgrad(top_diff->ptr, isbf(top_diff), ly, weight->ptr, isbf(weight), bottom_diff->ptr,
+                           isbf(bottom_diff), nhwc(bottom_diff), beta, g, s),
+           "ip dgrad fp32");
         return CAFFE_OK;
     }
     size_t need;
@@ -707,8 +885,10 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
     char* cur = (char*)ws;
     const void *A, *B;
     long long lda, ldb;
-    CK(stage(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
-    CK(stage(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
+    CK(stage_rows(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
+    CK(stage_rows(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
+    const bool permute = nhwc(bottom_diff) && xs.h * xs.w > 1 && xs.c > 1;
+    float* rows = permute ? (float*)cur : nullptr;
     TcLaunch L;
     memset(&L, 0, sizeof L);
     L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
@@ -718,10 +898,16 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip dgrad)");
     a.M = N; a.N = (int)K; a.m_tiles = (int)cdiv(N, 128); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1; a.splits = 1;
     a.kblocks = (int)cdiv(O, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
-    a.out = bottom_diff->ptr; a.out_bf16 = bottom_diff->dtype == CAFFE_BF16; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1;
-    a.beta = beta;
+    if (permute) {
+        a.out = rows; a.out_bf16 = 0; a.beta = 0.f;
+    } else {
+        a.out = bottom_diff->ptr; a.out_bf16 = isbf(bottom_diff); a.beta = beta;
+    }
+    a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1;
     finish_args(a, a.b_nchunks * 64 * 128);
-    return run_tc(L, s);
+    if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
+    if (permute) CK(rows_to_nhwc(rows, K, bottom_diff->ptr, isbf(bottom_diff), N, xs.c, xs.h * xs.w, beta, s), "ip dgrad to NHWC");
+    return CAFFE_OK;
 }
 
 caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom, const caffe_blob* top_diff,
@@ -748,22 +934,27 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16) return fail(CAFFE_E_INVALID, "bad math");
     if (N == 0) return CAFFE_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if (bias_diff) CK(bias_grad(top_diff->ptr, top_diff->dtype == CAFFE_BF16, (float*)bias_diff->ptr, beta, N, O, 1, s), "ip bias grad");
+    size_t need;
+    caffe_ip_workspace_size(math, bottom->shape, O, CAFFE_PASS_BACKWARD_WEIGHT, &need);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    char* cur = (char*)ws;
+    float* bpart = (float*)cur;
+    cur += align1k((size_t)bias_grad_splits(N, O, 1) * O * 4);
+    if (bias_diff) CK(bias_grad(top_diff->ptr, isbf(top_diff), 1, (float*)bias_diff->ptr, beta, N, O, 1, bpart, s), "ip bias grad");
     if (math == CAFFE_MATH_FP32) {
-        ConvGeom g{N, bottom->shape.c, bottom->shape.h, bottom->shape.w, O, bottom->shape.h, bottom->shape.w, 1, 1, 0, 0, 1, 1, 1};
-        CK(fp32_conv_wgrad(bottom->ptr, bottom->dtype == CAFFE_BF16, top_diff->ptr, top_diff->dtype == CAFFE_BF16,
-                           (float*)weight_diff->ptr, beta, g, s), "ip wgrad fp32");
+        const caffe_shape4& b = bottom->shape;
+        ConvGeom g{N, b.c, b.h, b.w, O, b.h, b.w, 1, 1, 0, 0, 1, 1, 1};
+        L4 ly{O, 1, 1, 1};
+        CK(fp32_conv_wgrad(bottom->ptr, isbf(bottom), strides(bottom), top_diff->ptr, isbf(top_diff), ly,
+                           (float*)weight_diff->ptr, beta, g, s),
+           "ip wgrad fp32");
         return CAFFE_OK;
     }
-    size_t need;
-    caffe_ip_workspace_size(math, bottom->shape, O, 2, &need);
-    if ((st = check_ws(ws, ws_bytes, need))) return st;
     const int E = 2;
-    char* cur = (char*)ws;
     const void *A, *B;
     long long lda, ldb;
-    CK(stage(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
-    CK(stage(bottom, N, K, E, cur, &B, &ldb, s), "stage bottom");
+    CK(stage_rows(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
+    CK(stage_rows(bottom, N, K, E, cur, &B, &ldb, s), "stage bottom");
     TcLaunch L;
     memset(&L, 0, sizeof L);
     L.esz = E; L.amode = A_TILED_MN; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
@@ -775,7 +966,7 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
     a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
     finish_args(a, a.b_nchunks * 64 * 128);
-    return run_tc(L, s);
+    return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }
 
 // ------------------------------------------------------------------ im2col / col2im
@@ -784,6 +975,8 @@ caffe_status caffe_im2col(const caffe_conv_desc* desc, const caffe_blob* bottom,
     caffe_status st;
     if ((st = check_blob(bottom, "bottom")) || (st = check_blob(col, "col"))) return st;
     if (bottom->dtype != CAFFE_F32 || col->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "im2col is F32 only");
+    if (nhwc(bottom) || nhwc(col)) return fail(CAFFE_E_INVALID, "im2col is defined on NCHW blobs (S:297)");
+    if (!desc) return fail(CAFFE_E_INVALID, "desc is NULL");
     caffe_conv_desc d = *desc;
     d.group = 1;
     Plan p;
@@ -800,6 +993,8 @@ caffe_status caffe_col2im(const caffe_conv_desc* desc, const caffe_blob* col, in
     caffe_status st;
     if ((st = check_blob(bottom_diff, "bottom_diff")) || (st = check_blob(col, "col"))) return st;
     if (bottom_diff->dtype != CAFFE_F32 || col->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "col2im is F32 only");
+    if (nhwc(bottom_diff) || nhwc(col)) return fail(CAFFE_E_INVALID, "col2im is defined on NCHW blobs (S:297)");
+    if (!desc) return fail(CAFFE_E_INVALID, "desc is NULL");
     caffe_conv_desc d = *desc;
     d.group = 1;
     Plan p;
@@ -819,14 +1014,16 @@ caffe_status caffe_softmax_loss(const caffe_blob* scores, const int32_t* labels,
     if (!labels || !loss) return fail(CAFFE_E_INVALID, "labels and loss are required");
     const int N = scores->shape.n;
     const long long K = (long long)scores->shape.c * scores->shape.h * scores->shape.w;
+    if (scores->shape.h * scores->shape.w != 1 && nhwc(scores)) return fail(CAFFE_E_INVALID, "scores must be (N,K,1,1) or NCHW");
     if (score_diff) {
         if ((st = check_blob(score_diff, "score_diff"))) return st;
         if (!same_shape(score_diff->shape, scores->shape)) return fail(CAFFE_E_SHAPE, "score_diff must match scores");
+        if (score_diff->shape.h * score_diff->shape.w != 1 && nhwc(score_diff)) return fail(CAFFE_E_INVALID, "score_diff must be NCHW");
         if (overlap(score_diff, scores)) return fail(CAFFE_E_ALIAS, "score_diff overlaps scores");
     }
     if (N == 0) return CAFFE_OK;
-    CK(softmax_loss_k(scores->ptr, scores->dtype == CAFFE_BF16, labels, loss, score_diff ? score_diff->ptr : nullptr,
-                      score_diff ? score_diff->dtype == CAFFE_BF16 : 0, N, (int)K, (cudaStream_t)stream),
+    CK(softmax_loss_k(scores->ptr, isbf(scores), labels, loss, score_diff ? score_diff->ptr : nullptr,
+                      score_diff ? isbf(score_diff) : 0, N, (int)K, (cudaStream_t)stream),
        "softmax loss");
     return CAFFE_OK;
 }
@@ -836,6 +1033,8 @@ caffe_status caffe_sgd_update(float* w, const float* g, float* v, void* w_bf16, 
     if (count < 0) return fail(CAFFE_E_SHAPE, "negative count");
     if (count == 0) return CAFFE_OK;
     if (!w || !g || !v) return fail(CAFFE_E_INVALID, "w, g and v are required");
+    if (!aligned16(w) || !aligned16(g) || !aligned16(v) || (reinterpret_cast<uintptr_t>(w_bf16) & 7))
+        return fail(CAFFE_E_ALIGN, "SGD buffers must be 16-byte aligned (w_bf16 8-byte)");
     CK(sgd_k(w, g, v, w_bf16, count, lr, momentum, decay, grad_scale, (cudaStream_t)stream), "sgd update");
     return CAFFE_OK;
 }

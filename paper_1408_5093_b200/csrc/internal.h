@@ -49,6 +49,8 @@ struct TcLaunch {
 };
 
 size_t tc_smem_bytes(const TcArgs& a);
+// instrumentation (abi.cu): every kernel launch of the library is counted.
+void note_launch();
 cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s);
 int num_sms();
 
@@ -58,22 +60,30 @@ bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, 
 bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
                       int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels);
 
-// ------------------------------------------------------------------ packing kernels (pack.cu)
-// Activation NCHW -> packed NHWC [N][Hp][Wp][G*Cgp] in bf16 (esz 2) or tf32-rounded fp32 (esz 4).
-// Space-to-depth for stride s>1: channel (dy*sw+dx)*Cg+c of packed pixel (Y,X) is
-// X[n][g*Cg+c][Y*sh+dy-ph][X*sw+dx-pw] (0 outside); for s=1 (no s2d) the padding is left to TMA.
-struct PackGeom {
-    int N, C, H, W, G, Cg;              // source (NCHW) geometry
-    int sh, sw, ph, pw;                 // s2d block (1,1 = plain transpose) and the pad folded into s2d
-    int Hp, Wp, Cgp;                    // packed geometry
+// element strides of a 4-D blob (n, c, h, w) -> n*sn + c*sc + h*sh + w*sw (32-bit: blobs < 2^31)
+struct L4 {
+    int sn, sc, sh, sw;
 };
-cudaError_t pack_nhwc(const void* src, int src_bf16, void* dst, int dst_esz, const PackGeom& g, cudaStream_t s);
-// Inverse for the s2d data gradient: dX[n][c][h][w] = beta*dX + T[n][(h+ph)/sh][(w+pw)/sw][g*Cgp+((h+ph)%sh*sw+(w+pw)%sw)*Cg+c]
-cudaError_t unpack_s2d_grad(const float* T, void* dX, int dx_bf16, float beta, const PackGeom& g, cudaStream_t s);
-// Weights (O, Cg, kh, kw) -> forward B operand [G*Og rows][taps'*Cgp] (s2d-aware).
+
+// ------------------------------------------------------------------ packing kernels (pack.cu)
+// Activation -> packed channels-last operand [N][Hp][Wp][Ctot] in bf16 (esz 2) or tf32-rounded
+// fp32 (esz 4); group g's channels start at g*cpg.  Space-to-depth for stride s>1: channel
+// (dy*sw+dx)*Cg+c of packed pixel (Y,X) of group g is X[n][g*Cg+c][Y*sh+dy-ph][X*sw+dx-pw] (0 outside);
+// for s=1 (sh=sw=1, ph=pw=0) it is a plain transpose and TMA supplies the zero padding.
+struct PackGeom {
+    int N, C, H, W, G, Cg;              // source geometry
+    int sh, sw, ph, pw;                 // s2d block (1,1 = plain) and the pad folded into s2d
+    int Hp, Wp, cpg, Ctot;              // packed geometry
+};
+cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* dst, int dst_esz, const PackGeom& g,
+                     cudaStream_t s);
+// Inverse for the s2d data gradient into a blob of either layout, with beta.
+cudaError_t unpack_s2d_grad(const float* T, void* dX, int dx_bf16, int xnhwc, float beta, const PackGeom& g,
+                            cudaStream_t s);
+// Weights (O, Cg, kh, kw) -> forward B operand [G*Og rows][taps'*Cgp] (s2d-aware, zero K padding).
 struct WGeom {
     int O, G, Cg, Og, kh, kw, sh, sw;   // original filter geometry (sh,sw = s2d block)
-    int khp, kwp, Cgp, Ogp;             // effective (s2d) kernel, padded channels
+    int khp, kwp, Cgp, Ogp;             // effective (s2d) kernel, K-padded channels
 };
 cudaError_t repack_w_fwd(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, cudaStream_t s);
 // dgrad B operand [G*Cge rows][taps'*Ogp]: row (g, c''), k = (i',j', o), value = fwd-packed W at
@@ -86,35 +96,42 @@ cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeo
 // Generic 2-D convert/pad: dst[r][c] (ld_dst, esz) = src[r][c] (ld_src, f32|bf16) for c < cols, 0 up to ld_dst.
 cudaError_t convert_pad_2d(const void* src, int src_bf16, long long ld_src, void* dst, int dst_esz,
                            long long ld_dst, long long rows, long long cols, cudaStream_t s);
+// NHWC blob -> (N, ld) rows in the (c,h,w) flatten order of S:130, and back (fp32 rows, beta).
+cudaError_t nhwc_to_rows(const void* src, int src_bf16, void* dst, int dst_esz, int N, int C, int HW, long long ld,
+                         cudaStream_t s);
+cudaError_t rows_to_nhwc(const float* src, long long ld, void* dst, int dst_bf16, int N, int C, int HW, float beta,
+                         cudaStream_t s);
 
 // ------------------------------------------------------------------ CUDA-core kernels (simple.cu)
 struct ConvGeom {
     int N, C, H, W, O, kh, kw, sh, sw, ph, pw, G, OH, OW;
 };
-cudaError_t fp32_conv_fwd(const void* x, int x_bf16, const void* w, int w_bf16, const float* b, void* y, int y_bf16,
-                          int relu, const ConvGeom& g, cudaStream_t s);
-cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, const void* w, int w_bf16, void* dx, int dx_bf16,
+cudaError_t fp32_conv_fwd(const void* x, int x_bf16, L4 lx, const void* w, int w_bf16, const float* b, void* y,
+                          int y_bf16, L4 ly, int ynhwc, int relu, const ConvGeom& g, cudaStream_t s);
+cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, L4 ly, const void* w, int w_bf16, void* dx, int dx_bf16,
+                            int xnhwc, float beta, const ConvGeom& g, cudaStream_t s);
+cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, L4 lx, const void* dy, int dy_bf16, L4 ly, float* dw,
                             float beta, const ConvGeom& g, cudaStream_t s);
-cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, const void* dy, int dy_bf16, float* dw, float beta,
-                            const ConvGeom& g, cudaStream_t s);
-cudaError_t bias_grad(const void* dy, int dy_bf16, float* db, float beta, int N, int O, long long P,
+int bias_grad_splits(int N, int O, int P);
+cudaError_t bias_grad(const void* dy, int dy_bf16, int nhwc, float* db, float beta, int N, int O, int P, float* part,
                       cudaStream_t s);
 cudaError_t im2col_k(const float* x, int n, const ConvGeom& g, float* col, cudaStream_t s);
 cudaError_t col2im_k(const float* col, int n, const ConvGeom& g, float* dx, cudaStream_t s);
-cudaError_t relu_fwd(const void* x, void* y, int bf16, long long count, cudaStream_t s);
-cudaError_t relu_bwd(const void* x, const void* dy, void* dx, int x_bf16, int d_bf16, long long count,
-                     cudaStream_t s);
+cudaError_t relu_fwd(const void* x, void* y, int bf16, int count, cudaStream_t s);
+cudaError_t relu_bwd(const void* x, const void* dy, void* dx, int x_bf16, int d_bf16, int count, cudaStream_t s);
 struct PoolGeom {
     int N, C, H, W, kh, kw, sh, sw, ph, pw, OH, OW;
 };
-cudaError_t maxpool_fwd(const void* x, void* y, int32_t* mask, int bf16, const PoolGeom& g, cudaStream_t s);
-cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, void* dx, int bf16, const PoolGeom& g, cudaStream_t s);
-cudaError_t avepool_fwd(const void* x, void* y, int bf16, const PoolGeom& g, cudaStream_t s);
-cudaError_t avepool_bwd(const void* dy, void* dx, int bf16, const PoolGeom& g, cudaStream_t s);
-cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int N, int C, long long P, int size,
+cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask, int bf16, const PoolGeom& g,
+                        cudaStream_t s);
+cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g,
+                        cudaStream_t s);
+cudaError_t avepool_fwd(const void* x, L4 lx, void* y, int ynhwc, int bf16, const PoolGeom& g, cudaStream_t s);
+cudaError_t avepool_bwd(const void* dy, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g, cudaStream_t s);
+cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int nhwc, int N, int C, int H, int W, int size,
                     float alpha, float beta, float k, cudaStream_t s);
-cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* scale, void* dx, int bf16, int N,
-                    int C, long long P, int size, float alpha, float beta, float k, cudaStream_t s);
+cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* scale, void* dx, int bf16, int nhwc,
+                    int N, int C, int H, int W, int size, float alpha, float beta, float k, cudaStream_t s);
 cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff,
                            int diff_bf16, int N, int K, cudaStream_t s);
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,

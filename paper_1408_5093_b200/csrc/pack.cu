@@ -1,7 +1,8 @@
-// pack.cu -- layout kernels around the tensor-core GEMM: NCHW -> packed NHWC activations
-// (with space-to-depth for strided convolutions), weight repacks for forward and data-gradient
-// operands, the s2d data-gradient unpack, and the fixed-order weight-gradient split reduction.
-// These are bandwidth kernels: one read and one write of each element, 16-byte stores.
+// pack.cu -- layout kernels around the tensor-core GEMM: activations into the packed channels-last
+// operand layout (transpose of NCHW blobs, space-to-depth for strided convolutions, dtype
+// conversion), weight repacks for the forward and data-gradient operands, the s2d data-gradient
+// unpack, the fixed-order weight-gradient split reduction and a generic 2-D convert/pad.
+// Bandwidth kernels: one read and one write per element, 16-byte stores.
 #include "internal.h"
 
 #include <cuda_bf16.h>
@@ -16,43 +17,53 @@ __device__ __forceinline__ float tf32_rn(float x) {
     asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
 }
-
 static inline unsigned blocks_for(long long n, int t) {
     long long b = (n + t - 1) / t;
-    return (unsigned)(b > 0x7fffffff ? 0x7fffffff : b);
+    if (b > 148LL * 32) b = 148LL * 32;
+    return (unsigned)(b < 1 ? 1 : b);
 }
 
 // ---------------------------------------------------------------- activations
-// One thread = one packed pixel x 8 consecutive packed channels.  Pixel index fastest so the
-// NCHW reads of a warp are consecutive w.
-__global__ void pack_nhwc_kernel(const void* __restrict__ src, int src_bf16, void* __restrict__ dst, int dst_esz,
-                                 PackGeom g, long long total) {
-    const int Ctot = g.G * g.Cgp;
-    const int cvecs = Ctot / 8;
-    const long long HWp = (long long)g.Hp * g.Wp;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long pix = t % HWp;
-        long long r = t / HWp;
-        const int cv = (int)(r % cvecs);
-        const int n = (int)(r / cvecs);
-        const int Y = (int)(pix / g.Wp), X = (int)(pix % g.Wp);
+// Generic: one thread = one packed pixel x one 16-byte vector of packed channels; pixel fastest so
+// NCHW reads of a warp are consecutive w.  Handles s2d, any source layout, any dtype.
+__global__ void pack_generic_kernel(const void* __restrict__ src, int src_bf16, L4 ls, void* __restrict__ dst,
+                                    int dst_esz, PackGeom g, int total, int cvec_fastest) {
+    const int vec = 16 / dst_esz;
+    const int cvecs = g.Ctot / vec;
+    const int HWp = g.Hp * g.Wp;
+    const int real = g.Cg * g.sh * g.sw;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        int pix, cv, n;
+        if (cvec_fastest) {   // channels-last source: neighbouring threads read neighbouring channels
+            cv = t % cvecs;
+            const int r = t / cvecs;
+            pix = r % HWp;
+            n = r / HWp;
+        } else {              // NCHW source: neighbouring threads read neighbouring pixels
+            pix = t % HWp;
+            const int r = t / HWp;
+            cv = r % cvecs;
+            n = r / cvecs;
+        }
+        const int Y = pix / g.Wp, X = pix - (pix / g.Wp) * g.Wp;
         float v[8];
 #pragma unroll
         for (int e = 0; e < 8; e++) {
-            const int cpk = cv * 8 + e;
-            const int grp = cpk / g.Cgp, cc = cpk % g.Cgp;
-            float x = 0.f;
-            if (cc < g.Cg * g.sh * g.sw) {
-                const int d = cc / g.Cg, c = cc % g.Cg;
-                const int dy = d / g.sw, dx = d % g.sw;
-                const int h = Y * g.sh + dy - g.ph, w = X * g.sw + dx - g.pw;
-                if (h >= 0 && h < g.H && w >= 0 && w < g.W)
-                    x = ld_any(src, (((long long)n * g.C + grp * g.Cg + c) * g.H + h) * g.W + w, src_bf16);
+            v[e] = 0.f;
+            if (e < vec) {
+                const int cpk = cv * vec + e;
+                const int grp = cpk / g.cpg, cc = cpk - grp * g.cpg;
+                if (cc < real && grp < g.G) {
+                    const int d = cc / g.Cg, c = cc - d * g.Cg;
+                    const int dy = d / g.sw, dx = d - dy * g.sw;
+                    const int h = Y * g.sh + dy - g.ph, w = X * g.sw + dx - g.pw;
+                    if (h >= 0 && h < g.H && w >= 0 && w < g.W)
+                        v[e] = ld_any(src, (long long)n * ls.sn + (grp * g.Cg + c) * ls.sc + h * ls.sh + w * ls.sw,
+                                      src_bf16);
+                }
             }
-            v[e] = x;
         }
-        const long long o = ((long long)n * HWp + pix) * Ctot + cv * 8;
+        const long long o = ((long long)n * HWp + pix) * g.Ctot + cv * vec;
         if (dst_esz == 2) {
             uint4 pk;
             __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
@@ -60,37 +71,77 @@ __global__ void pack_nhwc_kernel(const void* __restrict__ src, int src_bf16, voi
             for (int e = 0; e < 4; e++) h2[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
             *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + o) = pk;
         } else {
-            float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o);
-            d4[0] = make_float4(tf32_rn(v[0]), tf32_rn(v[1]), tf32_rn(v[2]), tf32_rn(v[3]));
-            d4[1] = make_float4(tf32_rn(v[4]), tf32_rn(v[5]), tf32_rn(v[6]), tf32_rn(v[7]));
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o) =
+                make_float4(tf32_rn(v[0]), tf32_rn(v[1]), tf32_rn(v[2]), tf32_rn(v[3]));
         }
     }
 }
 
-cudaError_t pack_nhwc(const void* src, int src_bf16, void* dst, int dst_esz, const PackGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.Hp * g.Wp * (g.G * g.Cgp / 8);
-    if (total == 0) return cudaSuccess;
-    pack_nhwc_kernel<<<blocks_for(total, 256), 256, 0, s>>>(src, src_bf16, dst, dst_esz, g, total);
+// Fast path for a stride-1 NCHW source into bf16 NHWC with natural (unpadded, cpg == Cg) channels:
+// a 64-channel x 64-pixel tile is read coalesced along pixels into shared memory and written
+// coalesced along channels.
+__global__ void pack_transpose_kernel(const void* __restrict__ src, int src_bf16, __nv_bfloat16* __restrict__ dst,
+                                      int C, int P, int Ctot) {
+    __shared__ float tile[64][65];
+    const int n = blockIdx.z, p0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 256 threads: 64 x 4
+    const long long sbase = (long long)n * C * P;
+    for (int r = ty; r < 64; r += 4) {
+        const int c = c0 + r, p = p0 + tx;
+        tile[r][tx] = (c < C && p < P) ? ld_any(src, sbase + (long long)c * P + p, src_bf16) : 0.f;
+    }
+    __syncthreads();
+    // write: each thread stores 2 consecutive channels (bf16x2) of one pixel
+    const int cpair = threadIdx.x & 31, prow = threadIdx.x >> 5;  // 32 pairs x 8 pixel rows
+    for (int r = prow; r < 64; r += 8) {
+        const int p = p0 + r, c = c0 + 2 * cpair;
+        if (p < P && c < Ctot) {
+            __nv_bfloat162 v = __floats2bfloat162_rn(tile[2 * cpair][r], tile[2 * cpair + 1][r]);
+            if (c + 1 < Ctot)
+                *reinterpret_cast<__nv_bfloat162*>(dst + ((long long)n * P + p) * Ctot + c) = v;
+            else
+                dst[((long long)n * P + p) * Ctot + c] = v.x;
+        }
+    }
+}
+
+cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* dst, int dst_esz, const PackGeom& g,
+                     cudaStream_t s) {
+    const bool plain = g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.Hp == g.H && g.Wp == g.W;
+    if (plain && !src_nhwc && dst_esz == 2 && g.cpg == g.Cg && g.G * g.Cg <= g.Ctot) {
+        const int P = g.H * g.W;
+        dim3 grid((P + 63) / 64, (g.Ctot + 63) / 64, g.N);
+        pack_transpose_kernel<<<grid, 256, 0, s>>>(src, src_bf16, (__nv_bfloat16*)dst, g.C, P, g.Ctot);
+    } else {
+        const int total = g.N * g.Hp * g.Wp * (g.Ctot * dst_esz / 16);
+        if (total == 0) return cudaSuccess;
+        pack_generic_kernel<<<blocks_for(total, 256), 256, 0, s>>>(src, src_bf16, ls, dst, dst_esz, g, total,
+                                                                    src_nhwc);
+    }
+    note_launch();
     return cudaGetLastError();
 }
 
-__global__ void unpack_s2d_kernel(const float* __restrict__ T, void* __restrict__ dX, int dx_bf16, float beta,
-                                  PackGeom g, long long total) {
-    const int Ctot = g.G * g.Cgp;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int w = (int)(t % g.W);
-        long long r = t / g.W;
-        const int h = (int)(r % g.H);
-        r /= g.H;
-        const int cfull = (int)(r % g.C);
-        const int n = (int)(r / g.C);
-        const int grp = cfull / g.Cg, c = cfull % g.Cg;
+// Inverse of the s2d packing for the data gradient, into a blob of any layout (lx), with beta.
+__global__ void unpack_s2d_kernel(const float* __restrict__ T, void* __restrict__ dX, int dx_bf16, int xnhwc,
+                                  float beta, PackGeom g, int total) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        int n, cfull, h, w, r = t;
+        if (xnhwc) {
+            cfull = r % g.C; r /= g.C;
+            w = r % g.W; r /= g.W;
+            h = r % g.H; n = r / g.H;
+        } else {
+            w = r % g.W; r /= g.W;
+            h = r % g.H; r /= g.H;
+            cfull = r % g.C; n = r / g.C;
+        }
+        const int grp = cfull / g.Cg, c = cfull - grp * g.Cg;
         const int hh = h + g.ph, ww = w + g.pw;
-        const int Y = hh / g.sh, dy = hh % g.sh, X = ww / g.sw, dx = ww % g.sw;
+        const int Y = hh / g.sh, dy = hh - Y * g.sh, X = ww / g.sw, dx = ww - X * g.sw;
         float v = 0.f;
         if (Y < g.Hp && X < g.Wp)
-            v = T[(((long long)n * g.Hp + Y) * g.Wp + X) * Ctot + grp * g.Cgp + (dy * g.sw + dx) * g.Cg + c];
+            v = T[(((long long)n * g.Hp + Y) * g.Wp + X) * g.Ctot + grp * g.cpg + (dy * g.sw + dx) * g.Cg + c];
         if (dx_bf16) {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dX) + t;
             if (beta != 0.f) v += beta * __bfloat162float(*o);
@@ -103,10 +154,12 @@ __global__ void unpack_s2d_kernel(const float* __restrict__ T, void* __restrict_
     }
 }
 
-cudaError_t unpack_s2d_grad(const float* T, void* dX, int dx_bf16, float beta, const PackGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.C * g.H * g.W;
+cudaError_t unpack_s2d_grad(const float* T, void* dX, int dx_bf16, int xnhwc, float beta, const PackGeom& g,
+                            cudaStream_t s) {
+    const int total = g.N * g.C * g.H * g.W;
     if (total == 0) return cudaSuccess;
-    unpack_s2d_kernel<<<blocks_for(total, 256), 256, 0, s>>>(T, dX, dx_bf16, beta, g, total);
+    unpack_s2d_kernel<<<blocks_for(total, 256), 256, 0, s>>>(T, dX, dx_bf16, xnhwc, beta, g, total);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -126,35 +179,34 @@ __device__ __forceinline__ void st_elem(void* dst, long long i, int esz, float v
 }
 
 __global__ void repack_w_fwd_kernel(const void* __restrict__ w, int w_bf16, void* __restrict__ dst, int esz, WGeom g,
-                                    long long total) {
+                                    int total) {
     const int taps = g.khp * g.kwp;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int cc = (int)(t % g.Cgp);
-        long long r = t / g.Cgp;
-        const int tap = (int)(r % taps);
-        const int ofull = (int)(r / taps);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int cc = t % g.Cgp;
+        const int r = t / g.Cgp;
+        const int tap = r % taps;
+        const int ofull = r / taps;
         st_elem(dst, t, esz, w_packed(w, w_bf16, g, ofull, tap / g.kwp, tap % g.kwp, cc));
     }
 }
 
 cudaError_t repack_w_fwd(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.O * g.khp * g.kwp * g.Cgp;
+    const int total = g.O * g.khp * g.kwp * g.Cgp;
     repack_w_fwd_kernel<<<blocks_for(total, 256), 256, 0, s>>>(w, w_bf16, dst, dst_esz, g, total);
+    note_launch();
     return cudaGetLastError();
 }
 
 __global__ void repack_w_dgrad_kernel(const void* __restrict__ w, int w_bf16, void* __restrict__ dst, int esz,
-                                      WGeom g, int Cge, long long total) {
+                                      WGeom g, int Cge, int total) {
     const int taps = g.khp * g.kwp;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int o = (int)(t % g.Ogp);
-        long long r = t / g.Ogp;
-        const int tap = (int)(r % taps);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int o = t % g.Ogp;
+        int r = t / g.Ogp;
+        const int tap = r % taps;
         r /= taps;
-        const int cc = (int)(r % Cge);
-        const int grp = (int)(r / Cge);
+        const int cc = r % Cge;
+        const int grp = r / Cge;
         float v = 0.f;
         if (o < g.Og) {
             const int ip = tap / g.kwp, jp = tap % g.kwp;
@@ -166,8 +218,9 @@ __global__ void repack_w_dgrad_kernel(const void* __restrict__ w, int w_bf16, vo
 
 cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, int Cge,
                            cudaStream_t s) {
-    const long long total = (long long)g.G * Cge * g.khp * g.kwp * g.Ogp;
+    const int total = g.G * Cge * g.khp * g.kwp * g.Ogp;
     repack_w_dgrad_kernel<<<blocks_for(total, 256), 256, 0, s>>>(w, w_bf16, dst, dst_esz, g, Cge, total);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -177,16 +230,15 @@ cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, co
 // packed (tap, cc) back to (c, i, j) of the original filter.
 __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dW, float beta, WGeom g,
                                     int m_tiles, int n_tiles, int splits, int BN, int chunk, int cblocks,
-                                    int chunks_per_tile, long long total) {
+                                    int chunks_per_tile, int total) {
     const int nq = g.khp * g.kwp * cblocks;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int rr = (int)(t % chunk);
-        long long r = t / chunk;
-        const int q = (int)(r % nq);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int rr = t % chunk;
+        int r = t / chunk;
+        const int q = r % nq;
         r /= nq;
-        const int o = (int)(r % g.Og);
-        const int grp = (int)(r / g.Og);
+        const int o = r % g.Og;
+        const int grp = r / g.Og;
         const int tap = q / cblocks;
         const int cc = (q % cblocks) * chunk + rr;
         if (cc >= g.Cg * g.sh * g.sw) continue;
@@ -207,9 +259,10 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __
 
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
                          int splits, int BN, int chunk, int cblocks, cudaStream_t s) {
-    const long long total = (long long)g.G * g.Og * g.khp * g.kwp * cblocks * chunk;
+    const int total = g.G * g.Og * g.khp * g.kwp * cblocks * chunk;
     wgrad_reduce_kernel<<<blocks_for(total, 256), 256, 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
                                                                chunk, cblocks, 128 / chunk, total);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -230,6 +283,62 @@ cudaError_t convert_pad_2d(const void* src, int src_bf16, long long ld_src, void
     if (total == 0) return cudaSuccess;
     convert_pad_kernel<<<blocks_for(total, 256), 256, 0, s>>>(src, src_bf16, ld_src, dst, dst_esz, ld_dst, cols,
                                                                total);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// NHWC (N,H,W,C) -> NCHW-flattened rows (N, C*H*W) with dtype conversion and padded row length:
+// used to stage an NHWC inner-product input in the (c,h,w) flatten order of S:130.
+__global__ void nhwc_to_rows_kernel(const void* __restrict__ src, int src_bf16, void* __restrict__ dst, int esz,
+                                    int C, int HW, long long ld, long long total) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long k = t % ld, n = t / ld;
+        float v = 0.f;
+        if (k < (long long)C * HW) {
+            const int c = (int)(k / HW), p = (int)(k % HW);
+            v = ld_any(src, (n * HW + p) * C + c, src_bf16);
+        }
+        st_elem(dst, t, esz, v);
+    }
+}
+
+cudaError_t nhwc_to_rows(const void* src, int src_bf16, void* dst, int dst_esz, int N, int C, int HW, long long ld,
+                         cudaStream_t s) {
+    const long long total = (long long)N * ld;
+    nhwc_to_rows_kernel<<<blocks_for(total, 256), 256, 0, s>>>(src, src_bf16, dst, dst_esz, C, HW, ld, total);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// rows (N, C*H*W) fp32 -> blob of layout lx (for an NHWC inner-product data gradient), with beta.
+__global__ void rows_to_blob_kernel(const float* __restrict__ src, long long ld, void* __restrict__ dst, int dbf16,
+                                    int C, int HW, float beta, long long total) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        // dst is NHWC: t = (n*HW + p)*C + c
+        const int c = (int)(t % C);
+        const long long r = t / C;
+        const int p = (int)(r % HW);
+        const long long n = r / HW;
+        float v = src[n * ld + (long long)c * HW + p];
+        if (dbf16) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dst) + t;
+            if (beta != 0.f) v += beta * __bfloat162float(*o);
+            *o = __float2bfloat16_rn(v);
+        } else {
+            float* o = reinterpret_cast<float*>(dst) + t;
+            if (beta != 0.f) v += beta * *o;
+            *o = v;
+        }
+    }
+}
+
+cudaError_t rows_to_nhwc(const float* src, long long ld, void* dst, int dst_bf16, int N, int C, int HW, float beta,
+                         cudaStream_t s) {
+    const long long total = (long long)N * C * HW;
+    rows_to_blob_kernel<<<blocks_for(total, 256), 256, 0, s>>>(src, ld, dst, dst_bf16, C, HW, beta, total);
+    note_launch();
     return cudaGetLastError();
 }
 

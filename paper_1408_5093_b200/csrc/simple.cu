@@ -3,39 +3,52 @@
 // LRN), softmax-with-loss, bias gradient and the SGD update.
 // Formulas: conv S:145/S:154, pool S:163/S:172 (+R5..R8), LRN S:217/S:226 (R9), ReLU S:199/S:208,
 // softmax loss S:253/S:262, SGD S:523 (R18).
+//
+// Every activation kernel is layout-generic: element (n,c,h,w) lives at n*sn + c*sc + h*sh + w*sw
+// (L4), and threads walk the OUTPUT in its memory order so warps read/write consecutive addresses
+// in either NCHW or NHWC.  Index math is 32-bit (blobs < 2^31 elements, checked by the ABI).
 #include "internal.h"
 
 #include <cuda_bf16.h>
 
 namespace cb {
 
-__device__ __forceinline__ float ldv(const void* p, long long i, int bf16) {
+__device__ __forceinline__ float ldv(const void* p, int i, int bf16) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
 }
-__device__ __forceinline__ void stv(void* p, long long i, int bf16, float v) {
+__device__ __forceinline__ void stv(void* p, int i, int bf16, float v) {
     if (bf16) reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
     else reinterpret_cast<float*>(p)[i] = v;
 }
 static inline unsigned nblk(long long n, int t) {
     long long b = (n + t - 1) / t;
-    if (b > 148LL * 64) b = 148LL * 64;
+    if (b > 148LL * 32) b = 148LL * 32;
     return (unsigned)(b < 1 ? 1 : b);
 }
 #define GRID_STRIDE(t, total) \
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (total); t += (long long)gridDim.x * blockDim.x)
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < (total); t += gridDim.x * blockDim.x)
+
+// decode a linear index t of a (N,C,H,W) tensor stored with layout `nhwc` into (n,c,h,w)
+__device__ __forceinline__ void decode(int t, int C, int H, int W, bool nhwc, int& n, int& c, int& h, int& w) {
+    if (nhwc) {
+        c = t % C; t /= C;
+        w = t % W; t /= W;
+        h = t % H; n = t / H;
+    } else {
+        w = t % W; t /= W;
+        h = t % H; t /= H;
+        c = t % C; n = t / C;
+    }
+}
 
 // ================================================================ FP32 reference convolution
-__global__ void conv_fwd_fp32_kernel(const void* __restrict__ x, int xb, const void* __restrict__ w, int wb,
-                                     const float* __restrict__ b, void* __restrict__ y, int yb, int relu, ConvGeom g,
-                                     long long total) {
+__global__ void conv_fwd_fp32_kernel(const void* __restrict__ x, int xb, L4 lx, const void* __restrict__ w, int wb,
+                                     const float* __restrict__ b, void* __restrict__ y, int yb, L4 ly, int ynhwc,
+                                     int relu, ConvGeom g, int total) {
     const int Cg = g.C / g.G, Og = g.O / g.G;
     GRID_STRIDE(t, total) {
-        const int ox = (int)(t % g.OW);
-        long long r = t / g.OW;
-        const int oy = (int)(r % g.OH);
-        r /= g.OH;
-        const int o = (int)(r % g.O);
-        const int n = (int)(r / g.O);
+        int n, o, oy, ox;
+        decode(t, g.O, g.OH, g.OW, ynhwc, n, o, oy, ox);
         const int cb = (o / Og) * Cg;
         float acc = 0.f;
         for (int c = 0; c < Cg; c++)
@@ -45,8 +58,8 @@ __global__ void conv_fwd_fp32_kernel(const void* __restrict__ x, int xb, const v
                 for (int j = 0; j < g.kw; j++) {
                     const int ww = ox * g.sw - g.pw + j;
                     if (ww < 0 || ww >= g.W) continue;
-                    acc = fmaf(ldv(w, (((long long)o * Cg + c) * g.kh + i) * g.kw + j, wb),
-                               ldv(x, (((long long)n * g.C + cb + c) * g.H + h) * g.W + ww, xb), acc);
+                    acc = fmaf(ldv(w, ((o * Cg + c) * g.kh + i) * g.kw + j, wb),
+                               ldv(x, n * lx.sn + (cb + c) * lx.sc + h * lx.sh + ww * lx.sw, xb), acc);
                 }
             }
         if (b) acc += b[o];
@@ -55,24 +68,22 @@ __global__ void conv_fwd_fp32_kernel(const void* __restrict__ x, int xb, const v
     }
 }
 
-cudaError_t fp32_conv_fwd(const void* x, int x_bf16, const void* w, int w_bf16, const float* b, void* y, int y_bf16,
-                          int relu, const ConvGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.O * g.OH * g.OW;
-    conv_fwd_fp32_kernel<<<nblk(total, 256), 256, 0, s>>>(x, x_bf16, w, w_bf16, b, y, y_bf16, relu, g, total);
+cudaError_t fp32_conv_fwd(const void* x, int x_bf16, L4 lx, const void* w, int w_bf16, const float* b, void* y,
+                          int y_bf16, L4 ly, int ynhwc, int relu, const ConvGeom& g, cudaStream_t s) {
+    const int total = g.N * g.O * g.OH * g.OW;
+    conv_fwd_fp32_kernel<<<nblk(total, 256), 256, 0, s>>>(x, x_bf16, lx, w, w_bf16, b, y, y_bf16, ly, ynhwc, relu, g,
+                                                           total);
+    note_launch();
     return cudaGetLastError();
 }
 
 // gather form of the data gradient: dX[n,c,h,w] = sum_{o in grp(c), i, j : y=(h+ph-i)/sh, x=(w+pw-j)/sw integral}
-__global__ void conv_dgrad_fp32_kernel(const void* __restrict__ dy, int dyb, const void* __restrict__ w, int wb,
-                                       void* __restrict__ dx, int dxb, float beta, ConvGeom g, long long total) {
+__global__ void conv_dgrad_fp32_kernel(const void* __restrict__ dy, int dyb, L4 ly, const void* __restrict__ w, int wb,
+                                       void* __restrict__ dx, int dxb, int xnhwc, float beta, ConvGeom g, int total) {
     const int Cg = g.C / g.G, Og = g.O / g.G;
     GRID_STRIDE(t, total) {
-        const int ww = (int)(t % g.W);
-        long long r = t / g.W;
-        const int h = (int)(r % g.H);
-        r /= g.H;
-        const int c = (int)(r % g.C);
-        const int n = (int)(r / g.C);
+        int n, c, h, ww;
+        decode(t, g.C, g.H, g.W, xnhwc, n, c, h, ww);
         const int grp = c / Cg, cl = c % Cg;
         float acc = 0.f;
         for (int o = grp * Og; o < (grp + 1) * Og; o++)
@@ -86,8 +97,8 @@ __global__ void conv_dgrad_fp32_kernel(const void* __restrict__ dy, int dyb, con
                     if (xx < 0 || xx % g.sw) continue;
                     const int ox = xx / g.sw;
                     if (ox >= g.OW) continue;
-                    acc = fmaf(ldv(w, (((long long)o * Cg + cl) * g.kh + i) * g.kw + j, wb),
-                               ldv(dy, (((long long)n * g.O + o) * g.OH + oy) * g.OW + ox, dyb), acc);
+                    acc = fmaf(ldv(w, ((o * Cg + cl) * g.kh + i) * g.kw + j, wb),
+                               ldv(dy, n * ly.sn + o * ly.sc + oy * ly.sh + ox * ly.sw, dyb), acc);
                 }
             }
         if (beta != 0.f) acc += beta * ldv(dx, t, dxb);
@@ -95,37 +106,39 @@ __global__ void conv_dgrad_fp32_kernel(const void* __restrict__ dy, int dyb, con
     }
 }
 
-cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, const void* w, int w_bf16, void* dx, int dx_bf16,
-                            float beta, const ConvGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.C * g.H * g.W;
-    conv_dgrad_fp32_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, dy_bf16, w, w_bf16, dx, dx_bf16, beta, g, total);
+cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, L4 ly, const void* w, int w_bf16, void* dx, int dx_bf16,
+                            int xnhwc, float beta, const ConvGeom& g, cudaStream_t s) {
+    const int total = g.N * g.C * g.H * g.W;
+    conv_dgrad_fp32_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, dy_bf16, ly, w, w_bf16, dx, dx_bf16, xnhwc, beta, g,
+                                                             total);
+    note_launch();
     return cudaGetLastError();
 }
 
 // Block per weight element; each thread sums a fixed strided subset of the (n, y, x) range, then a
 // fixed-shape tree reduction -> deterministic, blocked FP32 summation (reading R13).
-__global__ void conv_wgrad_fp32_kernel(const void* __restrict__ x, int xb, const void* __restrict__ dy, int dyb,
-                                       float* __restrict__ dw, float beta, ConvGeom g) {
+__global__ void conv_wgrad_fp32_kernel(const void* __restrict__ x, int xb, L4 lx, const void* __restrict__ dy, int dyb,
+                                       L4 ly, float* __restrict__ dw, float beta, ConvGeom g) {
     __shared__ float red[256];
     const int Cg = g.C / g.G, Og = g.O / g.G;
-    const long long widx = blockIdx.x;
-    const int j = (int)(widx % g.kw);
-    long long r = widx / g.kw;
-    const int i = (int)(r % g.kh);
+    const int widx = blockIdx.x;
+    const int j = widx % g.kw;
+    int r = widx / g.kw;
+    const int i = r % g.kh;
     r /= g.kh;
-    const int c = (int)(r % Cg);
-    const int o = (int)(r / Cg);
+    const int c = r % Cg;
+    const int o = r / Cg;
     const int cfull = (o / Og) * Cg + c;
-    const long long P = (long long)g.OH * g.OW, tot = (long long)g.N * P;
+    const int P = g.OH * g.OW, tot = g.N * P;
     float acc = 0.f;
-    for (long long q = threadIdx.x; q < tot; q += blockDim.x) {
-        const int n = (int)(q / P);
-        const int p = (int)(q % P);
-        const int oy = p / g.OW, ox = p % g.OW;
+    for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+        const int n = q / P;
+        const int p = q - n * P;
+        const int oy = p / g.OW, ox = p - oy * g.OW;
         const int h = oy * g.sh - g.ph + i, ww = ox * g.sw - g.pw + j;
         if (h < 0 || h >= g.H || ww < 0 || ww >= g.W) continue;
-        acc = fmaf(ldv(dy, ((long long)n * g.O + o) * P + p, dyb),
-                   ldv(x, (((long long)n * g.C + cfull) * g.H + h) * g.W + ww, xb), acc);
+        acc = fmaf(ldv(dy, n * ly.sn + o * ly.sc + oy * ly.sh + ox * ly.sw, dyb),
+                   ldv(x, n * lx.sn + cfull * lx.sc + h * lx.sh + ww * lx.sw, xb), acc);
     }
     red[threadIdx.x] = acc;
     __syncthreads();
@@ -136,22 +149,46 @@ __global__ void conv_wgrad_fp32_kernel(const void* __restrict__ x, int xb, const
     if (threadIdx.x == 0) dw[widx] = (beta != 0.f ? beta * dw[widx] : 0.f) + red[0];
 }
 
-cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, const void* dy, int dy_bf16, float* dw, float beta,
-                            const ConvGeom& g, cudaStream_t s) {
-    const long long nw = (long long)g.O * (g.C / g.G) * g.kh * g.kw;
-    conv_wgrad_fp32_kernel<<<(unsigned)nw, 256, 0, s>>>(x, x_bf16, dy, dy_bf16, dw, beta, g);
+cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, L4 lx, const void* dy, int dy_bf16, L4 ly, float* dw,
+                            float beta, const ConvGeom& g, cudaStream_t s) {
+    const int nw = g.O * (g.C / g.G) * g.kh * g.kw;
+    conv_wgrad_fp32_kernel<<<(unsigned)nw, 256, 0, s>>>(x, x_bf16, lx, dy, dy_bf16, ly, dw, beta, g);
+    note_launch();
     return cudaGetLastError();
 }
 
-// db[o] = beta*db + sum_{n,p} dY[n,o,p]; block per o, fixed-order strided partials + tree.
-__global__ void bias_grad_kernel(const void* __restrict__ dy, int dyb, float* __restrict__ db, float beta, int N,
-                                 int O, long long P) {
-    __shared__ float red[256];
-    const int o = blockIdx.x;
+// ================================================================ bias gradient (deterministic, 2 stages)
+// db[o] = beta*db + sum_{n,p} dY[n,o,p].  Stage 1: partial[s][o] over a fixed pixel range s.
+//   NHWC (channels contiguous): lane -> channel, 8 warps stride over the pixels of the range.
+//   NCHW (pixels contiguous):   block = (range, channel), threads stride over the range.
+// Stage 2: sum of the partials in ascending s.
+constexpr int BG_SPLITS_MAX = 256;
+
+__global__ void bias_partial_nhwc(const void* __restrict__ dy, int dyb, int O, int M, int R, float* __restrict__ part) {
+    __shared__ float red[8][33];
+    const int s = blockIdx.x, c = blockIdx.y * 32 + (threadIdx.x & 31), wp = threadIdx.x >> 5;
     float acc = 0.f;
-    const long long tot = (long long)N * P;
-    for (long long q = threadIdx.x; q < tot; q += blockDim.x) {
-        const long long n = q / P, p = q % P;
+    if (c < O) {
+        const int m1 = min(M, (s + 1) * R);
+        for (int m = s * R + wp; m < m1; m += 8) acc += ldv(dy, m * O + c, dyb);
+    }
+    red[wp][threadIdx.x & 31] = acc;
+    __syncthreads();
+    if (wp == 0 && c < O) {
+        float t = 0.f;
+        for (int k = 0; k < 8; k++) t += red[k][threadIdx.x];
+        part[s * O + c] = t;
+    }
+}
+
+__global__ void bias_partial_nchw(const void* __restrict__ dy, int dyb, int O, int P, int N, int R,
+                                  float* __restrict__ part) {
+    __shared__ float red[256];
+    const int s = blockIdx.x, o = blockIdx.y;
+    const int M = N * P, m1 = min(M, (s + 1) * R);
+    float acc = 0.f;
+    for (int m = s * R + threadIdx.x; m < m1; m += blockDim.x) {
+        const int n = m / P, p = m - n * P;
         acc += ldv(dy, (n * O + o) * P + p, dyb);
     }
     red[threadIdx.x] = acc;
@@ -160,41 +197,68 @@ __global__ void bias_grad_kernel(const void* __restrict__ dy, int dyb, float* __
         if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
         __syncthreads();
     }
-    if (threadIdx.x == 0) db[o] = (beta != 0.f ? beta * db[o] : 0.f) + red[0];
+    if (threadIdx.x == 0) part[s * O + o] = red[0];
 }
 
-cudaError_t bias_grad(const void* dy, int dy_bf16, float* db, float beta, int N, int O, long long P, cudaStream_t s) {
-    bias_grad_kernel<<<O, 256, 0, s>>>(dy, dy_bf16, db, beta, N, O, P);
+__global__ void bias_final(const float* __restrict__ part, int S, int O, float* __restrict__ db, float beta) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= O) return;
+    float t = 0.f;
+    for (int s = 0; s < S; s++) t += part[s * O + o];
+    db[o] = (beta != 0.f ? beta * db[o] : 0.f) + t;
+}
+
+int bias_grad_splits(int N, int O, int P) {
+    const long long M = (long long)N * P;
+    int S = (int)((M + 2047) / 2048);
+    if (S > BG_SPLITS_MAX) S = BG_SPLITS_MAX;
+    return S < 1 ? 1 : S;
+}
+
+cudaError_t bias_grad(const void* dy, int dy_bf16, int nhwc, float* db, float beta, int N, int O, int P, float* part,
+                      cudaStream_t s) {
+    const int M = N * P;
+    const int S = bias_grad_splits(N, O, P);
+    const int R = (M + S - 1) / S;
+    if (nhwc || P == 1) {
+        bias_partial_nhwc<<<dim3(S, (O + 31) / 32), 256, 0, s>>>(dy, dy_bf16, O, M, R, part);
+    } else {
+        bias_partial_nchw<<<dim3(S, O), 256, 0, s>>>(dy, dy_bf16, O, P, N, R, part);
+    }
+    note_launch();
+    bias_final<<<(O + 255) / 256, 256, 0, s>>>(part, S, O, db, beta);
+    note_launch();
     return cudaGetLastError();
 }
 
 // ================================================================ im2col / col2im (bit-exact test entry points)
-__global__ void im2col_kernel(const float* __restrict__ x, int n, ConvGeom g, float* __restrict__ col, long long total) {
-    const long long P = (long long)g.OH * g.OW;
+__global__ void im2col_kernel(const float* __restrict__ x, int n, ConvGeom g, float* __restrict__ col, int total) {
+    const int P = g.OH * g.OW;
     GRID_STRIDE(t, total) {
-        const long long p = t % P, row = t / P;
-        const int j = (int)(row % g.kw);
-        const int i = (int)((row / g.kw) % g.kh);
-        const int c = (int)(row / ((long long)g.kw * g.kh));
-        const int oy = (int)(p / g.OW), ox = (int)(p % g.OW);
+        const int p = t % P, row = t / P;
+        const int j = row % g.kw;
+        const int i = (row / g.kw) % g.kh;
+        const int c = row / (g.kw * g.kh);
+        const int oy = p / g.OW, ox = p % g.OW;
         const int h = oy * g.sh - g.ph + i, w = ox * g.sw - g.pw + j;
-        col[t] = (h >= 0 && h < g.H && w >= 0 && w < g.W) ? x[(((long long)n * g.C + c) * g.H + h) * g.W + w] : 0.f;
+        col[t] = (h >= 0 && h < g.H && w >= 0 && w < g.W) ? x[((n * g.C + c) * g.H + h) * g.W + w] : 0.f;
     }
 }
 
 cudaError_t im2col_k(const float* x, int n, const ConvGeom& g, float* col, cudaStream_t s) {
-    const long long total = (long long)g.C * g.kh * g.kw * g.OH * g.OW;
+    const int total = g.C * g.kh * g.kw * g.OH * g.OW;
     im2col_kernel<<<nblk(total, 256), 256, 0, s>>>(x, n, g, col, total);
+    note_launch();
     return cudaGetLastError();
 }
 
 // gather: for each (c,h,w) sum col over (y asc, x asc) -- the FP32 order fixed by the reading.
-__global__ void col2im_kernel(const float* __restrict__ col, int n, ConvGeom g, float* __restrict__ dx, long long total) {
-    const long long P = (long long)g.OH * g.OW;
+__global__ void col2im_kernel(const float* __restrict__ col, int n, ConvGeom g, float* __restrict__ dx, int total) {
+    const int P = g.OH * g.OW;
     GRID_STRIDE(t, total) {
-        const int w = (int)(t % g.W);
-        const int h = (int)((t / g.W) % g.H);
-        const int c = (int)(t / ((long long)g.W * g.H));
+        const int w = t % g.W;
+        const int h = (t / g.W) % g.H;
+        const int c = t / (g.W * g.H);
         float acc = 0.f;
         for (int oy = 0; oy < g.OH; oy++) {
             const int i = h + g.ph - oy * g.sh;
@@ -202,22 +266,23 @@ __global__ void col2im_kernel(const float* __restrict__ col, int n, ConvGeom g, 
             for (int ox = 0; ox < g.OW; ox++) {
                 const int j = w + g.pw - ox * g.sw;
                 if (j < 0 || j >= g.kw) continue;
-                acc += col[(((long long)c * g.kh + i) * g.kw + j) * P + (long long)oy * g.OW + ox];
+                acc += col[((c * g.kh + i) * g.kw + j) * P + oy * g.OW + ox];
             }
         }
-        dx[(long long)n * g.C * g.H * g.W + t] = acc;
+        dx[n * g.C * g.H * g.W + t] = acc;
     }
 }
 
 cudaError_t col2im_k(const float* col, int n, const ConvGeom& g, float* dx, cudaStream_t s) {
-    const long long total = (long long)g.C * g.H * g.W;
+    const int total = g.C * g.H * g.W;
     col2im_kernel<<<nblk(total, 256), 256, 0, s>>>(col, n, g, dx, total);
+    note_launch();
     return cudaGetLastError();
 }
 
 // ================================================================ ReLU (vectorised, in-place safe)
-__global__ void relu_fwd_f32(const float* __restrict__ x, float* y, long long n) {
-    const long long n4 = n / 4;
+__global__ void relu_fwd_f32(const float* __restrict__ x, float* y, int n) {
+    const int n4 = n / 4;
     GRID_STRIDE(t, n4) {
         float4 v = reinterpret_cast<const float4*>(x)[t];
         v.x = v.x > 0.f ? v.x : 0.f; v.y = v.y > 0.f ? v.y : 0.f;
@@ -226,18 +291,17 @@ __global__ void relu_fwd_f32(const float* __restrict__ x, float* y, long long n)
     }
     GRID_STRIDE(t, n - n4 * 4) { const float v = x[n4 * 4 + t]; y[n4 * 4 + t] = v > 0.f ? v : 0.f; }
 }
-__global__ void relu_fwd_bf16(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* y, long long n) {
-    const long long n8 = n / 8;
-    const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
+__device__ __forceinline__ __nv_bfloat162 relu2(__nv_bfloat162 h) {
+    const float2 f = __bfloat1622float2(h);
+    return __floats2bfloat162_rn(f.x > 0.f ? f.x : 0.f, f.y > 0.f ? f.y : 0.f);
+}
+__global__ void relu_fwd_bf16(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* y, int n) {
+    const int n8 = n / 8;
     GRID_STRIDE(t, n8) {
         uint4 v = reinterpret_cast<const uint4*>(x)[t];
         __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-            float2 f = __bfloat1622float2(h[e]);
-            h[e] = __floats2bfloat162_rn(f.x > 0.f ? f.x : 0.f, f.y > 0.f ? f.y : 0.f);
-        }
-        (void)z;
+        for (int e = 0; e < 4; e++) h[e] = relu2(h[e]);
         reinterpret_cast<uint4*>(y)[t] = v;
     }
     GRID_STRIDE(t, n - n8 * 8) {
@@ -246,20 +310,32 @@ __global__ void relu_fwd_bf16(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
     }
 }
 
-cudaError_t relu_fwd(const void* x, void* y, int bf16, long long count, cudaStream_t s) {
-    const int vec = bf16 ? 8 : 4;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
-    if (bf16) {
-        if (!aligned) return cudaErrorMisalignedAddress;
-        relu_fwd_bf16<<<nblk(count / vec + 1, 256), 256, 0, s>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)y, count);
-    } else {
-        if (!aligned) return cudaErrorMisalignedAddress;
-        relu_fwd_f32<<<nblk(count / vec + 1, 256), 256, 0, s>>>((const float*)x, (float*)y, count);
-    }
+cudaError_t relu_fwd(const void* x, void* y, int bf16, int count, cudaStream_t s) {
+    if (bf16) relu_fwd_bf16<<<nblk(count / 8 + 1, 256), 256, 0, s>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)y, count);
+    else relu_fwd_f32<<<nblk(count / 4 + 1, 256), 256, 0, s>>>((const float*)x, (float*)y, count);
+    note_launch();
     return cudaGetLastError();
 }
 
-__global__ void relu_bwd_kernel(const void* __restrict__ x, const void* dy, void* dx, int xb, int db, long long n) {
+// dx = x > 0 ? dy : 0 -- vectorised for bf16 x and bf16 dy (8 per thread), scalar otherwise.
+__global__ void relu_bwd_bf16(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* dy, __nv_bfloat16* dx, int n) {
+    const int n8 = n / 8;
+    GRID_STRIDE(t, n8) {
+        uint4 xv = reinterpret_cast<const uint4*>(x)[t];
+        uint4 gv = reinterpret_cast<const uint4*>(dy)[t];
+        const __nv_bfloat16* xh = reinterpret_cast<const __nv_bfloat16*>(&xv);
+        __nv_bfloat16* gh = reinterpret_cast<__nv_bfloat16*>(&gv);
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+            if (!(__bfloat162float(xh[e]) > 0.f)) gh[e] = __float2bfloat16_rn(0.f);
+        reinterpret_cast<uint4*>(dx)[t] = gv;
+    }
+    GRID_STRIDE(t, n - n8 * 8) {
+        const int i = n8 * 8 + t;
+        dx[i] = __bfloat162float(x[i]) > 0.f ? dy[i] : __float2bfloat16_rn(0.f);
+    }
+}
+__global__ void relu_bwd_kernel(const void* __restrict__ x, const void* dy, void* dx, int xb, int db, int n) {
     GRID_STRIDE(t, n) {
         const float xv = ldv(x, t, xb);
         const float g = ldv(dy, t, db);
@@ -267,29 +343,34 @@ __global__ void relu_bwd_kernel(const void* __restrict__ x, const void* dy, void
     }
 }
 
-cudaError_t relu_bwd(const void* x, const void* dy, void* dx, int x_bf16, int d_bf16, long long count, cudaStream_t s) {
-    relu_bwd_kernel<<<nblk(count, 256), 256, 0, s>>>(x, dy, dx, x_bf16, d_bf16, count);
+cudaError_t relu_bwd(const void* x, const void* dy, void* dx, int x_bf16, int d_bf16, int count, cudaStream_t s) {
+    const bool al = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx)) & 15) == 0;
+    if (x_bf16 && d_bf16 && al)
+        relu_bwd_bf16<<<nblk(count / 8 + 1, 256), 256, 0, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy,
+                                                               (__nv_bfloat16*)dx, count);
+    else
+        relu_bwd_kernel<<<nblk(count, 256), 256, 0, s>>>(x, dy, dx, x_bf16, d_bf16, count);
+    note_launch();
     return cudaGetLastError();
 }
 
 // ================================================================ pooling
-__global__ void maxpool_fwd_kernel(const void* __restrict__ x, void* __restrict__ y, int32_t* __restrict__ mask,
-                                   int bf16, PoolGeom g, long long total) {
+// Forward: thread per output element in the top's memory order.
+__global__ void maxpool_fwd_kernel(const void* __restrict__ x, L4 lx, void* __restrict__ y, int ynhwc,
+                                   int32_t* __restrict__ mask, int bf16, PoolGeom g, int total) {
     GRID_STRIDE(t, total) {
-        const int px = (int)(t % g.OW);
-        long long r = t / g.OW;
-        const int py = (int)(r % g.OH);
-        const long long plane = r / g.OH;
+        int n, c, py, px;
+        decode(t, g.C, g.OH, g.OW, ynhwc, n, c, py, px);
         int hs = py * g.sh - g.ph, ws = px * g.sw - g.pw;
         const int he = min(hs + g.kh, g.H), we = min(ws + g.kw, g.W);
         hs = max(hs, 0);
         ws = max(ws, 0);
-        const long long base = plane * g.H * g.W;
+        const int base = n * lx.sn + c * lx.sc;
         float best = 0.f;
         int arg = -1;
         for (int h = hs; h < he; h++)
             for (int w = ws; w < we; w++) {
-                const float v = ldv(x, base + (long long)h * g.W + w, bf16);
+                const float v = ldv(x, base + h * lx.sh + w * lx.sw, bf16);
                 if (arg < 0 || v > best) { best = v; arg = h * g.W + w; }
             }
         stv(y, t, bf16, best);
@@ -297,37 +378,141 @@ __global__ void maxpool_fwd_kernel(const void* __restrict__ x, void* __restrict_
     }
 }
 
-cudaError_t maxpool_fwd(const void* x, void* y, int32_t* mask, int bf16, const PoolGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.C * g.OH * g.OW;
-    maxpool_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, y, mask, bf16, g, total);
-    return cudaGetLastError();
+// ---- channels-last BF16 fast paths: one thread = one pixel x 8 consecutive channels (16-byte
+// vectors), so every window access is a coalesced 16-byte load and index math is per pixel.
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const float2 t = __bfloat1622float2(h[e]);
+        f[2 * e] = t.x;
+        f[2 * e + 1] = t.y;
+    }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; e++) h[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+    return u;
 }
 
-// gather per input element over the windows that may contain it, ascending (py, px) -- R8, bit-exact.
-__global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const int32_t* __restrict__ mask, void* __restrict__ dx,
-                                   int bf16, PoolGeom g, long long total) {
+__global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                  int32_t* __restrict__ mask, PoolGeom g, int total) {
+    const int cv = g.C / 8;
     GRID_STRIDE(t, total) {
-        const int w = (int)(t % g.W);
-        long long r = t / g.W;
-        const int h = (int)(r % g.H);
-        const long long plane = r / g.H;
+        const int c0 = (t % cv) * 8;
+        int r = t / cv;
+        const int px = r % g.OW; r /= g.OW;
+        const int py = r % g.OH;
+        const int n = r / g.OH;
+        int hs = py * g.sh - g.ph, ws = px * g.sw - g.pw;
+        const int he = min(hs + g.kh, g.H), we = min(ws + g.kw, g.W);
+        hs = max(hs, 0);
+        ws = max(ws, 0);
+        float best[8];
+        int arg[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) { best[e] = 0.f; arg[e] = -1; }
+        for (int h = hs; h < he; h++)
+            for (int w = ws; w < we; w++) {
+                float v[8];
+                unpack8(*reinterpret_cast<const uint4*>(x + (((long long)n * g.H + h) * g.W + w) * g.C + c0), v);
+                const int me = h * g.W + w;
+#pragma unroll
+                for (int e = 0; e < 8; e++)
+                    if (arg[e] < 0 || v[e] > best[e]) { best[e] = v[e]; arg[e] = me; }
+            }
+        const long long o = (long long)t * 8;
+        *reinterpret_cast<uint4*>(y + o) = pack8(best);
+        if (mask) {
+            int4* m = reinterpret_cast<int4*>(mask + o);
+            m[0] = make_int4(arg[0], arg[1], arg[2], arg[3]);
+            m[1] = make_int4(arg[4], arg[5], arg[6], arg[7]);
+        }
+    }
+}
+
+__global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const int32_t* __restrict__ mask,
+                                  __nv_bfloat16* __restrict__ dx, PoolGeom g, int total) {
+    const int cv = g.C / 8;
+    GRID_STRIDE(t, total) {
+        const int c0 = (t % cv) * 8;
+        int r = t / cv;
+        const int w = r % g.W; r /= g.W;
+        const int h = r % g.H;
+        const int n = r / g.H;
         const int py0 = max(0, (h + g.ph - g.kh + g.sh) / g.sh), py1 = min(g.OH - 1, (h + g.ph) / g.sh);
         const int px0 = max(0, (w + g.pw - g.kw + g.sw) / g.sw), px1 = min(g.OW - 1, (w + g.pw) / g.sw);
         const int me = h * g.W + w;
-        const long long base = plane * g.OH * g.OW;
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) acc[e] = 0.f;
+        for (int py = py0; py <= py1; py++)
+            for (int px = px0; px <= px1; px++) {
+                const long long q = (((long long)n * g.OH + py) * g.OW + px) * g.C + c0;
+                const int4 m0 = *reinterpret_cast<const int4*>(mask + q);
+                const int4 m1 = *reinterpret_cast<const int4*>(mask + q + 4);
+                const int mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+                float v[8];
+                unpack8(*reinterpret_cast<const uint4*>(dy + q), v);
+#pragma unroll
+                for (int e = 0; e < 8; e++)
+                    if (mm[e] == me) acc[e] += v[e];
+            }
+        *reinterpret_cast<uint4*>(dx + (long long)t * 8) = pack8(acc);
+    }
+}
+
+static inline bool nhwc8_ok(const void* a, const void* b, int C) {
+    return (C % 8) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+
+cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask, int bf16, const PoolGeom& g,
+                        cudaStream_t s) {
+    const int total = g.N * g.C * g.OH * g.OW;
+    const bool xnhwc = lx.sc == 1 && g.C > 1;
+    if (bf16 && xnhwc && ynhwc && nhwc8_ok(x, y, g.C) && ((reinterpret_cast<uintptr_t>(mask) & 15) == 0)) {
+        maxpool_fwd_nhwc8<<<nblk(total / 8, 256), 256, 0, s>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)y, mask, g,
+                                                               total / 8);
+    } else {
+        maxpool_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, lx, y, ynhwc, mask, bf16, g, total);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+// Backward: gather per input element (in the bottom_diff's memory order) over the windows that may
+// contain it, ascending (py, px) -- R8, bit-exact.  ly = layout strides of top_diff and mask.
+__global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const int32_t* __restrict__ mask, L4 ly,
+                                   void* __restrict__ dx, int xnhwc, int bf16, PoolGeom g, int total) {
+    GRID_STRIDE(t, total) {
+        int n, c, h, w;
+        decode(t, g.C, g.H, g.W, xnhwc, n, c, h, w);
+        const int py0 = max(0, (h + g.ph - g.kh + g.sh) / g.sh), py1 = min(g.OH - 1, (h + g.ph) / g.sh);
+        const int px0 = max(0, (w + g.pw - g.kw + g.sw) / g.sw), px1 = min(g.OW - 1, (w + g.pw) / g.sw);
+        const int me = h * g.W + w;
+        const int base = n * ly.sn + c * ly.sc;
         float acc = 0.f;
         for (int py = py0; py <= py1; py++)
             for (int px = px0; px <= px1; px++) {
-                const long long q = base + (long long)py * g.OW + px;
+                const int q = base + py * ly.sh + px * ly.sw;
                 if (mask[q] == me) acc += ldv(dy, q, bf16);
             }
         stv(dx, t, bf16, acc);
     }
 }
 
-cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, void* dx, int bf16, const PoolGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.C * g.H * g.W;
-    maxpool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, mask, dx, bf16, g, total);
+cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g,
+                        cudaStream_t s) {
+    const int total = g.N * g.C * g.H * g.W;
+    const bool ynhwc = ly.sc == 1 && g.C > 1;
+    if (bf16 && xnhwc && ynhwc && nhwc8_ok(dy, dx, g.C) && ((reinterpret_cast<uintptr_t>(mask) & 15) == 0))
+        maxpool_bwd_nhwc8<<<nblk(total / 8, 256), 256, 0, s>>>((const __nv_bfloat16*)dy, mask, (__nv_bfloat16*)dx, g,
+                                                               total / 8);
+    else
+        maxpool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, mask, ly, dx, xnhwc, bf16, g, total);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -344,103 +529,203 @@ __device__ __forceinline__ void ave_window(int py, int px, const PoolGeom& g, in
     we = min(we, g.W);
 }
 
-__global__ void avepool_fwd_kernel(const void* __restrict__ x, void* __restrict__ y, int bf16, PoolGeom g, long long total) {
+__global__ void avepool_fwd_kernel(const void* __restrict__ x, L4 lx, void* __restrict__ y, int ynhwc, int bf16,
+                                   PoolGeom g, int total) {
     GRID_STRIDE(t, total) {
-        const int px = (int)(t % g.OW);
-        long long r = t / g.OW;
-        const int py = (int)(r % g.OH);
-        const long long plane = r / g.OH;
+        int n, c, py, px;
+        decode(t, g.C, g.OH, g.OW, ynhwc, n, c, py, px);
         int hs, he, ws, we, size;
         ave_window(py, px, g, hs, he, ws, we, size);
+        const int base = n * lx.sn + c * lx.sc;
         float acc = 0.f;
         for (int h = hs; h < he; h++)
-            for (int w = ws; w < we; w++) acc += ldv(x, plane * g.H * g.W + (long long)h * g.W + w, bf16);
+            for (int w = ws; w < we; w++) acc += ldv(x, base + h * lx.sh + w * lx.sw, bf16);
         stv(y, t, bf16, acc / size);
     }
 }
 
-cudaError_t avepool_fwd(const void* x, void* y, int bf16, const PoolGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.C * g.OH * g.OW;
-    avepool_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, y, bf16, g, total);
+cudaError_t avepool_fwd(const void* x, L4 lx, void* y, int ynhwc, int bf16, const PoolGeom& g, cudaStream_t s) {
+    const int total = g.N * g.C * g.OH * g.OW;
+    avepool_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, lx, y, ynhwc, bf16, g, total);
+    note_launch();
     return cudaGetLastError();
 }
 
-__global__ void avepool_bwd_kernel(const void* __restrict__ dy, void* __restrict__ dx, int bf16, PoolGeom g, long long total) {
+__global__ void avepool_bwd_kernel(const void* __restrict__ dy, L4 ly, void* __restrict__ dx, int xnhwc, int bf16,
+                                   PoolGeom g, int total) {
     GRID_STRIDE(t, total) {
-        const int w = (int)(t % g.W);
-        long long r = t / g.W;
-        const int h = (int)(r % g.H);
-        const long long plane = r / g.H;
+        int n, c, h, w;
+        decode(t, g.C, g.H, g.W, xnhwc, n, c, h, w);
         const int py0 = max(0, (h + g.ph - g.kh + g.sh) / g.sh), py1 = min(g.OH - 1, (h + g.ph) / g.sh);
         const int px0 = max(0, (w + g.pw - g.kw + g.sw) / g.sw), px1 = min(g.OW - 1, (w + g.pw) / g.sw);
+        const int base = n * ly.sn + c * ly.sc;
         float acc = 0.f;
         for (int py = py0; py <= py1; py++)
             for (int px = px0; px <= px1; px++) {
                 int hs, he, ws, we, size;
                 ave_window(py, px, g, hs, he, ws, we, size);
-                if (h >= hs && h < he && w >= ws && w < we)
-                    acc += ldv(dy, plane * g.OH * g.OW + (long long)py * g.OW + px, bf16) / size;
+                if (h >= hs && h < he && w >= ws && w < we) acc += ldv(dy, base + py * ly.sh + px * ly.sw, bf16) / size;
             }
         stv(dx, t, bf16, acc);
     }
 }
 
-cudaError_t avepool_bwd(const void* dy, void* dx, int bf16, const PoolGeom& g, cudaStream_t s) {
-    const long long total = (long long)g.N * g.C * g.H * g.W;
-    avepool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, dx, bf16, g, total);
+cudaError_t avepool_bwd(const void* dy, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g, cudaStream_t s) {
+    const int total = g.N * g.C * g.H * g.W;
+    avepool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, ly, dx, xnhwc, bf16, g, total);
+    note_launch();
     return cudaGetLastError();
 }
 
 // ================================================================ LRN across channels
-__device__ __forceinline__ float lrn_scale(const void* x, int bf16, long long base, long long P, int c, int C, int r,
+// All LRN blobs share one layout (checked by the ABI); sc = channel stride.
+__device__ __forceinline__ float lrn_scale(const void* x, int bf16, int base, int sc, int c, int C, int r,
                                            float alpha_n, float k) {
     float s = 0.f;
     const int lo = max(0, c - r), hi = min(C - 1, c + r);
     for (int cc = lo; cc <= hi; cc++) {
-        const float v = ldv(x, base + cc * P, bf16);
+        const float v = ldv(x, base + cc * sc, bf16);
         s = fmaf(v, v, s);
     }
     return k + alpha_n * s;
 }
 
 __global__ void lrn_fwd_kernel(const void* __restrict__ x, void* __restrict__ y, float* __restrict__ scale, int bf16,
-                               int C, long long P, int size, float alpha, float beta, float k, long long total) {
+                               int nhwc, int C, int H, int W, int sc, int size, float alpha, float beta, float k,
+                               int total) {
     const int r = (size - 1) / 2;
     const float an = alpha / size;
     GRID_STRIDE(t, total) {
-        const long long p = t % P;
-        const long long nc = t / P;
-        const int c = (int)(nc % C);
-        const long long base = (nc - c) * P + p;
-        const float S = lrn_scale(x, bf16, base, P, c, C, r, an, k);
+        int n, c, h, w;
+        decode(t, C, H, W, nhwc, n, c, h, w);
+        const int base = t - c * sc;
+        const float S = lrn_scale(x, bf16, base, sc, c, C, r, an, k);
         stv(y, t, bf16, ldv(x, t, bf16) * exp2f(-beta * log2f(S)));
         if (scale) scale[t] = S;
     }
 }
 
-cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int N, int C, long long P, int size, float alpha,
-                    float beta, float k, cudaStream_t s) {
-    const long long total = (long long)N * C * P;
-    lrn_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, y, scale, bf16, C, P, size, alpha, beta, k, total);
+// channels-last BF16 LRN: a thread owns 8 channels of one pixel and keeps the neighbouring 8-channel
+// vectors (c0-8 .. c0+15) in registers; channels outside [0, C) contribute 0 (clipped window).
+__device__ __forceinline__ void load24(const __nv_bfloat16* p, int c0, int C, float (&v)[24]) {
+    float a[8], b[8], c[8];
+    unpack8(*reinterpret_cast<const uint4*>(p + c0), b);
+    if (c0 >= 8) unpack8(*reinterpret_cast<const uint4*>(p + c0 - 8), a);
+    else {
+#pragma unroll
+        for (int e = 0; e < 8; e++) a[e] = 0.f;
+    }
+    if (c0 + 8 < C) unpack8(*reinterpret_cast<const uint4*>(p + c0 + 8), c);
+    else {
+#pragma unroll
+        for (int e = 0; e < 8; e++) c[e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; e++) { v[e] = a[e]; v[8 + e] = b[e]; v[16 + e] = c[e]; }
+}
+
+template <int R>
+__global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                              float* __restrict__ scale, int C, int size, float alpha, float beta, float k, int total) {
+    const int cv = C / 8;
+    const float an = alpha / size;
+    GRID_STRIDE(t, total) {
+        const int c0 = (t % cv) * 8;
+        const long long base = (long long)(t / cv) * C;
+        float xv[24];
+        load24(x + base, c0, C, xv);
+        float out[8], S[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            float s2 = 0.f;
+#pragma unroll
+            for (int j = -R; j <= R; j++) s2 = fmaf(xv[8 + e + j], xv[8 + e + j], s2);
+            S[e] = k + an * s2;
+            out[e] = xv[8 + e] * exp2f(-beta * log2f(S[e]));
+        }
+        *reinterpret_cast<uint4*>(y + base + c0) = pack8(out);
+        if (scale) {
+            float4* sp = reinterpret_cast<float4*>(scale + base + c0);
+            sp[0] = make_float4(S[0], S[1], S[2], S[3]);
+            sp[1] = make_float4(S[4], S[5], S[6], S[7]);
+        }
+    }
+}
+
+template <int R>
+__global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
+                              const __nv_bfloat16* __restrict__ dy, __nv_bfloat16* __restrict__ dx, int C, int size,
+                              float alpha, float beta, float k, int total) {
+    const int cv = C / 8;
+    const float an = alpha / size;
+    GRID_STRIDE(t, total) {
+        const int c0 = (t % cv) * 8;
+        const long long base = (long long)(t / cv) * C;
+        float xv[24], yv[24], gv[24];
+        load24(x + base, c0, C, xv);
+        load24(y + base, c0, C, yv);
+        load24(dy + base, c0, C, gv);
+        float S[24], tv[24];
+#pragma unroll
+        for (int i = 8 - R; i < 16 + R; i++) {
+            float s2 = 0.f;
+#pragma unroll
+            for (int j = -R; j <= R; j++) s2 = fmaf(xv[i + j], xv[i + j], s2);
+            S[i] = k + an * s2;
+            tv[i] = gv[i] * yv[i] / S[i];
+        }
+        float out[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            float acc = 0.f;
+#pragma unroll
+            for (int j = -R; j <= R; j++) acc += tv[8 + e + j];
+            out[e] = gv[8 + e] * exp2f(-beta * log2f(S[8 + e])) - 2.f * an * beta * xv[8 + e] * acc;
+        }
+        *reinterpret_cast<uint4*>(dx + base + c0) = pack8(out);
+    }
+}
+
+cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int nhwc, int N, int C, int H, int W, int size,
+                    float alpha, float beta, float k, cudaStream_t s) {
+    const int total = N * C * H * W;
+    const int sc = nhwc ? 1 : H * W;
+    if (bf16 && nhwc && nhwc8_ok(x, y, C) && ((reinterpret_cast<uintptr_t>(scale) & 15) == 0) && size <= 9) {
+        const int tv = total / 8;
+        const unsigned nb = nblk(tv, 256);
+        auto X = (const __nv_bfloat16*)x;
+        auto Y = (__nv_bfloat16*)y;
+        switch ((size - 1) / 2) {
+            case 0: lrn_fwd_nhwc8<0><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+            case 1: lrn_fwd_nhwc8<1><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+            case 2: lrn_fwd_nhwc8<2><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+            case 3: lrn_fwd_nhwc8<3><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+            default: lrn_fwd_nhwc8<4><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+        }
+        note_launch();
+        return cudaGetLastError();
+    }
+    lrn_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, y, scale, bf16, nhwc, C, H, W, sc, size, alpha, beta, k, total);
+    note_launch();
     return cudaGetLastError();
 }
 
 __global__ void lrn_bwd_kernel(const void* __restrict__ x, const void* __restrict__ y, const void* __restrict__ dy,
-                               const float* __restrict__ scale, void* __restrict__ dx, int bf16, int C, long long P,
-                               int size, float alpha, float beta, float k, long long total) {
+                               const float* __restrict__ scale, void* __restrict__ dx, int bf16, int nhwc, int C, int H,
+                               int W, int sc, int size, float alpha, float beta, float k, int total) {
     const int r = (size - 1) / 2;
     const float an = alpha / size;
     GRID_STRIDE(t, total) {
-        const long long p = t % P;
-        const long long nc = t / P;
-        const int c = (int)(nc % C);
-        const long long base = (nc - c) * P + p;
-        const float Sc = scale ? scale[t] : lrn_scale(x, bf16, base, P, c, C, r, an, k);
+        int n, c, h, w;
+        decode(t, C, H, W, nhwc, n, c, h, w);
+        const int base = t - c * sc;
+        // window sums of x^2 for the 2r+1 neighbours from one pass over 4r+1 channels
+        const float Sc = scale ? scale[t] : lrn_scale(x, bf16, base, sc, c, C, r, an, k);
         float acc = 0.f;
         const int lo = max(0, c - r), hi = min(C - 1, c + r);
         for (int cc = lo; cc <= hi; cc++) {
-            const long long q = base + cc * P;
-            const float S = scale ? scale[q] : lrn_scale(x, bf16, base, P, cc, C, r, an, k);
+            const int q = base + cc * sc;
+            const float S = scale ? scale[q] : lrn_scale(x, bf16, base, sc, cc, C, r, an, k);
             acc += ldv(dy, q, bf16) * ldv(y, q, bf16) / S;
         }
         const float v = ldv(dy, t, bf16) * exp2f(-beta * log2f(Sc)) - 2.f * an * beta * ldv(x, t, bf16) * acc;
@@ -448,10 +733,30 @@ __global__ void lrn_bwd_kernel(const void* __restrict__ x, const void* __restric
     }
 }
 
-cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* scale, void* dx, int bf16, int N, int C,
-                    long long P, int size, float alpha, float beta, float k, cudaStream_t s) {
-    const long long total = (long long)N * C * P;
-    lrn_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, y, dy, scale, dx, bf16, C, P, size, alpha, beta, k, total);
+cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* scale, void* dx, int bf16, int nhwc,
+                    int N, int C, int H, int W, int size, float alpha, float beta, float k, cudaStream_t s) {
+    const int total = N * C * H * W;
+    const int sc = nhwc ? 1 : H * W;
+    if (bf16 && nhwc && nhwc8_ok(x, y, C) && nhwc8_ok(dy, dx, C) && size <= 9) {
+        const int tv = total / 8;
+        const unsigned nb = nblk(tv, 256);
+        auto X = (const __nv_bfloat16*)x;
+        auto Y = (const __nv_bfloat16*)y;
+        auto G = (const __nv_bfloat16*)dy;
+        auto D = (__nv_bfloat16*)dx;
+        switch ((size - 1) / 2) {
+            case 0: lrn_bwd_nhwc8<0><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
+            case 1: lrn_bwd_nhwc8<1><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
+            case 2: lrn_bwd_nhwc8<2><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
+            case 3: lrn_bwd_nhwc8<3><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
+            default: lrn_bwd_nhwc8<4><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
+        }
+        note_launch();
+        return cudaGetLastError();
+    }
+    lrn_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, y, dy, scale, dx, bf16, nhwc, C, H, W, sc, size, alpha, beta, k,
+                                                     total);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -464,7 +769,7 @@ __global__ void softmax_loss_kernel(const void* __restrict__ s, int sb, const in
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float my = 0.f;
     for (int n = warp; n < N; n += 32) {
-        const long long base = (long long)n * K;
+        const int base = n * K;
         float mx = -INFINITY;
         for (int k = lane; k < K; k += 32) mx = fmaxf(mx, ldv(s, base + k, sb));
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -495,16 +800,36 @@ __global__ void softmax_loss_kernel(const void* __restrict__ s, int sb, const in
 cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff, int diff_bf16,
                            int N, int K, cudaStream_t s) {
     softmax_loss_kernel<<<1, 1024, 0, s>>>(scores, bf16, labels, loss, diff, diff_bf16, N, K);
+    note_launch();
     return cudaGetLastError();
 }
 
 // ================================================================ SGD (R18)
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
                            __nv_bfloat16* __restrict__ wb, long long n, float lr, float mom, float decay, float gs) {
-    GRID_STRIDE(t, n) {
+    const long long n4 = n / 4;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n4; t += (long long)gridDim.x * blockDim.x) {
+        float4 wv = reinterpret_cast<const float4*>(w)[t];
+        const float4 gv = reinterpret_cast<const float4*>(g)[t];
+        float4 vv = reinterpret_cast<const float4*>(v)[t];
+        vv.x = mom * vv.x - lr * (gv.x * gs + decay * wv.x);
+        vv.y = mom * vv.y - lr * (gv.y * gs + decay * wv.y);
+        vv.z = mom * vv.z - lr * (gv.z * gs + decay * wv.z);
+        vv.w = mom * vv.w - lr * (gv.w * gs + decay * wv.w);
+        wv.x += vv.x; wv.y += vv.y; wv.z += vv.z; wv.w += vv.w;
+        reinterpret_cast<float4*>(v)[t] = vv;
+        reinterpret_cast<float4*>(w)[t] = wv;
+        if (wb) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(wv.x, wv.y), b = __floats2bfloat162_rn(wv.z, wv.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&a);
+            pk.y = *reinterpret_cast<uint32_t*>(&b);
+            reinterpret_cast<uint2*>(wb)[t] = pk;
+        }
+    }
+    for (long long t = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
         const float wv = w[t];
-        const float gp = g[t] * gs + decay * wv;
-        const float vv = mom * v[t] - lr * gp;
+        const float vv = mom * v[t] - lr * (g[t] * gs + decay * wv);
         const float nw = wv + vv;
         v[t] = vv;
         w[t] = nw;
@@ -514,7 +839,11 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, f
 
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom, float decay,
                   float gscale, cudaStream_t s) {
-    sgd_kernel<<<nblk(count, 256), 256, 0, s>>>(w, g, v, (__nv_bfloat16*)w_bf16, count, lr, mom, decay, gscale);
+    const bool al = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(w_bf16) & 7) == 0;
+    if (!al) return cudaErrorMisalignedAddress;
+    sgd_kernel<<<148 * 8, 256, 0, s>>>(w, g, v, (__nv_bfloat16*)w_bf16, count, lr, mom, decay, gscale);
+    note_launch();
     return cudaGetLastError();
 }
 

@@ -200,35 +200,96 @@ __global__ void __launch_bounds__(256, 1)
                     for (int j = 0; j < 16; j++) dst[(size_t)(c0 + j) * BM] = __uint_as_float(v[j]);
                 }
             } else {
-                const long long m = (long long)m_tile * BM + row;
+                const int m = m_tile * BM + row;
                 const bool row_ok = m < args.M;
-                const long long img = m / args.P, pix = m - img * args.P;
-                const long long rbase = img * args.s_n + pix * args.s_p;
+                const int img = m / args.P, pix = m - img * args.P;
+                const long long rbase = (long long)img * args.s_n + (long long)pix * args.s_p;
                 const int col0 = n_tile * args.BN;
+                const bool rowvec = args.s_c == 1;        // channels-last / row-major output
+                const bool bf = args.out_bf16 != 0;
+                const float beta = args.beta;
+                const int relu = args.relu;
                 for (int c0 = 0; c0 < args.BN; c0 += 16) {
                     if (col0 + c0 >= args.N) break;  // warp-uniform
                     uint32_t v[16];
                     tmem_ld16(taddr + c0, v);
                     tmem_wait_ld();
-                    if (row_ok) {
+                    if (!row_ok) continue;
+                    const int cb = g * args.col_g + col0 + c0;   // first output channel of this chunk
+                    const int nvalid = min(16, args.N - (col0 + c0));
+                    float x[16];
 #pragma unroll
-                        for (int j = 0; j < 16; j++) {
-                            const int col = col0 + c0 + j;
-                            if (col < args.N) {
-                                const int oc = g * args.col_g + col;
-                                float x = __uint_as_float(v[j]);
-                                if (args.bias) x += args.bias[oc];
-                                const long long off = rbase + (long long)oc * args.s_c;
-                                if (args.out_bf16) {
-                                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + off;
-                                    if (args.beta != 0.f) x += args.beta * __bfloat162float(*o);
-                                    if (args.relu) x = x > 0.f ? x : 0.f;
-                                    *o = __float2bfloat16_rn(x);
-                                } else {
-                                    float* o = reinterpret_cast<float*>(args.out) + off;
-                                    if (args.beta != 0.f) x += args.beta * *o;
-                                    if (args.relu) x = x > 0.f ? x : 0.f;
-                                    *o = x;
+                    for (int j = 0; j < 16; j++) x[j] = __uint_as_float(v[j]);
+                    if (args.bias) {
+#pragma unroll
+                        for (int j = 0; j < 16; j++)
+                            if (j < nvalid) x[j] += __ldg(args.bias + cb + j);
+                    }
+                    const long long off0 = rbase + (long long)cb * args.s_c;
+                    if (rowvec && nvalid == 16 && (off0 & (bf ? 7 : 3)) == 0) {
+                        if (bf) {
+                            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off0);
+                            if (beta != 0.f) {
+                                uint4 a = o[0], b = o[1];
+                                const __nv_bfloat16* ha = reinterpret_cast<const __nv_bfloat16*>(&a);
+                                const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&b);
+#pragma unroll
+                                for (int j = 0; j < 8; j++) {
+                                    x[j] += beta * __bfloat162float(ha[j]);
+                                    x[j + 8] += beta * __bfloat162float(hb[j]);
+                                }
+                            }
+                            if (relu) {
+#pragma unroll
+                                for (int j = 0; j < 16; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
+                            }
+                            uint4 pk[2];
+                            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+                            for (int j = 0; j < 8; j++) h2[j] = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+                            o[0] = pk[0];
+                            o[1] = pk[1];
+                        } else {
+                            float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + off0);
+                            if (beta != 0.f) {
+#pragma unroll
+                                for (int q4 = 0; q4 < 4; q4++) {
+                                    const float4 a = o[q4];
+                                    x[4 * q4] += beta * a.x; x[4 * q4 + 1] += beta * a.y;
+                                    x[4 * q4 + 2] += beta * a.z; x[4 * q4 + 3] += beta * a.w;
+                                }
+                            }
+                            if (relu) {
+#pragma unroll
+                                for (int j = 0; j < 16; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
+                            }
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; q4++)
+                                o[q4] = make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
+                        }
+                    } else {
+                        // column-coalesced scalar path (NCHW: the 32 lanes write 32 consecutive pixels)
+                        const long long sc = args.s_c;
+                        if (bf) {
+                            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + off0;
+#pragma unroll
+                            for (int j = 0; j < 16; j++) {
+                                if (j < nvalid) {
+                                    float y = x[j];
+                                    if (beta != 0.f) y += beta * __bfloat162float(o[j * sc]);
+                                    if (relu) y = y > 0.f ? y : 0.f;
+                                    o[j * sc] = __float2bfloat16_rn(y);
+                                }
+                            }
+                        } else {
+                            float* o = reinterpret_cast<float*>(args.out) + off0;
+#pragma unroll
+                            for (int j = 0; j < 16; j++) {
+                                if (j < nvalid) {
+                                    float y = x[j];
+                                    if (beta != 0.f) y += beta * o[j * sc];
+                                    if (relu) y = y > 0.f ? y : 0.f;
+                                    o[j * sc] = y;
                                 }
                             }
                         }
@@ -267,6 +328,7 @@ static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+    note_launch();
     return cudaGetLastError();
 }
 

@@ -135,22 +135,27 @@ class Net:
             self.dW[i] = self.grads[ow:ow + nw].view(ws)
             self.dB[i] = self.grads[ob:ob + nb]
             self.Wq[i] = self.params_bf16[ow:ow + nw].view(ws)
+        # gradient segments (layer index, offset, numel incl. bias) for the data-parallel buckets
+        self.segments = [(i, ow, ob + nb - ow) for (i, _, _), (ow, nw, ob, nb) in zip(pspecs, offs)]
         self.params.copy_(torch.from_numpy(host))
         self.params_bf16.copy_(self.params.to(torch.bfloat16))
         self.pspecs = pspecs
         # activations: a[i] = input of layer i; d[i] = diff w.r.t. a[i]
         self.a, self.d, self.mask = [], [], {}
         ad = self.act_dtype
+        # activations between conv/pool/LRN layers are channels-last (NHWC): the tensor-core conv
+        # reads and writes them without a transpose; the net input (data layer) and the inner-product
+        # inputs stay NCHW (S:130 flatten order).
+        self.nhwc = [L.kind not in ("ip", "loss") and len(self.shapes[i]) == 4 for i, L in enumerate(layers)]
         for i, L in enumerate(layers):
             s = self.shapes[i]
-            self.a.append(torch.empty(s, dtype=ad, device=device))
-            self.d.append(torch.empty(s, dtype=ad, device=device) if i > 0 else None)
+            self.a.append(cb.empty_like_layout(s, ad, device, nhwc=self.nhwc[i]))
+            self.d.append(cb.empty_like_layout(s, ad, device, nhwc=self.nhwc[i]) if i > 0 else None)
         self.scores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
         self.dscores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
         for i, L in enumerate(layers):
             if L.kind == "pool":
-                out = self.shapes[i + 1]
-                self.mask[i] = torch.empty(out, dtype=torch.int32, device=device)
+                self.mask[i] = cb.empty_like_layout(self.shapes[i + 1], torch.int32, device, nhwc=self.nhwc[i + 1])
         self.labels = torch.zeros(batch, dtype=torch.int32, device=device)
         self.loss = torch.zeros((), dtype=torch.float32, device=device)
 
@@ -219,3 +224,18 @@ class Net:
             allreduce.finish()
             scale = 1.0 / allreduce.world
         self.update(lr, momentum, decay, grad_scale=scale)
+
+    def capture(self, **kw):
+        """Record one whole training step (every library launch) into a CUDA graph; replaying it
+        re-runs the identical kernel sequence on the same buffers without host launch overhead.
+        Call after at least one eager step (so the cached workspace has reached its size)."""
+        torch = self.torch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.step(**kw)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        return g

@@ -138,3 +138,55 @@ def test_conv_empty_batch_is_noop():
     Wt = torch.zeros((4, 3, 3, 3), device="cuda")
     Y = cb.conv_forward(X, Wt, None, pad=1, math="bf16")
     assert Y.shape == (0, 4, 8, 8)
+
+
+# ---------------------------------------------------------------- channels-last (NHWC) BF16 blobs:
+# the tensor-core path reads/writes them directly (no transpose), the FP32 path via strides.
+NHWC_CASES = [CASES[1], CASES[2], CASES[3], CASES[7], (2, 16, 9, 9, 24, (3, 3), (1, 1), (1, 1), 2)]
+
+
+@pytest.mark.parametrize("math", ["bf16", "fp32"])
+@pytest.mark.parametrize("case", NHWC_CASES, ids=[f"N{c[0]}C{c[1]}H{c[2]}O{c[4]}k{c[5][0]}g{c[8]}" for c in NHWC_CASES])
+def test_conv_nhwc_bf16_storage(oracle, case, math):
+    import torch
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 5)
+    cl = torch.channels_last
+    Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    Xq, dYq = host(Xd), host(dYd)
+    Wq = oracle.quant_bf16(Wt) if math == "bf16" else Wt
+    chk = assert_tc_close if math == "bf16" else (lambda a, r, w: assert_fp32_close(a, r, w))
+    Y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, math=math, relu=True, out_dtype=torch.float32)
+    assert cb.layout_of(Y) == 1 or min(Y.shape[1], Y.shape[2] * Y.shape[3]) == 1
+    chk(host(Y), oracle.conv_forward(Xq, Wq, b, stride=s, pad=p, group=g, relu=True), "fwd nhwc")
+    dX = cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, math=math, out_dtype=torch.float32)
+    chk(host(dX), oracle.conv_backward_data(dYq, Wq, X.shape, stride=s, pad=p, group=g), "dgrad nhwc")
+    dW, db = cb.conv_backward_weight(Xd, dYd, Wt.shape, stride=s, pad=p, group=g, math=math)
+    rW, rb = oracle.conv_backward_weight(Xq, dYq, Wt.shape, stride=s, pad=p, group=g)
+    chk(host(dW), rW, "wgrad nhwc")
+    assert_fp32_close(host(db), rb, "bias grad nhwc")
+    # bf16 NHWC output epilogue == RNE of the fp32 result (vectorised row stores)
+    Y16 = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, math=math, relu=True)
+    np.testing.assert_array_equal(host(Y16), oracle.quant_bf16(host(Y)))
+
+
+@pytest.mark.parametrize("dy_layout", ["nchw_f32", "nhwc_f32", "nhwc_bf16"])
+def test_caffenet_conv1_full_image_wgrad(oracle, dy_layout):
+    """conv1 at its real geometry (227x227, 11x11/s4, space-to-depth path), 2 images, every dY layout."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    X = synth.int_pixels((2, 3, 227, 227), 13)
+    Wt = synth.gaussian((96, 3, 11, 11), 0.01, 13)
+    dY = synth.uniform((2, 96, 55, 55), 13, synth.S_DY)
+    dYd = cuda(dY)
+    if dy_layout != "nchw_f32":
+        dYd = dYd.contiguous(memory_format=torch.channels_last)
+    if dy_layout == "nhwc_bf16":
+        dYd = dYd.to(torch.bfloat16)
+    dW, db = cb.conv_backward_weight(cuda(X), dYd, Wt.shape, stride=4, pad=0, group=1, math="bf16")
+    rW, _ = oracle.conv_backward_weight(X, oracle.quant_bf16(dY), Wt.shape, stride=(4, 4))
+    assert_tc_close(host(dW), rW, f"conv1 wgrad {dy_layout}")
+    Y = cb.conv_forward(cuda(X), cuda(Wt), None, stride=4, math="bf16")
+    assert_tc_close(host(Y), oracle.conv_forward(X, oracle.quant_bf16(Wt), None, stride=(4, 4)), "conv1 fwd")

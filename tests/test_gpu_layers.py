@@ -157,3 +157,85 @@ def test_sgd(oracle):
     w0 = wt.clone()
     cb.sgd_update(wt, gt, torch.zeros_like(vt), 0.0, 0.0, 0.0)  # S:558 zero-LR fixed point
     np.testing.assert_array_equal(host(wt), host(w0))
+
+
+@pytest.mark.parametrize("case", POOLS)
+def test_pool_lrn_relu_nhwc(oracle, case):
+    """Channels-last blobs (and mixed in/out layouts) give the same bits as NCHW."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    shape, k, s, p = case
+    X = synth.uniform(shape, 11, synth.S_X)
+    X[0, 0] = np.round(X[0, 0] * 2)
+    cl = torch.channels_last
+    xn = cuda(X)
+    xh = xn.contiguous(memory_format=cl)
+    Yn, Mn = cb.pool_forward(xn, "max", k, s, p)
+    Yh, Mh = cb.pool_forward(xh, "max", k, s, p)
+    assert cb.layout_of(Yh) == 1 or Yh.shape[2] * Yh.shape[3] == 1
+    np.testing.assert_array_equal(host(Yh), host(Yn))
+    np.testing.assert_array_equal(host(Mh), host(Mn))
+    # NHWC in -> NCHW out
+    Yx = torch.empty(tuple(Yn.shape), device="cuda")
+    cb.pool_forward(xh, "max", k, s, p, out=Yx, mask=torch.empty(tuple(Yn.shape), dtype=torch.int32, device="cuda"))
+    np.testing.assert_array_equal(host(Yx), host(Yn))
+    dY = synth.uniform(tuple(Yn.shape), 11, synth.S_DY)
+    dXn = cb.pool_backward(cuda(dY), Mn, shape, "max", k, s, p)
+    dXh = cb.pool_backward(cuda(dY).contiguous(memory_format=cl), Mh, shape, "max", k, s, p)
+    np.testing.assert_array_equal(host(dXh), host(dXn))
+    Ya, _ = cb.pool_forward(xh, "ave", k, s, p)
+    assert_fp32_close(host(Ya), oracle.avepool_forward(X, k, s, p), "avepool nhwc")
+    L = cb.lrn_forward(xh)
+    assert_fp32_close(host(L), oracle.lrn_forward(X), "lrn nhwc")
+    dXl = cb.lrn_backward(xh, L, cuda(X * 0.5).contiguous(memory_format=cl))
+    assert_fp32_close(host(dXl), oracle.lrn_backward(X, X * 0.5), "lrn bwd nhwc")
+    R = cb.relu_forward(xh)
+    np.testing.assert_array_equal(host(R), oracle.relu_forward(X))
+
+
+@pytest.mark.parametrize("shape", [(2, 96, 27, 27), (2, 256, 13, 13), (1, 16, 7, 9)])
+def test_pool_lrn_nhwc_bf16_vector_paths(oracle, shape):
+    """The 8-channel vectorised channels-last BF16 kernels (CaffeNet's layout): max pool values,
+    argmax and backward bit-exact; LRN within one BF16 rounding of the fp64 oracle."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    cl = torch.channels_last
+    q = oracle.quant_bf16
+    X = q(synth.uniform(shape, 14, synth.S_X) * 3)
+    X[0, 0] = np.round(X[0, 0])
+    xh = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    Y, M = cb.pool_forward(xh, "max", 3, 2)
+    rY, rM = oracle.maxpool_forward(X, (3, 3), (2, 2))
+    np.testing.assert_array_equal(host(Y), rY)
+    np.testing.assert_array_equal(host(M), rM)
+    dY = q(synth.uniform(rY.shape, 14, synth.S_DY))
+    dX = cb.pool_backward(cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl), M, shape, "max", 3, 2)
+    np.testing.assert_array_equal(host(dX), q(oracle.maxpool_backward(dY, rM, shape, (3, 3), (2, 2))))
+    for size, a, b, k in ((5, 1e-4, 0.75, 1.0), (3, 0.5, 0.75, 2.0), (9, 2.0, 1.3, 1.0)):
+        L, S = cb.lrn_forward(xh, size, a, b, k, want_scale=True)
+        rL, rS = oracle.lrn_forward(X, size, a, b, k, want_scale=True)
+        assert_tc_close(host(L), q(rL.astype(np.float32)), f"lrn fwd bf16 nhwc n={size}", tol=2e-3)
+        assert_fp32_close(host(S), rS, "lrn scale")
+        G = q(synth.uniform(shape, 15, synth.S_DY))
+        dL = cb.lrn_backward(xh, L, cuda(G).to(torch.bfloat16).contiguous(memory_format=cl), size, a, b, k)
+        rdL = oracle.lrn_backward(X, G, size, a, b, k)
+        assert_tc_close(host(dL), rdL, f"lrn bwd bf16 nhwc n={size}", tol=5e-3)
+
+
+def test_ip_nhwc_bottom(oracle):
+    """An NHWC bottom is flattened in Caffe's (c,h,w) order."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    X = synth.uniform((8, 16, 3, 3), 12, synth.S_X)
+    Wt = synth.xavier((10, 144), 12)
+    dY = synth.uniform((8, 10), 12, synth.S_DY)
+    xh = cuda(X).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    Xq = host(xh)
+    Y = cb.ip_forward(xh, cuda(Wt), None, math="bf16", out_dtype=torch.float32)
+    assert_tc_close(host(Y), oracle.ip_forward(Xq, oracle.quant_bf16(Wt)), "ip fwd nhwc")
+    dW, _ = cb.ip_backward_weight(xh, cuda(dY), (10, 144), math="bf16")
+    rdX, rdW, _ = oracle.ip_backward(Xq, oracle.quant_bf16(Wt), oracle.quant_bf16(dY))
+    assert_tc_close(host(dW), rdW, "ip wgrad nhwc")
+    dX = torch.zeros((8, 16, 3, 3), device="cuda").contiguous(memory_format=torch.channels_last)
+    cb.ip_backward_data(cuda(dY), cuda(Wt), X.shape, math="bf16", out=dX)
+    assert_tc_close(host(dX), rdX, "ip dgrad nhwc")

@@ -1,0 +1,126 @@
+"""Net-level parity (-m gpu): the straight-line LeNet / CaffeNet training step run through the C ABI
+(paper_1408_5093_b200.nets) against the oracle on the same seeded inputs and weights.
+
+* end to end: the loss of the GPU step matches oracle/net.py's forward to 1e-3 relative
+  (SURVEY 8(c) "Nets"), with BF16 GEMM operands on both sides;
+* teacher-forced: every layer's forward output and every parameter / data gradient is compared with
+  the oracle layer applied to the GPU's OWN inputs (its stored activation and the top diff that
+  layer consumed).  Max-pool and ReLU discontinuities make a free-running comparison of gradients
+  meaningless (a 1-ulp difference flips an argmax), so the chain is checked link by link.
+  Tolerances: the per-layer bars (rel-L2 1e-3 for tensor-core passes; BF16-stored results are
+  compared after rounding the oracle's value to BF16 the same way).
+"""
+import numpy as np
+import pytest
+
+import synth
+from _helpers import assert_tc_close, host
+
+pytestmark = pytest.mark.gpu
+
+LRN = dict(size=5, alpha=1e-4, beta=0.75, k=1.0)
+
+
+def _build(which, batch, act):
+    import torch
+    from paper_1408_5093_b200 import nets
+    layers, shape = (nets.LENET, nets.LENET_INPUT) if which == "lenet" else (nets.CAFFENET, nets.CAFFENET_INPUT)
+    dt = torch.float32 if act == "f32" else torch.bfloat16
+    net = nets.Net(layers, batch, shape, torch.device("cuda"), act_dtype=dt, math="bf16", seed=0)
+    X = synth.int_pixels((batch,) + tuple(shape), 7) if which == "caffenet" else \
+        synth.mnist_pixels((batch,) + tuple(shape), 7)
+    lab = synth.labels(batch, net.shapes[-1][1], 7)
+    net.a[0].copy_(torch.from_numpy(X))
+    net.labels.copy_(torch.from_numpy(lab))
+    net.grads.zero_()
+    net.forward()
+    net.backward()
+    torch.cuda.synchronize()
+    return net, X, lab
+
+
+def _stored(net, ref, i_out):
+    """Round an oracle result the way the GPU stored blob i_out is stored (BF16 activations)."""
+    import torch
+    import oracle
+    t = net.a[i_out] if i_out < len(net.a) else None
+    if t is not None and t.dtype == torch.bfloat16:
+        return oracle.quant_bf16(np.asarray(ref, np.float32))
+    return ref
+
+
+@pytest.mark.parametrize("which,batch,act", [("lenet", 16, "f32"), ("lenet", 16, "bf16"),
+                                             ("caffenet", 2, "f32"), ("caffenet", 2, "bf16")])
+def test_net_teacher_forced(oracle, which, batch, act):
+    from oracle import net as onet
+    net, X, lab = _build(which, batch, act)
+    q = oracle.quant_bf16
+    n = len(net.layers)
+    # ---------------- end-to-end loss vs the oracle's own forward (BF16 GEMM operands)
+    olayers = onet.LENET if which == "lenet" else onet.CAFFENET
+    params = {net.layers[i].name: (host(net.W[i]).astype(np.float64), host(net.B[i]).astype(np.float64))
+              for (i, _, _) in net.pspecs}
+    oloss, _, _ = onet.forward_backward(olayers, X, params, lab, quant=q)
+    assert abs(float(net.loss) - oloss) <= 1e-3 * abs(oloss), (float(net.loss), oloss)
+    # ---------------- forward, layer by layer on the GPU's own inputs
+    for i, L in enumerate(net.layers[:-1]):
+        x = host(net.a[i]).astype(np.float64)
+        last = i + 1 == n - 1
+        y = host(net.scores if last else net.a[i + 1])
+        W = host(net.W[i]) if i in net.W else None
+        if L.kind == "conv":
+            ref = oracle.conv_forward(q(x), q(W), host(net.B[i]), stride=(L.stride,) * 2, pad=(L.pad,) * 2,
+                                      group=L.group, relu=L.relu)
+        elif L.kind == "pool":
+            ref = oracle.maxpool_forward(x.astype(np.float32), (L.kernel,) * 2, (L.stride,) * 2)[0]
+            np.testing.assert_array_equal(y, ref.reshape(y.shape))
+            continue
+        elif L.kind == "lrn":
+            ref = oracle.lrn_forward(x, **LRN)
+        else:
+            ref = oracle.ip_forward(q(x), q(W), host(net.B[i]))
+            if L.relu:
+                ref = np.maximum(ref, 0)
+        ref = ref.reshape(y.shape)
+        assert_tc_close(y, ref if last else _stored(net, ref, i + 1), f"{which} {L.name} fwd")
+    # ---------------- softmax-loss gradient on the GPU's scores
+    lo, dref = oracle.softmax_loss(host(net.scores), lab)
+    assert abs(float(net.loss) - lo) <= 1e-5 * (abs(lo) + 1)
+    # ---------------- backward, layer by layer on the GPU's own (x, consumed dy)
+    for i in range(n - 2, -1, -1):
+        L = net.layers[i]
+        x = host(net.a[i]).astype(np.float64)
+        dy = host(net.dscores if i + 1 == n - 1 else net.d[i + 1]).astype(np.float64)  # after in-place ReLU mask
+        mask_in = None
+        if i > 0 and net.layers[i - 1].kind in ("conv", "ip") and net.layers[i - 1].relu:
+            mask_in = x > 0            # d[i] was masked in place by the layer below's ReLU backward
+        if L.kind == "conv":
+            W = host(net.W[i])
+            dW, db = oracle.conv_backward_weight(q(x), q(dy), W.shape, stride=(L.stride,) * 2, pad=(L.pad,) * 2,
+                                                 group=L.group)
+            assert_tc_close(host(net.dW[i]), dW, f"{which} {L.name} dW")
+            assert_tc_close(host(net.dB[i]), dy.sum(axis=(0, 2, 3)), f"{which} {L.name} db")
+            if i == 0:
+                continue
+            ref = oracle.conv_backward_data(q(dy), q(W), x.shape, stride=(L.stride,) * 2, pad=(L.pad,) * 2,
+                                            group=L.group)
+        elif L.kind == "ip":
+            W = host(net.W[i])
+            dX, dW, _ = oracle.ip_backward(q(x), q(W), q(dy.reshape(dy.shape[0], -1)))
+            assert_tc_close(host(net.dW[i]), dW, f"{which} {L.name} dW")
+            assert_tc_close(host(net.dB[i]), dy.reshape(dy.shape[0], -1).sum(0), f"{which} {L.name} db")
+            ref = dX.reshape(x.shape)
+        elif L.kind == "pool":
+            _, m = oracle.maxpool_forward(x.astype(np.float32), (L.kernel,) * 2, (L.stride,) * 2)
+            ref = oracle.maxpool_backward(dy.astype(np.float32), m, x.shape, (L.kernel,) * 2, (L.stride,) * 2)
+        else:  # lrn
+            ref = oracle.lrn_backward(x, dy, **LRN)
+        if mask_in is not None:
+            ref = np.where(mask_in, ref, 0.0)
+        got = host(net.d[i])
+        ref = _stored(net, ref, i)
+        if L.kind == "pool" and act == "f32":
+            np.testing.assert_array_equal(got, ref)
+        else:
+            assert_tc_close(got, ref, f"{which} {L.name} dX")
+    assert np.isfinite(float(net.loss))

@@ -1,0 +1,86 @@
+"""Micro-benchmark of the tcgen05 GEMM paths (run on the B200 box).
+
+Times single ABI calls with CUDA events (median of 20 after warm-up) and prints TFLOP/s:
+plain 2-D-tiled GEMMs through caffe_ip_forward and the CaffeNet conv passes with channels-last
+BF16 operands (TMA im2col).
+"""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1408_5093_b200 as cb  # noqa: E402
+
+
+def timeit(fn, reps=5, inner=20):
+    """Median over `reps` of the mean time of `inner` back-to-back calls captured in a CUDA graph
+    (so host launch overhead does not leak into the device time)."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+        for _ in range(inner):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) / inner)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def main():
+    torch.manual_seed(0)
+    dev = torch.device("cuda")
+    out = {}
+    if "--only-gemm" in sys.argv:   # for ncu: a few launches of one plain GEMM
+        M, N, K = 65536, 256, 1152
+        x = torch.randn(M, K, device=dev).to(torch.bfloat16)
+        w = torch.randn(N, K, device=dev).to(torch.bfloat16)
+        y = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        for _ in range(4):
+            cb.ip_forward(x, w, None, out=y)
+        torch.cuda.synchronize()
+        return
+    for (M, N, K) in [(65536, 128, 1600), (65536, 256, 1152), (65536, 192, 1728), (256, 4096, 9216)]:
+        x = torch.randn(M, K, device=dev).to(torch.bfloat16)
+        w = torch.randn(N, K, device=dev).to(torch.bfloat16)
+        y = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        ms = timeit(lambda: cb.ip_forward(x, w, None, out=y))
+        out[f"gemm M{M} N{N} K{K}"] = round(2 * M * N * K / ms / 1e9, 1)
+    cl = torch.channels_last
+    B = 256
+    for name, (C, H, O, k, p, g) in {"conv2": (96, 27, 256, 5, 2, 2), "conv3": (256, 13, 384, 3, 1, 1),
+                                     "conv4": (384, 13, 384, 3, 1, 2), "conv5": (384, 13, 256, 3, 1, 2)}.items():
+        x = torch.randn(B, C, H, H, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+        w = torch.randn(O, C // g, k, k, device=dev) * 0.05
+        bias = torch.zeros(O, device=dev)
+        y = cb.conv_forward(x, w, bias, 1, p, g, relu=True)
+        flops = 2 * B * O * H * H * (C // g) * k * k
+        ms = timeit(lambda: cb.conv_forward(x, w, bias, 1, p, g, relu=True, out=y))
+        dy = torch.randn_like(y)
+        ms_d = timeit(lambda: cb.conv_backward_data(dy, w, x.shape, 1, p, g, out=torch.empty_like(x)))
+        dw = torch.zeros_like(w)
+        db = torch.zeros(O, device=dev)
+        ms_w = timeit(lambda: cb.conv_backward_weight(x, dy, w.shape, 1, p, g, dw=dw, db=db))
+        out[name] = {"fwd_tflops": round(flops / ms / 1e9, 1), "dgrad_tflops": round(flops / ms_d / 1e9, 1),
+                     "wgrad_tflops": round(flops / ms_w / 1e9, 1), "fwd_us": round(ms * 1e3, 1),
+                     "dgrad_us": round(ms_d * 1e3, 1), "wgrad_us": round(ms_w * 1e3, 1)}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
