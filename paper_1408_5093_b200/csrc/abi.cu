@@ -235,14 +235,27 @@ WgradSplit wgrad_split(const Plan& p) {
     w.BN = choose_bn(p.Og);
     w.n_tiles = (int)cdiv(p.Og, w.BN);
     w.kblocks = (int)cdiv((long long)p.N * p.OH * p.OW, p.CH);
+    // Split the pixel reduction so that (tiles x splits) work units fill the SMs in whole waves:
+    // maximise wave efficiency x split balance x kb/(kb + 2) (per-unit prologue/epilogue cost).
     const int tiles = w.m_tiles * w.n_tiles * p.G;
     const int sms = 148;
-    int s = (int)cdiv(2 * sms, tiles);
-    if (s < 1) s = 1;
-    int kb_per = (int)cdiv(w.kblocks, s);
-    if (kb_per < 4) kb_per = 4;
-    w.kb_per = kb_per;
-    w.splits = (int)cdiv(w.kblocks, kb_per);
+    double best = -1.0;
+    w.kb_per = w.kblocks;
+    w.splits = 1;
+    for (int s = 1; s <= 1024 && s <= w.kblocks; s++) {
+        const int kb_per = (int)cdiv(w.kblocks, s);
+        if (kb_per < 4 && s > 1) break;
+        const int ss = (int)cdiv(w.kblocks, kb_per);
+        const long long units = (long long)tiles * ss;
+        const double wave = (double)units / (double)(cdiv(units, sms) * sms);
+        const double bal = (double)w.kblocks / ((double)ss * kb_per);
+        const double eff = wave * bal * kb_per / (kb_per + 2.0);
+        if (eff > best + 1e-9) {
+            best = eff;
+            w.kb_per = kb_per;
+            w.splits = ss;
+        }
+    }
     return w;
 }
 size_t ws_partial(const Plan& p) {

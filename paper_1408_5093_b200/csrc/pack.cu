@@ -105,10 +105,60 @@ __global__ void pack_transpose_kernel(const void* __restrict__ src, int src_bf16
     }
 }
 
+// Space-to-depth into bf16: one thread builds one packed pixel row (all Ctot channels) with
+// incremental (division-free) channel bookkeeping, writing 16-byte vectors.
+__global__ void pack_s2d_kernel(const void* __restrict__ src, int src_bf16, L4 ls, __nv_bfloat16* __restrict__ dst,
+                                PackGeom g, int total) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int X = t % g.Wp;
+        const int r = t / g.Wp;
+        const int Y = r % g.Hp;
+        const int n = r / g.Hp;
+        __nv_bfloat16* out = dst + (long long)t * g.Ctot;
+        const long long sb = (long long)n * ls.sn;
+        for (int grp = 0; grp < g.G; grp++) {
+            float v[8];
+            int e = 0;
+            int cc = 0;
+            auto flush = [&](int upto) {
+                for (int q = e; q < 8; q++) v[q] = 0.f;
+                uint4 pk;
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+                for (int q = 0; q < 4; q++) h2[q] = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+                *reinterpret_cast<uint4*>(out + grp * g.cpg + upto) = pk;
+                e = 0;
+            };
+            for (int dy = 0; dy < g.sh; dy++) {
+                const int h = Y * g.sh + dy - g.ph;
+                for (int dx = 0; dx < g.sw; dx++) {
+                    const int w = X * g.sw + dx - g.pw;
+                    const bool in = h >= 0 && h < g.H && w >= 0 && w < g.W;
+                    const long long pb = sb + (long long)h * ls.sh + (long long)w * ls.sw + (long long)grp * g.Cg * ls.sc;
+                    for (int c = 0; c < g.Cg; c++) {
+                        v[e++] = in ? ld_any(src, pb + (long long)c * ls.sc, src_bf16) : 0.f;
+                        cc++;
+                        if (e == 8) flush(cc - 8);
+                    }
+                }
+            }
+            // zero tail up to cpg
+            while (cc < g.cpg) {
+                v[e++] = 0.f;
+                cc++;
+                if (e == 8) flush(cc - 8);
+            }
+        }
+    }
+}
+
 cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* dst, int dst_esz, const PackGeom& g,
                      cudaStream_t s) {
     const bool plain = g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.Hp == g.H && g.Wp == g.W;
-    if (plain && !src_nhwc && dst_esz == 2 && g.cpg == g.Cg && g.G * g.Cg <= g.Ctot) {
+    if (!plain && dst_esz == 2 && g.cpg % 8 == 0) {
+        const int total = g.N * g.Hp * g.Wp;
+        pack_s2d_kernel<<<blocks_for(total, 128), 128, 0, s>>>(src, src_bf16, ls, (__nv_bfloat16*)dst, g, total);
+    } else if (plain && !src_nhwc && dst_esz == 2 && g.cpg == g.Cg && g.G * g.Cg <= g.Ctot) {
         const int P = g.H * g.W;
         dim3 grid((P + 63) / 64, (g.Ctot + 63) / 64, g.N);
         pack_transpose_kernel<<<grid, 256, 0, s>>>(src, src_bf16, (__nv_bfloat16*)dst, g.C, P, g.Ctot);

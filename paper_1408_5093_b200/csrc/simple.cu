@@ -181,6 +181,38 @@ __global__ void bias_partial_nhwc(const void* __restrict__ dy, int dyb, int O, i
     }
 }
 
+// BF16 channels-last, O % 8 == 0: thread = (row group, 8-channel vector); 16-byte loads; the row
+// groups of a block are summed in fixed order through shared memory.
+__global__ void bias_partial_nhwc8(const __nv_bfloat16* __restrict__ dy, int O, int M, int R, float* __restrict__ part) {
+    extern __shared__ float red8[];   // [RG][O]
+    const int CV = O / 8, RG = blockDim.x / CV;
+    const int s = blockIdx.x, cv = threadIdx.x % CV, rg = threadIdx.x / CV;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) acc[e] = 0.f;
+    if (rg < RG) {
+        const int m1 = min(M, (s + 1) * R);
+        for (int m = s * R + rg; m < m1; m += RG) {
+            const uint4 u = *reinterpret_cast<const uint4*>(dy + (long long)m * O + cv * 8);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const float2 f = __bfloat1622float2(h[e]);
+                acc[2 * e] += f.x;
+                acc[2 * e + 1] += f.y;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++) red8[rg * O + cv * 8 + e] = acc[e];
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < O; o += blockDim.x) {
+        float t = 0.f;
+        for (int k = 0; k < RG; k++) t += red8[k * O + o];
+        part[s * O + o] = t;
+    }
+}
+
 __global__ void bias_partial_nchw(const void* __restrict__ dy, int dyb, int O, int P, int N, int R,
                                   float* __restrict__ part) {
     __shared__ float red[256];
@@ -220,7 +252,10 @@ cudaError_t bias_grad(const void* dy, int dy_bf16, int nhwc, float* db, float be
     const int M = N * P;
     const int S = bias_grad_splits(N, O, P);
     const int R = (M + S - 1) / S;
-    if (nhwc || P == 1) {
+    if ((nhwc || P == 1) && dy_bf16 && O % 8 == 0 && O <= 2048 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0) {
+        const int CV = O / 8, RG = 256 / CV;
+        bias_partial_nhwc8<<<S, 256, (size_t)RG * O * sizeof(float), s>>>((const __nv_bfloat16*)dy, O, M, R, part);
+    } else if (nhwc || P == 1) {
         bias_partial_nhwc<<<dim3(S, (O + 31) / 32), 256, 0, s>>>(dy, dy_bf16, O, M, R, part);
     } else {
         bias_partial_nchw<<<dim3(S, O), 256, 0, s>>>(dy, dy_bf16, O, P, N, R, part);
@@ -761,15 +796,50 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
 }
 
 // ================================================================ softmax with loss
-// One block of 32 warps; warp w owns rows w, w+32, ...; per-warp loss sums in row order, then a
+// One block of 16 warps; warp w owns rows w, w+16, ...; per-warp loss sums in row order, then a
 // fixed-order sum over warps -> deterministic mean.
 __global__ void softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restrict__ labels,
                                     float* __restrict__ loss, void* __restrict__ diff, int db, int N, int K) {
     __shared__ float wl[32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     float my = 0.f;
-    for (int n = warp; n < N; n += 32) {
+    for (int n = warp; n < N; n += nw) {
         const int base = n * K;
+        const int lab = labels[n];
+        if (K <= 1024) {
+            // the row lives in registers: one global read, one write
+            float v[32];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+                const int k = lane + 32 * q;
+                v[q] = k < K ? ldv(s, base + k, sb) : -INFINITY;
+                mx = fmaxf(mx, v[q]);
+            }
+            for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            float se = 0.f;
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+                v[q] = (lane + 32 * q < K) ? expf(v[q] - mx) : 0.f;
+                se += v[q];
+            }
+            for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+            const float lse = logf(se);
+            if (lane == 0) my += lse - (ldv(s, base + lab, sb) - mx);
+            if (diff) {
+                const float inv = 1.f / N, rse = 1.f / se;
+#pragma unroll
+                for (int q = 0; q < 32; q++) {
+                    const int k = lane + 32 * q;
+                    if (k < K) {
+                        float p = v[q] * rse;
+                        if (k == lab) p -= 1.f;
+                        stv(diff, base + k, db, p * inv);
+                    }
+                }
+            }
+            continue;
+        }
         float mx = -INFINITY;
         for (int k = lane; k < K; k += 32) mx = fmaxf(mx, ldv(s, base + k, sb));
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -777,7 +847,6 @@ __global__ void softmax_loss_kernel(const void* __restrict__ s, int sb, const in
         for (int k = lane; k < K; k += 32) se += expf(ldv(s, base + k, sb) - mx);
         for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
         const float lse = logf(se);
-        const int lab = labels[n];
         if (lane == 0) my += lse - (ldv(s, base + lab, sb) - mx);
         if (diff) {
             const float inv = 1.f / N;
@@ -792,14 +861,14 @@ __global__ void softmax_loss_kernel(const void* __restrict__ s, int sb, const in
     __syncthreads();
     if (threadIdx.x == 0) {
         float t = 0.f;
-        for (int w = 0; w < 32; w++) t += wl[w];
+        for (int w = 0; w < nw; w++) t += wl[w];
         *loss = t / N;
     }
 }
 
 cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff, int diff_bf16,
                            int N, int K, cudaStream_t s) {
-    softmax_loss_kernel<<<1, 1024, 0, s>>>(scores, bf16, labels, loss, diff, diff_bf16, N, K);
+    softmax_loss_kernel<<<1, 512, 0, s>>>(scores, bf16, labels, loss, diff, diff_bf16, N, K);
     note_launch();
     return cudaGetLastError();
 }

@@ -143,10 +143,10 @@ class Net:
         # activations: a[i] = input of layer i; d[i] = diff w.r.t. a[i]
         self.a, self.d, self.mask = [], [], {}
         ad = self.act_dtype
-        # activations between conv/pool/LRN layers are channels-last (NHWC): the tensor-core conv
-        # reads and writes them without a transpose; the net input (data layer) and the inner-product
-        # inputs stay NCHW (S:130 flatten order).
-        self.nhwc = [L.kind not in ("ip", "loss") and len(self.shapes[i]) == 4 for i, L in enumerate(layers)]
+        # every 4-D activation is channels-last (NHWC): the tensor-core conv reads and writes it
+        # without a transpose and pool/LRN use 16-byte channel vectors; the inner product flattens
+        # its NHWC input in the (c,h,w) order of S:130 inside the library.
+        self.nhwc = [L.kind != "loss" and len(self.shapes[i]) == 4 for i, L in enumerate(layers)]
         for i, L in enumerate(layers):
             s = self.shapes[i]
             self.a.append(cb.empty_like_layout(s, ad, device, nhwc=self.nhwc[i]))
@@ -176,8 +176,7 @@ class Net:
                 cb.lrn_forward(x, **LRN, out=nxt)
             elif L.kind == "ip":
                 out = nxt if nxt is not None else self.scores
-                cb.ip_forward(x.view(x.shape[0], -1), self._wop(i), self.B[i], self.math, relu=L.relu,
-                              out=out.view(out.shape[0], -1))
+                cb.ip_forward(x, self._wop(i), self.B[i], self.math, relu=L.relu, out=out.view(out.shape[0], -1))
             elif L.kind == "loss":
                 cb.softmax_loss(self.scores, self.labels, loss=self.loss, diff=self.dscores)
 
@@ -200,13 +199,12 @@ class Net:
                     cb.conv_backward_data(dy, self._wop(i), a[i].shape, L.stride, L.pad, L.group, self.math,
                                           beta=0.0, out=d[i])
             elif L.kind == "ip":
-                x2 = a[i].view(a[i].shape[0], -1)
                 dy2 = dy.view(dy.shape[0], -1)
-                cb.ip_backward_weight(x2, dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i], db=self.dB[i])
+                cb.ip_backward_weight(a[i], dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i], db=self.dB[i])
                 if hook:
                     hook(i)
                 if i > 0:
-                    cb.ip_backward_data(dy2, self._wop(i), x2.shape, self.math, beta=0.0, out=d[i].view(x2.shape))
+                    cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
             elif L.kind == "pool":
                 cb.pool_backward(dy, self.mask[i], a[i].shape, L.method, L.kernel, L.stride, L.pad, out=d[i])
             elif L.kind == "lrn":
