@@ -113,6 +113,13 @@ const char* caffe_last_error(void);
 /* Checks that a CUDA device of compute capability 10.0 is current. */
 caffe_status caffe_device_check(void);
 
+/* Tuning knobs (process-wide; never change results beyond FP32 summation order, which is still
+   deterministic for a fixed setting):
+   CAFFE_TUNE_CTA_PAIR: 0 = automatic (default), 1 = force single-CTA M=128 tensor-core tiles,
+   2 = force CTA-pair M=256 tiles (tcgen05 cta_group::2) where the kernel supports them. */
+#define CAFFE_TUNE_CTA_PAIR 1
+caffe_status caffe_set_tuning(int32_t key, int32_t value);
+
 /* ------------------------------------------------------------------ instrumentation
    (for benchmarks; never changes results)
    caffe_launch_count: cumulative number of kernels this library launched in the process.

@@ -21,6 +21,7 @@ CAFFE_MATH_FP32, CAFFE_MATH_TF32, CAFFE_MATH_BF16 = 0, 1, 2
 CAFFE_FUSE_RELU = 1
 CAFFE_POOL_MAX, CAFFE_POOL_AVE = 0, 1
 CAFFE_PASS_FORWARD, CAFFE_PASS_BACKWARD_DATA, CAFFE_PASS_BACKWARD_WEIGHT = 0, 1, 2
+CAFFE_TUNE_CTA_PAIR = 1
 
 
 class Shape4(ctypes.Structure):
@@ -57,6 +58,7 @@ SIGNATURES = {
     "caffe_abi_version": [],
     "caffe_last_error": [],
     "caffe_device_check": [],
+    "caffe_set_tuning": [i32, i32],
     "caffe_launch_count": [],
     "caffe_profiler_enable": [i32],
     "caffe_profiler_read": [i32, P(ctypes.c_double), P(ctypes.c_double), P(i64)],

@@ -200,6 +200,14 @@ int choose_bn(int n) {
     const int t = (int)cdiv(n, 256);
     return (int)rup(cdiv(n, t), 16);
 }
+// CTA pairs (M=256 tiles, cta_group::2) whenever the pair-tiles still fill every SM pair once.
+int g_force_cg = 0;   // caffe_set_tuning(CAFFE_TUNE_CTA_PAIR, 1|2) overrides the automatic choice
+int pick_cg(long long M, int ntiles_x_groups, int E) {
+    if (E != 2) return 1;
+    if (g_force_cg == 1 || g_force_cg == 2) return g_force_cg;
+    const long long pair_units = cdiv(M, 256) * ntiles_x_groups;
+    return pair_units >= num_sms() / 2 ? 2 : 1;
+}
 int pow2ceil(int x) {
     int p = 32;
     while (p < x) p <<= 1;
@@ -283,7 +291,9 @@ caffe_status check_ws(void* ws, size_t have, size_t need) {
 
 // kind: 0 = convolution pass, 1 = inner product; flops = algorithmic FLOPs of the call
 caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
-    L.grid = L.args.units < num_sms() ? L.args.units : num_sms();
+    if (L.cg < 1) L.cg = 1;
+    const int slots = num_sms() / L.cg;                  // CTAs (or CTA pairs) resident at once
+    L.grid = (L.args.units < slots ? L.args.units : slots) * L.cg;
     ProfRec rec{nullptr, nullptr, flops, kind};
     if (g_prof) {
         std::lock_guard<std::mutex> lk(g_pmu);
@@ -341,6 +351,15 @@ caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_
     *flops = f;
     *launches = n;
     return CAFFE_OK;
+}
+
+caffe_status caffe_set_tuning(int32_t key, int32_t value) {
+    if (key == CAFFE_TUNE_CTA_PAIR) {
+        if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "CTA-pair mode must be 0 (auto), 1 or 2");
+        g_force_cg = value;
+        return CAFFE_OK;
+    }
+    return fail(CAFFE_E_INVALID, "unknown tuning key %d", key);
 }
 
 caffe_status caffe_device_check(void) {
@@ -434,17 +453,19 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (activation)");
     TcArgs& a = L.args;
     a.BN = choose_bn(p.Og);
-    if (!encode_tiled_2d(&L.mapB, p.E, WB, (uint64_t)p.taps * p.Cgp, (uint64_t)p.O, (uint64_t)p.taps * p.Cgp * p.E,
-                         p.CH, a.BN))
-        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (weights)");
     a.M = p.N * p.OH * p.OW; a.N = p.Og;
-    a.m_tiles = (int)cdiv(a.M, 128); a.n_tiles = (int)cdiv(p.Og, a.BN); a.groups = p.G; a.splits = 1;
+    a.n_tiles = (int)cdiv(p.Og, a.BN); a.groups = p.G; a.splits = 1;
+    L.cg = pick_cg(a.M, a.n_tiles * p.G, p.E);
+    a.m_tiles = (int)cdiv(a.M, 128 * L.cg);
+    if (!encode_tiled_2d(&L.mapB, p.E, WB, (uint64_t)p.taps * p.Cgp, (uint64_t)p.O, (uint64_t)p.taps * p.Cgp * p.E,
+                         p.CH, a.BN / L.cg))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (weights)");
     a.kblocks = p.taps * (p.Cgp / p.CH); a.kb_per_split = a.kblocks;
     a.a_P = p.OH * p.OW; a.a_OW = p.OW; a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_kw = p.kwp;
     a.a_cblocks = p.Cgp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Og;
     set_out(a, top);
     a.col_g = p.Og; a.bias = bptr; a.relu = relu; a.beta = 0.f;
-    finish_args(a, a.BN * 128);
+    finish_args(a, a.BN / L.cg * 128);
     return run_tc(L, s, conv_flops(p), 0);
 }
 
@@ -490,11 +511,13 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (top_diff)");
     TcArgs& a = L.args;
     a.BN = choose_bn(p.Cge);
-    if (!encode_tiled_2d(&L.mapB, p.E, WD, (uint64_t)p.taps * p.Ogp, (uint64_t)p.G * p.Cge,
-                         (uint64_t)p.taps * p.Ogp * p.E, p.CH, a.BN))
-        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (dgrad weights)");
     a.M = p.N * Hd * Wd; a.N = p.Cge;
-    a.m_tiles = (int)cdiv(a.M, 128); a.n_tiles = (int)cdiv(p.Cge, a.BN); a.groups = p.G; a.splits = 1;
+    a.n_tiles = (int)cdiv(p.Cge, a.BN); a.groups = p.G; a.splits = 1;
+    L.cg = pick_cg(a.M, a.n_tiles * p.G, p.E);
+    a.m_tiles = (int)cdiv(a.M, 128 * L.cg);
+    if (!encode_tiled_2d(&L.mapB, p.E, WD, (uint64_t)p.taps * p.Ogp, (uint64_t)p.G * p.Cge,
+                         (uint64_t)p.taps * p.Ogp * p.E, p.CH, a.BN / L.cg))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (dgrad weights)");
     a.kblocks = p.taps * (p.Ogp / p.CH); a.kb_per_split = a.kblocks;
     a.a_P = Hd * Wd; a.a_OW = Wd; a.a_pad_h = lo_h; a.a_pad_w = lo_w; a.a_kw = p.kwp;
     a.a_cblocks = p.Ogp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Cge;
@@ -507,7 +530,7 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
         a.s_n = (long long)p.Hp * p.Wp * tg.Ctot; a.s_c = 1; a.s_p = tg.Ctot;
         a.col_g = p.Cge; a.beta = 0.f;
     }
-    finish_args(a, a.BN * 128);
+    finish_args(a, a.BN / L.cg * 128);
     if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
     if (p.s2d) CK(unpack_s2d_grad(T, bottom_diff->ptr, isbf(bottom_diff), nhwc(bottom_diff), beta, tg, s), "unpack s2d gradient");
     return CAFFE_OK;

@@ -45,6 +45,7 @@ struct TcLaunch {
     TcArgs args;
     int esz;                            // 2 = bf16 (kind::f16), 4 = fp32 (kind::tf32)
     int amode, bmode, epi;
+    int cg;                             // 1 = single CTA (M=128), 2 = CTA pair (cta_group::2, M=256)
     int grid;
 };
 

@@ -162,7 +162,7 @@ cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, L4 lx, const void* dy, in
 //   NHWC (channels contiguous): lane -> channel, 8 warps stride over the pixels of the range.
 //   NCHW (pixels contiguous):   block = (range, channel), threads stride over the range.
 // Stage 2: sum of the partials in ascending s.
-constexpr int BG_SPLITS_MAX = 256;
+constexpr int BG_SPLITS_MAX = 148 * 8;
 
 __global__ void bias_partial_nhwc(const void* __restrict__ dy, int dyb, int O, int M, int R, float* __restrict__ part) {
     __shared__ float red[8][33];
@@ -232,19 +232,27 @@ __global__ void bias_partial_nchw(const void* __restrict__ dy, int dyb, int O, i
     if (threadIdx.x == 0) part[s * O + o] = red[0];
 }
 
+// Stage 2: block per output channel; threads take partials s = t, t+128, ... then a fixed tree.
 __global__ void bias_final(const float* __restrict__ part, int S, int O, float* __restrict__ db, float beta) {
-    const int o = blockIdx.x * blockDim.x + threadIdx.x;
-    if (o >= O) return;
+    __shared__ float red[128];
+    const int o = blockIdx.x;
     float t = 0.f;
-    for (int s = 0; s < S; s++) t += part[s * O + o];
-    db[o] = (beta != 0.f ? beta * db[o] : 0.f) + t;
+    for (int s = threadIdx.x; s < S; s += 128) t += part[s * O + o];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int st = 64; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) db[o] = (beta != 0.f ? beta * db[o] : 0.f) + red[0];
 }
 
+// splits of the pixel range: ~8 blocks per SM, >= 64 rows each
 int bias_grad_splits(int N, int O, int P) {
     const long long M = (long long)N * P;
-    int S = (int)((M + 2047) / 2048);
+    long long S = (M + 63) / 64;
     if (S > BG_SPLITS_MAX) S = BG_SPLITS_MAX;
-    return S < 1 ? 1 : S;
+    return S < 1 ? 1 : (int)S;
 }
 
 cudaError_t bias_grad(const void* dy, int dy_bf16, int nhwc, float* db, float beta, int N, int O, int P, float* part,
@@ -261,7 +269,7 @@ cudaError_t bias_grad(const void* dy, int dy_bf16, int nhwc, float* db, float be
         bias_partial_nchw<<<dim3(S, O), 256, 0, s>>>(dy, dy_bf16, O, P, N, R, part);
     }
     note_launch();
-    bias_final<<<(O + 255) / 256, 256, 0, s>>>(part, S, O, db, beta);
+    bias_final<<<O, 128, 0, s>>>(part, S, O, db, beta);
     note_launch();
     return cudaGetLastError();
 }

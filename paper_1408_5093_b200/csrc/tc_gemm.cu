@@ -1,9 +1,9 @@
 // tc_gemm.cu -- the tensor-core core of the hot path: one persistent, warp-specialised
-// tcgen05 GEMM whose operand loaders understand convolution (TMA im2col mode over packed
-// NHWC activations) as well as plain 2-D tiles.  The same kernel serves
-//   conv forward            (A = im2col(X) K-major, B = repacked W K-major, NCHW epilogue, bias+ReLU)
+// tcgen05 GEMM whose operand loaders understand convolution (TMA im2col mode over channels-last
+// activations) as well as plain 2-D tiles.  The same kernel serves
+//   conv forward            (A = im2col(X) K-major, B = repacked W K-major, epilogue bias+ReLU)
 //   conv backward-data s=1  (A = im2col(dY) with pad k-1-p K-major, B = flipped W^T K-major)
-//   conv backward-weight    (A = im2col(X) MN-major, B = dY NHWC MN-major, split-K partials)
+//   conv backward-weight    (A = im2col(X) MN-major, B = dY MN-major, split-K FP32 partials)
 //   inner product f/d/w     (plain 2-D tiles, K- or MN-major)
 // Paper: the conv layer's forward/backward contract P:156 (Sec. 3.2); formulas S:145.
 //
@@ -12,6 +12,11 @@
 //   warp 1 lane 0 : tcgen05.mma issuer    (accumulator double buffer in TMEM)
 //   warp 2        : TMEM allocator
 //   warps 4..7    : epilogue (tcgen05.ld -> bias/ReLU/beta -> global), TMEM lanes 32*(w-4)..
+// CG = 2 runs the CTA-pair form: a cluster of 2 CTAs computes a 256-row tile with
+// tcgen05.mma.cta_group::2 (issued by the leader CTA); each CTA stages its own 128 rows of A and
+// half of the B tile, so per-SM shared-memory operand traffic for B is halved.  TMA completions of
+// both CTAs land on the leader's full barrier; MMA commits are multicast to both CTAs; both
+// epilogues release the accumulator on the leader's barrier.
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -30,13 +35,14 @@ size_t tc_smem_bytes(const TcArgs& a) {
     return (size_t)a.stages * (A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + SMEM_ALIGN;
 }
 
-template <int ESZ, int AMODE, int BMODE, int EPI>
+template <int ESZ, int AMODE, int BMODE, int EPI, int CG>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const TcArgs args) {
     constexpr int CH = 128 / ESZ;          // elements per 128-byte row (= K per stage, = MN per chunk)
     constexpr int UMMA_K = 32 / ESZ;       // K per tcgen05.mma
     constexpr int KSTEPS = CH / UMMA_K;    // MMAs per stage (4)
+    constexpr int TM = BM * CG;            // rows of a work tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + SMEM_ALIGN - 1) &
                                                ~uintptr_t(SMEM_ALIGN - 1));
@@ -49,32 +55,40 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapA);
         tma_prefetch(&mapB);
         for (int i = 0; i < stages; i++) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&full[i], CG);          // leader: own arrive(+tx) and the peer's arrive
+            mbar_init(&empty[i], 1);          // one (multicast) MMA commit
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 128);
+            mbar_init(&tempty[i], 128 * CG);  // every epilogue thread of the pair
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_holder, args.tmem_cols);
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_cg2(tmem_holder, args.tmem_cols);
+        else tmem_alloc(tmem_holder, args.tmem_cols);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
     if (warp == 0 && lane == 0) {
-        // ===================== TMA producer =====================
+        // ===================== TMA producer (both CTAs) =====================
         int stage = 0;
         uint32_t phase = 0;
-        const uint32_t tx = A_STAGE_BYTES + (BMODE == B_TILED_K ? args.BN * 128 : args.b_nchunks * CH * 128);
-        for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+        const uint32_t tx = A_STAGE_BYTES + args.b_stage_bytes;   // bytes landing in THIS CTA per stage
+        const int bn_cta = args.BN / CG;                            // B rows (K-major) staged by this CTA
+        for (int u = cid; u < args.units; u += ncl) {
             int t = u;
             const int n_tile = t % args.n_tiles; t /= args.n_tiles;
             const int m_tile = t % args.m_tiles; t /= args.m_tiles;
@@ -82,10 +96,9 @@ __global__ void __launch_bounds__(256, 1)
             const int split = t / args.groups;
             const int kb0 = split * args.kb_per_split;
             const int kb1 = min(args.kblocks, kb0 + args.kb_per_split);
-            // per-tile A base for K-major im2col
+            const int m0 = m_tile * TM + (int)rank * BM;   // first row staged by this CTA
             int an = 0, ay = 0, ax = 0;
             if (AMODE == A_IM2COL_K) {
-                const int m0 = m_tile * BM;
                 an = m0 / args.a_P;
                 const int r = m0 - an * args.a_P;
                 ay = r / args.a_OW;
@@ -95,23 +108,29 @@ __global__ void __launch_bounds__(256, 1)
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * stage_bytes;
                 uint8_t* sb = sa + A_STAGE_BYTES;
-                mbar_arrive_expect_tx(&full[stage], tx);
+                if (CG == 1 || leader) mbar_arrive_expect_tx(&full[stage], tx * CG);
+                else mbar_arrive_cluster(mapa_shared(smem_u32(&full[stage]), 0));
                 // ---- A
                 if (AMODE == A_TILED_K) {
-                    tma_load_2d(sa, &mapA, &full[stage], kb * CH, g * args.a_row_g + m_tile * BM);
+                    if (CG == 2) tma_load_2d_cg2(sa, &mapA, &full[stage], kb * CH, g * args.a_row_g + m0);
+                    else tma_load_2d(sa, &mapA, &full[stage], kb * CH, g * args.a_row_g + m0);
                 } else if (AMODE == A_IM2COL_K) {
                     const int tap = kb / args.a_cblocks, cbk = kb - tap * args.a_cblocks;
                     const int i = tap / args.a_kw, j = tap - i * args.a_kw;
-                    tma_load_im2col_4d(sa, &mapA, &full[stage], g * args.a_cpg + cbk * CH, ax - args.a_pad_w,
-                                       ay - args.a_pad_h, an, (uint16_t)j, (uint16_t)i);
+                    if (CG == 2)
+                        tma_load_im2col_4d_cg2(sa, &mapA, &full[stage], g * args.a_cpg + cbk * CH, ax - args.a_pad_w,
+                                               ay - args.a_pad_h, an, (uint16_t)j, (uint16_t)i);
+                    else
+                        tma_load_im2col_4d(sa, &mapA, &full[stage], g * args.a_cpg + cbk * CH, ax - args.a_pad_w,
+                                           ay - args.a_pad_h, an, (uint16_t)j, (uint16_t)i);
                 } else if (AMODE == A_IM2COL_MN) {
-                    const int m0 = kb * CH;   // first pixel of this reduction block
-                    const int n0 = m0 / args.a_P;
-                    const int r = m0 - n0 * args.a_P;
+                    const int p0 = kb * CH;   // first pixel of this reduction block
+                    const int n0 = p0 / args.a_P;
+                    const int r = p0 - n0 * args.a_P;
                     const int y0 = r / args.a_OW, x0 = r - (r / args.a_OW) * args.a_OW;
 #pragma unroll
                     for (int q = 0; q < ESZ; q++) {   // 128 rows of M = ESZ chunks of CH
-                        int chunk = m_tile * ESZ + q;
+                        int chunk = (m_tile * CG + (int)rank) * ESZ + q;
                         if (chunk >= args.a_nchunks_total) chunk = args.a_nchunks_total - 1;  // rows discarded
                         const int tap = chunk / args.a_cblocks, cbk = chunk - tap * args.a_cblocks;
                         const int i = tap / args.a_kw, j = tap - i * args.a_kw;
@@ -121,12 +140,13 @@ __global__ void __launch_bounds__(256, 1)
                 } else {  // A_TILED_MN
 #pragma unroll
                     for (int q = 0; q < ESZ; q++)
-                        tma_load_2d(sa + q * CH * 128, &mapA, &full[stage], g * args.a_row_g + m_tile * BM + q * CH,
-                                    kb * CH);
+                        tma_load_2d(sa + q * CH * 128, &mapA, &full[stage], g * args.a_row_g + m0 + q * CH, kb * CH);
                 }
                 // ---- B
                 if (BMODE == B_TILED_K) {
-                    tma_load_2d(sb, &mapB, &full[stage], kb * CH, g * args.b_row_g + n_tile * args.BN);
+                    const int row = g * args.b_row_g + n_tile * args.BN + (int)rank * bn_cta;
+                    if (CG == 2) tma_load_2d_cg2(sb, &mapB, &full[stage], kb * CH, row);
+                    else tma_load_2d(sb, &mapB, &full[stage], kb * CH, row);
                 } else {
                     for (int q = 0; q < args.b_nchunks; q++)
                         tma_load_2d(sb + q * CH * 128, &mapB, &full[stage],
@@ -135,19 +155,20 @@ __global__ void __launch_bounds__(256, 1)
                 if (++stage == stages) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ===================== MMA issuer =====================
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ===================== MMA issuer (leader CTA) =====================
         // instruction descriptor: D=f32, A/B format (bf16=1, tf32=2), majors, N>>3, M>>4
         const uint32_t fmt = (ESZ == 2) ? 1u : 2u;
         const uint32_t a_mn = (AMODE == A_IM2COL_MN || AMODE == A_TILED_MN) ? 1u : 0u;
         const uint32_t b_mn = (BMODE == B_TILED_MN) ? 1u : 0u;
         const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn << 15) | (b_mn << 16) |
-                               ((uint32_t)(args.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                               ((uint32_t)(args.BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+        int iters = 0;
+        for (int u = cid; u < args.units; u += ncl, iters++) {
             int t = u / (args.n_tiles * args.m_tiles);
             const int split = t / args.groups;
             const int kb0 = split * args.kb_per_split;
@@ -167,22 +188,32 @@ __global__ void __launch_bounds__(256, 1)
                     else      ad = smem_desc_sw128(sa + k * 32, 16, 1024);
                     if (b_mn) bd = smem_desc_sw128(sb + k * UMMA_K * 128, CH * 128, 1024);
                     else      bd = smem_desc_sw128(sb + k * 32, 16, 1024);
-                    umma<ESZ>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    if (CG == 2) umma_cg2<ESZ>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    else umma<ESZ>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                 }
-                umma_commit(&empty[stage]);
+                if (CG == 2) umma_commit_cg2(&empty[stage]);
+                else umma_commit(&empty[stage]);
                 if (++stage == stages) { stage = 0; phase ^= 1; }
             }
-            umma_commit(&tfull[acc]);
+            if (CG == 2) umma_commit_cg2(&tfull[acc]);
+            else umma_commit(&tfull[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        // the peer's epilogue arrives remotely on our tempty barriers: drain the last two phases
+        // before the pair tears down
+        if (CG == 2) {
+            for (int j = iters - 2; j < iters; j++)
+                if (j >= 0) mbar_wait(&tempty[j & 1], (uint32_t)((j >> 1) & 1));
+        }
     } else if (warp >= 4) {
-        // ===================== epilogue =====================
+        // ===================== epilogue (both CTAs) =====================
         const int q = warp - 4;
         const int row = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        for (int u = cid; u < args.units; u += ncl) {
             int t = u;
             const int n_tile = t % args.n_tiles; t /= args.n_tiles;
             const int m_tile = t % args.m_tiles; t /= args.m_tiles;
@@ -191,16 +222,16 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * args.acc_stride;
             if (EPI == EPI_PARTIAL) {
-                float* dst = args.partial + (size_t)u * args.BN * BM + row;
+                float* dst = args.partial + (size_t)u * args.BN * TM + (int)rank * BM + row;
                 for (int c0 = 0; c0 < args.BN; c0 += 16) {
                     uint32_t v[16];
                     tmem_ld16(taddr + c0, v);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 16; j++) dst[(size_t)(c0 + j) * BM] = __uint_as_float(v[j]);
+                    for (int j = 0; j < 16; j++) dst[(size_t)(c0 + j) * TM] = __uint_as_float(v[j]);
                 }
             } else {
-                const int m = m_tile * BM + row;
+                const int m = m_tile * TM + (int)rank * BM + row;
                 const bool row_ok = m < args.M;
                 const int img = m / args.P, pix = m - img * args.P;
                 const long long rbase = (long long)img * args.s_n + (long long)pix * args.s_p;
@@ -297,15 +328,19 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
+            else mbar_arrive(&tempty[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
     }
-    __syncthreads();
+    tc_fence_before();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, args.tmem_cols);
+        if (CG == 2) tmem_dealloc_cg2(tmem_base, args.tmem_cols);
+        else tmem_dealloc(tmem_base, args.tmem_cols);
     }
 }
 
@@ -321,28 +356,47 @@ int num_sms() {
     return n;
 }
 
-template <int ESZ, int AM, int BMd, int EP>
+template <int ESZ, int AM, int BMd, int EP, int CG>
 static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
-    auto kern = tc_gemm_kernel<ESZ, AM, BMd, EP>;
+    auto kern = tc_gemm_kernel<ESZ, AM, BMd, EP, CG>;
     const size_t smem = tc_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+    if (CG == 1) {
+        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(L.grid);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CG;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.args);
+        if (e != cudaSuccess) return e;
+    }
     note_launch();
     return cudaGetLastError();
 }
 
-#define TC_CASE(E, A, B, P)                                                          \
-    if (L.esz == E && L.amode == A && L.bmode == B && L.epi == P) return launch_one<E, A, B, P>(L, s);
+#define TC_CASE(E, A, B, P, G)                                                                   \
+    if (L.esz == E && L.amode == A && L.bmode == B && L.epi == P && L.cg == G) return launch_one<E, A, B, P, G>(L, s);
 
 cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s) {
-    TC_CASE(2, A_IM2COL_K, B_TILED_K, EPI_STRIDED)
-    TC_CASE(2, A_IM2COL_MN, B_TILED_MN, EPI_PARTIAL)
-    TC_CASE(2, A_TILED_K, B_TILED_K, EPI_STRIDED)
-    TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_STRIDED)
-    TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED)
-    TC_CASE(4, A_IM2COL_K, B_TILED_K, EPI_STRIDED)
-    TC_CASE(4, A_TILED_K, B_TILED_K, EPI_STRIDED)
+    TC_CASE(2, A_IM2COL_K, B_TILED_K, EPI_STRIDED, 1)
+    TC_CASE(2, A_IM2COL_K, B_TILED_K, EPI_STRIDED, 2)
+    TC_CASE(2, A_IM2COL_MN, B_TILED_MN, EPI_PARTIAL, 1)
+    TC_CASE(2, A_TILED_K, B_TILED_K, EPI_STRIDED, 1)
+    TC_CASE(2, A_TILED_K, B_TILED_K, EPI_STRIDED, 2)
+    TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_STRIDED, 1)
+    TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 1)
+    TC_CASE(4, A_IM2COL_K, B_TILED_K, EPI_STRIDED, 1)
+    TC_CASE(4, A_TILED_K, B_TILED_K, EPI_STRIDED, 1)
     return cudaErrorInvalidValue;
 }
 

@@ -172,6 +172,32 @@ def test_conv_nhwc_bf16_storage(oracle, case, math):
     np.testing.assert_array_equal(host(Y16), oracle.quant_bf16(host(Y)))
 
 
+@pytest.mark.parametrize("cta", [1, 2])
+@pytest.mark.parametrize("case", CASES + [(4, 64, 27, 27, 192, (3, 3), (1, 1), (1, 1), 1)],
+                         ids=IDS + ["N4C64H27O192"])
+def test_conv_cta_pair_modes(oracle, case, cta):
+    """The single-CTA (M=128) and CTA-pair (tcgen05 cta_group::2, M=256) tensor-core tiles give the
+    same parity for forward and data gradient, for every geometry (forced via caffe_set_tuning)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 6)
+    q = oracle.quant_bf16
+    cl = torch.channels_last
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, cta)
+    try:
+        Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+        Y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True, out_dtype=torch.float32)
+        assert_tc_close(host(Y), oracle.conv_forward(host(Xd), q(Wt), b, stride=s, pad=p, group=g, relu=True),
+                        f"fwd cta={cta}")
+        dX = cb.conv_backward_data(cuda(dY), cuda(Wt), X.shape, stride=s, pad=p, group=g)
+        assert_tc_close(host(dX), oracle.conv_backward_data(q(dY), q(Wt), X.shape, stride=s, pad=p, group=g),
+                        f"dgrad cta={cta}")
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
+
+
 @pytest.mark.parametrize("dy_layout", ["nchw_f32", "nhwc_f32", "nhwc_bf16"])
 def test_caffenet_conv1_full_image_wgrad(oracle, dy_layout):
     """conv1 at its real geometry (227x227, 11x11/s4, space-to-depth path), 2 images, every dY layout."""

@@ -46,6 +46,18 @@ def main():
     torch.manual_seed(0)
     dev = torch.device("cuda")
     out = {}
+    if "--cta" in sys.argv:
+        from paper_1408_5093_b200 import _abi
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, int(sys.argv[sys.argv.index("--cta") + 1]))
+    if "--only-conv3" in sys.argv:  # for ncu: a few launches of conv3 forward
+        cl = torch.channels_last
+        x = torch.randn(256, 256, 13, 13, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+        w = torch.randn(384, 256, 3, 3, device=dev) * 0.05
+        y = cb.conv_forward(x, w, None, 1, 1, 1, relu=True)
+        for _ in range(3):
+            cb.conv_forward(x, w, None, 1, 1, 1, relu=True, out=y)
+        torch.cuda.synchronize()
+        return
     if "--only-gemm" in sys.argv:   # for ncu: a few launches of one plain GEMM
         M, N, K = 65536, 256, 1152
         x = torch.randn(M, K, device=dev).to(torch.bfloat16)
