@@ -118,6 +118,9 @@ caffe_status caffe_device_check(void);
    CAFFE_TUNE_CTA_PAIR: 0 = automatic (default), 1 = force single-CTA M=128 tensor-core tiles,
    2 = force CTA-pair M=256 tiles (tcgen05 cta_group::2) where the kernel supports them. */
 #define CAFFE_TUNE_CTA_PAIR 1
+/* CAFFE_TUNE_MMA_SPIN: 0 (default) = the MMA-issuing thread waits on its stage barrier with the
+   suspending try_wait, 1 = it polls (test_wait). */
+#define CAFFE_TUNE_MMA_SPIN 2
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -202,6 +202,7 @@ int choose_bn(int n) {
 }
 // CTA pairs (M=256 tiles, cta_group::2) whenever the pair-tiles still fill every SM pair once.
 int g_force_cg = 0;   // caffe_set_tuning(CAFFE_TUNE_CTA_PAIR, 1|2) overrides the automatic choice
+int g_mma_spin = 0;   // CAFFE_TUNE_MMA_SPIN (polling measured slower: it steals issue slots from the epilogue)
 int pick_cg(long long M, int ntiles_x_groups, int E) {
     if (E != 2) return 1;
     if (g_force_cg == 1 || g_force_cg == 2) return g_force_cg;
@@ -292,6 +293,7 @@ caffe_status check_ws(void* ws, size_t have, size_t need) {
 // kind: 0 = convolution pass, 1 = inner product; flops = algorithmic FLOPs of the call
 caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     if (L.cg < 1) L.cg = 1;
+    L.args.spin = g_mma_spin;
     const int slots = num_sms() / L.cg;                  // CTAs (or CTA pairs) resident at once
     L.grid = (L.args.units < slots ? L.args.units : slots) * L.cg;
     ProfRec rec{nullptr, nullptr, flops, kind};
@@ -357,6 +359,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     if (key == CAFFE_TUNE_CTA_PAIR) {
         if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "CTA-pair mode must be 0 (auto), 1 or 2");
         g_force_cg = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_MMA_SPIN) {
+        g_mma_spin = value ? 1 : 0;
         return CAFFE_OK;
     }
     return fail(CAFFE_E_INVALID, "unknown tuning key %d", key);

@@ -38,6 +38,7 @@ struct TcArgs {
     int relu;
     float beta;
     float* partial;                     // EPI_PARTIAL: [unit][BN][128] fp32
+    int spin;                           // MMA thread polls (test_wait) instead of try_wait
 };
 
 struct TcLaunch {

@@ -32,7 +32,8 @@ constexpr int A_STAGE_BYTES = 16384;   // 128 rows x 128 B
 constexpr int SMEM_ALIGN = 1024;
 
 size_t tc_smem_bytes(const TcArgs& a) {
-    return (size_t)a.stages * (A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + SMEM_ALIGN;
+    return (size_t)a.stages * (A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + 2 * 256 * 4 /*bias*/ +
+           SMEM_ALIGN;
 }
 
 template <int ESZ, int AMODE, int BMODE, int EPI, int CG>
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tfull = empty + stages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* sbias = reinterpret_cast<float*>(smem + stages * stage_bytes + 256);   // [2][256]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -177,7 +179,8 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * args.acc_stride;
             for (int kb = kb0; kb < kb1; kb++) {
-                mbar_wait(&full[stage], phase);
+                if (args.spin) mbar_wait_spin(&full[stage], phase);
+                else mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 const uint32_t sa = smem_u32(smem + stage * stage_bytes);
                 const uint32_t sb = sa + A_STAGE_BYTES;
@@ -236,27 +239,32 @@ __global__ void __launch_bounds__(256, 1)
                 const int img = m / args.P, pix = m - img * args.P;
                 const long long rbase = (long long)img * args.s_n + (long long)pix * args.s_p;
                 const int col0 = n_tile * args.BN;
+                const int cbase = g * args.col_g + col0;   // output channel of tile column 0
                 const bool rowvec = args.s_c == 1;        // channels-last / row-major output
                 const bool bf = args.out_bf16 != 0;
                 const float beta = args.beta;
                 const int relu = args.relu;
-                for (int c0 = 0; c0 < args.BN; c0 += 16) {
-                    if (col0 + c0 >= args.N) break;  // warp-uniform
-                    uint32_t v[16];
-                    tmem_ld16(taddr + c0, v);
-                    tmem_wait_ld();
-                    if (!row_ok) continue;
-                    const int cb = g * args.col_g + col0 + c0;   // first output channel of this chunk
+                // stage this tile's bias once (double-buffered by accumulator: a warp can be at most
+                // one tile ahead of the slowest epilogue warp)
+                float* bs = sbias + acc * 256;
+                if (args.bias) {
+                    for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                }
+                auto emit16 = [&](const uint32_t (&v)[16], int c0) {
                     const int nvalid = min(16, args.N - (col0 + c0));
                     float x[16];
 #pragma unroll
                     for (int j = 0; j < 16; j++) x[j] = __uint_as_float(v[j]);
                     if (args.bias) {
+                        const float4* b4 = reinterpret_cast<const float4*>(bs + c0);
 #pragma unroll
-                        for (int j = 0; j < 16; j++)
-                            if (j < nvalid) x[j] += __ldg(args.bias + cb + j);
+                        for (int q4 = 0; q4 < 4; q4++) {
+                            const float4 b = b4[q4];
+                            x[4 * q4] += b.x; x[4 * q4 + 1] += b.y; x[4 * q4 + 2] += b.z; x[4 * q4 + 3] += b.w;
+                        }
                     }
-                    const long long off0 = rbase + (long long)cb * args.s_c;
+                    const long long off0 = rbase + (long long)(cbase + c0) * args.s_c;
                     if (rowvec && nvalid == 16 && (off0 & (bf ? 7 : 3)) == 0) {
                         if (bf) {
                             uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off0);
@@ -325,6 +333,18 @@ __global__ void __launch_bounds__(256, 1)
                             }
                         }
                     }
+                };
+                // two 16-column TMEM loads in flight per wait
+                for (int c0 = 0; c0 < args.BN; c0 += 32) {
+                    if (col0 + c0 >= args.N) break;  // warp-uniform
+                    const bool two = c0 + 16 < args.BN && col0 + c0 + 16 < args.N;
+                    uint32_t v0[16], v1[16];
+                    tmem_ld16(taddr + c0, v0);
+                    if (two) tmem_ld16(taddr + c0 + 16, v1);
+                    tmem_wait_ld();
+                    if (!row_ok) continue;
+                    emit16(v0, c0);
+                    if (two) emit16(v1, c0 + 16);
                 }
             }
             tc_fence_before();

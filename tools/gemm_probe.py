@@ -46,6 +46,9 @@ def main():
     torch.manual_seed(0)
     dev = torch.device("cuda")
     out = {}
+    if "--spin" in sys.argv:
+        from paper_1408_5093_b200 import _abi
+        _abi.call("caffe_set_tuning", 2, int(sys.argv[sys.argv.index("--spin") + 1]))
     if "--cta" in sys.argv:
         from paper_1408_5093_b200 import _abi
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, int(sys.argv[sys.argv.index("--cta") + 1]))
