@@ -121,6 +121,9 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_MMA_SPIN: 0 (default) = the MMA-issuing thread waits on its stage barrier with the
    suspending try_wait, 1 = it polls (test_wait). */
 #define CAFFE_TUNE_MMA_SPIN 2
+/* CAFFE_TUNE_WGRAD_MACC: 128-row M tiles per weight-gradient work unit (top_diff staged once for
+   all of them); 0 = automatic (default), 1..4 forced. */
+#define CAFFE_TUNE_WGRAD_MACC 3
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation
@@ -196,6 +199,14 @@ caffe_status caffe_pool_forward(const caffe_pool_desc* desc, const caffe_blob* b
                                 caffe_blob* mask, caffe_stream_t stream);
 caffe_status caffe_pool_backward(const caffe_pool_desc* desc, const caffe_blob* top_diff, const caffe_blob* mask,
                                  caffe_blob* bottom_diff, caffe_stream_t stream);
+/* MAX pool backward fused with the backward of the ReLU that produced the pool's bottom
+   (conv -> ReLU -> MAX pool, S:196-213 then S:160-177):
+   bottom_diff = relu_backward(bottom, pool_backward(top_diff)).  Since the window max `top`
+   equals the ReLU output at its argmax, a window passes its gradient iff top > 0 -- the same
+   result, bit for bit, as caffe_pool_backward followed by caffe_relu_backward.  `top` is the
+   pool forward output (shape, dtype and layout of top_diff).  AVE pooling is CAFFE_E_INVALID. */
+caffe_status caffe_pool_relu_backward(const caffe_pool_desc* desc, const caffe_blob* top, const caffe_blob* top_diff,
+                                      const caffe_blob* mask, caffe_blob* bottom_diff, caffe_stream_t stream);
 
 /* ------------------------------------------------------------------ LRN (R9)
    S = k + alpha/n * sum_{c' in [c-r, c+r] clipped} x^2, r=(n-1)/2;  top = bottom * S^-beta.

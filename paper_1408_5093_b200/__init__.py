@@ -252,6 +252,18 @@ def pool_backward(dy, mask, in_shape, method, kernel, stride, pad=0, out=None):
     return out
 
 
+def pool_relu_backward(top, dy, mask, in_shape, kernel, stride, pad=0, out=None):
+    """MAX-pool backward fused with the backward of the ReLU feeding the pool (caffe_pool_relu_backward):
+    equals relu_backward(bottom, pool_backward(dy)) bit for bit; `top` is the pool forward output."""
+    d = _pool_desc("max", kernel, stride, pad)
+    if out is None:
+        out = empty_like_layout(in_shape, dy.dtype, dy.device, like=dy)
+    bt, bdy, bm, bdx = blob(top), blob(dy), blob(mask), blob(out)
+    call("caffe_pool_relu_backward", ctypes.byref(d), ctypes.byref(bt), ctypes.byref(bdy), ctypes.byref(bm),
+         ctypes.byref(bdx), _stream())
+    return out
+
+
 # ------------------------------------------------------------------ LRN
 def lrn_forward(x, local_size=5, alpha=1e-4, beta=0.75, k=1.0, out=None, scale=None, want_scale=False):
     torch = _t()

@@ -22,6 +22,8 @@ CAFFE_FUSE_RELU = 1
 CAFFE_POOL_MAX, CAFFE_POOL_AVE = 0, 1
 CAFFE_PASS_FORWARD, CAFFE_PASS_BACKWARD_DATA, CAFFE_PASS_BACKWARD_WEIGHT = 0, 1, 2
 CAFFE_TUNE_CTA_PAIR = 1
+CAFFE_TUNE_MMA_SPIN = 2
+CAFFE_TUNE_WGRAD_MACC = 3
 
 
 class Shape4(ctypes.Structure):
@@ -72,6 +74,7 @@ SIGNATURES = {
     "caffe_pool_output_shape": [PD, Shape4, P(Shape4)],
     "caffe_pool_forward": [PD, B, B, B, vp],
     "caffe_pool_backward": [PD, B, B, B, vp],
+    "caffe_pool_relu_backward": [PD, B, B, B, B, vp],
     "caffe_lrn_forward": [LD, B, B, B, vp],
     "caffe_lrn_backward": [LD, B, B, B, B, B, vp],
     "caffe_ip_workspace_size": [ctypes.c_int, Shape4, i32, i32, P(sz)],

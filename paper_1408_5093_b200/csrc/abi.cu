@@ -216,11 +216,15 @@ int pow2ceil(int x) {
 }
 void finish_args(TcArgs& a, int bstage) {
     a.b_stage_bytes = bstage;
-    const int stage = 16384 + bstage;
+    const int macc = a.macc > 1 ? a.macc : 1;
+    const int stage = macc * 16384 + bstage;
     a.stages = (200 * 1024) / stage;
     if (a.stages > 8) a.stages = 8;
     a.acc_stride = pow2ceil(a.BN);
-    a.tmem_cols = 2 * a.acc_stride;
+    // two accumulator buffers when they fit in the 512 TMEM columns, else one
+    a.tmem_cols = 2 * macc * a.acc_stride <= 512 ? 2 * macc * a.acc_stride : macc * a.acc_stride;
+    if (a.tmem_cols < 32) a.tmem_cols = 32;
+    a.tmem_cols = pow2ceil(a.tmem_cols);
     a.units = a.m_tiles * a.n_tiles * a.groups * a.splits;
 }
 void set_out(TcArgs& a, const caffe_blob* b) {
@@ -235,7 +239,9 @@ void set_out(TcArgs& a, const caffe_blob* b) {
 
 struct WgradSplit {
     int m_tiles, n_tiles, BN, splits, kb_per, kblocks;
+    int macc, m_groups;   // accumulators (M tiles) per work unit and the resulting unit rows
 };
+int g_wgrad_macc = 0;     // CAFFE_TUNE_WGRAD_MACC: 0 = automatic, 1..4 forced
 WgradSplit wgrad_split(const Plan& p) {
     WgradSplit w;
     const int nchunks = p.taps * (p.Cgp / p.CH);
@@ -244,9 +250,28 @@ WgradSplit wgrad_split(const Plan& p) {
     w.BN = choose_bn(p.Og);
     w.n_tiles = (int)cdiv(p.Og, w.BN);
     w.kblocks = (int)cdiv((long long)p.N * p.OH * p.OW, p.CH);
+    // Several M tiles per unit stage dY (the B operand, re-read once per unit) once for all of
+    // them: the most accumulators that fit the 512 TMEM columns (single-buffered when two sets do
+    // not fit -- measured faster than fewer, double-buffered accumulators: the units are long)
+    // with stages still 3 deep in shared memory.
+    const int accs = pow2ceil(w.BN);
+    const int bstage = (int)cdiv(w.BN, p.CH) * p.CH * 128;
+    w.macc = 1;
+    if (g_wgrad_macc >= 1) {
+        w.macc = g_wgrad_macc;
+        while (w.macc > 1 && (w.macc * accs > 512 || (200 * 1024) / (w.macc * 16384 + bstage) < 2)) w.macc--;
+    } else {
+        for (int m = 2; m <= 4; m++) {
+            if (m * accs > 512 || (200 * 1024) / (m * 16384 + bstage) < 3) break;
+            w.macc = m;
+        }
+    }
+    if (w.macc > w.m_tiles) w.macc = w.m_tiles;
+    if (p.E != 2) w.macc = 1;
+    w.m_groups = (int)cdiv(w.m_tiles, w.macc);
     // Split the pixel reduction so that (tiles x splits) work units fill the SMs in whole waves:
     // maximise wave efficiency x split balance x kb/(kb + 2) (per-unit prologue/epilogue cost).
-    const int tiles = w.m_tiles * w.n_tiles * p.G;
+    const int tiles = w.m_groups * w.n_tiles * p.G;
     const int sms = 148;
     double best = -1.0;
     w.kb_per = w.kblocks;
@@ -363,6 +388,11 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     }
     if (key == CAFFE_TUNE_MMA_SPIN) {
         g_mma_spin = value ? 1 : 0;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_WGRAD_MACC) {
+        if (value < 0 || value > 4) return fail(CAFFE_E_PARAM, "weight-gradient accumulators per unit must be 0 (auto) .. 4");
+        g_wgrad_macc = value;
         return CAFFE_OK;
     }
     return fail(CAFFE_E_INVALID, "unknown tuning key %d", key);
@@ -605,7 +635,8 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (wgrad top_diff)");
     TcArgs& a = L.args;
     a.BN = w.BN; a.M = 128 * w.m_tiles; a.N = p.Og;
-    a.m_tiles = w.m_tiles; a.n_tiles = w.n_tiles; a.groups = p.G; a.splits = w.splits;
+    a.m_tiles = w.m_groups; a.m_tiles_real = w.m_tiles; a.macc = w.macc;
+    a.n_tiles = w.n_tiles; a.groups = p.G; a.splits = w.splits;
     a.kblocks = w.kblocks; a.kb_per_split = w.kb_per;
     a.a_P = p.OH * p.OW; a.a_OW = p.OW; a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_kw = p.kwp;
     a.a_cblocks = p.Cgp / p.CH; a.a_cpg = A.cpg; a.a_nchunks_total = p.taps * (p.Cgp / p.CH);
@@ -705,8 +736,8 @@ caffe_status caffe_pool_forward(const caffe_pool_desc* desc, const caffe_blob* b
     return CAFFE_OK;
 }
 
-caffe_status caffe_pool_backward(const caffe_pool_desc* desc, const caffe_blob* top_diff, const caffe_blob* mask,
-                                 caffe_blob* bottom_diff, caffe_stream_t stream) {
+static caffe_status pool_backward_impl(const caffe_pool_desc* desc, const caffe_blob* top, const caffe_blob* top_diff,
+                                       const caffe_blob* mask, caffe_blob* bottom_diff, caffe_stream_t stream) {
     caffe_status st;
     if ((st = check_blob(top_diff, "top_diff")) || (st = check_blob(bottom_diff, "bottom_diff"))) return st;
     PoolGeom g;
@@ -720,17 +751,35 @@ caffe_status caffe_pool_backward(const caffe_pool_desc* desc, const caffe_blob* 
         if (!same_shape(mask->shape, want) || mask->layout != top_diff->layout)
             return fail(CAFFE_E_SHAPE, "mask shape/layout must equal top_diff's");
     }
+    if (top) {
+        if (desc->method != CAFFE_POOL_MAX) return fail(CAFFE_E_INVALID, "the ReLU-fused backward needs MAX pooling");
+        if ((st = check_blob(top, "top"))) return st;
+        if (!same_shape(top->shape, want) || top->dtype != top_diff->dtype || top->layout != top_diff->layout)
+            return fail(CAFFE_E_SHAPE, "top must match top_diff (shape, dtype, layout)");
+        if (overlap(bottom_diff, top)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps top");
+    }
     if (overlap(bottom_diff, top_diff) || overlap(bottom_diff, mask)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
     if (g.N == 0) return CAFFE_OK;
     if (desc->method == CAFFE_POOL_MAX)
-        CK(maxpool_bwd(top_diff->ptr, (const int32_t*)mask->ptr, strides(top_diff), bottom_diff->ptr, nhwc(bottom_diff),
-                       isbf(top_diff), g, (cudaStream_t)stream),
+        CK(maxpool_bwd(top_diff->ptr, (const int32_t*)mask->ptr, top ? top->ptr : nullptr, strides(top_diff),
+                       bottom_diff->ptr, nhwc(bottom_diff), isbf(top_diff), g, (cudaStream_t)stream),
            "maxpool bwd");
     else
         CK(avepool_bwd(top_diff->ptr, strides(top_diff), bottom_diff->ptr, nhwc(bottom_diff), isbf(top_diff), g,
                        (cudaStream_t)stream),
            "avepool bwd");
     return CAFFE_OK;
+}
+
+caffe_status caffe_pool_backward(const caffe_pool_desc* desc, const caffe_blob* top_diff, const caffe_blob* mask,
+                                 caffe_blob* bottom_diff, caffe_stream_t stream) {
+    return pool_backward_impl(desc, nullptr, top_diff, mask, bottom_diff, stream);
+}
+
+caffe_status caffe_pool_relu_backward(const caffe_pool_desc* desc, const caffe_blob* top, const caffe_blob* top_diff,
+                                      const caffe_blob* mask, caffe_blob* bottom_diff, caffe_stream_t stream) {
+    if (!top) return fail(CAFFE_E_INVALID, "top is NULL");
+    return pool_backward_impl(desc, top, top_diff, mask, bottom_diff, stream);
 }
 
 // ------------------------------------------------------------------ LRN
@@ -807,6 +856,39 @@ static caffe_status ip_shapes(const caffe_blob* bottom, const caffe_blob* weight
     return CAFFE_OK;
 }
 
+// Split-K plan of an inner-product GEMM with M rows, Ncols columns and Kred reduction elements
+// (kchunk per 128-byte block): the fc layers have few (M, N) tiles at batch 256, so the reduction
+// is split until the units fill the SMs once; partials are reduced in a fixed order.
+struct IpPlan {
+    int BN, m_tiles, n_tiles, kblocks, splits, kb_per;
+    size_t part_bytes;
+};
+static IpPlan ip_plan(long long M, long long Ncols, long long Kred, int kchunk, int BN) {
+    IpPlan q;
+    q.BN = BN;
+    q.m_tiles = (int)cdiv(M, 128);
+    q.n_tiles = (int)cdiv(Ncols, BN);
+    q.kblocks = (int)cdiv(Kred, kchunk);
+    q.splits = 1;
+    q.kb_per = q.kblocks;
+    const long long tiles = (long long)q.m_tiles * q.n_tiles;
+    const int sms = 148;
+    if (tiles < sms / 2) {
+        int sp = (int)(sms / tiles);
+        if (sp > q.kblocks / 4) sp = q.kblocks / 4;
+        if (sp > 1) {
+            q.kb_per = (int)cdiv(q.kblocks, sp);
+            q.splits = (int)cdiv(q.kblocks, q.kb_per);
+        }
+    }
+    q.part_bytes = q.splits > 1 ? align1k((size_t)q.splits * tiles * BN * 128 * 4) : 0;
+    return q;
+}
+static IpPlan ip_plan_fwd(long long N, long long K, int O, int E) { return ip_plan(N, O, K, 128 / E, choose_bn(O)); }
+static IpPlan ip_plan_dgrad(long long N, long long K, int O) {
+    return ip_plan(N, K, O, 64, choose_bn((int)(K < 256 ? K : 256)));
+}
+
 caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32_t O, int32_t pass, size_t* bytes) {
     if (!bytes) return fail(CAFFE_E_INVALID, "bytes is NULL");
     if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16 && math != CAFFE_MATH_TF32) return fail(CAFFE_E_INVALID, "bad math mode");
@@ -814,9 +896,12 @@ caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32
     size_t bias = align1k((size_t)bias_grad_splits((int)N, O, 1) * O * 4);
     if (math == CAFFE_MATH_FP32) { *bytes = pass == CAFFE_PASS_BACKWARD_WEIGHT ? bias : 0; return CAFFE_OK; }
     const int E = math == CAFFE_MATH_TF32 ? 4 : 2, CHh = 128 / E;
-    // worst case: every operand staged (+ fp32 rows for an NHWC data gradient) + bias partials
+    size_t part = 0;
+    if (pass == CAFFE_PASS_FORWARD && N > 0 && O > 0 && K > 0) part = ip_plan_fwd(N, K, O, E).part_bytes;
+    if (pass == CAFFE_PASS_BACKWARD_DATA && N > 0 && O > 0 && K > 0) part = ip_plan_dgrad(N, K, O).part_bytes;
+    // worst case: every operand staged (+ fp32 rows for an NHWC data gradient) + bias partials + split-K partials
     *bytes = align1k((size_t)N * rup(K, CHh) * E) + align1k((size_t)O * rup(K, CHh) * E) +
-             align1k((size_t)N * rup(O, CHh) * E) + align1k((size_t)N * K * 4) + bias;
+             align1k((size_t)N * rup(O, CHh) * E) + align1k((size_t)N * K * 4) + bias + part;
     return CAFFE_OK;
 }
 
@@ -881,18 +966,26 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
     CK(stage_rows(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
     TcLaunch L;
     memset(&L, 0, sizeof L);
-    L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
+    const IpPlan q = ip_plan_fwd(N, K, O, E);
+    float* part = nullptr;
+    if (q.splits > 1) { part = (float*)cur; cur += q.part_bytes; }
+    L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_K; L.epi = q.splits > 1 ? EPI_PARTIAL : EPI_STRIDED;
     TcArgs& a = L.args;
-    a.BN = choose_bn(O);
+    a.BN = q.BN;
     if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 128 / E, 128) ||
         !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 128 / E, a.BN))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip fwd)");
-    a.M = N; a.N = O; a.m_tiles = (int)cdiv(N, 128); a.n_tiles = (int)cdiv(O, a.BN); a.groups = 1; a.splits = 1;
-    a.kblocks = (int)cdiv(K, 128 / E); a.kb_per_split = a.kblocks;
+    a.M = N; a.N = O; a.m_tiles = q.m_tiles; a.n_tiles = q.n_tiles; a.groups = 1; a.splits = q.splits;
+    a.kblocks = q.kblocks; a.kb_per_split = q.kb_per;
     a.out = top->ptr; a.out_bf16 = isbf(top); a.s_n = O; a.s_c = 1; a.s_p = 0; a.P = 1; a.col_g = 0;
-    a.bias = bptr; a.relu = relu; a.beta = 0.f;
+    a.bias = bptr; a.relu = relu; a.beta = 0.f; a.partial = part;
     finish_args(a, a.BN * 128);
-    return run_tc(L, s, 2.0 * N * O * (double)K, 1);
+    if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
+    if (part)
+        CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128, N, O, top->ptr, isbf(top), O, bptr, relu,
+                               0.f, 0, 0, s),
+           "ip fwd split-K reduce");
+    return CAFFE_OK;
 }
 
 caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
@@ -930,17 +1023,21 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
     CK(stage_rows(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
     CK(stage_rows(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
     const bool permute = nhwc(bottom_diff) && xs.h * xs.w > 1 && xs.c > 1;
-    float* rows = permute ? (float*)cur : nullptr;
+    const IpPlan q = ip_plan_dgrad(N, K, O);
+    float* part = nullptr;
+    if (q.splits > 1) { part = (float*)cur; cur += q.part_bytes; }
+    float* rows = permute && !part ? (float*)cur : nullptr;
     TcLaunch L;
     memset(&L, 0, sizeof L);
-    L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
+    L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_MN; L.epi = part ? EPI_PARTIAL : EPI_STRIDED;
     TcArgs& a = L.args;
-    a.BN = choose_bn((int)(K < 256 ? K : 256));
+    a.BN = q.BN;
     if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 128) || !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 64, 64))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip dgrad)");
-    a.M = N; a.N = (int)K; a.m_tiles = (int)cdiv(N, 128); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1; a.splits = 1;
-    a.kblocks = (int)cdiv(O, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
-    if (permute) {
+    a.M = N; a.N = (int)K; a.m_tiles = q.m_tiles; a.n_tiles = q.n_tiles; a.groups = 1; a.splits = q.splits;
+    a.kblocks = q.kblocks; a.kb_per_split = q.kb_per; a.b_nchunks = (int)cdiv(a.BN, 64);
+    a.partial = part;
+    if (rows) {
         a.out = rows; a.out_bf16 = 0; a.beta = 0.f;
     } else {
         a.out = bottom_diff->ptr; a.out_bf16 = isbf(bottom_diff); a.beta = beta;
@@ -948,7 +1045,12 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
     a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1;
     finish_args(a, a.b_nchunks * 64 * 128);
     if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
-    if (permute) CK(rows_to_nhwc(rows, K, bottom_diff->ptr, isbf(bottom_diff), N, xs.c, xs.h * xs.w, beta, s), "ip dgrad to NHWC");
+    if (part)
+        CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128, N, (int)K, bottom_diff->ptr,
+                               isbf(bottom_diff), K, nullptr, 0, beta, permute ? xs.c : 0, xs.h * xs.w, s),
+           "ip dgrad split-K reduce");
+    else if (rows)
+        CK(rows_to_nhwc(rows, K, bottom_diff->ptr, isbf(bottom_diff), N, xs.c, xs.h * xs.w, beta, s), "ip dgrad to NHWC");
     return CAFFE_OK;
 }
 
@@ -999,14 +1101,16 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     CK(stage_rows(bottom, N, K, E, cur, &B, &ldb, s), "stage bottom");
     TcLaunch L;
     memset(&L, 0, sizeof L);
+    // dW^T tiles: M runs over the fan-in k, N over the outputs o, so each epilogue store instruction
+    // writes 32 consecutive k of one dW row (coalesced); the reduction runs over the batch.
     L.esz = E; L.amode = A_TILED_MN; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
     TcArgs& a = L.args;
-    a.BN = choose_bn((int)(K < 256 ? K : 256));
-    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, 64, 64))
+    a.BN = choose_bn(O < 256 ? O : 256);
+    if (!encode_tiled_2d(&L.mapA, E, B, ldb, N, ldb * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, A, lda, N, lda * E, 64, 64))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip wgrad)");
-    a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1; a.splits = 1;
+    a.M = (int)K; a.N = O; a.m_tiles = (int)cdiv(K, 128); a.n_tiles = (int)cdiv(O, a.BN); a.groups = 1; a.splits = 1;
     a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
-    a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
+    a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = 1; a.s_c = K; a.s_p = 0; a.P = 1; a.beta = beta;
     finish_args(a, a.b_nchunks * 64 * 128);
     return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }

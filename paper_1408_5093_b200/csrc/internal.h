@@ -39,6 +39,12 @@ struct TcArgs {
     float beta;
     float* partial;                     // EPI_PARTIAL: [unit][BN][128] fp32
     int spin;                           // MMA thread polls (test_wait) instead of try_wait
+    // Multi-accumulator units (A_IM2COL_MN + EPI_PARTIAL, CG=1): a unit covers `macc` consecutive
+    // 128-row M tiles; each stage holds macc A tiles and ONE B tile, so B is staged once per macc
+    // tiles.  m_tiles then counts groups of macc tiles and m_tiles_real the tiles themselves;
+    // partials keep the one-tile unit layout (unit = ((split*G+g)*m_tiles_real+mt)*n_tiles+nt).
+    int macc;                           // 0/1 = one accumulator per unit
+    int m_tiles_real;
 };
 
 struct TcLaunch {
@@ -95,6 +101,12 @@ cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, co
 // Deterministic fixed-order reduction of wgrad partials into dW (O, Cg, kh, kw) fp32 with beta.
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
                          int splits, int BN, int chunk, int cblocks, cudaStream_t s);
+// Fixed-order reduction of split-K GEMM partials ([unit][BN][TM] fp32, unit = (s*m_tiles+mt)*n_tiles+nt)
+// into a row-major output (ldo) with bias, beta and ReLU; pC > 0 scatters each row's (c,h,w)-ordered
+// columns into an NHWC row of pC channels x pHW pixels.
+cudaError_t gemm_partial_reduce(const float* part, int splits, int m_tiles, int n_tiles, int BN, int TM, int M, int N,
+                                void* out, int out_bf16, long long ldo, const float* bias, int relu, float beta, int pC,
+                                int pHW, cudaStream_t s);
 // Generic 2-D convert/pad: dst[r][c] (ld_dst, esz) = src[r][c] (ld_src, f32|bf16) for c < cols, 0 up to ld_dst.
 cudaError_t convert_pad_2d(const void* src, int src_bf16, long long ld_src, void* dst, int dst_esz,
                            long long ld_dst, long long rows, long long cols, cudaStream_t s);
@@ -126,8 +138,9 @@ struct PoolGeom {
 };
 cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask, int bf16, const PoolGeom& g,
                         cudaStream_t s);
-cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g,
-                        cudaStream_t s);
+// top (optional): fuse the backward of the ReLU feeding the pool (window gradient passes iff top > 0)
+cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, const void* top, L4 ly, void* dx, int xnhwc, int bf16,
+                        const PoolGeom& g, cudaStream_t s);
 cudaError_t avepool_fwd(const void* x, L4 lx, void* y, int ynhwc, int bf16, const PoolGeom& g, cudaStream_t s);
 cudaError_t avepool_bwd(const void* dy, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g, cudaStream_t s);
 cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int nhwc, int N, int C, int H, int W, int size,

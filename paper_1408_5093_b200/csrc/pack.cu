@@ -152,10 +152,73 @@ __global__ void pack_s2d_kernel(const void* __restrict__ src, int src_bf16, L4 l
     }
 }
 
+// Space-to-depth of a channels-last BF16 source (the first conv layer's image batch).  One block
+// per packed row (n, Y): the sh source rows it needs are contiguous in NHWC, so they are copied
+// into shared memory with aligned 16-byte loads (enough bytes in flight to cover DRAM latency);
+// the packed row is then assembled as 16-byte vectors through a per-block table mapping packed
+// channel -> (dy, dx, source channel).  Packed channel (dy*sw + dx)*Cg + c of pixel (Y, X) of
+// group grp is X[n][grp*Cg + c][Y*sh + dy - ph][X*sw + dx - pw] (0 outside the image).
+__global__ void pack_s2d_rows_kernel(const __nv_bfloat16* __restrict__ src, L4 ls, __nv_bfloat16* __restrict__ dst,
+                                     PackGeom g) {
+    extern __shared__ uint4 sraw[];
+    const int WC = g.W * g.C;
+    const int row = blockIdx.x;
+    const int n = row / g.Hp, Y = row - n * g.Hp;
+    const int h0 = Y * g.sh - g.ph;
+    const int ha = max(h0, 0), hb = min(h0 + g.sh, g.H);           // valid source rows [ha, hb)
+    const int nrows = hb > ha ? hb - ha : 0;
+    const long long e0 = (long long)n * ls.sn + (long long)ha * WC; // first element (NHWC: rows contiguous)
+    const unsigned long long b0 = reinterpret_cast<unsigned long long>(src + e0);
+    const unsigned long long a0 = b0 & ~15ull;
+    const int head = (int)(b0 - a0);                                // bytes before the first element
+    const int nvec = (head + nrows * WC * 2 + 15) / 16;
+    int* tab = reinterpret_cast<int*>(sraw + ((g.sh * WC * 2 + 16 + 15) / 16 + 1));
+    const uint4* gsrc = reinterpret_cast<const uint4*>(a0);
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) sraw[i] = gsrc[i];
+    const int real = g.Cg * g.sh * g.sw;
+    for (int c = threadIdx.x; c < g.Ctot; c += blockDim.x) {
+        const int grp = c / g.cpg, cc = c - grp * g.cpg;
+        int e = -1;
+        if (cc < real && grp < g.G) {
+            const int d = cc / g.Cg, ch = cc - d * g.Cg;
+            const int dy = d / g.sw, dx = d - dy * g.sw;
+            e = (dy << 24) | (dx << 16) | (grp * g.Cg + ch);
+        }
+        tab[c] = e;
+    }
+    __syncthreads();
+    const uint16_t* sel = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(sraw) + head);
+    const int cvecs = g.Ctot / 8;
+    uint4* out = reinterpret_cast<uint4*>(dst + (long long)row * g.Wp * g.Ctot);
+    for (int v = threadIdx.x; v < g.Wp * cvecs; v += blockDim.x) {
+        const int X = v / cvecs, cv = v - X * cvecs;
+        uint32_t hv[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int e = tab[cv * 8 + q];
+            hv[q] = 0;
+            if (e >= 0) {
+                const int h = h0 + (e >> 24), w = X * g.sw - g.pw + ((e >> 16) & 0xff);
+                if (h >= ha && h < hb && w >= 0 && w < g.W) hv[q] = sel[(h - ha) * WC + w * g.C + (e & 0xffff)];
+            }
+        }
+        out[v] = make_uint4(hv[0] | (hv[1] << 16), hv[2] | (hv[3] << 16), hv[4] | (hv[5] << 16), hv[6] | (hv[7] << 16));
+    }
+}
+
 cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* dst, int dst_esz, const PackGeom& g,
                      cudaStream_t s) {
     const bool plain = g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.Hp == g.H && g.Wp == g.W;
-    if (!plain && dst_esz == 2 && g.cpg % 8 == 0) {
+    const size_t rows_smem = ((size_t)g.sh * g.W * g.C * 2 + 16 + 15) / 16 * 16 + 16 + (size_t)g.Ctot * 4;
+    if (!plain && dst_esz == 2 && src_bf16 && src_nhwc && ls.sc == 1 && ls.sw == g.C && g.Ctot % 8 == 0 &&
+        rows_smem <= 96 * 1024 && g.C < 65536 && g.sh < 128 && g.sw < 256) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(pack_s2d_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            attr_set = true;
+        }
+        pack_s2d_rows_kernel<<<g.N * g.Hp, 128, rows_smem, s>>>((const __nv_bfloat16*)src, ls, (__nv_bfloat16*)dst, g);
+    } else if (!plain && dst_esz == 2 && g.cpg % 8 == 0) {
         const int total = g.N * g.Hp * g.Wp;
         pack_s2d_kernel<<<blocks_for(total, 128), 128, 0, s>>>(src, src_bf16, ls, (__nv_bfloat16*)dst, g, total);
     } else if (plain && !src_nhwc && dst_esz == 2 && g.cpg == g.Cg && g.G * g.Cg <= g.Ctot) {
@@ -297,11 +360,17 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __
         if (i >= g.kh || j >= g.kw) continue;
         const int m_tile = q / chunks_per_tile, row = (q % chunks_per_tile) * chunk + rr;
         const int n_tile = o / BN, col = o % BN;
+        // fixed ascending-split order; loads batched 4 at a time so they are in flight together
+        const long long sstride = (long long)g.G * m_tiles * n_tiles * BN * 128;
+        const float* pp = partial + ((((long long)grp * m_tiles + m_tile) * n_tiles + n_tile) * BN + col) * 128 + row;
         float acc = 0.f;
-        for (int sp = 0; sp < splits; sp++) {
-            const long long unit = (((long long)sp * g.G + grp) * m_tiles + m_tile) * n_tiles + n_tile;
-            acc += partial[(unit * BN + col) * 128 + row];
+        int sp = 0;
+        for (; sp + 4 <= splits; sp += 4) {
+            const float a0 = pp[sp * sstride], a1 = pp[(sp + 1) * sstride], a2 = pp[(sp + 2) * sstride],
+                        a3 = pp[(sp + 3) * sstride];
+            acc += a0; acc += a1; acc += a2; acc += a3;
         }
+        for (; sp < splits; sp++) acc += pp[sp * sstride];
         float* p = dW + (((long long)(grp * g.Og + o) * g.Cg + c) * g.kh + i) * g.kw + j;
         *p = (beta != 0.f ? beta * *p : 0.f) + acc;
     }
@@ -312,6 +381,54 @@ cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeo
     const int total = g.G * g.Og * g.khp * g.kwp * cblocks * chunk;
     wgrad_reduce_kernel<<<blocks_for(total, 256), 256, 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
                                                                chunk, cblocks, 128 / chunk, total);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- split-K GEMM reduction
+// out[m*ldo + n] = act( sum_{s asc} partial[unit(s, m_tile, n_tile)][n % BN][m % TM] + bias[n] + beta*out )
+// unit = (s*m_tiles + m_tile)*n_tiles + n_tile (groups == 1).  m fastest -> coalesced partial reads.
+__global__ void gemm_partial_reduce_kernel(const float* __restrict__ part, int splits, int m_tiles, int n_tiles,
+                                           int BN, int TM, int M, int N, void* __restrict__ out, int obf16, long long ldo,
+                                           const float* __restrict__ bias, int relu, float beta, int pC, int pHW,
+                                           long long total) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int m = (int)(t % M), n = (int)(t / M);
+        const int mt = m / TM, mr = m - mt * TM, nt = n / BN, nc = n - nt * BN;
+        const long long sstride = (long long)m_tiles * n_tiles * BN * TM;
+        const float* pp = part + (((long long)mt * n_tiles + nt) * BN + nc) * TM + mr;
+        float acc = 0.f;
+        int s = 0;
+        for (; s + 4 <= splits; s += 4) {   // ascending order, 4 loads in flight
+            const float a0 = pp[s * sstride], a1 = pp[(s + 1) * sstride], a2 = pp[(s + 2) * sstride],
+                        a3 = pp[(s + 3) * sstride];
+            acc += a0; acc += a1; acc += a2; acc += a3;
+        }
+        for (; s < splits; s++) acc += pp[s * sstride];
+        if (bias) acc += bias[n];
+        // pC > 0: column n = c*HW + hw of the (c,h,w) flatten lands at hw*C + c of an NHWC row
+        const long long o = (long long)m * ldo + (pC > 0 ? (long long)(n % pHW) * pC + n / pHW : n);
+        if (obf16) {
+            __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(out) + o;
+            if (beta != 0.f) acc += beta * __bfloat162float(*p);
+            if (relu) acc = acc > 0.f ? acc : 0.f;
+            *p = __float2bfloat16_rn(acc);
+        } else {
+            float* p = reinterpret_cast<float*>(out) + o;
+            if (beta != 0.f) acc += beta * *p;
+            if (relu) acc = acc > 0.f ? acc : 0.f;
+            *p = acc;
+        }
+    }
+}
+
+cudaError_t gemm_partial_reduce(const float* part, int splits, int m_tiles, int n_tiles, int BN, int TM, int M, int N,
+                                void* out, int out_bf16, long long ldo, const float* bias, int relu, float beta, int pC,
+                                int pHW, cudaStream_t s) {
+    const long long total = (long long)M * N;
+    gemm_partial_reduce_kernel<<<blocks_for(total, 256), 256, 0, s>>>(part, splits, m_tiles, n_tiles, BN, TM, M, N, out,
+                                                                       out_bf16, ldo, bias, relu, beta, pC, pHW, total);
     note_launch();
     return cudaGetLastError();
 }

@@ -201,6 +201,15 @@ __device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
         : "memory");
 }
 
+// One lane of the (converged) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .b32 r;\n.reg .pred p;\nelect.sync r|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // Shared-memory matrix descriptor (sm_100 "version 1"), 128-byte swizzle.
 //   start address >>4 in [0,14), LBO>>4 in [16,30), SBO>>4 in [32,46), version=1 at bit 46,
 //   layout type SWIZZLE_128B = 2 at [61,64).

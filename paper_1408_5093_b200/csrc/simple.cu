@@ -10,6 +10,7 @@
 #include "internal.h"
 
 #include <cuda_bf16.h>
+#include <cooperative_groups.h>
 
 namespace cb {
 
@@ -192,6 +193,7 @@ __global__ void bias_partial_nhwc8(const __nv_bfloat16* __restrict__ dy, int O, 
     for (int e = 0; e < 8; e++) acc[e] = 0.f;
     if (rg < RG) {
         const int m1 = min(M, (s + 1) * R);
+#pragma unroll 4
         for (int m = s * R + rg; m < m1; m += RG) {
             const uint4 u = *reinterpret_cast<const uint4*>(dy + (long long)m * O + cv * 8);
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -440,6 +442,9 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
     return u;
 }
 
+// KH, KW > 0: compile-time window, fully unrolled so all of a thread's window loads are in flight
+// at once (a runtime-bounded loop leaves one load outstanding per thread: latency-bound).
+template <int KH, int KW>
 __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                   int32_t* __restrict__ mask, PoolGeom g, int total) {
     const int cv = g.C / 8;
@@ -457,15 +462,38 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
         int arg[8];
 #pragma unroll
         for (int e = 0; e < 8; e++) { best[e] = 0.f; arg[e] = -1; }
-        for (int h = hs; h < he; h++)
-            for (int w = ws; w < we; w++) {
-                float v[8];
-                unpack8(*reinterpret_cast<const uint4*>(x + (((long long)n * g.H + h) * g.W + w) * g.C + c0), v);
-                const int me = h * g.W + w;
+        if (KH > 0) {
+            uint4 raw[KH > 0 ? KH : 1][KW > 0 ? KW : 1];
 #pragma unroll
-                for (int e = 0; e < 8; e++)
-                    if (arg[e] < 0 || v[e] > best[e]) { best[e] = v[e]; arg[e] = me; }
-            }
+            for (int i = 0; i < KH; i++)
+#pragma unroll
+                for (int j = 0; j < KW; j++)
+                    if (hs + i < he && ws + j < we)
+                        raw[i][j] = *reinterpret_cast<const uint4*>(
+                            x + (((long long)n * g.H + hs + i) * g.W + ws + j) * g.C + c0);
+#pragma unroll
+            for (int i = 0; i < KH; i++)
+#pragma unroll
+                for (int j = 0; j < KW; j++)
+                    if (hs + i < he && ws + j < we) {
+                        float v[8];
+                        unpack8(raw[i][j], v);
+                        const int me = (hs + i) * g.W + ws + j;
+#pragma unroll
+                        for (int e = 0; e < 8; e++)
+                            if (arg[e] < 0 || v[e] > best[e]) { best[e] = v[e]; arg[e] = me; }
+                    }
+        } else {
+            for (int h = hs; h < he; h++)
+                for (int w = ws; w < we; w++) {
+                    float v[8];
+                    unpack8(*reinterpret_cast<const uint4*>(x + (((long long)n * g.H + h) * g.W + w) * g.C + c0), v);
+                    const int me = h * g.W + w;
+#pragma unroll
+                    for (int e = 0; e < 8; e++)
+                        if (arg[e] < 0 || v[e] > best[e]) { best[e] = v[e]; arg[e] = me; }
+                }
+        }
         const long long o = (long long)t * 8;
         *reinterpret_cast<uint4*>(y + o) = pack8(best);
         if (mask) {
@@ -476,34 +504,96 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
     }
 }
 
+// Thread = one SH x SW block of input positions x 8 channels (SH, SW = the pool stride when it is
+// 2x2, else 1x1).  Every window overlapping the block is loaded once -- mask, top_diff and, when
+// fused, top -- and added to each block position it selected, in ascending (py, px) order, so each
+// position's FP32 sum has R8's order (bit-exact); for 3x3/s2 windows this loads each window 4
+// times instead of 9.  top != nullptr: fused backward of the ReLU that feeds the pool -- a window
+// passes its gradient only when its max (= the ReLU output at the argmax) is > 0, which is exactly
+// relu_bwd(pool_bwd(dy)).
+// NPY x NPX (> 0): compile-time bound on the windows overlapping a block, so the window loads of
+// a thread are unrolled and all in flight together.
+template <int SH, int SW, int NPY, int NPX>
 __global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const int32_t* __restrict__ mask,
-                                  __nv_bfloat16* __restrict__ dx, PoolGeom g, int total) {
+                                  const __nv_bfloat16* __restrict__ top, __nv_bfloat16* __restrict__ dx, PoolGeom g,
+                                  int HB, int WB, int total) {
     const int cv = g.C / 8;
     GRID_STRIDE(t, total) {
         const int c0 = (t % cv) * 8;
         int r = t / cv;
-        const int w = r % g.W; r /= g.W;
-        const int h = r % g.H;
-        const int n = r / g.H;
-        const int py0 = max(0, (h + g.ph - g.kh + g.sh) / g.sh), py1 = min(g.OH - 1, (h + g.ph) / g.sh);
-        const int px0 = max(0, (w + g.pw - g.kw + g.sw) / g.sw), px1 = min(g.OW - 1, (w + g.pw) / g.sw);
-        const int me = h * g.W + w;
-        float acc[8];
+        const int bw = r % WB; r /= WB;
+        const int bh = r % HB;
+        const int n = r / HB;
+        const int h0 = bh * SH, w0 = bw * SW;
+        const int h1 = min(h0 + SH, g.H) - 1, w1 = min(w0 + SW, g.W) - 1;
+        const int py0 = max(0, (h0 + g.ph - g.kh + g.sh) / g.sh), py1 = min(g.OH - 1, (h1 + g.ph) / g.sh);
+        const int px0 = max(0, (w0 + g.pw - g.kw + g.sw) / g.sw), px1 = min(g.OW - 1, (w1 + g.pw) / g.sw);
+        float acc[SH][SW][8];
 #pragma unroll
-        for (int e = 0; e < 8; e++) acc[e] = 0.f;
-        for (int py = py0; py <= py1; py++)
-            for (int px = px0; px <= px1; px++) {
-                const long long q = (((long long)n * g.OH + py) * g.OW + px) * g.C + c0;
-                const int4 m0 = *reinterpret_cast<const int4*>(mask + q);
-                const int4 m1 = *reinterpret_cast<const int4*>(mask + q + 4);
-                const int mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-                float v[8];
-                unpack8(*reinterpret_cast<const uint4*>(dy + q), v);
+        for (int i = 0; i < SH; i++)
+#pragma unroll
+            for (int j = 0; j < SW; j++)
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[i][j][e] = 0.f;
+        auto window = [&](const int4& m0, const int4& m1, const uint4& dr, const uint4& tr) {
+            const int mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+            float v[8];
+            unpack8(dr, v);
+            if (top) {
+                float tv[8];
+                unpack8(tr, tv);
 #pragma unroll
                 for (int e = 0; e < 8; e++)
-                    if (mm[e] == me) acc[e] += v[e];
+                    if (!(tv[e] > 0.f)) v[e] = 0.f;
             }
-        *reinterpret_cast<uint4*>(dx + (long long)t * 8) = pack8(acc);
+#pragma unroll
+            for (int i = 0; i < SH; i++)
+#pragma unroll
+                for (int j = 0; j < SW; j++) {
+                    const int me = (h0 + i) * g.W + (w0 + j);
+#pragma unroll
+                    for (int e = 0; e < 8; e++)
+                        if (mm[e] == me) acc[i][j][e] += v[e];
+                }
+        };
+        if (NPY > 0) {
+            int4 m0[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1], m1[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1];
+            uint4 dr[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1], tr[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1];
+#pragma unroll
+            for (int a = 0; a < NPY; a++)
+#pragma unroll
+                for (int b = 0; b < NPX; b++)
+                    if (py0 + a <= py1 && px0 + b <= px1) {
+                        const long long q = (((long long)n * g.OH + py0 + a) * g.OW + px0 + b) * g.C + c0;
+                        m0[a][b] = *reinterpret_cast<const int4*>(mask + q);
+                        m1[a][b] = *reinterpret_cast<const int4*>(mask + q + 4);
+                        dr[a][b] = *reinterpret_cast<const uint4*>(dy + q);
+                        if (top) tr[a][b] = *reinterpret_cast<const uint4*>(top + q);
+                    }
+#pragma unroll
+            for (int a = 0; a < NPY; a++)
+#pragma unroll
+                for (int b = 0; b < NPX; b++)
+                    if (py0 + a <= py1 && px0 + b <= px1) window(m0[a][b], m1[a][b], dr[a][b], tr[a][b]);
+        } else {
+            for (int py = py0; py <= py1; py++)
+                for (int px = px0; px <= px1; px++) {
+                    const long long q = (((long long)n * g.OH + py) * g.OW + px) * g.C + c0;
+                    const int4 a0 = *reinterpret_cast<const int4*>(mask + q);
+                    const int4 a1 = *reinterpret_cast<const int4*>(mask + q + 4);
+                    const uint4 d = *reinterpret_cast<const uint4*>(dy + q);
+                    uint4 tt = make_uint4(0, 0, 0, 0);
+                    if (top) tt = *reinterpret_cast<const uint4*>(top + q);
+                    window(a0, a1, d, tt);
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < SH; i++)
+#pragma unroll
+            for (int j = 0; j < SW; j++)
+                if (h0 + i < g.H && w0 + j < g.W)
+                    *reinterpret_cast<uint4*>(dx + (((long long)n * g.H + h0 + i) * g.W + w0 + j) * g.C + c0) =
+                        pack8(acc[i][j]);
     }
 }
 
@@ -516,8 +606,12 @@ cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask,
     const int total = g.N * g.C * g.OH * g.OW;
     const bool xnhwc = lx.sc == 1 && g.C > 1;
     if (bf16 && xnhwc && ynhwc && nhwc8_ok(x, y, g.C) && ((reinterpret_cast<uintptr_t>(mask) & 15) == 0)) {
-        maxpool_fwd_nhwc8<<<nblk(total / 8, 256), 256, 0, s>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)y, mask, g,
-                                                               total / 8);
+        auto X = (const __nv_bfloat16*)x;
+        auto Y = (__nv_bfloat16*)y;
+        const unsigned nb = nblk(total / 8, 256);
+        if (g.kh == 3 && g.kw == 3) maxpool_fwd_nhwc8<3, 3><<<nb, 256, 0, s>>>(X, Y, mask, g, total / 8);
+        else if (g.kh == 2 && g.kw == 2) maxpool_fwd_nhwc8<2, 2><<<nb, 256, 0, s>>>(X, Y, mask, g, total / 8);
+        else maxpool_fwd_nhwc8<0, 0><<<nb, 256, 0, s>>>(X, Y, mask, g, total / 8);
     } else {
         maxpool_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, lx, y, ynhwc, mask, bf16, g, total);
     }
@@ -527,8 +621,9 @@ cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask,
 
 // Backward: gather per input element (in the bottom_diff's memory order) over the windows that may
 // contain it, ascending (py, px) -- R8, bit-exact.  ly = layout strides of top_diff and mask.
-__global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const int32_t* __restrict__ mask, L4 ly,
-                                   void* __restrict__ dx, int xnhwc, int bf16, PoolGeom g, int total) {
+__global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const int32_t* __restrict__ mask,
+                                   const void* __restrict__ top, L4 ly, void* __restrict__ dx, int xnhwc, int bf16,
+                                   PoolGeom g, int total) {
     GRID_STRIDE(t, total) {
         int n, c, h, w;
         decode(t, g.C, g.H, g.W, xnhwc, n, c, h, w);
@@ -540,21 +635,34 @@ __global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const int32_t* _
         for (int py = py0; py <= py1; py++)
             for (int px = px0; px <= px1; px++) {
                 const int q = base + py * ly.sh + px * ly.sw;
-                if (mask[q] == me) acc += ldv(dy, q, bf16);
+                if (mask[q] == me && (!top || ldv(top, q, bf16) > 0.f)) acc += ldv(dy, q, bf16);
             }
         stv(dx, t, bf16, acc);
     }
 }
 
-cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g,
-                        cudaStream_t s) {
+cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, const void* top, L4 ly, void* dx, int xnhwc, int bf16,
+                        const PoolGeom& g, cudaStream_t s) {
     const int total = g.N * g.C * g.H * g.W;
     const bool ynhwc = ly.sc == 1 && g.C > 1;
-    if (bf16 && xnhwc && ynhwc && nhwc8_ok(dy, dx, g.C) && ((reinterpret_cast<uintptr_t>(mask) & 15) == 0))
-        maxpool_bwd_nhwc8<<<nblk(total / 8, 256), 256, 0, s>>>((const __nv_bfloat16*)dy, mask, (__nv_bfloat16*)dx, g,
-                                                               total / 8);
-    else
-        maxpool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, mask, ly, dx, xnhwc, bf16, g, total);
+    if (bf16 && xnhwc && ynhwc && nhwc8_ok(dy, dx, g.C) && ((reinterpret_cast<uintptr_t>(mask) & 15) == 0) &&
+        ((reinterpret_cast<uintptr_t>(top) & 15) == 0)) {
+        auto DY = (const __nv_bfloat16*)dy;
+        auto T = (const __nv_bfloat16*)top;
+        auto DX = (__nv_bfloat16*)dx;
+        if (g.sh == 2 && g.sw == 2 && g.kh <= 3 && g.kw <= 3) {
+            // a 2x2 block of positions overlaps at most 2x2 windows of size <= 3
+            const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2, tb = g.N * HB * WB * (g.C / 8);
+            maxpool_bwd_nhwc8<2, 2, 2, 2><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
+        } else if (g.sh == 2 && g.sw == 2) {
+            const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2, tb = g.N * HB * WB * (g.C / 8);
+            maxpool_bwd_nhwc8<2, 2, 0, 0><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
+        } else {
+            maxpool_bwd_nhwc8<1, 1, 0, 0><<<nblk(total / 8, 256), 256, 0, s>>>(DY, mask, T, DX, g, g.H, g.W, total / 8);
+        }
+    } else {
+        maxpool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, mask, top, ly, dx, xnhwc, bf16, g, total);
+    }
     note_launch();
     return cudaGetLastError();
 }
@@ -806,12 +914,21 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
 // ================================================================ softmax with loss
 // One block of 16 warps; warp w owns rows w, w+16, ...; per-warp loss sums in row order, then a
 // fixed-order sum over warps -> deterministic mean.
-__global__ void softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restrict__ labels,
-                                    float* __restrict__ loss, void* __restrict__ diff, int db, int N, int K) {
+// One 8-CTA cluster, one warp per row (rows strided over the 8 x 16 warps); the loss is reduced in
+// a fixed order -- lanes, then warps of a CTA, then the 8 CTAs read through distributed shared
+// memory by rank 0 -- so it is deterministic without a workspace.
+#define SOFTMAX_CTAS 8
+__global__ void __cluster_dims__(SOFTMAX_CTAS, 1, 1)
+softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restrict__ labels, float* __restrict__ loss,
+                    void* __restrict__ diff, int db, int N, int K) {
     __shared__ float wl[32];
+    __shared__ float block_sum;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int gw = (int)cluster.block_rank() * nw + warp, gnw = nw * SOFTMAX_CTAS;
     float my = 0.f;
-    for (int n = warp; n < N; n += nw) {
+    for (int n = gw; n < N; n += gnw) {
         const int base = n * K;
         const int lab = labels[n];
         if (K <= 1024) {
@@ -870,13 +987,20 @@ __global__ void softmax_loss_kernel(const void* __restrict__ s, int sb, const in
     if (threadIdx.x == 0) {
         float t = 0.f;
         for (int w = 0; w < nw; w++) t += wl[w];
+        block_sum = t;
+    }
+    cluster.sync();
+    if (cluster.block_rank() == 0 && threadIdx.x == 0) {
+        float t = 0.f;
+        for (int r = 0; r < SOFTMAX_CTAS; r++) t += *cluster.map_shared_rank(&block_sum, r);
         *loss = t / N;
     }
+    cluster.sync();   // keep every CTA's shared memory alive until rank 0 has read it
 }
 
 cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff, int diff_bf16,
                            int N, int K, cudaStream_t s) {
-    softmax_loss_kernel<<<1, 512, 0, s>>>(scores, bf16, labels, loss, diff, diff_bf16, N, K);
+    softmax_loss_kernel<<<SOFTMAX_CTAS, 512, 0, s>>>(scores, bf16, labels, loss, diff, diff_bf16, N, K);
     note_launch();
     return cudaGetLastError();
 }

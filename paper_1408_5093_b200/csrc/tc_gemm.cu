@@ -32,7 +32,8 @@ constexpr int A_STAGE_BYTES = 16384;   // 128 rows x 128 B
 constexpr int SMEM_ALIGN = 1024;
 
 size_t tc_smem_bytes(const TcArgs& a) {
-    return (size_t)a.stages * (A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + 2 * 256 * 4 /*bias*/ +
+    const int macc = a.macc > 1 ? a.macc : 1;
+    return (size_t)a.stages * (macc * A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + 2 * 256 * 4 /*bias*/ +
            SMEM_ALIGN;
 }
 
@@ -48,7 +49,11 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + SMEM_ALIGN - 1) &
                                                ~uintptr_t(SMEM_ALIGN - 1));
     const int stages = args.stages;
-    const int stage_bytes = A_STAGE_BYTES + args.b_stage_bytes;
+    const int macc = args.macc > 1 ? args.macc : 1;                    // accumulators (M tiles) per unit
+    const int mt_real = args.m_tiles_real > 0 ? args.m_tiles_real : args.m_tiles * macc;
+    const int a_bytes = macc * A_STAGE_BYTES;
+    const int stage_bytes = a_bytes + args.b_stage_bytes;
+    const int nslots = 2 * macc * args.acc_stride <= args.tmem_cols ? 2 : 1;   // TMEM accumulator buffers
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
     uint64_t* empty = full + stages;
     uint64_t* tfull = empty + stages;
@@ -88,7 +93,6 @@ __global__ void __launch_bounds__(256, 1)
         // ===================== TMA producer (both CTAs) =====================
         int stage = 0;
         uint32_t phase = 0;
-        const uint32_t tx = A_STAGE_BYTES + args.b_stage_bytes;   // bytes landing in THIS CTA per stage
         const int bn_cta = args.BN / CG;                            // B rows (K-major) staged by this CTA
         for (int u = cid; u < args.units; u += ncl) {
             int t = u;
@@ -98,6 +102,9 @@ __global__ void __launch_bounds__(256, 1)
             const int split = t / args.groups;
             const int kb0 = split * args.kb_per_split;
             const int kb1 = min(args.kblocks, kb0 + args.kb_per_split);
+            const int nacc = min(macc, mt_real - m_tile * macc);         // M tiles present in this unit
+            // bytes landing in THIS CTA per stage
+            const uint32_t tx = (uint32_t)(nacc * A_STAGE_BYTES + args.b_stage_bytes);
             const int m0 = m_tile * TM + (int)rank * BM;   // first row staged by this CTA
             int an = 0, ay = 0, ax = 0;
             if (AMODE == A_IM2COL_K) {
@@ -109,7 +116,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int kb = kb0; kb < kb1; kb++) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * stage_bytes;
-                uint8_t* sb = sa + A_STAGE_BYTES;
+                uint8_t* sb = sa + a_bytes;
                 if (CG == 1 || leader) mbar_arrive_expect_tx(&full[stage], tx * CG);
                 else mbar_arrive_cluster(mapa_shared(smem_u32(&full[stage]), 0));
                 // ---- A
@@ -130,14 +137,17 @@ __global__ void __launch_bounds__(256, 1)
                     const int n0 = p0 / args.a_P;
                     const int r = p0 - n0 * args.a_P;
                     const int y0 = r / args.a_OW, x0 = r - (r / args.a_OW) * args.a_OW;
+                    for (int a = 0; a < nacc; a++) {
 #pragma unroll
-                    for (int q = 0; q < ESZ; q++) {   // 128 rows of M = ESZ chunks of CH
-                        int chunk = (m_tile * CG + (int)rank) * ESZ + q;
-                        if (chunk >= args.a_nchunks_total) chunk = args.a_nchunks_total - 1;  // rows discarded
-                        const int tap = chunk / args.a_cblocks, cbk = chunk - tap * args.a_cblocks;
-                        const int i = tap / args.a_kw, j = tap - i * args.a_kw;
-                        tma_load_im2col_4d(sa + q * CH * 128, &mapA, &full[stage], g * args.a_cpg + cbk * CH,
-                                           x0 - args.a_pad_w, y0 - args.a_pad_h, n0, (uint16_t)j, (uint16_t)i);
+                        for (int q = 0; q < ESZ; q++) {   // 128 rows of M = ESZ chunks of CH
+                            int chunk = ((m_tile * macc + a) * CG + (int)rank) * ESZ + q;
+                            if (chunk >= args.a_nchunks_total) chunk = args.a_nchunks_total - 1;  // rows discarded
+                            const int tap = chunk / args.a_cblocks, cbk = chunk - tap * args.a_cblocks;
+                            const int i = tap / args.a_kw, j = tap - i * args.a_kw;
+                            tma_load_im2col_4d(sa + a * A_STAGE_BYTES + q * CH * 128, &mapA, &full[stage],
+                                               g * args.a_cpg + cbk * CH, x0 - args.a_pad_w, y0 - args.a_pad_h, n0,
+                                               (uint16_t)j, (uint16_t)i);
+                        }
                     }
                 } else {  // A_TILED_MN
 #pragma unroll
@@ -157,51 +167,66 @@ __global__ void __launch_bounds__(256, 1)
                 if (++stage == stages) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp == 1 && lane == 0 && leader) {
-        // ===================== MMA issuer (leader CTA) =====================
+    } else if (warp == 1 && leader) {
+        // ===================== MMA issuer (leader CTA, whole warp) =====================
+        // The warp runs the loop convergently so descriptors stay warp-uniform (uniform registers,
+        // no per-MMA register->uniform waterfall); one elected lane issues the tcgen05 ops.
         // instruction descriptor: D=f32, A/B format (bf16=1, tf32=2), majors, N>>3, M>>4
         const uint32_t fmt = (ESZ == 2) ? 1u : 2u;
         const uint32_t a_mn = (AMODE == A_IM2COL_MN || AMODE == A_TILED_MN) ? 1u : 0u;
         const uint32_t b_mn = (BMODE == B_TILED_MN) ? 1u : 0u;
         const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn << 15) | (b_mn << 16) |
                                ((uint32_t)(args.BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+        // per-K-step descriptor advance (start address field is in 16-byte units):
+        // K-major: 32 bytes along the 128-byte row; MN-major: UMMA_K rows of 128 bytes
+        const uint64_t a_step = a_mn ? (uint64_t)(UMMA_K * 128 / 16) : 2ull;
+        const uint64_t b_step = b_mn ? (uint64_t)(UMMA_K * 128 / 16) : 2ull;
+        const uint32_t a_lbo = a_mn ? CH * 128 : 16, b_lbo = b_mn ? CH * 128 : 16;
+        const uint32_t smem_base = smem_u32(smem);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         int iters = 0;
         for (int u = cid; u < args.units; u += ncl, iters++) {
+            const int m_tile = (u / args.n_tiles) % args.m_tiles;
             int t = u / (args.n_tiles * args.m_tiles);
             const int split = t / args.groups;
             const int kb0 = split * args.kb_per_split;
             const int kb1 = min(args.kblocks, kb0 + args.kb_per_split);
+            const int nacc = min(macc, mt_real - m_tile * macc);
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * args.acc_stride;
+            const uint32_t d_tmem = tmem_base + acc * macc * args.acc_stride;
             for (int kb = kb0; kb < kb1; kb++) {
                 if (args.spin) mbar_wait_spin(&full[stage], phase);
                 else mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                const uint32_t sa = smem_u32(smem + stage * stage_bytes);
-                const uint32_t sb = sa + A_STAGE_BYTES;
+                const uint32_t sa = smem_base + stage * stage_bytes;
+                const uint64_t bd0 = smem_desc_sw128(sa + a_bytes, b_lbo, 1024);
+                if (elect_one()) {
+                    for (int a = 0; a < nacc; a++) {
+                        const uint64_t ad0 = smem_desc_sw128(sa + a * A_STAGE_BYTES, a_lbo, 1024);
+                        const uint32_t dt = d_tmem + a * args.acc_stride;
 #pragma unroll
-                for (int k = 0; k < KSTEPS; k++) {
-                    uint64_t ad, bd;
-                    if (a_mn) ad = smem_desc_sw128(sa + k * UMMA_K * 128, CH * 128, 1024);
-                    else      ad = smem_desc_sw128(sa + k * 32, 16, 1024);
-                    if (b_mn) bd = smem_desc_sw128(sb + k * UMMA_K * 128, CH * 128, 1024);
-                    else      bd = smem_desc_sw128(sb + k * 32, 16, 1024);
-                    if (CG == 2) umma_cg2<ESZ>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                    else umma<ESZ>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < KSTEPS; k++) {
+                            const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+                            if (CG == 2) umma_cg2<ESZ>(dt, ad0 + k * a_step, bd0 + k * b_step, idesc, accum);
+                            else umma<ESZ>(dt, ad0 + k * a_step, bd0 + k * b_step, idesc, accum);
+                        }
+                    }
+                    if (CG == 2) umma_commit_cg2(&empty[stage]);
+                    else umma_commit(&empty[stage]);
                 }
-                if (CG == 2) umma_commit_cg2(&empty[stage]);
-                else umma_commit(&empty[stage]);
+                __syncwarp();
                 if (++stage == stages) { stage = 0; phase ^= 1; }
             }
-            if (CG == 2) umma_commit_cg2(&tfull[acc]);
-            else umma_commit(&tfull[acc]);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            if (elect_one()) {
+                if (CG == 2) umma_commit_cg2(&tfull[acc]);
+                else umma_commit(&tfull[acc]);
+            }
+            __syncwarp();
+            if (++acc == nslots) { acc = 0; acc_phase ^= 1; }
         }
         // the peer's epilogue arrives remotely on our tempty barriers: drain the last two phases
         // before the pair tears down
@@ -223,15 +248,28 @@ __global__ void __launch_bounds__(256, 1)
             const int g = t % args.groups;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * args.acc_stride;
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * macc * args.acc_stride;
             if (EPI == EPI_PARTIAL) {
-                float* dst = args.partial + (size_t)u * args.BN * TM + (int)rank * BM + row;
-                for (int c0 = 0; c0 < args.BN; c0 += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(taddr + c0, v);
-                    tmem_wait_ld();
+                const int split = t / args.groups;
+                const int nacc = min(macc, mt_real - m_tile * macc);
+                for (int a = 0; a < nacc; a++) {
+                    // partial slot of the one-tile unit (split, g, m_tile*macc + a, n_tile)
+                    const size_t vu = (((size_t)split * args.groups + g) * mt_real + (m_tile * macc + a)) *
+                                          args.n_tiles + n_tile;
+                    float* dst = args.partial + vu * args.BN * TM + (int)rank * BM + row;
+                    for (int c0 = 0; c0 < args.BN; c0 += 32) {
+                        const bool two = c0 + 16 < args.BN;
+                        uint32_t v0[16], v1[16];
+                        tmem_ld16(taddr + a * args.acc_stride + c0, v0);
+                        if (two) tmem_ld16(taddr + a * args.acc_stride + c0 + 16, v1);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 16; j++) dst[(size_t)(c0 + j) * TM] = __uint_as_float(v[j]);
+                        for (int j = 0; j < 16; j++) dst[(size_t)(c0 + j) * TM] = __uint_as_float(v0[j]);
+                        if (two) {
+#pragma unroll
+                            for (int j = 0; j < 16; j++) dst[(size_t)(c0 + 16 + j) * TM] = __uint_as_float(v1[j]);
+                        }
+                    }
                 }
             } else {
                 const int m = m_tile * TM + (int)rank * BM + row;
@@ -350,8 +388,7 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_before();
             if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
             else mbar_arrive(&tempty[acc]);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            if (++acc == nslots) { acc = 0; acc_phase ^= 1; }
         }
     }
     tc_fence_before();
@@ -414,6 +451,9 @@ cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s) {
     TC_CASE(2, A_TILED_K, B_TILED_K, EPI_STRIDED, 1)
     TC_CASE(2, A_TILED_K, B_TILED_K, EPI_STRIDED, 2)
     TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_STRIDED, 1)
+    TC_CASE(2, A_TILED_K, B_TILED_K, EPI_PARTIAL, 1)
+    TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_PARTIAL, 1)
+    TC_CASE(4, A_TILED_K, B_TILED_K, EPI_PARTIAL, 1)
     TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 1)
     TC_CASE(4, A_IM2COL_K, B_TILED_K, EPI_STRIDED, 1)
     TC_CASE(4, A_TILED_K, B_TILED_K, EPI_STRIDED, 1)

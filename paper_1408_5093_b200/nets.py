@@ -180,6 +180,13 @@ class Net:
             elif L.kind == "loss":
                 cb.softmax_loss(self.scores, self.labels, loss=self.loss, diff=self.dscores)
 
+    def _relu_fused(self, i):
+        """True when layer i's ReLU backward is folded into the MAX-pool backward of layer i+1."""
+        if i < 0 or i + 1 >= len(self.layers):
+            return False
+        L, P = self.layers[i], self.layers[i + 1]
+        return L.kind in ("conv", "ip") and L.relu and P.kind == "pool" and P.method == "max"
+
     def backward(self, hook=None):
         """Backward in reverse; `hook(i)` is called after layer i's parameter gradients are enqueued
         (data-parallel bucketing point)."""
@@ -188,7 +195,7 @@ class Net:
             L = self.layers[i]
             dy = d[i + 1] if i + 1 < n - 1 else self.dscores
             y = a[i + 1] if i + 1 < n - 1 else self.scores
-            if L.kind in ("conv", "ip") and L.relu:
+            if L.kind in ("conv", "ip") and L.relu and not self._relu_fused(i):
                 cb.relu_backward(y, dy, inplace=True)  # sign of the ReLU output == sign test on its input
             if L.kind == "conv":
                 cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math, beta=0.0,
@@ -206,7 +213,10 @@ class Net:
                 if i > 0:
                     cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
             elif L.kind == "pool":
-                cb.pool_backward(dy, self.mask[i], a[i].shape, L.method, L.kernel, L.stride, L.pad, out=d[i])
+                if self._relu_fused(i - 1):  # conv -> ReLU -> MAX pool: ReLU backward folded in
+                    cb.pool_relu_backward(y, dy, self.mask[i], a[i].shape, L.kernel, L.stride, L.pad, out=d[i])
+                else:
+                    cb.pool_backward(dy, self.mask[i], a[i].shape, L.method, L.kernel, L.stride, L.pad, out=d[i])
             elif L.kind == "lrn":
                 cb.lrn_backward(a[i], y, dy, **LRN, out=d[i])
 

@@ -142,7 +142,9 @@ def test_conv_empty_batch_is_noop():
 
 # ---------------------------------------------------------------- channels-last (NHWC) BF16 blobs:
 # the tensor-core path reads/writes them directly (no transpose), the FP32 path via strides.
-NHWC_CASES = [CASES[1], CASES[2], CASES[3], CASES[7], (2, 16, 9, 9, 24, (3, 3), (1, 1), (1, 1), 2)]
+NHWC_CASES = [CASES[1], CASES[2], CASES[3], CASES[7], (2, 16, 9, 9, 24, (3, 3), (1, 1), (1, 1), 2),
+              (1, 4, 10, 9, 6, (3, 2), (2, 1), (1, 0), 1),    # padded s2d from a channels-last image
+              CASES[6]]                                        # the same, grouped
 
 
 @pytest.mark.parametrize("math", ["bf16", "fp32"])
@@ -198,6 +200,31 @@ def test_conv_cta_pair_modes(oracle, case, cta):
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
 
 
+@pytest.mark.parametrize("macc", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("case", [CASES[2], CASES[3], CASES[7], (2, 64, 13, 13, 192, (3, 3), (1, 1), (1, 1), 2)],
+                         ids=[IDS[2], IDS[3], IDS[7], "N2C64H13O192g2"])
+def test_conv_wgrad_multi_accumulator(oracle, case, macc):
+    """Weight gradient with 1..4 M tiles per work unit (top_diff staged once per unit; forced via
+    CAFFE_TUNE_WGRAD_MACC, 0 = automatic): same parity for every count, ragged last unit included."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 9)
+    q = oracle.quant_bf16
+    cl = torch.channels_last
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_MACC, macc)
+    try:
+        Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+        dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+        dW, db = cb.conv_backward_weight(Xd, dYd, Wt.shape, stride=s, pad=p, group=g, math="bf16")
+        rW, rb = oracle.conv_backward_weight(host(Xd), host(dYd), Wt.shape, stride=s, pad=p, group=g)
+        assert_tc_close(host(dW), rW, f"wgrad macc={macc}")
+        assert_fp32_close(host(db), rb, f"bias grad macc={macc}")
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_MACC, 0)
+
+
 @pytest.mark.parametrize("dy_layout", ["nchw_f32", "nhwc_f32", "nhwc_bf16"])
 def test_caffenet_conv1_full_image_wgrad(oracle, dy_layout):
     """conv1 at its real geometry (227x227, 11x11/s4, space-to-depth path), 2 images, every dY layout."""
@@ -215,4 +242,10 @@ def test_caffenet_conv1_full_image_wgrad(oracle, dy_layout):
     rW, _ = oracle.conv_backward_weight(X, oracle.quant_bf16(dY), Wt.shape, stride=(4, 4))
     assert_tc_close(host(dW), rW, f"conv1 wgrad {dy_layout}")
     Y = cb.conv_forward(cuda(X), cuda(Wt), None, stride=4, math="bf16")
-    assert_tc_close(host(Y), oracle.conv_forward(X, oracle.quant_bf16(Wt), None, stride=(4, 4)), "conv1 fwd")
+    rY = oracle.conv_forward(X, oracle.quant_bf16(Wt), None, stride=(4, 4))
+    assert_tc_close(host(Y), rY, "conv1 fwd")
+    # channels-last bf16 image batch (the training net's input blob): the direct s2d pack
+    Xh = cuda(X).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)   # integer pixels: exact
+    Yh = cb.conv_forward(Xh, cuda(Wt), None, stride=4, math="bf16")
+    np.testing.assert_array_equal(host(Yh), host(cb.conv_forward(cuda(X), cuda(Wt), None, stride=4, math="bf16")
+                                                  .to(torch.bfloat16).contiguous(memory_format=torch.channels_last)))

@@ -74,6 +74,38 @@ def test_avepool(oracle, case):
     assert_fp32_close(host(dX), oracle.avepool_backward(dY, shape, k, s, p), "avepool bwd")
 
 
+@pytest.mark.parametrize("case", [POOLS[0], POOLS[2], POOLS[3]])
+@pytest.mark.parametrize("layout", ["nchw_f32", "nhwc_bf16"])
+def test_pool_relu_backward_fused(oracle, case, layout):
+    """caffe_pool_relu_backward == oracle relu_backward(maxpool_backward(.)) bit for bit, on a
+    ReLU output with many exact zeros (whole zero windows included)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    shape, k, s, p = case
+    X = oracle.relu_forward(synth.uniform(shape, 6, synth.S_X) - 0.3)   # ~65% zeros after the ReLU
+    if layout == "nhwc_bf16":
+        X = oracle.quant_bf16(X)
+        xt = cuda(X).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    else:
+        xt = cuda(X)
+    Y, M = cb.pool_forward(xt, "max", k, s, p)
+    rY, rM = oracle.maxpool_forward(X, k, s, p)
+    dY = synth.uniform(rY.shape, 6, synth.S_DY)
+    if layout == "nhwc_bf16":
+        dY = oracle.quant_bf16(dY)
+        dyt = cuda(dY).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    else:
+        dyt = cuda(dY)
+    dX = cb.pool_relu_backward(Y, dyt, M, shape, k, s, p)
+    ref = oracle.relu_backward(X, oracle.maxpool_backward(dY, rM, shape, k, s, p))
+    if layout == "nhwc_bf16":
+        ref = oracle.quant_bf16(ref)
+    np.testing.assert_array_equal(host(dX), ref)
+    # and it equals the two-kernel sequence through the library
+    two = cb.relu_backward(xt, cb.pool_backward(dyt, M, shape, "max", k, s, p))
+    np.testing.assert_array_equal(host(dX), host(two))
+
+
 def test_pool_bf16_maxpool_bit_exact(oracle):
     import torch
     import paper_1408_5093_b200 as cb
@@ -222,20 +254,29 @@ def test_pool_lrn_nhwc_bf16_vector_paths(oracle, shape):
         assert_tc_close(host(dL), rdL, f"lrn bwd bf16 nhwc n={size}", tol=5e-3)
 
 
-def test_ip_nhwc_bottom(oracle):
-    """An NHWC bottom is flattened in Caffe's (c,h,w) order."""
+@pytest.mark.parametrize("shape", [(8, 16, 3, 3, 10), (256, 256, 6, 6, 512)])
+def test_ip_nhwc_bottom(oracle, shape):
+    """An NHWC bottom is flattened in Caffe's (c,h,w) order.  The pool5->fc6-like case
+    (256 x 9216 -> 512) runs the split-K forward and data-gradient with the NHWC scatter, and
+    checks beta accumulation into an existing bottom_diff."""
     import torch
     import paper_1408_5093_b200 as cb
-    X = synth.uniform((8, 16, 3, 3), 12, synth.S_X)
-    Wt = synth.xavier((10, 144), 12)
-    dY = synth.uniform((8, 10), 12, synth.S_DY)
+    N, C, H, W, O = shape
+    K = C * H * W
+    X = synth.uniform((N, C, H, W), 12, synth.S_X)
+    Wt = synth.xavier((O, K), 12)
+    dY = synth.uniform((N, O), 12, synth.S_DY)
     xh = cuda(X).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
     Xq = host(xh)
     Y = cb.ip_forward(xh, cuda(Wt), None, math="bf16", out_dtype=torch.float32)
     assert_tc_close(host(Y), oracle.ip_forward(Xq, oracle.quant_bf16(Wt)), "ip fwd nhwc")
-    dW, _ = cb.ip_backward_weight(xh, cuda(dY), (10, 144), math="bf16")
+    dW, _ = cb.ip_backward_weight(xh, cuda(dY), (O, K), math="bf16")
     rdX, rdW, _ = oracle.ip_backward(Xq, oracle.quant_bf16(Wt), oracle.quant_bf16(dY))
     assert_tc_close(host(dW), rdW, "ip wgrad nhwc")
-    dX = torch.zeros((8, 16, 3, 3), device="cuda").contiguous(memory_format=torch.channels_last)
+    dX = torch.zeros((N, C, H, W), device="cuda").contiguous(memory_format=torch.channels_last)
     cb.ip_backward_data(cuda(dY), cuda(Wt), X.shape, math="bf16", out=dX)
     assert_tc_close(host(dX), rdX, "ip dgrad nhwc")
+    prev = synth.uniform((N, C, H, W), 13, synth.S_AUX)
+    dX2 = cuda(prev).contiguous(memory_format=torch.channels_last)
+    cb.ip_backward_data(cuda(dY), cuda(Wt), X.shape, math="bf16", beta=1.0, out=dX2)
+    assert_tc_close(host(dX2), rdX + prev, "ip dgrad nhwc beta=1")

@@ -49,6 +49,9 @@ def main():
     if "--spin" in sys.argv:
         from paper_1408_5093_b200 import _abi
         _abi.call("caffe_set_tuning", 2, int(sys.argv[sys.argv.index("--spin") + 1]))
+    if "--macc" in sys.argv:
+        from paper_1408_5093_b200 import _abi
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_MACC, int(sys.argv[sys.argv.index("--macc") + 1]))
     if "--cta" in sys.argv:
         from paper_1408_5093_b200 import _abi
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, int(sys.argv[sys.argv.index("--cta") + 1]))
@@ -59,6 +62,20 @@ def main():
         y = cb.conv_forward(x, w, None, 1, 1, 1, relu=True)
         for _ in range(3):
             cb.conv_forward(x, w, None, 1, 1, 1, relu=True, out=y)
+        torch.cuda.synchronize()
+        return
+    if "--only-fc6w" in sys.argv:   # for ncu: fc6 weight gradient / forward / data gradient
+        x = torch.randn(256, 9216, device=dev).to(torch.bfloat16)
+        w = torch.randn(4096, 9216, device=dev).to(torch.bfloat16) * 0.01
+        dy = torch.randn(256, 4096, device=dev).to(torch.bfloat16)
+        dw = torch.empty(4096, 9216, device=dev)
+        db = torch.empty(4096, device=dev)
+        y = torch.empty(256, 4096, device=dev, dtype=torch.bfloat16)
+        dx = torch.empty(256, 9216, device=dev, dtype=torch.bfloat16)
+        for _ in range(2):
+            cb.ip_backward_weight(x, dy, w.shape, dw=dw, db=db)
+            cb.ip_forward(x, w, None, relu=True, out=y)
+            cb.ip_backward_data(dy, w, x.shape, out=dx)
         torch.cuda.synchronize()
         return
     if "--only-gemm" in sys.argv:   # for ncu: a few launches of one plain GEMM
@@ -78,8 +95,26 @@ def main():
         out[f"gemm M{M} N{N} K{K}"] = round(2 * M * N * K / ms / 1e9, 1)
     cl = torch.channels_last
     B = 256
+    # CaffeNet fc layers (bf16 rows; NHWC pool5 bottom for fc6)
+    for name, (K, O) in {"fc6": (9216, 4096), "fc7": (4096, 4096), "fc8": (4096, 1000)}.items():
+        x = torch.randn(B, K, device=dev).to(torch.bfloat16)
+        w = torch.randn(O, K, device=dev).to(torch.bfloat16) * 0.01
+        bias = torch.zeros(O, device=dev)
+        y = torch.empty(B, O, device=dev, dtype=torch.bfloat16)
+        dy = torch.randn(B, O, device=dev).to(torch.bfloat16)
+        dx = torch.empty(B, K, device=dev, dtype=torch.bfloat16)
+        dw = torch.empty(O, K, device=dev)
+        db = torch.empty(O, device=dev)
+        flops = 2 * B * K * O
+        ms = timeit(lambda: cb.ip_forward(x, w, bias, relu=True, out=y))
+        ms_d = timeit(lambda: cb.ip_backward_data(dy, w, x.shape, out=dx))
+        ms_w = timeit(lambda: cb.ip_backward_weight(x, dy, w.shape, dw=dw, db=db))
+        out[name] = {"fwd_us": round(ms * 1e3, 1), "dgrad_us": round(ms_d * 1e3, 1), "wgrad_us": round(ms_w * 1e3, 1),
+                     "fwd_tflops": round(flops / ms / 1e9, 1), "wgrad_tflops": round(flops / ms_w / 1e9, 1)}
     for name, (C, H, O, k, p, g) in {"conv2": (96, 27, 256, 5, 2, 2), "conv3": (256, 13, 384, 3, 1, 1),
                                      "conv4": (384, 13, 384, 3, 1, 2), "conv5": (384, 13, 256, 3, 1, 2)}.items():
+        if "--only-fc" in sys.argv:
+            break
         x = torch.randn(B, C, H, H, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
         w = torch.randn(O, C // g, k, k, device=dev) * 0.05
         bias = torch.zeros(O, device=dev)
