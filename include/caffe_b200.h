@@ -124,6 +124,10 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_WGRAD_MACC: 128-row M tiles per weight-gradient work unit (top_diff staged once for
    all of them); 0 = automatic (default), 1..4 forced. */
 #define CAFFE_TUNE_WGRAD_MACC 3
+/* CAFFE_TUNE_HALO: stride-1 forward / data-gradient tensor-core tiles that stage each input window
+   once for all filter taps (halo tiles); 0 = automatic (default), 1 = off (per-tap im2col tiles),
+   2 = wherever the geometry allows. */
+#define CAFFE_TUNE_HALO 4
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

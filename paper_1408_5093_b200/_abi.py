@@ -24,6 +24,7 @@ CAFFE_PASS_FORWARD, CAFFE_PASS_BACKWARD_DATA, CAFFE_PASS_BACKWARD_WEIGHT = 0, 1,
 CAFFE_TUNE_CTA_PAIR = 1
 CAFFE_TUNE_MMA_SPIN = 2
 CAFFE_TUNE_WGRAD_MACC = 3
+CAFFE_TUNE_HALO = 4
 
 
 class Shape4(ctypes.Structure):

@@ -3,6 +3,7 @@
 // pack.cu and simple.cu; nothing here touches device data.
 #include "../../include/caffe_b200.h"
 #include "internal.h"
+#include <algorithm>
 
 #include <atomic>
 #include <cstdarg>
@@ -316,6 +317,63 @@ caffe_status check_ws(void* ws, size_t have, size_t need) {
 }
 
 // kind: 0 = convolution pass, 1 = inner product; flops = algorithmic FLOPs of the call
+// ---- halo-tiled stride-1 convolution (tc_halo.cu)
+int g_halo = 0;   // CAFFE_TUNE_HALO: 0 = automatic, 1 = off (im2col tiles), 2 = wherever it applies
+struct HaloGeom {
+    int Hi, Wi, Ho, Wo, kh, kw, pad_h, pad_w;   // stride-1 geometry of the pass (input -> output)
+};
+// Tile shape and whether the halo form is used: halo_wt = Wo + kw - 1 columns, halo_th = 128 / halo_wt
+// output rows per 128-row tile.  Automatic use needs >= 4 taps and >= 75% useful accumulator rows
+// (CaffeNet conv1/conv2: 84% / 81%; the 13x13 layers reach only 66% and stay on im2col tiles).
+static bool halo_applies(int E, const HaloGeom& h) {
+    if (E != 2 || g_halo == 1) return false;
+    const int wt = h.Wo + h.kw - 1;
+    if (wt > 128 || h.Ho < 1) return false;
+    const int th = 128 / wt;
+    if (th + h.kh - 1 > 256) return false;
+    if (g_halo == 2) return true;
+    const int tpi = (h.Ho + th - 1) / th;
+    const double eff = (double)h.Ho * h.Wo / (tpi * 128.0);
+    return h.kh * h.kw >= 4 && eff >= 0.75;
+}
+// Fills the halo fields of L (A map over the channels-last operand `aptr` [N][Hi][Wi][Ctot]) after
+// the caller has set BN, N, n_tiles, groups, b_row_g, a_cpg, a_cblocks and the epilogue.
+static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Ctot, int N) {
+    TcArgs& a = L.args;
+    L.amode = A_HALO_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED; L.esz = 2;
+    a.halo_wt = h.Wo + h.kw - 1;
+    a.halo_th = 128 / a.halo_wt;
+    a.halo_rows = a.halo_th + h.kh - 1;
+    a.halo_kh = h.kh; a.a_kw = h.kw;
+    a.a_pad_h = h.pad_h; a.a_pad_w = h.pad_w;
+    a.tiles_per_img = (h.Ho + a.halo_th - 1) / a.halo_th;
+    a.total_tiles = N * a.tiles_per_img;
+    a.out_h = h.Ho; a.out_w = h.Wo;
+    const int need_rows = std::max(a.halo_rows * a.halo_wt, (h.kh - 1) * a.halo_wt + (h.kw - 1) + 128);
+    a.halo_slot = (int)rup((long long)need_rows * 128, 1024);
+    if (!encode_tiled_4d(&L.mapA, 2, aptr, Ctot, h.Wi, h.Hi, N, 64, (uint32_t)a.halo_wt, (uint32_t)a.halo_rows))
+        return false;
+    // CTA pairs when the B tile splits into 8-row halves and there is enough work for every pair
+    L.cg = 1;
+    if ((a.BN / 2) % 8 == 0 &&
+        (g_force_cg == 2 || (g_force_cg == 0 && (long long)a.total_tiles * a.n_tiles * a.groups >= 4LL * num_sms())))
+        L.cg = 2;
+    a.acc_stride = pow2ceil(a.BN);
+    a.a_stages = 2;
+    a.macc = 1;
+    if (2 * 2 * a.acc_stride <= 512 && a.a_stages * 2 * a.halo_slot <= 140 * 1024) a.macc = 2;
+    a.b_stage_bytes = a.BN / L.cg * 128;
+    const long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
+    a.stages = (int)std::min<long long>(24, budget / a.b_stage_bytes);
+    if (a.stages < 2) return false;
+    const int cols = (2 * a.macc * a.acc_stride <= 512 ? 2 : 1) * a.macc * a.acc_stride;
+    a.tmem_cols = pow2ceil(cols < 32 ? 32 : cols);
+    const int tgroups = (a.total_tiles + a.macc * L.cg - 1) / (a.macc * L.cg);
+    a.units = a.groups * a.n_tiles * tgroups;
+    a.m_tiles = tgroups; a.splits = 1;
+    return true;
+}
+
 caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     if (L.cg < 1) L.cg = 1;
     L.args.spin = g_mma_spin;
@@ -328,7 +386,7 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
         rec.b = prof_event();
         cudaEventRecord(rec.a, s);
     }
-    cudaError_t e = tc_launch(L, s);
+    cudaError_t e = L.amode == A_HALO_K ? tc_halo_launch(L, s) : tc_launch(L, s);
     if (g_prof) {
         cudaEventRecord(rec.b, s);
         std::lock_guard<std::mutex> lk(g_pmu);
@@ -388,6 +446,11 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     }
     if (key == CAFFE_TUNE_MMA_SPIN) {
         g_mma_spin = value ? 1 : 0;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_HALO) {
+        if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "halo mode must be 0 (auto), 1 (off) or 2 (force)");
+        g_halo = value;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_WGRAD_MACC) {
@@ -483,6 +546,20 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     CK(repack_w_fwd(weight->ptr, isbf(weight), WB, p.E, wgeom(p), s), "repack weights");
     TcLaunch L;
     memset(&L, 0, sizeof L);
+    const HaloGeom hg{A.H, A.W, p.OH, p.OW, p.khp, p.kwp, p.php, p.pwp};
+    if (halo_applies(p.E, hg)) {
+        TcArgs& a = L.args;
+        a.BN = choose_bn(p.Og); a.N = p.Og;
+        a.n_tiles = (int)cdiv(p.Og, a.BN); a.groups = p.G;
+        a.a_cblocks = p.Cgp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Og;
+        set_out(a, top);
+        a.col_g = p.Og; a.bias = bptr; a.relu = relu; a.beta = 0.f;
+        if (!halo_setup(L, hg, aptr, A.Ctot, p.N)) return fail(CAFFE_E_CUDA, "halo tile setup failed (activation)");
+        if (!encode_tiled_2d(&L.mapB, p.E, WB, (uint64_t)p.taps * p.Cgp, (uint64_t)p.O, (uint64_t)p.taps * p.Cgp * p.E,
+                             p.CH, a.BN / L.cg))
+            return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (weights)");
+        return run_tc(L, s, conv_flops(p), 0);
+    }
     L.esz = p.E; L.amode = A_IM2COL_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
     if (!encode_im2col_4d(&L.mapA, p.E, aptr, A.Ctot, A.W, A.H, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
                           p.php - (p.khp - 1), p.CH, 128))
@@ -541,6 +618,20 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
     const int lo_h = p.khp - 1 - p.php, lo_w = p.kwp - 1 - p.pwp;
     TcLaunch L;
     memset(&L, 0, sizeof L);
+    const HaloGeom hg{p.OH, p.OW, Hd, Wd, p.khp, p.kwp, lo_h, lo_w};
+    if (!p.s2d && halo_applies(p.E, hg)) {
+        TcArgs& a = L.args;
+        a.BN = choose_bn(p.Cge); a.N = p.Cge;
+        a.n_tiles = (int)cdiv(p.Cge, a.BN); a.groups = p.G;
+        a.a_cblocks = p.Ogp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Cge;
+        set_out(a, bottom_diff);
+        a.col_g = p.Cg; a.beta = beta;
+        if (!halo_setup(L, hg, aptr, A.Ctot, p.N)) return fail(CAFFE_E_CUDA, "halo tile setup failed (top_diff)");
+        if (!encode_tiled_2d(&L.mapB, p.E, WD, (uint64_t)p.taps * p.Ogp, (uint64_t)p.G * p.Cge,
+                             (uint64_t)p.taps * p.Ogp * p.E, p.CH, a.BN / L.cg))
+            return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (dgrad weights)");
+        return run_tc(L, s, conv_flops(p), 0);
+    }
     L.esz = p.E; L.amode = A_IM2COL_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED;
     if (!encode_im2col_4d(&L.mapA, p.E, aptr, A.Ctot, p.OW, p.OH, p.N, lo_w, lo_h, lo_w - (p.kwp - 1),
                           lo_h - (p.khp - 1), p.CH, 128))
@@ -1101,16 +1192,17 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     CK(stage_rows(bottom, N, K, E, cur, &B, &ldb, s), "stage bottom");
     TcLaunch L;
     memset(&L, 0, sizeof L);
-    // dW^T tiles: M runs over the fan-in k, N over the outputs o, so each epilogue store instruction
-    // writes 32 consecutive k of one dW row (coalesced); the reduction runs over the batch.
+    // dW tiles: M runs over the outputs o, N over the fan-in k; each epilogue thread writes 16
+    // consecutive k of its dW row as float4 vectors (measured faster than the transposed,
+    // lane-coalesced layout); the reduction runs over the batch.
     L.esz = E; L.amode = A_TILED_MN; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
     TcArgs& a = L.args;
-    a.BN = choose_bn(O < 256 ? O : 256);
-    if (!encode_tiled_2d(&L.mapA, E, B, ldb, N, ldb * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, A, lda, N, lda * E, 64, 64))
+    a.BN = choose_bn((int)(K < 256 ? K : 256));
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, 64, 64))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip wgrad)");
-    a.M = (int)K; a.N = O; a.m_tiles = (int)cdiv(K, 128); a.n_tiles = (int)cdiv(O, a.BN); a.groups = 1; a.splits = 1;
+    a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1; a.splits = 1;
     a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
-    a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = 1; a.s_c = K; a.s_p = 0; a.P = 1; a.beta = beta;
+    a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
     finish_args(a, a.b_nchunks * 64 * 128);
     return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }

@@ -1,0 +1,116 @@
+// epilogue.cuh -- the strided (bias / beta / ReLU / bf16-or-fp32) tensor-core epilogue shared by
+// the GEMM kernels: one thread owns one accumulator row (TMEM lane) and writes its BN columns.
+#pragma once
+#include "internal.h"
+#include "ptx.cuh"
+#include <cuda_bf16.h>
+
+namespace cb {
+
+// taddr: TMEM address of this warp's lanes, column 0 of the accumulator.  rbase: element offset of
+// the output row; col0: first tile column (for the N bound); cbase: output channel of tile column 0;
+// bs: this tile's bias staged in shared memory (or unused when args.bias == nullptr).
+__device__ __forceinline__ void epi_store_strided(const TcArgs& args, uint32_t taddr, bool row_ok, long long rbase,
+                                                  int col0, int cbase, const float* bs) {
+    const bool rowvec = args.s_c == 1;        // channels-last / row-major output
+    const bool bf = args.out_bf16 != 0;
+    const float beta = args.beta;
+    const int relu = args.relu;
+    auto emit16 = [&](const uint32_t (&v)[16], int c0) {
+        const int nvalid = min(16, args.N - (col0 + c0));
+        float x[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) x[j] = __uint_as_float(v[j]);
+        if (args.bias) {
+            const float4* b4 = reinterpret_cast<const float4*>(bs + c0);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; q4++) {
+                const float4 b = b4[q4];
+                x[4 * q4] += b.x; x[4 * q4 + 1] += b.y; x[4 * q4 + 2] += b.z; x[4 * q4 + 3] += b.w;
+            }
+        }
+        const long long off0 = rbase + (long long)(cbase + c0) * args.s_c;
+        if (rowvec && nvalid == 16 && (off0 & (bf ? 7 : 3)) == 0) {
+            if (bf) {
+                uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off0);
+                if (beta != 0.f) {
+                    uint4 a = o[0], b = o[1];
+                    const __nv_bfloat16* ha = reinterpret_cast<const __nv_bfloat16*>(&a);
+                    const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&b);
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        x[j] += beta * __bfloat162float(ha[j]);
+                        x[j + 8] += beta * __bfloat162float(hb[j]);
+                    }
+                }
+                if (relu) {
+#pragma unroll
+                    for (int j = 0; j < 16; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
+                }
+                uint4 pk[2];
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+                for (int j = 0; j < 8; j++) h2[j] = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+                o[0] = pk[0];
+                o[1] = pk[1];
+            } else {
+                float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + off0);
+                if (beta != 0.f) {
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; q4++) {
+                        const float4 a = o[q4];
+                        x[4 * q4] += beta * a.x; x[4 * q4 + 1] += beta * a.y;
+                        x[4 * q4 + 2] += beta * a.z; x[4 * q4 + 3] += beta * a.w;
+                    }
+                }
+                if (relu) {
+#pragma unroll
+                    for (int j = 0; j < 16; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
+                }
+#pragma unroll
+                for (int q4 = 0; q4 < 4; q4++)
+                    o[q4] = make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
+            }
+        } else {
+            // column-coalesced scalar path (NCHW: the 32 lanes write 32 consecutive pixels)
+            const long long sc = args.s_c;
+            if (bf) {
+                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + off0;
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    if (j < nvalid) {
+                        float y = x[j];
+                        if (beta != 0.f) y += beta * __bfloat162float(o[j * sc]);
+                        if (relu) y = y > 0.f ? y : 0.f;
+                        o[j * sc] = __float2bfloat16_rn(y);
+                    }
+                }
+            } else {
+                float* o = reinterpret_cast<float*>(args.out) + off0;
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    if (j < nvalid) {
+                        float y = x[j];
+                        if (beta != 0.f) y += beta * o[j * sc];
+                        if (relu) y = y > 0.f ? y : 0.f;
+                        o[j * sc] = y;
+                    }
+                }
+            }
+        }
+    };
+    // two 16-column TMEM loads in flight per wait
+    for (int c0 = 0; c0 < args.BN; c0 += 32) {
+        if (col0 + c0 >= args.N) break;  // warp-uniform
+        const bool two = c0 + 16 < args.BN && col0 + c0 + 16 < args.N;
+        uint32_t v0[16], v1[16];
+        tmem_ld16(taddr + c0, v0);
+        if (two) tmem_ld16(taddr + c0 + 16, v1);
+        tmem_wait_ld();
+        if (!row_ok) continue;
+        emit16(v0, c0);
+        if (two) emit16(v1, c0 + 16);
+    }
+}
+
+}  // namespace cb

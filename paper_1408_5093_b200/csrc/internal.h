@@ -10,7 +10,7 @@ namespace cb {
 // ------------------------------------------------------------------ tensor-core GEMM (tc_gemm.cu)
 // D[m, n] = sum_k A[m, k] * B[n, k], A/B staged by TMA in 128-byte-swizzled shared memory,
 // tcgen05.mma (M=128, N=BN, K=16 bf16 / 8 tf32) accumulating FP32 in TMEM.
-enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3 };
+enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3, A_HALO_K = 4 };
 enum BMode { B_TILED_K = 0, B_TILED_MN = 1 };
 enum EpiMode { EPI_STRIDED = 0, EPI_PARTIAL = 1 };
 
@@ -45,6 +45,14 @@ struct TcArgs {
     // partials keep the one-tile unit layout (unit = ((split*G+g)*m_tiles_real+mt)*n_tiles+nt).
     int macc;                           // 0/1 = one accumulator per unit
     int m_tiles_real;
+    // A_HALO_K (tc_halo.cu, stride-1 convolution): a tile is halo_th output rows x halo_wt columns
+    // (halo_wt = output width + kw - 1; columns >= out_w are discarded) of one image.  Its input
+    // window -- halo_rows = halo_th + kh - 1 rows x halo_wt columns x 64 channels -- is staged ONCE
+    // per channel block by a 4-D tiled TMA load, and every filter tap (i, j) reads it through a
+    // descriptor shifted by (i*halo_wt + j) rows of 128 bytes.
+    int halo_wt, halo_th, halo_rows, halo_kh, halo_slot;   // halo_slot: smem bytes per tile (1 KB multiple)
+    int tiles_per_img, total_tiles, out_h, out_w;
+    int a_stages;                       // halo stages in the A ring
 };
 
 struct TcLaunch {
@@ -60,11 +68,15 @@ size_t tc_smem_bytes(const TcArgs& a);
 // instrumentation (abi.cu): every kernel launch of the library is counted.
 void note_launch();
 cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s);
+cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s);
+size_t tc_halo_smem_bytes(const TcArgs& a);
 int num_sms();
 
 // TMA descriptor encoders (driver entry points resolved at runtime; no -lcuda needed).
 bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                      uint32_t box_inner, uint32_t box_outer);
+bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, uint32_t box_c,
+                     uint32_t box_w, uint32_t box_h);
 bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
                       int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels);
 

@@ -19,6 +19,7 @@
 // epilogues release the accumulator on the leader's barrier.
 #include "internal.h"
 #include "ptx.cuh"
+#include "epilogue.cuh"
 
 #include <cuda_bf16.h>
 
@@ -113,6 +114,14 @@ __global__ void __launch_bounds__(256, 1)
                 ay = r / args.a_OW;
                 ax = r - ay * args.a_OW;
             }
+            // im2col K order: kb = (i*kw + j)*cblocks + cbk, tracked incrementally (no per-stage division)
+            int cbk = 0, ti = 0, tj = 0;
+            if (AMODE == A_IM2COL_K) {
+                const int tap0 = kb0 / args.a_cblocks;
+                cbk = kb0 - tap0 * args.a_cblocks;
+                ti = tap0 / args.a_kw;
+                tj = tap0 - ti * args.a_kw;
+            }
             for (int kb = kb0; kb < kb1; kb++) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * stage_bytes;
@@ -124,14 +133,16 @@ __global__ void __launch_bounds__(256, 1)
                     if (CG == 2) tma_load_2d_cg2(sa, &mapA, &full[stage], kb * CH, g * args.a_row_g + m0);
                     else tma_load_2d(sa, &mapA, &full[stage], kb * CH, g * args.a_row_g + m0);
                 } else if (AMODE == A_IM2COL_K) {
-                    const int tap = kb / args.a_cblocks, cbk = kb - tap * args.a_cblocks;
-                    const int i = tap / args.a_kw, j = tap - i * args.a_kw;
                     if (CG == 2)
                         tma_load_im2col_4d_cg2(sa, &mapA, &full[stage], g * args.a_cpg + cbk * CH, ax - args.a_pad_w,
-                                               ay - args.a_pad_h, an, (uint16_t)j, (uint16_t)i);
+                                               ay - args.a_pad_h, an, (uint16_t)tj, (uint16_t)ti);
                     else
                         tma_load_im2col_4d(sa, &mapA, &full[stage], g * args.a_cpg + cbk * CH, ax - args.a_pad_w,
-                                           ay - args.a_pad_h, an, (uint16_t)j, (uint16_t)i);
+                                           ay - args.a_pad_h, an, (uint16_t)tj, (uint16_t)ti);
+                    if (++cbk == args.a_cblocks) {
+                        cbk = 0;
+                        if (++tj == args.a_kw) { tj = 0; ++ti; }
+                    }
                 } else if (AMODE == A_IM2COL_MN) {
                     const int p0 = kb * CH;   // first pixel of this reduction block
                     const int n0 = p0 / args.a_P;
@@ -278,10 +289,6 @@ __global__ void __launch_bounds__(256, 1)
                 const long long rbase = (long long)img * args.s_n + (long long)pix * args.s_p;
                 const int col0 = n_tile * args.BN;
                 const int cbase = g * args.col_g + col0;   // output channel of tile column 0
-                const bool rowvec = args.s_c == 1;        // channels-last / row-major output
-                const bool bf = args.out_bf16 != 0;
-                const float beta = args.beta;
-                const int relu = args.relu;
                 // stage this tile's bias once (double-buffered by accumulator: a warp can be at most
                 // one tile ahead of the slowest epilogue warp)
                 float* bs = sbias + acc * 256;
@@ -289,101 +296,7 @@ __global__ void __launch_bounds__(256, 1)
                     for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
-                auto emit16 = [&](const uint32_t (&v)[16], int c0) {
-                    const int nvalid = min(16, args.N - (col0 + c0));
-                    float x[16];
-#pragma unroll
-                    for (int j = 0; j < 16; j++) x[j] = __uint_as_float(v[j]);
-                    if (args.bias) {
-                        const float4* b4 = reinterpret_cast<const float4*>(bs + c0);
-#pragma unroll
-                        for (int q4 = 0; q4 < 4; q4++) {
-                            const float4 b = b4[q4];
-                            x[4 * q4] += b.x; x[4 * q4 + 1] += b.y; x[4 * q4 + 2] += b.z; x[4 * q4 + 3] += b.w;
-                        }
-                    }
-                    const long long off0 = rbase + (long long)(cbase + c0) * args.s_c;
-                    if (rowvec && nvalid == 16 && (off0 & (bf ? 7 : 3)) == 0) {
-                        if (bf) {
-                            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off0);
-                            if (beta != 0.f) {
-                                uint4 a = o[0], b = o[1];
-                                const __nv_bfloat16* ha = reinterpret_cast<const __nv_bfloat16*>(&a);
-                                const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&b);
-#pragma unroll
-                                for (int j = 0; j < 8; j++) {
-                                    x[j] += beta * __bfloat162float(ha[j]);
-                                    x[j + 8] += beta * __bfloat162float(hb[j]);
-                                }
-                            }
-                            if (relu) {
-#pragma unroll
-                                for (int j = 0; j < 16; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
-                            }
-                            uint4 pk[2];
-                            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(pk);
-#pragma unroll
-                            for (int j = 0; j < 8; j++) h2[j] = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
-                            o[0] = pk[0];
-                            o[1] = pk[1];
-                        } else {
-                            float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + off0);
-                            if (beta != 0.f) {
-#pragma unroll
-                                for (int q4 = 0; q4 < 4; q4++) {
-                                    const float4 a = o[q4];
-                                    x[4 * q4] += beta * a.x; x[4 * q4 + 1] += beta * a.y;
-                                    x[4 * q4 + 2] += beta * a.z; x[4 * q4 + 3] += beta * a.w;
-                                }
-                            }
-                            if (relu) {
-#pragma unroll
-                                for (int j = 0; j < 16; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
-                            }
-#pragma unroll
-                            for (int q4 = 0; q4 < 4; q4++)
-                                o[q4] = make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
-                        }
-                    } else {
-                        // column-coalesced scalar path (NCHW: the 32 lanes write 32 consecutive pixels)
-                        const long long sc = args.s_c;
-                        if (bf) {
-                            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + off0;
-#pragma unroll
-                            for (int j = 0; j < 16; j++) {
-                                if (j < nvalid) {
-                                    float y = x[j];
-                                    if (beta != 0.f) y += beta * __bfloat162float(o[j * sc]);
-                                    if (relu) y = y > 0.f ? y : 0.f;
-                                    o[j * sc] = __float2bfloat16_rn(y);
-                                }
-                            }
-                        } else {
-                            float* o = reinterpret_cast<float*>(args.out) + off0;
-#pragma unroll
-                            for (int j = 0; j < 16; j++) {
-                                if (j < nvalid) {
-                                    float y = x[j];
-                                    if (beta != 0.f) y += beta * o[j * sc];
-                                    if (relu) y = y > 0.f ? y : 0.f;
-                                    o[j * sc] = y;
-                                }
-                            }
-                        }
-                    }
-                };
-                // two 16-column TMEM loads in flight per wait
-                for (int c0 = 0; c0 < args.BN; c0 += 32) {
-                    if (col0 + c0 >= args.N) break;  // warp-uniform
-                    const bool two = c0 + 16 < args.BN && col0 + c0 + 16 < args.N;
-                    uint32_t v0[16], v1[16];
-                    tmem_ld16(taddr + c0, v0);
-                    if (two) tmem_ld16(taddr + c0 + 16, v1);
-                    tmem_wait_ld();
-                    if (!row_ok) continue;
-                    emit16(v0, c0);
-                    if (two) emit16(v1, c0 + 16);
-                }
+                epi_store_strided(args, taddr, row_ok, rbase, col0, cbase, bs);
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
@@ -495,6 +408,21 @@ bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, 
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// channels-last activation [N][H][W][C] as a 4-D tiled map; box (box_c channels, box_w, box_h, 1)
+bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, uint32_t box_c,
+                     uint32_t box_w, uint32_t box_h) {
+    if (!resolve()) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)C * esz, (cuuint64_t)C * W * esz, (cuuint64_t)C * W * H * esz};
+    cuuint32_t box[4] = {box_c, box_w, box_h, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                          const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

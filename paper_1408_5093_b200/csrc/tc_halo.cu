@@ -1,0 +1,280 @@
+// tc_halo.cu -- stride-1 convolution as a halo-tiled implicit GEMM on tcgen05.
+//
+// The im2col formulation (tc_gemm.cu, A_IM2COL_K) stages a 128-pixel x 64-channel A tile per filter
+// tap, so every activation byte crosses L2->SM once per tap (25x for 5x5) and the passes run at the
+// chip's TMA throughput.  Here a work tile is halo_th whole output rows (padded to halo_wt =
+// OW + kw - 1 columns) of one image; its input window -- (halo_th + kh - 1) rows x halo_wt columns x
+// 64 channels -- is loaded ONCE per channel block with a 4-D tiled TMA (zero fill supplies the
+// padding), and tap (i, j) feeds tcgen05.mma the same shared-memory tile through a descriptor whose
+// start is moved by (i*halo_wt + j) rows of 128 bytes.  Accumulator row m = r*halo_wt + x is output
+// pixel (y0 + r, x); columns x >= OW are discarded by the epilogue.  (The 128-byte swizzle is a
+// function of the absolute shared-memory address, so row-shifted descriptors with base offset 0
+// read exactly the rows they name -- checked by tools/desc_probe.cu.)
+//
+// Used for the conv forward (A = X, B = repacked W) and the stride-1 data gradient (A = dY with pad
+// k-1-p, B = flipped W^T).  Paper: the layer contract P:156; formulas S:145.
+//
+// Roles: warp 0 lane 0 TMA producer (A ring of halo stages + B ring of per-tap weight tiles),
+// warp 1 MMA issuer (leader CTA; whole warp, one elected lane issues), warp 2 TMEM allocator,
+// warps 4..7 epilogue.  A unit holds `macc` tiles per CTA (accumulators) that share every B tile;
+// CG = 2 pairs two SMs (cta_group::2): each CTA stages its own tiles and half of each B tile.
+#include "internal.h"
+#include "ptx.cuh"
+#include "epilogue.cuh"
+
+#include <cuda_bf16.h>
+
+namespace cb {
+
+constexpr int HALO_SMEM_ALIGN = 1024;
+
+size_t tc_halo_smem_bytes(const TcArgs& a) {
+    const int macc = a.macc > 1 ? a.macc : 1;
+    return (size_t)a.a_stages * macc * a.halo_slot + (size_t)a.stages * a.b_stage_bytes + 512 /*barriers*/ +
+           2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN;
+}
+
+template <int CG, int MACC>
+__global__ void __launch_bounds__(256, 1)
+    tc_halo_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const TcArgs args) {
+    constexpr int CH = 64;                 // bf16 channels per 128-byte row
+    constexpr int KSTEPS = 4;              // K = 16 per tcgen05.mma
+    constexpr int TM = 128 * CG;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + HALO_SMEM_ALIGN - 1) &
+                                               ~uintptr_t(HALO_SMEM_ALIGN - 1));
+    constexpr int macc = MACC;             // accumulators (tiles) per CTA per unit
+    const int a_stages = args.a_stages, b_stages = args.stages;
+    const int slot = args.halo_slot;
+    const int a_stage_bytes = macc * slot;
+    uint8_t* a_ring = smem;
+    uint8_t* b_ring = smem + a_stages * a_stage_bytes;
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(b_ring + b_stages * args.b_stage_bytes);
+    uint64_t* emptyA = fullA + a_stages;
+    uint64_t* fullB = emptyA + a_stages;
+    uint64_t* emptyB = fullB + b_stages;
+    uint64_t* tfull = emptyB + b_stages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* sbias = reinterpret_cast<float*>(b_ring + b_stages * args.b_stage_bytes + 512);   // [2][256]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+    const int nslots = 2 * macc * args.acc_stride <= args.tmem_cols ? 2 : 1;
+    const int taps = args.halo_kh * args.a_kw;
+    const int cblocks = args.a_cblocks;
+    const int tiles_per_unit = macc * CG;
+    const int tgroups = (args.total_tiles + tiles_per_unit - 1) / tiles_per_unit;
+    const int units = args.groups * args.n_tiles * tgroups;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&mapA);
+        tma_prefetch(&mapB);
+        for (int i = 0; i < a_stages; i++) { mbar_init(&fullA[i], CG); mbar_init(&emptyA[i], 1); }
+        for (int i = 0; i < b_stages; i++) { mbar_init(&fullB[i], CG); mbar_init(&emptyB[i], 1); }
+        for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * CG); }
+        fence_barrier_init();
+    }
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_cg2(tmem_holder, args.tmem_cols);
+        else tmem_alloc(tmem_holder, args.tmem_cols);
+    }
+    tc_fence_before();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0 && lane == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        const uint32_t txA = (uint32_t)(macc * args.halo_rows * args.halo_wt * 128);
+        const uint32_t txB = (uint32_t)args.b_stage_bytes;
+        const int bn_cta = args.BN / CG;
+        int sa = 0, sb = 0;
+        uint32_t pa = 0, pb = 0;
+        for (int u = cid; u < units; u += ncl) {
+            int t = u;
+            const int n_tile = t % args.n_tiles; t /= args.n_tiles;
+            const int tg = t % tgroups;
+            const int g = t / tgroups;
+            for (int cb = 0; cb < cblocks; cb++) {
+                mbar_wait(&emptyA[sa], pa ^ 1);
+                if (CG == 1 || leader) mbar_arrive_expect_tx(&fullA[sa], txA * CG);
+                else mbar_arrive_cluster(mapa_shared(smem_u32(&fullA[sa]), 0));
+                for (int a = 0; a < macc; a++) {
+                    int tile = tg * tiles_per_unit + a * CG + (int)rank;
+                    if (tile >= args.total_tiles) tile = args.total_tiles - 1;   // rows discarded
+                    const int n = tile / args.tiles_per_img;
+                    const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;
+                    uint8_t* dst = a_ring + sa * a_stage_bytes + a * slot;
+                    const int c = g * args.a_cpg + cb * CH;
+                    if (CG == 2) tma_load_4d_cg2(dst, &mapA, &fullA[sa], c, -args.a_pad_w, y0 - args.a_pad_h, n);
+                    else tma_load_4d(dst, &mapA, &fullA[sa], c, -args.a_pad_w, y0 - args.a_pad_h, n);
+                }
+                if (++sa == a_stages) { sa = 0; pa ^= 1; }
+                for (int tap = 0; tap < taps; tap++) {
+                    mbar_wait(&emptyB[sb], pb ^ 1);
+                    if (CG == 1 || leader) mbar_arrive_expect_tx(&fullB[sb], txB * CG);
+                    else mbar_arrive_cluster(mapa_shared(smem_u32(&fullB[sb]), 0));
+                    const int kb = tap * cblocks + cb;
+                    const int row = g * args.b_row_g + n_tile * args.BN + (int)rank * bn_cta;
+                    uint8_t* dst = b_ring + sb * args.b_stage_bytes;
+                    if (CG == 2) tma_load_2d_cg2(dst, &mapB, &fullB[sb], kb * CH, row);
+                    else tma_load_2d(dst, &mapB, &fullB[sb], kb * CH, row);
+                    if (++sb == b_stages) { sb = 0; pb ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1 && leader) {
+        // ===================== MMA issuer (leader CTA, whole warp) =====================
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(args.BN >> 3) << 17) |
+                               ((uint32_t)(TM >> 4) << 24);
+        const uint32_t a_base = smem_u32(a_ring), b_base = smem_u32(b_ring);
+        int sa = 0, sb = 0, acc = 0, iters = 0;
+        uint32_t pa = 0, pb = 0, acc_phase = 0;
+        for (int u = cid; u < units; u += ncl, iters++) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * macc * args.acc_stride;
+            for (int cb = 0; cb < cblocks; cb++) {
+                mbar_wait(&fullA[sa], pa);
+                tc_fence_after();
+                const uint32_t sa_addr = a_base + sa * a_stage_bytes;
+                // tap (i, j) reads the staged window shifted by i*halo_wt + j rows (no division in
+                // the issue loop: the MMA warp's instruction latency bounds small-N tiles)
+                uint32_t shift = 0;
+                int tj = 0;
+                const uint32_t row_skip = (uint32_t)(args.halo_wt - args.a_kw + 1) * 128u;
+                for (int tap = 0; tap < taps; tap++) {
+                    mbar_wait(&fullB[sb], pb);
+                    tc_fence_after();
+                    const uint64_t bd0 = smem_desc_sw128(b_base + sb * args.b_stage_bytes, 16, 1024);
+                    if (elect_one()) {
+#pragma unroll
+                        for (int a = 0; a < MACC; a++) {
+                            const uint64_t ad0 = smem_desc_sw128(sa_addr + a * slot + shift, 16, 1024);
+                            const uint32_t dt = d_tmem + a * args.acc_stride;
+#pragma unroll
+                            for (int k = 0; k < KSTEPS; k++) {
+                                const uint32_t accum = (cb > 0 || tap > 0 || k > 0) ? 1u : 0u;
+                                if (CG == 2) umma_cg2<2>(dt, ad0 + 2 * k, bd0 + 2 * k, idesc, accum);
+                                else umma<2>(dt, ad0 + 2 * k, bd0 + 2 * k, idesc, accum);
+                            }
+                        }
+                        if (CG == 2) umma_commit_cg2(&emptyB[sb]);
+                        else umma_commit(&emptyB[sb]);
+                    }
+                    __syncwarp();
+                    if (++sb == b_stages) { sb = 0; pb ^= 1; }
+                    if (++tj == args.a_kw) { tj = 0; shift += row_skip; }
+                    else shift += 128u;
+                }
+                if (elect_one()) {
+                    if (CG == 2) umma_commit_cg2(&emptyA[sa]);
+                    else umma_commit(&emptyA[sa]);
+                }
+                __syncwarp();
+                if (++sa == a_stages) { sa = 0; pa ^= 1; }
+            }
+            if (elect_one()) {
+                if (CG == 2) umma_commit_cg2(&tfull[acc]);
+                else umma_commit(&tfull[acc]);
+            }
+            __syncwarp();
+            if (++acc == nslots) { acc = 0; acc_phase ^= 1; }
+        }
+        if (CG == 2 && iters > 0) {   // the peer's epilogue arrives remotely on our tempty barriers
+            if (nslots == 2) {
+                for (int j = iters - 2; j < iters; j++)
+                    if (j >= 0) mbar_wait(&tempty[j & 1], (uint32_t)((j >> 1) & 1));
+            } else {
+                mbar_wait(&tempty[0], (uint32_t)((iters - 1) & 1));
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (both CTAs) =====================
+        const int q = warp - 4;
+        const int row = q * 32 + lane;
+        const int yy = row / args.halo_wt, xx = row - yy * args.halo_wt;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        for (int u = cid; u < units; u += ncl) {
+            int t = u;
+            const int n_tile = t % args.n_tiles; t /= args.n_tiles;
+            const int tg = t % tgroups;
+            const int g = t / tgroups;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * macc * args.acc_stride;
+            const int col0 = n_tile * args.BN;
+            const int cbase = g * args.col_g + col0;
+            float* bs = sbias + acc * 256;
+            if (args.bias) {
+                for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+            for (int a = 0; a < macc; a++) {
+                const int tile = tg * tiles_per_unit + a * CG + (int)rank;
+                const int n = tile / args.tiles_per_img;
+                const int y = (tile - n * args.tiles_per_img) * args.halo_th + yy;
+                const bool row_ok = tile < args.total_tiles && yy < args.halo_th && y < args.out_h && xx < args.out_w;
+                const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + xx) * args.s_p;
+                epi_store_strided(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs);
+            }
+            tc_fence_before();
+            if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
+            else mbar_arrive(&tempty[acc]);
+            if (++acc == nslots) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        if (CG == 2) tmem_dealloc_cg2(tmem_base, args.tmem_cols);
+        else tmem_dealloc(tmem_base, args.tmem_cols);
+    }
+}
+
+template <int CG, int MACC>
+static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
+    auto kern = tc_halo_kernel<CG, MACC>;
+    const size_t smem = tc_halo_smem_bytes(L.args);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (CG == 1) {
+        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(L.grid);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CG;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.args);
+        if (e != cudaSuccess) return e;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s) {
+    if (L.esz != 2) return cudaErrorInvalidValue;
+    const int macc = L.args.macc > 1 ? L.args.macc : 1;
+    if (macc > 2) return cudaErrorInvalidValue;
+    if (L.cg == 2) return macc == 2 ? halo_launch_one<2, 2>(L, s) : halo_launch_one<2, 1>(L, s);
+    return macc == 2 ? halo_launch_one<1, 2>(L, s) : halo_launch_one<1, 1>(L, s);
+}
+
+}  // namespace cb

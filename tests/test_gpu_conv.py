@@ -249,3 +249,50 @@ def test_caffenet_conv1_full_image_wgrad(oracle, dy_layout):
     Yh = cb.conv_forward(Xh, cuda(Wt), None, stride=4, math="bf16")
     np.testing.assert_array_equal(host(Yh), host(cb.conv_forward(cuda(X), cuda(Wt), None, stride=4, math="bf16")
                                                   .to(torch.bfloat16).contiguous(memory_format=torch.channels_last)))
+
+
+HALO_CASES = CASES + [(2, 96, 27, 27, 64, (5, 5), (1, 1), (2, 2), 2),     # conv2 geometry (Cg=48, K padding)
+                      (1, 3, 227, 227, 32, (11, 11), (4, 4), (0, 0), 1),  # conv1 geometry (s2d, 55x55 out)
+                      (2, 64, 20, 37, 48, (3, 3), (1, 1), (1, 1), 1)]     # ragged last tile rows
+HALO_IDS = IDS + ["conv2geom", "conv1geom", "H20W37"]
+
+
+@pytest.mark.parametrize("cta", [1, 2])
+@pytest.mark.parametrize("halo", [1, 2])
+@pytest.mark.parametrize("case", HALO_CASES, ids=HALO_IDS)
+def test_conv_halo_tiles(oracle, case, halo, cta):
+    """Stride-1 forward / data gradient with halo tiles (one staged input window per channel block,
+    row-shifted descriptors per tap; CAFFE_TUNE_HALO=2 forces them wherever the geometry allows,
+    1 = per-tap im2col tiles) give the same parity, single-CTA and CTA-pair, NHWC bf16 operands."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 11)
+    if C == 3 and H == 227:
+        X = synth.int_pixels((N, C, H, W), 11)
+    q = oracle.quant_bf16
+    cl = torch.channels_last
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, halo)
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, cta)
+    try:
+        Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+        Y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True, out_dtype=torch.float32)
+        assert_tc_close(host(Y), oracle.conv_forward(host(Xd), q(Wt), b, stride=s, pad=p, group=g, relu=True),
+                        f"fwd halo={halo} cta={cta}")
+        if C == 3 and H == 227:
+            return   # the first layer has no data gradient in the net (and its s2d dgrad is not halo-tiled)
+        dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+        dX = torch.empty((N, C, H, W), device="cuda").contiguous(memory_format=cl)
+        cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
+        assert_tc_close(host(dX), oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g),
+                        f"dgrad halo={halo} cta={cta}")
+        # beta accumulation through the halo epilogue
+        prev = synth.uniform(X.shape, 12, synth.S_AUX)
+        dX2 = cuda(prev).contiguous(memory_format=cl)
+        cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, beta=1.0, out=dX2)
+        assert_tc_close(host(dX2), oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g) + prev,
+                        f"dgrad beta=1 halo={halo} cta={cta}")
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)

@@ -49,6 +49,9 @@ def main():
     if "--spin" in sys.argv:
         from paper_1408_5093_b200 import _abi
         _abi.call("caffe_set_tuning", 2, int(sys.argv[sys.argv.index("--spin") + 1]))
+    if "--halo" in sys.argv:
+        from paper_1408_5093_b200 import _abi
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, int(sys.argv[sys.argv.index("--halo") + 1]))
     if "--macc" in sys.argv:
         from paper_1408_5093_b200 import _abi
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_MACC, int(sys.argv[sys.argv.index("--macc") + 1]))
@@ -62,6 +65,18 @@ def main():
         y = cb.conv_forward(x, w, None, 1, 1, 1, relu=True)
         for _ in range(3):
             cb.conv_forward(x, w, None, 1, 1, 1, relu=True, out=y)
+        torch.cuda.synchronize()
+        return
+    if "--only-conv2" in sys.argv:   # for ncu: conv2 forward + data gradient
+        cl = torch.channels_last
+        x = torch.randn(256, 96, 27, 27, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+        w = torch.randn(256, 48, 5, 5, device=dev) * 0.05
+        y = cb.conv_forward(x, w, None, 1, 2, 2, relu=True)
+        dy = torch.randn_like(y)
+        dx = torch.empty_like(x)
+        for _ in range(2):
+            cb.conv_forward(x, w, None, 1, 2, 2, relu=True, out=y)
+            cb.conv_backward_data(dy, w, x.shape, 1, 2, 2, out=dx)
         torch.cuda.synchronize()
         return
     if "--only-fc6w" in sys.argv:   # for ncu: fc6 weight gradient / forward / data gradient
@@ -111,21 +126,24 @@ def main():
         ms_w = timeit(lambda: cb.ip_backward_weight(x, dy, w.shape, dw=dw, db=db))
         out[name] = {"fwd_us": round(ms * 1e3, 1), "dgrad_us": round(ms_d * 1e3, 1), "wgrad_us": round(ms_w * 1e3, 1),
                      "fwd_tflops": round(flops / ms / 1e9, 1), "wgrad_tflops": round(flops / ms_w / 1e9, 1)}
-    for name, (C, H, O, k, p, g) in {"conv2": (96, 27, 256, 5, 2, 2), "conv3": (256, 13, 384, 3, 1, 1),
-                                     "conv4": (384, 13, 384, 3, 1, 2), "conv5": (384, 13, 256, 3, 1, 2)}.items():
+    for name, (C, H, O, k, st, p, g) in {"conv1": (3, 227, 96, 11, 4, 0, 1), "conv2": (96, 27, 256, 5, 1, 2, 2),
+                                         "conv3": (256, 13, 384, 3, 1, 1, 1), "conv4": (384, 13, 384, 3, 1, 1, 2),
+                                         "conv5": (384, 13, 256, 3, 1, 1, 2)}.items():
         if "--only-fc" in sys.argv:
             break
         x = torch.randn(B, C, H, H, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
         w = torch.randn(O, C // g, k, k, device=dev) * 0.05
         bias = torch.zeros(O, device=dev)
-        y = cb.conv_forward(x, w, bias, 1, p, g, relu=True)
-        flops = 2 * B * O * H * H * (C // g) * k * k
-        ms = timeit(lambda: cb.conv_forward(x, w, bias, 1, p, g, relu=True, out=y))
+        y = cb.conv_forward(x, w, bias, st, p, g, relu=True)
+        OH = y.shape[2]
+        flops = 2 * B * O * OH * OH * (C // g) * k * k
+        ms = timeit(lambda: cb.conv_forward(x, w, bias, st, p, g, relu=True, out=y))
         dy = torch.randn_like(y)
-        ms_d = timeit(lambda: cb.conv_backward_data(dy, w, x.shape, 1, p, g, out=torch.empty_like(x)))
+        dxo = torch.empty_like(x)
+        ms_d = timeit(lambda: cb.conv_backward_data(dy, w, x.shape, st, p, g, out=dxo)) if name != "conv1" else float("nan")
         dw = torch.zeros_like(w)
         db = torch.zeros(O, device=dev)
-        ms_w = timeit(lambda: cb.conv_backward_weight(x, dy, w.shape, 1, p, g, dw=dw, db=db))
+        ms_w = timeit(lambda: cb.conv_backward_weight(x, dy, w.shape, st, p, g, dw=dw, db=db))
         out[name] = {"fwd_tflops": round(flops / ms / 1e9, 1), "dgrad_tflops": round(flops / ms_d / 1e9, 1),
                      "wgrad_tflops": round(flops / ms_w / 1e9, 1), "fwd_us": round(ms * 1e3, 1),
                      "dgrad_us": round(ms_d * 1e3, 1), "wgrad_us": round(ms_w * 1e3, 1)}
