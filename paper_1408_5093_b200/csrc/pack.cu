@@ -423,10 +423,78 @@ __global__ void gemm_partial_reduce_kernel(const float* __restrict__ part, int s
     }
 }
 
+// Vector form: one thread = one row m x 8 consecutive columns (BN % 8 == 0, N % 8 == 0, ldo % 8 == 0,
+// row-major output): 8 coalesced partial loads per split, one 16-byte (bf16) / 32-byte (fp32) store.
+__global__ void gemm_partial_reduce8_kernel(const float* __restrict__ part, int splits, int m_tiles, int n_tiles, int BN,
+                                            int TM, int M, int N, void* __restrict__ out, int obf16, long long ldo,
+                                            const float* __restrict__ bias, int relu, float beta, long long total) {
+    const long long sstride = (long long)m_tiles * n_tiles * BN * TM;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int m = (int)(t % M), n0 = (int)(t / M) * 8;
+        const int mt = m / TM, mr = m - mt * TM, nt = n0 / BN, nc = n0 - nt * BN;
+        const float* pp = part + (((long long)mt * n_tiles + nt) * BN + nc) * TM + mr;
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) acc[e] = 0.f;
+        for (int sp = 0; sp < splits; sp++) {   // ascending split order
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; e++) v[e] = pp[sp * sstride + (long long)e * TM];
+#pragma unroll
+            for (int e = 0; e < 8; e++) acc[e] += v[e];
+        }
+        if (bias) {
+#pragma unroll
+            for (int e = 0; e < 8; e++) acc[e] += bias[n0 + e];
+        }
+        const long long o = (long long)m * ldo + n0;
+        if (obf16) {
+            uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o);
+            if (beta != 0.f) {
+                const uint4 old = *p;
+                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&old);
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[e] += beta * __bfloat162float(h[e]);
+            }
+            if (relu) {
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[e] = acc[e] > 0.f ? acc[e] : 0.f;
+            }
+            uint4 pk;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; e++) h2[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+            *p = pk;
+        } else {
+            float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + o);
+            if (beta != 0.f) {
+                const float4 a = p[0], b = p[1];
+                acc[0] += beta * a.x; acc[1] += beta * a.y; acc[2] += beta * a.z; acc[3] += beta * a.w;
+                acc[4] += beta * b.x; acc[5] += beta * b.y; acc[6] += beta * b.z; acc[7] += beta * b.w;
+            }
+            if (relu) {
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[e] = acc[e] > 0.f ? acc[e] : 0.f;
+            }
+            p[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            p[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        }
+    }
+}
+
 cudaError_t gemm_partial_reduce(const float* part, int splits, int m_tiles, int n_tiles, int BN, int TM, int M, int N,
                                 void* out, int out_bf16, long long ldo, const float* bias, int relu, float beta, int pC,
                                 int pHW, cudaStream_t s) {
     const long long total = (long long)M * N;
+    const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    if (pC == 0 && BN % 8 == 0 && N % 8 == 0 && ldo % 8 == 0 && al) {
+        gemm_partial_reduce8_kernel<<<blocks_for(total / 8, 256), 256, 0, s>>>(part, splits, m_tiles, n_tiles, BN, TM, M, N,
+                                                                               out, out_bf16, ldo, bias, relu, beta,
+                                                                               total / 8);
+        note_launch();
+        return cudaGetLastError();
+    }
     gemm_partial_reduce_kernel<<<blocks_for(total, 256), 256, 0, s>>>(part, splits, m_tiles, n_tiles, BN, TM, M, N, out,
                                                                        out_bf16, ldo, bias, relu, beta, pC, pHW, total);
     note_launch();

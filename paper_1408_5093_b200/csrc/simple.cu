@@ -463,6 +463,10 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
 #pragma unroll
         for (int e = 0; e < 8; e++) { best[e] = 0.f; arg[e] = -1; }
         if (KH > 0) {
+            // Packed form of the strict '>' scan (R7): per bf16 pair, __hgt2_mask gives 0xFFFF lanes
+            // where the new value is strictly greater (false for NaN, as in the scalar scan); the
+            // running max and the running local window index (two 16-bit indices per word) are
+            // updated with bit selects.  The first in-image element seeds (it is never clipped).
             uint4 raw[KH > 0 ? KH : 1][KW > 0 ? KW : 1];
 #pragma unroll
             for (int i = 0; i < KH; i++)
@@ -471,18 +475,40 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
                     if (hs + i < he && ws + j < we)
                         raw[i][j] = *reinterpret_cast<const uint4*>(
                             x + (((long long)n * g.H + hs + i) * g.W + ws + j) * g.C + c0);
+            uint32_t bw[4] = {raw[0][0].x, raw[0][0].y, raw[0][0].z, raw[0][0].w};
+            uint32_t aw[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
             for (int i = 0; i < KH; i++)
 #pragma unroll
-                for (int j = 0; j < KW; j++)
+                for (int j = 0; j < KW; j++) {
+                    if (i == 0 && j == 0) continue;
                     if (hs + i < he && ws + j < we) {
-                        float v[8];
-                        unpack8(raw[i][j], v);
-                        const int me = (hs + i) * g.W + ws + j;
+                        const uint32_t vw[4] = {raw[i][j].x, raw[i][j].y, raw[i][j].z, raw[i][j].w};
+                        const uint32_t pp = (uint32_t)(i * KW + j) * 0x00010001u;
 #pragma unroll
-                        for (int e = 0; e < 8; e++)
-                            if (arg[e] < 0 || v[e] > best[e]) { best[e] = v[e]; arg[e] = me; }
+                        for (int e = 0; e < 4; e++) {
+                            const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vw[e]),
+                                                           *reinterpret_cast<const __nv_bfloat162*>(&bw[e]));
+                            bw[e] = (vw[e] & m) | (bw[e] & ~m);
+                            aw[e] = (pp & m) | (aw[e] & ~m);
+                        }
                     }
+                }
+            const long long o = (long long)t * 8;
+            *reinterpret_cast<uint4*>(y + o) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+            if (mask) {
+                int am[8];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const int p0 = (int)(aw[e] & 0xFFFFu), p1 = (int)(aw[e] >> 16);
+                    am[2 * e] = (hs + p0 / KW) * g.W + ws + p0 % KW;
+                    am[2 * e + 1] = (hs + p1 / KW) * g.W + ws + p1 % KW;
+                }
+                int4* mp = reinterpret_cast<int4*>(mask + o);
+                mp[0] = make_int4(am[0], am[1], am[2], am[3]);
+                mp[1] = make_int4(am[4], am[5], am[6], am[7]);
+            }
+            continue;
         } else {
             for (int h = hs; h < he; h++)
                 for (int w = ws; w < we; w++) {
@@ -785,6 +811,7 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
         const long long base = (long long)(t / cv) * C;
         float xv[24];
         load24(x + base, c0, C, xv);
+        // bf16 output: the MUFU lg2/ex2 power (rel. err ~1e-7) is far below the bf16 rounding step
         float out[8], S[8];
 #pragma unroll
         for (int e = 0; e < 8; e++) {
@@ -792,7 +819,7 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
 #pragma unroll
             for (int j = -R; j <= R; j++) s2 = fmaf(xv[8 + e + j], xv[8 + e + j], s2);
             S[e] = k + an * s2;
-            out[e] = xv[8 + e] * exp2f(-beta * log2f(S[e]));
+            out[e] = xv[8 + e] * __powf(S[e], -beta);
         }
         *reinterpret_cast<uint4*>(y + base + c0) = pack8(out);
         if (scale) {
@@ -816,6 +843,7 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
         load24(x + base, c0, C, xv);
         load24(y + base, c0, C, yv);
         load24(dy + base, c0, C, gv);
+        // bf16 output: approximate MUFU reciprocal / power are far below the bf16 rounding step
         float S[24], tv[24];
 #pragma unroll
         for (int i = 8 - R; i < 16 + R; i++) {
@@ -823,7 +851,7 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
 #pragma unroll
             for (int j = -R; j <= R; j++) s2 = fmaf(xv[i + j], xv[i + j], s2);
             S[i] = k + an * s2;
-            tv[i] = gv[i] * yv[i] / S[i];
+            tv[i] = __fdividef(gv[i] * yv[i], S[i]);
         }
         float out[8];
 #pragma unroll
@@ -831,7 +859,7 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
             float acc = 0.f;
 #pragma unroll
             for (int j = -R; j <= R; j++) acc += tv[8 + e + j];
-            out[e] = gv[8 + e] * exp2f(-beta * log2f(S[8 + e])) - 2.f * an * beta * xv[8 + e] * acc;
+            out[e] = gv[8 + e] * __powf(S[8 + e], -beta) - 2.f * an * beta * xv[8 + e] * acc;
         }
         *reinterpret_cast<uint4*>(dx + base + c0) = pack8(out);
     }
