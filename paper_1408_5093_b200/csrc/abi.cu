@@ -293,9 +293,54 @@ WgradSplit wgrad_split(const Plan& p) {
     }
     return w;
 }
+// ---- halo-tiled weight gradient (tc_halo.cu, A_HALO_MN): single 64-channel block layers
+int g_halo = 0;   // CAFFE_TUNE_HALO: 0 = automatic, 1 = off (im2col tiles), 2 = wherever it applies
+struct WgHalo {
+    bool use;
+    int Wt, TH, rows, tpi, total;              // tile geometry (output tile = TH rows x Wt columns)
+    int BN, n_tiles, nch, acc_stride, macc, pairs, mgroups, splits, kb_per, slot, bchunk, stages;
+};
+WgHalo wgrad_halo_plan(const Plan& p) {
+    WgHalo h;
+    memset(&h, 0, sizeof h);
+    if (p.E != 2 || g_halo == 1 || p.Cgp != 64 || p.taps < 2) return h;
+    h.Wt = p.OW + p.kwp - 1;
+    if (h.Wt > 128) return h;
+    h.TH = 128 / h.Wt;
+    h.tpi = (int)cdiv(p.OH, h.TH);
+    const double eff = (double)p.OH * p.OW / (h.tpi * 128.0);
+    if (g_halo != 2 && (p.taps < 4 || eff < 0.75)) return h;
+    h.rows = h.TH + p.khp - 1;
+    h.total = p.N * h.tpi;
+    h.BN = choose_bn(p.Og);
+    if (h.BN > 256) return h;
+    h.n_tiles = (int)cdiv(p.Og, h.BN);
+    h.nch = (int)cdiv(h.BN, 64);
+    h.acc_stride = (int)rup(h.BN, 32);
+    const int mmax = std::min(5, 512 / h.acc_stride);
+    h.pairs = (int)cdiv(p.taps, 2);
+    h.mgroups = (int)cdiv(h.pairs, mmax);
+    h.macc = (int)cdiv(h.pairs, h.mgroups);          // largest balanced group
+    const int need_rows = std::max(h.rows * h.Wt, 128 + (p.khp - 1) * h.Wt + (p.kwp - 1));
+    h.slot = (int)rup((long long)need_rows * 128, 1024);
+    h.bchunk = 128 * 128;                            // 128 pixel rows x 64 channels
+    const int stage = h.slot + h.nch * h.bchunk;
+    h.stages = std::min(8, (232448 - 256 - 1024) / stage);
+    if (h.stages < 2) return h;
+    const int base = p.G * h.n_tiles * h.mgroups;   // units per pixel split
+    int sp = std::max(1, 148 / base);
+    sp = std::min(sp, std::max(1, h.total / 4));
+    h.kb_per = (int)cdiv(h.total, sp);
+    h.splits = (int)cdiv(h.total, h.kb_per);
+    h.use = true;
+    return h;
+}
 size_t ws_partial(const Plan& p) {
     WgradSplit w = wgrad_split(p);
-    return align1k((size_t)w.m_tiles * w.n_tiles * p.G * w.splits * w.BN * 128 * 4);
+    size_t b = (size_t)w.m_tiles * w.n_tiles * p.G * w.splits * w.BN * 128 * 4;
+    const WgHalo h = wgrad_halo_plan(p);
+    if (h.use) b = std::max(b, (size_t)h.splits * p.G * h.pairs * h.n_tiles * h.BN * 128 * 4);
+    return align1k(b);
 }
 
 size_t conv_ws(const Plan& p, int pass, caffe_math m) {
@@ -318,7 +363,6 @@ caffe_status check_ws(void* ws, size_t have, size_t need) {
 
 // kind: 0 = convolution pass, 1 = inner product; flops = algorithmic FLOPs of the call
 // ---- halo-tiled stride-1 convolution (tc_halo.cu)
-int g_halo = 0;   // CAFFE_TUNE_HALO: 0 = automatic, 1 = off (im2col tiles), 2 = wherever it applies
 struct HaloGeom {
     int Hi, Wi, Ho, Wo, kh, kw, pad_h, pad_w;   // stride-1 geometry of the pass (input -> output)
 };
@@ -386,7 +430,9 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
         rec.b = prof_event();
         cudaEventRecord(rec.a, s);
     }
-    cudaError_t e = L.amode == A_HALO_K ? tc_halo_launch(L, s) : tc_launch(L, s);
+    cudaError_t e = L.amode == A_HALO_K    ? tc_halo_launch(L, s)
+                    : L.amode == A_HALO_MN ? tc_halo_wgrad_launch(L, s)
+                                           : tc_launch(L, s);
     if (g_prof) {
         cudaEventRecord(rec.b, s);
         std::lock_guard<std::mutex> lk(g_pmu);
@@ -714,6 +760,28 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
     if ((st = pack_if(B, top_diff, DYA, p.E, s))) return st;
     const void* aptr = A.packed ? XA : A.ptr;
     const void* bptr = B.packed ? DYA : B.ptr;
+    const WgHalo hw = wgrad_halo_plan(p);
+    if (hw.use) {
+        TcLaunch L;
+        memset(&L, 0, sizeof L);
+        L.esz = 2; L.amode = A_HALO_MN; L.bmode = B_TILED_MN; L.epi = EPI_PARTIAL; L.cg = 1;
+        if (!encode_tiled_4d(&L.mapA, 2, aptr, A.Ctot, A.W, A.H, p.N, 64, (uint32_t)hw.Wt, (uint32_t)hw.rows) ||
+            !encode_tiled_4d(&L.mapB, 2, bptr, B.Ctot, p.OW, p.OH, p.N, 64, (uint32_t)hw.Wt, (uint32_t)hw.TH))
+            return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (halo weight gradient)");
+        TcArgs& a = L.args;
+        a.BN = hw.BN; a.N = p.Og; a.n_tiles = hw.n_tiles; a.groups = p.G;
+        a.splits = hw.splits; a.kb_per_split = hw.kb_per; a.total_tiles = hw.total; a.tiles_per_img = hw.tpi;
+        a.halo_wt = hw.Wt; a.halo_th = hw.TH; a.halo_rows = hw.rows; a.halo_kh = p.khp; a.a_kw = p.kwp;
+        a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_cpg = A.cpg; a.b_col_g = B.cpg;
+        a.b_nchunks = hw.nch; a.b_stage_bytes = hw.nch * hw.bchunk; a.halo_slot = hw.slot; a.stages = hw.stages;
+        a.acc_stride = hw.acc_stride; a.macc = hw.macc; a.m_tiles_real = hw.pairs; a.m_tiles = hw.mgroups;
+        a.tmem_cols = 512; a.partial = PART;
+        a.units = p.G * hw.n_tiles * hw.mgroups * hw.splits;
+        if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
+        CK(wgrad_reduce(PART, (float*)weight_diff->ptr, beta, wgeom(p), hw.pairs, hw.n_tiles, hw.splits, hw.BN, 64, 1, s),
+           "wgrad reduce");
+        return CAFFE_OK;
+    }
     WgradSplit w = wgrad_split(p);
     TcLaunch L;
     memset(&L, 0, sizeof L);

@@ -10,7 +10,7 @@ namespace cb {
 // ------------------------------------------------------------------ tensor-core GEMM (tc_gemm.cu)
 // D[m, n] = sum_k A[m, k] * B[n, k], A/B staged by TMA in 128-byte-swizzled shared memory,
 // tcgen05.mma (M=128, N=BN, K=16 bf16 / 8 tf32) accumulating FP32 in TMEM.
-enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3, A_HALO_K = 4 };
+enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3, A_HALO_K = 4, A_HALO_MN = 5 };
 enum BMode { B_TILED_K = 0, B_TILED_MN = 1 };
 enum EpiMode { EPI_STRIDED = 0, EPI_PARTIAL = 1 };
 
@@ -69,6 +69,8 @@ size_t tc_smem_bytes(const TcArgs& a);
 void note_launch();
 cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s);
 cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s);
+cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s);
+size_t tc_halo_wgrad_smem_bytes(const TcArgs& a);
 size_t tc_halo_smem_bytes(const TcArgs& a);
 int num_sms();
 

@@ -241,6 +241,212 @@ __global__ void __launch_bounds__(256, 1)
     }
 }
 
+// ------------------------------------------------------------------ weight gradient (halo along K)
+// dW[(tap, c)][o] = sum_pixels X[pixel + shift(tap)][c] * dY[pixel][o]: the reduction index is the
+// pixel, so a K block is one output tile -- halo_th rows x halo_wt columns (columns >= OW are
+// zero-filled in the dY box and contribute nothing).  Its input window (one 64-channel block,
+// Cgp == 64) is staged ONCE and serves every tap: the MN-major A operand of tap t is the window
+// shifted by shift(t) = i*halo_wt + j rows, and an M=128 tile pairs two taps' 64-channel chunks
+// (the descriptor's leading byte offset = the distance between their shifted starts).  A unit
+// holds up to MACC such pairs (accumulators, single TMEM buffer) for one o-block and a split of
+// the pixel tiles; partials keep the one-pair unit layout [unit][BN][128] so wgrad_reduce applies.
+// Rows of the staged tiles beyond the TMA boxes are zeroed once and never written.
+template <int MACC>
+__global__ void __launch_bounds__(256, 1)
+    tc_halo_wgrad_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                         const TcArgs args) {
+    constexpr int KSTEPS = 8;              // 128 pixel rows per tile, K = 16 per tcgen05.mma
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + HALO_SMEM_ALIGN - 1) &
+                                               ~uintptr_t(HALO_SMEM_ALIGN - 1));
+    const int stages = args.stages;
+    const int slot = args.halo_slot;                       // A window bytes
+    const int bchunk = args.b_stage_bytes / args.b_nchunks; // one 64-channel dY chunk: 128 rows x 128 B
+    const int stage_bytes = slot + args.b_stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+    uint64_t* empty = full + stages;
+    uint64_t* tfull = empty + stages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int taps = args.halo_kh * args.a_kw;
+    const int pairs = args.m_tiles_real;
+    const int mgroups = args.m_tiles;
+    const int units = args.groups * args.n_tiles * mgroups * args.splits;
+
+    // zero the staging ring once: rows outside the TMA boxes must read as 0 (finite) forever
+    {
+        uint4* z = reinterpret_cast<uint4*>(smem);
+        const int n16 = stages * stage_bytes / 16;
+        for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&mapA);
+        tma_prefetch(&mapB);
+        for (int i = 0; i < stages; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 128);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_holder, args.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    auto decode = [&](int u, int& n_tile, int& mg, int& g, int& t0, int& t1) {
+        int t = u;
+        n_tile = t % args.n_tiles; t /= args.n_tiles;
+        mg = t % mgroups; t /= mgroups;
+        g = t % args.groups;
+        const int split = t / args.groups;
+        t0 = split * args.kb_per_split;
+        t1 = min(args.total_tiles, t0 + args.kb_per_split);
+    };
+
+    if (warp == 0 && lane == 0) {
+        // ===================== TMA producer =====================
+        const uint32_t tx = (uint32_t)(args.halo_rows * args.halo_wt * 128 +
+                                       args.b_nchunks * args.halo_th * args.halo_wt * 128);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            int n_tile, mg, g, t0, t1;
+            decode(u, n_tile, mg, g, t0, t1);
+            for (int tile = t0; tile < t1; tile++) {
+                const int n = tile / args.tiles_per_img;
+                const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_arrive_expect_tx(&full[stage], tx);
+                uint8_t* sa = smem + stage * stage_bytes;
+                tma_load_4d(sa, &mapA, &full[stage], g * args.a_cpg, -args.a_pad_w, y0 - args.a_pad_h, n);
+                for (int c = 0; c < args.b_nchunks; c++)
+                    tma_load_4d(sa + slot + c * bchunk, &mapB, &full[stage], g * args.b_col_g + n_tile * args.BN + c * 64,
+                                0, y0, n);
+                if (++stage == stages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (whole warp, one elected lane issues) =====================
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                               ((uint32_t)(args.BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        const uint32_t base = smem_u32(smem);
+        int stage = 0;
+        uint32_t phase = 0, acc_phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            int n_tile, mg, g, t0, t1;
+            decode(u, n_tile, mg, g, t0, t1);
+            const int pa0 = mg * pairs / mgroups, pa1 = (mg + 1) * pairs / mgroups;
+            // per accumulator: shifted start (bytes) of its first chunk and the distance to its second
+            uint32_t off[MACC], lbo[MACC];
+#pragma unroll
+            for (int a = 0; a < MACC; a++) {
+                const int q0 = 2 * (pa0 + a), q1 = q0 + 1;
+                const int s0 = (q0 / args.a_kw) * args.halo_wt + q0 % args.a_kw;
+                const int s1 = q1 < taps ? (q1 / args.a_kw) * args.halo_wt + q1 % args.a_kw : s0 + 1;
+                off[a] = (uint32_t)s0 * 128u;
+                lbo[a] = (uint32_t)(s1 - s0) * 128u;
+            }
+            mbar_wait(tempty, acc_phase ^ 1);
+            tc_fence_after();
+            for (int tile = t0; tile < t1; tile++) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t sa = base + stage * stage_bytes;
+                const uint64_t bd0 = smem_desc_sw128(sa + slot, (uint32_t)bchunk, 1024);
+                if (elect_one()) {
+#pragma unroll
+                    for (int a = 0; a < MACC; a++) {
+                        if (a < pa1 - pa0) {
+                            const uint64_t ad0 = smem_desc_sw128(sa + off[a], lbo[a], 1024);
+                            const uint32_t dt = tmem_base + a * args.acc_stride;
+#pragma unroll
+                            for (int k = 0; k < KSTEPS; k++) {
+                                const uint32_t accum = (tile > t0 || k > 0) ? 1u : 0u;
+                                umma<2>(dt, ad0 + (uint64_t)(k * 128), bd0 + (uint64_t)(k * 128), idesc, accum);
+                            }
+                        }
+                    }
+                    umma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == stages) { stage = 0; phase ^= 1; }
+            }
+            if (elect_one()) umma_commit(tfull);
+            __syncwarp();
+            acc_phase ^= 1;
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue: FP32 partials =====================
+        const int q = warp - 4;
+        const int row = q * 32 + lane;
+        uint32_t acc_phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            int n_tile, mg, g, t0, t1;
+            decode(u, n_tile, mg, g, t0, t1);
+            const int split = t0 / args.kb_per_split;
+            const int pa0 = mg * pairs / mgroups, pa1 = (mg + 1) * pairs / mgroups;
+            mbar_wait(tfull, acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
+            for (int a = 0; a < pa1 - pa0; a++) {
+                const size_t vu = (((size_t)split * args.groups + g) * pairs + (pa0 + a)) * args.n_tiles + n_tile;
+                float* dst = args.partial + vu * args.BN * 128 + row;
+                for (int c0 = 0; c0 < args.BN; c0 += 32) {
+                    const bool two = c0 + 16 < args.BN;
+                    uint32_t v0[16], v1[16];
+                    tmem_ld16(taddr + a * args.acc_stride + c0, v0);
+                    if (two) tmem_ld16(taddr + a * args.acc_stride + c0 + 16, v1);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; j++) dst[(size_t)(c0 + j) * 128] = __uint_as_float(v0[j]);
+                    if (two) {
+#pragma unroll
+                        for (int j = 0; j < 16; j++) dst[(size_t)(c0 + 16 + j) * 128] = __uint_as_float(v1[j]);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty);
+            acc_phase ^= 1;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, args.tmem_cols);
+    }
+}
+
+size_t tc_halo_wgrad_smem_bytes(const TcArgs& a) {
+    return (size_t)a.stages * (a.halo_slot + a.b_stage_bytes) + 256 + HALO_SMEM_ALIGN;
+}
+
+template <int MACC>
+static cudaError_t halo_wgrad_launch_one(const TcLaunch& L, cudaStream_t s) {
+    auto kern = tc_halo_wgrad_kernel<MACC>;
+    const size_t smem = tc_halo_wgrad_smem_bytes(L.args);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s) {
+    switch (L.args.macc) {
+        case 1: return halo_wgrad_launch_one<1>(L, s);
+        case 2: return halo_wgrad_launch_one<2>(L, s);
+        case 3: return halo_wgrad_launch_one<3>(L, s);
+        case 4: return halo_wgrad_launch_one<4>(L, s);
+        case 5: return halo_wgrad_launch_one<5>(L, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <int CG, int MACC>
 static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
     auto kern = tc_halo_kernel<CG, MACC>;

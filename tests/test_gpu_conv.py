@@ -280,9 +280,17 @@ def test_conv_halo_tiles(oracle, case, halo, cta):
         Y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True, out_dtype=torch.float32)
         assert_tc_close(host(Y), oracle.conv_forward(host(Xd), q(Wt), b, stride=s, pad=p, group=g, relu=True),
                         f"fwd halo={halo} cta={cta}")
+        dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+        if cta == 1:   # weight gradient (single-CTA kernel): halo along the pixel reduction
+            dW, db = cb.conv_backward_weight(Xd, dYd, Wt.shape, stride=s, pad=p, group=g, math="bf16")
+            rW, rb = oracle.conv_backward_weight(host(Xd), host(dYd), Wt.shape, stride=s, pad=p, group=g)
+            assert_tc_close(host(dW), rW, f"wgrad halo={halo}")
+            assert_fp32_close(host(db), rb, f"bias grad halo={halo}")
+            dW2, _ = cb.conv_backward_weight(Xd, dYd, Wt.shape, stride=s, pad=p, group=g, math="bf16", beta=1.0,
+                                             dw=dW.clone(), db=db.clone())
+            np.testing.assert_array_equal(host(dW2), 2 * host(dW))
         if C == 3 and H == 227:
             return   # the first layer has no data gradient in the net (and its s2d dgrad is not halo-tiled)
-        dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
         dX = torch.empty((N, C, H, W), device="cuda").contiguous(memory_format=cl)
         cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
         assert_tc_close(host(dX), oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g),

@@ -22,9 +22,11 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uin
 constexpr int ROWS = 256;     // smem rows of 128 B (64 bf16) for A
 constexpr int N = 16;         // MMA N
 
+// mode 2: A MN-major, one tile of ROWS k-rows x 64 m; M chunk 0 starts at row r, chunk 1 at row r+d
+//         (LBO = d*128 bytes, not a multiple of the 1024-byte atom): D[m][n] = sum_k T[r+(m/64)*d+k][m%64]*B[n][k]
 // mode 0: A K-major, M rows shifted by r.   D[m][n] = sum_k A[r+m][k] * B[n][k]  (K = 64)
 // mode 1: A MN-major, K rows shifted by r.  D[m][n] = sum_k A[r+k][m] * B[n][k]  (M = 64 per chunk x2? use M=128: 2 chunks)
-__global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D, int mode, int r, int use_base) {
+__global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D, int mode, int r, int use_base, int d) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sa = smem;                          // mode 0: ROWS x 128 B; mode 1: 2 chunks x ROWS x 128 B
@@ -39,12 +41,12 @@ __global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D, 
         const int pc = c16 ^ ((addr >> 7) & 7);
         *reinterpret_cast<uint4*>(rowbase + pc * 16) = v;
     };
-    const int nchunkA = mode == 0 ? 1 : 2;
+    const int nchunkA = mode == 1 ? 2 : 1;
     for (int i = tid; i < nchunkA * ROWS * 8; i += blockDim.x) {
         const int ch = i / (ROWS * 8), row = (i / 8) % ROWS, c16 = i % 8;
         uint4 v;
         // mode 0: A row = m (global A is ROWS x 64, K contiguous); mode 1: A row = k, 64 m per chunk
-        if (mode == 0) v = *reinterpret_cast<const uint4*>(A + row * 64 + c16 * 8);
+        if (mode == 0 || mode == 2) v = *reinterpret_cast<const uint4*>(A + row * 64 + c16 * 8);
         else v = *reinterpret_cast<const uint4*>(A + row * 128 + ch * 64 + c16 * 8);   // A global: ROWS(k) x 128(m)
         put(sa + ch * ROWS * 128 + row * 128, c16, v);
     }
@@ -67,16 +69,19 @@ __global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D, 
     const uint32_t tmem = tmem_holder;
     if (tid == 0) {
         // idesc: D f32, A/B bf16, a_major (bit 15) = mode, b K-major, N>>3 at 17, M>>4 at 24 (M = 128)
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)mode << 15) | ((uint32_t)(N >> 3) << 17) |
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(mode != 0) << 15) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(128 >> 4) << 24);
         for (int k = 0; k < 4; k++) {   // K = 64 in 4 steps of 16
             uint64_t ad;
             if (mode == 0) {
                 const uint32_t s = smem_u32(sa) + r * 128 + k * 32;
                 ad = desc_sw128(s, 16, 1024, use_base ? ((s >> 7) & 7) : 0);
-            } else {
+            } else if (mode == 1) {
                 const uint32_t s = smem_u32(sa) + (r + k * 16) * 128;
                 ad = desc_sw128(s, ROWS * 128, 1024, use_base ? ((s >> 7) & 7) : 0);
+            } else {
+                const uint32_t s = smem_u32(sa) + (r + k * 16) * 128;
+                ad = desc_sw128(s, d * 128, 1024, 0);
             }
             const uint32_t sbb = smem_u32(sb) + k * 32;
             const uint64_t bd = desc_sw128(sbb, 16, 1024, 0);
@@ -125,12 +130,31 @@ int main() {
     const int smem = 2 * ROWS * 128 + N * 128 + 2048;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     std::vector<float> hD(128 * N);
+    // mode 2: chunk offsets d (rows) of 1, 3, 31, 57 and 8, for shifts r
+    for (int d : {1, 3, 8, 31, 57}) {
+        int bad = 0;
+        for (int r = 0; r < 16; r++) {
+            cudaMemset(dD, 0, 128 * N * 4);
+            probe<<<1, 128, smem>>>(dA, dB, dD, 2, r, 0, d);
+            if (cudaDeviceSynchronize() != cudaSuccess) { printf("CUDA error\n"); return 1; }
+            cudaMemcpy(hD.data(), dD, 128 * N * 4, cudaMemcpyDeviceToHost);
+            double maxerr = 0;
+            for (int m = 0; m < 128; m++)
+                for (int n = 0; n < N; n++) {
+                    double ref = 0;
+                    for (int k = 0; k < 64; k++) ref += (double)fA[(r + (m / 64) * d + k) * 64 + (m % 64)] * fB[n * 64 + k];
+                    maxerr = fmax(maxerr, fabs(ref - hD[m * N + n]));
+                }
+            if (maxerr > 0) bad++;
+        }
+        printf("==> mode 2 (MN-major, chunk LBO = %d rows): %d of 16 shifts wrong\n", d, bad);
+    }
     for (int mode = 0; mode < 2; mode++)
         for (int use_base = 0; use_base < 2; use_base++) {
             int bad_shifts = 0;
             for (int r = 0; r < 16; r++) {
                 cudaMemset(dD, 0, 128 * N * 4);
-                probe<<<1, 128, smem>>>(dA, dB, dD, mode, r, use_base);
+                probe<<<1, 128, smem>>>(dA, dB, dD, mode, r, use_base, 0);
                 cudaError_t e = cudaDeviceSynchronize();
                 if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
                 cudaMemcpy(hD.data(), dD, 128 * N * 4, cudaMemcpyDeviceToHost);
