@@ -128,6 +128,10 @@ caffe_status caffe_device_check(void);
    once for all filter taps (halo tiles); 0 = automatic (default), 1 = off (per-tap im2col tiles),
    2 = wherever the geometry allows. */
 #define CAFFE_TUNE_HALO 4
+/* CAFFE_TUNE_TMA_STORE: 1 (default) = tensor-core epilogues of row-major / channels-last outputs
+   (beta 0) stage 32-row tiles in shared memory and write them with TMA tensor stores; 0 = direct
+   per-thread vector stores.  Bit-identical results. */
+#define CAFFE_TUNE_TMA_STORE 5
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -25,6 +25,7 @@ CAFFE_TUNE_CTA_PAIR = 1
 CAFFE_TUNE_MMA_SPIN = 2
 CAFFE_TUNE_WGRAD_MACC = 3
 CAFFE_TUNE_HALO = 4
+CAFFE_TUNE_TMA_STORE = 5
 
 
 class Shape4(ctypes.Structure):

@@ -228,6 +228,21 @@ void finish_args(TcArgs& a, int bstage) {
     a.tmem_cols = pow2ceil(a.tmem_cols);
     a.units = a.m_tiles * a.n_tiles * a.groups * a.splits;
 }
+// TMA-store epilogue for a row-major output [rows][ld] (cols valid): only plain stores (beta == 0),
+// whole 128-byte column boxes inside each tile, 16-byte aligned rows.  Call after finish_args.
+int g_tma_store = 1;   // CAFFE_TUNE_TMA_STORE
+void enable_tma_store(TcLaunch& L, void* out, int esz, long long cols, long long rows, long long ld, bool groups_ok) {
+    TcArgs& a = L.args;
+    const int cw = 128 / esz;
+    if (!g_tma_store || a.beta != 0.f || !groups_ok || a.BN % cw != 0 || (ld * esz) % 16 != 0 ||
+        (reinterpret_cast<uintptr_t>(out) & 15) != 0 || (a.macc > 1))
+        return;
+    if (!encode_store_2d(&L.mapC, esz, out, (uint64_t)cols, (uint64_t)rows, (uint64_t)ld)) return;
+    a.tma_store = 1;
+    const int macc = a.macc > 1 ? a.macc : 1;
+    const int stage = macc * 16384 + a.b_stage_bytes;
+    a.stages = std::min(8, (200 * 1024 - 33 * 1024) / stage);
+}
 void set_out(TcArgs& a, const caffe_blob* b) {
     // m = image * P + pixel;  column = output channel
     const caffe_shape4& s = b->shape;
@@ -494,6 +509,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_mma_spin = value ? 1 : 0;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_TMA_STORE) {
+        g_tma_store = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_HALO) {
         if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "halo mode must be 0 (auto), 1 (off) or 2 (force)");
         g_halo = value;
@@ -625,6 +644,9 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     set_out(a, top);
     a.col_g = p.Og; a.bias = bptr; a.relu = relu; a.beta = 0.f;
     finish_args(a, a.BN / L.cg * 128);
+    if (nhwc(top))
+        enable_tma_store(L, top->ptr, isbf(top) ? 2 : 4, p.O, (long long)p.N * p.OH * p.OW, p.O,
+                         p.G == 1 || p.Og % a.BN == 0);
     return run_tc(L, s, conv_flops(p), 0);
 }
 
@@ -704,6 +726,9 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
         a.col_g = p.Cge; a.beta = 0.f;
     }
     finish_args(a, a.BN / L.cg * 128);
+    if (!p.s2d && nhwc(bottom_diff))
+        enable_tma_store(L, bottom_diff->ptr, isbf(bottom_diff) ? 2 : 4, p.C, (long long)p.N * p.H * p.W, p.C,
+                         p.G == 1 || p.Cg % a.BN == 0);
     if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
     if (p.s2d) CK(unpack_s2d_grad(T, bottom_diff->ptr, isbf(bottom_diff), nhwc(bottom_diff), beta, tg, s), "unpack s2d gradient");
     return CAFFE_OK;
@@ -1139,6 +1164,7 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
     a.out = top->ptr; a.out_bf16 = isbf(top); a.s_n = O; a.s_c = 1; a.s_p = 0; a.P = 1; a.col_g = 0;
     a.bias = bptr; a.relu = relu; a.beta = 0.f; a.partial = part;
     finish_args(a, a.BN * 128);
+    if (!part) enable_tma_store(L, top->ptr, isbf(top) ? 2 : 4, O, N, O, true);
     if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
     if (part)
         CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128, N, O, top->ptr, isbf(top), O, bptr, relu,
@@ -1203,6 +1229,7 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
     }
     a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1;
     finish_args(a, a.b_nchunks * 64 * 128);
+    if (!part) enable_tma_store(L, a.out, a.out_bf16 ? 2 : 4, K, N, K, true);
     if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
     if (part)
         CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128, N, (int)K, bottom_diff->ptr,
@@ -1272,6 +1299,7 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
     a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
     finish_args(a, a.b_nchunks * 64 * 128);
+    enable_tma_store(L, weight_diff->ptr, 4, K, O, K, true);
     return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }
 

@@ -113,4 +113,65 @@ __device__ __forceinline__ void epi_store_strided(const TcArgs& args, uint32_t t
     }
 }
 
+// TMA-store form (row-major output, beta == 0): each epilogue warp stages its 32 rows x 128 bytes
+// (32 FP32 or 64 BF16 columns) in a 128-byte-swizzled shared buffer -- conflict-free 16-byte
+// writes -- and one lane issues a tensor store; two buffers per warp keep one store in flight.
+// Full 128-byte lines reach L2 instead of 32 partial lines per warp store instruction.
+// row0: output row of this warp's lane 0; ccol: output column of tile column 0; stage: 8 KB.
+__device__ __forceinline__ void epi_store_tma(const TcArgs& args, const CUtensorMap* mapC, uint32_t taddr, int row0,
+                                              int col0, int ccol, const float* bs, uint8_t* stage, int& buf,
+                                              int lane) {
+    const bool bf = args.out_bf16 != 0;
+    const int cw = bf ? 64 : 32;
+    for (int c0 = 0; c0 < args.BN; c0 += cw) {
+        if (col0 + c0 >= args.N) break;   // warp-uniform
+        uint32_t v[64];
+        tmem_ld16(taddr + c0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+        tmem_ld16(taddr + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+        if (bf) {
+            tmem_ld16(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
+            tmem_ld16(taddr + c0 + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
+        }
+        tmem_wait_ld();
+        float x[64];
+#pragma unroll
+        for (int j = 0; j < 64; j++) x[j] = __uint_as_float(v[j]);
+        if (args.bias) {
+#pragma unroll
+            for (int j = 0; j < 64; j++)
+                if (j < cw) x[j] += bs[c0 + j];
+        }
+        if (args.relu) {
+#pragma unroll
+            for (int j = 0; j < 64; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
+        }
+        if (lane == 0) tma_store_wait_read1();
+        __syncwarp();
+        uint8_t* st = stage + buf * 4096 + lane * 128;
+        const int sw = lane & 7;
+        if (bf) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                uint4 pk;
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+                for (int e = 0; e < 4; e++) h2[e] = __floats2bfloat162_rn(x[8 * j + 2 * e], x[8 * j + 2 * e + 1]);
+                *reinterpret_cast<uint4*>(st + ((j ^ sw) << 4)) = pk;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                *reinterpret_cast<float4*>(st + ((j ^ sw) << 4)) =
+                    make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(mapC, stage + buf * 4096, ccol + c0, row0);
+            tma_store_commit();
+        }
+        buf ^= 1;
+    }
+}
+
 }  // namespace cb

@@ -53,10 +53,11 @@ struct TcArgs {
     int halo_wt, halo_th, halo_rows, halo_kh, halo_slot;   // halo_slot: smem bytes per tile (1 KB multiple)
     int tiles_per_img, total_tiles, out_h, out_w;
     int a_stages;                       // halo stages in the A ring
+    int tma_store;                      // EPI_STRIDED: store tiles with TMA (mapC; row-major output, beta 0)
 };
 
 struct TcLaunch {
-    CUtensorMap mapA, mapB;
+    CUtensorMap mapA, mapB, mapC;
     TcArgs args;
     int esz;                            // 2 = bf16 (kind::f16), 4 = fp32 (kind::tf32)
     int amode, bmode, epi;
@@ -77,6 +78,9 @@ int num_sms();
 // TMA descriptor encoders (driver entry points resolved at runtime; no -lcuda needed).
 bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                      uint32_t box_inner, uint32_t box_outer);
+// row-major output matrix [rows][cols] (row pitch = ld elements) for TMA stores: box (128 B of
+// columns, 32 rows), 128-byte swizzle
+bool encode_store_2d(CUtensorMap* m, int esz, const void* base, uint64_t cols, uint64_t rows, uint64_t ld);
 bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, uint32_t box_c,
                      uint32_t box_w, uint32_t box_h);
 bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,

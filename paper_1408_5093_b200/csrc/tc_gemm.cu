@@ -32,16 +32,17 @@ constexpr int BM = 128;
 constexpr int A_STAGE_BYTES = 16384;   // 128 rows x 128 B
 constexpr int SMEM_ALIGN = 1024;
 
+constexpr int EPI_STAGE_BYTES = 4 * 2 * 4096;   // TMA-store staging: 4 epilogue warps x 2 buffers
 size_t tc_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
     return (size_t)a.stages * (macc * A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + 2 * 256 * 4 /*bias*/ +
-           SMEM_ALIGN;
+           SMEM_ALIGN + (a.tma_store ? 1024 + EPI_STAGE_BYTES : 0);
 }
 
 template <int ESZ, int AMODE, int BMODE, int EPI, int CG>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                   const TcArgs args) {
+                   const __grid_constant__ CUtensorMap mapC, const TcArgs args) {
     constexpr int CH = 128 / ESZ;          // elements per 128-byte row (= K per stage, = MN per chunk)
     constexpr int UMMA_K = 32 / ESZ;       // K per tcgen05.mma
     constexpr int KSTEPS = CH / UMMA_K;    // MMAs per stage (4)
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
     float* sbias = reinterpret_cast<float*>(smem + stages * stage_bytes + 256);   // [2][256]
+    uint8_t* epi_stage = smem + ((stages * stage_bytes + 256 + 2048 + 1023) & ~1023);   // TMA-store buffers
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(256, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        int tbuf = 0;
         for (int u = cid; u < args.units; u += ncl) {
             int t = u;
             const int n_tile = t % args.n_tiles; t /= args.n_tiles;
@@ -296,13 +299,19 @@ __global__ void __launch_bounds__(256, 1)
                     for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
-                epi_store_strided(args, taddr, row_ok, rbase, col0, cbase, bs);
+                if (args.tma_store) {
+                    epi_store_tma(args, &mapC, taddr, m_tile * TM + (int)rank * BM + q * 32, col0, cbase, bs,
+                                  epi_stage + q * 8192, tbuf, lane);
+                } else {
+                    epi_store_strided(args, taddr, row_ok, rbase, col0, cbase, bs);
+                }
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
             else mbar_arrive(&tempty[acc]);
             if (++acc == nslots) { acc = 0; acc_phase ^= 1; }
         }
+        if (args.tma_store && lane == 0) tma_store_wait_all();
     }
     tc_fence_before();
     if (CG == 2) cluster_sync_all();
@@ -333,7 +342,7 @@ static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (CG == 1) {
-        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.mapC, L.args);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(L.grid);
@@ -347,7 +356,7 @@ static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.args);
+        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.mapC, L.args);
         if (e != cudaSuccess) return e;
     }
     note_launch();
@@ -406,6 +415,19 @@ bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, 
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {row_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool encode_store_2d(CUtensorMap* m, int esz, const void* base, uint64_t cols, uint64_t rows, uint64_t ld) {
+    if (!resolve()) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * esz};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32};
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                          const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,

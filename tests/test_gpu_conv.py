@@ -304,3 +304,48 @@ def test_conv_halo_tiles(oracle, case, halo, cta):
     finally:
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
+
+
+@pytest.mark.parametrize("case", [CASES[7], (2, 64, 13, 13, 256, (3, 3), (1, 1), (1, 1), 2),
+                                  (2, 128, 13, 13, 384, (3, 3), (1, 1), (1, 1), 1)],
+                         ids=["C128O96", "C64O256g2", "C128O384"])
+def test_tma_store_epilogue_bit_identical(oracle, case):
+    """The TMA-store epilogue (CAFFE_TUNE_TMA_STORE=1, default) writes exactly what the direct-store
+    epilogue writes: conv forward (bias+ReLU, NHWC bf16 and fp32 out), data gradient, inner
+    product forward / data / weight gradient; and both match the oracle."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 21)
+    cl = torch.channels_last
+    Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    K = C * H * W
+    Wip = cuda(synth.xavier((512, K), 21)).to(torch.bfloat16)
+    dYip = cuda(synth.uniform((N, 512), 21, synth.S_DY)).to(torch.bfloat16)
+    outs = {}
+    try:
+        for mode in (0, 1):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_TMA_STORE, mode)
+            r = {}
+            r["y16"] = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True)
+            r["y32"] = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True,
+                                       out_dtype=torch.float32)
+            dX = torch.empty((N, C, H, W), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl)
+            cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
+            r["dx"] = dX
+            rows = Xd.permute(0, 2, 3, 1).reshape(N, -1).contiguous()   # any (N, K) bf16 rows
+            r["ip"] = cb.ip_forward(rows, Wip, None)
+            r["ipd"] = cb.ip_backward_data(dYip, Wip, (N, K, 1, 1))
+            r["ipw"], _ = cb.ip_backward_weight(rows, dYip, (512, K))
+            outs[mode] = {kk: host(v) for kk, v in r.items()}
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_TMA_STORE, 1)
+    for kk in outs[0]:
+        np.testing.assert_array_equal(outs[0][kk], outs[1][kk], err_msg=kk)
+    q = oracle.quant_bf16
+    assert_tc_close(outs[1]["y32"], oracle.conv_forward(host(Xd), q(Wt), b, stride=s, pad=p, group=g, relu=True),
+                    "fwd tma store")
+    assert_tc_close(outs[1]["dx"], oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g),
+                    "dgrad tma store", tol=3e-3)
