@@ -85,11 +85,15 @@ typedef struct {
 } caffe_blob;
 
 #define CAFFE_FUSE_RELU 1u /* conv/ip forward: apply max(0, .) in the epilogue */
+/* conv forward / backward_weight: the workspace already starts with the tensor-core operand of
+   `bottom` written by caffe_conv_pack_bottom (same desc, same bottom data, same workspace), so the
+   call does not rebuild it.  Ignored by FP32 math and when the operand is read from bottom directly. */
+#define CAFFE_BOTTOM_PREPACKED 2u
 
 typedef struct {
     int32_t kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w, group;
     caffe_math math;
-    uint32_t flags; /* CAFFE_FUSE_RELU */
+    uint32_t flags; /* CAFFE_FUSE_RELU | CAFFE_BOTTOM_PREPACKED */
 } caffe_conv_desc;
 
 typedef enum { CAFFE_POOL_MAX = 0, CAFFE_POOL_AVE = 1 } caffe_pool_method;
@@ -165,6 +169,16 @@ caffe_status caffe_conv_output_shape(const caffe_conv_desc* desc, caffe_shape4 b
    forward/backward-data.  `weight` is the weight blob shape. */
 caffe_status caffe_conv_workspace_size(const caffe_conv_desc* desc, caffe_shape4 bottom, caffe_shape4 weight,
                                        int32_t pass /* caffe_pass */, size_t* bytes /* host */);
+
+/* Builds the tensor-core operand of `bottom` (channels-last, groups padded, space-to-depth for
+   strided convs) at the start of `workspace` -- the work caffe_conv_forward and
+   caffe_conv_backward_weight repeat for every call -- so both can then run with
+   CAFFE_BOTTOM_PREPACKED on that workspace (the first layer's image batch is packed once per
+   step instead of twice).  `weight` supplies the filter geometry only.  Workspace: at least the
+   larger of the forward and backward-weight sizes.  No-op (CAFFE_OK) for FP32 math or when the
+   operand is read from bottom directly. */
+caffe_status caffe_conv_pack_bottom(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
+                                    void* workspace, size_t workspace_bytes, caffe_stream_t stream);
 
 /* Forward.  bottom F32|BF16, weight F32|BF16, bias F32 (nullable), top
    F32|BF16 (overwritten).  Fused ReLU with CAFFE_FUSE_RELU. */

@@ -121,12 +121,44 @@ def workspace(nbytes: int, device=None):
     return ctypes.c_void_p(p + off), buf.numel() - off
 
 
-def _conv_desc(kernel, stride, pad, group, math, relu=False):
+def _conv_desc(kernel, stride, pad, group, math, relu=False, prepacked=False):
     kh, kw = _pair(kernel)
     sh, sw = _pair(stride)
     ph, pw = _pair(pad)
-    return _abi.ConvDesc(kh, kw, sh, sw, ph, pw, int(group), MATH[math] if isinstance(math, str) else int(math),
-                         _abi.CAFFE_FUSE_RELU if relu else 0)
+    flags = (_abi.CAFFE_FUSE_RELU if relu else 0) | (_abi.CAFFE_BOTTOM_PREPACKED if prepacked else 0)
+    return _abi.ConvDesc(kh, kw, sh, sw, ph, pw, int(group), MATH[math] if isinstance(math, str) else int(math), flags)
+
+
+def _ws_arg(ws):
+    """(ptr, bytes) of a caller-owned workspace tensor (1 KB aligned start)."""
+    p = ws.data_ptr()
+    off = (-p) % 1024
+    return ctypes.c_void_p(p + off), ws.numel() * ws.element_size() - off
+
+
+def conv_bottom_workspace(x_shape, w_shape, stride=1, pad=0, group=1, math="bf16", device=None):
+    """A dedicated workspace tensor for conv_pack_bottom + conv_forward/conv_backward_weight with
+    prepacked=True on one layer (the larger of the two passes' sizes)."""
+    torch = _t()
+    kh, kw = w_shape[2], w_shape[3]
+    d = _conv_desc((kh, kw), stride, pad, group, math)
+    n = 0
+    for pass_ in (_abi.CAFFE_PASS_FORWARD, _abi.CAFFE_PASS_BACKWARD_WEIGHT):
+        v = ctypes.c_size_t()
+        call("caffe_conv_workspace_size", ctypes.byref(d), _abi.Shape4(*_shape4(x_shape)),
+             _abi.Shape4(*_shape4(w_shape)), int(pass_), ctypes.byref(v))
+        n = max(n, v.value)
+    return torch.empty(n + 2048, dtype=torch.uint8, device=device or torch.device("cuda"))
+
+
+def conv_pack_bottom(x, w, stride=1, pad=0, group=1, math="bf16", ws=None):
+    """Build the tensor-core operand of x once into `ws` (caffe_conv_pack_bottom) for later
+    conv_forward / conv_backward_weight calls with prepacked=True and the same ws."""
+    kh, kw = w.shape[2], w.shape[3]
+    d = _conv_desc((kh, kw), stride, pad, group, math)
+    p, n = _ws_arg(ws)
+    bx, bw = blob(x), blob(w)
+    call("caffe_conv_pack_bottom", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(bw), p, n, _stream())
 
 
 def conv_output_shape(in_shape, num_output, kernel, stride=1, pad=0, group=1):
@@ -143,15 +175,17 @@ def _conv_ws(d, in_shape, w_shape, pass_):
     return workspace(n.value)
 
 
-def conv_forward(x, w, b=None, stride=1, pad=0, group=1, math="bf16", relu=False, out=None, out_dtype=None):
-    """Y = W (*) X + b with groups/stride/zero-pad; optional fused ReLU."""
+def conv_forward(x, w, b=None, stride=1, pad=0, group=1, math="bf16", relu=False, out=None, out_dtype=None,
+                 ws=None, prepacked=False):
+    """Y = W (*) X + b with groups/stride/zero-pad; optional fused ReLU.  `ws` (+ prepacked)
+    selects a caller workspace already holding conv_pack_bottom's operand."""
     torch = _t()
     kh, kw = w.shape[2], w.shape[3]
-    d = _conv_desc((kh, kw), stride, pad, group, math, relu)
+    d = _conv_desc((kh, kw), stride, pad, group, math, relu, prepacked)
     oshape = conv_output_shape(x.shape, w.shape[0], (kh, kw), stride, pad, group)
     if out is None:
         out = empty_like_layout(oshape, out_dtype or x.dtype, x.device, like=x)
-    ws, wsz = _conv_ws(d, x.shape, w.shape, _abi.CAFFE_PASS_FORWARD)
+    ws, wsz = _ws_arg(ws) if ws is not None else _conv_ws(d, x.shape, w.shape, _abi.CAFFE_PASS_FORWARD)
     bx, bw, bb, by = blob(x), blob(w), blob(b), blob(out)
     call("caffe_conv_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(bw), _bp(bb), ctypes.byref(by), ws, wsz,
          _stream())
@@ -174,16 +208,16 @@ def conv_backward_data(dy, w, in_shape, stride=1, pad=0, group=1, math="bf16", b
 
 
 def conv_backward_weight(x, dy, w_shape, stride=1, pad=0, group=1, math="bf16", beta=0.0, dw=None, db=None,
-                         bias=True):
+                         bias=True, ws=None, prepacked=False):
     """dW = beta*dW + dY (*) X, db = beta*db + sum dY.  Returns (dW, db)."""
     torch = _t()
     kh, kw = w_shape[2], w_shape[3]
-    d = _conv_desc((kh, kw), stride, pad, group, math)
+    d = _conv_desc((kh, kw), stride, pad, group, math, prepacked=prepacked)
     if dw is None:
         dw = torch.zeros(tuple(w_shape), dtype=torch.float32, device=x.device)
     if bias and db is None:
         db = torch.zeros((w_shape[0],), dtype=torch.float32, device=x.device)
-    ws, wsz = _conv_ws(d, x.shape, w_shape, _abi.CAFFE_PASS_BACKWARD_WEIGHT)
+    ws, wsz = _ws_arg(ws) if ws is not None else _conv_ws(d, x.shape, w_shape, _abi.CAFFE_PASS_BACKWARD_WEIGHT)
     bx, bdy, bdw, bdb = blob(x), blob(dy), blob(dw), blob(db) if bias else None
     call("caffe_conv_backward_weight", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(bdy), ctypes.byref(bdw),
          _bp(bdb), float(beta), ws, wsz, _stream())

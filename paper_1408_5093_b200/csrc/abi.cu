@@ -572,6 +572,19 @@ static caffe_status conv_common(const caffe_conv_desc* desc, const caffe_blob* b
     return CAFFE_OK;
 }
 
+caffe_status caffe_conv_pack_bottom(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
+                                    void* ws, size_t ws_bytes, caffe_stream_t stream) {
+    Plan p;
+    caffe_status st = conv_common(desc, bottom, weight, &p);
+    if (st) return st;
+    if (desc->math == CAFFE_MATH_FP32 || p.N == 0) return CAFFE_OK;
+    const size_t need = std::max(conv_ws(p, CAFFE_PASS_FORWARD, desc->math),
+                                 conv_ws(p, CAFFE_PASS_BACKWARD_WEIGHT, desc->math));
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    Operand A = plan_x(bottom, p);
+    return pack_if(A, bottom, ws, p.E, (cudaStream_t)stream);
+}
+
 caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
                                 const caffe_blob* bias, caffe_blob* top, void* ws, size_t ws_bytes,
                                 caffe_stream_t stream) {
@@ -606,7 +619,7 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     Operand A = plan_x(bottom, p);
     void* XA = w8;
     void* WB = w8 + ws_x_max(p);
-    if ((st = pack_if(A, bottom, XA, p.E, s))) return st;
+    if (!(desc->flags & CAFFE_BOTTOM_PREPACKED) && (st = pack_if(A, bottom, XA, p.E, s))) return st;
     const void* aptr = A.packed ? XA : A.ptr;
     CK(repack_w_fwd(weight->ptr, isbf(weight), WB, p.E, wgeom(p), s), "repack weights");
     TcLaunch L;
@@ -781,7 +794,7 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
         CK(bias_grad(top_diff->ptr, isbf(top_diff), nhwc(top_diff), (float*)bias_diff->ptr, beta, p.N, p.O,
                      p.OH * p.OW, BPART, s),
            "bias grad");
-    if ((st = pack_if(A, bottom, XA, p.E, s))) return st;
+    if (!(desc->flags & CAFFE_BOTTOM_PREPACKED) && (st = pack_if(A, bottom, XA, p.E, s))) return st;
     if ((st = pack_if(B, top_diff, DYA, p.E, s))) return st;
     const void* aptr = A.packed ? XA : A.ptr;
     const void* bptr = B.packed ? DYA : B.ptr;

@@ -483,6 +483,61 @@ __global__ void gemm_partial_reduce8_kernel(const float* __restrict__ part, int 
     }
 }
 
+// NHWC-scatter form (inner-product data gradient into a channels-last blob): one thread = row m x
+// pixel hw x 8 consecutive channels c..c+7 (columns n = c*HW + hw of the (c,h,w) flatten), one
+// 16-byte (bf16) / 32-byte (fp32) store.  Requires pC % 8 == 0.  32-bit index math.
+__global__ void gemm_partial_reduce_nhwc8_kernel(const float* __restrict__ part, int splits, int m_tiles, int n_tiles,
+                                                 int BN, int TM, int M, void* __restrict__ out, int obf16, long long ldo,
+                                                 float beta, int pC, int pHW, int total) {
+    const long long sstride = (long long)m_tiles * n_tiles * BN * TM;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int m = t % M;
+        const int r = t / M;
+        const int hw = r % pHW, c0 = (r / pHW) * 8;
+        const int mt = m / TM, mr = m - mt * TM;
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) acc[e] = 0.f;
+        const float* pp[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const int n = (c0 + e) * pHW + hw, nt = n / BN, nc = n - nt * BN;
+            pp[e] = part + (((long long)mt * n_tiles + nt) * BN + nc) * TM + mr;
+        }
+        for (int sp = 0; sp < splits; sp++) {   // ascending split order
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; e++) v[e] = pp[e][sp * sstride];
+#pragma unroll
+            for (int e = 0; e < 8; e++) acc[e] += v[e];
+        }
+        const long long o = (long long)m * ldo + (long long)hw * pC + c0;
+        if (obf16) {
+            uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o);
+            if (beta != 0.f) {
+                const uint4 old = *p;
+                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&old);
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[e] += beta * __bfloat162float(h[e]);
+            }
+            uint4 pk;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; e++) h2[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+            *p = pk;
+        } else {
+            float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + o);
+            if (beta != 0.f) {
+                const float4 a = p[0], b = p[1];
+                acc[0] += beta * a.x; acc[1] += beta * a.y; acc[2] += beta * a.z; acc[3] += beta * a.w;
+                acc[4] += beta * b.x; acc[5] += beta * b.y; acc[6] += beta * b.z; acc[7] += beta * b.w;
+            }
+            p[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            p[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        }
+    }
+}
+
 cudaError_t gemm_partial_reduce(const float* part, int splits, int m_tiles, int n_tiles, int BN, int TM, int M, int N,
                                 void* out, int out_bf16, long long ldo, const float* bias, int relu, float beta, int pC,
                                 int pHW, cudaStream_t s) {
@@ -492,6 +547,13 @@ cudaError_t gemm_partial_reduce(const float* part, int splits, int m_tiles, int 
         gemm_partial_reduce8_kernel<<<blocks_for(total / 8, 256), 256, 0, s>>>(part, splits, m_tiles, n_tiles, BN, TM, M, N,
                                                                                out, out_bf16, ldo, bias, relu, beta,
                                                                                total / 8);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (pC > 0 && pC % 8 == 0 && !bias && !relu && al && ldo % 8 == 0 && total / 8 < (1LL << 31)) {
+        const int tv = (int)(total / 8);
+        gemm_partial_reduce_nhwc8_kernel<<<blocks_for(tv, 256), 256, 0, s>>>(part, splits, m_tiles, n_tiles, BN, TM, M,
+                                                                            out, out_bf16, ldo, beta, pC, pHW, tv);
         note_launch();
         return cudaGetLastError();
     }
@@ -538,8 +600,57 @@ __global__ void nhwc_to_rows_kernel(const void* __restrict__ src, int src_bf16, 
     }
 }
 
+// One block per image: the (HW x C) channels-last image is read coalesced into shared memory
+// (padded pitch C+1) and written as the (c,h,w)-ordered row, coalesced; 32-bit index math.
+__global__ void nhwc_to_rows_tiled_kernel(const void* __restrict__ src, int src_bf16, void* __restrict__ dst, int esz,
+                                          int C, int HW, int ld) {
+    extern __shared__ float tr_tile[];   // [HW][C + 1]
+    const int n = blockIdx.x;
+    const int CHW = C * HW;
+    const long long sb = (long long)n * CHW;
+    if (src_bf16 && C % 8 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        // 16-byte vectors (8 channels of one pixel), several in flight per thread
+        const uint4* v = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(src) + sb);
+#pragma unroll 4
+        for (int i = threadIdx.x; i < CHW / 8; i += blockDim.x) {
+            const uint4 u = v[i];
+            const int e0 = i * 8, p = e0 / C, c = e0 - p * C;
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const float2 f = __bfloat1622float2(h[q]);
+                tr_tile[p * (C + 1) + c + 2 * q] = f.x;
+                tr_tile[p * (C + 1) + c + 2 * q + 1] = f.y;
+            }
+        }
+    } else {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < CHW; i += blockDim.x) {
+            const int p = i / C, c = i - p * C;
+            tr_tile[p * (C + 1) + c] = ld_any(src, sb + i, src_bf16);
+        }
+    }
+    __syncthreads();
+    const long long db = (long long)n * ld;
+#pragma unroll 4
+    for (int k = threadIdx.x; k < ld; k += blockDim.x) {
+        float v = 0.f;
+        if (k < CHW) {
+            const int c = k / HW, p = k - c * HW;
+            v = tr_tile[p * (C + 1) + c];
+        }
+        st_elem(dst, db + k, esz, v);
+    }
+}
+
 cudaError_t nhwc_to_rows(const void* src, int src_bf16, void* dst, int dst_esz, int N, int C, int HW, long long ld,
                          cudaStream_t s) {
+    const size_t tile = (size_t)HW * (C + 1) * sizeof(float);
+    if (tile <= 48 * 1024 && ld < (1LL << 31)) {
+        nhwc_to_rows_tiled_kernel<<<N, 256, tile, s>>>(src, src_bf16, dst, dst_esz, C, HW, (int)ld);
+        note_launch();
+        return cudaGetLastError();
+    }
     const long long total = (long long)N * ld;
     nhwc_to_rows_kernel<<<blocks_for(total, 256), 256, 0, s>>>(src, src_bf16, dst, dst_esz, C, HW, ld, total);
     note_launch();

@@ -158,6 +158,13 @@ class Net:
                 self.mask[i] = cb.empty_like_layout(self.shapes[i + 1], torch.int32, device, nhwc=self.nhwc[i + 1])
         self.labels = torch.zeros(batch, dtype=torch.int32, device=device)
         self.loss = torch.zeros((), dtype=torch.float32, device=device)
+        # the first conv's operand (space-to-depth packed image batch) is built once per step into a
+        # dedicated workspace and reused by its forward and weight-gradient passes
+        self.ws0 = None
+        if layers[0].kind == "conv" and math != "fp32":
+            L0 = layers[0]
+            self.ws0 = cb.conv_bottom_workspace(self.shapes[0], tuple(self.W[0].shape), L0.stride, L0.pad, L0.group,
+                                                math, device)
 
     # --------------------------------------------------------------- one training iteration
     def _wop(self, i):
@@ -169,7 +176,11 @@ class Net:
             x = a[i]
             nxt = a[i + 1] if i + 1 < n - 1 else None
             if L.kind == "conv":
-                cb.conv_forward(x, self._wop(i), self.B[i], L.stride, L.pad, L.group, self.math, relu=L.relu, out=nxt)
+                pre = i == 0 and self.ws0 is not None
+                if pre:
+                    cb.conv_pack_bottom(x, self._wop(i), L.stride, L.pad, L.group, self.math, ws=self.ws0)
+                cb.conv_forward(x, self._wop(i), self.B[i], L.stride, L.pad, L.group, self.math, relu=L.relu, out=nxt,
+                                ws=self.ws0 if pre else None, prepacked=pre)
             elif L.kind == "pool":
                 cb.pool_forward(x, L.method, L.kernel, L.stride, L.pad, out=nxt, mask=self.mask[i])
             elif L.kind == "lrn":
@@ -198,8 +209,9 @@ class Net:
             if L.kind in ("conv", "ip") and L.relu and not self._relu_fused(i):
                 cb.relu_backward(y, dy, inplace=True)  # sign of the ReLU output == sign test on its input
             if L.kind == "conv":
+                pre = i == 0 and self.ws0 is not None
                 cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math, beta=0.0,
-                                        dw=self.dW[i], db=self.dB[i])
+                                        dw=self.dW[i], db=self.dB[i], ws=self.ws0 if pre else None, prepacked=pre)
                 if hook:
                     hook(i)
                 if i > 0:

@@ -349,3 +349,27 @@ def test_tma_store_epilogue_bit_identical(oracle, case):
                     "fwd tma store")
     assert_tc_close(outs[1]["dx"], oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g),
                     "dgrad tma store", tol=3e-3)
+
+
+@pytest.mark.parametrize("case", [CASES[3], CASES[6], CASES[1]], ids=[IDS[3], IDS[6], IDS[1]])
+def test_conv_prepacked_bottom(oracle, case):
+    """caffe_conv_pack_bottom + CAFFE_BOTTOM_PREPACKED on a dedicated workspace give the same bits
+    as packing inside each call (forward and weight gradient), for packed (s2d, NCHW) and direct
+    operands."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 31)
+    for xt in (cuda(X), cuda(X).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)):
+        w = cuda(Wt).to(torch.bfloat16)
+        ws = cb.conv_bottom_workspace(X.shape, Wt.shape, s, p, g, "bf16")
+        cb.conv_pack_bottom(xt, w, s, p, g, "bf16", ws=ws)
+        y1 = cb.conv_forward(xt, w, cuda(b), s, p, g, relu=True, ws=ws, prepacked=True, out_dtype=torch.float32)
+        y0 = cb.conv_forward(xt, w, cuda(b), s, p, g, relu=True, out_dtype=torch.float32)
+        np.testing.assert_array_equal(host(y1), host(y0))
+        dyt = cuda(dY) if xt.dtype == torch.float32 else cuda(dY).to(torch.bfloat16).contiguous(
+            memory_format=torch.channels_last)
+        dw1, db1 = cb.conv_backward_weight(xt, dyt, Wt.shape, s, p, g, ws=ws, prepacked=True)
+        dw0, db0 = cb.conv_backward_weight(xt, dyt, Wt.shape, s, p, g)
+        np.testing.assert_array_equal(host(dw1), host(dw0))
+        np.testing.assert_array_equal(host(db1), host(db0))
