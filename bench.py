@@ -132,7 +132,12 @@ def oracle_rate(batch_cap: int, seconds: float, steps: int = 1):
 
     run(1)  # warm (OpenMP pool, page faults)
     t1 = run(1)
-    b = max(1, min(batch_cap, int(seconds / max(t1, 1e-3))))
+    t2 = run(2)
+    # a step has a batch-independent part (fc weight update over 61 M parameters): size the sample
+    # from the marginal per-image time so it takes about `seconds`
+    per = max(t2 - t1, 1e-3)
+    fixed = max(t1 - per, 0.0)
+    b = max(1, min(batch_cap, int((seconds - fixed) / per)))
     total, imgs = 0.0, 0
     for _ in range(steps):
         total += run(b)
@@ -164,7 +169,12 @@ def reference_arm(args):
     t0 = time.perf_counter()
     onet.train_step(onet.CAFFENET, X1, params, moms, synth.labels(1, 1000, 0))
     t1 = time.perf_counter() - t0
-    b = max(1, int(per_step / max(t1, 1e-3)))
+    X2 = synth.int_pixels((2, 3, 227, 227), 0)
+    t0 = time.perf_counter()
+    onet.train_step(onet.CAFFENET, X2, params, moms, synth.labels(2, 1000, 0))
+    t2 = time.perf_counter() - t0
+    per, fixed = max(t2 - t1, 1e-3), max(2 * t1 - t2, 0.0)   # marginal per-image and batch-independent time
+    b = max(1, min(256, int((per_step - fixed) / per)))
     X = synth.int_pixels((b, 3, 227, 227), 0)
     lab = synth.labels(b, 1000, 0)
     for _ in range(args.warmup):
