@@ -136,6 +136,10 @@ caffe_status caffe_device_check(void);
    (beta 0) stage 32-row tiles in shared memory and write them with TMA tensor stores; 0 = direct
    per-thread vector stores.  Bit-identical results. */
 #define CAFFE_TUNE_TMA_STORE 5
+/* CAFFE_TUNE_ROWS_EPILOGUE: 1 = channels-last / row-major tensor-core outputs (beta 0) are staged
+   per warp in shared memory and written as whole 128-byte row segments; 0 (default) = each thread
+   stores its own row.  Bit-identical results. */
+#define CAFFE_TUNE_ROWS_EPILOGUE 6
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

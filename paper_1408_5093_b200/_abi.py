@@ -27,6 +27,7 @@ CAFFE_TUNE_MMA_SPIN = 2
 CAFFE_TUNE_WGRAD_MACC = 3
 CAFFE_TUNE_HALO = 4
 CAFFE_TUNE_TMA_STORE = 5
+CAFFE_TUNE_ROWS_EPILOGUE = 6
 
 
 class Shape4(ctypes.Structure):

@@ -243,6 +243,19 @@ void enable_tma_store(TcLaunch& L, void* out, int esz, long long cols, long long
     const int stage = macc * 16384 + a.b_stage_bytes;
     a.stages = std::min(8, (200 * 1024 - 33 * 1024) / stage);
 }
+// Row-staged coalesced epilogue (epi_store_rows) for s_c == 1 outputs with beta 0: 16-byte aligned
+// rows, group column offsets and N; TMEM slots wide enough for whole 128-byte column chunks.
+int g_rows_epi = 0;   // off by default: measured no gain for 128-byte-aligned rows (conv2) and a loss
+                      // for 192-byte pixel rows (conv1), where each 128-byte segment straddles two lines
+void enable_rows_epilogue(TcArgs& a) {
+    const int esz = a.out_bf16 ? 2 : 4, cw = 128 / esz;
+    const long long chunked = (a.BN + cw - 1) / cw * cw;
+    const bool ok = g_rows_epi && !a.tma_store && a.s_c == 1 && a.beta == 0.f &&
+                    (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.s_p * esz) % 16 == 0 &&
+                    (a.s_n * esz) % 16 == 0 && ((long long)a.col_g * esz) % 16 == 0 && (a.N * esz) % 16 == 0 &&
+                    (a.BN * esz) % 16 == 0 && a.acc_stride >= chunked;
+    a.rows_epi = ok ? 1 : 0;
+}
 void set_out(TcArgs& a, const caffe_blob* b) {
     // m = image * P + pixel;  column = output channel
     const caffe_shape4& s = b->shape;
@@ -251,6 +264,15 @@ void set_out(TcArgs& a, const caffe_blob* b) {
     a.P = s.h * s.w;
     a.out = b->ptr;
     a.out_bf16 = isbf(b);
+}
+void finish_rows_epilogue(TcArgs& a) {
+    enable_rows_epilogue(a);
+    if (a.rows_epi) {   // 16 KB of staging: keep the total under the 227 KB limit
+        const int macc = a.macc > 1 ? a.macc : 1;
+        const int stage = macc * 16384 + a.b_stage_bytes;
+        const int budget = (a.tma_store ? 167 : 200) * 1024 - 16 * 1024;
+        a.stages = std::min(a.stages, std::max(2, budget / stage));
+    }
 }
 
 struct WgradSplit {
@@ -435,6 +457,20 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
 
 caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     if (L.cg < 1) L.cg = 1;
+    if (L.epi == EPI_STRIDED && L.amode != A_HALO_MN) {
+        if (L.amode == A_HALO_K) {
+            enable_rows_epilogue(L.args);
+            if (L.args.rows_epi) {   // take the staging out of the B ring
+                const int macc = L.args.macc > 1 ? L.args.macc : 1;
+                const long long budget = 232448 - 512 - 2048 - 1024 - 16384 -
+                                         (long long)L.args.a_stages * macc * L.args.halo_slot;
+                L.args.stages = (int)std::min<long long>(L.args.stages, budget / L.args.b_stage_bytes);
+                if (L.args.stages < 2) L.args.rows_epi = 0;
+            }
+        } else {
+            finish_rows_epilogue(L.args);
+        }
+    }
     L.args.spin = g_mma_spin;
     const int slots = num_sms() / L.cg;                  // CTAs (or CTA pairs) resident at once
     L.grid = (L.args.units < slots ? L.args.units : slots) * L.cg;
@@ -511,6 +547,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     }
     if (key == CAFFE_TUNE_TMA_STORE) {
         g_tma_store = value ? 1 : 0;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_ROWS_EPILOGUE) {
+        g_rows_epi = value ? 1 : 0;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO) {

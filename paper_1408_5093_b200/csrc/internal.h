@@ -54,6 +54,7 @@ struct TcArgs {
     int tiles_per_img, total_tiles, out_h, out_w;
     int a_stages;                       // halo stages in the A ring
     int tma_store;                      // EPI_STRIDED: store tiles with TMA (mapC; row-major output, beta 0)
+    int rows_epi;                       // EPI_STRIDED: row-staged coalesced stores (epi_store_rows)
 };
 
 struct TcLaunch {

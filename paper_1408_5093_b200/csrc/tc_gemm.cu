@@ -33,10 +33,11 @@ constexpr int A_STAGE_BYTES = 16384;   // 128 rows x 128 B
 constexpr int SMEM_ALIGN = 1024;
 
 constexpr int EPI_STAGE_BYTES = 4 * 2 * 4096;   // TMA-store staging: 4 epilogue warps x 2 buffers
+constexpr int ROWS_STAGE_BYTES = 4 * 4096;      // row-staged epilogue: 4 epilogue warps x 4 KB
 size_t tc_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
     return (size_t)a.stages * (macc * A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + 2 * 256 * 4 /*bias*/ +
-           SMEM_ALIGN + (a.tma_store ? 1024 + EPI_STAGE_BYTES : 0);
+           SMEM_ALIGN + 1024 + (a.tma_store ? EPI_STAGE_BYTES : 0) + (a.rows_epi ? ROWS_STAGE_BYTES : 0);
 }
 
 template <int ESZ, int AMODE, int BMODE, int EPI, int CG>
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
     float* sbias = reinterpret_cast<float*>(smem + stages * stage_bytes + 256);   // [2][256]
     uint8_t* epi_stage = smem + ((stages * stage_bytes + 256 + 2048 + 1023) & ~1023);   // TMA-store buffers
+    uint8_t* rows_stage = epi_stage + (args.tma_store ? EPI_STAGE_BYTES : 0);            // row-staged epilogue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -302,6 +304,8 @@ __global__ void __launch_bounds__(256, 1)
                 if (args.tma_store) {
                     epi_store_tma(args, &mapC, taddr, m_tile * TM + (int)rank * BM + q * 32, col0, cbase, bs,
                                   epi_stage + q * 8192, tbuf, lane);
+                } else if (args.rows_epi) {
+                    epi_store_rows(args, taddr, row_ok, rbase, col0, cbase, bs, rows_stage + q * 4096, lane);
                 } else {
                     epi_store_strided(args, taddr, row_ok, rbase, col0, cbase, bs);
                 }

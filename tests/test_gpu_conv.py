@@ -307,12 +307,14 @@ def test_conv_halo_tiles(oracle, case, halo, cta):
 
 
 @pytest.mark.parametrize("case", [CASES[7], (2, 64, 13, 13, 256, (3, 3), (1, 1), (1, 1), 2),
-                                  (2, 128, 13, 13, 384, (3, 3), (1, 1), (1, 1), 1)],
-                         ids=["C128O96", "C64O256g2", "C128O384"])
+                                  (2, 128, 13, 13, 384, (3, 3), (1, 1), (1, 1), 1),
+                                  (2, 96, 27, 27, 64, (5, 5), (1, 1), (2, 2), 2), CASES[3]],
+                         ids=["C128O96", "C64O256g2", "C128O384", "conv2geom", "conv1like"])
 def test_tma_store_epilogue_bit_identical(oracle, case):
-    """The TMA-store epilogue (CAFFE_TUNE_TMA_STORE=1, default) writes exactly what the direct-store
-    epilogue writes: conv forward (bias+ReLU, NHWC bf16 and fp32 out), data gradient, inner
-    product forward / data / weight gradient; and both match the oracle."""
+    """The TMA-store and row-staged epilogues (CAFFE_TUNE_TMA_STORE, on by default /
+    CAFFE_TUNE_ROWS_EPILOGUE, off by default) write exactly what the per-thread direct-store epilogue writes: conv forward
+    (bias+ReLU, NHWC bf16 and fp32 out; im2col and halo tiles), data gradient, inner product
+    forward / data / weight gradient; and match the oracle."""
     import torch
     import paper_1408_5093_b200 as cb
     from paper_1408_5093_b200 import _abi
@@ -326,8 +328,9 @@ def test_tma_store_epilogue_bit_identical(oracle, case):
     dYip = cuda(synth.uniform((N, 512), 21, synth.S_DY)).to(torch.bfloat16)
     outs = {}
     try:
-        for mode in (0, 1):
-            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_TMA_STORE, mode)
+        for mode in (0, 1, 2):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_TMA_STORE, 1 if mode == 1 else 0)
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_ROWS_EPILOGUE, 0 if mode == 0 else 1)
             r = {}
             r["y16"] = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True)
             r["y32"] = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True,
@@ -342,8 +345,10 @@ def test_tma_store_epilogue_bit_identical(oracle, case):
             outs[mode] = {kk: host(v) for kk, v in r.items()}
     finally:
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_TMA_STORE, 1)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_ROWS_EPILOGUE, 0)
     for kk in outs[0]:
         np.testing.assert_array_equal(outs[0][kk], outs[1][kk], err_msg=kk)
+        np.testing.assert_array_equal(outs[0][kk], outs[2][kk], err_msg=kk)
     q = oracle.quant_bf16
     assert_tc_close(outs[1]["y32"], oracle.conv_forward(host(Xd), q(Wt), b, stride=s, pad=p, group=g, relu=True),
                     "fwd tma store")
