@@ -140,6 +140,10 @@ caffe_status caffe_device_check(void);
    per warp in shared memory and written as whole 128-byte row segments; 0 (default) = each thread
    stores its own row.  Bit-identical results. */
 #define CAFFE_TUNE_ROWS_EPILOGUE 6
+/* CAFFE_TUNE_SGD_BLOCKS_PER_SM: grid of caffe_sgd_update in 256-thread blocks per SM (0 = default 4).
+   1 leaves registers and thread slots for kernels running concurrently on other streams (an update
+   overlapped with the backward pass).  Read at launch time. */
+#define CAFFE_TUNE_SGD_BLOCKS_PER_SM 7
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

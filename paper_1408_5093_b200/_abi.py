@@ -28,6 +28,7 @@ CAFFE_TUNE_WGRAD_MACC = 3
 CAFFE_TUNE_HALO = 4
 CAFFE_TUNE_TMA_STORE = 5
 CAFFE_TUNE_ROWS_EPILOGUE = 6
+CAFFE_TUNE_SGD_BLOCKS_PER_SM = 7
 
 
 class Shape4(ctypes.Structure):

@@ -549,6 +549,11 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_tma_store = value ? 1 : 0;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_SGD_BLOCKS_PER_SM) {
+        if (value < 0 || value > 8) return fail(CAFFE_E_PARAM, "SGD blocks per SM must be 0 (default 4) .. 8");
+        g_sgd_blocks_per_sm = value == 0 ? 4 : value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_ROWS_EPILOGUE) {
         g_rows_epi = value ? 1 : 0;
         return CAFFE_OK;

@@ -8,6 +8,7 @@
 // (L4), and threads walk the OUTPUT in its memory order so warps read/write consecutive addresses
 // in either NCHW or NHWC.  Index math is 32-bit (blobs < 2^31 elements, checked by the ABI).
 #include "internal.h"
+#include <algorithm>
 
 #include <cuda_bf16.h>
 #include <cooperative_groups.h>
@@ -1034,44 +1035,72 @@ cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, 
 }
 
 // ================================================================ SGD (R18)
+// Two float4 per thread per iteration (both loaded before either is stored) so a grid of 4 blocks per
+// SM keeps enough bytes in flight for HBM while leaving thread slots free for a concurrently running
+// tensor-core kernel (the net overlaps each layer's update with the rest of the backward pass).
+__device__ __forceinline__ void sgd4(float4& wv, const float4& gv, float4& vv, float lr, float mom, float decay,
+                                     float gs) {
+    vv.x = mom * vv.x - lr * (gv.x * gs + decay * wv.x);
+    vv.y = mom * vv.y - lr * (gv.y * gs + decay * wv.y);
+    vv.z = mom * vv.z - lr * (gv.z * gs + decay * wv.z);
+    vv.w = mom * vv.w - lr * (gv.w * gs + decay * wv.w);
+    wv.x += vv.x; wv.y += vv.y; wv.z += vv.z; wv.w += vv.w;
+}
+__device__ __forceinline__ uint2 bf16x4(const float4& wv) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(wv.x, wv.y), b = __floats2bfloat162_rn(wv.z, wv.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&a);
+    pk.y = *reinterpret_cast<uint32_t*>(&b);
+    return pk;
+}
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
                            __nv_bfloat16* __restrict__ wb, long long n, float lr, float mom, float decay, float gs) {
     const long long n4 = n / 4;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n4; t += (long long)gridDim.x * blockDim.x) {
-        float4 wv = reinterpret_cast<const float4*>(w)[t];
-        const float4 gv = reinterpret_cast<const float4*>(g)[t];
-        float4 vv = reinterpret_cast<const float4*>(v)[t];
-        vv.x = mom * vv.x - lr * (gv.x * gs + decay * wv.x);
-        vv.y = mom * vv.y - lr * (gv.y * gs + decay * wv.y);
-        vv.z = mom * vv.z - lr * (gv.z * gs + decay * wv.z);
-        vv.w = mom * vv.w - lr * (gv.w * gs + decay * wv.w);
-        wv.x += vv.x; wv.y += vv.y; wv.z += vv.z; wv.w += vv.w;
-        reinterpret_cast<float4*>(v)[t] = vv;
-        reinterpret_cast<float4*>(w)[t] = wv;
-        if (wb) {
-            __nv_bfloat162 a = __floats2bfloat162_rn(wv.x, wv.y), b = __floats2bfloat162_rn(wv.z, wv.w);
-            uint2 pk;
-            pk.x = *reinterpret_cast<uint32_t*>(&a);
-            pk.y = *reinterpret_cast<uint32_t*>(&b);
-            reinterpret_cast<uint2*>(wb)[t] = pk;
-        }
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    float4* w4 = reinterpret_cast<float4*>(w);
+    float4* v4 = reinterpret_cast<float4*>(v);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    uint2* b4 = reinterpret_cast<uint2*>(wb);
+    long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; t + stride < n4; t += 2 * stride) {
+        const long long u = t + stride;
+        float4 wa = w4[t], wc = w4[u];
+        const float4 ga = g4[t], gc = g4[u];
+        float4 va = v4[t], vc = v4[u];
+        sgd4(wa, ga, va, lr, mom, decay, gs);
+        sgd4(wc, gc, vc, lr, mom, decay, gs);
+        v4[t] = va; v4[u] = vc;
+        w4[t] = wa; w4[u] = wc;
+        if (wb) { b4[t] = bf16x4(wa); b4[u] = bf16x4(wc); }
     }
-    for (long long t = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-        const float wv = w[t];
-        const float vv = mom * v[t] - lr * (g[t] * gs + decay * wv);
+    for (; t < n4; t += stride) {
+        float4 wa = w4[t];
+        const float4 ga = g4[t];
+        float4 va = v4[t];
+        sgd4(wa, ga, va, lr, mom, decay, gs);
+        v4[t] = va;
+        w4[t] = wa;
+        if (wb) b4[t] = bf16x4(wa);
+    }
+    for (long long q = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += stride) {
+        const float wv = w[q];
+        const float vv = mom * v[q] - lr * (g[q] * gs + decay * wv);
         const float nw = wv + vv;
-        v[t] = vv;
-        w[t] = nw;
-        if (wb) wb[t] = __float2bfloat16_rn(nw);
+        v[q] = vv;
+        w[q] = nw;
+        if (wb) wb[q] = __float2bfloat16_rn(nw);
     }
 }
 
+int g_sgd_blocks_per_sm = 4;   // CAFFE_TUNE_SGD_BLOCKS_PER_SM
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom, float decay,
                   float gscale, cudaStream_t s) {
     const bool al = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(w_bf16) & 7) == 0;
     if (!al) return cudaErrorMisalignedAddress;
-    sgd_kernel<<<148 * 8, 256, 0, s>>>(w, g, v, (__nv_bfloat16*)w_bf16, count, lr, mom, decay, gscale);
+    const long long want = (count / 4 + 511) / 512;   // blocks for 2 vectors per thread
+    const int grid = (int)std::max(1LL, std::min<long long>(148LL * g_sgd_blocks_per_sm, want));
+    sgd_kernel<<<grid, 256, 0, s>>>(w, g, v, (__nv_bfloat16*)w_bf16, count, lr, mom, decay, gscale);
     note_launch();
     return cudaGetLastError();
 }

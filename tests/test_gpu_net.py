@@ -124,3 +124,24 @@ def test_net_teacher_forced(oracle, which, batch, act):
         else:
             assert_tc_close(got, ref, f"{which} {L.name} dX")
     assert np.isfinite(float(net.loss))
+
+
+def test_overlapped_update_matches_serial():
+    """Net.step(overlap_update=True) (per-layer SGD on a side stream) gives the same parameters,
+    bit for bit, as the single update after the backward pass."""
+    import torch
+    import synth
+    from paper_1408_5093_b200 import nets
+    dev = torch.device("cuda")
+    outs = []
+    for overlap in (False, True):
+        net = nets.Net(nets.LENET, 16, nets.LENET_INPUT, dev, math="bf16", seed=3)
+        net.a[0].copy_(torch.from_numpy(synth.mnist_pixels((16,) + tuple(nets.LENET_INPUT), 3)).to(torch.bfloat16))
+        net.labels.copy_(torch.from_numpy(synth.labels(16, 10, 3)))
+        for _ in range(2):
+            net.step(overlap_update=overlap)
+        torch.cuda.synchronize()
+        outs.append((net.params.cpu().numpy().copy(), net.params_bf16.float().cpu().numpy().copy()))
+    import numpy as np
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
