@@ -334,22 +334,40 @@ WgradSplit wgrad_split(const Plan& p) {
 int g_halo = 0;   // CAFFE_TUNE_HALO: 0 = automatic, 1 = off (im2col tiles), 2 = wherever it applies
 struct WgHalo {
     bool use;
-    int Wt, TH, rows, tpi, total;              // tile geometry (output tile = TH rows x Wt columns)
+    int Wt, TH, rows, tpi, total, ksteps, cblocks;  // tile geometry (output tile = TH rows x Wt columns)
     int BN, n_tiles, nch, acc_stride, macc, pairs, mgroups, splits, kb_per, slot, bchunk, stages;
 };
 WgHalo wgrad_halo_plan(const Plan& p) {
     WgHalo h;
     memset(&h, 0, sizeof h);
-    if (p.E != 2 || g_halo == 1 || p.Cgp != 64 || p.taps < 2) return h;
+    if (p.E != 2 || g_halo == 1 || p.taps < 2) return h;
     h.Wt = p.OW + p.kwp - 1;
-    if (h.Wt > 128) return h;
-    h.TH = 128 / h.Wt;
+    if (h.Wt > 256) return h;
+    // tile = TH whole output rows (K rows padded to 16): the TH with the fewest idle K rows, up to 256
+    // rows (13x13 maps: one whole image per tile, 81% useful rows instead of 66% with 8-row tiles)
+    // (tiles of >= 112 rows -- or the whole image -- so the staged window and the per-tile barrier
+    // traffic stay amortised; ties go to the larger tile)
+    double best = -1.0;
+    const int max_rows = g_halo == 3 ? 128 : 256;   // CAFFE_TUNE_HALO 3: tiles of <= 128 pixel rows
+    const long long min_rows = std::min<long long>(112, rup((long long)p.OH * h.Wt, 16));
+    for (int th = 1; th <= p.OH && th * h.Wt <= max_rows; th++) {
+        if (rup((long long)th * h.Wt, 16) < min_rows) continue;
+        const int tpi = (int)cdiv(p.OH, th);
+        const double eff = (double)p.OH * p.OW / ((double)tpi * rup((long long)th * h.Wt, 16));
+        if (eff >= best - 1e-9) { best = eff; h.TH = th; }
+    }
+    if (h.TH == 0) return h;
+    if (g_halo < 2 && (p.taps < 4 || best < 0.75)) return h;
     h.tpi = (int)cdiv(p.OH, h.TH);
-    const double eff = (double)p.OH * p.OW / (h.tpi * 128.0);
-    if (g_halo != 2 && (p.taps < 4 || eff < 0.75)) return h;
+    h.ksteps = (int)cdiv((long long)h.TH * h.Wt, 16);
     h.rows = h.TH + p.khp - 1;
     h.total = p.N * h.tpi;
+    h.cblocks = p.Cgp / 64;
     h.BN = choose_bn(p.Og);
+    if (h.cblocks > 1) {   // every tap of a channel block in one unit: 5 accumulators of <= 96 columns
+        if (p.Og % 96 == 0) h.BN = 96;
+        else if (p.Og % 64 == 0) h.BN = 64;
+    }
     if (h.BN > 256) return h;
     h.n_tiles = (int)cdiv(p.Og, h.BN);
     h.nch = (int)cdiv(h.BN, 64);
@@ -358,13 +376,14 @@ WgHalo wgrad_halo_plan(const Plan& p) {
     h.pairs = (int)cdiv(p.taps, 2);
     h.mgroups = (int)cdiv(h.pairs, mmax);
     h.macc = (int)cdiv(h.pairs, h.mgroups);          // largest balanced group
-    const int need_rows = std::max(h.rows * h.Wt, 128 + (p.khp - 1) * h.Wt + (p.kwp - 1));
+    const int krows = h.ksteps * 16;
+    const int need_rows = std::max(h.rows * h.Wt, krows + (p.khp - 1) * h.Wt + (p.kwp - 1));
     h.slot = (int)rup((long long)need_rows * 128, 1024);
-    h.bchunk = 128 * 128;                            // 128 pixel rows x 64 channels
+    h.bchunk = (int)rup((long long)krows * 128, 1024);   // K rows x 64 channels
     const int stage = h.slot + h.nch * h.bchunk;
     h.stages = std::min(8, (232448 - 256 - 1024) / stage);
     if (h.stages < 2) return h;
-    const int base = p.G * h.n_tiles * h.mgroups;   // units per pixel split
+    const int base = p.G * h.n_tiles * h.mgroups * h.cblocks;   // units per pixel split
     int sp = std::max(1, 148 / base);
     sp = std::min(sp, std::max(1, h.total / 4));
     h.kb_per = (int)cdiv(h.total, sp);
@@ -376,7 +395,7 @@ size_t ws_partial(const Plan& p) {
     WgradSplit w = wgrad_split(p);
     size_t b = (size_t)w.m_tiles * w.n_tiles * p.G * w.splits * w.BN * 128 * 4;
     const WgHalo h = wgrad_halo_plan(p);
-    if (h.use) b = std::max(b, (size_t)h.splits * p.G * h.pairs * h.n_tiles * h.BN * 128 * 4);
+    if (h.use) b = std::max(b, (size_t)h.splits * p.G * h.cblocks * h.pairs * h.n_tiles * h.BN * 128 * 4);
     return align1k(b);
 }
 
@@ -412,7 +431,7 @@ static bool halo_applies(int E, const HaloGeom& h) {
     if (wt > 128 || h.Ho < 1) return false;
     const int th = 128 / wt;
     if (th + h.kh - 1 > 256) return false;
-    if (g_halo == 2) return true;
+    if (g_halo >= 2) return true;
     const int tpi = (h.Ho + th - 1) / th;
     const double eff = (double)h.Ho * h.Wo / (tpi * 128.0);
     return h.kh * h.kw >= 4 && eff >= 0.75;
@@ -559,7 +578,7 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO) {
-        if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "halo mode must be 0 (auto), 1 (off) or 2 (force)");
+        if (value < 0 || value > 3) return fail(CAFFE_E_PARAM, "halo mode must be 0 (auto), 1 (off), 2 (force), 3 (force, <=128-row tiles)");
         g_halo = value;
         return CAFFE_OK;
     }
@@ -858,10 +877,12 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
         a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_cpg = A.cpg; a.b_col_g = B.cpg;
         a.b_nchunks = hw.nch; a.b_stage_bytes = hw.nch * hw.bchunk; a.halo_slot = hw.slot; a.stages = hw.stages;
         a.acc_stride = hw.acc_stride; a.macc = hw.macc; a.m_tiles_real = hw.pairs; a.m_tiles = hw.mgroups;
+        a.a_cblocks = hw.cblocks; a.halo_ksteps = hw.ksteps;
         a.tmem_cols = 512; a.partial = PART;
-        a.units = p.G * hw.n_tiles * hw.mgroups * hw.splits;
+        a.units = p.G * hw.n_tiles * hw.mgroups * hw.cblocks * hw.splits;
         if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
-        CK(wgrad_reduce(PART, (float*)weight_diff->ptr, beta, wgeom(p), hw.pairs, hw.n_tiles, hw.splits, hw.BN, 64, 1, s),
+        CK(wgrad_reduce(PART, (float*)weight_diff->ptr, beta, wgeom(p), hw.cblocks * hw.pairs, hw.n_tiles, hw.splits,
+                        hw.BN, 64, hw.cblocks, s, 1),
            "wgrad reduce");
         return CAFFE_OK;
     }

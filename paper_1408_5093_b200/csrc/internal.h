@@ -52,6 +52,7 @@ struct TcArgs {
     // descriptor shifted by (i*halo_wt + j) rows of 128 bytes.
     int halo_wt, halo_th, halo_rows, halo_kh, halo_slot;   // halo_slot: smem bytes per tile (1 KB multiple)
     int tiles_per_img, total_tiles, out_h, out_w;
+    int halo_ksteps;                    // A_HALO_MN: K steps (16 pixel rows each) per pixel tile
     int a_stages;                       // halo stages in the A ring
     int tma_store;                      // EPI_STRIDED: store tiles with TMA (mapC; row-major output, beta 0)
     int rows_epi;                       // EPI_STRIDED: row-staged coalesced stores (epi_store_rows)
@@ -118,8 +119,10 @@ cudaError_t repack_w_fwd(const void* w, int w_bf16, void* dst, int dst_esz, cons
 cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, int Cge,
                            cudaStream_t s);
 // Deterministic fixed-order reduction of wgrad partials into dW (O, Cg, kh, kw) fp32 with beta.
+// cbmajor = 0: M tile = 2 consecutive chunks of q = tap*cblocks + cb (im2col wgrad);
+// cbmajor = 1: M tile (pair) = taps (2p, 2p+1) of one channel block, index cb*pairs + p (halo wgrad).
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
-                         int splits, int BN, int chunk, int cblocks, cudaStream_t s);
+                         int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor = 0);
 // Fixed-order reduction of split-K GEMM partials ([unit][BN][TM] fp32, unit = (s*m_tiles+mt)*n_tiles+nt)
 // into a row-major output (ldo) with bias, beta and ReLU; pC > 0 scatters each row's (c,h,w)-ordered
 // columns into an NHWC row of pC channels x pHW pixels.

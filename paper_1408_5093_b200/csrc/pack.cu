@@ -343,7 +343,7 @@ cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, co
 // packed (tap, cc) back to (c, i, j) of the original filter.
 __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dW, float beta, WGeom g,
                                     int m_tiles, int n_tiles, int splits, int BN, int chunk, int cblocks,
-                                    int chunks_per_tile, int total) {
+                                    int chunks_per_tile, int total, int cbmajor) {
     const int nq = g.khp * g.kwp * cblocks;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
         const int rr = t % chunk;
@@ -358,7 +358,9 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __
         const int d = cc / g.Cg, c = cc % g.Cg;
         const int i = (tap / g.kwp) * g.sh + d / g.sw, j = (tap % g.kwp) * g.sw + d % g.sw;
         if (i >= g.kh || j >= g.kw) continue;
-        const int m_tile = q / chunks_per_tile, row = (q % chunks_per_tile) * chunk + rr;
+        const int pairs = (g.khp * g.kwp + 1) / 2;
+        const int m_tile = cbmajor ? (q % cblocks) * pairs + tap / 2 : q / chunks_per_tile;
+        const int row = cbmajor ? (tap & 1) * chunk + rr : (q % chunks_per_tile) * chunk + rr;
         const int n_tile = o / BN, col = o % BN;
         // fixed ascending-split order; loads batched 4 at a time so they are in flight together
         const long long sstride = (long long)g.G * m_tiles * n_tiles * BN * 128;
@@ -377,10 +379,10 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __
 }
 
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
-                         int splits, int BN, int chunk, int cblocks, cudaStream_t s) {
+                         int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor) {
     const int total = g.G * g.Og * g.khp * g.kwp * cblocks * chunk;
     wgrad_reduce_kernel<<<blocks_for(total, 256), 256, 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
-                                                               chunk, cblocks, 128 / chunk, total);
+                                                               chunk, cblocks, 128 / chunk, total, cbmajor);
     note_launch();
     return cudaGetLastError();
 }

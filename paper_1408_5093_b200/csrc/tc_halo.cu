@@ -253,14 +253,18 @@ __global__ void __launch_bounds__(256, 1)
 // Cgp == 64) is staged ONCE and serves every tap: the MN-major A operand of tap t is the window
 // shifted by shift(t) = i*halo_wt + j rows, and an M=128 tile pairs two taps' 64-channel chunks
 // (the descriptor's leading byte offset = the distance between their shifted starts).  A unit
-// holds up to MACC such pairs (accumulators, single TMEM buffer) for one o-block and a split of
-// the pixel tiles; partials keep the one-pair unit layout [unit][BN][128] so wgrad_reduce applies.
-// Rows of the staged tiles beyond the TMA boxes are zeroed once and never written.
-template <int MACC>
+// holds up to MACC such pairs (accumulators, single TMEM buffer) for one o-block, one 64-channel
+// block and a split of the pixel tiles; a tile has KSTEPS*16 pixel rows (halo_th whole output rows
+// -- for 13x13 maps one whole image, 208 rows).  Partials [unit][BN][128] use the one-pair unit
+// index ((split*G + g)*(cblocks*pairs) + cb*pairs + pair)*n_tiles + n_tile; wgrad_reduce's
+// cb-major pair mode maps them back.  Rows of the staged tiles beyond the TMA boxes are zeroed
+// once and never written.
+template <int MACC, int KST>
 __global__ void __launch_bounds__(256, 1)
     tc_halo_wgrad_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const TcArgs args) {
-    constexpr int KSTEPS = 8;              // 128 pixel rows per tile, K = 16 per tcgen05.mma
+    // K steps of 16 pixel rows per tile: compile-time when KST > 0 (straight-line issue loop)
+    const int ksteps = KST > 0 ? KST : args.halo_ksteps;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + HALO_SMEM_ALIGN - 1) &
                                                ~uintptr_t(HALO_SMEM_ALIGN - 1));
@@ -278,7 +282,8 @@ __global__ void __launch_bounds__(256, 1)
     const int taps = args.halo_kh * args.a_kw;
     const int pairs = args.m_tiles_real;
     const int mgroups = args.m_tiles;
-    const int units = args.groups * args.n_tiles * mgroups * args.splits;
+    const int cblocks = args.a_cblocks > 0 ? args.a_cblocks : 1;
+    const int units = args.groups * args.n_tiles * mgroups * cblocks * args.splits;
 
     // zero the staging ring once: rows outside the TMA boxes must read as 0 (finite) forever
     {
@@ -301,10 +306,11 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
-    auto decode = [&](int u, int& n_tile, int& mg, int& g, int& t0, int& t1) {
+    auto decode = [&](int u, int& n_tile, int& mg, int& cb, int& g, int& t0, int& t1) {
         int t = u;
         n_tile = t % args.n_tiles; t /= args.n_tiles;
         mg = t % mgroups; t /= mgroups;
+        cb = t % cblocks; t /= cblocks;
         g = t % args.groups;
         const int split = t / args.groups;
         t0 = split * args.kb_per_split;
@@ -318,15 +324,15 @@ __global__ void __launch_bounds__(256, 1)
         int stage = 0;
         uint32_t phase = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
-            int n_tile, mg, g, t0, t1;
-            decode(u, n_tile, mg, g, t0, t1);
+            int n_tile, mg, cb, g, t0, t1;
+            decode(u, n_tile, mg, cb, g, t0, t1);
             for (int tile = t0; tile < t1; tile++) {
                 const int n = tile / args.tiles_per_img;
                 const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;
                 mbar_wait(&empty[stage], phase ^ 1);
                 mbar_arrive_expect_tx(&full[stage], tx);
                 uint8_t* sa = smem + stage * stage_bytes;
-                tma_load_4d(sa, &mapA, &full[stage], g * args.a_cpg, -args.a_pad_w, y0 - args.a_pad_h, n);
+                tma_load_4d(sa, &mapA, &full[stage], g * args.a_cpg + cb * 64, -args.a_pad_w, y0 - args.a_pad_h, n);
                 for (int c = 0; c < args.b_nchunks; c++)
                     tma_load_4d(sa + slot + c * bchunk, &mapB, &full[stage], g * args.b_col_g + n_tile * args.BN + c * 64,
                                 0, y0, n);
@@ -341,8 +347,8 @@ __global__ void __launch_bounds__(256, 1)
         int stage = 0;
         uint32_t phase = 0, acc_phase = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
-            int n_tile, mg, g, t0, t1;
-            decode(u, n_tile, mg, g, t0, t1);
+            int n_tile, mg, cb, g, t0, t1;
+            decode(u, n_tile, mg, cb, g, t0, t1);
             const int pa0 = mg * pairs / mgroups, pa1 = (mg + 1) * pairs / mgroups;
             // per accumulator: shifted start (bytes) of its first chunk and the distance to its second
             uint32_t off[MACC], lbo[MACC];
@@ -361,16 +367,25 @@ __global__ void __launch_bounds__(256, 1)
                 tc_fence_after();
                 const uint32_t sa = base + stage * stage_bytes;
                 const uint64_t bd0 = smem_desc_sw128(sa + slot, (uint32_t)bchunk, 1024);
+                // descriptors built by the whole (converged) warp: uniform registers, no per-MMA
+                // register->uniform transfer inside the elected lane's issue sequence
+                uint64_t ad[MACC];
+#pragma unroll
+                for (int a = 0; a < MACC; a++) ad[a] = smem_desc_sw128(sa + off[a], lbo[a], 1024);
+                const uint32_t first = tile > t0 ? 1u : 0u;
                 if (elect_one()) {
 #pragma unroll
                     for (int a = 0; a < MACC; a++) {
                         if (a < pa1 - pa0) {
-                            const uint64_t ad0 = smem_desc_sw128(sa + off[a], lbo[a], 1024);
                             const uint32_t dt = tmem_base + a * args.acc_stride;
+                            umma<2>(dt, ad[a], bd0, idesc, first);
+                            if (KST > 0) {
 #pragma unroll
-                            for (int k = 0; k < KSTEPS; k++) {
-                                const uint32_t accum = (tile > t0 || k > 0) ? 1u : 0u;
-                                umma<2>(dt, ad0 + (uint64_t)(k * 128), bd0 + (uint64_t)(k * 128), idesc, accum);
+                                for (int k = 1; k < (KST > 0 ? KST : 1); k++)
+                                    umma<2>(dt, ad[a] + (uint64_t)(k * 128), bd0 + (uint64_t)(k * 128), idesc, 1u);
+                            } else {
+                                for (int k = 1; k < ksteps; k++)
+                                    umma<2>(dt, ad[a] + (uint64_t)(k * 128), bd0 + (uint64_t)(k * 128), idesc, 1u);
                             }
                         }
                     }
@@ -389,15 +404,16 @@ __global__ void __launch_bounds__(256, 1)
         const int row = q * 32 + lane;
         uint32_t acc_phase = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
-            int n_tile, mg, g, t0, t1;
-            decode(u, n_tile, mg, g, t0, t1);
+            int n_tile, mg, cb, g, t0, t1;
+            decode(u, n_tile, mg, cb, g, t0, t1);
             const int split = t0 / args.kb_per_split;
             const int pa0 = mg * pairs / mgroups, pa1 = (mg + 1) * pairs / mgroups;
             mbar_wait(tfull, acc_phase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
             for (int a = 0; a < pa1 - pa0; a++) {
-                const size_t vu = (((size_t)split * args.groups + g) * pairs + (pa0 + a)) * args.n_tiles + n_tile;
+                const size_t vu = (((size_t)split * args.groups + g) * (cblocks * pairs) + cb * pairs + (pa0 + a)) *
+                                      args.n_tiles + n_tile;
                 float* dst = args.partial + vu * args.BN * 128 + row;
                 for (int c0 = 0; c0 < args.BN; c0 += 32) {
                     const bool two = c0 + 16 < args.BN;
@@ -430,9 +446,9 @@ size_t tc_halo_wgrad_smem_bytes(const TcArgs& a) {
     return (size_t)a.stages * (a.halo_slot + a.b_stage_bytes) + 256 + HALO_SMEM_ALIGN;
 }
 
-template <int MACC>
+template <int MACC, int KST>
 static cudaError_t halo_wgrad_launch_one(const TcLaunch& L, cudaStream_t s) {
-    auto kern = tc_halo_wgrad_kernel<MACC>;
+    auto kern = tc_halo_wgrad_kernel<MACC, KST>;
     const size_t smem = tc_halo_wgrad_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -441,13 +457,24 @@ static cudaError_t halo_wgrad_launch_one(const TcLaunch& L, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int MACC>
+static cudaError_t halo_wgrad_dispatch_k(const TcLaunch& L, cudaStream_t s) {
+    switch (L.args.halo_ksteps) {
+        case 8: return halo_wgrad_launch_one<MACC, 8>(L, s);
+        case 11: return halo_wgrad_launch_one<MACC, 11>(L, s);   // conv1 (s2d 57-wide, 3-row tiles)
+        case 13: return halo_wgrad_launch_one<MACC, 13>(L, s);   // 13x13 maps, whole image
+        case 14: return halo_wgrad_launch_one<MACC, 14>(L, s);   // conv2 (31-wide, 7-row tiles)
+        default: return halo_wgrad_launch_one<MACC, 0>(L, s);
+    }
+}
+
 cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s) {
     switch (L.args.macc) {
-        case 1: return halo_wgrad_launch_one<1>(L, s);
-        case 2: return halo_wgrad_launch_one<2>(L, s);
-        case 3: return halo_wgrad_launch_one<3>(L, s);
-        case 4: return halo_wgrad_launch_one<4>(L, s);
-        case 5: return halo_wgrad_launch_one<5>(L, s);
+        case 1: return halo_wgrad_launch_one<1, 0>(L, s);
+        case 2: return halo_wgrad_launch_one<2, 0>(L, s);
+        case 3: return halo_wgrad_launch_one<3, 0>(L, s);
+        case 4: return halo_wgrad_dispatch_k<4>(L, s);
+        case 5: return halo_wgrad_dispatch_k<5>(L, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -253,8 +253,10 @@ def test_caffenet_conv1_full_image_wgrad(oracle, dy_layout):
 
 HALO_CASES = CASES + [(2, 96, 27, 27, 64, (5, 5), (1, 1), (2, 2), 2),     # conv2 geometry (Cg=48, K padding)
                       (1, 3, 227, 227, 32, (11, 11), (4, 4), (0, 0), 1),  # conv1 geometry (s2d, 55x55 out)
-                      (2, 64, 20, 37, 48, (3, 3), (1, 1), (1, 1), 1)]     # ragged last tile rows
-HALO_IDS = IDS + ["conv2geom", "conv1geom", "H20W37"]
+                      (2, 64, 20, 37, 48, (3, 3), (1, 1), (1, 1), 1),     # ragged last tile rows
+                      (2, 256, 13, 13, 192, (3, 3), (1, 1), (1, 1), 2),   # conv4-like: 2 channel blocks, BN 96
+                      (2, 384, 13, 13, 128, (3, 3), (1, 1), (1, 1), 2)]   # conv5-like: 3 channel blocks, BN 64
+HALO_IDS = IDS + ["conv2geom", "conv1geom", "H20W37", "conv4like", "conv5like"]
 
 
 @pytest.mark.parametrize("cta", [1, 2])
