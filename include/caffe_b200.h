@@ -136,9 +136,10 @@ caffe_status caffe_device_check(void);
    (beta 0) stage 32-row tiles in shared memory and write them with TMA tensor stores; 0 = direct
    per-thread vector stores.  Bit-identical results. */
 #define CAFFE_TUNE_TMA_STORE 5
-/* CAFFE_TUNE_ROWS_EPILOGUE: 1 = channels-last / row-major tensor-core outputs (beta 0) are staged
-   per warp in shared memory and written as whole 128-byte row segments; 0 (default) = each thread
-   stores its own row.  Bit-identical results. */
+/* CAFFE_TUNE_ROWS_EPILOGUE: 1 = channels-last BF16 tensor-core outputs (beta 0, <= 128 columns per
+   tile) are staged per warp in shared memory and written back in memory order (contiguous 512-byte
+   stores when a tile holds whole pixels); 0 (default) = each thread stores its own row.
+   Bit-identical results. */
 #define CAFFE_TUNE_ROWS_EPILOGUE 6
 /* CAFFE_TUNE_SGD_BLOCKS_PER_SM: grid of caffe_sgd_update in 256-thread blocks per SM (0 = default 4).
    1 leaves registers and thread slots for kernels running concurrently on other streams (an update

@@ -245,15 +245,12 @@ void enable_tma_store(TcLaunch& L, void* out, int esz, long long cols, long long
 }
 // Row-staged coalesced epilogue (epi_store_rows) for s_c == 1 outputs with beta 0: 16-byte aligned
 // rows, group column offsets and N; TMEM slots wide enough for whole 128-byte column chunks.
-int g_rows_epi = 0;   // off by default: measured no gain for 128-byte-aligned rows (conv2) and a loss
-                      // for 192-byte pixel rows (conv1), where each 128-byte segment straddles two lines
+int g_rows_epi = 0;   // CAFFE_TUNE_ROWS_EPILOGUE (off: adds epilogue instructions where the epilogue is the
+                      // bottleneck -- conv1 forward 106 -> 149 us; no gain elsewhere)
 void enable_rows_epilogue(TcArgs& a) {
-    const int esz = a.out_bf16 ? 2 : 4, cw = 128 / esz;
-    const long long chunked = (a.BN + cw - 1) / cw * cw;
-    const bool ok = g_rows_epi && !a.tma_store && a.s_c == 1 && a.beta == 0.f &&
-                    (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.s_p * esz) % 16 == 0 &&
-                    (a.s_n * esz) % 16 == 0 && ((long long)a.col_g * esz) % 16 == 0 && (a.N * esz) % 16 == 0 &&
-                    (a.BN * esz) % 16 == 0 && a.acc_stride >= chunked;
+    const bool ok = g_rows_epi && !a.tma_store && a.s_c == 1 && a.beta == 0.f && a.out_bf16 && a.BN <= 128 &&
+                    a.BN % 8 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.s_p * 2) % 16 == 0 &&
+                    (a.s_n * 2) % 16 == 0 && ((long long)a.col_g * 2) % 16 == 0 && a.N % 8 == 0;
     a.rows_epi = ok ? 1 : 0;
 }
 void set_out(TcArgs& a, const caffe_blob* b) {
@@ -270,7 +267,7 @@ void finish_rows_epilogue(TcArgs& a) {
     if (a.rows_epi) {   // 16 KB of staging: keep the total under the 227 KB limit
         const int macc = a.macc > 1 ? a.macc : 1;
         const int stage = macc * 16384 + a.b_stage_bytes;
-        const int budget = (a.tma_store ? 167 : 200) * 1024 - 16 * 1024;
+        const int budget = (a.tma_store ? 167 : 200) * 1024 - 35 * 1024;
         a.stages = std::min(a.stages, std::max(2, budget / stage));
     }
 }
@@ -481,7 +478,7 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
             enable_rows_epilogue(L.args);
             if (L.args.rows_epi) {   // take the staging out of the B ring
                 const int macc = L.args.macc > 1 ? L.args.macc : 1;
-                const long long budget = 232448 - 512 - 2048 - 1024 - 16384 -
+                const long long budget = 232448 - 512 - 2048 - 1024 - 34816 -
                                          (long long)L.args.a_stages * macc * L.args.halo_slot;
                 L.args.stages = (int)std::min<long long>(L.args.stages, budget / L.args.b_stage_bytes);
                 if (L.args.stages < 2) L.args.rows_epi = 0;

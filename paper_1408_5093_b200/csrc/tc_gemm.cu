@@ -33,7 +33,7 @@ constexpr int A_STAGE_BYTES = 16384;   // 128 rows x 128 B
 constexpr int SMEM_ALIGN = 1024;
 
 constexpr int EPI_STAGE_BYTES = 4 * 2 * 4096;   // TMA-store staging: 4 epilogue warps x 2 buffers
-constexpr int ROWS_STAGE_BYTES = 4 * 4096;      // row-staged epilogue: 4 epilogue warps x 4 KB
+constexpr int ROWS_STAGE_BYTES = 4 * 32 * 17 * 16;   // row-staged epilogue: 4 epilogue warps x 8.5 KB
 size_t tc_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
     return (size_t)a.stages * (macc * A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + 2 * 256 * 4 /*bias*/ +
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(256, 1)
                     epi_store_tma(args, &mapC, taddr, m_tile * TM + (int)rank * BM + q * 32, col0, cbase, bs,
                                   epi_stage + q * 8192, tbuf, lane);
                 } else if (args.rows_epi) {
-                    epi_store_rows(args, taddr, row_ok, rbase, col0, cbase, bs, rows_stage + q * 4096, lane);
+                    epi_store_rows(args, taddr, row_ok, rbase, col0, cbase, bs, rows_stage + q * (32 * 17 * 16), lane);
                 } else {
                     epi_store_strided(args, taddr, row_ok, rbase, col0, cbase, bs);
                 }

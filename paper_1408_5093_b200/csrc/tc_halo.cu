@@ -31,7 +31,7 @@ constexpr int HALO_SMEM_ALIGN = 1024;
 size_t tc_halo_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
     return (size_t)a.a_stages * macc * a.halo_slot + (size_t)a.stages * a.b_stage_bytes + 512 /*barriers*/ +
-           2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN + (a.rows_epi ? 4 * 4096 : 0);
+           2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN + (a.rows_epi ? 4 * 32 * 17 * 16 : 0);
 }
 
 template <int CG, int MACC>
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
     float* sbias = reinterpret_cast<float*>(b_ring + b_stages * args.b_stage_bytes + 512);   // [2][256]
-    uint8_t* rows_stage = b_ring + b_stages * args.b_stage_bytes + 512 + 2048;                 // [4][4 KB]
+    uint8_t* rows_stage = b_ring + b_stages * args.b_stage_bytes + 512 + 2048;                 // [4][8.5 KB]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256, 1)
                 const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + xx) * args.s_p;
                 if (args.rows_epi)
                     epi_store_rows(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs,
-                                   rows_stage + q * 4096, lane);
+                                   rows_stage + q * (32 * 17 * 16), lane);
                 else
                     epi_store_strided(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs);
             }

@@ -67,6 +67,22 @@ def main():
             cb.conv_forward(x, w, None, 1, 1, 1, relu=True, out=y)
         torch.cuda.synchronize()
         return
+    if "--rows" in sys.argv:
+        from paper_1408_5093_b200 import _abi
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_ROWS_EPILOGUE, int(sys.argv[sys.argv.index("--rows") + 1]))
+    if "--only-conv1" in sys.argv:   # for ncu: conv1 forward (halo, s2d) with rows epilogue off then on
+        from paper_1408_5093_b200 import _abi
+        cl = torch.channels_last
+        x = (torch.rand(256, 3, 227, 227, device=dev) * 255 - 128).round().to(torch.bfloat16).contiguous(memory_format=cl)
+        w = torch.randn(96, 3, 11, 11, device=dev) * 0.01
+        wb = w.to(torch.bfloat16)
+        b = torch.zeros(96, device=dev)
+        y = cb.conv_forward(x, wb, b, 4, 0, 1, relu=True)
+        for mode in (0, 1):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_ROWS_EPILOGUE, mode)
+            cb.conv_forward(x, wb, b, 4, 0, 1, relu=True, out=y)
+        torch.cuda.synchronize()
+        return
     if "--only-conv2" in sys.argv:   # for ncu: conv2 forward + data gradient
         cl = torch.channels_last
         x = torch.randn(256, 96, 27, 27, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
