@@ -475,14 +475,7 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     if (L.cg < 1) L.cg = 1;
     if (L.epi == EPI_STRIDED && L.amode != A_HALO_MN) {
         if (L.amode == A_HALO_K) {
-            enable_rows_epilogue(L.args);
-            if (L.args.rows_epi) {   // take the staging out of the B ring
-                const int macc = L.args.macc > 1 ? L.args.macc : 1;
-                const long long budget = 232448 - 512 - 2048 - 1024 - 34816 -
-                                         (long long)L.args.a_stages * macc * L.args.halo_slot;
-                L.args.stages = (int)std::min<long long>(L.args.stages, budget / L.args.b_stage_bytes);
-                if (L.args.stages < 2) L.args.rows_epi = 0;
-            }
+            L.args.rows_epi = 0;   // the halo kernel splits its columns over two epilogue warp groups
         } else {
             finish_rows_epilogue(L.args);
         }

@@ -10,8 +10,10 @@ namespace cb {
 // taddr: TMEM address of this warp's lanes, column 0 of the accumulator.  rbase: element offset of
 // the output row; col0: first tile column (for the N bound); cbase: output channel of tile column 0;
 // bs: this tile's bias staged in shared memory (or unused when args.bias == nullptr).
+// [c_begin, c_end): the tile columns this thread writes (multiples of 16; default all BN).
 __device__ __forceinline__ void epi_store_strided(const TcArgs& args, uint32_t taddr, bool row_ok, long long rbase,
-                                                  int col0, int cbase, const float* bs) {
+                                                  int col0, int cbase, const float* bs, int c_begin = 0,
+                                                  int c_end = 1 << 30) {
     const bool rowvec = args.s_c == 1;        // channels-last / row-major output
     const bool bf = args.out_bf16 != 0;
     const float beta = args.beta;
@@ -101,9 +103,10 @@ __device__ __forceinline__ void epi_store_strided(const TcArgs& args, uint32_t t
     };
     // two 16-column TMEM loads in flight per wait (measured: batching four per wait was slower --
     // conv1 forward 96 -> 120 us)
-    for (int c0 = 0; c0 < args.BN; c0 += 32) {
+    const int cend = min(args.BN, c_end);
+    for (int c0 = c_begin; c0 < cend; c0 += 32) {
         if (col0 + c0 >= args.N) break;  // warp-uniform
-        const bool two = c0 + 16 < args.BN && col0 + c0 + 16 < args.N;
+        const bool two = c0 + 16 < cend && col0 + c0 + 16 < args.N;
         uint32_t v0[16], v1[16];
         tmem_ld16(taddr + c0, v0);
         if (two) tmem_ld16(taddr + c0 + 16, v1);

@@ -35,7 +35,7 @@ size_t tc_halo_smem_bytes(const TcArgs& a) {
 }
 
 template <int CG, int MACC>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     tc_halo_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const TcArgs args) {
     constexpr int CH = 64;                 // bf16 channels per 128-byte row
@@ -58,7 +58,6 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
     float* sbias = reinterpret_cast<float*>(b_ring + b_stages * args.b_stage_bytes + 512);   // [2][256]
-    uint8_t* rows_stage = b_ring + b_stages * args.b_stage_bytes + 512 + 2048;                 // [4][8.5 KB]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -76,7 +75,7 @@ __global__ void __launch_bounds__(256, 1)
         tma_prefetch(&mapB);
         for (int i = 0; i < a_stages; i++) { mbar_init(&fullA[i], CG); mbar_init(&emptyA[i], 1); }
         for (int i = 0; i < b_stages; i++) { mbar_init(&fullB[i], CG); mbar_init(&emptyB[i], 1); }
-        for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * CG); }
+        for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 256 * CG); }
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -196,10 +195,16 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     } else if (warp >= 4) {
-        // ===================== epilogue (both CTAs) =====================
-        const int q = warp - 4;
+        // ===================== epilogue (both CTAs): two groups of 4 warps =====================
+        // Group e (warps 4-7, 8-11) writes columns [e*half, ...) of the tiles; both groups read the
+        // same TMEM lanes (warp % 4 selects the lane quadrant).  Two warps per SM sub-partition hide
+        // the TMEM-load and store latency of the epilogue, which bounds the wide-output layers.
+        const int q = warp & 3;
+        const int eg = (warp - 4) >> 2;
         const int row = q * 32 + lane;
         const int yy = row / args.halo_wt, xx = row - yy * args.halo_wt;
+        const int half = ((args.BN / 2) + 15) & ~15;
+        const int cb_ = eg == 0 ? 0 : half, ce_ = eg == 0 ? half : args.BN;
         int acc = 0;
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
@@ -215,8 +220,9 @@ __global__ void __launch_bounds__(256, 1)
             const int cbase = g * args.col_g + col0;
             float* bs = sbias + acc * 256;
             if (args.bias) {
-                for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                for (int c = cb_ + row; c < ce_; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
+                if (eg == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+                else asm volatile("bar.sync 2, 128;" ::: "memory");
             }
             for (int a = 0; a < macc; a++) {
                 const int tile = tg * tiles_per_unit + a * CG + (int)rank;
@@ -224,11 +230,8 @@ __global__ void __launch_bounds__(256, 1)
                 const int y = (tile - n * args.tiles_per_img) * args.halo_th + yy;
                 const bool row_ok = tile < args.total_tiles && yy < args.halo_th && y < args.out_h && xx < args.out_w;
                 const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + xx) * args.s_p;
-                if (args.rows_epi)
-                    epi_store_rows(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs,
-                                   rows_stage + q * (32 * 17 * 16), lane);
-                else
-                    epi_store_strided(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs);
+                if (cb_ < ce_)
+                    epi_store_strided(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs, cb_, ce_);
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
@@ -486,11 +489,11 @@ static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (CG == 1) {
-        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+        kern<<<L.grid, 384, smem, s>>>(L.mapA, L.mapB, L.args);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(L.grid);
-        cfg.blockDim = dim3(256);
+        cfg.blockDim = dim3(384);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
