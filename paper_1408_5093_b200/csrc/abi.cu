@@ -378,7 +378,7 @@ WgHalo wgrad_halo_plan(const Plan& p) {
     h.slot = (int)rup((long long)need_rows * 128, 1024);
     h.bchunk = (int)rup((long long)krows * 128, 1024);   // K rows x 64 channels
     const int stage = h.slot + h.nch * h.bchunk;
-    h.stages = std::min(8, (232448 - 256 - 1024) / stage);
+    h.stages = std::min(8, (232448 - 1024 - 2048 - 1024) / stage);
     if (h.stages < 2) return h;
     const int base = p.G * h.n_tiles * h.mgroups * h.cblocks;   // units per pixel split
     int sp = std::max(1, 148 / base);
@@ -844,7 +844,11 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
     void* DYA = w8 + ws_x_max(p);
     float* PART = (float*)(w8 + ws_x_max(p) + ws_dy_max(p));
     float* BPART = (float*)(w8 + ws_x_max(p) + ws_dy_max(p) + ws_partial(p));
-    if (bias_diff)
+    const WgHalo hw = wgrad_halo_plan(p);
+    // bias gradient inside the halo weight gradient (ones chunk) when dY feeds the MMA unmodified
+    // (bf16, read in place) and the tap count leaves a spare chunk; else a separate reduction
+    const bool bias_mma = bias_diff && hw.use && !B.packed && isbf(top_diff) && (p.taps & 1) == 1;
+    if (bias_diff && !bias_mma)
         CK(bias_grad(top_diff->ptr, isbf(top_diff), nhwc(top_diff), (float*)bias_diff->ptr, beta, p.N, p.O,
                      p.OH * p.OW, BPART, s),
            "bias grad");
@@ -852,7 +856,6 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
     if ((st = pack_if(B, top_diff, DYA, p.E, s))) return st;
     const void* aptr = A.packed ? XA : A.ptr;
     const void* bptr = B.packed ? DYA : B.ptr;
-    const WgHalo hw = wgrad_halo_plan(p);
     if (hw.use) {
         TcLaunch L;
         memset(&L, 0, sizeof L);
@@ -867,12 +870,12 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
         a.a_pad_h = p.php; a.a_pad_w = p.pwp; a.a_cpg = A.cpg; a.b_col_g = B.cpg;
         a.b_nchunks = hw.nch; a.b_stage_bytes = hw.nch * hw.bchunk; a.halo_slot = hw.slot; a.stages = hw.stages;
         a.acc_stride = hw.acc_stride; a.macc = hw.macc; a.m_tiles_real = hw.pairs; a.m_tiles = hw.mgroups;
-        a.a_cblocks = hw.cblocks; a.halo_ksteps = hw.ksteps;
+        a.a_cblocks = hw.cblocks; a.halo_ksteps = hw.ksteps; a.bias_mma = bias_mma ? 1 : 0;
         a.tmem_cols = 512; a.partial = PART;
         a.units = p.G * hw.n_tiles * hw.mgroups * hw.cblocks * hw.splits;
         if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
         CK(wgrad_reduce(PART, (float*)weight_diff->ptr, beta, wgeom(p), hw.cblocks * hw.pairs, hw.n_tiles, hw.splits,
-                        hw.BN, 64, hw.cblocks, s, 1),
+                        hw.BN, 64, hw.cblocks, s, 1, bias_mma ? (float*)bias_diff->ptr : nullptr),
            "wgrad reduce");
         return CAFFE_OK;
     }

@@ -53,6 +53,8 @@ struct TcArgs {
     int halo_wt, halo_th, halo_rows, halo_kh, halo_slot;   // halo_slot: smem bytes per tile (1 KB multiple)
     int tiles_per_img, total_tiles, out_h, out_w;
     int halo_ksteps;                    // A_HALO_MN: K steps (16 pixel rows each) per pixel tile
+    int bias_mma;                       // A_HALO_MN, odd taps: the last pair's spare chunk is all ones, so
+                                        // its accumulator rows 64-127 hold sum_pixels dY (bias gradient)
     int a_stages;                       // halo stages in the A ring
     int tma_store;                      // EPI_STRIDED: store tiles with TMA (mapC; row-major output, beta 0)
     int rows_epi;                       // EPI_STRIDED: row-staged coalesced stores (epi_store_rows)
@@ -121,8 +123,11 @@ cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, co
 // Deterministic fixed-order reduction of wgrad partials into dW (O, Cg, kh, kw) fp32 with beta.
 // cbmajor = 0: M tile = 2 consecutive chunks of q = tap*cblocks + cb (im2col wgrad);
 // cbmajor = 1: M tile (pair) = taps (2p, 2p+1) of one channel block, index cb*pairs + p (halo wgrad).
+// db (optional, cbmajor only): db = beta*db + sum_splits of row 64 of the last pair of channel block 0
+// (the ones chunk of the halo weight gradient).
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
-                         int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor = 0);
+                         int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor = 0,
+                         float* db = nullptr);
 // Fixed-order reduction of split-K GEMM partials ([unit][BN][TM] fp32, unit = (s*m_tiles+mt)*n_tiles+nt)
 // into a row-major output (ldo) with bias, beta and ReLU; pC > 0 scatters each row's (c,h,w)-ordered
 // columns into an NHWC row of pC channels x pHW pixels.

@@ -343,8 +343,20 @@ cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, co
 // packed (tap, cc) back to (c, i, j) of the original filter.
 __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dW, float beta, WGeom g,
                                     int m_tiles, int n_tiles, int splits, int BN, int chunk, int cblocks,
-                                    int chunks_per_tile, int total, int cbmajor) {
+                                    int chunks_per_tile, int total, int cbmajor, float* __restrict__ db) {
     const int nq = g.khp * g.kwp * cblocks;
+    if (db) {   // bias gradient from the ones chunk: pair (pairs-1) of channel block 0, row 64
+        const int pairs = (g.khp * g.kwp + 1) / 2;
+        const long long sstride = (long long)g.G * m_tiles * n_tiles * BN * 128;
+        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < g.G * g.Og; t += gridDim.x * blockDim.x) {
+            const int o = t % g.Og, grp = t / g.Og;
+            const int n_tile = o / BN, col = o % BN;
+            const float* pp = partial + ((((long long)grp * m_tiles + (pairs - 1)) * n_tiles + n_tile) * BN + col) * 128 + 64;
+            float acc = 0.f;
+            for (int sp = 0; sp < splits; sp++) acc += pp[sp * sstride];
+            db[t] = (beta != 0.f ? beta * db[t] : 0.f) + acc;
+        }
+    }
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
         const int rr = t % chunk;
         int r = t / chunk;
@@ -379,10 +391,10 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __
 }
 
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
-                         int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor) {
+                         int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor, float* db) {
     const int total = g.G * g.Og * g.khp * g.kwp * cblocks * chunk;
     wgrad_reduce_kernel<<<blocks_for(total, 256), 256, 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
-                                                               chunk, cblocks, 128 / chunk, total, cbmajor);
+                                                               chunk, cblocks, 128 / chunk, total, cbmajor, db);
     note_launch();
     return cudaGetLastError();
 }

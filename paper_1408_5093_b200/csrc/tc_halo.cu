@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tfull = empty + stages;
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint8_t* ones = smem + stages * stage_bytes + 1024;   // 16 rows x 128 B of bf16 1.0
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int taps = args.halo_kh * args.a_kw;
@@ -293,6 +294,8 @@ __global__ void __launch_bounds__(256, 1)
         uint4* z = reinterpret_cast<uint4*>(smem);
         const int n16 = stages * stage_bytes / 16;
         for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+        uint4* o4 = reinterpret_cast<uint4*>(ones);
+        for (int i = threadIdx.x; i < 2048 / 16; i += blockDim.x) o4[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
@@ -376,11 +379,23 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                 for (int a = 0; a < MACC; a++) ad[a] = smem_desc_sw128(sa + off[a], lbo[a], 1024);
                 const uint32_t first = tile > t0 ? 1u : 0u;
+                // the bias accumulator: last pair of channel block 0 with an odd tap count -- its second
+                // chunk is the constant ones block, reached by a per-K-step leading byte offset
+                const int abias = (args.bias_mma && cb == 0 && pa1 == pairs) ? (pairs - 1 - pa0) : -1;
+                const uint32_t ones_addr = smem_u32(ones);
                 if (elect_one()) {
 #pragma unroll
                     for (int a = 0; a < MACC; a++) {
                         if (a < pa1 - pa0) {
                             const uint32_t dt = tmem_base + a * args.acc_stride;
+                            if (a == abias) {
+                                for (int k = 0; k < ksteps; k++) {
+                                    const uint32_t st0 = sa + off[a] + (uint32_t)k * 2048u;
+                                    umma<2>(dt, smem_desc_sw128(st0, ones_addr - st0, 1024), bd0 + (uint64_t)(k * 128),
+                                            idesc, (k > 0 || first) ? 1u : 0u);
+                                }
+                                continue;
+                            }
                             umma<2>(dt, ad[a], bd0, idesc, first);
                             if (KST > 0) {
 #pragma unroll
@@ -446,7 +461,7 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 size_t tc_halo_wgrad_smem_bytes(const TcArgs& a) {
-    return (size_t)a.stages * (a.halo_slot + a.b_stage_bytes) + 256 + HALO_SMEM_ALIGN;
+    return (size_t)a.stages * (a.halo_slot + a.b_stage_bytes) + 1024 /*barriers*/ + 2048 /*ones*/ + HALO_SMEM_ALIGN;
 }
 
 template <int MACC, int KST>
