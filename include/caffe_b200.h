@@ -64,7 +64,7 @@ typedef enum {
     CAFFE_E_ARCH = 9       /* device is not sm_100 */
 } caffe_status;
 
-typedef enum { CAFFE_F32 = 0, CAFFE_BF16 = 1, CAFFE_I32 = 2 } caffe_dtype;
+typedef enum { CAFFE_F32 = 0, CAFFE_BF16 = 1, CAFFE_I32 = 2, CAFFE_U8 = 3 } caffe_dtype;
 
 typedef enum { CAFFE_MATH_FP32 = 0, CAFFE_MATH_TF32 = 1, CAFFE_MATH_BF16 = 2 } caffe_math;
 
@@ -221,7 +221,9 @@ caffe_status caffe_relu_backward(const caffe_blob* bottom_or_top, const caffe_bl
 /* ------------------------------------------------------------------ pooling
    Output size: ceil((H+2p-k)/s)+1, minus 1 if (OH-1)*s >= H+p (reading R5).
    MAX: strict '>' row-major scan seeded by the first in-image element; mask =
-   int32 h*W+w in the (n,c) plane (R7), mask nullable in forward.
+   int32 h*W+w in the (n,c) plane (R7), mask nullable in forward.  A CAFFE_U8 mask blob stores
+   the same argmax as the window-local index (h - (py*sh - ph))*kw + (w - (px*sw - pw)) (requires
+   kh*kw <= 255): a quarter of the mask bytes for the backward pass to read; same results.
    AVE: divisor (min(hs+k,H+p)-hs)*(min(ws+k,W+p)-ws) (R6).
    backward overwrites bottom_diff; MAX sums top_diff in ascending (py,px) order
    in FP32 (R8, bit-exact); MAX backward without mask is CAFFE_E_INVALID. */

@@ -49,6 +49,8 @@ def _dtype_code(t) -> int:
         return CAFFE_BF16
     if t.dtype == torch.int32:
         return CAFFE_I32
+    if t.dtype == torch.uint8:
+        return _abi.CAFFE_U8
     raise TypeError(f"unsupported dtype {t.dtype}")
 
 
@@ -263,14 +265,16 @@ def pool_output_shape(in_shape, method, kernel, stride, pad=0):
     return (out.n, out.c, out.h, out.w)
 
 
-def pool_forward(x, method, kernel, stride, pad=0, out=None, mask=None, want_mask=True):
+def pool_forward(x, method, kernel, stride, pad=0, out=None, mask=None, want_mask=True, mask_dtype=None):
+    """MAX/AVE pooling.  The MAX argmax mask is int32 h*W+w (Caffe) or, with mask_dtype=torch.uint8
+    (or a uint8 `mask`), the window-local index -- a quarter of the bytes for the backward pass."""
     torch = _t()
     d = _pool_desc(method, kernel, stride, pad)
     oshape = pool_output_shape(x.shape, method, kernel, stride, pad)
     if out is None:
         out = empty_like_layout(oshape, x.dtype, x.device, like=x)
     if d.method == _abi.CAFFE_POOL_MAX and want_mask and mask is None:
-        mask = empty_like_layout(oshape, torch.int32, x.device, like=out)
+        mask = empty_like_layout(oshape, mask_dtype or torch.int32, x.device, like=out)
     bx, by, bm = blob(x), blob(out), blob(mask) if d.method == _abi.CAFFE_POOL_MAX else None
     call("caffe_pool_forward", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(by), _bp(bm), _stream())
     return out, (mask if d.method == _abi.CAFFE_POOL_MAX else None)

@@ -62,7 +62,7 @@ caffe_status cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 inline long long cnt(const caffe_shape4& s) { return (long long)s.n * s.c * s.h * s.w; }
-inline size_t esize(caffe_dtype d) { return d == CAFFE_BF16 ? 2 : 4; }
+inline size_t esize(caffe_dtype d) { return d == CAFFE_BF16 ? 2 : d == CAFFE_U8 ? 1 : 4; }
 inline size_t bytes_of(const caffe_blob* b) { return (size_t)cnt(b->shape) * esize(b->dtype); }
 inline long long rup(long long a, long long b) { return (a + b - 1) / b * b; }
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
@@ -88,7 +88,8 @@ caffe_status check_blob(const caffe_blob* b, const char* name, bool float_only =
     if (b->layout != CAFFE_NCHW && b->layout != CAFFE_NHWC) return fail(CAFFE_E_INVALID, "%s has a bad layout %d", name, b->layout);
     if (float_only && b->dtype != CAFFE_F32 && b->dtype != CAFFE_BF16)
         return fail(CAFFE_E_DTYPE, "%s dtype must be F32 or BF16", name);
-    if (!float_only && b->dtype != CAFFE_I32) return fail(CAFFE_E_DTYPE, "%s dtype must be I32", name);
+    if (!float_only && b->dtype != CAFFE_I32 && b->dtype != CAFFE_U8)
+        return fail(CAFFE_E_DTYPE, "%s dtype must be I32 or U8", name);
     return CAFFE_OK;
 }
 bool overlap(const caffe_blob* a, const caffe_blob* b) {
@@ -979,11 +980,14 @@ caffe_status caffe_pool_forward(const caffe_pool_desc* desc, const caffe_blob* b
         if (!same_shape(mask->shape, want) || mask->layout != top->layout)
             return fail(CAFFE_E_SHAPE, "mask shape/layout must equal top's");
         if (desc->method != CAFFE_POOL_MAX) return fail(CAFFE_E_INVALID, "mask is only produced by MAX pooling");
+        if (mask->dtype == CAFFE_U8 && g.kh * g.kw > 255)
+            return fail(CAFFE_E_PARAM, "a U8 (window-local) mask needs kernel_h*kernel_w <= 255");
     }
     if (overlap(top, bottom) || overlap(mask, bottom) || overlap(mask, top)) return fail(CAFFE_E_ALIAS, "pool outputs overlap");
     if (g.N == 0) return CAFFE_OK;
     if (desc->method == CAFFE_POOL_MAX)
-        CK(maxpool_fwd(bottom->ptr, strides(bottom), top->ptr, nhwc(top), mask ? (int32_t*)mask->ptr : nullptr,
+        CK(maxpool_fwd(bottom->ptr, strides(bottom), top->ptr, nhwc(top), mask ? mask->ptr : nullptr,
+                       mask ? (mask->dtype == CAFFE_U8) : 0,
                        isbf(bottom), g, (cudaStream_t)stream),
            "maxpool fwd");
     else
@@ -1006,6 +1010,8 @@ static caffe_status pool_backward_impl(const caffe_pool_desc* desc, const caffe_
         if ((st = check_blob(mask, "mask", false))) return st;
         if (!same_shape(mask->shape, want) || mask->layout != top_diff->layout)
             return fail(CAFFE_E_SHAPE, "mask shape/layout must equal top_diff's");
+        if (mask->dtype == CAFFE_U8 && g.kh * g.kw > 255)
+            return fail(CAFFE_E_PARAM, "a U8 (window-local) mask needs kernel_h*kernel_w <= 255");
     }
     if (top) {
         if (desc->method != CAFFE_POOL_MAX) return fail(CAFFE_E_INVALID, "the ReLU-fused backward needs MAX pooling");
@@ -1017,7 +1023,7 @@ static caffe_status pool_backward_impl(const caffe_pool_desc* desc, const caffe_
     if (overlap(bottom_diff, top_diff) || overlap(bottom_diff, mask)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
     if (g.N == 0) return CAFFE_OK;
     if (desc->method == CAFFE_POOL_MAX)
-        CK(maxpool_bwd(top_diff->ptr, (const int32_t*)mask->ptr, top ? top->ptr : nullptr, strides(top_diff),
+        CK(maxpool_bwd(top_diff->ptr, mask->ptr, mask->dtype == CAFFE_U8, top ? top->ptr : nullptr, strides(top_diff),
                        bottom_diff->ptr, nhwc(bottom_diff), isbf(top_diff), g, (cudaStream_t)stream),
            "maxpool bwd");
     else

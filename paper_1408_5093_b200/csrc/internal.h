@@ -163,10 +163,11 @@ cudaError_t relu_bwd(const void* x, const void* dy, void* dx, int x_bf16, int d_
 struct PoolGeom {
     int N, C, H, W, kh, kw, sh, sw, ph, pw, OH, OW;
 };
-cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask, int bf16, const PoolGeom& g,
+// mask: int32 absolute h*W+w, or (mask_u8) uint8 window-local (h - hs0)*kw + (w - ws0) with the unclipped window start
+cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, void* mask, int mask_u8, int bf16, const PoolGeom& g,
                         cudaStream_t s);
 // top (optional): fuse the backward of the ReLU feeding the pool (window gradient passes iff top > 0)
-cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, const void* top, L4 ly, void* dx, int xnhwc, int bf16,
+cudaError_t maxpool_bwd(const void* dy, const void* mask, int mask_u8, const void* top, L4 ly, void* dx, int xnhwc, int bf16,
                         const PoolGeom& g, cudaStream_t s);
 cudaError_t avepool_fwd(const void* x, L4 lx, void* y, int ynhwc, int bf16, const PoolGeom& g, cudaStream_t s);
 cudaError_t avepool_bwd(const void* dy, L4 ly, void* dx, int xnhwc, int bf16, const PoolGeom& g, cudaStream_t s);

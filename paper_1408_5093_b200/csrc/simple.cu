@@ -403,24 +403,26 @@ cudaError_t relu_bwd(const void* x, const void* dy, void* dx, int x_bf16, int d_
 // ================================================================ pooling
 // Forward: thread per output element in the top's memory order.
 __global__ void maxpool_fwd_kernel(const void* __restrict__ x, L4 lx, void* __restrict__ y, int ynhwc,
-                                   int32_t* __restrict__ mask, int bf16, PoolGeom g, int total) {
+                                   void* __restrict__ mask, int mask_u8, int bf16, PoolGeom g, int total) {
     GRID_STRIDE(t, total) {
         int n, c, py, px;
         decode(t, g.C, g.OH, g.OW, ynhwc, n, c, py, px);
-        int hs = py * g.sh - g.ph, ws = px * g.sw - g.pw;
-        const int he = min(hs + g.kh, g.H), we = min(ws + g.kw, g.W);
-        hs = max(hs, 0);
-        ws = max(ws, 0);
+        const int hs0 = py * g.sh - g.ph, ws0 = px * g.sw - g.pw;
+        const int he = min(hs0 + g.kh, g.H), we = min(ws0 + g.kw, g.W);
+        const int hs = max(hs0, 0), ws = max(ws0, 0);
         const int base = n * lx.sn + c * lx.sc;
         float best = 0.f;
-        int arg = -1;
+        int ah = -1, aw = 0;
         for (int h = hs; h < he; h++)
             for (int w = ws; w < we; w++) {
                 const float v = ldv(x, base + h * lx.sh + w * lx.sw, bf16);
-                if (arg < 0 || v > best) { best = v; arg = h * g.W + w; }
+                if (ah < 0 || v > best) { best = v; ah = h; aw = w; }
             }
         stv(y, t, bf16, best);
-        if (mask) mask[t] = arg;
+        if (mask) {
+            if (mask_u8) reinterpret_cast<uint8_t*>(mask)[t] = (uint8_t)((ah - hs0) * g.kw + (aw - ws0));
+            else reinterpret_cast<int32_t*>(mask)[t] = ah * g.W + aw;
+        }
     }
 }
 
@@ -447,7 +449,7 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 // at once (a runtime-bounded loop leaves one load outstanding per thread: latency-bound).
 template <int KH, int KW>
 __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                                  int32_t* __restrict__ mask, PoolGeom g, int total) {
+                                  void* __restrict__ mask, int mask_u8, PoolGeom g, int total) {
     const int cv = g.C / 8;
     GRID_STRIDE(t, total) {
         const int c0 = (t % cv) * 8;
@@ -456,6 +458,7 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
         const int py = r % g.OH;
         const int n = r / g.OH;
         int hs = py * g.sh - g.ph, ws = px * g.sw - g.pw;
+        const int hs0 = hs, ws0 = ws;   // unclipped window start (origin of a U8 window-local mask)
         const int he = min(hs + g.kh, g.H), we = min(ws + g.kw, g.W);
         hs = max(hs, 0);
         ws = max(ws, 0);
@@ -498,16 +501,30 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
             const long long o = (long long)t * 8;
             *reinterpret_cast<uint4*>(y + o) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
             if (mask) {
-                int am[8];
+                if (mask_u8) {
+                    // local index in the unclipped window: (hs - hs0 + i)*kw + (ws - ws0 + j)
+                    const int shift = (hs - hs0) * g.kw + (ws - ws0);
+                    uint32_t pk[2] = {0u, 0u};
 #pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const int p0 = (int)(aw[e] & 0xFFFFu), p1 = (int)(aw[e] >> 16);
-                    am[2 * e] = (hs + p0 / KW) * g.W + ws + p0 % KW;
-                    am[2 * e + 1] = (hs + p1 / KW) * g.W + ws + p1 % KW;
+                    for (int e = 0; e < 4; e++) {
+                        const int p0 = (int)(aw[e] & 0xFFFFu), p1 = (int)(aw[e] >> 16);
+                        const uint32_t l0 = (uint32_t)(shift + (p0 / KW) * g.kw + p0 % KW);
+                        const uint32_t l1 = (uint32_t)(shift + (p1 / KW) * g.kw + p1 % KW);
+                        pk[e >> 1] |= (l0 | (l1 << 8)) << (16 * (e & 1));
+                    }
+                    *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(mask) + o) = make_uint2(pk[0], pk[1]);
+                } else {
+                    int am[8];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int p0 = (int)(aw[e] & 0xFFFFu), p1 = (int)(aw[e] >> 16);
+                        am[2 * e] = (hs + p0 / KW) * g.W + ws + p0 % KW;
+                        am[2 * e + 1] = (hs + p1 / KW) * g.W + ws + p1 % KW;
+                    }
+                    int4* mp = reinterpret_cast<int4*>(reinterpret_cast<int32_t*>(mask) + o);
+                    mp[0] = make_int4(am[0], am[1], am[2], am[3]);
+                    mp[1] = make_int4(am[4], am[5], am[6], am[7]);
                 }
-                int4* mp = reinterpret_cast<int4*>(mask + o);
-                mp[0] = make_int4(am[0], am[1], am[2], am[3]);
-                mp[1] = make_int4(am[4], am[5], am[6], am[7]);
             }
             continue;
         } else {
@@ -524,9 +541,15 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
         const long long o = (long long)t * 8;
         *reinterpret_cast<uint4*>(y + o) = pack8(best);
         if (mask) {
-            int4* m = reinterpret_cast<int4*>(mask + o);
-            m[0] = make_int4(arg[0], arg[1], arg[2], arg[3]);
-            m[1] = make_int4(arg[4], arg[5], arg[6], arg[7]);
+            if (mask_u8) {
+                uint8_t* m = reinterpret_cast<uint8_t*>(mask) + o;
+#pragma unroll
+                for (int e = 0; e < 8; e++) m[e] = (uint8_t)((arg[e] / g.W - hs0) * g.kw + (arg[e] % g.W - ws0));
+            } else {
+                int4* m = reinterpret_cast<int4*>(reinterpret_cast<int32_t*>(mask) + o);
+                m[0] = make_int4(arg[0], arg[1], arg[2], arg[3]);
+                m[1] = make_int4(arg[4], arg[5], arg[6], arg[7]);
+            }
         }
     }
 }
@@ -540,8 +563,8 @@ __global__ void maxpool_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bflo
 // relu_bwd(pool_bwd(dy)).
 // NPY x NPX (> 0): compile-time bound on the windows overlapping a block, so the window loads of
 // a thread are unrolled and all in flight together.
-template <int SH, int SW, int NPY, int NPX>
-__global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const int32_t* __restrict__ mask,
+template <int SH, int SW, int NPY, int NPX, bool MU8>
+__global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const void* __restrict__ mask,
                                   const __nv_bfloat16* __restrict__ top, __nv_bfloat16* __restrict__ dx, PoolGeom g,
                                   int HB, int WB, int total) {
     const int cv = g.C / 8;
@@ -562,8 +585,20 @@ __global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const in
             for (int j = 0; j < SW; j++)
 #pragma unroll
                 for (int e = 0; e < 8; e++) acc[i][j][e] = 0.f;
-        auto window = [&](const int4& m0, const int4& m1, const uint4& dr, const uint4& tr) {
-            const int mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        // window (py, px): mask words (int32: 8 absolute indices; U8: 8 window-local bytes)
+        auto window = [&](int py, int px, const int4& m0, const int4& m1, const uint2& mb, const uint4& dr,
+                          const uint4& tr) {
+            int mm[8];
+            if (MU8) {
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    mm[e] = (int)((mb.x >> (8 * e)) & 0xffu);
+                    mm[4 + e] = (int)((mb.y >> (8 * e)) & 0xffu);
+                }
+            } else {
+                mm[0] = m0.x; mm[1] = m0.y; mm[2] = m0.z; mm[3] = m0.w;
+                mm[4] = m1.x; mm[5] = m1.y; mm[6] = m1.z; mm[7] = m1.w;
+            }
             float v[8];
             unpack8(dr, v);
             if (top) {
@@ -573,18 +608,26 @@ __global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const in
                 for (int e = 0; e < 8; e++)
                     if (!(tv[e] > 0.f)) v[e] = 0.f;
             }
+            const int hs0 = py * g.sh - g.ph, ws0 = px * g.sw - g.pw;
 #pragma unroll
             for (int i = 0; i < SH; i++)
 #pragma unroll
                 for (int j = 0; j < SW; j++) {
-                    const int me = (h0 + i) * g.W + (w0 + j);
+                    // U8: the block position's index local to this window, -1 when the position lies
+                    // outside it (a local index would otherwise alias another row of the window)
+                    const int li = h0 + i - hs0, lj = w0 + j - ws0;
+                    const int me = MU8 ? ((li >= 0 && li < g.kh && lj >= 0 && lj < g.kw) ? li * g.kw + lj : -1)
+                                       : (h0 + i) * g.W + (w0 + j);
 #pragma unroll
                     for (int e = 0; e < 8; e++)
                         if (mm[e] == me) acc[i][j][e] += v[e];
                 }
         };
+        const int32_t* mask32 = reinterpret_cast<const int32_t*>(mask);
+        const uint8_t* mask8 = reinterpret_cast<const uint8_t*>(mask);
         if (NPY > 0) {
             int4 m0[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1], m1[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1];
+            uint2 mb[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1];
             uint4 dr[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1], tr[NPY > 0 ? NPY : 1][NPX > 0 ? NPX : 1];
 #pragma unroll
             for (int a = 0; a < NPY; a++)
@@ -592,8 +635,12 @@ __global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const in
                 for (int b = 0; b < NPX; b++)
                     if (py0 + a <= py1 && px0 + b <= px1) {
                         const long long q = (((long long)n * g.OH + py0 + a) * g.OW + px0 + b) * g.C + c0;
-                        m0[a][b] = *reinterpret_cast<const int4*>(mask + q);
-                        m1[a][b] = *reinterpret_cast<const int4*>(mask + q + 4);
+                        if (MU8) {
+                            mb[a][b] = *reinterpret_cast<const uint2*>(mask8 + q);
+                        } else {
+                            m0[a][b] = *reinterpret_cast<const int4*>(mask32 + q);
+                            m1[a][b] = *reinterpret_cast<const int4*>(mask32 + q + 4);
+                        }
                         dr[a][b] = *reinterpret_cast<const uint4*>(dy + q);
                         if (top) tr[a][b] = *reinterpret_cast<const uint4*>(top + q);
                     }
@@ -601,17 +648,23 @@ __global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const in
             for (int a = 0; a < NPY; a++)
 #pragma unroll
                 for (int b = 0; b < NPX; b++)
-                    if (py0 + a <= py1 && px0 + b <= px1) window(m0[a][b], m1[a][b], dr[a][b], tr[a][b]);
+                    if (py0 + a <= py1 && px0 + b <= px1)
+                        window(py0 + a, px0 + b, m0[a][b], m1[a][b], mb[a][b], dr[a][b], tr[a][b]);
         } else {
             for (int py = py0; py <= py1; py++)
                 for (int px = px0; px <= px1; px++) {
                     const long long q = (((long long)n * g.OH + py) * g.OW + px) * g.C + c0;
-                    const int4 a0 = *reinterpret_cast<const int4*>(mask + q);
-                    const int4 a1 = *reinterpret_cast<const int4*>(mask + q + 4);
+                    int4 a0 = make_int4(0, 0, 0, 0), a1 = make_int4(0, 0, 0, 0);
+                    uint2 ab = make_uint2(0, 0);
+                    if (MU8) ab = *reinterpret_cast<const uint2*>(mask8 + q);
+                    else {
+                        a0 = *reinterpret_cast<const int4*>(mask32 + q);
+                        a1 = *reinterpret_cast<const int4*>(mask32 + q + 4);
+                    }
                     const uint4 d = *reinterpret_cast<const uint4*>(dy + q);
                     uint4 tt = make_uint4(0, 0, 0, 0);
                     if (top) tt = *reinterpret_cast<const uint4*>(top + q);
-                    window(a0, a1, d, tt);
+                    window(py, px, a0, a1, ab, d, tt);
                 }
         }
 #pragma unroll
@@ -628,19 +681,19 @@ static inline bool nhwc8_ok(const void* a, const void* b, int C) {
     return (C % 8) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
 }
 
-cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask, int bf16, const PoolGeom& g,
-                        cudaStream_t s) {
+cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, void* mask, int mask_u8, int bf16,
+                        const PoolGeom& g, cudaStream_t s) {
     const int total = g.N * g.C * g.OH * g.OW;
     const bool xnhwc = lx.sc == 1 && g.C > 1;
     if (bf16 && xnhwc && ynhwc && nhwc8_ok(x, y, g.C) && ((reinterpret_cast<uintptr_t>(mask) & 15) == 0)) {
         auto X = (const __nv_bfloat16*)x;
         auto Y = (__nv_bfloat16*)y;
         const unsigned nb = nblk(total / 8, 256);
-        if (g.kh == 3 && g.kw == 3) maxpool_fwd_nhwc8<3, 3><<<nb, 256, 0, s>>>(X, Y, mask, g, total / 8);
-        else if (g.kh == 2 && g.kw == 2) maxpool_fwd_nhwc8<2, 2><<<nb, 256, 0, s>>>(X, Y, mask, g, total / 8);
-        else maxpool_fwd_nhwc8<0, 0><<<nb, 256, 0, s>>>(X, Y, mask, g, total / 8);
+        if (g.kh == 3 && g.kw == 3) maxpool_fwd_nhwc8<3, 3><<<nb, 256, 0, s>>>(X, Y, mask, mask_u8, g, total / 8);
+        else if (g.kh == 2 && g.kw == 2) maxpool_fwd_nhwc8<2, 2><<<nb, 256, 0, s>>>(X, Y, mask, mask_u8, g, total / 8);
+        else maxpool_fwd_nhwc8<0, 0><<<nb, 256, 0, s>>>(X, Y, mask, mask_u8, g, total / 8);
     } else {
-        maxpool_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, lx, y, ynhwc, mask, bf16, g, total);
+        maxpool_fwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, lx, y, ynhwc, mask, mask_u8, bf16, g, total);
     }
     note_launch();
     return cudaGetLastError();
@@ -648,7 +701,7 @@ cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, int32_t* mask,
 
 // Backward: gather per input element (in the bottom_diff's memory order) over the windows that may
 // contain it, ascending (py, px) -- R8, bit-exact.  ly = layout strides of top_diff and mask.
-__global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const int32_t* __restrict__ mask,
+__global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const void* __restrict__ mask, int mask_u8,
                                    const void* __restrict__ top, L4 ly, void* __restrict__ dx, int xnhwc, int bf16,
                                    PoolGeom g, int total) {
     GRID_STRIDE(t, total) {
@@ -662,14 +715,17 @@ __global__ void maxpool_bwd_kernel(const void* __restrict__ dy, const int32_t* _
         for (int py = py0; py <= py1; py++)
             for (int px = px0; px <= px1; px++) {
                 const int q = base + py * ly.sh + px * ly.sw;
-                if (mask[q] == me && (!top || ldv(top, q, bf16) > 0.f)) acc += ldv(dy, q, bf16);
+                const bool hit = mask_u8 ? reinterpret_cast<const uint8_t*>(mask)[q] ==
+                                               (h - (py * g.sh - g.ph)) * g.kw + (w - (px * g.sw - g.pw))
+                                         : reinterpret_cast<const int32_t*>(mask)[q] == me;
+                if (hit && (!top || ldv(top, q, bf16) > 0.f)) acc += ldv(dy, q, bf16);
             }
         stv(dx, t, bf16, acc);
     }
 }
 
-cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, const void* top, L4 ly, void* dx, int xnhwc, int bf16,
-                        const PoolGeom& g, cudaStream_t s) {
+cudaError_t maxpool_bwd(const void* dy, const void* mask, int mask_u8, const void* top, L4 ly, void* dx, int xnhwc,
+                        int bf16, const PoolGeom& g, cudaStream_t s) {
     const int total = g.N * g.C * g.H * g.W;
     const bool ynhwc = ly.sc == 1 && g.C > 1;
     if (bf16 && xnhwc && ynhwc && nhwc8_ok(dy, dx, g.C) && ((reinterpret_cast<uintptr_t>(mask) & 15) == 0) &&
@@ -677,18 +733,24 @@ cudaError_t maxpool_bwd(const void* dy, const int32_t* mask, const void* top, L4
         auto DY = (const __nv_bfloat16*)dy;
         auto T = (const __nv_bfloat16*)top;
         auto DX = (__nv_bfloat16*)dx;
+        const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2, tb = g.N * HB * WB * (g.C / 8);
         if (g.sh == 2 && g.sw == 2 && g.kh <= 3 && g.kw <= 3) {
             // a 2x2 block of positions overlaps at most 2x2 windows of size <= 3
-            const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2, tb = g.N * HB * WB * (g.C / 8);
-            maxpool_bwd_nhwc8<2, 2, 2, 2><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
+            if (mask_u8) maxpool_bwd_nhwc8<2, 2, 2, 2, true><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
+            else maxpool_bwd_nhwc8<2, 2, 2, 2, false><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
         } else if (g.sh == 2 && g.sw == 2) {
-            const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2, tb = g.N * HB * WB * (g.C / 8);
-            maxpool_bwd_nhwc8<2, 2, 0, 0><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
+            if (mask_u8) maxpool_bwd_nhwc8<2, 2, 0, 0, true><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
+            else maxpool_bwd_nhwc8<2, 2, 0, 0, false><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
         } else {
-            maxpool_bwd_nhwc8<1, 1, 0, 0><<<nblk(total / 8, 256), 256, 0, s>>>(DY, mask, T, DX, g, g.H, g.W, total / 8);
+            if (mask_u8)
+                maxpool_bwd_nhwc8<1, 1, 0, 0, true><<<nblk(total / 8, 256), 256, 0, s>>>(DY, mask, T, DX, g, g.H, g.W,
+                                                                                     total / 8);
+            else
+                maxpool_bwd_nhwc8<1, 1, 0, 0, false><<<nblk(total / 8, 256), 256, 0, s>>>(DY, mask, T, DX, g, g.H, g.W,
+                                                                                      total / 8);
         }
     } else {
-        maxpool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, mask, top, ly, dx, xnhwc, bf16, g, total);
+        maxpool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, mask, mask_u8, top, ly, dx, xnhwc, bf16, g, total);
     }
     note_launch();
     return cudaGetLastError();

@@ -156,7 +156,8 @@ class Net:
         self.dscores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
         for i, L in enumerate(layers):
             if L.kind == "pool":
-                self.mask[i] = cb.empty_like_layout(self.shapes[i + 1], torch.int32, device, nhwc=self.nhwc[i + 1])
+                # window-local uint8 argmax (a quarter of the int32 mask traffic; same results)
+                self.mask[i] = cb.empty_like_layout(self.shapes[i + 1], torch.uint8, device, nhwc=self.nhwc[i + 1])
         self.labels = torch.zeros(batch, dtype=torch.int32, device=device)
         self.loss = torch.zeros((), dtype=torch.float32, device=device)
         # the first conv's operand (space-to-depth packed image batch) is built once per step into a

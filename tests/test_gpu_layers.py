@@ -280,3 +280,48 @@ def test_ip_nhwc_bottom(oracle, shape):
     dX2 = cuda(prev).contiguous(memory_format=torch.channels_last)
     cb.ip_backward_data(cuda(dY), cuda(Wt), X.shape, math="bf16", beta=1.0, out=dX2)
     assert_tc_close(host(dX2), rdX + prev, "ip dgrad nhwc beta=1")
+
+
+@pytest.mark.parametrize("case", POOLS + [((2, 96, 55, 55), (3, 3), (2, 2), (1, 1)), ((1, 16, 9, 11), (2, 3), (1, 2), (1, 1))])
+@pytest.mark.parametrize("layout", ["nchw_f32", "nhwc_bf16"])
+def test_maxpool_u8_window_local_mask(oracle, case, layout):
+    """A CAFFE_U8 mask holds the same argmax as the int32 mask, as the index local to the unclipped
+    window: h*W+w == (py*sh-ph + l//kw)*W + (px*sw-pw + l%kw).  Backward (and the ReLU-fused
+    backward) from it equals the oracle bit for bit."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    shape, k, s, p = case
+    kh, kw = k
+    X = synth.uniform(shape, 16, synth.S_X)
+    X[0, 0] = np.round(X[0, 0] * 2)   # ties
+    if layout == "nhwc_bf16":
+        X = oracle.quant_bf16(X)
+        xt = cuda(X).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    else:
+        xt = cuda(X)
+    Y, M8 = cb.pool_forward(xt, "max", k, s, p, mask_dtype=torch.uint8)
+    rY, rM = oracle.maxpool_forward(X, k, s, p)
+    np.testing.assert_array_equal(host(Y), rY)
+    loc = host(M8).astype(np.int64)
+    N, C, OH, OW = rY.shape
+    py = np.arange(OH).reshape(1, 1, OH, 1)
+    px = np.arange(OW).reshape(1, 1, 1, OW)
+    H, W = shape[2], shape[3]
+    absidx = (py * s[0] - p[0] + loc // kw) * W + (px * s[1] - p[1] + loc % kw)
+    np.testing.assert_array_equal(absidx, rM)
+    dY = synth.uniform(rY.shape, 16, synth.S_DY)
+    if layout == "nhwc_bf16":
+        dY = oracle.quant_bf16(dY)
+        dyt = cuda(dY).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    else:
+        dyt = cuda(dY)
+    dX = cb.pool_backward(dyt, M8, shape, "max", k, s, p)
+    ref = oracle.maxpool_backward(dY, rM, shape, k, s, p)
+    if layout == "nhwc_bf16":
+        ref = oracle.quant_bf16(ref)
+    np.testing.assert_array_equal(host(dX), ref)
+    dXr = cb.pool_relu_backward(Y, dyt, M8, shape, k, s, p)
+    refr = oracle.relu_backward(X, oracle.maxpool_backward(dY, rM, shape, k, s, p))
+    if layout == "nhwc_bf16":
+        refr = oracle.quant_bf16(refr)
+    np.testing.assert_array_equal(host(dXr), refr)
