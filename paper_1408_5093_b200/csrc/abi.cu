@@ -1122,33 +1122,41 @@ static caffe_status ip_shapes(const caffe_blob* bottom, const caffe_blob* weight
 // (kchunk per 128-byte block): the fc layers have few (M, N) tiles at batch 256, so the reduction
 // is split until the units fill the SMs once; partials are reduced in a fixed order.
 struct IpPlan {
-    int BN, m_tiles, n_tiles, kblocks, splits, kb_per;
+    int BN, m_tiles, n_tiles, kblocks, splits, kb_per, cg;
     size_t part_bytes;
 };
-static IpPlan ip_plan(long long M, long long Ncols, long long Kred, int kchunk, int BN) {
+// cg_ok: the operand layouts allow a CTA pair (B split in halves); a pair (M = 256 rows) is used
+// when the GEMM has more than 128 rows, so each weight tile is staged once for the whole batch.
+static IpPlan ip_plan(long long M, long long Ncols, long long Kred, int kchunk, int BN, int E, bool cg_ok) {
     IpPlan q;
     q.BN = BN;
-    q.m_tiles = (int)cdiv(M, 128);
+    q.cg = (E == 2 && cg_ok && M > 128 && g_force_cg != 1) ? 2 : 1;
+    const int TM = 128 * q.cg;
+    q.m_tiles = (int)cdiv(M, TM);
     q.n_tiles = (int)cdiv(Ncols, BN);
     q.kblocks = (int)cdiv(Kred, kchunk);
     q.splits = 1;
     q.kb_per = q.kblocks;
     const long long tiles = (long long)q.m_tiles * q.n_tiles;
-    const int sms = 148;
-    if (tiles < sms / 2) {
-        int sp = (int)(sms / tiles);
+    const int slots = 148 / q.cg;   // CTAs (or pairs) resident at once
+    if (tiles < slots / 2) {
+        int sp = (int)(slots / tiles);
         if (sp > q.kblocks / 4) sp = q.kblocks / 4;
         if (sp > 1) {
             q.kb_per = (int)cdiv(q.kblocks, sp);
             q.splits = (int)cdiv(q.kblocks, q.kb_per);
         }
     }
-    q.part_bytes = q.splits > 1 ? align1k((size_t)q.splits * tiles * BN * 128 * 4) : 0;
+    q.part_bytes = q.splits > 1 ? align1k((size_t)q.splits * tiles * BN * TM * 4) : 0;
     return q;
 }
-static IpPlan ip_plan_fwd(long long N, long long K, int O, int E) { return ip_plan(N, O, K, 128 / E, choose_bn(O)); }
+static IpPlan ip_plan_fwd(long long N, long long K, int O, int E) {
+    const int BN = choose_bn(O);
+    return ip_plan(N, O, K, 128 / E, BN, E, (BN / 2) % 8 == 0);
+}
 static IpPlan ip_plan_dgrad(long long N, long long K, int O) {
-    return ip_plan(N, K, O, 64, choose_bn((int)(K < 256 ? K : 256)));
+    const int BN = choose_bn((int)(K < 256 ? K : 256));
+    return ip_plan(N, K, O, 64, BN, 2, (BN / 64) % 2 == 0 && BN % 64 == 0);
 }
 
 caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32_t O, int32_t pass, size_t* bytes) {
@@ -1232,21 +1240,22 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
     float* part = nullptr;
     if (q.splits > 1) { part = (float*)cur; cur += q.part_bytes; }
     L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_K; L.epi = q.splits > 1 ? EPI_PARTIAL : EPI_STRIDED;
+    L.cg = q.cg;
     TcArgs& a = L.args;
     a.BN = q.BN;
     if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 128 / E, 128) ||
-        !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 128 / E, a.BN))
+        !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 128 / E, a.BN / q.cg))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip fwd)");
     a.M = N; a.N = O; a.m_tiles = q.m_tiles; a.n_tiles = q.n_tiles; a.groups = 1; a.splits = q.splits;
     a.kblocks = q.kblocks; a.kb_per_split = q.kb_per;
     a.out = top->ptr; a.out_bf16 = isbf(top); a.s_n = O; a.s_c = 1; a.s_p = 0; a.P = 1; a.col_g = 0;
     a.bias = bptr; a.relu = relu; a.beta = 0.f; a.partial = part;
-    finish_args(a, a.BN * 128);
+    finish_args(a, a.BN / q.cg * 128);
     if (!part) enable_tma_store(L, top->ptr, isbf(top) ? 2 : 4, O, N, O, true);
     if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
     if (part)
-        CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128, N, O, top->ptr, isbf(top), O, bptr, relu,
-                               0.f, 0, 0, s),
+        CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128 * q.cg, N, O, top->ptr, isbf(top), O, bptr,
+                               relu, 0.f, 0, 0, s),
            "ip fwd split-K reduce");
     return CAFFE_OK;
 }
@@ -1293,6 +1302,7 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
     TcLaunch L;
     memset(&L, 0, sizeof L);
     L.esz = E; L.amode = A_TILED_K; L.bmode = B_TILED_MN; L.epi = part ? EPI_PARTIAL : EPI_STRIDED;
+    L.cg = q.cg;
     TcArgs& a = L.args;
     a.BN = q.BN;
     if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 128) || !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 64, 64))
@@ -1306,11 +1316,11 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
         a.out = bottom_diff->ptr; a.out_bf16 = isbf(bottom_diff); a.beta = beta;
     }
     a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1;
-    finish_args(a, a.b_nchunks * 64 * 128);
+    finish_args(a, a.b_nchunks / q.cg * 64 * 128);
     if (!part) enable_tma_store(L, a.out, a.out_bf16 ? 2 : 4, K, N, K, true);
     if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
     if (part)
-        CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128, N, (int)K, bottom_diff->ptr,
+        CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128 * q.cg, N, (int)K, bottom_diff->ptr,
                                isbf(bottom_diff), K, nullptr, 0, beta, permute ? xs.c : 0, xs.h * xs.w, s),
            "ip dgrad split-K reduce");
     else if (rows)
@@ -1371,12 +1381,15 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     L.esz = E; L.amode = A_TILED_MN; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
     TcArgs& a = L.args;
     a.BN = choose_bn((int)(K < 256 ? K : 256));
+    // CTA pairs (M = 256 output rows) stage each bottom tile once for 256 outputs
+    L.cg = (O > 128 && a.BN % 128 == 0 && g_force_cg != 1) ? 2 : 1;
     if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, 64, 64))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip wgrad)");
-    a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1; a.splits = 1;
+    a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128 * L.cg); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1;
+    a.splits = 1;
     a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
     a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
-    finish_args(a, a.b_nchunks * 64 * 128);
+    finish_args(a, a.b_nchunks / L.cg * 64 * 128);
     enable_tma_store(L, weight_diff->ptr, 4, K, O, K, true);
     return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }

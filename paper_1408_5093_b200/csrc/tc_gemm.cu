@@ -166,8 +166,13 @@ __global__ void __launch_bounds__(256, 1)
                     }
                 } else {  // A_TILED_MN
 #pragma unroll
-                    for (int q = 0; q < ESZ; q++)
-                        tma_load_2d(sa + q * CH * 128, &mapA, &full[stage], g * args.a_row_g + m0 + q * CH, kb * CH);
+                    for (int q = 0; q < ESZ; q++) {
+                        if (CG == 2)
+                            tma_load_2d_cg2(sa + q * CH * 128, &mapA, &full[stage], g * args.a_row_g + m0 + q * CH,
+                                            kb * CH);
+                        else
+                            tma_load_2d(sa + q * CH * 128, &mapA, &full[stage], g * args.a_row_g + m0 + q * CH, kb * CH);
+                    }
                 }
                 // ---- B
                 if (BMODE == B_TILED_K) {
@@ -175,9 +180,13 @@ __global__ void __launch_bounds__(256, 1)
                     if (CG == 2) tma_load_2d_cg2(sb, &mapB, &full[stage], kb * CH, row);
                     else tma_load_2d(sb, &mapB, &full[stage], kb * CH, row);
                 } else {
-                    for (int q = 0; q < args.b_nchunks; q++)
-                        tma_load_2d(sb + q * CH * 128, &mapB, &full[stage],
-                                    g * args.b_col_g + n_tile * args.BN + q * CH, kb * CH);
+                    // MN-major B: 64-column chunks; a CTA pair splits them (each CTA stages its half)
+                    const int nch = args.b_nchunks / CG;
+                    for (int q = 0; q < nch; q++) {
+                        const int col = g * args.b_col_g + n_tile * args.BN + ((int)rank * nch + q) * CH;
+                        if (CG == 2) tma_load_2d_cg2(sb + q * CH * 128, &mapB, &full[stage], col, kb * CH);
+                        else tma_load_2d(sb + q * CH * 128, &mapB, &full[stage], col, kb * CH);
+                    }
                 }
                 if (++stage == stages) { stage = 0; phase ^= 1; }
             }
@@ -378,7 +387,11 @@ cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s) {
     TC_CASE(2, A_TILED_K, B_TILED_K, EPI_STRIDED, 2)
     TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_STRIDED, 1)
     TC_CASE(2, A_TILED_K, B_TILED_K, EPI_PARTIAL, 1)
+    TC_CASE(2, A_TILED_K, B_TILED_K, EPI_PARTIAL, 2)
     TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_PARTIAL, 1)
+    TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_PARTIAL, 2)
+    TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_STRIDED, 2)
+    TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 2)
     TC_CASE(4, A_TILED_K, B_TILED_K, EPI_PARTIAL, 1)
     TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 1)
     TC_CASE(4, A_IM2COL_K, B_TILED_K, EPI_STRIDED, 1)
