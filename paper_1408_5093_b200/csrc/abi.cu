@@ -399,7 +399,7 @@ size_t ws_partial(const Plan& p) {
 
 size_t conv_ws(const Plan& p, int pass, caffe_math m) {
     if (pass == CAFFE_PASS_BACKWARD_WEIGHT) {
-        if (m == CAFFE_MATH_FP32) return ws_bias(p);
+        if (m == CAFFE_MATH_FP32 || m == CAFFE_MATH_TF32) return ws_bias(p);
         return ws_x_max(p) + ws_dy_max(p) + ws_partial(p) + ws_bias(p);
     }
     if (m == CAFFE_MATH_FP32) return 0;
@@ -823,19 +823,20 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
         overlap(bias_diff, top_diff) || overlap(bias_diff, weight_diff))
         return fail(CAFFE_E_ALIAS, "weight_diff/bias_diff overlaps an input");
     if (desc->math == CAFFE_MATH_TF32 && top_diff->dtype == CAFFE_BF16) return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
-    if (desc->math == CAFFE_MATH_TF32) return fail(CAFFE_E_DTYPE, "TF32 weight gradient not built yet (use BF16 or FP32 math)");
     if (p.N == 0) return CAFFE_OK;
     const size_t need = conv_ws(p, CAFFE_PASS_BACKWARD_WEIGHT, desc->math);
     if ((st = check_ws(ws, ws_bytes, need))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     char* w8 = (char*)ws;
-    if (desc->math == CAFFE_MATH_FP32) {
+    // TF32 weight gradient: CUDA-core FP32 FMA on TF32-rounded operands (the MN-major TF32
+    // tensor-core operand layout is not built); FP32: the same kernel without rounding.
+    if (desc->math == CAFFE_MATH_FP32 || desc->math == CAFFE_MATH_TF32) {
         if (bias_diff)
             CK(bias_grad(top_diff->ptr, isbf(top_diff), nhwc(top_diff), (float*)bias_diff->ptr, beta, p.N, p.O,
                          p.OH * p.OW, (float*)w8, s),
                "bias grad");
         CK(fp32_conv_wgrad(bottom->ptr, isbf(bottom), strides(bottom), top_diff->ptr, isbf(top_diff), strides(top_diff),
-                           (float*)weight_diff->ptr, beta, cgeom(p), s),
+                           (float*)weight_diff->ptr, beta, cgeom(p), s, desc->math == CAFFE_MATH_TF32),
            "conv wgrad fp32");
         return CAFFE_OK;
     }
@@ -1272,16 +1273,17 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
     if (top_diff->shape.n != N || top_diff->shape.c != O || top_diff->shape.h != 1 || top_diff->shape.w != 1)
         return fail(CAFFE_E_SHAPE, "top_diff must be (%d,%d,1,1)", N, O);
     if (overlap(bottom_diff, top_diff) || overlap(bottom_diff, weight)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
-    if (math == CAFFE_MATH_TF32) return fail(CAFFE_E_DTYPE, "TF32 inner-product backward not built yet");
-    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16) return fail(CAFFE_E_INVALID, "bad math");
+    if (math == CAFFE_MATH_TF32 && (top_diff->dtype == CAFFE_BF16 || weight->dtype == CAFFE_BF16))
+        return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
+    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16 && math != CAFFE_MATH_TF32) return fail(CAFFE_E_INVALID, "bad math");
     if (N == 0) return CAFFE_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const caffe_shape4& xs = bottom_diff->shape;
-    if (math == CAFFE_MATH_FP32) {
+    if (math == CAFFE_MATH_FP32 || math == CAFFE_MATH_TF32) {   // TF32: CUDA cores on TF32-rounded operands
         ConvGeom g{N, xs.c, xs.h, xs.w, O, xs.h, xs.w, 1, 1, 0, 0, 1, 1, 1};
         L4 ly{O, 1, 1, 1};
         CK(fp32_conv_dgrad(top_diff->ptr, isbf(top_diff), ly, weight->ptr, isbf(weight), bottom_diff->ptr,
-                           isbf(bottom_diff), nhwc(bottom_diff), beta, g, s),
+                           isbf(bottom_diff), nhwc(bottom_diff), beta, g, s, math == CAFFE_MATH_TF32),
            "ip dgrad fp32");
         return CAFFE_OK;
     }
@@ -1348,8 +1350,9 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     if (overlap(weight_diff, bottom) || overlap(weight_diff, top_diff) || overlap(bias_diff, bottom) ||
         overlap(bias_diff, top_diff) || overlap(bias_diff, weight_diff))
         return fail(CAFFE_E_ALIAS, "weight_diff/bias_diff overlaps an input");
-    if (math == CAFFE_MATH_TF32) return fail(CAFFE_E_DTYPE, "TF32 inner-product backward not built yet");
-    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16) return fail(CAFFE_E_INVALID, "bad math");
+    if (math == CAFFE_MATH_TF32 && (top_diff->dtype == CAFFE_BF16 || bottom->dtype == CAFFE_BF16))
+        return fail(CAFFE_E_DTYPE, "TF32 math with BF16 storage");
+    if (math != CAFFE_MATH_FP32 && math != CAFFE_MATH_BF16 && math != CAFFE_MATH_TF32) return fail(CAFFE_E_INVALID, "bad math");
     if (N == 0) return CAFFE_OK;
     cudaStream_t s = (cudaStream_t)stream;
     size_t need;
@@ -1359,12 +1362,12 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     float* bpart = (float*)cur;
     cur += align1k((size_t)bias_grad_splits(N, O, 1) * O * 4);
     if (bias_diff) CK(bias_grad(top_diff->ptr, isbf(top_diff), 1, (float*)bias_diff->ptr, beta, N, O, 1, bpart, s), "ip bias grad");
-    if (math == CAFFE_MATH_FP32) {
+    if (math == CAFFE_MATH_FP32 || math == CAFFE_MATH_TF32) {   // TF32: CUDA cores on TF32-rounded operands
         const caffe_shape4& b = bottom->shape;
         ConvGeom g{N, b.c, b.h, b.w, O, b.h, b.w, 1, 1, 0, 0, 1, 1, 1};
         L4 ly{O, 1, 1, 1};
         CK(fp32_conv_wgrad(bottom->ptr, isbf(bottom), strides(bottom), top_diff->ptr, isbf(top_diff), ly,
-                           (float*)weight_diff->ptr, beta, g, s),
+                           (float*)weight_diff->ptr, beta, g, s, math == CAFFE_MATH_TF32),
            "ip wgrad fp32");
         return CAFFE_OK;
     }

@@ -149,10 +149,11 @@ struct ConvGeom {
 };
 cudaError_t fp32_conv_fwd(const void* x, int x_bf16, L4 lx, const void* w, int w_bf16, const float* b, void* y,
                           int y_bf16, L4 ly, int ynhwc, int relu, const ConvGeom& g, cudaStream_t s);
+// tf32 = 1: operands rounded to TF32 (cvt.rn.tf32.f32, as the tensor-core packs do) before the FP32 FMA
 cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, L4 ly, const void* w, int w_bf16, void* dx, int dx_bf16,
-                            int xnhwc, float beta, const ConvGeom& g, cudaStream_t s);
+                            int xnhwc, float beta, const ConvGeom& g, cudaStream_t s, int tf32 = 0);
 cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, L4 lx, const void* dy, int dy_bf16, L4 ly, float* dw,
-                            float beta, const ConvGeom& g, cudaStream_t s);
+                            float beta, const ConvGeom& g, cudaStream_t s, int tf32 = 0);
 int bias_grad_splits(int N, int O, int P);
 cudaError_t bias_grad(const void* dy, int dy_bf16, int nhwc, float* db, float beta, int N, int O, int P, float* part,
                       cudaStream_t s);

@@ -43,6 +43,12 @@ __device__ __forceinline__ void decode(int t, int C, int H, int W, bool nhwc, in
     }
 }
 
+__device__ __forceinline__ float tf32_round(float x) {
+    uint32_t r;
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
 // ================================================================ FP32 reference convolution
 __global__ void conv_fwd_fp32_kernel(const void* __restrict__ x, int xb, L4 lx, const void* __restrict__ w, int wb,
                                      const float* __restrict__ b, void* __restrict__ y, int yb, L4 ly, int ynhwc,
@@ -81,7 +87,8 @@ cudaError_t fp32_conv_fwd(const void* x, int x_bf16, L4 lx, const void* w, int w
 
 // gather form of the data gradient: dX[n,c,h,w] = sum_{o in grp(c), i, j : y=(h+ph-i)/sh, x=(w+pw-j)/sw integral}
 __global__ void conv_dgrad_fp32_kernel(const void* __restrict__ dy, int dyb, L4 ly, const void* __restrict__ w, int wb,
-                                       void* __restrict__ dx, int dxb, int xnhwc, float beta, ConvGeom g, int total) {
+                                       void* __restrict__ dx, int dxb, int xnhwc, float beta, ConvGeom g, int total,
+                                       int tf32) {
     const int Cg = g.C / g.G, Og = g.O / g.G;
     GRID_STRIDE(t, total) {
         int n, c, h, ww;
@@ -99,8 +106,10 @@ __global__ void conv_dgrad_fp32_kernel(const void* __restrict__ dy, int dyb, L4 
                     if (xx < 0 || xx % g.sw) continue;
                     const int ox = xx / g.sw;
                     if (ox >= g.OW) continue;
-                    acc = fmaf(ldv(w, ((o * Cg + cl) * g.kh + i) * g.kw + j, wb),
-                               ldv(dy, n * ly.sn + o * ly.sc + oy * ly.sh + ox * ly.sw, dyb), acc);
+                    float a = ldv(w, ((o * Cg + cl) * g.kh + i) * g.kw + j, wb);
+                    float d = ldv(dy, n * ly.sn + o * ly.sc + oy * ly.sh + ox * ly.sw, dyb);
+                    if (tf32) { a = tf32_round(a); d = tf32_round(d); }
+                    acc = fmaf(a, d, acc);
                 }
             }
         if (beta != 0.f) acc += beta * ldv(dx, t, dxb);
@@ -109,10 +118,10 @@ __global__ void conv_dgrad_fp32_kernel(const void* __restrict__ dy, int dyb, L4 
 }
 
 cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, L4 ly, const void* w, int w_bf16, void* dx, int dx_bf16,
-                            int xnhwc, float beta, const ConvGeom& g, cudaStream_t s) {
+                            int xnhwc, float beta, const ConvGeom& g, cudaStream_t s, int tf32) {
     const int total = g.N * g.C * g.H * g.W;
     conv_dgrad_fp32_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, dy_bf16, ly, w, w_bf16, dx, dx_bf16, xnhwc, beta, g,
-                                                             total);
+                                                             total, tf32);
     note_launch();
     return cudaGetLastError();
 }
@@ -120,7 +129,7 @@ cudaError_t fp32_conv_dgrad(const void* dy, int dy_bf16, L4 ly, const void* w, i
 // Block per weight element; each thread sums a fixed strided subset of the (n, y, x) range, then a
 // fixed-shape tree reduction -> deterministic, blocked FP32 summation (reading R13).
 __global__ void conv_wgrad_fp32_kernel(const void* __restrict__ x, int xb, L4 lx, const void* __restrict__ dy, int dyb,
-                                       L4 ly, float* __restrict__ dw, float beta, ConvGeom g) {
+                                       L4 ly, float* __restrict__ dw, float beta, ConvGeom g, int tf32) {
     __shared__ float red[256];
     const int Cg = g.C / g.G, Og = g.O / g.G;
     const int widx = blockIdx.x;
@@ -139,8 +148,10 @@ __global__ void conv_wgrad_fp32_kernel(const void* __restrict__ x, int xb, L4 lx
         const int oy = p / g.OW, ox = p - oy * g.OW;
         const int h = oy * g.sh - g.ph + i, ww = ox * g.sw - g.pw + j;
         if (h < 0 || h >= g.H || ww < 0 || ww >= g.W) continue;
-        acc = fmaf(ldv(dy, n * ly.sn + o * ly.sc + oy * ly.sh + ox * ly.sw, dyb),
-                   ldv(x, n * lx.sn + cfull * lx.sc + h * lx.sh + ww * lx.sw, xb), acc);
+        float d = ldv(dy, n * ly.sn + o * ly.sc + oy * ly.sh + ox * ly.sw, dyb);
+        float v = ldv(x, n * lx.sn + cfull * lx.sc + h * lx.sh + ww * lx.sw, xb);
+        if (tf32) { d = tf32_round(d); v = tf32_round(v); }
+        acc = fmaf(d, v, acc);
     }
     red[threadIdx.x] = acc;
     __syncthreads();
@@ -152,9 +163,9 @@ __global__ void conv_wgrad_fp32_kernel(const void* __restrict__ x, int xb, L4 lx
 }
 
 cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, L4 lx, const void* dy, int dy_bf16, L4 ly, float* dw,
-                            float beta, const ConvGeom& g, cudaStream_t s) {
+                            float beta, const ConvGeom& g, cudaStream_t s, int tf32) {
     const int nw = g.O * (g.C / g.G) * g.kh * g.kw;
-    conv_wgrad_fp32_kernel<<<(unsigned)nw, 256, 0, s>>>(x, x_bf16, lx, dy, dy_bf16, ly, dw, beta, g);
+    conv_wgrad_fp32_kernel<<<(unsigned)nw, 256, 0, s>>>(x, x_bf16, lx, dy, dy_bf16, ly, dw, beta, g, tf32);
     note_launch();
     return cudaGetLastError();
 }

@@ -80,7 +80,7 @@ def test_conv_backward_data(oracle, case, math):
         assert_tc_close(host(dX2), ref + dX0, "conv dgrad beta=1")
 
 
-@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("math", ["fp32", "bf16", "tf32"])
 @pytest.mark.parametrize("case", CASES, ids=IDS)
 def test_conv_backward_weight(oracle, case, math):
     import paper_1408_5093_b200 as cb

@@ -136,7 +136,7 @@ def test_lrn(oracle, params):
 IPS = [(4, (3, 2, 5), 7), (64, (50, 4, 4), 500), (64, (500, 1, 1), 10), (256, (256, 6, 6), 300)]
 
 
-@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("math", ["fp32", "bf16", "tf32"])
 @pytest.mark.parametrize("case", IPS)
 def test_inner_product(oracle, case, math):
     import paper_1408_5093_b200 as cb
@@ -146,7 +146,7 @@ def test_inner_product(oracle, case, math):
     Wt = synth.xavier((O, K), 7)
     b = synth.uniform((O,), 7, synth.S_B)
     dY = synth.uniform((N, O), 7, synth.S_DY)
-    q = (lambda v: v) if math == "fp32" else oracle.quant_bf16
+    q = {"fp32": (lambda v: v), "bf16": oracle.quant_bf16, "tf32": oracle.quant_tf32_rn}[math]
     chk = assert_fp32_close if math == "fp32" else assert_tc_close
     Y = cb.ip_forward(cuda(X), cuda(Wt), cuda(b), math=math)
     chk(host(Y), oracle.ip_forward(q(X), q(Wt), b), "ip fwd")
