@@ -462,7 +462,16 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     if (2 * 2 * a.acc_stride <= 512 && a.a_stages * 2 * a.halo_slot <= 140 * 1024) a.macc = 2;
     a.b_stage_bytes = a.BN / L.cg * 128;
     const long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
-    a.stages = (int)std::min<long long>(24, budget / a.b_stage_bytes);
+    // weights resident in shared memory when the whole filter (this CTA's half) fits: staged once
+    // per kernel instead of once per unit (the first layer: 9 taps x 6 KB)
+    const long long nb = (long long)h.kh * h.kw * a.a_cblocks;
+    a.b_resident = 0;
+    if (a.groups == 1 && a.n_tiles == 1 && nb <= 24 && nb * a.b_stage_bytes <= budget) {
+        a.b_resident = 1;
+        a.stages = (int)nb;
+    } else {
+        a.stages = (int)std::min<long long>(24, budget / a.b_stage_bytes);
+    }
     if (a.stages < 2) return false;
     const int cols = (2 * a.macc * a.acc_stride <= 512 ? 2 : 1) * a.macc * a.acc_stride;
     a.tmem_cols = pow2ceil(cols < 32 ? 32 : cols);

@@ -56,6 +56,8 @@ struct TcArgs {
     int bias_mma;                       // A_HALO_MN, odd taps: the last pair's spare chunk is all ones, so
                                         // its accumulator rows 64-127 hold sum_pixels dY (bias gradient)
     int a_stages;                       // halo stages in the A ring
+    int b_resident;                     // A_HALO_K: all B tiles (taps x channel blocks) stay in shared
+                                        // memory for the whole kernel (one group, one N tile)
     int tma_store;                      // EPI_STRIDED: store tiles with TMA (mapC; row-major output, beta 0)
     int rows_epi;                       // EPI_STRIDED: row-staged coalesced stores (epi_store_rows)
 };

@@ -95,6 +95,17 @@ __global__ void __launch_bounds__(384, 1)
         const int bn_cta = args.BN / CG;
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
+        if (args.b_resident) {
+            // every (tap, channel block) weight tile once, into its own slot, on one barrier
+            const int nb = taps * cblocks;
+            if (CG == 1 || leader) mbar_arrive_expect_tx(&fullB[0], txB * CG * nb);
+            else mbar_arrive_cluster(mapa_shared(smem_u32(&fullB[0]), 0));
+            for (int kb = 0; kb < nb; kb++) {
+                uint8_t* dst = b_ring + kb * args.b_stage_bytes;
+                if (CG == 2) tma_load_2d_cg2(dst, &mapB, &fullB[0], kb * CH, (int)rank * bn_cta);
+                else tma_load_2d(dst, &mapB, &fullB[0], kb * CH, (int)rank * bn_cta);
+            }
+        }
         for (int u = cid; u < units; u += ncl) {
             int t = u;
             const int n_tile = t % args.n_tiles; t /= args.n_tiles;
@@ -115,6 +126,7 @@ __global__ void __launch_bounds__(384, 1)
                     else tma_load_4d(dst, &mapA, &fullA[sa], c, -args.a_pad_w, y0 - args.a_pad_h, n);
                 }
                 if (++sa == a_stages) { sa = 0; pa ^= 1; }
+                if (args.b_resident) continue;
                 for (int tap = 0; tap < taps; tap++) {
                     mbar_wait(&emptyB[sb], pb ^ 1);
                     if (CG == 1 || leader) mbar_arrive_expect_tx(&fullB[sb], txB * CG);
@@ -135,6 +147,10 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t a_base = smem_u32(a_ring), b_base = smem_u32(b_ring);
         int sa = 0, sb = 0, acc = 0, iters = 0;
         uint32_t pa = 0, pb = 0, acc_phase = 0;
+        if (args.b_resident) {
+            mbar_wait(&fullB[0], 0);
+            tc_fence_after();
+        }
         for (int u = cid; u < units; u += ncl, iters++) {
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
@@ -149,9 +165,13 @@ __global__ void __launch_bounds__(384, 1)
                 int tj = 0;
                 const uint32_t row_skip = (uint32_t)(args.halo_wt - args.a_kw + 1) * 128u;
                 for (int tap = 0; tap < taps; tap++) {
-                    mbar_wait(&fullB[sb], pb);
-                    tc_fence_after();
-                    const uint64_t bd0 = smem_desc_sw128(b_base + sb * args.b_stage_bytes, 16, 1024);
+                    const bool bres = args.b_resident != 0;
+                    if (!bres) {
+                        mbar_wait(&fullB[sb], pb);
+                        tc_fence_after();
+                    }
+                    const uint32_t bslot = bres ? (uint32_t)(tap * cblocks + cb) : (uint32_t)sb;
+                    const uint64_t bd0 = smem_desc_sw128(b_base + bslot * args.b_stage_bytes, 16, 1024);
                     if (elect_one()) {
 #pragma unroll
                         for (int a = 0; a < MACC; a++) {
@@ -164,11 +184,13 @@ __global__ void __launch_bounds__(384, 1)
                                 else umma<2>(dt, ad0 + 2 * k, bd0 + 2 * k, idesc, accum);
                             }
                         }
-                        if (CG == 2) umma_commit_cg2(&emptyB[sb]);
-                        else umma_commit(&emptyB[sb]);
+                        if (!bres) {
+                            if (CG == 2) umma_commit_cg2(&emptyB[sb]);
+                            else umma_commit(&emptyB[sb]);
+                        }
                     }
                     __syncwarp();
-                    if (++sb == b_stages) { sb = 0; pb ^= 1; }
+                    if (!bres && ++sb == b_stages) { sb = 0; pb ^= 1; }
                     if (++tj == args.a_kw) { tj = 0; shift += row_skip; }
                     else shift += 128u;
                 }
