@@ -1171,6 +1171,13 @@ cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long co
     const bool al = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(w_bf16) & 7) == 0;
     if (!al) return cudaErrorMisalignedAddress;
+    // prefer the maximal shared-memory carveout: an SM running update blocks can then also host a
+    // tensor-core CTA (200+ KB of shared memory) without first draining to reconfigure L1/shared
+    static bool carve = false;
+    if (!carve) {
+        cudaFuncSetAttribute(sgd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        carve = true;
+    }
     const long long want = (count / 4 + 511) / 512;   // blocks for 2 vectors per thread
     const int grid = (int)std::max(1LL, std::min<long long>(148LL * g_sgd_blocks_per_sm, want));
     sgd_kernel<<<grid, 256, 0, s>>>(w, g, v, (__nv_bfloat16*)w_bf16, count, lr, mom, decay, gscale);
