@@ -148,6 +148,9 @@ caffe_status caffe_device_check(void);
    1 leaves registers and thread slots for kernels running concurrently on other streams (an update
    overlapped with the backward pass).  Read at launch time. */
 #define CAFFE_TUNE_SGD_BLOCKS_PER_SM 7
+/* CAFFE_TUNE_POOL_STRIP_ROWS: block rows per thread in the channels-last 3x3/s2 max-pool backward
+   (0 = auto).  Results are identical for every value. */
+#define CAFFE_TUNE_POOL_STRIP_ROWS 8
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -573,6 +573,11 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_sgd_blocks_per_sm = value == 0 ? 4 : value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_POOL_STRIP_ROWS) {
+        if (value < 0 || value > 1024) return fail(CAFFE_E_PARAM, "pool strip rows must be 0 (auto) .. 1024");
+        g_pool_strip_rows = value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_ROWS_EPILOGUE) {
         g_rows_epi = value ? 1 : 0;
         return CAFFE_OK;

@@ -688,6 +688,201 @@ __global__ void maxpool_bwd_nhwc8(const __nv_bfloat16* __restrict__ dy, const vo
     }
 }
 
+// ---- 3x3 / stride-2 / unpadded windows that all lie inside the image (every CaffeNet pool: 55->27,
+// 27->13, 13->6).  The general kernels above spend ~1.4k instructions per thread on runtime window
+// geometry and are issue-bound at 2-3x the HBM time; here the geometry is compile-time.
+//
+// Forward: thread = one window x 8 channels; the same packed strict-'>' scan as maxpool_fwd_nhwc8
+// (first element seeds, NaN never wins), the local index i*3+j being the U8 mask byte directly.
+__global__ void maxpool_fwd_k3s2_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                       uint8_t* __restrict__ mask, PoolGeom g, int total) {
+    const int cv = g.C / 8;
+    GRID_STRIDE(t, total) {
+        const int c0 = (t % cv) * 8;
+        int r = t / cv;
+        const int px = r % g.OW; r /= g.OW;
+        const int py = r % g.OH;
+        const int n = r / g.OH;
+        const __nv_bfloat16* base = x + (((long long)n * g.H + 2 * py) * g.W + 2 * px) * g.C + c0;
+        const long long rs = (long long)g.W * g.C;
+        uint4 raw[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) raw[i][j] = __ldg(reinterpret_cast<const uint4*>(base + i * rs + j * g.C));
+        uint32_t bw[4] = {raw[0][0].x, raw[0][0].y, raw[0][0].z, raw[0][0].w};
+        uint32_t aw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                if (i == 0 && j == 0) continue;
+                const uint32_t vw[4] = {raw[i][j].x, raw[i][j].y, raw[i][j].z, raw[i][j].w};
+                const uint32_t pp = (uint32_t)(i * 3 + j) * 0x00010001u;
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vw[e]),
+                                                   *reinterpret_cast<const __nv_bfloat162*>(&bw[e]));
+                    bw[e] = (vw[e] & m) | (bw[e] & ~m);
+                    aw[e] = (pp & m) | (aw[e] & ~m);
+                }
+            }
+        const long long o = (long long)t * 8;
+        *reinterpret_cast<uint4*>(y + o) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+        if (mask)   // 16-bit lane indices (< 9) -> bytes
+            *reinterpret_cast<uint2*>(mask + o) = make_uint2(__byte_perm(aw[0], aw[1], 0x6420),
+                                                             __byte_perm(aw[2], aw[3], 0x6420));
+    }
+}
+
+// Backward: a thread owns a column strip of 2x2 blocks of input positions (block (bh, bw) = rows
+// 2bh, 2bh+1; cols 2bw, 2bw+1) x 8 channels and walks it downwards.  The windows overlapping block
+// (bh, bw) are W11 = (bh-1, bw-1), W10 = (bh-1, bw), W01 = (bh, bw-1), W00 = (bh, bw) -- ascending
+// (py, px), R8's order -- so the lower pair of one block is the upper pair of the next: each window
+// row is fetched once per strip (plus one row per strip start) instead of twice, and the next row's
+// pair is prefetched while the current block is summed.  The window-local index of each block
+// position is fixed: (0,0) is 8 / 6 / 2 / 0 in the four windows, (0,1) is 7 in W10 and 1 in W00,
+// (1,0) is 5 in W01 and 3 in W00, (1,1) is 4 in W00.  A missing window contributes nothing (mask
+// 0xFF).  RELU: the window's gradient passes only when its max y > 0 (packed bf16 compare, false
+// for NaN) -- the fused ReLU backward.  Adding a masked-out +0 leaves an FP32 sum unchanged, so the
+// straight-line sums equal the hit-only sums of maxpool_bwd_kernel bit for bit.
+struct PoolWin {
+    uint4 d, y;
+    uint2 m;
+};
+
+// window at element offset q (valid) or the empty window (mask 0xFF: no position selected)
+template <bool RELU>
+__device__ __forceinline__ void pool_win_load(PoolWin& w, const __nv_bfloat16* __restrict__ dy,
+                                              const uint8_t* __restrict__ mask, const __nv_bfloat16* __restrict__ top,
+                                              long long q, bool valid) {
+    w.d = make_uint4(0u, 0u, 0u, 0u);
+    w.y = make_uint4(0u, 0u, 0u, 0u);
+    w.m = make_uint2(0xffffffffu, 0xffffffffu);
+    if (valid) {
+        w.d = __ldg(reinterpret_cast<const uint4*>(dy + q));
+        w.m = __ldg(reinterpret_cast<const uint2*>(mask + q));
+        if (RELU) w.y = __ldg(reinterpret_cast<const uint4*>(top + q));
+    }
+}
+
+template <bool RELU>
+__device__ __forceinline__ uint32_t pool_gate(uint32_t d, uint32_t y) {
+    if (!RELU) return d;
+    return d & __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&y), __float2bfloat162_rn(0.f));
+}
+
+__device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 v) { return *reinterpret_cast<const uint32_t*>(&v); }
+__device__ __forceinline__ __nv_bfloat162 bits_bf2(uint32_t v) { return *reinterpret_cast<const __nv_bfloat162*>(&v); }
+
+// One 2x2 block from its four windows W11, W10, W01, W00 (ascending (py, px), R8's order); the
+// window-local index of each block position is fixed: (0,0) is 8 / 6 / 2 / 0 in the four windows,
+// (0,1) is 7 in W10 and 1 in W00, (1,0) is 5 in W01 and 3 in W00, (1,1) is 4 in W00.
+template <bool RELU>
+__device__ __forceinline__ void pool_block_k3s2(const PoolWin& w11, const PoolWin& w10, const PoolWin& w01,
+                                                const PoolWin& w00, __nv_bfloat16* o, long long rs, int C, bool right,
+                                                bool lower) {
+    const PoolWin* W[4] = {&w11, &w10, &w01, &w00};
+    // sel(k, t, q): bf16 pair q of window k where the mask byte == t, else +0.  The pair's two mask
+    // bytes are XORed with t and moved into the high byte of each 16-bit lane (0x0000 iff equal;
+    // otherwise a normal number or NaN -- never -0 or subnormal -- as bf16), and a packed bf16
+    // == 0 compare turns that into the lane mask.
+    auto sel = [&](int k, uint32_t t, int q) -> uint32_t {
+        const uint32_t x = ((q < 2) ? W[k]->m.x : W[k]->m.y) ^ (t * 0x01010101u);
+        const uint32_t sp = __byte_perm(x, 0u, (q & 1) ? 0x3424 : 0x1404);
+        const uint32_t dq = q == 0 ? W[k]->d.x : q == 1 ? W[k]->d.y : q == 2 ? W[k]->d.z : W[k]->d.w;
+        const uint32_t yq = q == 0 ? W[k]->y.x : q == 1 ? W[k]->y.y : q == 2 ? W[k]->y.z : W[k]->y.w;
+        return pool_gate<RELU>(dq, yq) & __heq2_mask(bits_bf2(sp), __float2bfloat162_rn(0.f));
+    };
+    const __nv_bfloat162 z2 = __float2bfloat162_rn(0.f);
+    uint32_t o00[4], o01[4], o10[4], o11[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        // (0,0): four windows -> FP32 sum in R8's order, one rounding
+        const uint32_t s0 = sel(0, 8, q), s1 = sel(1, 6, q), s2 = sel(2, 2, q), s3 = sel(3, 0, q);
+        float lo = 0.f, hi = 0.f;
+        lo += __uint_as_float(s0 << 16); hi += __uint_as_float(s0 & 0xffff0000u);
+        lo += __uint_as_float(s1 << 16); hi += __uint_as_float(s1 & 0xffff0000u);
+        lo += __uint_as_float(s2 << 16); hi += __uint_as_float(s2 & 0xffff0000u);
+        lo += __uint_as_float(s3 << 16); hi += __uint_as_float(s3 & 0xffff0000u);
+        o00[q] = bf2_bits(__floats2bfloat162_rn(lo, hi));
+        // (0,1), (1,0): two windows.  RN_bf16(RN_fp32(a + b)) == RN_bf16(a + b) for two bf16 addends
+        // (when a + b is inexact in FP32 the smaller is below 2^-9 ulp_bf16 of the larger), so a
+        // packed bf16 add gives R8's result; the trailing + (+0) maps (-0) + (-0) to R8's +0.
+        o01[q] = bf2_bits(__hadd2(__hadd2(bits_bf2(sel(1, 7, q)), bits_bf2(sel(3, 1, q))), z2));
+        o10[q] = bf2_bits(__hadd2(__hadd2(bits_bf2(sel(2, 5, q)), bits_bf2(sel(3, 3, q))), z2));
+        // (1,1): one window; + (+0) as R8's 0 + v
+        o11[q] = bf2_bits(__hadd2(bits_bf2(sel(3, 4, q)), z2));
+    }
+    *reinterpret_cast<uint4*>(o) = make_uint4(o00[0], o00[1], o00[2], o00[3]);
+    if (right) *reinterpret_cast<uint4*>(o + C) = make_uint4(o01[0], o01[1], o01[2], o01[3]);
+    if (lower) {
+        *reinterpret_cast<uint4*>(o + rs) = make_uint4(o10[0], o10[1], o10[2], o10[3]);
+        if (right) *reinterpret_cast<uint4*>(o + rs + C) = make_uint4(o11[0], o11[1], o11[2], o11[3]);
+    }
+}
+
+// Backward: a thread owns a column strip of 2x2 blocks of input positions (block (bh, bw) = rows
+// 2bh, 2bh+1; cols 2bw, 2bw+1) x 8 channels and walks it downwards.  Block (bh, bw) reads windows
+// (bh-1, bw-1), (bh-1, bw), (bh, bw-1), (bh, bw), so the lower pair of one block is the upper pair
+// of the next: each window row is fetched once per strip (plus one row per strip start) instead
+// of twice, and the next pair is in flight while the current block is summed (three pair slots,
+// rotated by a 3x unrolled loop, so the rotation costs no register moves).  A missing window
+// contributes nothing.  RELU: a window's gradient passes only when its max y > 0 (packed bf16
+// compare, false for NaN) -- the fused ReLU backward.  Adding a masked-out +0 leaves the sums
+// unchanged, so the straight-line sums equal maxpool_bwd_kernel's hit-only sums bit for bit.
+template <bool RELU>
+__global__ void maxpool_bwd_k3s2_nhwc8(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ mask,
+                                       const __nv_bfloat16* __restrict__ top, __nv_bfloat16* __restrict__ dx,
+                                       PoolGeom g, int HB, int WB, int rows, int nstrip, int total) {
+    const unsigned cv = (unsigned)g.C / 8u;
+    const long long wrs = (long long)g.OW * g.C;   // window row stride
+    const long long rs = (long long)g.W * g.C;     // input row stride
+    GRID_STRIDE(t, total) {
+        const int c0 = (int)((unsigned)t % cv) * 8;
+        unsigned r = (unsigned)t / cv;
+        const int bw = (int)(r % (unsigned)WB); r /= (unsigned)WB;
+        const int st = (int)(r % (unsigned)nstrip);
+        const int n = (int)(r / (unsigned)nstrip);
+        const int bh0 = st * rows, bh1 = min(bh0 + rows, HB);
+        const bool lv = bw >= 1, rv = bw < g.OW;
+        // element offset of window (py, bw) -- (py, bw-1) is one C before
+        const long long q0 = ((long long)n * g.OH * g.OW + bw) * g.C + c0;
+        auto load_pair = [&](PoolWin& a, PoolWin& b, int py) {
+            const bool yv = py >= 0 && py < g.OH;
+            const long long q = q0 + (long long)py * wrs;
+            pool_win_load<RELU>(a, dy, mask, top, q - g.C, yv && lv);
+            pool_win_load<RELU>(b, dy, mask, top, q, yv && rv);
+        };
+        PoolWin A0, A1, B0, B1, C0, C1;
+        load_pair(A0, A1, bh0 - 1);
+        load_pair(B0, B1, bh0);
+        __nv_bfloat16* o = dx + (((long long)n * g.H + 2 * bh0) * g.W + 2 * bw) * g.C + c0;
+        const bool right = 2 * bw + 1 < g.W;
+        // step: block bh from upper pair (u0, u1) and lower pair (l0, l1), prefetching row bh+1 into (p0, p1)
+        auto step = [&](const PoolWin& u0, const PoolWin& u1, const PoolWin& l0, const PoolWin& l1, PoolWin& p0,
+                        PoolWin& p1, int bh) {
+            load_pair(p0, p1, bh + 1 < bh1 ? bh + 1 : -1);
+            pool_block_k3s2<RELU>(u0, u1, l0, l1, o, rs, g.C, right, 2 * bh + 1 < g.H);
+            o += 2 * rs;
+        };
+        for (int bh = bh0; bh < bh1; bh += 3) {
+            step(A0, A1, B0, B1, C0, C1, bh);
+            if (bh + 1 >= bh1) break;
+            step(B0, B1, C0, C1, A0, A1, bh + 1);
+            if (bh + 2 >= bh1) break;
+            step(C0, C1, A0, A1, B0, B1, bh + 2);
+        }
+    }
+}
+
+int g_pool_strip_rows = 0;
+
+static inline bool k3s2_full(const PoolGeom& g) {
+    return g.kh == 3 && g.kw == 3 && g.sh == 2 && g.sw == 2 && g.ph == 0 && g.pw == 0 && 2 * (g.OH - 1) + 3 <= g.H &&
+           2 * (g.OW - 1) + 3 <= g.W && g.H <= 2 * g.OH + 1 && g.W <= 2 * g.OW + 1;
+}
+
 static inline bool nhwc8_ok(const void* a, const void* b, int C) {
     return (C % 8) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
 }
@@ -700,7 +895,9 @@ cudaError_t maxpool_fwd(const void* x, L4 lx, void* y, int ynhwc, void* mask, in
         auto X = (const __nv_bfloat16*)x;
         auto Y = (__nv_bfloat16*)y;
         const unsigned nb = nblk(total / 8, 256);
-        if (g.kh == 3 && g.kw == 3) maxpool_fwd_nhwc8<3, 3><<<nb, 256, 0, s>>>(X, Y, mask, mask_u8, g, total / 8);
+        if (k3s2_full(g) && (mask_u8 || !mask))
+            maxpool_fwd_k3s2_nhwc8<<<nb, 256, 0, s>>>(X, Y, (uint8_t*)mask, g, total / 8);
+        else if (g.kh == 3 && g.kw == 3) maxpool_fwd_nhwc8<3, 3><<<nb, 256, 0, s>>>(X, Y, mask, mask_u8, g, total / 8);
         else if (g.kh == 2 && g.kw == 2) maxpool_fwd_nhwc8<2, 2><<<nb, 256, 0, s>>>(X, Y, mask, mask_u8, g, total / 8);
         else maxpool_fwd_nhwc8<0, 0><<<nb, 256, 0, s>>>(X, Y, mask, mask_u8, g, total / 8);
     } else {
@@ -745,7 +942,15 @@ cudaError_t maxpool_bwd(const void* dy, const void* mask, int mask_u8, const voi
         auto T = (const __nv_bfloat16*)top;
         auto DX = (__nv_bfloat16*)dx;
         const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2, tb = g.N * HB * WB * (g.C / 8);
-        if (g.sh == 2 && g.sw == 2 && g.kh <= 3 && g.kw <= 3) {
+        if (mask_u8 && k3s2_full(g)) {
+            const uint8_t* M = (const uint8_t*)mask;
+            // strips of 4 block rows (measured best of 1..28 on pool1/pool2): window rows fetched 5/4
+            // times instead of twice, with enough strips in flight to cover HBM latency
+            const int rows = g_pool_strip_rows > 0 ? g_pool_strip_rows : (HB >= 7 ? 4 : HB);
+            const int nstrip = (HB + rows - 1) / rows, ts = g.N * nstrip * WB * (g.C / 8);
+            if (top) maxpool_bwd_k3s2_nhwc8<true><<<nblk(ts, 256), 256, 0, s>>>(DY, M, T, DX, g, HB, WB, rows, nstrip, ts);
+            else maxpool_bwd_k3s2_nhwc8<false><<<nblk(ts, 256), 256, 0, s>>>(DY, M, T, DX, g, HB, WB, rows, nstrip, ts);
+        } else if (g.sh == 2 && g.sw == 2 && g.kh <= 3 && g.kw <= 3) {
             // a 2x2 block of positions overlaps at most 2x2 windows of size <= 3
             if (mask_u8) maxpool_bwd_nhwc8<2, 2, 2, 2, true><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);
             else maxpool_bwd_nhwc8<2, 2, 2, 2, false><<<nblk(tb, 256), 256, 0, s>>>(DY, mask, T, DX, g, HB, WB, tb);

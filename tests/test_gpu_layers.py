@@ -282,7 +282,10 @@ def test_ip_nhwc_bottom(oracle, shape):
     assert_tc_close(host(dX2), rdX + prev, "ip dgrad nhwc beta=1")
 
 
-@pytest.mark.parametrize("case", POOLS + [((2, 96, 55, 55), (3, 3), (2, 2), (1, 1)), ((1, 16, 9, 11), (2, 3), (1, 2), (1, 1))])
+@pytest.mark.parametrize("case", POOLS + [((2, 96, 55, 55), (3, 3), (2, 2), (1, 1)), ((1, 16, 9, 11), (2, 3), (1, 2), (1, 1)),
+                                  # full 3x3/s2 windows (the specialised kernels), and a clipped last window
+                                  ((2, 256, 13, 13), (3, 3), (2, 2), (0, 0)), ((3, 8, 13, 15), (3, 3), (2, 2), (0, 0)),
+                                  ((1, 8, 14, 14), (3, 3), (2, 2), (0, 0))])
 @pytest.mark.parametrize("layout", ["nchw_f32", "nhwc_bf16"])
 def test_maxpool_u8_window_local_mask(oracle, case, layout):
     """A CAFFE_U8 mask holds the same argmax as the int32 mask, as the index local to the unclipped

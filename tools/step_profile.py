@@ -34,7 +34,7 @@ def main():
     for _ in range(3):
         net.step()
     torch.cuda.synchronize()
-    graph = net.capture()
+    graph = net.capture(overlap_update=os.environ.get("OVERLAP", "0") == "1")
     for _ in range(3):
         graph.replay()
     torch.cuda.synchronize()
