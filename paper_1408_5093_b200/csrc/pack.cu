@@ -286,6 +286,9 @@ __device__ __forceinline__ float w_packed(const void* w, int w_bf16, const WGeom
     return ld_any(w, (((long long)ofull * g.Cg + c) * g.kh + i) * g.kw + j, w_bf16);
 }
 
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+
 __device__ __forceinline__ void st_elem(void* dst, long long i, int esz, float v) {
     if (esz == 2) reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(v);
     else reinterpret_cast<float*>(dst)[i] = tf32_rn(v);
@@ -303,8 +306,40 @@ __global__ void repack_w_fwd_kernel(const void* __restrict__ w, int w_bf16, void
     }
 }
 
+// Plain filters (no s2d) into BF16: thread = one (o, tap) x 8 consecutive packed channels, one
+// 16-byte store; the index arithmetic of the element-wise kernel (several runtime divisions per
+// element) made it issue-bound at ~8 us for a 1.7 MB filter.
+template <typename T>
+__global__ void repack_w_fwd_plain8(const T* __restrict__ w, __nv_bfloat16* __restrict__ dst, WGeom g, int total) {
+    const int taps = g.kh * g.kw;
+    const unsigned cv = (unsigned)g.Cgp / 8u;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int c0 = (int)((unsigned)t % cv) * 8;
+        const unsigned r = (unsigned)t / cv;
+        const int tap = (int)(r % (unsigned)taps);
+        const int o = (int)(r / (unsigned)taps);
+        const T* src = w + ((long long)o * g.Cg + c0) * taps + tap;
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) v[e] = c0 + e < g.Cg ? to_f32(src[(long long)e * taps]) : 0.f;
+        __nv_bfloat162 h[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) h[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+        *reinterpret_cast<uint4*>(dst + (long long)t * 8) = *reinterpret_cast<const uint4*>(h);
+    }
+}
+
 cudaError_t repack_w_fwd(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, cudaStream_t s) {
     const int total = g.O * g.khp * g.kwp * g.Cgp;
+    if (dst_esz == 2 && g.sh == 1 && g.sw == 1 && g.Cgp % 8 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        const int t8 = total / 8;
+        if (w_bf16)
+            repack_w_fwd_plain8<<<blocks_for(t8, 256), 256, 0, s>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)dst, g, t8);
+        else
+            repack_w_fwd_plain8<<<blocks_for(t8, 256), 256, 0, s>>>((const float*)w, (__nv_bfloat16*)dst, g, t8);
+        note_launch();
+        return cudaGetLastError();
+    }
     repack_w_fwd_kernel<<<blocks_for(total, 256), 256, 0, s>>>(w, w_bf16, dst, dst_esz, g, total);
     note_launch();
     return cudaGetLastError();
@@ -329,9 +364,44 @@ __global__ void repack_w_dgrad_kernel(const void* __restrict__ w, int w_bf16, vo
     }
 }
 
+// Plain filters into BF16: thread = one (group, c, tap') x 8 consecutive o, one 16-byte store.
+template <typename T>
+__global__ void repack_w_dgrad_plain8(const T* __restrict__ w, __nv_bfloat16* __restrict__ dst, WGeom g, int total) {
+    const int taps = g.kh * g.kw;
+    const unsigned ov = (unsigned)g.Ogp / 8u;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int o0 = (int)((unsigned)t % ov) * 8;
+        unsigned r = (unsigned)t / ov;
+        const int tap = (int)(r % (unsigned)taps);
+        r /= (unsigned)taps;
+        const int c = (int)(r % (unsigned)g.Cg);
+        const int grp = (int)(r / (unsigned)g.Cg);
+        const int ftap = taps - 1 - tap;   // (kh-1-i', kw-1-j')
+        const T* src = w + (((long long)grp * g.Og + o0) * g.Cg + c) * taps + ftap;
+        const long long os = (long long)g.Cg * taps;
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) v[e] = o0 + e < g.Og ? to_f32(src[e * os]) : 0.f;
+        __nv_bfloat162 h[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) h[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+        *reinterpret_cast<uint4*>(dst + (long long)t * 8) = *reinterpret_cast<const uint4*>(h);
+    }
+}
+
 cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, const WGeom& g, int Cge,
                            cudaStream_t s) {
     const int total = g.G * Cge * g.khp * g.kwp * g.Ogp;
+    if (dst_esz == 2 && g.sh == 1 && g.sw == 1 && Cge == g.Cg && g.Ogp % 8 == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        const int t8 = total / 8;
+        if (w_bf16)
+            repack_w_dgrad_plain8<<<blocks_for(t8, 256), 256, 0, s>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)dst, g, t8);
+        else
+            repack_w_dgrad_plain8<<<blocks_for(t8, 256), 256, 0, s>>>((const float*)w, (__nv_bfloat16*)dst, g, t8);
+        note_launch();
+        return cudaGetLastError();
+    }
     repack_w_dgrad_kernel<<<blocks_for(total, 256), 256, 0, s>>>(w, w_bf16, dst, dst_esz, g, Cge, total);
     note_launch();
     return cudaGetLastError();
