@@ -151,6 +151,10 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_POOL_STRIP_ROWS: block rows per thread in the channels-last 3x3/s2 max-pool backward
    (0 = auto).  Results are identical for every value. */
 #define CAFFE_TUNE_POOL_STRIP_ROWS 8
+/* CAFFE_TUNE_WGRAD_REDUCE_SG: weight-gradient split reductions with at least this many splits use
+   several threads per output (fixed-order tree; 0 = default 24).  Deterministic for every value;
+   values differ only in the FP32 summation order. */
+#define CAFFE_TUNE_WGRAD_REDUCE_SG 9
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

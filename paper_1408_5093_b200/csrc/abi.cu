@@ -573,6 +573,11 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_sgd_blocks_per_sm = value == 0 ? 4 : value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_WGRAD_REDUCE_SG) {
+        if (value < 0) return fail(CAFFE_E_PARAM, "split-group reduction threshold must be >= 0 (0 = default 24)");
+        g_wgrad_reduce_sg_min = value == 0 ? 24 : value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_POOL_STRIP_ROWS) {
         if (value < 0 || value > 1024) return fail(CAFFE_E_PARAM, "pool strip rows must be 0 (auto) .. 1024");
         g_pool_strip_rows = value;

@@ -182,6 +182,7 @@ cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, 
                            int diff_bf16, int N, int K, cudaStream_t s);
 extern int g_sgd_blocks_per_sm;
 extern int g_pool_strip_rows;   // CAFFE_TUNE_POOL_STRIP_ROWS
+extern int g_wgrad_reduce_sg_min;   // CAFFE_TUNE_WGRAD_REDUCE_SG
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,
                   float decay, float gscale, cudaStream_t s);
 

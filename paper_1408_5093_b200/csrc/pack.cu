@@ -1,3 +1,4 @@
+#include <algorithm>
 // pack.cu -- layout kernels around the tensor-core GEMM: activations into the packed channels-last
 // operand layout (transpose of NCHW blobs, space-to-depth for strided convolutions, dtype
 // conversion), weight repacks for the forward and data-gradient operands, the s2d data-gradient
@@ -460,9 +461,93 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __
     }
 }
 
+int g_wgrad_reduce_sg_min = 24;
+
+// Many splits (the halo weight gradients split the pixel reduction over ~all SMs): SG threads per
+// output each sum a contiguous range of splits (ascending, 4 loads in flight), and the SG range
+// sums are added in ascending range order -- a fixed tree, so deterministic, with SG x the loads
+// in flight of the one-thread-per-output form (which was latency-bound: ~150 dependent rounds).
+// blockDim = (32, SG); lanes = consecutive outputs (coalesced partial rows).  The bias gradient
+// (db) rides along as G*Og extra outputs after the weights.
+template <int SG>
+__global__ void wgrad_reduce_sg_kernel(const float* __restrict__ partial, float* __restrict__ dW, float beta, WGeom g,
+                                       int m_tiles, int n_tiles, int splits, int BN, int chunk, int cblocks,
+                                       int chunks_per_tile, int total, int cbmajor, float* __restrict__ db) {
+    __shared__ float part[SG][33];
+    const int nq = g.khp * g.kwp * cblocks;
+    const int pairs = (g.khp * g.kwp + 1) / 2;
+    const long long sstride = (long long)g.G * m_tiles * n_tiles * BN * 128;
+    const int per = (splits + SG - 1) / SG;
+    const int sp0 = min(splits, (int)threadIdx.y * per), sp1 = min(splits, sp0 + per);
+    const int nout = total + (db ? g.G * g.Og : 0);
+    for (int base = blockIdx.x * 32; base < nout; base += gridDim.x * 32) {
+        const int t = base + threadIdx.x;
+        const float* pp = nullptr;
+        float* dst = nullptr;
+        if (t < total) {
+            const int rr = t % chunk;
+            int r = t / chunk;
+            const int q = r % nq;
+            r /= nq;
+            const int o = r % g.Og;
+            const int grp = r / g.Og;
+            const int tap = q / cblocks;
+            const int cc = (q % cblocks) * chunk + rr;
+            if (cc < g.Cg * g.sh * g.sw) {
+                const int d = cc / g.Cg, c = cc % g.Cg;
+                const int i = (tap / g.kwp) * g.sh + d / g.sw, j = (tap % g.kwp) * g.sw + d % g.sw;
+                if (i < g.kh && j < g.kw) {
+                    const int m_tile = cbmajor ? (q % cblocks) * pairs + tap / 2 : q / chunks_per_tile;
+                    const int row = cbmajor ? (tap & 1) * chunk + rr : (q % chunks_per_tile) * chunk + rr;
+                    const int n_tile = o / BN, col = o % BN;
+                    pp = partial + ((((long long)grp * m_tiles + m_tile) * n_tiles + n_tile) * BN + col) * 128 + row;
+                    dst = dW + (((long long)(grp * g.Og + o) * g.Cg + c) * g.kh + i) * g.kw + j;
+                }
+            }
+        } else if (t < nout) {   // bias gradient: the ones chunk, pair (pairs-1) of channel block 0, row 64
+            const int u = t - total;
+            const int o = u % g.Og, grp = u / g.Og;
+            const int n_tile = o / BN, col = o % BN;
+            pp = partial + ((((long long)grp * m_tiles + (pairs - 1)) * n_tiles + n_tile) * BN + col) * 128 + 64;
+            dst = db + u;
+        }
+        float acc = 0.f;
+        if (pp) {
+            int sp = sp0;
+            for (; sp + 4 <= sp1; sp += 4) {
+                const float a0 = pp[sp * sstride], a1 = pp[(sp + 1) * sstride], a2 = pp[(sp + 2) * sstride],
+                            a3 = pp[(sp + 3) * sstride];
+                acc += a0; acc += a1; acc += a2; acc += a3;
+            }
+            for (; sp < sp1; sp++) acc += pp[sp * sstride];
+        }
+        part[threadIdx.y][threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.y == 0 && dst) {
+            float r = part[0][threadIdx.x];
+#pragma unroll
+            for (int k = 1; k < SG; k++) r += part[k][threadIdx.x];
+            *dst = (beta != 0.f ? beta * *dst : 0.f) + r;
+        }
+        __syncthreads();
+    }
+}
+
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
                          int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor, float* db) {
     const int total = g.G * g.Og * g.khp * g.kwp * cblocks * chunk;
+    if (splits >= g_wgrad_reduce_sg_min) {
+        const int nout = total + (db ? g.G * g.Og : 0);
+        const unsigned nb = (unsigned)std::min<long long>((nout + 31) / 32, 148LL * 16);
+        if (splits >= 32)
+            wgrad_reduce_sg_kernel<8><<<nb, dim3(32, 8), 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
+                                                                chunk, cblocks, 128 / chunk, total, cbmajor, db);
+        else
+            wgrad_reduce_sg_kernel<4><<<nb, dim3(32, 4), 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
+                                                                chunk, cblocks, 128 / chunk, total, cbmajor, db);
+        note_launch();
+        return cudaGetLastError();
+    }
     wgrad_reduce_kernel<<<blocks_for(total, 256), 256, 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
                                                                chunk, cblocks, 128 / chunk, total, cbmajor, db);
     note_launch();

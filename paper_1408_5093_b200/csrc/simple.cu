@@ -1331,7 +1331,10 @@ __device__ __forceinline__ uint2 bf16x4(const float4& wv) {
     pk.y = *reinterpret_cast<uint32_t*>(&b);
     return pk;
 }
-__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
+// <= 48 registers (launch bounds 256 x 5): a 256-thread update block then fits beside a 200-register
+// tensor-core GEMM CTA (256 x 208 of the 64K registers), so the per-layer side-stream update
+// co-runs with the backward GEMMs instead of delaying their launch.
+__global__ void __launch_bounds__(256, 5) sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
                            __nv_bfloat16* __restrict__ wb, long long n, float lr, float mom, float decay, float gs) {
     const long long n4 = n / 4;
     const long long stride = (long long)gridDim.x * blockDim.x;

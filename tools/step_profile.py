@@ -26,6 +26,11 @@ def main():
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
     dev = torch.device("cuda")
+    # CAFFE_TUNE="key=value,..." : library tuning knobs (caffe_set_tuning) for A/B runs
+    from paper_1408_5093_b200 import _abi
+    for kv in filter(None, os.environ.get("CAFFE_TUNE", "").split(",")):
+        k, v = kv.split("=")
+        _abi.call("caffe_set_tuning", int(k), int(v))
     net = nets.Net(nets.CAFFENET, args.batch, nets.CAFFENET_INPUT, dev, math="bf16", seed=0)
     import synth
     net.a[0].copy_(torch.from_numpy(synth.int_pixels((args.batch,) + tuple(nets.CAFFENET_INPUT), 1000))
@@ -59,6 +64,13 @@ def main():
     print(f"kernels per step: {per_step}; summed kernel time per step: {total:.1f} us")
     for pos, name, us in rows:
         print(f"{pos:4d} {us:9.1f} us  {name}")
+    if os.environ.get("TIMELINE") == "1":
+        # last profiled step: start / end relative to its first kernel, and the stream
+        last = evs[per_step * (args.steps - 1): per_step * args.steps]
+        t0 = min(e.time_range.start for e in last)
+        print("--- timeline of the last step (us from its first kernel)")
+        for e in sorted(last, key=lambda e: e.time_range.start):
+            print(f"{e.time_range.start - t0:9.1f} {e.time_range.end - t0:9.1f}  s{getattr(e, 'device_resource_id', '?')}  {e.name.split('(')[0][:70]}")
     print("--- by kernel name")
     for name, us in sorted(by_name.items(), key=lambda kv: -kv[1]):
         print(f"{us:9.1f} us  {100 * us / total:5.1f}%  {name}")
