@@ -207,9 +207,76 @@ __global__ void pack_s2d_rows_kernel(const __nv_bfloat16* __restrict__ src, L4 l
     }
 }
 
+// Space-to-depth of a channels-last BF16 image batch without padding, one group (conv1: 3
+// channels, 4x4 blocks).  Packed channels [dy*sw*C, (dy+1)*sw*C) of packed pixel (Y, X) are the
+// sw*C consecutive source elements of row Y*sh + dy starting at column X*sw -- one contiguous
+// segment.  Thread = one (n, Y, X, dy) segment of NW 32-bit words: the covering source words are
+// loaded 4-byte aligned (NHWC rows of 3 channels are only 2-byte aligned) and realigned with a
+// byte permute, stored as 8-byte words; the dy = sh-1 thread also zero-fills the channel padding.
+// Source elements past the image (last block column / row) are 0.  ~20 instructions per 24-byte
+// segment instead of the row-staged kernel's table lookups per element.
+template <int NW>
+__global__ void pack_s2d_seg_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, PackGeom g,
+                                    int total) {
+    constexpr int L = 2 * NW;   // elements per segment (= sw * C)
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int dy = t % g.sh;
+        int r = t / g.sh;
+        const int X = r % g.Wp; r /= g.Wp;
+        const int Y = r % g.Hp;
+        const int n = r / g.Hp;
+        const int h = Y * g.sh + dy;
+        const int nv = h < g.H ? max(0, min(L, (g.W - X * g.sw) * g.C)) : 0;   // valid elements
+        uint32_t o[NW];
+        if (nv > 0) {
+            const __nv_bfloat16* p = src + (((long long)n * g.H + h) * g.W + (long long)X * g.sw) * g.C;
+            const uintptr_t b = reinterpret_cast<uintptr_t>(p);
+            const uint32_t* wp = reinterpret_cast<const uint32_t*>(b & ~uintptr_t(3));
+            if ((b & 3) == 0) {
+#pragma unroll
+                for (int i = 0; i < NW; i++) o[i] = 2 * i < nv ? __ldg(wp + i) : 0u;
+            } else {   // element k sits in word (k + 1) / 2
+                uint32_t w[NW + 1];
+#pragma unroll
+                for (int j = 0; j <= NW; j++) w[j] = 2 * j - 1 < nv ? __ldg(wp + j) : 0u;
+#pragma unroll
+                for (int i = 0; i < NW; i++) o[i] = __byte_perm(w[i], w[i + 1], 0x5432);
+            }
+            if (nv < L) {   // clear the elements past the image edge
+#pragma unroll
+                for (int i = 0; i < NW; i++) {
+                    if (2 * i >= nv) o[i] = 0u;
+                    else if (2 * i + 1 >= nv) o[i] &= 0xffffu;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NW; i++) o[i] = 0u;
+        }
+        __nv_bfloat16* q = dst + (((long long)n * g.Hp + Y) * g.Wp + X) * g.Ctot + dy * L;
+        uint2* q2 = reinterpret_cast<uint2*>(q);
+#pragma unroll
+        for (int i = 0; i < NW / 2; i++) q2[i] = make_uint2(o[2 * i], o[2 * i + 1]);
+        if (dy == g.sh - 1) {
+            __nv_bfloat16* z = q + L;   // channels [sh*L, Ctot)
+            for (int c = 0; c < g.Ctot - g.sh * L; c += 4) *reinterpret_cast<uint2*>(z + c) = make_uint2(0u, 0u);
+        }
+    }
+}
+
 cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* dst, int dst_esz, const PackGeom& g,
                      cudaStream_t s) {
     const bool plain = g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.Hp == g.H && g.Wp == g.W;
+    if (!plain && dst_esz == 2 && src_bf16 && src_nhwc && ls.sc == 1 && ls.sw == g.C && g.G == 1 && g.ph == 0 &&
+        g.pw == 0 && g.sw * g.C == 12 && g.cpg == g.Ctot && g.Ctot % 8 == 0 && g.Ctot >= g.sh * 12 &&
+        (g.Ctot - g.sh * 12) % 4 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+        ls.sn == (long long)g.H * g.W * g.C) {
+        const int total = g.N * g.Hp * g.Wp * g.sh;
+        pack_s2d_seg_kernel<6><<<blocks_for(total, 256), 256, 0, s>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, g,
+                                                                       total);
+        note_launch();
+        return cudaGetLastError();
+    }
     const size_t rows_smem = ((size_t)g.sh * g.W * g.C * 2 + 16 + 15) / 16 * 16 + 16 + (size_t)g.Ctot * 4;
     if (!plain && dst_esz == 2 && src_bf16 && src_nhwc && ls.sc == 1 && ls.sw == g.C && g.Ctot % 8 == 0 &&
         rows_smem <= 96 * 1024 && g.C < 65536 && g.sh < 128 && g.sw < 256) {
