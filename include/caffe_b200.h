@@ -155,6 +155,9 @@ caffe_status caffe_device_check(void);
    several threads per output (fixed-order tree; 0 = default 24).  Deterministic for every value;
    values differ only in the FP32 summation order. */
 #define CAFFE_TUNE_WGRAD_REDUCE_SG 9
+/* CAFFE_TUNE_HALO_KTRIM: halo-tiled forward / data gradient skip the K steps of the padding
+   channels of the last 64-channel block (1 = default, 0 = multiply the zero padding). */
+#define CAFFE_TUNE_HALO_KTRIM 10
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

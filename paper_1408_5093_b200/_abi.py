@@ -31,6 +31,7 @@ CAFFE_TUNE_ROWS_EPILOGUE = 6
 CAFFE_TUNE_SGD_BLOCKS_PER_SM = 7
 CAFFE_TUNE_POOL_STRIP_ROWS = 8
 CAFFE_TUNE_WGRAD_REDUCE_SG = 9
+CAFFE_TUNE_HALO_KTRIM = 10
 
 
 class Shape4(ctypes.Structure):

@@ -436,6 +436,7 @@ static bool halo_applies(int E, const HaloGeom& h) {
 }
 // Fills the halo fields of L (A map over the channels-last operand `aptr` [N][Hi][Wi][Ctot]) after
 // the caller has set BN, N, n_tiles, groups, b_row_g, a_cpg, a_cblocks and the epilogue.
+int g_halo_ktrim = 1;   // CAFFE_TUNE_HALO_KTRIM
 static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Ctot, int N) {
     TcArgs& a = L.args;
     L.amode = A_HALO_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED; L.esz = 2;
@@ -573,6 +574,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_sgd_blocks_per_sm = value == 0 ? 4 : value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_HALO_KTRIM) {
+        g_halo_ktrim = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_WGRAD_REDUCE_SG) {
         if (value < 0) return fail(CAFFE_E_PARAM, "split-group reduction threshold must be >= 0 (0 = default 24)");
         g_wgrad_reduce_sg_min = value == 0 ? 24 : value;
@@ -706,6 +711,7 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
         a.a_cblocks = p.Cgp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Og;
         set_out(a, top);
         a.col_g = p.Og; a.bias = bptr; a.relu = relu; a.beta = 0.f;
+        a.k_last = g_halo_ktrim ? (int)cdiv(p.Cge - p.CH * (a.a_cblocks - 1), 16) : 0;
         if (!halo_setup(L, hg, aptr, A.Ctot, p.N)) return fail(CAFFE_E_CUDA, "halo tile setup failed (activation)");
         if (!encode_tiled_2d(&L.mapB, p.E, WB, (uint64_t)p.taps * p.Cgp, (uint64_t)p.O, (uint64_t)p.taps * p.Cgp * p.E,
                              p.CH, a.BN / L.cg))
@@ -781,6 +787,7 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
         a.a_cblocks = p.Ogp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Cge;
         set_out(a, bottom_diff);
         a.col_g = p.Cg; a.beta = beta;
+        a.k_last = g_halo_ktrim ? (int)cdiv(p.Og - p.CH * (a.a_cblocks - 1), 16) : 0;
         if (!halo_setup(L, hg, aptr, A.Ctot, p.N)) return fail(CAFFE_E_CUDA, "halo tile setup failed (top_diff)");
         if (!encode_tiled_2d(&L.mapB, p.E, WD, (uint64_t)p.taps * p.Ogp, (uint64_t)p.G * p.Cge,
                              (uint64_t)p.taps * p.Ogp * p.E, p.CH, a.BN / L.cg))

@@ -60,6 +60,8 @@ struct TcArgs {
                                         // memory for the whole kernel (one group, one N tile)
     int tma_store;                      // EPI_STRIDED: store tiles with TMA (mapC; row-major output, beta 0)
     int rows_epi;                       // EPI_STRIDED: row-staged coalesced stores (epi_store_rows)
+    int k_last;                         // A_HALO_K: 16-channel K steps needed by the last channel block
+                                        // (0 = all 4); 3 with a single block selects the KS = 3 kernel
 };
 
 struct TcLaunch {

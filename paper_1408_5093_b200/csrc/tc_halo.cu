@@ -34,12 +34,14 @@ size_t tc_halo_smem_bytes(const TcArgs& a) {
            2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN + (a.rows_epi ? 4 * 32 * 17 * 16 : 0);
 }
 
-template <int CG, int MACC>
+// KS: 16-channel K steps issued per 64-channel block (4; 3 when the only block holds 48 real
+// channels -- conv1 after space-to-depth, conv2 per group -- so the zero padding is not multiplied)
+template <int CG, int MACC, int KS>
 __global__ void __launch_bounds__(384, 1)
     tc_halo_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const TcArgs args) {
     constexpr int CH = 64;                 // bf16 channels per 128-byte row
-    constexpr int KSTEPS = 4;              // K = 16 per tcgen05.mma
+    constexpr int KSTEPS = KS;             // K = 16 per tcgen05.mma
     constexpr int TM = 128 * CG;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + HALO_SMEM_ALIGN - 1) &
@@ -519,9 +521,9 @@ cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s) {
     }
 }
 
-template <int CG, int MACC>
+template <int CG, int MACC, int KS>
 static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
-    auto kern = tc_halo_kernel<CG, MACC>;
+    auto kern = tc_halo_kernel<CG, MACC, KS>;
     const size_t smem = tc_halo_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -551,8 +553,12 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s) {
     if (L.esz != 2) return cudaErrorInvalidValue;
     const int macc = L.args.macc > 1 ? L.args.macc : 1;
     if (macc > 2) return cudaErrorInvalidValue;
-    if (L.cg == 2) return macc == 2 ? halo_launch_one<2, 2>(L, s) : halo_launch_one<2, 1>(L, s);
-    return macc == 2 ? halo_launch_one<1, 2>(L, s) : halo_launch_one<1, 1>(L, s);
+    if (L.args.k_last == 3 && L.args.a_cblocks == 1) {
+        if (L.cg == 2) return macc == 2 ? halo_launch_one<2, 2, 3>(L, s) : halo_launch_one<2, 1, 3>(L, s);
+        return macc == 2 ? halo_launch_one<1, 2, 3>(L, s) : halo_launch_one<1, 1, 3>(L, s);
+    }
+    if (L.cg == 2) return macc == 2 ? halo_launch_one<2, 2, 4>(L, s) : halo_launch_one<2, 1, 4>(L, s);
+    return macc == 2 ? halo_launch_one<1, 2, 4>(L, s) : halo_launch_one<1, 1, 4>(L, s);
 }
 
 }  // namespace cb
