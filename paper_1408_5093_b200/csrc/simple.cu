@@ -1080,6 +1080,24 @@ __device__ __forceinline__ void load24(const __nv_bfloat16* p, int c0, int C, fl
     for (int e = 0; e < 8; e++) { v[e] = a[e]; v[8 + e] = b[e]; v[16 + e] = c[e]; }
 }
 
+// MUFU forms without the subnormal range handling of __powf / __fdividef: S >= k > 0 here (k = 1
+// in CaffeNet), and the results are rounded to BF16, far above the ~2^-22 error of the approximations.
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 template <int R>
 __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                               float* __restrict__ scale, int C, int size, float alpha, float beta, float k, int total) {
@@ -1090,7 +1108,6 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
         const long long base = (long long)(t / cv) * C;
         float xv[24];
         load24(x + base, c0, C, xv);
-        // bf16 output: the MUFU lg2/ex2 power (rel. err ~1e-7) is far below the bf16 rounding step
         float out[8], S[8];
 #pragma unroll
         for (int e = 0; e < 8; e++) {
@@ -1098,7 +1115,7 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
 #pragma unroll
             for (int j = -R; j <= R; j++) s2 = fmaf(xv[8 + e + j], xv[8 + e + j], s2);
             S[e] = k + an * s2;
-            out[e] = xv[8 + e] * __powf(S[e], -beta);
+            out[e] = xv[8 + e] * ex2_ftz(-beta * lg2_ftz(S[e]));
         }
         *reinterpret_cast<uint4*>(y + base + c0) = pack8(out);
         if (scale) {
@@ -1109,12 +1126,15 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
     }
 }
 
+// Backward: the window sums over the 8 + 2R channel scales and the 8 outputs slide (one add and one
+// subtract per step instead of 2R + 1 terms); FP32 throughout, BF16 output.
 template <int R>
 __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
                               const __nv_bfloat16* __restrict__ dy, __nv_bfloat16* __restrict__ dx, int C, int size,
                               float alpha, float beta, float k, int total) {
     const int cv = C / 8;
     const float an = alpha / size;
+    const float cb = 2.f * an * beta;
     GRID_STRIDE(t, total) {
         const int c0 = (t % cv) * 8;
         const long long base = (long long)(t / cv) * C;
@@ -1122,23 +1142,27 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
         load24(x + base, c0, C, xv);
         load24(y + base, c0, C, yv);
         load24(dy + base, c0, C, gv);
-        // bf16 output: approximate MUFU reciprocal / power are far below the bf16 rounding step
         float S[24], tv[24];
+        float s2 = 0.f;
+#pragma unroll
+        for (int j = 8 - 2 * R; j <= 8; j++) s2 = fmaf(xv[j], xv[j], s2);   // window of channel 8 - R
 #pragma unroll
         for (int i = 8 - R; i < 16 + R; i++) {
-            float s2 = 0.f;
-#pragma unroll
-            for (int j = -R; j <= R; j++) s2 = fmaf(xv[i + j], xv[i + j], s2);
+            if (i > 8 - R) {
+                s2 = fmaf(xv[i + R], xv[i + R], s2);
+                s2 = fmaf(-xv[i - R - 1], xv[i - R - 1], s2);
+            }
             S[i] = k + an * s2;
-            tv[i] = __fdividef(gv[i] * yv[i], S[i]);
+            tv[i] = gv[i] * yv[i] * rcp_ftz(S[i]);
         }
         float out[8];
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 8 - R; j <= 8 + R; j++) acc += tv[j];
 #pragma unroll
         for (int e = 0; e < 8; e++) {
-            float acc = 0.f;
-#pragma unroll
-            for (int j = -R; j <= R; j++) acc += tv[8 + e + j];
-            out[e] = gv[8 + e] * __powf(S[8 + e], -beta) - 2.f * an * beta * xv[8 + e] * acc;
+            if (e > 0) acc = acc + tv[8 + e + R] - tv[8 + e - R - 1];
+            out[e] = gv[8 + e] * ex2_ftz(-beta * lg2_ftz(S[8 + e])) - cb * xv[8 + e] * acc;
         }
         *reinterpret_cast<uint4*>(dx + base + c0) = pack8(out);
     }
