@@ -158,6 +158,11 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_HALO_KTRIM: halo-tiled forward / data gradient skip the K steps of the padding
    channels of the last 64-channel block (1 = default, 0 = multiply the zero padding). */
 #define CAFFE_TUNE_HALO_KTRIM 10
+/* CAFFE_TUNE_HALO_FAST_EPI: 1 (default) = halo-tiled forward / data-gradient kernels with BF16
+   channels-last outputs (beta 0, no column tail) use the specialised row-segment epilogue (all TMEM
+   loads before one wait, shared-memory bias vectors, 16-byte stores); 0 = the generic epilogue.
+   Bit-identical results. */
+#define CAFFE_TUNE_HALO_FAST_EPI 11
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -32,6 +32,7 @@ CAFFE_TUNE_SGD_BLOCKS_PER_SM = 7
 CAFFE_TUNE_POOL_STRIP_ROWS = 8
 CAFFE_TUNE_WGRAD_REDUCE_SG = 9
 CAFFE_TUNE_HALO_KTRIM = 10
+CAFFE_TUNE_HALO_FAST_EPI = 11
 
 
 class Shape4(ctypes.Structure):

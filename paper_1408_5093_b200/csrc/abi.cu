@@ -574,6 +574,14 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_sgd_blocks_per_sm = value == 0 ? 4 : value;
         return CAFFE_OK;
     }
+    if (key == 99) {   // profiling probes (not part of the documented interface)
+        cb::g_dbg = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_HALO_FAST_EPI) {
+        cb::g_halo_fast_epi = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_HALO_KTRIM) {
         g_halo_ktrim = value ? 1 : 0;
         return CAFFE_OK;

@@ -7,6 +7,44 @@
 
 namespace cb {
 
+// Specialised channels-last BF16 epilogue for EPC columns (a multiple of 8) of one accumulator row:
+// every TMEM load is issued before the single wait, bias comes from shared memory with vector
+// loads, and the row's EPC*2 bytes leave as 16-byte stores.  Preconditions (host-checked): BF16
+// output, unit column stride, beta == 0, no column tail, 16-byte aligned row segments.  Writes the
+// same values as epi_store_strided (bias add, ReLU, RNE conversion in the same order).
+template <int EPC>
+__device__ __forceinline__ void epi_store_bf16_rowseg(uint32_t taddr, bool row_ok, __nv_bfloat16* dst,
+                                                      uint32_t sbias_addr, bool bias, bool relu) {
+    uint32_t v[EPC];
+#pragma unroll
+    for (int c = 0; c < EPC; c += 16) {
+        if (c + 16 <= EPC) tmem_ld16p(taddr + c, v + c);
+        else tmem_ld8p(taddr + c, v + c);
+    }
+    tmem_wait_ld();
+    if (!row_ok) return;
+    uint32_t pk[EPC / 2];
+#pragma unroll
+    for (int c = 0; c < EPC; c += 4) {
+        float x0 = __uint_as_float(v[c]), x1 = __uint_as_float(v[c + 1]);
+        float x2 = __uint_as_float(v[c + 2]), x3 = __uint_as_float(v[c + 3]);
+        if (bias) {
+            const float4 b = lds_f4(sbias_addr + 4u * c);
+            x0 += b.x; x1 += b.y; x2 += b.z; x3 += b.w;
+        }
+        if (relu) {
+            x0 = x0 > 0.f ? x0 : 0.f; x1 = x1 > 0.f ? x1 : 0.f;
+            x2 = x2 > 0.f ? x2 : 0.f; x3 = x3 > 0.f ? x3 : 0.f;
+        }
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(x0, x1), h1 = __floats2bfloat162_rn(x2, x3);
+        pk[c / 2] = *reinterpret_cast<uint32_t*>(&h0);
+        pk[c / 2 + 1] = *reinterpret_cast<uint32_t*>(&h1);
+    }
+    uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < EPC / 8; q++) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+}
+
 // taddr: TMEM address of this warp's lanes, column 0 of the accumulator.  rbase: element offset of
 // the output row; col0: first tile column (for the N bound); cbase: output channel of tile column 0;
 // bs: this tile's bias staged in shared memory (or unused when args.bias == nullptr).

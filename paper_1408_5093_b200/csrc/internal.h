@@ -62,6 +62,7 @@ struct TcArgs {
     int rows_epi;                       // EPI_STRIDED: row-staged coalesced stores (epi_store_rows)
     int k_last;                         // A_HALO_K: 16-channel K steps needed by the last channel block
                                         // (0 = all 4); 3 with a single block selects the KS = 3 kernel
+    int dbg;                            // profiling probes only (0 in normal use)
 };
 
 struct TcLaunch {
@@ -185,6 +186,8 @@ cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, 
 extern int g_sgd_blocks_per_sm;
 extern int g_pool_strip_rows;   // CAFFE_TUNE_POOL_STRIP_ROWS
 extern int g_wgrad_reduce_sg_min;   // CAFFE_TUNE_WGRAD_REDUCE_SG
+extern int g_halo_fast_epi;   // CAFFE_TUNE_HALO_FAST_EPI
+extern int g_dbg;
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,
                   float decay, float gscale, cudaStream_t s);
 

@@ -27,6 +27,8 @@
 namespace cb {
 
 constexpr int HALO_SMEM_ALIGN = 1024;
+int g_halo_fast_epi = 1;   // CAFFE_TUNE_HALO_FAST_EPI
+int g_dbg = 0;
 
 size_t tc_halo_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
@@ -36,7 +38,9 @@ size_t tc_halo_smem_bytes(const TcArgs& a) {
 
 // KS: 16-channel K steps issued per 64-channel block (4; 3 when the only block holds 48 real
 // channels -- conv1 after space-to-depth, conv2 per group -- so the zero padding is not multiplied)
-template <int CG, int MACC, int KS>
+// EPC > 0: the specialised channels-last BF16 epilogue (epi_store_bf16_rowseg), each of the two
+// epilogue groups writing EPC = BN/2 columns
+template <int CG, int MACC, int KS, int EPC>
 __global__ void __launch_bounds__(384, 1)
     tc_halo_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const TcArgs args) {
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(384, 1)
         const int eg = (warp - 4) >> 2;
         const int row = q * 32 + lane;
         const int yy = row / args.halo_wt, xx = row - yy * args.halo_wt;
-        const int half = ((args.BN / 2) + 15) & ~15;
+        const int half = EPC > 0 ? EPC : ((args.BN / 2) + 15) & ~15;
         const int cb_ = eg == 0 ? 0 : half, ce_ = eg == 0 ? half : args.BN;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -254,8 +258,14 @@ __global__ void __launch_bounds__(384, 1)
                 const int y = (tile - n * args.tiles_per_img) * args.halo_th + yy;
                 const bool row_ok = tile < args.total_tiles && yy < args.halo_th && y < args.out_h && xx < args.out_w;
                 const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + xx) * args.s_p;
-                if (cb_ < ce_)
+                if constexpr (EPC > 0) {
+                    if (args.dbg == 2) continue;
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + rbase + cbase + cb_;
+                    epi_store_bf16_rowseg<EPC>(taddr + a * args.acc_stride + cb_, row_ok && args.dbg != 1, dst,
+                                               smem_u32(bs + cb_), args.bias != nullptr, args.relu != 0);
+                } else if (cb_ < ce_) {
                     epi_store_strided(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs, cb_, ce_);
+                }
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
@@ -521,9 +531,9 @@ cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s) {
     }
 }
 
-template <int CG, int MACC, int KS>
+template <int CG, int MACC, int KS, int EPC = 0>
 static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
-    auto kern = tc_halo_kernel<CG, MACC, KS>;
+    auto kern = tc_halo_kernel<CG, MACC, KS, EPC>;
     const size_t smem = tc_halo_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -553,6 +563,25 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s) {
     if (L.esz != 2) return cudaErrorInvalidValue;
     const int macc = L.args.macc > 1 ? L.args.macc : 1;
     if (macc > 2) return cudaErrorInvalidValue;
+    // specialised epilogue: BF16 channels-last output, beta 0, no column tail, 16-byte row segments
+    TcLaunch& LL = const_cast<TcLaunch&>(L);
+    LL.args.dbg = g_dbg;
+    const TcArgs& a = L.args;
+    const int epc = g_halo_fast_epi && a.out_bf16 && a.s_c == 1 && a.beta == 0.f && a.N % a.BN == 0 &&
+                            (a.BN / 2) % 8 == 0 && a.s_n % 8 == 0 && a.s_p % 8 == 0 && a.col_g % 8 == 0 &&
+                            (reinterpret_cast<uintptr_t>(a.out) & 15) == 0
+                        ? a.BN / 2
+                        : 0;
+    if (L.cg == 2 && macc == 2 && epc > 0) {
+        if (a.k_last == 3 && a.a_cblocks == 1) {
+            if (epc == 48) return halo_launch_one<2, 2, 3, 48>(L, s);
+            if (epc == 64) return halo_launch_one<2, 2, 3, 64>(L, s);
+        } else {
+            if (epc == 24) return halo_launch_one<2, 2, 4, 24>(L, s);
+            if (epc == 48) return halo_launch_one<2, 2, 4, 48>(L, s);
+            if (epc == 64) return halo_launch_one<2, 2, 4, 64>(L, s);
+        }
+    }
     if (L.args.k_last == 3 && L.args.a_cblocks == 1) {
         if (L.cg == 2) return macc == 2 ? halo_launch_one<2, 2, 3>(L, s) : halo_launch_one<2, 1, 3>(L, s);
         return macc == 2 ? halo_launch_one<1, 2, 3>(L, s) : halo_launch_one<1, 1, 3>(L, s);

@@ -380,3 +380,57 @@ def test_conv_prepacked_bottom(oracle, case):
         dw0, db0 = cb.conv_backward_weight(xt, dyt, Wt.shape, s, p, g)
         np.testing.assert_array_equal(host(dw1), host(dw0))
         np.testing.assert_array_equal(host(db1), host(db0))
+
+
+@pytest.mark.parametrize("case", [(2, 3, 67, 67, 96, (11, 11), (4, 4), (0, 0), 1),      # conv1 geometry: 48 cols/group
+                                  (2, 96, 27, 27, 256, (5, 5), (1, 1), (2, 2), 2),      # conv2: fwd 64, dgrad 24
+                                  (3, 64, 20, 20, 96, (3, 3), (1, 1), (1, 1), 1)],      # fwd 48, dgrad 64 (K=96 -> 2 blocks)
+                         ids=["conv1geom", "conv2geom", "C64O96"])
+def test_halo_fast_epilogue_bit_identical(oracle, case):
+    """The specialised BF16 channels-last halo epilogue (CAFFE_TUNE_HALO_FAST_EPI, default on) writes
+    exactly the bits of the generic per-chunk epilogue (bias + ReLU forward, data gradient), CTA
+    pairs with two accumulators per unit, and matches the oracle."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 41)
+    if C == 3:
+        X = synth.int_pixels((N, C, H, W), 41)
+    cl = torch.channels_last
+    Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    outs = {}
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 2)
+    try:
+        for fast in (0, 1):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_FAST_EPI, fast)
+            y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True)
+            y0 = cb.conv_forward(Xd, cuda(Wt), None, stride=s, pad=p, group=g, relu=False)
+            r = {"y": host(y), "y_nobias": host(y0)}
+            if s[0] == 1:
+                dX = torch.empty((N, C, H, W), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl)
+                cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
+                r["dx"] = host(dX)
+            outs[fast] = r
+        # same tiles, FP32 output (generic epilogue): the BF16 outputs must be its RNE rounding (R12)
+        y32 = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True, out_dtype=torch.float32)
+        dX32 = torch.empty((N, C, H, W), device="cuda").contiguous(memory_format=cl)
+        if s[0] == 1:
+            cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX32)
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_FAST_EPI, 1)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
+    for kk in outs[0]:
+        np.testing.assert_array_equal(outs[0][kk], outs[1][kk], err_msg=kk)
+    # the BF16 outputs are the RNE rounding of the FP32-output pass (R12), which meets the oracle bar
+    q = oracle.quant_bf16
+    np.testing.assert_array_equal(outs[1]["y"], host(y32.to(torch.bfloat16)))
+    assert_tc_close(host(y32), oracle.conv_forward(host(Xd), q(Wt), b, stride=s, pad=p, group=g, relu=True),
+                    "fwd fp32")
+    if "dx" in outs[1]:
+        np.testing.assert_array_equal(outs[1]["dx"], host(dX32.to(torch.bfloat16)))
+        assert_tc_close(host(dX32), oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g),
+                        "dgrad fp32", tol=3e-3)
