@@ -163,6 +163,14 @@ caffe_status caffe_device_check(void);
    loads before one wait, shared-memory bias vectors, 16-byte stores); 0 = the generic epilogue.
    Bit-identical results. */
 #define CAFFE_TUNE_HALO_FAST_EPI 11
+/* CAFFE_TUNE_HALO_TMA_STORE: 1 = the specialised halo epilogue stages each tile in shared memory and
+   writes it with 4-D TMA tensor stores; 0 (default) = per-thread 16-byte global stores (measured:
+   equal for conv1, faster for conv2 whose B ring keeps more stages).  Bit-identical results. */
+#define CAFFE_TUNE_HALO_TMA_STORE 12
+/* CAFFE_TUNE_WGRAD_REDUCE_ROWS: 1 (default) = the split reduction of the halo weight gradients runs
+   one block per filter row (shared-memory gather, contiguous dW stores); 0 = one thread per weight.
+   Bit-identical results (same summation order). */
+#define CAFFE_TUNE_WGRAD_REDUCE_ROWS 13
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -33,6 +33,8 @@ CAFFE_TUNE_POOL_STRIP_ROWS = 8
 CAFFE_TUNE_WGRAD_REDUCE_SG = 9
 CAFFE_TUNE_HALO_KTRIM = 10
 CAFFE_TUNE_HALO_FAST_EPI = 11
+CAFFE_TUNE_HALO_TMA_STORE = 12
+CAFFE_TUNE_WGRAD_REDUCE_ROWS = 13
 
 
 class Shape4(ctypes.Structure):

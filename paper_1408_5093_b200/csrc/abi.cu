@@ -462,7 +462,29 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     a.macc = 1;
     if (2 * 2 * a.acc_stride <= 512 && a.a_stages * 2 * a.halo_slot <= 140 * 1024) a.macc = 2;
     a.b_stage_bytes = a.BN / L.cg * 128;
-    const long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
+    long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
+    // TMA tensor-store epilogue (specialised-epilogue launches): the unit's tiles are staged in
+    // shared memory as boxes of cw channels x Wo pixels x halo_th rows and leave through mapC
+    a.tma_store = 0;
+    const int epc = halo_fast_epc(a, L.cg);
+    if (epc > 0 && cb::g_halo_tma_store) {
+        const int cwl = epc % 64 == 0 ? 6 : epc % 32 == 0 ? 5 : epc % 16 == 0 ? 4 : 0;
+        const int cw = cwl ? 1 << cwl : epc;
+        const int align = cwl ? 16 * cw : 128;   // the swizzle pattern repeats every 8 rows
+        if (cwl > 0 || (epc / 8) % 2 == 1) {
+            const int chunk = (int)rup((long long)a.halo_th * h.Wo * cw * 2, align);
+            const int tile = (int)rup((long long)(a.BN / cw) * chunk, 1024);
+            if ((long long)a.macc * tile <= 64 * 1024 &&
+                encode_store_4d(&L.mapC, 2, a.out, (int)a.s_p, h.Wo, h.Ho, N, a.s_p, a.s_n, (uint32_t)cw,
+                                (uint32_t)h.Wo, (uint32_t)a.halo_th, cwl ? cw * 2 : 0)) {
+                a.tma_store = 1;
+                a.st_cw = cwl;
+                a.st_chunk_bytes = chunk;
+                a.st_tile_bytes = tile;
+                budget -= (long long)a.macc * tile + 1024;
+            }
+        }
+    }
     // weights resident in shared memory when the whole filter (this CTA's half) fits: staged once
     // per kernel instead of once per unit (the first layer: 9 taps x 6 KB)
     const long long nb = (long long)h.kh * h.kw * a.a_cblocks;
@@ -576,6 +598,14 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     }
     if (key == 99) {   // profiling probes (not part of the documented interface)
         cb::g_dbg = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_WGRAD_REDUCE_ROWS) {
+        cb::g_wgrad_reduce_rows = value ? 1 : 0;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_HALO_TMA_STORE) {
+        cb::g_halo_tma_store = value ? 1 : 0;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO_FAST_EPI) {

@@ -45,6 +45,59 @@ __device__ __forceinline__ void epi_store_bf16_rowseg(uint32_t taddr, bool row_o
     for (int q = 0; q < EPC / 8; q++) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
 }
 
+// Same arithmetic as epi_store_bf16_rowseg, but the row's EPC columns (tile columns
+// [col_begin, col_begin + EPC)) go to the shared-memory TMA staging of the tile: chunk q of cw
+// channels holds box row r (= pixel) at q*chunk_bytes + r*cw*2, 16-byte piece k stored at
+// k ^ swizzle(r) (the TMA SWIZZLE_{128,64,32}B pattern for cw = 64/32/16; none otherwise).
+// cw_log2 = 0: one chunk per epilogue group (cw == EPC, unswizzled: an odd number of 16-byte
+// pieces per row keeps the 32 lanes' stores conflict-free).
+template <int EPC>
+__device__ __forceinline__ void epi_stage_bf16_row(uint32_t taddr, bool row_ok, uint32_t stg, int r, int col_begin,
+                                                   int cw_log2, int chunk_bytes, uint32_t sbias_addr, bool bias,
+                                                   bool relu) {
+    uint32_t v[EPC];
+#pragma unroll
+    for (int c = 0; c < EPC; c += 16) {
+        if (c + 16 <= EPC) tmem_ld16p(taddr + c, v + c);
+        else tmem_ld8p(taddr + c, v + c);
+    }
+    tmem_wait_ld();
+    if (!row_ok) return;
+    uint32_t pk[EPC / 2];
+#pragma unroll
+    for (int c = 0; c < EPC; c += 4) {
+        float x0 = __uint_as_float(v[c]), x1 = __uint_as_float(v[c + 1]);
+        float x2 = __uint_as_float(v[c + 2]), x3 = __uint_as_float(v[c + 3]);
+        if (bias) {
+            const float4 b = lds_f4(sbias_addr + 4u * c);
+            x0 += b.x; x1 += b.y; x2 += b.z; x3 += b.w;
+        }
+        if (relu) {
+            x0 = x0 > 0.f ? x0 : 0.f; x1 = x1 > 0.f ? x1 : 0.f;
+            x2 = x2 > 0.f ? x2 : 0.f; x3 = x3 > 0.f ? x3 : 0.f;
+        }
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(x0, x1), h1 = __floats2bfloat162_rn(x2, x3);
+        pk[c / 2] = *reinterpret_cast<uint32_t*>(&h0);
+        pk[c / 2 + 1] = *reinterpret_cast<uint32_t*>(&h1);
+    }
+    if (cw_log2 == 0) {
+        const uint32_t row = stg + (uint32_t)(col_begin / EPC) * chunk_bytes + (uint32_t)r * (EPC * 2);
+#pragma unroll
+        for (int q = 0; q < EPC / 8; q++) sts_u4(row + 16u * q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    } else {
+        const int cw = 1 << cw_log2;
+        const int sw = cw_log2 == 6 ? (r & 7) : cw_log2 == 5 ? ((r >> 1) & 3) : cw_log2 == 4 ? ((r >> 2) & 1) : 0;
+        const uint32_t rowoff = (uint32_t)r * (uint32_t)(cw * 2);
+#pragma unroll
+        for (int q = 0; q < EPC / 8; q++) {
+            const int c = col_begin + 8 * q;
+            const int chunk = c >> cw_log2, k = (c & (cw - 1)) >> 3;
+            sts_u4(stg + (uint32_t)chunk * chunk_bytes + rowoff + ((uint32_t)(k ^ sw) << 4), pk[4 * q], pk[4 * q + 1],
+                   pk[4 * q + 2], pk[4 * q + 3]);
+        }
+    }
+}
+
 // taddr: TMEM address of this warp's lanes, column 0 of the accumulator.  rbase: element offset of
 // the output row; col0: first tile column (for the N bound); cbase: output channel of tile column 0;
 // bs: this tile's bias staged in shared memory (or unused when args.bias == nullptr).

@@ -63,6 +63,10 @@ struct TcArgs {
     int k_last;                         // A_HALO_K: 16-channel K steps needed by the last channel block
                                         // (0 = all 4); 3 with a single block selects the KS = 3 kernel
     int dbg;                            // profiling probes only (0 in normal use)
+    // A_HALO_K + tma_store: the tile is staged in shared memory as TMA boxes of st_cw channels x
+    // out_w pixels x halo_th rows (swizzled by the box row width: 128/64/32 B, or none when the
+    // row is an odd number of 16-byte pieces) and written by 4-D tensor stores through mapC
+    int st_cw, st_chunk_bytes, st_tile_bytes;
 };
 
 struct TcLaunch {
@@ -82,6 +86,8 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s);
 cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s);
 size_t tc_halo_wgrad_smem_bytes(const TcArgs& a);
 size_t tc_halo_smem_bytes(const TcArgs& a);
+int halo_fast_epc(const TcArgs& a, int cg);
+extern int g_halo_tma_store;   // CAFFE_TUNE_HALO_TMA_STORE
 int num_sms();
 
 // TMA descriptor encoders (driver entry points resolved at runtime; no -lcuda needed).
@@ -92,6 +98,10 @@ bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, 
 bool encode_store_2d(CUtensorMap* m, int esz, const void* base, uint64_t cols, uint64_t rows, uint64_t ld);
 bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, uint32_t box_c,
                      uint32_t box_w, uint32_t box_h);
+// channels-last output [N][H][W][C] (pixel stride s_p, image stride s_n elements) for TMA stores:
+// box (box_c channels, box_w, box_h, 1); swizzle 0 / 32 / 64 / 128 bytes
+bool encode_store_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, long long s_p,
+                     long long s_n, uint32_t box_c, uint32_t box_w, uint32_t box_h, int swizzle_bytes);
 bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
                       int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels);
 
@@ -186,6 +196,7 @@ cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, 
 extern int g_sgd_blocks_per_sm;
 extern int g_pool_strip_rows;   // CAFFE_TUNE_POOL_STRIP_ROWS
 extern int g_wgrad_reduce_sg_min;   // CAFFE_TUNE_WGRAD_REDUCE_SG
+extern int g_wgrad_reduce_rows;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS
 extern int g_halo_fast_epi;   // CAFFE_TUNE_HALO_FAST_EPI
 extern int g_dbg;
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,

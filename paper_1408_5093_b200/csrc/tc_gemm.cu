@@ -468,6 +468,23 @@ bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, in
     return r == CUDA_SUCCESS;
 }
 
+bool encode_store_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, long long s_p,
+                     long long s_n, uint32_t box_c, uint32_t box_w, uint32_t box_h, int swizzle_bytes) {
+    if (!resolve()) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)(s_p * esz), (cuuint64_t)(s_p * W * esz), (cuuint64_t)(s_n * esz)};
+    cuuint32_t box[4] = {box_c, box_w, box_h, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                        : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                         const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
                       int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels) {
     if (!resolve()) return false;

@@ -29,11 +29,13 @@ namespace cb {
 constexpr int HALO_SMEM_ALIGN = 1024;
 int g_halo_fast_epi = 1;   // CAFFE_TUNE_HALO_FAST_EPI
 int g_dbg = 0;
+int g_halo_tma_store = 0;   // CAFFE_TUNE_HALO_TMA_STORE (off: measured no gain for conv1, conv2 fwd 92 -> 106 us)
 
 size_t tc_halo_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
     return (size_t)a.a_stages * macc * a.halo_slot + (size_t)a.stages * a.b_stage_bytes + 512 /*barriers*/ +
-           2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN + (a.rows_epi ? 4 * 32 * 17 * 16 : 0);
+           2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN + (a.rows_epi ? 4 * 32 * 17 * 16 : 0) +
+           (a.tma_store ? (size_t)macc * a.st_tile_bytes + 1024 : 0);
 }
 
 // KS: 16-channel K steps issued per 64-channel block (4; 3 when the only block holds 48 real
@@ -43,7 +45,7 @@ size_t tc_halo_smem_bytes(const TcArgs& a) {
 template <int CG, int MACC, int KS, int EPC>
 __global__ void __launch_bounds__(384, 1)
     tc_halo_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                   const TcArgs args) {
+                   const __grid_constant__ CUtensorMap mapC, const TcArgs args) {
     constexpr int CH = 64;                 // bf16 channels per 128-byte row
     constexpr int KSTEPS = KS;             // K = 16 per tcgen05.mma
     constexpr int TM = 128 * CG;
@@ -236,11 +238,19 @@ __global__ void __launch_bounds__(384, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        // TMA-store staging (EPC > 0 && args.tma_store): one tile image per accumulator of the unit
+        const bool tstore = EPC > 0 && args.tma_store != 0;
+        const uint32_t stg = (smem_u32(sbias + 2 * 256) + 1023u) & ~1023u;
+        const bool issuer = warp == 4 && lane == 0;
         for (int u = cid; u < units; u += ncl) {
             int t = u;
             const int n_tile = t % args.n_tiles; t /= args.n_tiles;
             const int tg = t % tgroups;
             const int g = t / tgroups;
+            if (tstore) {   // the previous unit's tensor stores must have finished reading the staging
+                if (issuer) tma_store_wait_read0();
+                asm volatile("bar.sync 3, 256;" ::: "memory");
+            }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * macc * args.acc_stride;
@@ -260,6 +270,13 @@ __global__ void __launch_bounds__(384, 1)
                 const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + xx) * args.s_p;
                 if constexpr (EPC > 0) {
                     if (args.dbg == 2) continue;
+                    if (tstore) {
+                        epi_stage_bf16_row<EPC>(taddr + a * args.acc_stride + cb_, row_ok && args.dbg != 1,
+                                                stg + (uint32_t)(a * args.st_tile_bytes), yy * args.out_w + xx, cb_,
+                                                args.st_cw, args.st_chunk_bytes, smem_u32(bs + cb_),
+                                                args.bias != nullptr, args.relu != 0);
+                        continue;
+                    }
                     __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + rbase + cbase + cb_;
                     epi_store_bf16_rowseg<EPC>(taddr + a * args.acc_stride + cb_, row_ok && args.dbg != 1, dst,
                                                smem_u32(bs + cb_), args.bias != nullptr, args.relu != 0);
@@ -271,7 +288,26 @@ __global__ void __launch_bounds__(384, 1)
             if (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
             else mbar_arrive(&tempty[acc]);
             if (++acc == nslots) { acc = 0; acc_phase ^= 1; }
+            if (tstore) {   // staged tiles -> global: one 4-D tensor store per channel chunk
+                fence_proxy_async_smem();
+                asm volatile("bar.sync 3, 256;" ::: "memory");
+                if (issuer) {
+                    const int cw = args.st_cw > 0 ? (1 << args.st_cw) : EPC;
+                    const int nch = args.BN / cw;
+                    for (int a = 0; a < macc; a++) {
+                        const int tile = tg * tiles_per_unit + a * CG + (int)rank;
+                        if (tile >= args.total_tiles) continue;
+                        const int n = tile / args.tiles_per_img;
+                        const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;
+                        for (int ch = 0; ch < nch; ch++)
+                            tma_store_4d(&mapC, stg + (uint32_t)(a * args.st_tile_bytes + ch * args.st_chunk_bytes),
+                                         cbase + ch * cw, 0, y0, n);
+                    }
+                    tma_store_commit();
+                }
+            }
         }
+        if (tstore && issuer) tma_store_wait_all();
     }
     tc_fence_before();
     if (CG == 2) cluster_sync_all();
@@ -531,6 +567,20 @@ cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s) {
     }
 }
 
+// Columns per epilogue group of the specialised epilogue, or 0 for the generic one: BF16
+// channels-last output, beta 0, no column tail, 16-byte row segments, CTA pairs with two
+// accumulators per unit, and a compiled instance for BN/2.
+int halo_fast_epc(const TcArgs& a, int cg) {
+    const int macc = a.macc > 1 ? a.macc : 1;
+    if (!g_halo_fast_epi || cg != 2 || macc != 2) return 0;
+    if (!(a.out_bf16 && a.s_c == 1 && a.beta == 0.f && a.N % a.BN == 0 && (a.BN / 2) % 8 == 0 && a.s_n % 8 == 0 &&
+          a.s_p % 8 == 0 && a.col_g % 8 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0))
+        return 0;
+    const int epc = a.BN / 2;
+    if (a.k_last == 3 && a.a_cblocks == 1) return (epc == 48 || epc == 64) ? epc : 0;
+    return (epc == 24 || epc == 48 || epc == 64) ? epc : 0;
+}
+
 template <int CG, int MACC, int KS, int EPC = 0>
 static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
     auto kern = tc_halo_kernel<CG, MACC, KS, EPC>;
@@ -538,7 +588,7 @@ static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (CG == 1) {
-        kern<<<L.grid, 384, smem, s>>>(L.mapA, L.mapB, L.args);
+        kern<<<L.grid, 384, smem, s>>>(L.mapA, L.mapB, L.mapC, L.args);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(L.grid);
@@ -552,7 +602,7 @@ static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.args);
+        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.mapC, L.args);
         if (e != cudaSuccess) return e;
     }
     note_launch();
@@ -563,16 +613,11 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s) {
     if (L.esz != 2) return cudaErrorInvalidValue;
     const int macc = L.args.macc > 1 ? L.args.macc : 1;
     if (macc > 2) return cudaErrorInvalidValue;
-    // specialised epilogue: BF16 channels-last output, beta 0, no column tail, 16-byte row segments
     TcLaunch& LL = const_cast<TcLaunch&>(L);
     LL.args.dbg = g_dbg;
     const TcArgs& a = L.args;
-    const int epc = g_halo_fast_epi && a.out_bf16 && a.s_c == 1 && a.beta == 0.f && a.N % a.BN == 0 &&
-                            (a.BN / 2) % 8 == 0 && a.s_n % 8 == 0 && a.s_p % 8 == 0 && a.col_g % 8 == 0 &&
-                            (reinterpret_cast<uintptr_t>(a.out) & 15) == 0
-                        ? a.BN / 2
-                        : 0;
-    if (L.cg == 2 && macc == 2 && epc > 0) {
+    const int epc = halo_fast_epc(a, L.cg);
+    if (epc > 0) {
         if (a.k_last == 3 && a.a_cblocks == 1) {
             if (epc == 48) return halo_launch_one<2, 2, 3, 48>(L, s);
             if (epc == 64) return halo_launch_one<2, 2, 3, 64>(L, s);

@@ -200,11 +200,31 @@ class Net:
         L, P = self.layers[i], self.layers[i + 1]
         return L.kind in ("conv", "ip") and L.relu and P.kind == "pool" and P.method == "max"
 
-    def backward(self, hook=None, done_hook=None):
+    def _wgrad_workspace(self):
+        """Dedicated workspace of the side-stream weight-gradient passes (largest conv layer i > 0)."""
+        if getattr(self, "_ws_wgrad", None) is None:
+            n = 0
+            for i, L in enumerate(self.layers):
+                if L.kind == "conv" and i > 0:
+                    d = cb._conv_desc((L.kernel, L.kernel), L.stride, L.pad, L.group, self.math)
+                    v = cb.ctypes.c_size_t()
+                    cb.call("caffe_conv_workspace_size", cb.ctypes.byref(d), _abi.Shape4(*cb._shape4(self.shapes[i])),
+                            _abi.Shape4(*cb._shape4(tuple(self.W[i].shape))), int(_abi.CAFFE_PASS_BACKWARD_WEIGHT),
+                            cb.ctypes.byref(v))
+                    n = max(n, v.value)
+            self._ws_wgrad = self.torch.empty(n + 2048, dtype=self.torch.uint8, device=self.device)
+        return self._ws_wgrad
+
+    def backward(self, hook=None, done_hook=None, wgrad_stream=None):
         """Backward in reverse; `hook(i)` is called after layer i's parameter gradients are enqueued
         (data-parallel bucketing point), `done_hook(i)` once nothing later in the step reads layer
-        i's parameters (after its data gradient; after its weight gradient for the first layer)."""
+        i's parameters (after its data gradient; after its weight gradient for the first layer).
+        wgrad_stream: the weight gradients of conv layers i > 0 run there, concurrently with the
+        data gradient and the rest of the backward on the current stream (they share only reads);
+        self.wgrad_done[i] is the event recorded after layer i's weight gradient."""
         a, d, n = self.a, self.d, len(self.layers)
+        torch = self.torch
+        self.wgrad_done = {}
         for i in range(n - 2, -1, -1):
             L = self.layers[i]
             dy = d[i + 1] if i + 1 < n - 1 else self.dscores
@@ -213,8 +233,18 @@ class Net:
                 cb.relu_backward(y, dy, inplace=True)  # sign of the ReLU output == sign test on its input
             if L.kind == "conv":
                 pre = i == 0 and self.ws0 is not None
-                cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math, beta=0.0,
-                                        dw=self.dW[i], db=self.dB[i], ws=self.ws0 if pre else None, prepacked=pre)
+                if wgrad_stream is not None and i > 0:
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream())
+                    wgrad_stream.wait_event(ev)
+                    with torch.cuda.stream(wgrad_stream):
+                        cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math,
+                                                beta=0.0, dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
+                        self.wgrad_done[i] = torch.cuda.Event()
+                        self.wgrad_done[i].record(wgrad_stream)
+                else:
+                    cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math, beta=0.0,
+                                            dw=self.dW[i], db=self.dB[i], ws=self.ws0 if pre else None, prepacked=pre)
                 if hook:
                     hook(i)
                 if i > 0:
@@ -250,6 +280,8 @@ class Net:
     # instead of the L2-bound conv3-5 passes.  Measured (graph replay, one B200): 1.758 ms/step
     # with immediate updates, 1.675 held to conv3, 1.842 held to conv2.
     sgd_flush_layer = None
+    # conv weight gradients (layers > 0) on their own stream, concurrent with the data gradients
+    wgrad_side = False
 
     def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4, overlap_update=True):
         self.forward()
@@ -270,14 +302,23 @@ class Net:
                 pl = [i for i, L in enumerate(self.layers) if L.kind in ("conv", "ip")]
                 flush_at = pl[min(2, len(pl) - 1)]
 
+            wstream = None
+            if self.wgrad_side:
+                if getattr(self, "_wside", None) is None:
+                    self._wside = torch.cuda.Stream()
+                wstream = self._wside
+
             def launch():
                 # pending layers hold one contiguous range of the flat parameter buffer (backward order)
                 lo = min(seg[i][0] for i in pending)
                 hi = max(seg[i][0] + seg[i][1] for i in pending)
+                wev = [self.wgrad_done[i] for i in pending if i in getattr(self, "wgrad_done", {})]
                 pending.clear()
                 ev = torch.cuda.Event()
                 ev.record(main)
                 self._side.wait_event(ev)
+                for e in wev:
+                    self._side.wait_event(e)
                 # one 256-thread block per SM: leaves registers / thread slots for the main stream
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_BLOCKS_PER_SM, self.side_sgd_blocks)
                 with torch.cuda.stream(self._side):
@@ -290,10 +331,12 @@ class Net:
                 if i <= flush_at:
                     launch()
 
-            self.backward(done_hook=done)
+            self.backward(done_hook=done, wgrad_stream=wstream)
             if pending:
                 launch()
             main.wait_stream(self._side)
+            if wstream is not None:
+                main.wait_stream(wstream)
             return
         self.backward(hook=allreduce.on_grad if allreduce else None)
         scale = 1.0

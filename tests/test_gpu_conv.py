@@ -387,8 +387,10 @@ def test_conv_prepacked_bottom(oracle, case):
                                   (3, 64, 20, 20, 96, (3, 3), (1, 1), (1, 1), 1)],      # fwd 48, dgrad 64 (K=96 -> 2 blocks)
                          ids=["conv1geom", "conv2geom", "C64O96"])
 def test_halo_fast_epilogue_bit_identical(oracle, case):
-    """The specialised BF16 channels-last halo epilogue (CAFFE_TUNE_HALO_FAST_EPI, default on) writes
-    exactly the bits of the generic per-chunk epilogue (bias + ReLU forward, data gradient), CTA
+    """The specialised BF16 channels-last halo epilogue (CAFFE_TUNE_HALO_FAST_EPI, default on), with
+    direct 16-byte stores or shared-memory staging + 4-D TMA tensor stores (CAFFE_TUNE_HALO_TMA_STORE,
+    default off; swizzled 32/128-byte and unswizzled 48-byte box rows), writes exactly the bits of
+    the generic per-chunk epilogue (bias + ReLU forward, data gradient), CTA
     pairs with two accumulators per unit, and matches the oracle."""
     import torch
     import paper_1408_5093_b200 as cb
@@ -404,8 +406,9 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
     _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
     _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 2)
     try:
-        for fast in (0, 1):
-            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_FAST_EPI, fast)
+        for fast in (0, 1, 2):   # generic; specialised with direct stores; specialised with TMA stores
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_FAST_EPI, 1 if fast else 0)
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_TMA_STORE, 1 if fast == 2 else 0)
             y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True)
             y0 = cb.conv_forward(Xd, cuda(Wt), None, stride=s, pad=p, group=g, relu=False)
             r = {"y": host(y), "y_nobias": host(y0)}
@@ -421,10 +424,12 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
             cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX32)
     finally:
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_FAST_EPI, 1)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_TMA_STORE, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
     for kk in outs[0]:
         np.testing.assert_array_equal(outs[0][kk], outs[1][kk], err_msg=kk)
+        np.testing.assert_array_equal(outs[0][kk], outs[2][kk], err_msg=kk)
     # the BF16 outputs are the RNE rounding of the FP32-output pass (R12), which meets the oracle bar
     q = oracle.quant_bf16
     np.testing.assert_array_equal(outs[1]["y"], host(y32.to(torch.bfloat16)))
@@ -434,3 +439,47 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
         np.testing.assert_array_equal(outs[1]["dx"], host(dX32.to(torch.bfloat16)))
         assert_tc_close(host(dX32), oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g),
                         "dgrad fp32", tol=3e-3)
+
+
+@pytest.mark.parametrize("case", [(2, 3, 67, 67, 96, (11, 11), (4, 4), (0, 0), 1),
+                                  (2, 96, 27, 27, 256, (5, 5), (1, 1), (2, 2), 2),
+                                  CASES[7], (3, 64, 20, 20, 96, (3, 3), (1, 1), (1, 1), 1)],
+                         ids=["conv1geom", "conv2geom", IDS[7], "C64O96"])
+@pytest.mark.parametrize("sg", [0, 2])
+def test_wgrad_reduce_rows_bit_identical(oracle, case, sg):
+    """The per-filter-row split reduction of the halo weight gradient (CAFFE_TUNE_WGRAD_REDUCE_ROWS,
+    default on) gives the bits of the one-thread-per-weight reduction, in the plain ascending-split
+    form and the split-range form (CAFFE_TUNE_WGRAD_REDUCE_SG lowered to 2), with beta = 0 and 1
+    and the bias gradient from the ones chunk; and matches the oracle."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 51)
+    if C == 3:
+        X = synth.int_pixels((N, C, H, W), 51)
+    cl = torch.channels_last
+    Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    prevW = cuda(synth.uniform(Wt.shape, 52, synth.S_AUX))
+    prevb = cuda(synth.uniform((O,), 53, synth.S_AUX))
+    outs = {}
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
+    if sg:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_REDUCE_SG, sg)
+    try:
+        for rows in (0, 1):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_REDUCE_ROWS, rows)
+            dW, db = cb.conv_backward_weight(Xd, dYd, Wt.shape, stride=s, pad=p, group=g, math="bf16")
+            dW1, db1 = cb.conv_backward_weight(Xd, dYd, Wt.shape, stride=s, pad=p, group=g, math="bf16", beta=1.0,
+                                               dw=prevW.clone(), db=prevb.clone())
+            outs[rows] = [host(t) for t in (dW, db, dW1, db1)]
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_REDUCE_ROWS, 1)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_REDUCE_SG, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
+    for a, b_ in zip(outs[0], outs[1]):
+        np.testing.assert_array_equal(a, b_)
+    rW, rb = oracle.conv_backward_weight(host(Xd), host(dYd), Wt.shape, stride=s, pad=p, group=g)
+    assert_tc_close(outs[1][0], rW, "wgrad rows")
+    assert_fp32_close(outs[1][1], rb, "bias grad rows")

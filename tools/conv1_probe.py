@@ -26,15 +26,20 @@ def main():
     w2 = (torch.randn(256, 48, 5, 5, device=dev) * 0.01).to(torch.bfloat16)
     b2 = torch.zeros(256, device=dev)
     y2 = torch.empty((B, 256, 27, 27), device=dev, dtype=torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    # conv2 data gradient (N = 48 per group)
+    dy2 = torch.randn(B, 256, 27, 27, device=dev).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    dx2 = torch.empty((B, 96, 27, 27), device=dev, dtype=torch.bfloat16).contiguous(memory_format=torch.channels_last)
     for cfg in sys.argv[1:] or ["11=1", "11=0", "99=1", "99=2"]:
         kv = [tuple(map(int, s.split("="))) for s in cfg.split(",")]
         for k, v in kv:
             _abi.call("caffe_set_tuning", k, v)
         t1 = timeit(lambda: cb.conv_forward(x, w, b, 4, 0, 1, "bf16", relu=True, out=y, ws=ws, prepacked=True))
         t2 = timeit(lambda: cb.conv_forward(x2, w2, b2, 1, 2, 2, "bf16", relu=True, out=y2))
-        print(f"{cfg:20s} conv1 fwd {t1 * 1e3:7.1f} us   conv2 fwd {t2 * 1e3:7.1f} us", flush=True)
+        t3 = timeit(lambda: cb.conv_backward_data(dy2, w2, x2.shape, 1, 2, 2, "bf16", out=dx2))
+        print(f"{cfg:20s} conv1 fwd {t1 * 1e3:7.1f} us   conv2 fwd {t2 * 1e3:7.1f} us   conv2 dgrad {t3 * 1e3:7.1f} us",
+              flush=True)
         for k, v in kv:
-            _abi.call("caffe_set_tuning", k, 1 if k in (5, 10, 11) else 0)
+            _abi.call("caffe_set_tuning", k, 1 if k in (5, 10, 11, 12) else 0)
 
 
 if __name__ == "__main__":

@@ -4,7 +4,7 @@ options (run on the B200 box).
     python tools/sched_probe.py "flush=1073741824" "flush=6" "flush=6,blocks=2" "tune11=0"
 
 Each argument is one configuration: comma-separated key=value with keys flush (Net.sgd_flush_layer),
-blocks (Net.side_sgd_blocks) and tuneK (caffe_set_tuning(K, value)).  Configurations are timed
+blocks (Net.side_sgd_blocks), wside (Net.wgrad_side) and tuneK (caffe_set_tuning(K, value)).  Configurations are timed
 round-robin (3 rounds x 20 replays) and the median ms/step of each is printed.
 """
 import os
@@ -42,15 +42,17 @@ def main():
                 _abi.call("caffe_set_tuning", int(k[4:]), v)
         net.sgd_flush_layer = p.get("flush", None)
         net.side_sgd_blocks = p.get("blocks", 1)
+        net.wgrad_side = bool(p.get("wside", 0))
         for _ in range(2):
             net.step()
         torch.cuda.synchronize()
         graphs.append(net.capture())
         for k, v in p.items():   # restore library defaults (tuning is process-wide)
             if k.startswith("tune"):
-                _abi.call("caffe_set_tuning", int(k[4:]), 1 if int(k[4:]) in (5, 10, 11) else 0)
+                _abi.call("caffe_set_tuning", int(k[4:]), 1 if int(k[4:]) in (5, 10, 11, 13) else 0)
     res = {c: [] for c in cfgs}
-    for _ in range(3):
+    rounds = int(os.environ.get("ROUNDS", "3"))
+    for _ in range(rounds):
         for c, g in zip(cfgs, graphs):
             for _ in range(3):
                 g.replay()
@@ -63,7 +65,8 @@ def main():
             torch.cuda.synchronize()
             res[c].append(a.elapsed_time(b) / 20)
     for c in cfgs:
-        print(f"{c:40s} {statistics.median(res[c]):.4f} ms/step  {['%.4f' % x for x in res[c]]}")
+        print(f"{c:40s} median {statistics.median(res[c]):.4f}  min {min(res[c]):.4f} ms/step  "
+              f"{['%.4f' % x for x in res[c]]}")
 
 
 if __name__ == "__main__":
