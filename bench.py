@@ -288,7 +288,12 @@ def main():
     value = world * B * args.steps / (ms / 1000.0)
     # ---------------- instrumented eager pass: the same kernels with a CUDA-event pair around every
     # tcgen05 GEMM launch (library profiler, on the launching stream) -> roofline of the dominant kernel
+    # (weight gradients serialised with the data gradients here, so each event pair times one kernel
+    # alone rather than two time-sharing the SMs)
+    wside = net.wgrad_side
+    net.wgrad_side = False
     ms_eager, nl_eager = timed(args.steps, instrument=True)
+    net.wgrad_side = wside
     launches = nl_eager  # graph replays launch exactly the eager kernel sequence
     import ctypes
     g_ms, g_fl, g_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()

@@ -167,9 +167,10 @@ caffe_status caffe_device_check(void);
    writes it with 4-D TMA tensor stores; 0 (default) = per-thread 16-byte global stores (measured:
    equal for conv1, faster for conv2 whose B ring keeps more stages).  Bit-identical results. */
 #define CAFFE_TUNE_HALO_TMA_STORE 12
-/* CAFFE_TUNE_WGRAD_REDUCE_ROWS: 1 (default) = the split reduction of the halo weight gradients runs
-   one block per filter row (shared-memory gather, contiguous dW stores); 0 = one thread per weight.
-   Bit-identical results (same summation order). */
+/* CAFFE_TUNE_WGRAD_REDUCE_ROWS: 1 (default) = the split reduction of the halo weight gradients of
+   plain filters (fewer splits than CAFFE_TUNE_WGRAD_REDUCE_SG) runs one block per (filter row,
+   64-channel block) with a shared-memory gather and contiguous dW stores; 0 = one thread per
+   weight.  Bit-identical results (same summation order). */
 #define CAFFE_TUNE_WGRAD_REDUCE_ROWS 13
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
@@ -226,6 +227,20 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
 caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_blob* top_diff,
                                       const caffe_blob* weight, caffe_blob* bottom_diff, float beta,
                                       void* workspace, size_t workspace_bytes, caffe_stream_t stream);
+
+/* Data gradient through the ReLU that produced this layer's bottom (S:151-159 with the ReLU
+   backward of S:205-213 folded in; the net's in-place ReLU keeps only its output, whose sign is
+   the sign of its input):
+     bottom_diff = [relu_top > 0] * conv^T(top_diff)        (overwritten; beta is 0)
+   relu_top: the ReLU output (= this layer's bottom), F32|BF16, same shape and layout as
+   bottom_diff, must not overlap it.  Same workspace as caffe_conv_backward_data.  The mask is
+   applied in the tensor-core epilogue where it can (channels-last BF16 im2col / halo tiles),
+   else by an in-place ReLU-backward pass after the convolution.  Errors: as
+   caffe_conv_backward_data, plus E_SHAPE (relu_top shape), E_INVALID (layouts differ), E_ALIAS. */
+caffe_status caffe_conv_backward_data_relu(const caffe_conv_desc* desc, const caffe_blob* top_diff,
+                                           const caffe_blob* weight, const caffe_blob* relu_top,
+                                           caffe_blob* bottom_diff, void* workspace, size_t workspace_bytes,
+                                           caffe_stream_t stream);
 
 /* Weight/bias gradient (accumulate S:154 via beta, R4):
      weight_diff[o,c',i,j] = beta*weight_diff + sum_{n,y,x} top_diff[n,o,y,x]*bottom[n,g(o)C/g+c',y*sh-ph+i,x*sw-pw+j]

@@ -106,6 +106,7 @@ def _stream():
 
 # ------------------------------------------------------------------ workspace (caller-owned device memory)
 _ws = {}
+_ws_retired = []
 
 
 def workspace(nbytes: int, device=None):
@@ -116,6 +117,9 @@ def workspace(nbytes: int, device=None):
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     buf = _ws.get(dev)
     if buf is None or buf.numel() < nbytes + 1024:
+        if buf is not None:
+            # a CUDA graph captured earlier may still replay kernels on the old buffer: keep it alive
+            _ws_retired.append(buf)
         buf = torch.empty(int(nbytes * 1.1) + 2048, dtype=torch.uint8, device=dev)
         _ws[dev] = buf
     p = buf.data_ptr()
@@ -206,6 +210,20 @@ def conv_backward_data(dy, w, in_shape, stride=1, pad=0, group=1, math="bf16", b
     bdy, bw, bdx = blob(dy), blob(w), blob(out)
     call("caffe_conv_backward_data", ctypes.byref(d), ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(bdx),
          float(beta), ws, wsz, _stream())
+    return out
+
+
+def conv_backward_data_relu(dy, w, relu_top, stride=1, pad=0, group=1, math="bf16", out=None):
+    """dX = [relu_top > 0] * (W^T (*) dY): the data gradient through the ReLU whose output is this
+    layer's bottom (S:154 with S:208 folded in)."""
+    kh, kw = w.shape[2], w.shape[3]
+    d = _conv_desc((kh, kw), stride, pad, group, math)
+    if out is None:
+        out = empty_like_layout(tuple(relu_top.shape), relu_top.dtype, dy.device, like=relu_top)
+    ws, wsz = _conv_ws(d, tuple(relu_top.shape), w.shape, _abi.CAFFE_PASS_BACKWARD_DATA)
+    bdy, bw, br, bdx = blob(dy), blob(w), blob(relu_top), blob(out)
+    call("caffe_conv_backward_data_relu", ctypes.byref(d), ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(br),
+         ctypes.byref(bdx), ws, wsz, _stream())
     return out
 
 

@@ -80,6 +80,7 @@ SIGNATURES = {
     "caffe_conv_forward": [CD, B, B, B, B, vp, sz, vp],
     "caffe_conv_pack_bottom": [CD, B, B, vp, sz, vp],
     "caffe_conv_backward_data": [CD, B, B, B, f32, vp, sz, vp],
+    "caffe_conv_backward_data_relu": [CD, B, B, B, B, vp, sz, vp],
     "caffe_conv_backward_weight": [CD, B, B, B, B, f32, vp, sz, vp],
     "caffe_relu_forward": [B, B, vp],
     "caffe_relu_backward": [B, B, B, vp],

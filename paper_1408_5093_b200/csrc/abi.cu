@@ -249,7 +249,7 @@ void enable_tma_store(TcLaunch& L, void* out, int esz, long long cols, long long
 int g_rows_epi = 0;   // CAFFE_TUNE_ROWS_EPILOGUE (off: adds epilogue instructions where the epilogue is the
                       // bottleneck -- conv1 forward 106 -> 149 us; no gain elsewhere)
 void enable_rows_epilogue(TcArgs& a) {
-    const bool ok = g_rows_epi && !a.tma_store && a.s_c == 1 && a.beta == 0.f && a.out_bf16 && a.BN <= 128 &&
+    const bool ok = g_rows_epi && !a.tma_store && !a.relu_top && a.s_c == 1 && a.beta == 0.f && a.out_bf16 && a.BN <= 128 &&
                     a.BN % 8 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.s_p * 2) % 16 == 0 &&
                     (a.s_n * 2) % 16 == 0 && ((long long)a.col_g * 2) % 16 == 0 && a.N % 8 == 0;
     a.rows_epi = ok ? 1 : 0;
@@ -781,9 +781,34 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     return run_tc(L, s, conv_flops(p), 0);
 }
 
+static caffe_status conv_bwd_data(const caffe_conv_desc* desc, const caffe_blob* top_diff, const caffe_blob* weight,
+                                  const caffe_blob* relu_top, caffe_blob* bottom_diff, float beta, void* ws,
+                                  size_t ws_bytes, caffe_stream_t stream);
+
 caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_blob* top_diff, const caffe_blob* weight,
                                       caffe_blob* bottom_diff, float beta, void* ws, size_t ws_bytes,
                                       caffe_stream_t stream) {
+    return conv_bwd_data(desc, top_diff, weight, nullptr, bottom_diff, beta, ws, ws_bytes, stream);
+}
+
+caffe_status caffe_conv_backward_data_relu(const caffe_conv_desc* desc, const caffe_blob* top_diff,
+                                           const caffe_blob* weight, const caffe_blob* relu_top, caffe_blob* bottom_diff,
+                                           void* ws, size_t ws_bytes, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(relu_top, "relu_top"))) return st;
+    if ((st = check_blob(bottom_diff, "bottom_diff"))) return st;
+    if (!same_shape(relu_top->shape, bottom_diff->shape))
+        return fail(CAFFE_E_SHAPE, "relu_top shape (%d,%d,%d,%d) != bottom_diff shape (%d,%d,%d,%d)", relu_top->shape.n,
+                    relu_top->shape.c, relu_top->shape.h, relu_top->shape.w, bottom_diff->shape.n, bottom_diff->shape.c,
+                    bottom_diff->shape.h, bottom_diff->shape.w);
+    if (nhwc(relu_top) != nhwc(bottom_diff)) return fail(CAFFE_E_INVALID, "relu_top and bottom_diff layouts differ");
+    if (overlap(bottom_diff, relu_top)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps relu_top");
+    return conv_bwd_data(desc, top_diff, weight, relu_top, bottom_diff, 0.f, ws, ws_bytes, stream);
+}
+
+static caffe_status conv_bwd_data(const caffe_conv_desc* desc, const caffe_blob* top_diff, const caffe_blob* weight,
+                                  const caffe_blob* relu_top, caffe_blob* bottom_diff, float beta, void* ws,
+                                  size_t ws_bytes, caffe_stream_t stream) {
     Plan p;
     caffe_status st;
     if ((st = check_blob(bottom_diff, "bottom_diff"))) return st;
@@ -799,11 +824,20 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
     const size_t need = conv_ws(p, CAFFE_PASS_BACKWARD_DATA, desc->math);
     if ((st = check_ws(ws, ws_bytes, need))) return st;
     cudaStream_t s = (cudaStream_t)stream;
+    // ReLU backward by a separate in-place pass where the epilogue does not take it (beta is 0 here)
+    const long long bcount = (long long)p.N * p.C * p.H * p.W;
+    auto relu_after = [&]() -> caffe_status {
+        if (relu_top)
+            CK(relu_bwd(relu_top->ptr, bottom_diff->ptr, bottom_diff->ptr, isbf(relu_top), isbf(bottom_diff), (int)bcount,
+                        s),
+               "relu backward");
+        return CAFFE_OK;
+    };
     if (desc->math == CAFFE_MATH_FP32) {
         CK(fp32_conv_dgrad(top_diff->ptr, isbf(top_diff), strides(top_diff), weight->ptr, isbf(weight), bottom_diff->ptr,
                            isbf(bottom_diff), nhwc(bottom_diff), beta, cgeom(p), s),
            "conv dgrad fp32");
-        return CAFFE_OK;
+        return relu_after();
     }
     char* w8 = (char*)ws;
     Operand A = plan_dy(top_diff, p);
@@ -825,6 +859,7 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
         a.a_cblocks = p.Ogp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Cge;
         set_out(a, bottom_diff);
         a.col_g = p.Cg; a.beta = beta;
+        if (relu_top) { a.relu_top = relu_top->ptr; a.relu_top_bf16 = isbf(relu_top); }
         a.k_last = g_halo_ktrim ? (int)cdiv(p.Og - p.CH * (a.a_cblocks - 1), 16) : 0;
         if (!halo_setup(L, hg, aptr, A.Ctot, p.N)) return fail(CAFFE_E_CUDA, "halo tile setup failed (top_diff)");
         if (!encode_tiled_2d(&L.mapB, p.E, WD, (uint64_t)p.taps * p.Ogp, (uint64_t)p.G * p.Cge,
@@ -852,17 +887,23 @@ caffe_status caffe_conv_backward_data(const caffe_conv_desc* desc, const caffe_b
     if (!p.s2d) {
         set_out(a, bottom_diff);
         a.col_g = p.Cg; a.beta = beta;
+        if (relu_top) { a.relu_top = relu_top->ptr; a.relu_top_bf16 = isbf(relu_top); }
     } else {
         a.out = T; a.out_bf16 = 0; a.P = p.Hp * p.Wp;
         a.s_n = (long long)p.Hp * p.Wp * tg.Ctot; a.s_c = 1; a.s_p = tg.Ctot;
         a.col_g = p.Cge; a.beta = 0.f;
     }
     finish_args(a, a.BN / L.cg * 128);
-    if (!p.s2d && nhwc(bottom_diff))
+    // the TMA-store epilogue takes the ReLU mask for BF16 output and reference in whole 64-column chunks
+    const bool tma_ok = !relu_top || (isbf(bottom_diff) && isbf(relu_top) && p.Cge % 64 == 0);
+    if (!p.s2d && nhwc(bottom_diff) && tma_ok)
         enable_tma_store(L, bottom_diff->ptr, isbf(bottom_diff) ? 2 : 4, p.C, (long long)p.N * p.H * p.W, p.C,
                          p.G == 1 || p.Cg % a.BN == 0);
     if ((st = run_tc(L, s, conv_flops(p), 0))) return st;
-    if (p.s2d) CK(unpack_s2d_grad(T, bottom_diff->ptr, isbf(bottom_diff), nhwc(bottom_diff), beta, tg, s), "unpack s2d gradient");
+    if (p.s2d) {
+        CK(unpack_s2d_grad(T, bottom_diff->ptr, isbf(bottom_diff), nhwc(bottom_diff), beta, tg, s), "unpack s2d gradient");
+        return relu_after();
+    }
     return CAFFE_OK;
 }
 

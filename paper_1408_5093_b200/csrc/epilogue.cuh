@@ -123,6 +123,17 @@ __device__ __forceinline__ void epi_store_strided(const TcArgs& args, uint32_t t
             }
         }
         const long long off0 = rbase + (long long)(cbase + c0) * args.s_c;
+        if (args.relu_top) {   // ReLU backward folded in: keep where the ReLU output is positive
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                if (j < nvalid) {
+                    const float r = args.relu_top_bf16
+                                        ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.relu_top)[off0 + j * args.s_c])
+                                        : reinterpret_cast<const float*>(args.relu_top)[off0 + j * args.s_c];
+                    x[j] = r > 0.f ? x[j] : 0.f;
+                }
+            }
+        }
         if (rowvec && nvalid == 16 && (off0 & (bf ? 7 : 3)) == 0) {
             if (bf) {
                 uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off0);
@@ -239,6 +250,27 @@ __device__ __forceinline__ void epi_store_tma(const TcArgs& args, const CUtensor
         if (args.relu) {
 #pragma unroll
             for (int j = 0; j < 64; j++) x[j] = x[j] > 0.f ? x[j] : 0.f;
+        }
+        if (args.relu_top) {   // ReLU backward folded in (channels-last BF16 reference, row m = row0 + lane)
+            const int m = row0 + lane;
+            if (m < args.M) {
+                const int img = m / args.P, pix = m - img * args.P;
+                const uint4* r4 = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(args.relu_top) +
+                                                                 (long long)img * args.s_n + (long long)pix * args.s_p +
+                                                                 ccol + c0);
+                // (host: BF16 output and reference, N a multiple of 64 -- whole 64-column chunks)
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const uint4 rv = r4[j];
+                    const uint32_t w4[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const uint16_t h = (uint16_t)(w4[e >> 1] >> ((e & 1) * 16));
+                        const bool pos = (h & 0x8000u) == 0 && (h & 0x7fffu) != 0;   // > 0 (no NaN inputs)
+                        x[8 * j + e] = pos ? x[8 * j + e] : 0.f;
+                    }
+                }
+            }
         }
         if (lane == 0) tma_store_wait_read1();
         __syncwarp();

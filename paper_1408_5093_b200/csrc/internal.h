@@ -67,6 +67,11 @@ struct TcArgs {
     // out_w pixels x halo_th rows (swizzled by the box row width: 128/64/32 B, or none when the
     // row is an odd number of 16-byte pieces) and written by 4-D tensor stores through mapC
     int st_cw, st_chunk_bytes, st_tile_bytes;
+    // EPI_STRIDED data gradient through a ReLU (caffe_conv_backward_data_relu): the result of the
+    // pass is kept where relu_top (same element strides as out) is > 0 and zeroed elsewhere,
+    // before beta*old is added
+    const void* relu_top;
+    int relu_top_bf16;
 };
 
 struct TcLaunch {

@@ -600,92 +600,48 @@ __global__ void wgrad_reduce_sg_kernel(const float* __restrict__ partial, float*
     }
 }
 
-// Pair-mode (halo weight gradient, chunk 64) reduction with one block per filter row (g, o): the
-// (channel block, tap, channel) sums are gathered into a shared-memory copy of the row
-// dW[g*Og+o][Cg][kh][kw] and written out contiguously (the one-thread-per-weight kernels scatter
-// 4-byte stores at the kh*kw stride and spend most of their instructions on index divisions).
-// Summation order per weight is exactly theirs: SG = 1 ascending splits; SG > 1 ascending splits
-// within SG equal ranges, the range sums added in ascending order -- so the results are
-// bit-identical.  blockDim = (64, NY): x = channel within the 64-channel chunk; y = item (SG = 1,
-// NY items in flight) or split range (SG > 1).
-template <int SG>
+// Pair-mode (halo weight gradient, chunk 64) reduction, one block per (filter row g*Og+o, 64-channel
+// block): thread (rr, tap) sums channel rr of tap `tap` over the splits (ascending -- the order of
+// wgrad_reduce_kernel, so the results are bit-identical), the block gathers its 64 x kh*kw weights
+// in shared memory and writes them as one contiguous run of dW[g*Og+o][c][kh][kw] (the
+// one-thread-per-weight kernel scatters 4-byte stores at the kh*kw stride and spends most of its
+// instructions on index divisions).  Plain (non-space-to-depth) filters; blockDim = (64, 16).
 __global__ void wgrad_reduce_rows_kernel(const float* __restrict__ partial, float* __restrict__ dW, float beta,
                                          WGeom g, int m_tiles, int n_tiles, int splits, int BN, int cblocks,
                                          float* __restrict__ db) {
-    extern __shared__ float rowbuf[];   // [Cg*kh*kw] (+ [SG][64] range partials)
-    const int row_len = g.Cg * g.kh * g.kw;
-    float* part = rowbuf + ((row_len + 3) & ~3);
-    const int go = blockIdx.x;
+    extern __shared__ float rowbuf[];   // [64][kh*kw]
+    const int taps = g.kh * g.kw;
+    const int go = blockIdx.x / cblocks, cbk = blockIdx.x - go * cblocks;
     const int grp = go / g.Og, o = go - grp * g.Og;
     const int n_tile = o / BN, col = o - n_tile * BN;
-    const int taps = g.khp * g.kwp;
     const int pairs = (taps + 1) / 2;
     const long long sstride = (long long)g.G * m_tiles * n_tiles * BN * 128;
     const float* base = partial + ((long long)grp * m_tiles * n_tiles + n_tile) * BN * 128 + (long long)col * 128;
     const long long mstride = (long long)n_tiles * BN * 128;   // one m_tile
     const int rr = threadIdx.x;
-    const int nitems = cblocks * taps + (db ? 1 : 0);   // the last item: bias gradient (row 64 of the ones pair)
-    auto sum_range = [&](const float* pp, int sp0, int sp1) {
+    const int c0 = cbk * 64, nc = min(64, g.Cg - c0);
+    for (int tap = threadIdx.y; tap < taps; tap += blockDim.y) {
+        if (rr >= nc) continue;
+        const float* pp = base + (long long)(cbk * pairs + tap / 2) * mstride + (tap & 1) * 64 + rr;
         float acc = 0.f;
-        int sp = sp0;
-        for (; sp + 4 <= sp1; sp += 4) {
+        int sp = 0;
+        for (; sp + 4 <= splits; sp += 4) {
             const float a0 = pp[sp * sstride], a1 = pp[(sp + 1) * sstride], a2 = pp[(sp + 2) * sstride],
                         a3 = pp[(sp + 3) * sstride];
             acc += a0; acc += a1; acc += a2; acc += a3;
         }
-        for (; sp < sp1; sp++) acc += pp[sp * sstride];
-        return acc;
-    };
-    // item -> (source pointer, destination index in rowbuf or -1 = bias, -2 = none)
-    auto item = [&](int it, const float*& pp, int& dst) {
-        dst = -2;
-        if (it == cblocks * taps) {
-            if (rr == 0) { pp = base + (long long)(pairs - 1) * mstride + 64; dst = -1; }
-            return;
-        }
-        const int cbk = it / taps, tap = it - cbk * taps;
-        const int cc = cbk * 64 + rr;
-        if (cc >= g.Cg * g.sh * g.sw) return;
-        const int d = cc / g.Cg, c = cc - d * g.Cg;
-        const int i = (tap / g.kwp) * g.sh + d / g.sw, j = (tap % g.kwp) * g.sw + d % g.sw;
-        if (i >= g.kh || j >= g.kw) return;
-        pp = base + (long long)(cbk * pairs + tap / 2) * mstride + (tap & 1) * 64 + rr;
-        dst = (c * g.kh + i) * g.kw + j;
-    };
-    float bias_sum = 0.f;
-    if (SG == 1) {
-        for (int it = threadIdx.y; it < nitems; it += blockDim.y) {
-            const float* pp = nullptr;
-            int dst;
-            item(it, pp, dst);
-            if (dst == -2) continue;
-            const float acc = sum_range(pp, 0, splits);
-            if (dst >= 0) rowbuf[dst] = acc;
-            else bias_sum = acc, db[go] = (beta != 0.f ? beta * db[go] : 0.f) + acc;
-        }
-    } else {
-        const int per = (splits + SG - 1) / SG;
-        const int sp0 = min(splits, (int)threadIdx.y * per), sp1 = min(splits, sp0 + per);
-        for (int it = 0; it < nitems; it++) {
-            const float* pp = nullptr;
-            int dst;
-            item(it, pp, dst);
-            if (dst != -2) part[threadIdx.y * 64 + rr] = sum_range(pp, sp0, sp1);
-            __syncthreads();
-            if (threadIdx.y == 0 && dst != -2) {
-                float r = part[rr];
-#pragma unroll
-                for (int k = 1; k < SG; k++) r += part[k * 64 + rr];
-                if (dst >= 0) rowbuf[dst] = r;
-                else db[go] = (beta != 0.f ? beta * db[go] : 0.f) + r;
-            }
-            __syncthreads();
-        }
+        for (; sp < splits; sp++) acc += pp[sp * sstride];
+        rowbuf[rr * taps + tap] = acc;
     }
-    (void)bias_sum;
+    if (db && cbk == 0 && threadIdx.x == 0 && threadIdx.y == 0) {   // bias gradient: row 64 of the ones pair
+        const float* pp = base + (long long)(pairs - 1) * mstride + 64;
+        float acc = 0.f;
+        for (int sp = 0; sp < splits; sp++) acc += pp[sp * sstride];
+        db[go] = (beta != 0.f ? beta * db[go] : 0.f) + acc;
+    }
     __syncthreads();
-    float* out = dW + (long long)go * row_len;
-    for (int k = threadIdx.y * 64 + threadIdx.x; k < row_len; k += 64 * blockDim.y)
+    float* out = dW + ((long long)go * g.Cg + c0) * taps;
+    for (int k = threadIdx.y * 64 + threadIdx.x; k < nc * taps; k += 64 * blockDim.y)
         out[k] = (beta != 0.f ? beta * out[k] : 0.f) + rowbuf[k];
 }
 
@@ -694,20 +650,12 @@ int g_wgrad_reduce_rows = 1;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
                          int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor, float* db) {
     const int total = g.G * g.Og * g.khp * g.kwp * cblocks * chunk;
-    const int row_len = g.Cg * g.kh * g.kw;
-    if (g_wgrad_reduce_rows && cbmajor && chunk == 64 && row_len <= 11776) {
-        const int SG = splits >= g_wgrad_reduce_sg_min ? (splits >= 32 ? 8 : 4) : 1;
-        const size_t smem = (size_t)(((row_len + 3) & ~3) + (SG > 1 ? SG * 64 : 0)) * 4;
-        const unsigned nb = (unsigned)(g.G * g.Og);
-        if (SG == 8)
-            wgrad_reduce_rows_kernel<8><<<nb, dim3(64, 8), smem, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits,
-                                                                      BN, cblocks, db);
-        else if (SG == 4)
-            wgrad_reduce_rows_kernel<4><<<nb, dim3(64, 4), smem, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits,
-                                                                      BN, cblocks, db);
-        else
-            wgrad_reduce_rows_kernel<1><<<nb, dim3(64, 4), smem, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits,
-                                                                      BN, cblocks, db);
+    // plain filters (no space-to-depth), pair mode, fewer splits than the split-range threshold
+    if (g_wgrad_reduce_rows && cbmajor && chunk == 64 && g.sh == 1 && g.sw == 1 && g.khp == g.kh && g.kwp == g.kw &&
+        splits < g_wgrad_reduce_sg_min && g.kh * g.kw <= 64) {
+        const size_t smem = (size_t)64 * g.kh * g.kw * 4;
+        wgrad_reduce_rows_kernel<<<(unsigned)(g.G * g.Og * cblocks), dim3(64, 16), smem, s>>>(
+            partial, dW, beta, g, m_tiles, n_tiles, splits, BN, cblocks, db);
         note_launch();
         return cudaGetLastError();
     }

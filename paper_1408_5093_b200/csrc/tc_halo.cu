@@ -572,7 +572,7 @@ cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s) {
 // accumulators per unit, and a compiled instance for BN/2.
 int halo_fast_epc(const TcArgs& a, int cg) {
     const int macc = a.macc > 1 ? a.macc : 1;
-    if (!g_halo_fast_epi || cg != 2 || macc != 2) return 0;
+    if (!g_halo_fast_epi || cg != 2 || macc != 2 || a.relu_top) return 0;
     if (!(a.out_bf16 && a.s_c == 1 && a.beta == 0.f && a.N % a.BN == 0 && (a.BN / 2) % 8 == 0 && a.s_n % 8 == 0 &&
           a.s_p % 8 == 0 && a.col_g % 8 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0))
         return 0;

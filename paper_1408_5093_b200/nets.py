@@ -215,6 +215,14 @@ class Net:
             self._ws_wgrad = self.torch.empty(n + 2048, dtype=self.torch.uint8, device=self.device)
         return self._ws_wgrad
 
+    def _relu_into_dgrad(self, i):
+        """True when the ReLU backward of layer i-1 is folded into layer i's conv data gradient
+        (caffe_conv_backward_data_relu: conv3 -> relu3 -> conv4, conv4 -> relu4 -> conv5)."""
+        if i <= 0 or self.layers[i].kind != "conv":
+            return False
+        P = self.layers[i - 1]
+        return P.kind in ("conv", "ip") and P.relu
+
     def backward(self, hook=None, done_hook=None, wgrad_stream=None):
         """Backward in reverse; `hook(i)` is called after layer i's parameter gradients are enqueued
         (data-parallel bucketing point), `done_hook(i)` once nothing later in the step reads layer
@@ -229,7 +237,7 @@ class Net:
             L = self.layers[i]
             dy = d[i + 1] if i + 1 < n - 1 else self.dscores
             y = a[i + 1] if i + 1 < n - 1 else self.scores
-            if L.kind in ("conv", "ip") and L.relu and not self._relu_fused(i):
+            if L.kind in ("conv", "ip") and L.relu and not self._relu_fused(i) and not self._relu_into_dgrad(i + 1):
                 cb.relu_backward(y, dy, inplace=True)  # sign of the ReLU output == sign test on its input
             if L.kind == "conv":
                 pre = i == 0 and self.ws0 is not None
@@ -247,7 +255,9 @@ class Net:
                                             dw=self.dW[i], db=self.dB[i], ws=self.ws0 if pre else None, prepacked=pre)
                 if hook:
                     hook(i)
-                if i > 0:
+                if i > 0 and self._relu_into_dgrad(i):
+                    cb.conv_backward_data_relu(dy, self._wop(i), a[i], L.stride, L.pad, L.group, self.math, out=d[i])
+                elif i > 0:
                     cb.conv_backward_data(dy, self._wop(i), a[i].shape, L.stride, L.pad, L.group, self.math,
                                           beta=0.0, out=d[i])
                 if done_hook:
@@ -274,14 +284,14 @@ class Net:
                       w_bf16=self.params_bf16 if self.math == "bf16" else None)
 
     side_sgd_blocks = 1
-    # side-stream SGD updates of the layers whose gradients are final are held back until the
-    # backward pass reaches this layer index (default: the third parameter layer from the input,
-    # CaffeNet conv3), so they overlap the tensor-core-bound tail of the backward (conv2 / conv1)
-    # instead of the L2-bound conv3-5 passes.  Measured (graph replay, one B200): 1.758 ms/step
-    # with immediate updates, 1.675 held to conv3, 1.842 held to conv2.
+    # side-stream SGD updates of the layers whose gradients are final may be held back until the
+    # backward pass reaches this layer index (None: each layer's update is launched as soon as its
+    # gradients are final).  Measured (graph replay, one B200, ms/step): with the weight gradients
+    # on the main stream, 1.758 immediate / 1.675 held to conv3 / 1.842 held to conv2; with them on
+    # their side stream (wgrad_side), 1.624 immediate / 1.726 held to conv3; no update at all 1.537.
     sgd_flush_layer = None
     # conv weight gradients (layers > 0) on their own stream, concurrent with the data gradients
-    wgrad_side = False
+    wgrad_side = True
 
     def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4, overlap_update=True):
         self.forward()
@@ -299,8 +309,7 @@ class Net:
             pending = []
             flush_at = self.sgd_flush_layer
             if flush_at is None:
-                pl = [i for i, L in enumerate(self.layers) if L.kind in ("conv", "ip")]
-                flush_at = pl[min(2, len(pl) - 1)]
+                flush_at = len(self.layers)
 
             wstream = None
             if self.wgrad_side:
@@ -308,7 +317,10 @@ class Net:
                     self._wside = torch.cuda.Stream()
                 wstream = self._wside
 
+            launched = []
+
             def launch():
+                launched.append(1)
                 # pending layers hold one contiguous range of the flat parameter buffer (backward order)
                 lo = min(seg[i][0] for i in pending)
                 hi = max(seg[i][0] + seg[i][1] for i in pending)
@@ -327,6 +339,8 @@ class Net:
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_BLOCKS_PER_SM, 0)
 
             def done(i):
+                if getattr(self, "skip_update", False):
+                    return
                 pending.append(i)
                 if i <= flush_at:
                     launch()
@@ -334,8 +348,9 @@ class Net:
             self.backward(done_hook=done, wgrad_stream=wstream)
             if pending:
                 launch()
-            main.wait_stream(self._side)
-            if wstream is not None:
+            if launched:
+                main.wait_stream(self._side)
+            if wstream is not None and self.wgrad_done:
                 main.wait_stream(wstream)
             return
         self.backward(hook=allreduce.on_grad if allreduce else None)

@@ -447,10 +447,11 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
                          ids=["conv1geom", "conv2geom", IDS[7], "C64O96"])
 @pytest.mark.parametrize("sg", [0, 2])
 def test_wgrad_reduce_rows_bit_identical(oracle, case, sg):
-    """The per-filter-row split reduction of the halo weight gradient (CAFFE_TUNE_WGRAD_REDUCE_ROWS,
-    default on) gives the bits of the one-thread-per-weight reduction, in the plain ascending-split
-    form and the split-range form (CAFFE_TUNE_WGRAD_REDUCE_SG lowered to 2), with beta = 0 and 1
-    and the bias gradient from the ones chunk; and matches the oracle."""
+    """The per-(filter row, channel block) split reduction of the halo weight gradient
+    (CAFFE_TUNE_WGRAD_REDUCE_ROWS, default on) gives the bits of the one-thread-per-weight reduction
+    (and leaves the split-range form, CAFFE_TUNE_WGRAD_REDUCE_SG lowered to 2, and space-to-depth
+    filters to it), with beta = 0 and 1 and the bias gradient from the ones chunk; and matches the
+    oracle."""
     import torch
     import paper_1408_5093_b200 as cb
     from paper_1408_5093_b200 import _abi
@@ -483,3 +484,42 @@ def test_wgrad_reduce_rows_bit_identical(oracle, case, sg):
     rW, rb = oracle.conv_backward_weight(host(Xd), host(dYd), Wt.shape, stride=s, pad=p, group=g)
     assert_tc_close(outs[1][0], rW, "wgrad rows")
     assert_fp32_close(outs[1][1], rb, "bias grad rows")
+
+
+@pytest.mark.parametrize("case,act,math,nhwc", [
+    ((2, 128, 13, 13, 96, (3, 3), (1, 1), (1, 1), 1), "bf16", "bf16", True),    # im2col, TMA-store epilogue
+    ((2, 64, 13, 13, 256, (3, 3), (1, 1), (1, 1), 2), "bf16", "bf16", True),    # grouped im2col (conv5-like)
+    ((2, 96, 27, 27, 64, (5, 5), (1, 1), (2, 2), 2), "bf16", "bf16", True),     # halo tiles (generic epilogue)
+    ((2, 8, 13, 13, 12, (3, 3), (1, 1), (1, 1), 2), "f32", "bf16", True),       # FP32 output, strided epilogue
+    ((2, 3, 35, 35, 16, (11, 11), (4, 4), (0, 0), 1), "bf16", "bf16", True),    # space-to-depth: separate pass
+    ((2, 8, 13, 13, 12, (3, 3), (1, 1), (1, 1), 2), "f32", "fp32", False),      # FP32 math, NCHW
+], ids=["im2col", "grouped", "halo", "f32out", "s2d", "fp32math"])
+def test_conv_backward_data_relu(oracle, case, act, math, nhwc):
+    """caffe_conv_backward_data_relu (the data gradient through the ReLU that produced the layer's
+    bottom, S:154 + S:208) gives exactly the bits of caffe_conv_backward_data followed by the ReLU
+    backward, on every epilogue path; and the masked result matches the oracle."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 61)
+    dt = torch.bfloat16 if act == "bf16" else torch.float32
+    mf = torch.channels_last if nhwc else torch.contiguous_format
+    top = cuda(X).to(dt).contiguous(memory_format=mf).relu_()     # ReLU output: zeros and positives
+    dYd = cuda(dY).to(dt).contiguous(memory_format=mf)
+    w = cuda(Wt)
+    ref = torch.empty((N, C, H, W), device="cuda", dtype=dt).contiguous(memory_format=mf)
+    cb.conv_backward_data(dYd, w, X.shape, stride=s, pad=p, group=g, math=math, out=ref)
+    cb.relu_backward(top, ref, inplace=True)
+    got = cb.conv_backward_data_relu(dYd, w, top, stride=s, pad=p, group=g, math=math)
+    np.testing.assert_array_equal(host(got), host(ref))
+    q = (lambda a: a) if math == "fp32" else oracle.quant_bf16
+    want = oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g) * (host(top) > 0)
+    if act == "bf16":
+        assert_tc_close(host(got), want, "masked dgrad", tol=5e-3)
+    elif math == "fp32":
+        assert_fp32_close(host(got), want, "masked dgrad fp32")
+    else:
+        assert_tc_close(host(got), want, "masked dgrad", tol=3e-3)
+    # errors: shape and layout mismatches
+    with pytest.raises(RuntimeError):
+        cb.conv_backward_data_relu(dYd, w, top[:1], stride=s, pad=p, group=g, math=math)

@@ -42,7 +42,8 @@ def main():
                 _abi.call("caffe_set_tuning", int(k[4:]), v)
         net.sgd_flush_layer = p.get("flush", None)
         net.side_sgd_blocks = p.get("blocks", 1)
-        net.wgrad_side = bool(p.get("wside", 0))
+        net.wgrad_side = bool(p.get("wside", 1))
+        net.skip_update = bool(p.get("nosgd", 0))   # probe only: no parameter update (SGD cost)
         for _ in range(2):
             net.step()
         torch.cuda.synchronize()
