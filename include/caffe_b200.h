@@ -172,6 +172,13 @@ caffe_status caffe_device_check(void);
    64-channel block) with a shared-memory gather and contiguous dW stores; 0 = one thread per
    weight.  Bit-identical results (same summation order). */
 #define CAFFE_TUNE_WGRAD_REDUCE_ROWS 13
+/* CAFFE_TUNE_HALO_STACKED: stacked halo tiles for same-size stride-1 convolutions (odd kernel, centred
+   padding) on maps too small for whole-row halo tiles (CaffeNet conv3-5 forward and data
+   gradient): images laid end to end as one pixel sequence with shared zero rows/columns, one
+   staged window per 128-pixel tile serving every tap.  0 = off (per-tap im2col tiles), 1 (default)
+   = where whole-row halo tiles do not apply and N tiles are <= 128 columns (CaffeNet conv5
+   forward), 2 = wherever the geometry allows. */
+#define CAFFE_TUNE_HALO_STACKED 14
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -35,6 +35,7 @@ CAFFE_TUNE_HALO_KTRIM = 10
 CAFFE_TUNE_HALO_FAST_EPI = 11
 CAFFE_TUNE_HALO_TMA_STORE = 12
 CAFFE_TUNE_WGRAD_REDUCE_ROWS = 13
+CAFFE_TUNE_HALO_STACKED = 14
 
 
 class Shape4(ctypes.Structure):

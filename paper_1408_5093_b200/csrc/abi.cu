@@ -434,24 +434,58 @@ static bool halo_applies(int E, const HaloGeom& h) {
     const double eff = (double)h.Ho * h.Wo / (tpi * 128.0);
     return h.kh * h.kw >= 4 && eff >= 0.75;
 }
+// Stacked halo tiles (TcArgs::stk) for same-size stride-1 convolutions with odd kernels and
+// centred padding (CaffeNet conv3-5 forward and data gradient: 3x3/pad 1 on 13x13), whose maps
+// are too small for whole-row halo tiles (66% useful rows) and whose per-tap im2col tiles stream
+// every activation 9x from L2: rows W + pad_w wide and images H + pad_h tall in one pixel sequence,
+// 86% useful rows for 13x13.  CAFFE_TUNE_HALO_STACKED: 0 off, 1 (default) where whole-row halo tiles
+// do not apply, 2 wherever the geometry allows.
+int g_halo_stacked = 1;
+int g_stk_astages = 4;   // probe knob (key 98)
+static bool stacked_geom(const HaloGeom& h) {
+    return h.Ho == h.Hi && h.Wo == h.Wi && (h.kh & 1) && (h.kw & 1) && h.pad_h == (h.kh - 1) / 2 &&
+           h.pad_w == (h.kw - 1) / 2 && h.kh * h.kw >= 4 && h.Wi + h.pad_w <= 256 && h.Wo >= 4;
+}
+// Automatic use only with N tiles of <= 128 columns (two accumulators per CTA share each weight
+// tile): measured on CaffeNet (us, per-tap im2col -> stacked) conv5 forward 46.2 -> 39.7, but
+// conv3/conv4 forward 60.3/48.1 -> 63.2/51.0 and the 192/256-column data gradients 59.0/48.4/35.1 ->
+// 67.5/52.2/38.8 (one accumulator per CTA: every weight tile feeds a single 128-pixel tile).
+static bool stacked_applies(int E, const HaloGeom& h, int BN) {
+    if (E != 2 || g_halo == 1 || g_halo_stacked == 0 || !stacked_geom(h)) return false;
+    if (g_halo_stacked == 2) return true;
+    return !halo_applies(E, h) && BN <= 128;
+}
 // Fills the halo fields of L (A map over the channels-last operand `aptr` [N][Hi][Wi][Ctot]) after
 // the caller has set BN, N, n_tiles, groups, b_row_g, a_cpg, a_cblocks and the epilogue.
 int g_halo_ktrim = 1;   // CAFFE_TUNE_HALO_KTRIM
 static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Ctot, int N) {
     TcArgs& a = L.args;
     L.amode = A_HALO_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED; L.esz = 2;
-    a.halo_wt = h.Wo + h.kw - 1;
-    a.halo_th = 128 / a.halo_wt;
-    a.halo_rows = a.halo_th + h.kh - 1;
     a.halo_kh = h.kh; a.a_kw = h.kw;
     a.a_pad_h = h.pad_h; a.a_pad_w = h.pad_w;
-    a.tiles_per_img = (h.Ho + a.halo_th - 1) / a.halo_th;
-    a.total_tiles = N * a.tiles_per_img;
     a.out_h = h.Ho; a.out_w = h.Wo;
-    const int need_rows = std::max(a.halo_rows * a.halo_wt, (h.kh - 1) * a.halo_wt + (h.kw - 1) + 128);
-    a.halo_slot = (int)rup((long long)need_rows * 128, 1024);
-    if (!encode_tiled_4d(&L.mapA, 2, aptr, Ctot, h.Wi, h.Hi, N, 64, (uint32_t)a.halo_wt, (uint32_t)a.halo_rows))
-        return false;
+    a.stk = stacked_applies(2, h, a.BN) ? 1 : 0;
+    if (a.stk) {
+        a.stk_wt = h.Wi + h.pad_w; a.stk_hs = h.Hi + h.pad_h; a.stk_nimg = N;
+        a.stk_off = a.stk_wt - 1;
+        a.halo_wt = a.stk_wt;             // tap (i, j) shift = i*stk_wt + j rows
+        a.halo_th = 1; a.halo_rows = 1; a.tiles_per_img = 1;
+        const int r_last = a.stk_off + 127 + (h.kh - 1) * a.stk_wt + (h.kw - 1);
+        a.stk_nb = (r_last + a.stk_wt) / a.stk_wt;   // ceil((r_last + 1) / wt)
+        a.halo_slot = (int)rup((long long)(a.stk_off + a.stk_nb * a.stk_wt) * 128, 1024);
+        a.total_tiles = (int)cdiv((long long)N * a.stk_hs * a.stk_wt, 128);
+        if (!encode_tiled_4d(&L.mapA, 2, aptr, Ctot, h.Wi, h.Hi, N, 64, (uint32_t)a.stk_wt, 1)) return false;
+    } else {
+        a.halo_wt = h.Wo + h.kw - 1;
+        a.halo_th = 128 / a.halo_wt;
+        a.halo_rows = a.halo_th + h.kh - 1;
+        a.tiles_per_img = (h.Ho + a.halo_th - 1) / a.halo_th;
+        a.total_tiles = N * a.tiles_per_img;
+        const int need_rows = std::max(a.halo_rows * a.halo_wt, (h.kh - 1) * a.halo_wt + (h.kw - 1) + 128);
+        a.halo_slot = (int)rup((long long)need_rows * 128, 1024);
+        if (!encode_tiled_4d(&L.mapA, 2, aptr, Ctot, h.Wi, h.Hi, N, 64, (uint32_t)a.halo_wt, (uint32_t)a.halo_rows))
+            return false;
+    }
     // CTA pairs when the B tile splits into 8-row halves and there is enough work for every pair
     L.cg = 1;
     if ((a.BN / 2) % 8 == 0 &&
@@ -461,13 +495,15 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     a.a_stages = 2;
     a.macc = 1;
     if (2 * 2 * a.acc_stride <= 512 && a.a_stages * 2 * a.halo_slot <= 140 * 1024) a.macc = 2;
+    // stacked tiles turn their A stages over faster (fewer taps per staged window): deeper A ring
+    if (a.stk) a.a_stages = std::max(2, std::min(g_stk_astages, (int)((140 * 1024) / (a.macc * a.halo_slot))));
     a.b_stage_bytes = a.BN / L.cg * 128;
     long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
     // TMA tensor-store epilogue (specialised-epilogue launches): the unit's tiles are staged in
     // shared memory as boxes of cw channels x Wo pixels x halo_th rows and leave through mapC
     a.tma_store = 0;
     const int epc = halo_fast_epc(a, L.cg);
-    if (epc > 0 && cb::g_halo_tma_store) {
+    if (epc > 0 && cb::g_halo_tma_store && !a.stk) {
         const int cwl = epc % 64 == 0 ? 6 : epc % 32 == 0 ? 5 : epc % 16 == 0 ? 4 : 0;
         const int cw = cwl ? 1 << cwl : epc;
         const int align = cwl ? 16 * cw : 128;   // the swizzle pattern repeats every 8 rows
@@ -596,8 +632,17 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_sgd_blocks_per_sm = value == 0 ? 4 : value;
         return CAFFE_OK;
     }
+    if (key == 98) {   // profiling probe: A stages of stacked halo tiles
+        g_stk_astages = value;
+        return CAFFE_OK;
+    }
     if (key == 99) {   // profiling probes (not part of the documented interface)
         cb::g_dbg = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_HALO_STACKED) {
+        if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "stacked halo mode must be 0 (off), 1 (auto), 2 (force)");
+        g_halo_stacked = value;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_WGRAD_REDUCE_ROWS) {
@@ -742,7 +787,7 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     TcLaunch L;
     memset(&L, 0, sizeof L);
     const HaloGeom hg{A.H, A.W, p.OH, p.OW, p.khp, p.kwp, p.php, p.pwp};
-    if (halo_applies(p.E, hg)) {
+    if (halo_applies(p.E, hg) || stacked_applies(p.E, hg, choose_bn(p.Og))) {
         TcArgs& a = L.args;
         a.BN = choose_bn(p.Og); a.N = p.Og;
         a.n_tiles = (int)cdiv(p.Og, a.BN); a.groups = p.G;
@@ -852,7 +897,7 @@ static caffe_status conv_bwd_data(const caffe_conv_desc* desc, const caffe_blob*
     TcLaunch L;
     memset(&L, 0, sizeof L);
     const HaloGeom hg{p.OH, p.OW, Hd, Wd, p.khp, p.kwp, lo_h, lo_w};
-    if (!p.s2d && halo_applies(p.E, hg)) {
+    if (!p.s2d && (halo_applies(p.E, hg) || stacked_applies(p.E, hg, choose_bn(p.Cge)))) {
         TcArgs& a = L.args;
         a.BN = choose_bn(p.Cge); a.N = p.Cge;
         a.n_tiles = (int)cdiv(p.Cge, a.BN); a.groups = p.G;

@@ -72,6 +72,13 @@ struct TcArgs {
     // before beta*old is added
     const void* relu_top;
     int relu_top_bf16;
+    // A_HALO_K stacked mode (same-size convolutions on small maps, e.g. 3x3/pad 1 on 13x13): the
+    // images are laid end to end in one pixel sequence whose rows are stk_wt = W + pad_w wide (one
+    // zero column shared by the right pad of a row and the left pad of the next) and whose images
+    // are stk_hs = H + pad_h rows tall (one shared zero row); 128-row tiles run over that sequence
+    // regardless of image boundaries.  A tile's window is staged as stk_nb one-row TMA boxes placed
+    // so that the tile's first pixel lands at shared-memory row stk_off in every CTA.
+    int stk, stk_wt, stk_hs, stk_nimg, stk_nb, stk_off;
 };
 
 struct TcLaunch {

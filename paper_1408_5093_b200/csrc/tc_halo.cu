@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp == 0 && lane == 0) {
         // ===================== TMA producer (both CTAs) =====================
-        const uint32_t txA = (uint32_t)(macc * args.halo_rows * args.halo_wt * 128);
+        const uint32_t txA = args.stk ? (uint32_t)(macc * args.stk_nb * args.stk_wt * 128)
+                                      : (uint32_t)(macc * args.halo_rows * args.halo_wt * 128);
         const uint32_t txB = (uint32_t)args.b_stage_bytes;
         const int bn_cta = args.BN / CG;
         int sa = 0, sb = 0;
@@ -126,10 +127,25 @@ __global__ void __launch_bounds__(384, 1)
                 for (int a = 0; a < macc; a++) {
                     int tile = tg * tiles_per_unit + a * CG + (int)rank;
                     if (tile >= args.total_tiles) tile = args.total_tiles - 1;   // rows discarded
-                    const int n = tile / args.tiles_per_img;
-                    const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;
                     uint8_t* dst = a_ring + sa * a_stage_bytes + a * slot;
                     const int c = g * args.a_cpg + cb * CH;
+                    if (args.stk) {
+                        // one-row boxes: stacked row b (image b / hs, padded row b % hs) at shared row
+                        // stk_off - (m0 - b0*wt) + q*wt, so the tile's first pixel is at row stk_off
+                        const int m0 = tile * 128;
+                        const int b0 = m0 / args.stk_wt;
+                        int img = b0 / args.stk_hs, lb = b0 - img * args.stk_hs;
+                        uint8_t* d = dst + (args.stk_off - (m0 - b0 * args.stk_wt)) * 128;
+                        for (int q = 0; q < args.stk_nb; q++) {
+                            if (CG == 2) tma_load_4d_cg2(d, &mapA, &fullA[sa], c, -args.a_pad_w, lb - args.a_pad_h, img);
+                            else tma_load_4d(d, &mapA, &fullA[sa], c, -args.a_pad_w, lb - args.a_pad_h, img);
+                            d += args.stk_wt * 128;
+                            if (++lb == args.stk_hs) { lb = 0; img++; }
+                        }
+                        continue;
+                    }
+                    const int n = tile / args.tiles_per_img;
+                    const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;
                     if (CG == 2) tma_load_4d_cg2(dst, &mapA, &fullA[sa], c, -args.a_pad_w, y0 - args.a_pad_h, n);
                     else tma_load_4d(dst, &mapA, &fullA[sa], c, -args.a_pad_w, y0 - args.a_pad_h, n);
                 }
@@ -168,8 +184,9 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 const uint32_t sa_addr = a_base + sa * a_stage_bytes;
                 // tap (i, j) reads the staged window shifted by i*halo_wt + j rows (no division in
-                // the issue loop: the MMA warp's instruction latency bounds small-N tiles)
-                uint32_t shift = 0;
+                // the issue loop: the MMA warp's instruction latency bounds small-N tiles); stacked
+                // tiles start at row stk_off of their slot
+                uint32_t shift = (uint32_t)args.stk_off * 128u;
                 int tj = 0;
                 const uint32_t row_skip = (uint32_t)(args.halo_wt - args.a_kw + 1) * 128u;
                 for (int tap = 0; tap < taps; tap++) {
@@ -264,10 +281,23 @@ __global__ void __launch_bounds__(384, 1)
             }
             for (int a = 0; a < macc; a++) {
                 const int tile = tg * tiles_per_unit + a * CG + (int)rank;
-                const int n = tile / args.tiles_per_img;
-                const int y = (tile - n * args.tiles_per_img) * args.halo_th + yy;
-                const bool row_ok = tile < args.total_tiles && yy < args.halo_th && y < args.out_h && xx < args.out_w;
-                const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + xx) * args.s_p;
+                int n, y, x;
+                bool row_ok;
+                if (args.stk) {   // stacked pixel m = n*(hs*wt) + y*wt + x
+                    const int m = tile * 128 + row;
+                    const int per = args.stk_hs * args.stk_wt;
+                    n = m / per;
+                    const int l = m - n * per;
+                    y = l / args.stk_wt;
+                    x = l - y * args.stk_wt;
+                    row_ok = tile < args.total_tiles && n < args.stk_nimg && y < args.out_h && x < args.out_w;
+                } else {
+                    n = tile / args.tiles_per_img;
+                    y = (tile - n * args.tiles_per_img) * args.halo_th + yy;
+                    x = xx;
+                    row_ok = tile < args.total_tiles && yy < args.halo_th && y < args.out_h && xx < args.out_w;
+                }
+                const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + x) * args.s_p;
                 if constexpr (EPC > 0) {
                     if (args.dbg == 2) continue;
                     if (tstore) {

@@ -523,3 +523,42 @@ def test_conv_backward_data_relu(oracle, case, act, math, nhwc):
     # errors: shape and layout mismatches
     with pytest.raises(RuntimeError):
         cb.conv_backward_data_relu(dYd, w, top[:1], stride=s, pad=p, group=g, math=math)
+
+
+@pytest.mark.parametrize("case", [CASES[7], CASES[1], (2, 64, 13, 13, 256, (3, 3), (1, 1), (1, 1), 2),
+                                  (3, 40, 9, 11, 72, (5, 3), (1, 1), (2, 1), 1),
+                                  (2, 96, 27, 27, 64, (5, 5), (1, 1), (2, 2), 2)],
+                         ids=[IDS[7], IDS[1], "conv5geom", "k5x3", "conv2geom"])
+@pytest.mark.parametrize("cta", [0, 1, 2])
+def test_conv_stacked_halo(oracle, case, cta):
+    """Stacked halo tiles (CAFFE_TUNE_HALO_STACKED=2: the images as one pixel sequence with shared
+    zero rows/columns, 128-pixel tiles across image boundaries, one-row TMA boxes placed so every
+    CTA's tile starts at the same shared-memory row) give oracle parity for the forward (bias, ReLU,
+    FP32 and BF16 outputs) and the data gradient, single-CTA and CTA-pair, ragged last tile."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 71)
+    q = oracle.quant_bf16
+    cl = torch.channels_last
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_STACKED, 2)
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, cta)
+    try:
+        Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+        dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+        Y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True, out_dtype=torch.float32)
+        Y16 = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True)
+        dX = torch.empty((N, C, H, W), device="cuda").contiguous(memory_format=cl)
+        cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
+        dX16 = torch.empty((N, C, H, W), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl)
+        cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX16)
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_STACKED, 1)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
+    ry = oracle.conv_forward(host(Xd), q(Wt), b, stride=s, pad=p, group=g, relu=True)
+    rx = oracle.conv_backward_data(host(dYd), q(Wt), X.shape, stride=s, pad=p, group=g)
+    assert_tc_close(host(Y), ry, f"stacked fwd cta={cta}")
+    assert_tc_close(host(dX), rx, f"stacked dgrad cta={cta}", tol=3e-3)
+    np.testing.assert_array_equal(host(Y16), host(Y.to(torch.bfloat16)))
+    np.testing.assert_array_equal(host(dX16), host(dX.to(torch.bfloat16)))
