@@ -380,14 +380,14 @@ def ip_backward_data(dy, w, in_shape, math="bf16", beta=0.0, out=None, out_dtype
     return out
 
 
-def ip_backward_weight(x, dy, w_shape, math="bf16", beta=0.0, dw=None, db=None, bias=True):
+def ip_backward_weight(x, dy, w_shape, math="bf16", beta=0.0, dw=None, db=None, bias=True, ws=None):
     torch = _t()
     O = w_shape[0]
     if dw is None:
         dw = torch.zeros(tuple(w_shape), dtype=torch.float32, device=x.device)
     if bias and db is None:
         db = torch.zeros((O,), dtype=torch.float32, device=x.device)
-    ws, wsz = _ip_ws(math, x.shape, O, 2)
+    ws, wsz = _ws_arg(ws) if ws is not None else _ip_ws(math, x.shape, O, 2)
     bx, bdy, bdw = blob(x), blob(dy, (dy.shape[0], O, 1, 1)), _wblob(dw)
     bdb = blob(db) if bias else None
     call("caffe_ip_backward_weight", MATH[math], ctypes.byref(bx), ctypes.byref(bdy), ctypes.byref(bdw), _bp(bdb),

@@ -153,7 +153,9 @@ class Net:
             self.a.append(cb.empty_like_layout(s, ad, device, nhwc=self.nhwc[i]))
             self.d.append(cb.empty_like_layout(s, ad, device, nhwc=self.nhwc[i]) if i > 0 else None)
         self.scores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
-        self.dscores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
+        # the loss gradient in the activation dtype: the softmax kernel writes the RNE BF16 value the
+        # fc8 tensor-core passes would otherwise convert it to (no separate convert pass)
+        self.dscores = torch.empty(self.shapes[-1], dtype=self.act_dtype, device=device)
         for i, L in enumerate(layers):
             if L.kind == "pool":
                 # window-local uint8 argmax (a quarter of the int32 mask traffic; same results)
@@ -201,10 +203,16 @@ class Net:
         return L.kind in ("conv", "ip") and L.relu and P.kind == "pool" and P.method == "max"
 
     def _wgrad_workspace(self):
-        """Dedicated workspace of the side-stream weight-gradient passes (largest conv layer i > 0)."""
+        """Dedicated workspace of the side-stream weight-gradient passes (largest conv layer i > 0
+        or inner-product layer; the passes run one after another on that stream)."""
         if getattr(self, "_ws_wgrad", None) is None:
             n = 0
             for i, L in enumerate(self.layers):
+                if L.kind == "ip":
+                    v = cb.ctypes.c_size_t()
+                    cb.call("caffe_ip_workspace_size", cb.MATH[self.math], _abi.Shape4(*cb._shape4(self.shapes[i])),
+                            int(L.num_output), 2, cb.ctypes.byref(v))
+                    n = max(n, v.value)
                 if L.kind == "conv" and i > 0:
                     d = cb._conv_desc((L.kernel, L.kernel), L.stride, L.pad, L.group, self.math)
                     v = cb.ctypes.c_size_t()
@@ -264,7 +272,18 @@ class Net:
                     done_hook(i)
             elif L.kind == "ip":
                 dy2 = dy.view(dy.shape[0], -1)
-                cb.ip_backward_weight(a[i], dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i], db=self.dB[i])
+                if wgrad_stream is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream())
+                    wgrad_stream.wait_event(ev)
+                    with torch.cuda.stream(wgrad_stream):
+                        cb.ip_backward_weight(a[i], dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i],
+                                              db=self.dB[i], ws=self._wgrad_workspace())
+                        self.wgrad_done[i] = torch.cuda.Event()
+                        self.wgrad_done[i].record(wgrad_stream)
+                else:
+                    cb.ip_backward_weight(a[i], dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i],
+                                          db=self.dB[i])
                 if hook:
                     hook(i)
                 if i > 0:
