@@ -314,9 +314,32 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
 caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
                                     caffe_blob* bottom_diff, float beta, void* workspace, size_t workspace_bytes,
                                     caffe_stream_t stream);
+/* Data gradient through the ReLU that produced this layer's bottom (S:187-195 with S:205-213 folded
+   in): bottom_diff = [relu_top > 0] * (top_diff . W) (overwritten).  relu_top: the ReLU output
+   (= this layer's bottom), F32|BF16, same shape and layout as bottom_diff, no overlap.  The mask is
+   applied in the split-K reduce or the tensor-core epilogue where it can, else by an in-place
+   ReLU-backward pass.  Errors: as caffe_ip_backward_data, plus E_SHAPE, E_INVALID, E_ALIAS. */
+caffe_status caffe_ip_backward_data_relu(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
+                                         const caffe_blob* relu_top, caffe_blob* bottom_diff, void* workspace,
+                                         size_t workspace_bytes, caffe_stream_t stream);
 caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom, const caffe_blob* top_diff,
                                       caffe_blob* weight_diff, caffe_blob* bias_diff, float beta, void* workspace,
                                       size_t workspace_bytes, caffe_stream_t stream);
+
+/* Inner-product weight gradient with the SGD update fused in (S:187-195 then S:520-528; one GPU,
+   where nothing needs the gradient itself): for every weight,
+     g' = dW*grad_scale + decay*W;  v = momentum*v - lr*g';  W = W + v;  weight_bf16 = RNE(W)
+   with dW = top_diff^T . bottom computed by the tensor cores and consumed in the epilogue (never
+   stored; bit-identical to caffe_ip_backward_weight followed by caffe_sgd_update).  bias_diff
+   (nullable, F32, overwritten) receives the bias gradient; the bias update stays with
+   caffe_sgd_update.  weight/momentum F32 and weight_bf16 BF16, all (O, K) row-major, K % 32 == 0,
+   16-byte aligned, mutually non-overlapping.  BF16 tensor-core math only.  Errors: E_SHAPE, E_DTYPE,
+   E_INVALID (layout), E_ALIGN, E_ALIAS, E_WORKSPACE (size as caffe_ip_workspace_size(BF16, ...,
+   CAFFE_PASS_BACKWARD_WEIGHT)). */
+caffe_status caffe_ip_backward_weight_sgd(const caffe_blob* bottom, const caffe_blob* top_diff, caffe_blob* weight,
+                                          caffe_blob* momentum, caffe_blob* weight_bf16, caffe_blob* bias_diff,
+                                          float lr, float momentum_coef, float decay, float grad_scale,
+                                          void* workspace, size_t workspace_bytes, caffe_stream_t stream);
 
 /* ------------------------------------------------------------------ im2col / col2im (test entry points)
    S:297 / S:806 lowering of image n: col[(c*kh+i)*kw+j][y*OW+x] = bottom[n,c,y*sh-ph+i,x*sw-pw+j]

@@ -380,6 +380,33 @@ def ip_backward_data(dy, w, in_shape, math="bf16", beta=0.0, out=None, out_dtype
     return out
 
 
+def ip_backward_weight_sgd(x, dy, w, mom, w_bf16, lr, momentum, decay, grad_scale=1.0, db=None, ws=None):
+    """Fused inner-product weight gradient + SGD update (S:190 then S:523): updates the FP32 master
+    weights w and momentum mom in place, writes the BF16 copy w_bf16; db (optional) receives the
+    bias gradient."""
+    O = w.shape[0]
+    ws, wsz = _ws_arg(ws) if ws is not None else _ip_ws("bf16", x.shape, O, 2)
+    bx, bdy = blob(x), blob(dy, (dy.shape[0], O, 1, 1))
+    bw, bm, bb = _wblob(w), _wblob(mom), _wblob(w_bf16)
+    bdb = blob(db) if db is not None else None
+    call("caffe_ip_backward_weight_sgd", ctypes.byref(bx), ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(bm),
+         ctypes.byref(bb), _bp(bdb), float(lr), float(momentum), float(decay), float(grad_scale), ws, wsz, _stream())
+    return w
+
+
+def ip_backward_data_relu(dy, w, relu_top, math="bf16", out=None):
+    """dX = [relu_top > 0] * (dY W): the data gradient through the ReLU whose output is this layer's
+    bottom (S:190 with S:208 folded in)."""
+    torch = _t()
+    if out is None:
+        out = torch.empty_like(relu_top)
+    ws, wsz = _ip_ws(math, tuple(relu_top.shape), w.shape[0], 1)
+    bdy, bw, br, bdx = blob(dy, (dy.shape[0], w.shape[0], 1, 1)), _wblob(w), blob(relu_top), blob(out)
+    call("caffe_ip_backward_data_relu", MATH[math], ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(br),
+         ctypes.byref(bdx), ws, wsz, _stream())
+    return out
+
+
 def ip_backward_weight(x, dy, w_shape, math="bf16", beta=0.0, dw=None, db=None, bias=True, ws=None):
     torch = _t()
     O = w_shape[0]

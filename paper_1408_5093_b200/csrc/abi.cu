@@ -1411,8 +1411,33 @@ caffe_status caffe_ip_forward(caffe_math math, uint32_t flags, const caffe_blob*
     return CAFFE_OK;
 }
 
+static caffe_status ip_bwd_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
+                                const caffe_blob* relu_top, caffe_blob* bottom_diff, float beta, void* ws, size_t ws_bytes,
+                                caffe_stream_t stream);
+
 caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
                                     caffe_blob* bottom_diff, float beta, void* ws, size_t ws_bytes, caffe_stream_t stream) {
+    return ip_bwd_data(math, top_diff, weight, nullptr, bottom_diff, beta, ws, ws_bytes, stream);
+}
+
+caffe_status caffe_ip_backward_data_relu(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
+                                         const caffe_blob* relu_top, caffe_blob* bottom_diff, void* ws, size_t ws_bytes,
+                                         caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(relu_top, "relu_top"))) return st;
+    if ((st = check_blob(bottom_diff, "bottom_diff"))) return st;
+    if (!same_shape(relu_top->shape, bottom_diff->shape))
+        return fail(CAFFE_E_SHAPE, "relu_top shape (%d,%d,%d,%d) != bottom_diff shape (%d,%d,%d,%d)", relu_top->shape.n,
+                    relu_top->shape.c, relu_top->shape.h, relu_top->shape.w, bottom_diff->shape.n, bottom_diff->shape.c,
+                    bottom_diff->shape.h, bottom_diff->shape.w);
+    if (nhwc(relu_top) != nhwc(bottom_diff)) return fail(CAFFE_E_INVALID, "relu_top and bottom_diff layouts differ");
+    if (overlap(bottom_diff, relu_top)) return fail(CAFFE_E_ALIAS, "bottom_diff overlaps relu_top");
+    return ip_bwd_data(math, top_diff, weight, relu_top, bottom_diff, 0.f, ws, ws_bytes, stream);
+}
+
+static caffe_status ip_bwd_data(caffe_math math, const caffe_blob* top_diff, const caffe_blob* weight,
+                                const caffe_blob* relu_top, caffe_blob* bottom_diff, float beta, void* ws, size_t ws_bytes,
+                                caffe_stream_t stream) {
     caffe_status st;
     if ((st = check_blob(top_diff, "top_diff")) || (st = check_blob(weight, "weight")) ||
         (st = check_blob(bottom_diff, "bottom_diff")))
@@ -1435,6 +1460,10 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
         CK(fp32_conv_dgrad(top_diff->ptr, isbf(top_diff), ly, weight->ptr, isbf(weight), bottom_diff->ptr,
                            isbf(bottom_diff), nhwc(bottom_diff), beta, g, s, math == CAFFE_MATH_TF32),
            "ip dgrad fp32");
+        if (relu_top)
+            CK(relu_bwd(relu_top->ptr, bottom_diff->ptr, bottom_diff->ptr, isbf(relu_top), isbf(bottom_diff),
+                        (int)((long long)N * K), s),
+               "relu backward");
         return CAFFE_OK;
     }
     size_t need;
@@ -1468,15 +1497,37 @@ caffe_status caffe_ip_backward_data(caffe_math math, const caffe_blob* top_diff,
         a.out = bottom_diff->ptr; a.out_bf16 = isbf(bottom_diff); a.beta = beta;
     }
     a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1;
+    // ReLU backward folded in (beta is 0 then): in the split-K reduce (row-major output), in the
+    // tensor-core epilogue (direct output), else by a separate in-place pass
+    bool masked = false;
+    if (relu_top && !part && !rows) {
+        a.relu_top = relu_top->ptr; a.relu_top_bf16 = isbf(relu_top);
+        masked = true;
+    }
     finish_args(a, a.b_nchunks / q.cg * 64 * 128);
-    if (!part) enable_tma_store(L, a.out, a.out_bf16 ? 2 : 4, K, N, K, true);
+    if (!part && (!masked || (a.out_bf16 && a.relu_top_bf16 && K % 64 == 0)))
+        enable_tma_store(L, a.out, a.out_bf16 ? 2 : 4, K, N, K, true);
     if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
-    if (part)
-        CK(gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128 * q.cg, N, (int)K, bottom_diff->ptr,
-                               isbf(bottom_diff), K, nullptr, 0, beta, permute ? xs.c : 0, xs.h * xs.w, s),
-           "ip dgrad split-K reduce");
-    else if (rows)
+    if (part) {
+        const bool mred = relu_top && !permute;
+        cudaError_t e = gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128 * q.cg, N, (int)K,
+                                            bottom_diff->ptr, isbf(bottom_diff), K, nullptr, 0, beta, permute ? xs.c : 0,
+                                            xs.h * xs.w, s, mred ? relu_top->ptr : nullptr, mred ? isbf(relu_top) : 0);
+        if (e == cudaErrorNotSupported && mred) {   // no masked form for this layout: plain reduce + ReLU pass
+            e = gemm_partial_reduce(part, q.splits, q.m_tiles, q.n_tiles, q.BN, 128 * q.cg, N, (int)K, bottom_diff->ptr,
+                                    isbf(bottom_diff), K, nullptr, 0, beta, 0, xs.h * xs.w, s);
+            if (e == cudaSuccess) masked = false;
+        } else if (mred) {
+            masked = true;
+        }
+        CK(e, "ip dgrad split-K reduce");
+    } else if (rows) {
         CK(rows_to_nhwc(rows, K, bottom_diff->ptr, isbf(bottom_diff), N, xs.c, xs.h * xs.w, beta, s), "ip dgrad to NHWC");
+    }
+    if (relu_top && !masked)
+        CK(relu_bwd(relu_top->ptr, bottom_diff->ptr, bottom_diff->ptr, isbf(relu_top), isbf(bottom_diff),
+                    (int)((long long)N * K), s),
+           "relu backward");
     return CAFFE_OK;
 }
 
@@ -1544,6 +1595,73 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
     finish_args(a, a.b_nchunks / L.cg * 64 * 128);
     enable_tma_store(L, weight_diff->ptr, 4, K, O, K, true);
+    return run_tc(L, s, 2.0 * N * O * (double)K, 1);
+}
+
+caffe_status caffe_ip_backward_weight_sgd(const caffe_blob* bottom, const caffe_blob* top_diff, caffe_blob* weight,
+                                          caffe_blob* momentum, caffe_blob* weight_bf16, caffe_blob* bias_diff, float lr,
+                                          float mom, float decay, float grad_scale, void* ws, size_t ws_bytes,
+                                          caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom, "bottom")) || (st = check_blob(top_diff, "top_diff")) ||
+        (st = check_blob(weight, "weight")) || (st = check_blob(momentum, "momentum")) ||
+        (st = check_blob(weight_bf16, "weight_bf16")))
+        return st;
+    long long K; int O;
+    if ((st = ip_shapes(bottom, weight, &K, &O))) return st;
+    const int N = bottom->shape.n;
+    if (top_diff->shape.n != N || top_diff->shape.c != O || top_diff->shape.h != 1 || top_diff->shape.w != 1)
+        return fail(CAFFE_E_SHAPE, "top_diff must be (%d,%d,1,1)", N, O);
+    if (weight->dtype != CAFFE_F32 || momentum->dtype != CAFFE_F32 || weight_bf16->dtype != CAFFE_BF16)
+        return fail(CAFFE_E_DTYPE, "weight and momentum must be F32, weight_bf16 BF16");
+    if (!same_shape(momentum->shape, weight->shape) || !same_shape(weight_bf16->shape, weight->shape))
+        return fail(CAFFE_E_SHAPE, "momentum and weight_bf16 must have the weight's shape");
+    if (nhwc(weight) || nhwc(momentum) || nhwc(weight_bf16)) return fail(CAFFE_E_INVALID, "weights must be row-major (O, K)");
+    if (K % 32 != 0 || !aligned16(weight->ptr) || !aligned16(momentum->ptr) || !aligned16(weight_bf16->ptr))
+        return fail(CAFFE_E_ALIGN, "fused update needs K %% 32 == 0 and 16-byte aligned weights (K = %lld)", K);
+    if (bias_diff) {
+        if ((st = check_blob(bias_diff, "bias_diff"))) return st;
+        if (bias_diff->dtype != CAFFE_F32 || cnt(bias_diff->shape) != O) return fail(CAFFE_E_SHAPE, "bias_diff must be F32 with %d elements", O);
+    }
+    if (overlap(weight, bottom) || overlap(weight, top_diff) || overlap(momentum, weight) || overlap(weight_bf16, weight) ||
+        overlap(weight_bf16, momentum) || overlap(weight_bf16, bottom) || overlap(weight_bf16, top_diff))
+        return fail(CAFFE_E_ALIAS, "weight / momentum / weight_bf16 overlap each other or an input");
+    if (N == 0) return CAFFE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t need;
+    caffe_ip_workspace_size(CAFFE_MATH_BF16, bottom->shape, O, CAFFE_PASS_BACKWARD_WEIGHT, &need);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    char* cur = (char*)ws;
+    float* bpart = (float*)cur;
+    cur += align1k((size_t)bias_grad_splits(N, O, 1) * O * 4);
+    if (bias_diff) CK(bias_grad(top_diff->ptr, isbf(top_diff), 1, (float*)bias_diff->ptr, 0.f, N, O, 1, bpart, s), "ip bias grad");
+    const int E = 2;
+    const void *A, *B;
+    long long lda, ldb;
+    CK(stage_rows(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
+    CK(stage_rows(bottom, N, K, E, cur, &B, &ldb, s), "stage bottom");
+    TcLaunch L;
+    memset(&L, 0, sizeof L);
+    L.esz = E; L.amode = A_TILED_MN; L.bmode = B_TILED_MN; L.epi = EPI_STRIDED;
+    TcArgs& a = L.args;
+    a.BN = choose_bn((int)(K < 256 ? K : 256));
+    L.cg = (O > 128 && a.BN % 128 == 0 && g_force_cg != 1) ? 2 : 1;
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, 64, 64))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip wgrad sgd)");
+    a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128 * L.cg); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1;
+    a.splits = 1;
+    a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
+    a.out = weight->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = 0.f;
+    a.sgd = 1; a.sgd_v = (float*)momentum->ptr;
+    a.sgd_lr = lr; a.sgd_mom = mom; a.sgd_decay = decay; a.sgd_gs = grad_scale;
+    finish_args(a, a.b_nchunks / L.cg * 64 * 128);
+    if (!encode_store_2d(&L.mapC, 4, weight->ptr, K, O, K) || !encode_store_2d(&L.mapV, 4, momentum->ptr, K, O, K) ||
+        !encode_store_2d_bf16_32(&L.mapWb, weight_bf16->ptr, K, O, K))
+        return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (fused update stores)");
+    a.tma_store = 1;
+    // stages: the SGD staging (80 KB) leaves ~130 KB for the operand ring
+    const int stage = (a.macc > 1 ? a.macc : 1) * 16384 + a.b_stage_bytes;
+    a.stages = std::max(2, std::min(a.stages, (227 * 1024 - 80 * 1024 - 8 * 1024) / stage));
     return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }
 

@@ -301,6 +301,70 @@ __device__ __forceinline__ void epi_store_tma(const TcArgs& args, const CUtensor
     }
 }
 
+// Fused SGD form (inner-product weight gradient, caffe_ip_backward_weight_sgd): the accumulator
+// is dW for this warp's 32 weight rows; each lane reads its row's W and momentum (32 FP32 columns,
+// full 128-byte lines), applies sgd1 (the update kernel's arithmetic, bit for bit), and stages W, v
+// (128-byte swizzle) and the BF16 copy (64-byte swizzle) for three tensor stores -- dW itself never
+// reaches memory.  Two 10 KB buffers per warp keep one store group in flight.  Host guarantees:
+// beta 0, N a multiple of 32, FP32 W/v rows 16-byte aligned.
+__device__ __forceinline__ void epi_sgd_tma(const TcArgs& args, const CUtensorMap* mapW, const CUtensorMap* mapV,
+                                            const CUtensorMap* mapWb, uint32_t taddr, int row0, int col0, int ccol,
+                                            uint8_t* stage, int& buf, int lane) {
+    const int m = row0 + lane;
+    const bool row_ok = m < args.M;
+    const float* wrow = reinterpret_cast<const float*>(args.out) + (long long)(row_ok ? m : 0) * args.s_n + ccol;
+    const float* vrow = args.sgd_v + (long long)(row_ok ? m : 0) * args.s_n + ccol;
+    const float lr = args.sgd_lr, mom = args.sgd_mom, decay = args.sgd_decay, gs = args.sgd_gs;
+    for (int c0 = 0; c0 < args.BN; c0 += 32) {
+        if (col0 + c0 >= args.N) break;   // warp-uniform
+        uint32_t g[32];
+        tmem_ld16(taddr + c0, *reinterpret_cast<uint32_t(*)[16]>(&g[0]));
+        tmem_ld16(taddr + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&g[16]));
+        float w[32], v[32];
+        {
+            const float4* w4 = reinterpret_cast<const float4*>(wrow + c0);
+            const float4* v4 = reinterpret_cast<const float4*>(vrow + c0);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const float4 a = w4[q], b = v4[q];
+                w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+                v[4 * q] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
+            }
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; j++) sgd1(w[j], __uint_as_float(g[j]), v[j], lr, mom, decay, gs);
+        if (lane == 0) tma_store_wait_read1();
+        __syncwarp();
+        uint8_t* st = stage + buf * 10240;
+        const int sw = lane & 7, sw64 = (lane >> 1) & 3;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            *reinterpret_cast<float4*>(st + lane * 128 + ((j ^ sw) << 4)) =
+                make_float4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+            *reinterpret_cast<float4*>(st + 4096 + lane * 128 + ((j ^ sw) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            uint4 pk;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; e++) h2[e] = __floats2bfloat162_rn(w[8 * j + 2 * e], w[8 * j + 2 * e + 1]);
+            *reinterpret_cast<uint4*>(st + 8192 + lane * 64 + ((j ^ sw64) << 4)) = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(mapW, st, ccol + c0, row0);
+            tma_store_2d(mapV, st + 4096, ccol + c0, row0);
+            tma_store_2d(mapWb, st + 8192, ccol + c0, row0);
+            tma_store_commit();
+        }
+        buf ^= 1;
+    }
+}
+
 // Row-staged form for channels-last BF16 outputs (s_c == 1, beta == 0, BN*2 <= 256 bytes): each
 // warp stages its 32 rows x BN columns -- a whole row segment per lane, pitch padded to an odd
 // number of 16-byte chunks so the staging writes are bank-conflict-free -- then writes the 32

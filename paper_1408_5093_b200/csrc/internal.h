@@ -79,10 +79,17 @@ struct TcArgs {
     // regardless of image boundaries.  A tile's window is staged as stk_nb one-row TMA boxes placed
     // so that the tile's first pixel lands at shared-memory row stk_off in every CTA.
     int stk, stk_wt, stk_hs, stk_nimg, stk_nb, stk_off;
+    // EPI_STRIDED + tma_store, inner-product weight gradient with the SGD update fused in
+    // (caffe_ip_backward_weight_sgd): out = the FP32 master weights W (read and rewritten),
+    // sgd_v = momentum (same layout), mapC / mapV / mapWb store W, v and the BF16 copy
+    int sgd;
+    float* sgd_v;
+    float sgd_lr, sgd_mom, sgd_decay, sgd_gs;
 };
 
 struct TcLaunch {
     CUtensorMap mapA, mapB, mapC;
+    CUtensorMap mapV, mapWb;            // fused SGD epilogue: momentum and BF16-weight stores
     TcArgs args;
     int esz;                            // 2 = bf16 (kind::f16), 4 = fp32 (kind::tf32)
     int amode, bmode, epi;
@@ -108,6 +115,8 @@ bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, 
 // row-major output matrix [rows][cols] (row pitch = ld elements) for TMA stores: box (128 B of
 // columns, 32 rows), 128-byte swizzle
 bool encode_store_2d(CUtensorMap* m, int esz, const void* base, uint64_t cols, uint64_t rows, uint64_t ld);
+// row-major BF16 matrix, box (32 columns = 64 bytes, 32 rows), 64-byte swizzle (fused SGD: BF16 weights)
+bool encode_store_2d_bf16_32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld);
 bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, uint32_t box_c,
                      uint32_t box_w, uint32_t box_h);
 // channels-last output [N][H][W][C] (pixel stride s_p, image stride s_n elements) for TMA stores:
@@ -160,7 +169,7 @@ cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeo
 // columns into an NHWC row of pC channels x pHW pixels.
 cudaError_t gemm_partial_reduce(const float* part, int splits, int m_tiles, int n_tiles, int BN, int TM, int M, int N,
                                 void* out, int out_bf16, long long ldo, const float* bias, int relu, float beta, int pC,
-                                int pHW, cudaStream_t s);
+                                int pHW, cudaStream_t s, const void* mref = nullptr, int mref_bf16 = 0);
 // Generic 2-D convert/pad: dst[r][c] (ld_dst, esz) = src[r][c] (ld_src, f32|bf16) for c < cols, 0 up to ld_dst.
 cudaError_t convert_pad_2d(const void* src, int src_bf16, long long ld_src, void* dst, int dst_esz,
                            long long ld_dst, long long rows, long long cols, cudaStream_t s);

@@ -719,7 +719,8 @@ __global__ void gemm_partial_reduce_kernel(const float* __restrict__ part, int s
 // row-major output): 8 coalesced partial loads per split, one 16-byte (bf16) / 32-byte (fp32) store.
 __global__ void gemm_partial_reduce8_kernel(const float* __restrict__ part, int splits, int m_tiles, int n_tiles, int BN,
                                             int TM, int M, int N, void* __restrict__ out, int obf16, long long ldo,
-                                            const float* __restrict__ bias, int relu, float beta, long long total) {
+                                            const float* __restrict__ bias, int relu, float beta, long long total,
+                                            const void* __restrict__ mref, int mref_bf16) {
     const long long sstride = (long long)m_tiles * n_tiles * BN * TM;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
@@ -741,6 +742,14 @@ __global__ void gemm_partial_reduce8_kernel(const float* __restrict__ part, int 
             for (int e = 0; e < 8; e++) acc[e] += bias[n0 + e];
         }
         const long long o = (long long)m * ldo + n0;
+        if (mref) {   // the backward of the ReLU whose output (same layout as out) is mref
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const float r = mref_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(mref)[o + e])
+                                          : reinterpret_cast<const float*>(mref)[o + e];
+                acc[e] = r > 0.f ? acc[e] : 0.f;
+            }
+        }
         if (obf16) {
             uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o);
             if (beta != 0.f) {
@@ -832,16 +841,17 @@ __global__ void gemm_partial_reduce_nhwc8_kernel(const float* __restrict__ part,
 
 cudaError_t gemm_partial_reduce(const float* part, int splits, int m_tiles, int n_tiles, int BN, int TM, int M, int N,
                                 void* out, int out_bf16, long long ldo, const float* bias, int relu, float beta, int pC,
-                                int pHW, cudaStream_t s) {
+                                int pHW, cudaStream_t s, const void* mref, int mref_bf16) {
     const long long total = (long long)M * N;
     const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     if (pC == 0 && BN % 8 == 0 && N % 8 == 0 && ldo % 8 == 0 && al) {
         gemm_partial_reduce8_kernel<<<blocks_for(total / 8, 256), 256, 0, s>>>(part, splits, m_tiles, n_tiles, BN, TM, M, N,
                                                                                out, out_bf16, ldo, bias, relu, beta,
-                                                                               total / 8);
+                                                                               total / 8, mref, mref_bf16);
         note_launch();
         return cudaGetLastError();
     }
+    if (mref) return cudaErrorNotSupported;   // the caller falls back to a separate ReLU-backward pass
     if (pC > 0 && pC % 8 == 0 && !bias && !relu && al && ldo % 8 == 0 && total / 8 < (1LL << 31)) {
         const int tv = (int)(total / 8);
         gemm_partial_reduce_nhwc8_kernel<<<blocks_for(tv, 256), 256, 0, s>>>(part, splits, m_tiles, n_tiles, BN, TM, M,

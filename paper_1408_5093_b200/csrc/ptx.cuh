@@ -141,6 +141,14 @@ __device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* v) {
         : "r"(taddr)
         : "memory");
 }
+// One momentum-SGD step (R18 sign convention) with every rounding explicit, so the update
+// kernel and the fused weight-gradient epilogue produce the same bits:
+//   g' = g*gs + decay*w;  v = mom*v - lr*g';  w = w + v
+__device__ __forceinline__ void sgd1(float& w, float g, float& v, float lr, float mom, float decay, float gs) {
+    const float gd = __fmaf_rn(g, gs, __fmul_rn(decay, w));
+    v = __fmaf_rn(mom, v, -__fmul_rn(lr, gd));
+    w = __fadd_rn(w, v);
+}
 __device__ __forceinline__ float4 lds_f4(uint32_t saddr) {
     float4 r;
     asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(saddr));

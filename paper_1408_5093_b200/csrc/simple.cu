@@ -8,6 +8,7 @@
 // (L4), and threads walk the OUTPUT in its memory order so warps read/write consecutive addresses
 // in either NCHW or NHWC.  Index math is 32-bit (blobs < 2^31 elements, checked by the ABI).
 #include "internal.h"
+#include "ptx.cuh"
 #include <algorithm>
 
 #include <cuda_bf16.h>
@@ -1342,11 +1343,10 @@ cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, 
 // tensor-core kernel (the net overlaps each layer's update with the rest of the backward pass).
 __device__ __forceinline__ void sgd4(float4& wv, const float4& gv, float4& vv, float lr, float mom, float decay,
                                      float gs) {
-    vv.x = mom * vv.x - lr * (gv.x * gs + decay * wv.x);
-    vv.y = mom * vv.y - lr * (gv.y * gs + decay * wv.y);
-    vv.z = mom * vv.z - lr * (gv.z * gs + decay * wv.z);
-    vv.w = mom * vv.w - lr * (gv.w * gs + decay * wv.w);
-    wv.x += vv.x; wv.y += vv.y; wv.z += vv.z; wv.w += vv.w;
+    sgd1(wv.x, gv.x, vv.x, lr, mom, decay, gs);
+    sgd1(wv.y, gv.y, vv.y, lr, mom, decay, gs);
+    sgd1(wv.z, gv.z, vv.z, lr, mom, decay, gs);
+    sgd1(wv.w, gv.w, vv.w, lr, mom, decay, gs);
 }
 __device__ __forceinline__ uint2 bf16x4(const float4& wv) {
     __nv_bfloat162 a = __floats2bfloat162_rn(wv.x, wv.y), b = __floats2bfloat162_rn(wv.z, wv.w);
@@ -1388,9 +1388,8 @@ __global__ void __launch_bounds__(256, 5) sgd_kernel(float* __restrict__ w, cons
         if (wb) b4[t] = bf16x4(wa);
     }
     for (long long q = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += stride) {
-        const float wv = w[q];
-        const float vv = mom * v[q] - lr * (g[q] * gs + decay * wv);
-        const float nw = wv + vv;
+        float nw = w[q], vv = v[q];
+        sgd1(nw, g[q], vv, lr, mom, decay, gs);
         v[q] = vv;
         w[q] = nw;
         if (wb) wb[q] = __float2bfloat16_rn(nw);

@@ -33,17 +33,20 @@ constexpr int A_STAGE_BYTES = 16384;   // 128 rows x 128 B
 constexpr int SMEM_ALIGN = 1024;
 
 constexpr int EPI_STAGE_BYTES = 4 * 2 * 4096;   // TMA-store staging: 4 epilogue warps x 2 buffers
+constexpr int SGD_STAGE_BYTES = 4 * 2 * 10240;  // fused SGD: 4 warps x 2 buffers x (W 4 KB + v 4 KB + W_bf16 2 KB)
 constexpr int ROWS_STAGE_BYTES = 4 * 32 * 17 * 16;   // row-staged epilogue: 4 epilogue warps x 8.5 KB
 size_t tc_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
     return (size_t)a.stages * (macc * A_STAGE_BYTES + a.b_stage_bytes) + 256 /*barriers*/ + 2 * 256 * 4 /*bias*/ +
-           SMEM_ALIGN + 1024 + (a.tma_store ? EPI_STAGE_BYTES : 0) + (a.rows_epi ? ROWS_STAGE_BYTES : 0);
+           SMEM_ALIGN + 1024 + (a.tma_store ? (a.sgd ? SGD_STAGE_BYTES : EPI_STAGE_BYTES) : 0) +
+           (a.rows_epi ? ROWS_STAGE_BYTES : 0);
 }
 
 template <int ESZ, int AMODE, int BMODE, int EPI, int CG>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                   const __grid_constant__ CUtensorMap mapC, const TcArgs args) {
+                   const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapV,
+                   const __grid_constant__ CUtensorMap mapWb, const TcArgs args) {
     constexpr int CH = 128 / ESZ;          // elements per 128-byte row (= K per stage, = MN per chunk)
     constexpr int UMMA_K = 32 / ESZ;       // K per tcgen05.mma
     constexpr int KSTEPS = CH / UMMA_K;    // MMAs per stage (4)
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
     float* sbias = reinterpret_cast<float*>(smem + stages * stage_bytes + 256);   // [2][256]
     uint8_t* epi_stage = smem + ((stages * stage_bytes + 256 + 2048 + 1023) & ~1023);   // TMA-store buffers
-    uint8_t* rows_stage = epi_stage + (args.tma_store ? EPI_STAGE_BYTES : 0);            // row-staged epilogue
+    uint8_t* rows_stage = epi_stage + (args.tma_store ? (args.sgd ? SGD_STAGE_BYTES : EPI_STAGE_BYTES) : 0);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -310,7 +313,10 @@ __global__ void __launch_bounds__(256, 1)
                     for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
-                if (args.tma_store) {
+                if (args.sgd) {
+                    epi_sgd_tma(args, &mapC, &mapV, &mapWb, taddr, m_tile * TM + (int)rank * BM + q * 32, col0, cbase,
+                                epi_stage + q * 20480, tbuf, lane);
+                } else if (args.tma_store) {
                     epi_store_tma(args, &mapC, taddr, m_tile * TM + (int)rank * BM + q * 32, col0, cbase, bs,
                                   epi_stage + q * 8192, tbuf, lane);
                 } else if (args.rows_epi) {
@@ -355,7 +361,7 @@ static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (CG == 1) {
-        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.mapC, L.args);
+        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.mapC, L.mapV, L.mapWb, L.args);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(L.grid);
@@ -369,7 +375,7 @@ static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.mapC, L.args);
+        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.mapC, L.mapV, L.mapWb, L.args);
         if (e != cudaSuccess) return e;
     }
     note_launch();
@@ -464,6 +470,18 @@ bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, in
     CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                          const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool encode_store_2d_bf16_32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld) {
+    if (!resolve()) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }

@@ -124,7 +124,7 @@ class Net:
         self.grads = torch.zeros(total, dtype=f32, device=device)
         self.mom = torch.zeros(total, dtype=f32, device=device)
         self.params_bf16 = torch.zeros(total, dtype=torch.bfloat16, device=device)
-        self.W, self.B, self.dW, self.dB, self.Wq = {}, {}, {}, {}, {}
+        self.W, self.B, self.dW, self.dB, self.Wq, self.Mw = {}, {}, {}, {}, {}, {}
         host = np.zeros(total, np.float32)
         for k, ((i, ws, bs), (ow, nw, ob, nb)) in enumerate(zip(pspecs, offs)):
             L = layers[i]
@@ -136,8 +136,10 @@ class Net:
             self.dW[i] = self.grads[ow:ow + nw].view(ws)
             self.dB[i] = self.grads[ob:ob + nb]
             self.Wq[i] = self.params_bf16[ow:ow + nw].view(ws)
+            self.Mw[i] = self.mom[ow:ow + nw].view(ws)
         # gradient segments (layer index, offset, numel incl. bias) for the data-parallel buckets
         self.segments = [(i, ow, ob + nb - ow) for (i, _, _), (ow, nw, ob, nb) in zip(pspecs, offs)]
+        self.bias_seg = {i: (ob, nb) for (i, _, _), (ow, nw, ob, nb) in zip(pspecs, offs)}
         self.params.copy_(torch.from_numpy(host))
         self.params_bf16.copy_(self.params.to(torch.bfloat16))
         self.pspecs = pspecs
@@ -224,14 +226,19 @@ class Net:
         return self._ws_wgrad
 
     def _relu_into_dgrad(self, i):
-        """True when the ReLU backward of layer i-1 is folded into layer i's conv data gradient
-        (caffe_conv_backward_data_relu: conv3 -> relu3 -> conv4, conv4 -> relu4 -> conv5)."""
-        if i <= 0 or self.layers[i].kind != "conv":
+        """True when the ReLU backward of layer i-1 is folded into layer i's data gradient
+        (caffe_conv_backward_data_relu: conv3 -> relu3 -> conv4, conv4 -> relu4 -> conv5;
+        caffe_ip_backward_data_relu: fc6 -> relu6 -> fc7, fc7 -> relu7 -> fc8)."""
+        if i <= 0 or self.layers[i].kind not in ("conv", "ip"):
             return False
         P = self.layers[i - 1]
         return P.kind in ("conv", "ip") and P.relu
 
-    def backward(self, hook=None, done_hook=None, wgrad_stream=None):
+    def _sgd_fusable(self, i):
+        """caffe_ip_backward_weight_sgd applies: BF16 math, fan-in a multiple of 32 (TMA boxes)."""
+        return self.math == "bf16" and self.layers[i].kind == "ip" and self.W[i].shape[1] % 32 == 0
+
+    def backward(self, hook=None, done_hook=None, wgrad_stream=None, fused_sgd=None):
         """Backward in reverse; `hook(i)` is called after layer i's parameter gradients are enqueued
         (data-parallel bucketing point), `done_hook(i)` once nothing later in the step reads layer
         i's parameters (after its data gradient; after its weight gradient for the first layer).
@@ -270,6 +277,25 @@ class Net:
                                           beta=0.0, out=d[i])
                 if done_hook:
                     done_hook(i)
+            elif L.kind == "ip" and fused_sgd is not None and wgrad_stream is not None and self._sgd_fusable(i):
+                # one GPU: the weight update is fused into the weight-gradient GEMM; it rewrites the
+                # BF16 weights, so it follows this layer's data gradient
+                dy2 = dy.view(dy.shape[0], -1)
+                if i > 0 and self._relu_into_dgrad(i):
+                    cb.ip_backward_data_relu(dy2, self._wop(i), a[i], self.math, out=d[i])
+                elif i > 0:
+                    cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream())
+                wgrad_stream.wait_event(ev)
+                with torch.cuda.stream(wgrad_stream):
+                    cb.ip_backward_weight_sgd(a[i], dy2, self.W[i], self.Mw[i], self.Wq[i], fused_sgd["lr"],
+                                              fused_sgd["momentum"], fused_sgd["decay"], 1.0, db=self.dB[i],
+                                              ws=self._wgrad_workspace())
+                    self.wgrad_done[i] = torch.cuda.Event()
+                    self.wgrad_done[i].record(wgrad_stream)
+                if done_hook:
+                    done_hook(i)
             elif L.kind == "ip":
                 dy2 = dy.view(dy.shape[0], -1)
                 if wgrad_stream is not None:
@@ -286,7 +312,9 @@ class Net:
                                           db=self.dB[i])
                 if hook:
                     hook(i)
-                if i > 0:
+                if i > 0 and self._relu_into_dgrad(i):
+                    cb.ip_backward_data_relu(dy2, self._wop(i), a[i], self.math, out=d[i])
+                elif i > 0:
                     cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
                 if done_hook:
                     done_hook(i)
@@ -311,6 +339,9 @@ class Net:
     sgd_flush_layer = None
     # conv weight gradients (layers > 0) on their own stream, concurrent with the data gradients
     wgrad_side = True
+    # one GPU: the inner-product weight updates fused into their weight-gradient GEMMs
+    # (caffe_ip_backward_weight_sgd; the gradient never reaches memory)
+    fuse_ip_sgd = True
 
     def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4, overlap_update=True):
         self.forward()
@@ -338,13 +369,20 @@ class Net:
 
             launched = []
 
+            fused = dict(lr=lr, momentum=momentum, decay=decay) if (self.fuse_ip_sgd and wstream is not None) else None
+
             def launch():
                 launched.append(1)
-                # pending layers hold one contiguous range of the flat parameter buffer (backward order)
-                lo = min(seg[i][0] for i in pending)
-                hi = max(seg[i][0] + seg[i][1] for i in pending)
-                wev = [self.wgrad_done[i] for i in pending if i in getattr(self, "wgrad_done", {})]
+                # pending (layer, lo, hi) ranges of the flat parameter buffer; adjacent ones are merged
+                wev = [self.wgrad_done[i] for i, _, _ in pending if i in getattr(self, "wgrad_done", {})]
+                rng = sorted((lo, hi) for _, lo, hi in pending)
                 pending.clear()
+                runs = []
+                for lo, hi in rng:
+                    if runs and runs[-1][1] >= lo - 64:   # 256-byte alignment padding between tensors
+                        runs[-1][1] = max(runs[-1][1], hi)
+                    else:
+                        runs.append([lo, hi])
                 ev = torch.cuda.Event()
                 ev.record(main)
                 self._side.wait_event(ev)
@@ -353,18 +391,24 @@ class Net:
                 # one 256-thread block per SM: leaves registers / thread slots for the main stream
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_BLOCKS_PER_SM, self.side_sgd_blocks)
                 with torch.cuda.stream(self._side):
-                    cb.sgd_update(self.params[lo:hi], self.grads[lo:hi], self.mom[lo:hi], lr,
-                                  momentum, decay, 1.0, w_bf16=wb[lo:hi] if wb is not None else None)
+                    for lo, hi in runs:
+                        cb.sgd_update(self.params[lo:hi], self.grads[lo:hi], self.mom[lo:hi], lr,
+                                      momentum, decay, 1.0, w_bf16=wb[lo:hi] if wb is not None else None)
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_BLOCKS_PER_SM, 0)
 
             def done(i):
                 if getattr(self, "skip_update", False):
                     return
-                pending.append(i)
+                if fused is not None and self._sgd_fusable(i):
+                    ob, nb = self.bias_seg[i]          # weights already updated by the fused pass
+                    pending.append((i, ob, ob + nb))
+                else:
+                    off, n = seg[i]
+                    pending.append((i, off, off + n))
                 if i <= flush_at:
                     launch()
 
-            self.backward(done_hook=done, wgrad_stream=wstream)
+            self.backward(done_hook=done, wgrad_stream=wstream, fused_sgd=fused)
             if pending:
                 launch()
             if launched:

@@ -328,3 +328,76 @@ def test_maxpool_u8_window_local_mask(oracle, case, layout):
     if layout == "nhwc_bf16":
         refr = oracle.quant_bf16(refr)
     np.testing.assert_array_equal(host(dXr), refr)
+
+
+@pytest.mark.parametrize("N,K,O,math,act,nhwc", [
+    (256, 4096, 4096, "bf16", "bf16", False),   # fc7 shape: split-K, masked in the reduce
+    (256, 4096, 1000, "bf16", "bf16", False),   # fc8 shape
+    (8, 96, 40, "bf16", "bf16", False),         # small: direct tensor-core epilogue
+    (8, 96, 40, "bf16", "f32", False),          # FP32 output: strided epilogue
+    (6, 64, 20, "fp32", "f32", False),          # CUDA-core math: separate ReLU pass
+    (4, 32, 24, "bf16", "bf16", True),          # NHWC (C,H,W) bottom: permuted output, separate pass
+], ids=["fc7", "fc8", "small", "f32out", "fp32math", "nhwc"])
+def test_ip_backward_data_relu(oracle, N, K, O, math, act, nhwc):
+    """caffe_ip_backward_data_relu (S:190 + S:208) gives exactly the bits of caffe_ip_backward_data
+    followed by the ReLU backward on every reduction / epilogue path, and matches the oracle."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    dt = torch.bfloat16 if act == "bf16" else torch.float32
+    shape = (N, K // 8, 2, 4) if nhwc else (N, K)
+    top = cuda(synth.uniform(shape, 81, synth.S_X)).to(dt).relu_()
+    if nhwc:
+        top = top.contiguous(memory_format=torch.channels_last)
+    dY = cuda(synth.uniform((N, O), 81, synth.S_DY)).to(dt)
+    Wt = cuda(synth.xavier((O, K), 81)).to(torch.bfloat16 if math == "bf16" else torch.float32)
+    ref = torch.empty_like(top)
+    cb.ip_backward_data(dY, Wt, tuple(top.shape), math=math, out=ref)
+    cb.relu_backward(top, ref, inplace=True)
+    got = cb.ip_backward_data_relu(dY, Wt, top, math=math)
+    np.testing.assert_array_equal(host(got), host(ref))
+    want = (host(dY).astype(np.float64) @ host(Wt).astype(np.float64)).reshape(N, -1)
+    mask = host(top).reshape(N, -1) > 0 if not nhwc else (host(top) > 0).reshape(N, -1)
+    g = host(got).reshape(N, -1)
+    assert_tc_close(g, want * mask, "masked ip dgrad", tol=5e-3)
+    with pytest.raises(RuntimeError):
+        cb.ip_backward_data_relu(dY, Wt, top[:1], math=math)
+
+
+@pytest.mark.parametrize("N,bshape,O", [
+    (256, (256, 4096), 1000),            # fc8: ragged output rows (1000 of 1024)
+    (256, (256, 256, 6, 6), 512),        # fc6-like: channels-last (C,H,W) bottom, permuted staging
+    (64, (64, 96), 40),                  # small, single-CTA tiles
+], ids=["fc8", "fc6like", "small"])
+def test_ip_backward_weight_sgd_fused(oracle, N, bshape, O):
+    """caffe_ip_backward_weight_sgd (weight gradient consumed by the SGD step in the GEMM epilogue)
+    leaves exactly the bits of caffe_ip_backward_weight + caffe_sgd_update in W, the momentum and
+    the BF16 copy, writes the same bias gradient, and the update matches the oracle's SGD step."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    x = cuda(synth.uniform(bshape, 91, synth.S_X)).to(torch.bfloat16)
+    if len(bshape) == 4:
+        x = x.contiguous(memory_format=torch.channels_last)
+    K = int(np.prod(bshape[1:]))
+    dy = cuda(synth.uniform((N, O), 91, synth.S_DY)).to(torch.bfloat16)
+    W0 = cuda(synth.xavier((O, K), 91))
+    V0 = cuda(synth.uniform((O, K), 92, synth.S_AUX)) * 0.01
+    lr, mom, decay, gs = 0.01, 0.9, 5e-4, 0.5
+    # reference: separate gradient + update kernels
+    Wr, Vr = W0.clone(), V0.clone()
+    Br = torch.empty((O, K), device="cuda", dtype=torch.bfloat16)
+    dW, db_r = cb.ip_backward_weight(x, dy, (O, K), beta=0.0)
+    cb.sgd_update(Wr, dW, Vr, lr, mom, decay, gs, w_bf16=Br)
+    # fused
+    Wf, Vf = W0.clone(), V0.clone()
+    Bf = torch.empty((O, K), device="cuda", dtype=torch.bfloat16)
+    db_f = torch.empty((O,), device="cuda")
+    cb.ip_backward_weight_sgd(x, dy, Wf, Vf, Bf, lr, mom, decay, gs, db=db_f)
+    np.testing.assert_array_equal(host(Wf), host(Wr))
+    np.testing.assert_array_equal(host(Vf), host(Vr))
+    np.testing.assert_array_equal(host(Bf), host(Br))
+    np.testing.assert_array_equal(host(db_f), host(db_r))
+    # and the step itself against the oracle's SGD on the oracle's gradient (S:523)
+    xr = host(x).astype(np.float64).reshape(N, -1)
+    g = host(dy).astype(np.float64).T @ xr
+    w_o, v_o = oracle.sgd_update(host(W0).astype(np.float64), g, host(V0).astype(np.float64), lr, mom, decay, gs)
+    assert_tc_close(host(Wf) - host(W0), w_o - host(W0), "fused update step", tol=2e-3)
