@@ -1652,6 +1652,7 @@ caffe_status caffe_ip_backward_weight_sgd(const caffe_blob* bottom, const caffe_
     a.splits = 1;
     a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
     a.out = weight->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = 0.f;
+    L.epi = EPI_SGD;
     a.sgd = 1; a.sgd_v = (float*)momentum->ptr;
     a.sgd_lr = lr; a.sgd_mom = mom; a.sgd_decay = decay; a.sgd_gs = grad_scale;
     finish_args(a, a.b_nchunks / L.cg * 64 * 128);

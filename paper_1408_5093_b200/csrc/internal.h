@@ -12,7 +12,7 @@ namespace cb {
 // tcgen05.mma (M=128, N=BN, K=16 bf16 / 8 tf32) accumulating FP32 in TMEM.
 enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3, A_HALO_K = 4, A_HALO_MN = 5 };
 enum BMode { B_TILED_K = 0, B_TILED_MN = 1 };
-enum EpiMode { EPI_STRIDED = 0, EPI_PARTIAL = 1 };
+enum EpiMode { EPI_STRIDED = 0, EPI_PARTIAL = 1, EPI_SGD = 2 /* fused inner-product update (its own instance) */ };
 
 struct TcArgs {
     int M, N, BN;                       // valid rows, valid cols (per group), N tile

@@ -743,11 +743,17 @@ __global__ void gemm_partial_reduce8_kernel(const float* __restrict__ part, int 
         }
         const long long o = (long long)m * ldo + n0;
         if (mref) {   // the backward of the ReLU whose output (same layout as out) is mref
+            if (mref_bf16) {   // 8 BF16 values, one 16-byte load (o is a multiple of 8)
+                const uint4 rv = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(mref) + o);
+                const uint32_t w4[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
-                const float r = mref_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(mref)[o + e])
-                                          : reinterpret_cast<const float*>(mref)[o + e];
-                acc[e] = r > 0.f ? acc[e] : 0.f;
+                for (int e = 0; e < 8; e++) {
+                    const uint16_t h = (uint16_t)(w4[e >> 1] >> ((e & 1) * 16));
+                    acc[e] = ((h & 0x8000u) == 0 && (h & 0x7fffu) != 0) ? acc[e] : 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[e] = reinterpret_cast<const float*>(mref)[o + e] > 0.f ? acc[e] : 0.f;
             }
         }
         if (obf16) {

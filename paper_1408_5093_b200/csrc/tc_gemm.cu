@@ -313,7 +313,9 @@ __global__ void __launch_bounds__(256, 1)
                     for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
-                if (args.sgd) {
+                // (the fused-update epilogue is its own template instance: its registers would
+                // otherwise stop the 48-register update kernel co-residing beside every GEMM CTA)
+                if constexpr (EPI == EPI_SGD) {
                     epi_sgd_tma(args, &mapC, &mapV, &mapWb, taddr, m_tile * TM + (int)rank * BM + q * 32, col0, cbase,
                                 epi_stage + q * 20480, tbuf, lane);
                 } else if (args.tma_store) {
@@ -398,6 +400,8 @@ cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s) {
     TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_PARTIAL, 2)
     TC_CASE(2, A_TILED_K, B_TILED_MN, EPI_STRIDED, 2)
     TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 2)
+    TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_SGD, 2)
+    TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_SGD, 1)
     TC_CASE(4, A_TILED_K, B_TILED_K, EPI_PARTIAL, 1)
     TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 1)
     TC_CASE(4, A_IM2COL_K, B_TILED_K, EPI_STRIDED, 1)

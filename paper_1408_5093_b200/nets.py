@@ -231,6 +231,8 @@ class Net:
         caffe_ip_backward_data_relu: fc6 -> relu6 -> fc7, fc7 -> relu7 -> fc8)."""
         if i <= 0 or self.layers[i].kind not in ("conv", "ip"):
             return False
+        if self.layers[i].kind == "ip" and not self.fuse_ip_relu:
+            return False
         P = self.layers[i - 1]
         return P.kind in ("conv", "ip") and P.relu
 
@@ -340,8 +342,12 @@ class Net:
     # conv weight gradients (layers > 0) on their own stream, concurrent with the data gradients
     wgrad_side = True
     # one GPU: the inner-product weight updates fused into their weight-gradient GEMMs
-    # (caffe_ip_backward_weight_sgd; the gradient never reaches memory)
-    fuse_ip_sgd = True
+    # (caffe_ip_backward_weight_sgd; the gradient never reaches memory).  Off by default: measured
+    # slower in the three-stream step (1.606 -> 1.691 ms/step) -- the fused fc6 pass is a persistent
+    # GEMM that holds every SM for ~210 us beside the conv backward, where the separate update
+    # kernel (one small block per SM) trickles alongside.
+    fuse_ip_sgd = False
+    fuse_ip_relu = True
 
     def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4, overlap_update=True):
         self.forward()

@@ -126,9 +126,12 @@ def test_net_teacher_forced(oracle, which, batch, act):
     assert np.isfinite(float(net.loss))
 
 
-def test_overlapped_update_matches_serial():
-    """Net.step(overlap_update=True) (per-layer SGD on a side stream) gives the same parameters,
-    bit for bit, as the single update after the backward pass."""
+@pytest.mark.parametrize("fuse", [False, True])
+def test_overlapped_update_matches_serial(fuse):
+    """Net.step(overlap_update=True) (per-layer SGD on a side stream, weight gradients on their own
+    stream; with fuse, the inner-product updates fused into their weight-gradient GEMMs where the
+    fan-in allows -- LeNet ip1) gives the same parameters, bit for bit, as the single update after
+    the backward pass."""
     import torch
     import synth
     from paper_1408_5093_b200 import nets
@@ -136,6 +139,7 @@ def test_overlapped_update_matches_serial():
     outs = []
     for overlap in (False, True):
         net = nets.Net(nets.LENET, 16, nets.LENET_INPUT, dev, math="bf16", seed=3)
+        net.fuse_ip_sgd = fuse
         net.a[0].copy_(torch.from_numpy(synth.mnist_pixels((16,) + tuple(nets.LENET_INPUT), 3)).to(torch.bfloat16))
         net.labels.copy_(torch.from_numpy(synth.labels(16, 10, 3)))
         for _ in range(2):

@@ -44,7 +44,8 @@ def main():
         net.side_sgd_blocks = p.get("blocks", 1)
         net.wgrad_side = bool(p.get("wside", 1))
         net.skip_update = bool(p.get("nosgd", 0))   # probe only: no parameter update (SGD cost)
-        net.fuse_ip_sgd = bool(p.get("fuse", 1))
+        net.fuse_ip_sgd = bool(p.get("fuse", 0))
+        net.fuse_ip_relu = bool(p.get("iprelu", 1))
         for _ in range(2):
             net.step()
         torch.cuda.synchronize()
