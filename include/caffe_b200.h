@@ -167,10 +167,10 @@ caffe_status caffe_device_check(void);
    writes it with 4-D TMA tensor stores; 0 (default) = per-thread 16-byte global stores (measured:
    equal for conv1, faster for conv2 whose B ring keeps more stages).  Bit-identical results. */
 #define CAFFE_TUNE_HALO_TMA_STORE 12
-/* CAFFE_TUNE_WGRAD_REDUCE_ROWS: 1 (default) = the split reduction of the halo weight gradients of
+/* CAFFE_TUNE_WGRAD_REDUCE_ROWS: 1 = the split reduction of the halo weight gradients of
    plain filters (fewer splits than CAFFE_TUNE_WGRAD_REDUCE_SG) runs one block per (filter row,
-   64-channel block) with a shared-memory gather and contiguous dW stores; 0 = one thread per
-   weight.  Bit-identical results (same summation order). */
+   64-channel block) with a shared-memory gather and contiguous dW stores; 0 (default) = one thread
+   per weight (measured slightly faster in the step).  Bit-identical results (same summation order). */
 #define CAFFE_TUNE_WGRAD_REDUCE_ROWS 13
 /* CAFFE_TUNE_HALO_STACKED: stacked halo tiles for same-size stride-1 convolutions (odd kernel, centred
    padding) on maps too small for whole-row halo tiles (CaffeNet conv3-5 forward and data

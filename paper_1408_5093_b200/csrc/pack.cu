@@ -645,7 +645,8 @@ __global__ void wgrad_reduce_rows_kernel(const float* __restrict__ partial, floa
         out[k] = (beta != 0.f ? beta * out[k] : 0.f) + rowbuf[k];
 }
 
-int g_wgrad_reduce_rows = 1;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS
+int g_wgrad_reduce_rows = 0;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS (off: 58.7 vs 52.6 us per step serialised, and its
+                               // 1024-thread blocks co-schedule worse beside the side-stream GEMMs)
 
 cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeom& g, int m_tiles, int n_tiles,
                          int splits, int BN, int chunk, int cblocks, cudaStream_t s, int cbmajor, float* db) {

@@ -448,7 +448,7 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
 @pytest.mark.parametrize("sg", [0, 2])
 def test_wgrad_reduce_rows_bit_identical(oracle, case, sg):
     """The per-(filter row, channel block) split reduction of the halo weight gradient
-    (CAFFE_TUNE_WGRAD_REDUCE_ROWS, default on) gives the bits of the one-thread-per-weight reduction
+    (CAFFE_TUNE_WGRAD_REDUCE_ROWS, default off) gives the bits of the one-thread-per-weight reduction
     (and leaves the split-range form, CAFFE_TUNE_WGRAD_REDUCE_SG lowered to 2, and space-to-depth
     filters to it), with beta = 0 and 1 and the bias gradient from the ones chunk; and matches the
     oracle."""
@@ -476,7 +476,7 @@ def test_wgrad_reduce_rows_bit_identical(oracle, case, sg):
                                                dw=prevW.clone(), db=prevb.clone())
             outs[rows] = [host(t) for t in (dW, db, dW1, db1)]
     finally:
-        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_REDUCE_ROWS, 1)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_REDUCE_ROWS, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_WGRAD_REDUCE_SG, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
     for a, b_ in zip(outs[0], outs[1]):

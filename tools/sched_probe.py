@@ -52,7 +52,7 @@ def main():
         graphs.append(net.capture())
         for k, v in p.items():   # restore library defaults (tuning is process-wide)
             if k.startswith("tune"):
-                _abi.call("caffe_set_tuning", int(k[4:]), 1 if int(k[4:]) in (5, 10, 11, 13) else 0)
+                _abi.call("caffe_set_tuning", int(k[4:]), 1 if int(k[4:]) in (5, 10, 11) else (1 if int(k[4:]) == 14 else 0))
     res = {c: [] for c in cfgs}
     rounds = int(os.environ.get("ROUNDS", "3"))
     for _ in range(rounds):
