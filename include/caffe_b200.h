@@ -67,7 +67,12 @@ typedef enum {
     CAFFE_E_ARCH = 9       /* device is not sm_100 */
 } caffe_status;
 
-typedef enum { CAFFE_F32 = 0, CAFFE_BF16 = 1, CAFFE_I32 = 2, CAFFE_U8 = 3 } caffe_dtype;
+typedef enum { CAFFE_F32 = 0, CAFFE_BF16 = 1, CAFFE_I32 = 2, CAFFE_U8 = 3, CAFFE_I8 = 4 } caffe_dtype;
+/* CAFFE_I8: signed 8-bit activations -- integer image data (e.g. mean-subtracted pixels in
+   [-128, 127], exact in BF16) accepted only as the bottom of caffe_conv_pack_bottom (channels-last,
+   BF16 math), which converts it exactly into the packed BF16 operand, and of the prepacked
+   caffe_conv_forward / caffe_conv_backward_weight calls that read that operand.  It halves the
+   host->device bytes of an input batch. */
 
 typedef enum { CAFFE_MATH_FP32 = 0, CAFFE_MATH_TF32 = 1, CAFFE_MATH_BF16 = 2 } caffe_math;
 

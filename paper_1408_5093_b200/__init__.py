@@ -51,6 +51,8 @@ def _dtype_code(t) -> int:
         return CAFFE_I32
     if t.dtype == torch.uint8:
         return _abi.CAFFE_U8
+    if t.dtype == torch.int8:
+        return _abi.CAFFE_I8
     raise TypeError(f"unsupported dtype {t.dtype}")
 
 

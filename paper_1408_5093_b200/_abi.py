@@ -15,7 +15,7 @@ CAFFE_OK, CAFFE_E_INVALID, CAFFE_E_SHAPE, CAFFE_E_PARAM, CAFFE_E_DTYPE = 0, 1, 2
 CAFFE_E_ALIGN, CAFFE_E_WORKSPACE, CAFFE_E_ALIAS, CAFFE_E_CUDA, CAFFE_E_ARCH = 5, 6, 7, 8, 9
 STATUS_NAMES = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_PARAM", 4: "E_DTYPE", 5: "E_ALIGN",
                 6: "E_WORKSPACE", 7: "E_ALIAS", 8: "E_CUDA", 9: "E_ARCH"}
-CAFFE_F32, CAFFE_BF16, CAFFE_I32, CAFFE_U8 = 0, 1, 2, 3
+CAFFE_F32, CAFFE_BF16, CAFFE_I32, CAFFE_U8, CAFFE_I8 = 0, 1, 2, 3, 4
 CAFFE_NCHW, CAFFE_NHWC = 0, 1
 CAFFE_MATH_FP32, CAFFE_MATH_TF32, CAFFE_MATH_BF16 = 0, 1, 2
 CAFFE_FUSE_RELU = 1

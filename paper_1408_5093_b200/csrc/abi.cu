@@ -721,9 +721,18 @@ caffe_status caffe_conv_workspace_size(const caffe_conv_desc* desc, caffe_shape4
 }
 
 static caffe_status conv_common(const caffe_conv_desc* desc, const caffe_blob* bottom_like, const caffe_blob* weight,
-                                Plan* p) {
+                                Plan* p, bool i8_ok = false) {
     caffe_status st;
-    if ((st = check_blob(bottom_like, "bottom"))) return st;
+    if (i8_ok && bottom_like && bottom_like->dtype == CAFFE_I8) {
+        // integer image input: channels-last, tensor-core math, packed by caffe_conv_pack_bottom
+        caffe_blob tmp = *bottom_like;
+        tmp.dtype = CAFFE_BF16;
+        if ((st = check_blob(&tmp, "bottom"))) return st;
+        if (!nhwc(bottom_like) || desc->math != CAFFE_MATH_BF16)
+            return fail(CAFFE_E_DTYPE, "I8 bottom needs channels-last layout and BF16 math");
+    } else if ((st = check_blob(bottom_like, "bottom"))) {
+        return st;
+    }
     if ((st = check_blob(weight, "weight"))) return st;
     if ((st = conv_validate(desc, bottom_like->shape, weight->shape.n, p))) return st;
     if (weight->shape.c != p->Cg || weight->shape.h != p->kh || weight->shape.w != p->kw)
@@ -737,13 +746,20 @@ static caffe_status conv_common(const caffe_conv_desc* desc, const caffe_blob* b
 caffe_status caffe_conv_pack_bottom(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
                                     void* ws, size_t ws_bytes, caffe_stream_t stream) {
     Plan p;
-    caffe_status st = conv_common(desc, bottom, weight, &p);
+    caffe_status st = conv_common(desc, bottom, weight, &p, true);
     if (st) return st;
     if (desc->math == CAFFE_MATH_FP32 || p.N == 0) return CAFFE_OK;
     const size_t need = std::max(conv_ws(p, CAFFE_PASS_FORWARD, desc->math),
                                  conv_ws(p, CAFFE_PASS_BACKWARD_WEIGHT, desc->math));
     if ((st = check_ws(ws, ws_bytes, need))) return st;
     Operand A = plan_x(bottom, p);
+    if (bottom->dtype == CAFFE_I8) {
+        if (!A.packed) A = Operand{nullptr, 0, 0, 0, 0, true, PackGeom{p.N, p.C, p.H, p.W, p.G, p.Cg, p.bh, p.bw, 0, 0,
+                                                                          p.H, p.W, round_ch(p.Cge, p.E),
+                                                                          p.G * round_ch(p.Cge, p.E)}};
+        CK(pack_act_i8(bottom->ptr, ws, A.pg, (cudaStream_t)stream), "pack I8 activations");
+        return CAFFE_OK;
+    }
     return pack_if(A, bottom, ws, p.E, (cudaStream_t)stream);
 }
 
@@ -751,7 +767,7 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
                                 const caffe_blob* bias, caffe_blob* top, void* ws, size_t ws_bytes,
                                 caffe_stream_t stream) {
     Plan p;
-    caffe_status st = conv_common(desc, bottom, weight, &p);
+    caffe_status st = conv_common(desc, bottom, weight, &p, desc && (desc->flags & CAFFE_BOTTOM_PREPACKED));
     if (st) return st;
     if ((st = check_blob(top, "top"))) return st;
     if (bias) {
@@ -957,7 +973,7 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
                                         float beta, void* ws, size_t ws_bytes, caffe_stream_t stream) {
     Plan p;
     caffe_status st;
-    if ((st = conv_common(desc, bottom, weight_diff, &p))) return st;
+    if ((st = conv_common(desc, bottom, weight_diff, &p, desc && (desc->flags & CAFFE_BOTTOM_PREPACKED)))) return st;
     if ((st = check_blob(top_diff, "top_diff"))) return st;
     if (weight_diff->dtype != CAFFE_F32) return fail(CAFFE_E_DTYPE, "weight_diff must be F32");
     caffe_shape4 want{p.N, p.O, p.OH, p.OW};

@@ -303,6 +303,76 @@ cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* d
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- I8 image input
+// Integer image batch (channels-last int8, e.g. mean-subtracted pixels) -> packed BF16 operand,
+// the same space-to-depth / channel-padding layout as pack_act (exact: |v| <= 128 is a BF16).
+// Segment form (one thread per (n, Y, X, dy): the sw*C contiguous bytes of one source row, L <= 16)
+// with the channel padding cleared by the dy = sh-1 thread; element form otherwise.
+__global__ void pack_i8_seg_kernel(const int8_t* __restrict__ src, __nv_bfloat16* __restrict__ dst, PackGeom g,
+                                   int total) {
+    const int L = g.sw * g.C;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int dy = t % g.sh;
+        int r = t / g.sh;
+        const int X = r % g.Wp; r /= g.Wp;
+        const int Y = r % g.Hp;
+        const int n = r / g.Hp;
+        const int h = Y * g.sh + dy;
+        const int nv = h < g.H ? max(0, min(L, (g.W - X * g.sw) * g.C)) : 0;   // valid elements
+        const int8_t* p = src + (((long long)n * g.H + h) * g.W + (long long)X * g.sw) * g.C;
+        uint32_t o[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const float a = 2 * i < nv ? (float)__ldg(p + 2 * i) : 0.f;
+            const float b = 2 * i + 1 < nv ? (float)__ldg(p + 2 * i + 1) : 0.f;
+            __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+            o[i] = *reinterpret_cast<uint32_t*>(&v);
+        }
+        __nv_bfloat16* q = dst + (((long long)n * g.Hp + Y) * g.Wp + X) * g.Ctot + dy * L;
+        uint32_t* q4 = reinterpret_cast<uint32_t*>(q);   // L even, q 4-byte aligned
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (2 * i < L) q4[i] = o[i];
+        if (dy == g.sh - 1) {
+            __nv_bfloat16* z = q + L;   // channels [sh*L, Ctot)
+            for (int c = 0; c < g.Ctot - g.sh * L; c += 2) *reinterpret_cast<uint32_t*>(z + c) = 0u;
+        }
+    }
+}
+__global__ void pack_i8_generic_kernel(const int8_t* __restrict__ src, __nv_bfloat16* __restrict__ dst, PackGeom g,
+                                       long long total) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(t % g.Ctot);
+        long long r = t / g.Ctot;
+        const int X = (int)(r % g.Wp); r /= g.Wp;
+        const int Y = (int)(r % g.Hp);
+        const long long n = r / g.Hp;
+        const int grp = c / g.cpg, cc = c - grp * g.cpg;
+        float v = 0.f;
+        if (grp < g.G && cc < g.Cg * g.sh * g.sw) {
+            const int d = cc / g.Cg, ch = cc - d * g.Cg;
+            const int h = Y * g.sh + d / g.sw - g.ph, w = X * g.sw + d % g.sw - g.pw;
+            if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = (float)src[((n * g.H + h) * g.W + w) * g.C + grp * g.Cg + ch];
+        }
+        dst[t] = __float2bfloat16_rn(v);
+    }
+}
+
+cudaError_t pack_act_i8(const void* src, void* dst, const PackGeom& g, cudaStream_t s) {
+    const int L = g.sw * g.C;
+    if (g.G == 1 && g.ph == 0 && g.pw == 0 && L <= 16 && L % 2 == 0 && g.cpg == g.Ctot && g.Ctot >= g.sh * L &&
+        (g.Ctot - g.sh * L) % 2 == 0 && g.Ctot % 2 == 0) {
+        const int total = g.N * g.Hp * g.Wp * g.sh;
+        pack_i8_seg_kernel<<<blocks_for(total, 256), 256, 0, s>>>((const int8_t*)src, (__nv_bfloat16*)dst, g, total);
+    } else {
+        const long long total = (long long)g.N * g.Hp * g.Wp * g.Ctot;
+        pack_i8_generic_kernel<<<blocks_for(total, 256), 256, 0, s>>>((const int8_t*)src, (__nv_bfloat16*)dst, g, total);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
 // Inverse of the s2d packing for the data gradient, into a blob of any layout (lx), with beta.
 __global__ void unpack_s2d_kernel(const float* __restrict__ T, void* __restrict__ dX, int dx_bf16, int xnhwc,
                                   float beta, PackGeom g, int total) {

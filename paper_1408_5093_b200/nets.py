@@ -80,7 +80,8 @@ def conv_flops(in_shape, L: Layer) -> Tuple[int, Tuple[int, int, int, int]]:
 
 
 class Net:
-    def __init__(self, layers: List[Layer], batch: int, input_shape, device, act_dtype=None, math="bf16", seed=0):
+    def __init__(self, layers: List[Layer], batch: int, input_shape, device, act_dtype=None, math="bf16", seed=0,
+                 input_i8=False):
         import torch
         import synth
         self.torch = torch
@@ -150,9 +151,13 @@ class Net:
         # without a transpose and pool/LRN use 16-byte channel vectors; the inner product flattens
         # its NHWC input in the (c,h,w) order of S:130 inside the library.
         self.nhwc = [L.kind != "loss" and len(self.shapes[i]) == 4 for i, L in enumerate(layers)]
+        # input_i8: the image batch is stored as int8 (integer pixels, e.g. mean-subtracted, exact in
+        # BF16) and converted by the first layer's pack (CAFFE_I8): half the input bytes
+        self.input_i8 = bool(input_i8 and math == "bf16" and layers[0].kind == "conv" and self.nhwc[0])
         for i, L in enumerate(layers):
             s = self.shapes[i]
-            self.a.append(cb.empty_like_layout(s, ad, device, nhwc=self.nhwc[i]))
+            dt0 = torch.int8 if (i == 0 and self.input_i8) else ad
+            self.a.append(cb.empty_like_layout(s, dt0, device, nhwc=self.nhwc[i]))
             self.d.append(cb.empty_like_layout(s, ad, device, nhwc=self.nhwc[i]) if i > 0 else None)
         self.scores = torch.empty(self.shapes[-1], dtype=torch.float32, device=device)
         # the loss gradient in the activation dtype: the softmax kernel writes the RNE BF16 value the

@@ -562,3 +562,36 @@ def test_conv_stacked_halo(oracle, case, cta):
     assert_tc_close(host(dX), rx, f"stacked dgrad cta={cta}", tol=3e-3)
     np.testing.assert_array_equal(host(Y16), host(Y.to(torch.bfloat16)))
     np.testing.assert_array_equal(host(dX16), host(dX.to(torch.bfloat16)))
+
+
+@pytest.mark.parametrize("case", [CASES[3], (2, 3, 67, 67, 96, (11, 11), (4, 4), (0, 0), 1),
+                                  (2, 4, 9, 9, 8, (3, 3), (1, 1), (1, 1), 1)],
+                         ids=["conv1like", "conv1geom", "plain3x3"])
+def test_conv_i8_bottom(oracle, case):
+    """An int8 channels-last image batch (CAFFE_I8) packed by caffe_conv_pack_bottom gives the same
+    bits as the same integers stored in BF16, for the prepacked forward and weight gradient
+    (space-to-depth segment kernel and the element-form pack)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    Xi = synth.int_pixels((N, C, H, W), 101)
+    _, Wt, b, dY = _inputs(case, 101)
+    cl = torch.channels_last
+    w = cuda(Wt).to(torch.bfloat16)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    outs = []
+    for dt in (torch.bfloat16, torch.int8):
+        x = cuda(Xi).to(dt).contiguous(memory_format=cl)
+        ws = cb.conv_bottom_workspace(Xi.shape, Wt.shape, s, p, g, "bf16")
+        cb.conv_pack_bottom(x, w, s, p, g, "bf16", ws=ws)
+        y = cb.conv_forward(x, w, cuda(b), s, p, g, relu=True, ws=ws, prepacked=True, out_dtype=torch.float32)
+        dW, db = cb.conv_backward_weight(x, dYd, Wt.shape, s, p, g, "bf16", ws=ws, prepacked=True)
+        outs.append([host(t) for t in (y, dW, db)])
+    for a, c in zip(*outs):
+        np.testing.assert_array_equal(a, c)
+    assert_tc_close(outs[1][0], oracle.conv_forward(Xi.astype(np.float64), oracle.quant_bf16(Wt), b, stride=s, pad=p,
+                                                    group=g, relu=True), "i8 fwd")
+    # an I8 bottom is refused where it is not packed
+    import paper_1408_5093_b200._abi as abi
+    with pytest.raises(abi.CaffeError):
+        cb.conv_forward(cuda(Xi).to(torch.int8).contiguous(memory_format=cl), w, cuda(b), s, p, g)

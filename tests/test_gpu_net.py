@@ -149,3 +149,26 @@ def test_overlapped_update_matches_serial(fuse):
     import numpy as np
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
+def test_int8_input_batch_matches_bf16():
+    """Net(input_i8=True) (integer image batch stored as int8, converted by conv1's pack) trains to
+    the same parameters, bit for bit, as the same integers stored in BF16."""
+    import torch
+    import synth
+    from paper_1408_5093_b200 import nets
+    dev = torch.device("cuda")
+    B = 4
+    X = synth.int_pixels((B,) + tuple(nets.CAFFENET_INPUT), 7)
+    outs = []
+    for i8 in (False, True):
+        net = nets.Net(nets.CAFFENET, B, nets.CAFFENET_INPUT, dev, math="bf16", seed=5, input_i8=i8)
+        assert net.input_i8 == i8
+        net.a[0].copy_(torch.from_numpy(X).to(net.a[0].dtype))
+        net.labels.copy_(torch.from_numpy(synth.labels(B, 1000, 7)))
+        for _ in range(2):
+            net.step()
+        torch.cuda.synchronize()
+        outs.append(net.params.cpu().numpy().copy())
+    import numpy as np
+    np.testing.assert_array_equal(outs[0], outs[1])

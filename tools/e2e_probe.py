@@ -1,0 +1,73 @@
+"""Where does the end-to-end step lose time against the device-only step?  Times K graph-replayed
+steps with (a) the bench's full input pipeline, (b) without the host->device copy, (c) without
+the device copy into the input blob, (d) replays only (run on the B200 box)."""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_1408_5093_b200 import nets  # noqa: E402
+
+
+def main():
+    B, K = 256, 20
+    dev = torch.device("cuda")
+    net = nets.Net(nets.CAFFENET, B, nets.CAFFENET_INPUT, dev, math="bf16", seed=0, input_i8=True)
+    X = synth.int_pixels((B, 3, 227, 227), 1000)
+    net.a[0].copy_(torch.from_numpy(X).to(net.a[0].dtype))
+    net.labels.copy_(torch.from_numpy(synth.labels(B, 1000, 1000)))
+    for _ in range(3):
+        net.step()
+    torch.cuda.synchronize()
+    g = net.capture()
+    stream = torch.cuda.current_stream()
+    cl = torch.channels_last
+    hX = torch.from_numpy(X).to(net.a[0].dtype).contiguous(memory_format=cl).pin_memory()
+    hL = torch.from_numpy(synth.labels(B, 1000, 1000)).pin_memory()
+    hloss = torch.empty((), dtype=torch.float32).pin_memory()
+    dstage = [torch.empty_like(net.a[0]) for _ in range(2)]
+    cs = torch.cuda.Stream()
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+
+    def run(h2d, dcopy, labels, loss):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+
+        def prefetch(i):
+            k = i % 2
+            cs.wait_stream(stream) if i < 2 else cs.wait_event(consumed[k])
+            with torch.cuda.stream(cs):
+                dstage[k].copy_(hX, non_blocking=True)
+                copied[k].record(cs)
+        if h2d:
+            prefetch(0)
+        for i in range(K):
+            k = i % 2
+            if h2d:
+                if i + 1 < K:
+                    prefetch(i + 1)
+                stream.wait_event(copied[k])
+            if dcopy:
+                net.a[0].copy_(dstage[k], non_blocking=True)
+                consumed[k].record(stream)
+            if labels:
+                net.labels.copy_(hL, non_blocking=True)
+            g.replay()
+            if loss:
+                hloss.copy_(net.loss, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / K
+
+    for name, cfg in [("full", (1, 1, 1, 1)), ("no_h2d", (0, 1, 1, 1)), ("no_dcopy", (1, 0, 1, 1)),
+                      ("no_labels_loss", (1, 1, 0, 0)), ("replay_only", (0, 0, 0, 0)), ("full2", (1, 1, 1, 1))]:
+        print(f"{name:16s} {run(*cfg):.4f} ms/step", flush=True)
+
+
+if __name__ == "__main__":
+    main()
