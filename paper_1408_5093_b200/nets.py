@@ -353,6 +353,13 @@ class Net:
     # kernel (one small block per SM) trickles alongside.
     fuse_ip_sgd = False
     fuse_ip_relu = True
+    # CUDA stream priorities (lower = more urgent; 0 is the default, -3 the most urgent on B200):
+    # the critical path first, then the weight gradients, the updates last.  Measured (graph replay,
+    # ms/step): all equal 1.538; main -2 / weight gradients -1 / updates 0: 1.509; main -3 / -2 / 0:
+    # 1.509; main -2 alone 1.592; weight gradients -1 alone 1.646.
+    main_priority = -2
+    wgrad_priority = -1
+    sgd_priority = 0
 
     def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4, overlap_update=True):
         self.forward()
@@ -364,7 +371,7 @@ class Net:
             torch = self.torch
             main = torch.cuda.current_stream()
             if getattr(self, "_side", None) is None:
-                self._side = torch.cuda.Stream()
+                self._side = torch.cuda.Stream(priority=self.sgd_priority)
             seg = {i: (off, n) for (i, off, n) in self.segments}
             wb = self.params_bf16 if self.math == "bf16" else None
             pending = []
@@ -375,7 +382,7 @@ class Net:
             wstream = None
             if self.wgrad_side:
                 if getattr(self, "_wside", None) is None:
-                    self._wside = torch.cuda.Stream()
+                    self._wside = torch.cuda.Stream(priority=self.wgrad_priority)
                 wstream = self._wside
 
             launched = []
@@ -439,7 +446,9 @@ class Net:
         re-runs the identical kernel sequence on the same buffers without host launch overhead.
         Call after at least one eager step (so the cached workspace has reached its size)."""
         torch = self.torch
-        s = torch.cuda.Stream()
+        # the critical path (forward, data gradients) is captured at the main priority; the weight-
+        # gradient and update streams run at theirs (stream priorities are kept by graph kernel nodes)
+        s = torch.cuda.Stream(priority=self.main_priority)
         s.wait_stream(torch.cuda.current_stream())
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):

@@ -46,6 +46,11 @@ def main():
         net.skip_update = bool(p.get("nosgd", 0))   # probe only: no parameter update (SGD cost)
         net.fuse_ip_sgd = bool(p.get("fuse", 0))
         net.fuse_ip_relu = bool(p.get("iprelu", 1))
+        net.main_priority = -p.get("pmain", 2)
+        net.wgrad_priority = -p.get("pwgrad", 1)
+        net.sgd_priority = -p.get("psgd", 0)
+        net._side = None
+        net._wside = None
         for _ in range(2):
             net.step()
         torch.cuda.synchronize()
