@@ -346,6 +346,11 @@ caffe_status caffe_ip_backward_weight_sgd(const caffe_blob* bottom, const caffe_
                                           float lr, float momentum_coef, float decay, float grad_scale,
                                           void* workspace, size_t workspace_bytes, caffe_stream_t stream);
 
+/* Layout change (S:130's (c,h,w) order): dst (NCHW, BF16) = src (channels-last, F32|BF16), same
+   logical shape, RNE when narrowing: plain (N, C*H*W) inner-product rows from a channels-last map.
+   Errors: E_SHAPE, E_INVALID (layouts), E_ALIAS, E_DTYPE (dst not BF16). */
+caffe_status caffe_blob_to_nchw(const caffe_blob* src, caffe_blob* dst, caffe_stream_t stream);
+
 /* ------------------------------------------------------------------ im2col / col2im (test entry points)
    S:297 / S:806 lowering of image n: col[(c*kh+i)*kw+j][y*OW+x] = bottom[n,c,y*sh-ph+i,x*sw-pw+j]
    (0 outside), col is an F32 blob of shape (1,1,C*kh*kw,OH*OW).  col2im is its

@@ -396,6 +396,16 @@ def ip_backward_weight_sgd(x, dy, w, mom, w_bf16, lr, momentum, decay, grad_scal
     return w
 
 
+def to_nchw(x, out=None):
+    """NCHW copy of a channels-last blob (caffe_blob_to_nchw)."""
+    torch = _t()
+    if out is None:
+        out = torch.empty(tuple(x.shape), dtype=x.dtype, device=x.device)
+    bs, bd = blob(x), blob(out)
+    call("caffe_blob_to_nchw", ctypes.byref(bs), ctypes.byref(bd), _stream())
+    return out
+
+
 def ip_backward_data_relu(dy, w, relu_top, math="bf16", out=None):
     """dX = [relu_top > 0] * (dY W): the data gradient through the ReLU whose output is this layer's
     bottom (S:190 with S:208 folded in)."""

@@ -97,6 +97,7 @@ SIGNATURES = {
     "caffe_ip_backward_data_relu": [ctypes.c_int, B, B, B, B, vp, sz, vp],
     "caffe_ip_backward_weight": [ctypes.c_int, B, B, B, B, f32, vp, sz, vp],
     "caffe_ip_backward_weight_sgd": [B, B, B, B, B, B, f32, f32, f32, f32, vp, sz, vp],
+    "caffe_blob_to_nchw": [B, B, vp],
     "caffe_im2col": [CD, B, i32, B, vp],
     "caffe_col2im": [CD, B, i32, B, vp],
     "caffe_softmax_loss": [B, vp, vp, B, vp],

@@ -1682,6 +1682,21 @@ caffe_status caffe_ip_backward_weight_sgd(const caffe_blob* bottom, const caffe_
     return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }
 
+caffe_status caffe_blob_to_nchw(const caffe_blob* src, caffe_blob* dst, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(src, "src")) || (st = check_blob(dst, "dst"))) return st;
+    if (!same_shape(src->shape, dst->shape)) return fail(CAFFE_E_SHAPE, "src and dst shapes differ");
+    if (!nhwc(src) || nhwc(dst)) return fail(CAFFE_E_INVALID, "src must be channels-last and dst NCHW");
+    if (overlap(src, dst)) return fail(CAFFE_E_ALIAS, "dst overlaps src");
+    if (dst->dtype != CAFFE_BF16) return fail(CAFFE_E_DTYPE, "dst must be BF16 (F32 rows are staged TF32-rounded)");
+    const caffe_shape4& b = src->shape;
+    if (b.n == 0) return CAFFE_OK;
+    CK(nhwc_to_rows(src->ptr, isbf(src), dst->ptr, isbf(dst) ? 2 : 4, b.n, b.c, b.h * b.w, (long long)b.c * b.h * b.w,
+                    (cudaStream_t)stream),
+       "nhwc to nchw");
+    return CAFFE_OK;
+}
+
 // ------------------------------------------------------------------ im2col / col2im
 caffe_status caffe_im2col(const caffe_conv_desc* desc, const caffe_blob* bottom, int32_t n, caffe_blob* col,
                           caffe_stream_t stream) {

@@ -1249,8 +1249,9 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
 // One 8-CTA cluster, one warp per row (rows strided over the 8 x 16 warps); the loss is reduced in
 // a fixed order -- lanes, then warps of a CTA, then the 8 CTAs read through distributed shared
 // memory by rank 0 -- so it is deterministic without a workspace.
-#define SOFTMAX_CTAS 8
-__global__ void __cluster_dims__(SOFTMAX_CTAS, 1, 1)
+// One cluster of SOFTMAX_CTAS (16, a non-portable size) x 16 warps: one row per warp at batch 256.
+#define SOFTMAX_CTAS 16
+__global__ void __launch_bounds__(512, 1)
 softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restrict__ labels, float* __restrict__ loss,
                     void* __restrict__ diff, int db, int N, int K) {
     __shared__ float wl[32];
@@ -1332,7 +1333,25 @@ softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restric
 
 cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff, int diff_bf16,
                            int N, int K, cudaStream_t s) {
-    softmax_loss_kernel<<<SOFTMAX_CTAS, 512, 0, s>>>(scores, bf16, labels, loss, diff, diff_bf16, N, K);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(softmax_loss_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(SOFTMAX_CTAS);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = SOFTMAX_CTAS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, softmax_loss_kernel, scores, bf16, labels, loss, diff, diff_bf16, N, K);
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
 }

@@ -167,6 +167,9 @@ class Net:
             if L.kind == "pool":
                 # window-local uint8 argmax (a quarter of the int32 mask traffic; same results)
                 self.mask[i] = cb.empty_like_layout(self.shapes[i + 1], torch.uint8, device, nhwc=self.nhwc[i + 1])
+        # (an NCHW copy of fc6's channels-last input shared by its forward and weight gradient --
+        # caffe_blob_to_nchw -- measured slower: 1.542 -> 1.572 ms/step; each pass stages its own)
+        self.rows = {}
         self.labels = torch.zeros(batch, dtype=torch.int32, device=device)
         self.loss = torch.zeros((), dtype=torch.float32, device=device)
         # the first conv's operand (space-to-depth packed image batch) is built once per step into a
@@ -198,6 +201,8 @@ class Net:
                 cb.lrn_forward(x, **LRN, out=nxt)
             elif L.kind == "ip":
                 out = nxt if nxt is not None else self.scores
+                if i in self.rows:
+                    x = cb.to_nchw(x, out=self.rows[i])
                 cb.ip_forward(x, self._wop(i), self.B[i], self.math, relu=L.relu, out=out.view(out.shape[0], -1))
             elif L.kind == "loss":
                 cb.softmax_loss(self.scores, self.labels, loss=self.loss, diff=self.dscores)
@@ -296,7 +301,7 @@ class Net:
                 ev.record(torch.cuda.current_stream())
                 wgrad_stream.wait_event(ev)
                 with torch.cuda.stream(wgrad_stream):
-                    cb.ip_backward_weight_sgd(a[i], dy2, self.W[i], self.Mw[i], self.Wq[i], fused_sgd["lr"],
+                    cb.ip_backward_weight_sgd(self.rows.get(i, a[i]), dy2, self.W[i], self.Mw[i], self.Wq[i], fused_sgd["lr"],
                                               fused_sgd["momentum"], fused_sgd["decay"], 1.0, db=self.dB[i],
                                               ws=self._wgrad_workspace())
                     self.wgrad_done[i] = torch.cuda.Event()
@@ -310,13 +315,13 @@ class Net:
                     ev.record(torch.cuda.current_stream())
                     wgrad_stream.wait_event(ev)
                     with torch.cuda.stream(wgrad_stream):
-                        cb.ip_backward_weight(a[i], dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i],
-                                              db=self.dB[i], ws=self._wgrad_workspace())
+                        cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
+                                              dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
                         self.wgrad_done[i] = torch.cuda.Event()
                         self.wgrad_done[i].record(wgrad_stream)
                 else:
-                    cb.ip_backward_weight(a[i], dy2, self.W[i].shape, self.math, beta=0.0, dw=self.dW[i],
-                                          db=self.dB[i])
+                    cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
+                                          dw=self.dW[i], db=self.dB[i])
                 if hook:
                     hook(i)
                 if i > 0 and self._relu_into_dgrad(i):

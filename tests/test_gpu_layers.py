@@ -401,3 +401,20 @@ def test_ip_backward_weight_sgd_fused(oracle, N, bshape, O):
     g = host(dy).astype(np.float64).T @ xr
     w_o, v_o = oracle.sgd_update(host(W0).astype(np.float64), g, host(V0).astype(np.float64), lr, mom, decay, gs)
     assert_tc_close(host(Wf) - host(W0), w_o - host(W0), "fused update step", tol=2e-3)
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_blob_to_nchw(dt):
+    """caffe_blob_to_nchw: the channels-last blob's elements in NCHW order (BF16 out: bit for bit from
+    BF16, RNE from F32); an F32 destination is refused."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    d = torch.bfloat16 if dt == "bf16" else torch.float32
+    x = cuda(synth.uniform((5, 256, 6, 6), 111, synth.S_X)).to(d).contiguous(memory_format=torch.channels_last)
+    y = cb.to_nchw(x, out=torch.empty(tuple(x.shape), dtype=torch.bfloat16, device="cuda"))
+    assert y.is_contiguous()
+    np.testing.assert_array_equal(host(y), host(x.to(torch.bfloat16)))
+    with pytest.raises(RuntimeError):
+        cb.to_nchw(x, out=torch.empty(tuple(x.shape), dtype=torch.float32, device="cuda"))
+    with pytest.raises(RuntimeError):
+        cb.to_nchw(x, out=torch.empty((5, 256, 6, 5), dtype=d, device="cuda"))
