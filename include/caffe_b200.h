@@ -97,11 +97,15 @@ typedef struct {
    `bottom` written by caffe_conv_pack_bottom (same desc, same bottom data, same workspace), so the
    call does not rebuild it.  Ignored by FP32 math and when the operand is read from bottom directly. */
 #define CAFFE_BOTTOM_PREPACKED 2u
+/* conv forward / backward_data (tensor-core math): the workspace already holds this pass's weight
+   operand, written by caffe_conv_pack_weights (same desc, same weight values, same workspace), so
+   the call does not repack the filter.  Ignored by FP32 math. */
+#define CAFFE_WEIGHTS_PREPACKED 4u
 
 typedef struct {
     int32_t kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w, group;
     caffe_math math;
-    uint32_t flags; /* CAFFE_FUSE_RELU | CAFFE_BOTTOM_PREPACKED */
+    uint32_t flags; /* CAFFE_FUSE_RELU | CAFFE_BOTTOM_PREPACKED | CAFFE_WEIGHTS_PREPACKED */
 } caffe_conv_desc;
 
 typedef enum { CAFFE_POOL_MAX = 0, CAFFE_POOL_AVE = 1 } caffe_pool_method;
@@ -227,6 +231,18 @@ caffe_status caffe_conv_workspace_size(const caffe_conv_desc* desc, caffe_shape4
    operand is read from bottom directly. */
 caffe_status caffe_conv_pack_bottom(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
                                     void* workspace, size_t workspace_bytes, caffe_stream_t stream);
+
+/* Builds the tensor-core weight operand of one pass -- pass CAFFE_PASS_FORWARD: (O, C/g, kh, kw)
+   repacked K-major per tap and channel block; CAFFE_PASS_BACKWARD_DATA: flipped and transposed --
+   at its place in `workspace` (the place caffe_conv_forward / caffe_conv_backward_data use), so
+   calls with CAFFE_WEIGHTS_PREPACKED on that workspace skip the repack.  The caller repacks after
+   every change of the weights (the training step does it right after each layer's update, off the
+   critical path).  `bottom` gives the input geometry.  Workspace: the pass's size.  No-op for FP32
+   math.  Errors: as the pass itself (E_SHAPE, E_PARAM, E_WORKSPACE, E_ALIGN, E_INVALID for another
+   pass). */
+caffe_status caffe_conv_pack_weights(const caffe_conv_desc* desc, caffe_shape4 bottom, const caffe_blob* weight,
+                                     int32_t pass /* caffe_pass */, void* workspace, size_t workspace_bytes,
+                                     caffe_stream_t stream);
 
 /* Forward.  bottom F32|BF16, weight F32|BF16, bias F32 (nullable), top
    F32|BF16 (overwritten).  Fused ReLU with CAFFE_FUSE_RELU. */

@@ -129,11 +129,12 @@ def workspace(nbytes: int, device=None):
     return ctypes.c_void_p(p + off), buf.numel() - off
 
 
-def _conv_desc(kernel, stride, pad, group, math, relu=False, prepacked=False):
+def _conv_desc(kernel, stride, pad, group, math, relu=False, prepacked=False, wprepacked=False):
     kh, kw = _pair(kernel)
     sh, sw = _pair(stride)
     ph, pw = _pair(pad)
-    flags = (_abi.CAFFE_FUSE_RELU if relu else 0) | (_abi.CAFFE_BOTTOM_PREPACKED if prepacked else 0)
+    flags = ((_abi.CAFFE_FUSE_RELU if relu else 0) | (_abi.CAFFE_BOTTOM_PREPACKED if prepacked else 0) |
+             (_abi.CAFFE_WEIGHTS_PREPACKED if wprepacked else 0))
     return _abi.ConvDesc(kh, kw, sh, sw, ph, pw, int(group), MATH[math] if isinstance(math, str) else int(math), flags)
 
 
@@ -183,13 +184,35 @@ def _conv_ws(d, in_shape, w_shape, pass_):
     return workspace(n.value)
 
 
+def conv_pack_weights(w, in_shape, stride=1, pad=0, group=1, math="bf16", pass_=0, ws=None):
+    """Write the weight operand of pass_ (0 forward, 1 data gradient) into the caller workspace `ws`
+    for later calls with wprepacked=True (caffe_conv_pack_weights)."""
+    kh, kw = w.shape[2], w.shape[3]
+    d = _conv_desc((kh, kw), stride, pad, group, math)
+    p, n = _ws_arg(ws)
+    bw = blob(w)
+    call("caffe_conv_pack_weights", ctypes.byref(d), _abi.Shape4(*_shape4(in_shape)), ctypes.byref(bw), int(pass_), p,
+         n, _stream())
+
+
+def conv_workspace(in_shape, w_shape, stride=1, pad=0, group=1, math="bf16", pass_=0, device=None):
+    """A dedicated workspace tensor for one conv pass (caffe_conv_workspace_size)."""
+    torch = _t()
+    d = _conv_desc((w_shape[2], w_shape[3]), stride, pad, group, math)
+    v = ctypes.c_size_t()
+    call("caffe_conv_workspace_size", ctypes.byref(d), _abi.Shape4(*_shape4(in_shape)), _abi.Shape4(*_shape4(w_shape)),
+         int(pass_), ctypes.byref(v))
+    return torch.empty(v.value + 2048, dtype=torch.uint8, device=device or torch.device("cuda"))
+
+
 def conv_forward(x, w, b=None, stride=1, pad=0, group=1, math="bf16", relu=False, out=None, out_dtype=None,
-                 ws=None, prepacked=False):
+                 ws=None, prepacked=False, wprepacked=False):
     """Y = W (*) X + b with groups/stride/zero-pad; optional fused ReLU.  `ws` (+ prepacked)
-    selects a caller workspace already holding conv_pack_bottom's operand."""
+    selects a caller workspace already holding conv_pack_bottom's operand (+ wprepacked: and
+    conv_pack_weights' forward weight operand)."""
     torch = _t()
     kh, kw = w.shape[2], w.shape[3]
-    d = _conv_desc((kh, kw), stride, pad, group, math, relu, prepacked)
+    d = _conv_desc((kh, kw), stride, pad, group, math, relu, prepacked, wprepacked)
     oshape = conv_output_shape(x.shape, w.shape[0], (kh, kw), stride, pad, group)
     if out is None:
         out = empty_like_layout(oshape, out_dtype or x.dtype, x.device, like=x)
@@ -200,29 +223,32 @@ def conv_forward(x, w, b=None, stride=1, pad=0, group=1, math="bf16", relu=False
     return out
 
 
-def conv_backward_data(dy, w, in_shape, stride=1, pad=0, group=1, math="bf16", beta=0.0, out=None, out_dtype=None):
+def conv_backward_data(dy, w, in_shape, stride=1, pad=0, group=1, math="bf16", beta=0.0, out=None, out_dtype=None,
+                       ws=None, wprepacked=False):
     """dX = beta*dX + W^T (*) dY (S:154)."""
     torch = _t()
     kh, kw = w.shape[2], w.shape[3]
-    d = _conv_desc((kh, kw), stride, pad, group, math)
+    d = _conv_desc((kh, kw), stride, pad, group, math, wprepacked=wprepacked)
     if out is None:
         out = empty_like_layout(in_shape, out_dtype or dy.dtype, dy.device, like=dy)
         out.zero_()
-    ws, wsz = _conv_ws(d, in_shape, w.shape, _abi.CAFFE_PASS_BACKWARD_DATA)
+    ws, wsz = _ws_arg(ws) if ws is not None else _conv_ws(d, in_shape, w.shape, _abi.CAFFE_PASS_BACKWARD_DATA)
     bdy, bw, bdx = blob(dy), blob(w), blob(out)
     call("caffe_conv_backward_data", ctypes.byref(d), ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(bdx),
          float(beta), ws, wsz, _stream())
     return out
 
 
-def conv_backward_data_relu(dy, w, relu_top, stride=1, pad=0, group=1, math="bf16", out=None):
+def conv_backward_data_relu(dy, w, relu_top, stride=1, pad=0, group=1, math="bf16", out=None, ws=None,
+                            wprepacked=False):
     """dX = [relu_top > 0] * (W^T (*) dY): the data gradient through the ReLU whose output is this
     layer's bottom (S:154 with S:208 folded in)."""
     kh, kw = w.shape[2], w.shape[3]
-    d = _conv_desc((kh, kw), stride, pad, group, math)
+    d = _conv_desc((kh, kw), stride, pad, group, math, wprepacked=wprepacked)
     if out is None:
         out = empty_like_layout(tuple(relu_top.shape), relu_top.dtype, dy.device, like=relu_top)
-    ws, wsz = _conv_ws(d, tuple(relu_top.shape), w.shape, _abi.CAFFE_PASS_BACKWARD_DATA)
+    ws, wsz = (_ws_arg(ws) if ws is not None
+               else _conv_ws(d, tuple(relu_top.shape), w.shape, _abi.CAFFE_PASS_BACKWARD_DATA))
     bdy, bw, br, bdx = blob(dy), blob(w), blob(relu_top), blob(out)
     call("caffe_conv_backward_data_relu", ctypes.byref(d), ctypes.byref(bdy), ctypes.byref(bw), ctypes.byref(br),
          ctypes.byref(bdx), ws, wsz, _stream())

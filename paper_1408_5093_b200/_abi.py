@@ -20,6 +20,7 @@ CAFFE_NCHW, CAFFE_NHWC = 0, 1
 CAFFE_MATH_FP32, CAFFE_MATH_TF32, CAFFE_MATH_BF16 = 0, 1, 2
 CAFFE_FUSE_RELU = 1
 CAFFE_BOTTOM_PREPACKED = 2
+CAFFE_WEIGHTS_PREPACKED = 4
 CAFFE_POOL_MAX, CAFFE_POOL_AVE = 0, 1
 CAFFE_PASS_FORWARD, CAFFE_PASS_BACKWARD_DATA, CAFFE_PASS_BACKWARD_WEIGHT = 0, 1, 2
 CAFFE_TUNE_CTA_PAIR = 1
@@ -80,6 +81,7 @@ SIGNATURES = {
     "caffe_conv_workspace_size": [CD, Shape4, Shape4, i32, P(sz)],
     "caffe_conv_forward": [CD, B, B, B, B, vp, sz, vp],
     "caffe_conv_pack_bottom": [CD, B, B, vp, sz, vp],
+    "caffe_conv_pack_weights": [CD, Shape4, B, i32, vp, sz, vp],
     "caffe_conv_backward_data": [CD, B, B, B, f32, vp, sz, vp],
     "caffe_conv_backward_data_relu": [CD, B, B, B, B, vp, sz, vp],
     "caffe_conv_backward_weight": [CD, B, B, B, B, f32, vp, sz, vp],

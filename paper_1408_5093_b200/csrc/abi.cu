@@ -763,6 +763,30 @@ caffe_status caffe_conv_pack_bottom(const caffe_conv_desc* desc, const caffe_blo
     return pack_if(A, bottom, ws, p.E, (cudaStream_t)stream);
 }
 
+caffe_status caffe_conv_pack_weights(const caffe_conv_desc* desc, caffe_shape4 bottom, const caffe_blob* weight,
+                                     int32_t pass, void* ws, size_t ws_bytes, caffe_stream_t stream) {
+    caffe_status st;
+    if (!desc) return fail(CAFFE_E_INVALID, "desc is NULL");
+    if ((st = check_blob(weight, "weight"))) return st;
+    Plan p;
+    if ((st = conv_validate(desc, bottom, weight->shape.n, &p))) return st;
+    if (weight->shape.c != p.Cg || weight->shape.h != p.kh || weight->shape.w != p.kw)
+        return fail(CAFFE_E_SHAPE, "weight shape (%d,%d,%d,%d) != (O,C/g,kh,kw) = (%d,%d,%d,%d)", weight->shape.n,
+                    weight->shape.c, weight->shape.h, weight->shape.w, p.O, p.Cg, p.kh, p.kw);
+    if (pass != CAFFE_PASS_FORWARD && pass != CAFFE_PASS_BACKWARD_DATA)
+        return fail(CAFFE_E_INVALID, "pass must be CAFFE_PASS_FORWARD or CAFFE_PASS_BACKWARD_DATA");
+    if (desc->math == CAFFE_MATH_FP32 || p.N == 0) return CAFFE_OK;
+    const size_t need = conv_ws(p, pass, desc->math);
+    if ((st = check_ws(ws, ws_bytes, need))) return st;
+    char* w8 = (char*)ws;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (pass == CAFFE_PASS_FORWARD)
+        CK(repack_w_fwd(weight->ptr, isbf(weight), w8 + ws_x_max(p), p.E, wgeom(p), s), "repack weights");
+    else
+        CK(repack_w_dgrad(weight->ptr, isbf(weight), w8 + ws_dy_max(p), p.E, wgeom(p), p.Cge, s), "repack weights (dgrad)");
+    return CAFFE_OK;
+}
+
 caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* bottom, const caffe_blob* weight,
                                 const caffe_blob* bias, caffe_blob* top, void* ws, size_t ws_bytes,
                                 caffe_stream_t stream) {
@@ -799,7 +823,7 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     void* WB = w8 + ws_x_max(p);
     if (!(desc->flags & CAFFE_BOTTOM_PREPACKED) && (st = pack_if(A, bottom, XA, p.E, s))) return st;
     const void* aptr = A.packed ? XA : A.ptr;
-    CK(repack_w_fwd(weight->ptr, isbf(weight), WB, p.E, wgeom(p), s), "repack weights");
+    if (!(desc->flags & CAFFE_WEIGHTS_PREPACKED)) CK(repack_w_fwd(weight->ptr, isbf(weight), WB, p.E, wgeom(p), s), "repack weights");
     TcLaunch L;
     memset(&L, 0, sizeof L);
     const HaloGeom hg{A.H, A.W, p.OH, p.OW, p.khp, p.kwp, p.php, p.pwp};
@@ -907,7 +931,8 @@ static caffe_status conv_bwd_data(const caffe_conv_desc* desc, const caffe_blob*
     float* T = (float*)(w8 + ws_dy_max(p) + ws_wd(p));
     if ((st = pack_if(A, top_diff, DYA, p.E, s))) return st;
     const void* aptr = A.packed ? DYA : A.ptr;
-    CK(repack_w_dgrad(weight->ptr, isbf(weight), WD, p.E, wgeom(p), p.Cge, s), "repack weights (dgrad)");
+    if (!(desc->flags & CAFFE_WEIGHTS_PREPACKED))
+        CK(repack_w_dgrad(weight->ptr, isbf(weight), WD, p.E, wgeom(p), p.Cge, s), "repack weights (dgrad)");
     const int Hd = p.s2d ? p.Hp : p.H, Wd = p.s2d ? p.Wp : p.W;
     const int lo_h = p.khp - 1 - p.php, lo_w = p.kwp - 1 - p.pwp;
     TcLaunch L;

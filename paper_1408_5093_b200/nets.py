@@ -180,6 +180,33 @@ class Net:
             self.ws0 = cb.conv_bottom_workspace(self.shapes[0], tuple(self.W[0].shape), L0.stride, L0.pad, L0.group,
                                                 math, device)
 
+        # conv weight operands packed once per weight change into dedicated per-layer workspaces
+        # (caffe_conv_pack_weights + CAFFE_WEIGHTS_PREPACKED): the forward and data-gradient passes
+        # then skip their per-call repack, and the repack runs right after each layer's update
+        self.wsf, self.wsd = {}, {}
+        if math != "fp32" and self.prepack_weights:
+            for i, L in enumerate(layers):
+                if L.kind != "conv":
+                    continue
+                ws_shape = tuple(self.W[i].shape)
+                self.wsf[i] = (self.ws0 if (i == 0 and self.ws0 is not None) else
+                               cb.conv_workspace(self.shapes[i], ws_shape, L.stride, L.pad, L.group, math, 0, device))
+                if i > 0:
+                    self.wsd[i] = cb.conv_workspace(self.shapes[i], ws_shape, L.stride, L.pad, L.group, math, 1, device)
+                self.repack_weights(i)
+
+    def repack_weights(self, i=None):
+        """Rebuild the packed conv weight operands (all conv layers, or layer i) from the current
+        weights; call after any change of the weights outside step()."""
+        for j in ([i] if i is not None else list(self.wsf)):
+            L = self.layers[j]
+            self.cb_pack(j, L)
+
+    def cb_pack(self, j, L):
+        cb.conv_pack_weights(self._wop(j), self.shapes[j], L.stride, L.pad, L.group, self.math, 0, ws=self.wsf[j])
+        if j in self.wsd:
+            cb.conv_pack_weights(self._wop(j), self.shapes[j], L.stride, L.pad, L.group, self.math, 1, ws=self.wsd[j])
+
     # --------------------------------------------------------------- one training iteration
     def _wop(self, i):
         return self.Wq[i] if self.math == "bf16" else self.W[i]
@@ -193,8 +220,9 @@ class Net:
                 pre = i == 0 and self.ws0 is not None
                 if pre:
                     cb.conv_pack_bottom(x, self._wop(i), L.stride, L.pad, L.group, self.math, ws=self.ws0)
+                wpre = i in self.wsf
                 cb.conv_forward(x, self._wop(i), self.B[i], L.stride, L.pad, L.group, self.math, relu=L.relu, out=nxt,
-                                ws=self.ws0 if pre else None, prepacked=pre)
+                                ws=self.wsf[i] if wpre else (self.ws0 if pre else None), prepacked=pre, wprepacked=wpre)
             elif L.kind == "pool":
                 cb.pool_forward(x, L.method, L.kernel, L.stride, L.pad, out=nxt, mask=self.mask[i])
             elif L.kind == "lrn":
@@ -282,11 +310,14 @@ class Net:
                                             dw=self.dW[i], db=self.dB[i], ws=self.ws0 if pre else None, prepacked=pre)
                 if hook:
                     hook(i)
+                wpre = i in self.wsd
+                wsd = self.wsd.get(i)
                 if i > 0 and self._relu_into_dgrad(i):
-                    cb.conv_backward_data_relu(dy, self._wop(i), a[i], L.stride, L.pad, L.group, self.math, out=d[i])
+                    cb.conv_backward_data_relu(dy, self._wop(i), a[i], L.stride, L.pad, L.group, self.math, out=d[i],
+                                               ws=wsd, wprepacked=wpre)
                 elif i > 0:
                     cb.conv_backward_data(dy, self._wop(i), a[i].shape, L.stride, L.pad, L.group, self.math,
-                                          beta=0.0, out=d[i])
+                                          beta=0.0, out=d[i], ws=wsd, wprepacked=wpre)
                 if done_hook:
                     done_hook(i)
             elif L.kind == "ip" and fused_sgd is not None and wgrad_stream is not None and self._sgd_fusable(i):
@@ -341,6 +372,7 @@ class Net:
     def update(self, lr=0.01, momentum=0.9, decay=5e-4, grad_scale=1.0):
         cb.sgd_update(self.params, self.grads, self.mom, lr, momentum, decay, grad_scale,
                       w_bf16=self.params_bf16 if self.math == "bf16" else None)
+        self.repack_weights()
 
     side_sgd_blocks = 1
     # side-stream SGD updates of the layers whose gradients are final may be held back until the
@@ -358,6 +390,10 @@ class Net:
     # kernel (one small block per SM) trickles alongside.
     fuse_ip_sgd = False
     fuse_ip_relu = True
+    # conv weight operands packed after each update (caffe_conv_pack_weights) instead of inside every
+    # forward / data-gradient call.  Off by default: measured slower in the step (1.534 -> 1.561
+    # ms/step, A/B on one box) although each pass loses its repack launch.
+    prepack_weights = False
     # CUDA stream priorities (lower = more urgent; 0 is the default, -3 the most urgent on B200):
     # the critical path first, then the weight gradients, the updates last.  Measured (graph replay,
     # ms/step): all equal 1.538; main -2 / weight gradients -1 / updates 0: 1.509; main -3 / -2 / 0:
@@ -398,6 +434,7 @@ class Net:
                 launched.append(1)
                 # pending (layer, lo, hi) ranges of the flat parameter buffer; adjacent ones are merged
                 wev = [self.wgrad_done[i] for i, _, _ in pending if i in getattr(self, "wgrad_done", {})]
+                layers_done = sorted({i for i, _, _ in pending})
                 rng = sorted((lo, hi) for _, lo, hi in pending)
                 pending.clear()
                 runs = []
@@ -417,6 +454,9 @@ class Net:
                     for lo, hi in runs:
                         cb.sgd_update(self.params[lo:hi], self.grads[lo:hi], self.mom[lo:hi], lr,
                                       momentum, decay, 1.0, w_bf16=wb[lo:hi] if wb is not None else None)
+                    for i in layers_done:
+                        if i in self.wsf:
+                            self.repack_weights(i)
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_BLOCKS_PER_SM, 0)
 
             def done(i):

@@ -595,3 +595,33 @@ def test_conv_i8_bottom(oracle, case):
     import paper_1408_5093_b200._abi as abi
     with pytest.raises(abi.CaffeError):
         cb.conv_forward(cuda(Xi).to(torch.int8).contiguous(memory_format=cl), w, cuda(b), s, p, g)
+
+
+@pytest.mark.parametrize("case", [CASES[3], CASES[7], (2, 96, 27, 27, 256, (5, 5), (1, 1), (2, 2), 2), CASES[1]],
+                         ids=[IDS[3], IDS[7], "conv2geom", IDS[1]])
+def test_conv_weights_prepacked(oracle, case):
+    """caffe_conv_pack_weights + CAFFE_WEIGHTS_PREPACKED on a dedicated workspace gives the same bits
+    as repacking the filter inside the forward / data-gradient call (im2col, halo, stacked and
+    space-to-depth tiles)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 121)
+    cl = torch.channels_last
+    Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    w = cuda(Wt).to(torch.bfloat16)
+    wsf = cb.conv_workspace(X.shape, Wt.shape, s, p, g, "bf16", 0)
+    wsd = cb.conv_workspace(X.shape, Wt.shape, s, p, g, "bf16", 1)
+    cb.conv_pack_weights(w, X.shape, s, p, g, "bf16", 0, ws=wsf)
+    cb.conv_pack_weights(w, X.shape, s, p, g, "bf16", 1, ws=wsd)
+    y0 = cb.conv_forward(Xd, w, cuda(b), s, p, g, relu=True, out_dtype=torch.float32)
+    y1 = cb.conv_forward(Xd, w, cuda(b), s, p, g, relu=True, out_dtype=torch.float32, ws=wsf, wprepacked=True)
+    np.testing.assert_array_equal(host(y0), host(y1))
+    dx0 = torch.empty((N, C, H, W), device="cuda").contiguous(memory_format=cl)
+    dx1 = torch.empty((N, C, H, W), device="cuda").contiguous(memory_format=cl)
+    cb.conv_backward_data(dYd, w, X.shape, s, p, g, out=dx0)
+    cb.conv_backward_data(dYd, w, X.shape, s, p, g, out=dx1, ws=wsd, wprepacked=True)
+    np.testing.assert_array_equal(host(dx0), host(dx1))
+    with pytest.raises(RuntimeError):   # only the forward / data-gradient operands exist
+        cb.conv_pack_weights(w, X.shape, s, p, g, "bf16", 2, ws=wsd)
