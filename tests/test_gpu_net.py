@@ -172,3 +172,31 @@ def test_int8_input_batch_matches_bf16():
         outs.append(net.params.cpu().numpy().copy())
     import numpy as np
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_prepacked_weights_step_matches():
+    """Net.prepack_weights (conv weight operands repacked after each update into per-layer
+    workspaces, CAFFE_WEIGHTS_PREPACKED in the passes) trains to the same parameters, bit for bit."""
+    import torch
+    import synth
+    from paper_1408_5093_b200 import nets
+    dev = torch.device("cuda")
+    B = 4
+    X = synth.int_pixels((B,) + tuple(nets.CAFFENET_INPUT), 9)
+    outs = []
+    for pre in (False, True):
+        old = nets.Net.prepack_weights
+        nets.Net.prepack_weights = pre
+        try:
+            net = nets.Net(nets.CAFFENET, B, nets.CAFFENET_INPUT, dev, math="bf16", seed=6)
+        finally:
+            nets.Net.prepack_weights = old
+        assert bool(net.wsf) == pre
+        net.a[0].copy_(torch.from_numpy(X).to(net.a[0].dtype))
+        net.labels.copy_(torch.from_numpy(synth.labels(B, 1000, 9)))
+        for _ in range(2):
+            net.step()
+        torch.cuda.synchronize()
+        outs.append(net.params.cpu().numpy().copy())
+    import numpy as np
+    np.testing.assert_array_equal(outs[0], outs[1])
