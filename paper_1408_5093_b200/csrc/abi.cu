@@ -62,7 +62,7 @@ caffe_status cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 inline long long cnt(const caffe_shape4& s) { return (long long)s.n * s.c * s.h * s.w; }
-inline size_t esize(caffe_dtype d) { return d == CAFFE_BF16 ? 2 : d == CAFFE_U8 ? 1 : 4; }
+inline size_t esize(caffe_dtype d) { return d == CAFFE_BF16 ? 2 : (d == CAFFE_U8 || d == CAFFE_I8) ? 1 : 4; }
 inline size_t bytes_of(const caffe_blob* b) { return (size_t)cnt(b->shape) * esize(b->dtype); }
 inline long long rup(long long a, long long b) { return (a + b - 1) / b * b; }
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
