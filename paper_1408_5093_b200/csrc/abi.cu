@@ -441,7 +441,6 @@ static bool halo_applies(int E, const HaloGeom& h) {
 // 86% useful rows for 13x13.  CAFFE_TUNE_HALO_STACKED: 0 off, 1 (default) where whole-row halo tiles
 // do not apply, 2 wherever the geometry allows.
 int g_halo_stacked = 1;
-int g_stk_astages = 4;   // probe knob (key 98)
 static bool stacked_geom(const HaloGeom& h) {
     return h.Ho == h.Hi && h.Wo == h.Wi && (h.kh & 1) && (h.kw & 1) && h.pad_h == (h.kh - 1) / 2 &&
            h.pad_w == (h.kw - 1) / 2 && h.kh * h.kw >= 4 && h.Wi + h.pad_w <= 256 && h.Wo >= 4;
@@ -495,8 +494,7 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     a.a_stages = 2;
     a.macc = 1;
     if (2 * 2 * a.acc_stride <= 512 && a.a_stages * 2 * a.halo_slot <= 140 * 1024) a.macc = 2;
-    // stacked tiles turn their A stages over faster (fewer taps per staged window): deeper A ring
-    if (a.stk) a.a_stages = std::max(2, std::min(g_stk_astages, (int)((140 * 1024) / (a.macc * a.halo_slot))));
+    // (a deeper A ring for stacked tiles -- 3 or 4 stages -- measured no faster: 2 stages kept)
     a.b_stage_bytes = a.BN / L.cg * 128;
     long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
     // TMA tensor-store epilogue (specialised-epilogue launches): the unit's tiles are staged in
@@ -630,14 +628,6 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     if (key == CAFFE_TUNE_SGD_BLOCKS_PER_SM) {
         if (value < 0 || value > 8) return fail(CAFFE_E_PARAM, "SGD blocks per SM must be 0 (default 4) .. 8");
         g_sgd_blocks_per_sm = value == 0 ? 4 : value;
-        return CAFFE_OK;
-    }
-    if (key == 98) {   // profiling probe: A stages of stacked halo tiles
-        g_stk_astages = value;
-        return CAFFE_OK;
-    }
-    if (key == 99) {   // profiling probes (not part of the documented interface)
-        cb::g_dbg = value;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO_STACKED) {

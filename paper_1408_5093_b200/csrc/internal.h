@@ -62,7 +62,6 @@ struct TcArgs {
     int rows_epi;                       // EPI_STRIDED: row-staged coalesced stores (epi_store_rows)
     int k_last;                         // A_HALO_K: 16-channel K steps needed by the last channel block
                                         // (0 = all 4); 3 with a single block selects the KS = 3 kernel
-    int dbg;                            // profiling probes only (0 in normal use)
     // A_HALO_K + tma_store: the tile is staged in shared memory as TMA boxes of st_cw channels x
     // out_w pixels x halo_th rows (swizzled by the box row width: 128/64/32 B, or none when the
     // row is an odd number of 16-byte pieces) and written by 4-D tensor stores through mapC
@@ -221,7 +220,6 @@ extern int g_pool_strip_rows;   // CAFFE_TUNE_POOL_STRIP_ROWS
 extern int g_wgrad_reduce_sg_min;   // CAFFE_TUNE_WGRAD_REDUCE_SG
 extern int g_wgrad_reduce_rows;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS
 extern int g_halo_fast_epi;   // CAFFE_TUNE_HALO_FAST_EPI
-extern int g_dbg;
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,
                   float decay, float gscale, cudaStream_t s);
 

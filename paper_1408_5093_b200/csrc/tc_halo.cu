@@ -28,7 +28,6 @@ namespace cb {
 
 constexpr int HALO_SMEM_ALIGN = 1024;
 int g_halo_fast_epi = 1;   // CAFFE_TUNE_HALO_FAST_EPI
-int g_dbg = 0;
 int g_halo_tma_store = 0;   // CAFFE_TUNE_HALO_TMA_STORE (off: measured no gain for conv1, conv2 fwd 92 -> 106 us)
 
 size_t tc_halo_smem_bytes(const TcArgs& a) {
@@ -299,16 +298,15 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 const long long rbase = (long long)n * args.s_n + (long long)(y * args.out_w + x) * args.s_p;
                 if constexpr (EPC > 0) {
-                    if (args.dbg == 2) continue;
                     if (tstore) {
-                        epi_stage_bf16_row<EPC>(taddr + a * args.acc_stride + cb_, row_ok && args.dbg != 1,
+                        epi_stage_bf16_row<EPC>(taddr + a * args.acc_stride + cb_, row_ok,
                                                 stg + (uint32_t)(a * args.st_tile_bytes), yy * args.out_w + xx, cb_,
                                                 args.st_cw, args.st_chunk_bytes, smem_u32(bs + cb_),
                                                 args.bias != nullptr, args.relu != 0);
                         continue;
                     }
                     __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + rbase + cbase + cb_;
-                    epi_store_bf16_rowseg<EPC>(taddr + a * args.acc_stride + cb_, row_ok && args.dbg != 1, dst,
+                    epi_store_bf16_rowseg<EPC>(taddr + a * args.acc_stride + cb_, row_ok, dst,
                                                smem_u32(bs + cb_), args.bias != nullptr, args.relu != 0);
                 } else if (cb_ < ce_) {
                     epi_store_strided(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs, cb_, ce_);
@@ -643,8 +641,6 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s) {
     if (L.esz != 2) return cudaErrorInvalidValue;
     const int macc = L.args.macc > 1 ? L.args.macc : 1;
     if (macc > 2) return cudaErrorInvalidValue;
-    TcLaunch& LL = const_cast<TcLaunch&>(L);
-    LL.args.dbg = g_dbg;
     const TcArgs& a = L.args;
     const int epc = halo_fast_epc(a, L.cg);
     if (epc > 0) {

@@ -200,3 +200,35 @@ def test_prepacked_weights_step_matches():
         outs.append(net.params.cpu().numpy().copy())
     import numpy as np
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_dp_path_single_rank_nccl():
+    """The data-parallel step (bucketed NCCL all-reduce hooks, finish, update with 1/W) run as a
+    one-rank NCCL group equals the serial single-GPU step bit for bit (the sum over one rank is the
+    identity): covers the W > 1 code path on one GPU."""
+    import os
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_1408_5093_b200 import nets
+    from paper_1408_5093_b200.dp import GradAllReduce
+    dev = torch.device("cuda")
+    dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1)
+    try:
+        outs = []
+        for dp in (False, True):
+            net = nets.Net(nets.LENET, 16, nets.LENET_INPUT, dev, math="bf16", seed=4)
+            net.a[0].copy_(torch.from_numpy(synth.mnist_pixels((16,) + tuple(nets.LENET_INPUT), 4)).to(torch.bfloat16))
+            net.labels.copy_(torch.from_numpy(synth.labels(16, 10, 4)))
+            ar = GradAllReduce(net.grads, net.segments, 1, bucket_bytes=64 << 10) if dp else None
+            for _ in range(2):
+                if dp:
+                    net.step(ar)
+                else:
+                    net.step(overlap_update=False)
+            torch.cuda.synchronize()
+            outs.append(net.params.cpu().numpy().copy())
+        import numpy as np
+        np.testing.assert_array_equal(outs[0], outs[1])
+    finally:
+        dist.destroy_process_group()
