@@ -64,9 +64,16 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / K
 
-    for name, cfg in [("full", (1, 1, 1, 1)), ("no_h2d", (0, 1, 1, 1)), ("no_dcopy", (1, 0, 1, 1)),
-                      ("no_labels_loss", (1, 1, 0, 0)), ("replay_only", (0, 0, 0, 0)), ("full2", (1, 1, 1, 1))]:
-        print(f"{name:16s} {run(*cfg):.4f} ms/step", flush=True)
+    import statistics
+    cfgs = [("full", (1, 1, 1, 1)), ("no_h2d", (0, 1, 1, 1)), ("no_dcopy", (1, 0, 1, 1)),
+            ("replay_only", (0, 0, 0, 0))]
+    res = {n: [] for n, _ in cfgs}
+    for _ in range(6):
+        for name, cfg in cfgs:
+            res[name].append(run(*cfg))
+    for name, _ in cfgs:
+        print(f"{name:16s} median {statistics.median(res[name]):.4f} ms/step  {['%.3f' % x for x in res[name]]}",
+              flush=True)
 
 
 if __name__ == "__main__":
