@@ -79,6 +79,11 @@ def conv_flops(in_shape, L: Layer) -> Tuple[int, Tuple[int, int, int, int]]:
     return 2 * macs, (N, L.num_output, OH, OW)
 
 
+def torch_cuda_ok(net) -> bool:
+    """Side streams need CUDA tensors (the CPU tests drive the oracle net, not this class)."""
+    return net.params.is_cuda
+
+
 class Net:
     def __init__(self, layers: List[Layer], batch: int, input_shape, device, act_dtype=None, math="bf16", seed=0,
                  input_i8=False):
@@ -478,6 +483,28 @@ class Net:
                 main.wait_stream(self._side)
             if wstream is not None and self.wgrad_done:
                 main.wait_stream(wstream)
+            return
+        if allreduce is not None and self.wgrad_side and torch_cuda_ok(self):
+            # data parallel: weight gradients on their stream as on one GPU; each bucket's all-reduce
+            # is issued from that stream after it has also caught up with the main stream, so the
+            # collective follows every gradient of the bucket (the layer-0 gradient runs on main)
+            torch = self.torch
+            main = torch.cuda.current_stream()
+            if getattr(self, "_wside", None) is None:
+                self._wside = torch.cuda.Stream(priority=self.wgrad_priority)
+            wstream = self._wside
+
+            def hook(i):
+                ev = torch.cuda.Event()
+                ev.record(main)
+                wstream.wait_event(ev)
+                with torch.cuda.stream(wstream):
+                    allreduce.on_grad(i)
+
+            self.backward(hook=hook, wgrad_stream=wstream)
+            main.wait_stream(wstream)
+            allreduce.finish()
+            self.update(lr, momentum, decay, grad_scale=1.0 / allreduce.world)
             return
         self.backward(hook=allreduce.on_grad if allreduce else None)
         scale = 1.0
