@@ -188,6 +188,10 @@ caffe_status caffe_device_check(void);
    = where whole-row halo tiles do not apply and N tiles are <= 128 columns (CaffeNet conv5
    forward), 2 = wherever the geometry allows. */
 #define CAFFE_TUNE_HALO_STACKED 14
+/* CAFFE_TUNE_SGD_THREADS: threads per block of caffe_sgd_update (0 = default 256; 64, 128): with
+   CAFFE_TUNE_SGD_BLOCKS_PER_SM it sets how much of an SM an update running beside the backward
+   takes.  Results are identical. */
+#define CAFFE_TUNE_SGD_THREADS 15
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

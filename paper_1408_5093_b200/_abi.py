@@ -37,6 +37,7 @@ CAFFE_TUNE_HALO_FAST_EPI = 11
 CAFFE_TUNE_HALO_TMA_STORE = 12
 CAFFE_TUNE_WGRAD_REDUCE_ROWS = 13
 CAFFE_TUNE_HALO_STACKED = 14
+CAFFE_TUNE_SGD_THREADS = 15
 
 
 class Shape4(ctypes.Structure):

@@ -630,6 +630,12 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_sgd_blocks_per_sm = value == 0 ? 4 : value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_SGD_THREADS) {
+        if (value != 0 && value != 64 && value != 128 && value != 256)
+            return fail(CAFFE_E_PARAM, "SGD threads per block must be 0 (default 256), 64, 128 or 256");
+        cb::g_sgd_threads = value == 0 ? 256 : value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_HALO_STACKED) {
         if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "stacked halo mode must be 0 (off), 1 (auto), 2 (force)");
         g_halo_stacked = value;

@@ -216,6 +216,7 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
 cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff,
                            int diff_bf16, int N, int K, cudaStream_t s);
 extern int g_sgd_blocks_per_sm;
+extern int g_sgd_threads;   // CAFFE_TUNE_SGD_THREADS
 extern int g_pool_strip_rows;   // CAFFE_TUNE_POOL_STRIP_ROWS
 extern int g_wgrad_reduce_sg_min;   // CAFFE_TUNE_WGRAD_REDUCE_SG
 extern int g_wgrad_reduce_rows;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS

@@ -1416,6 +1416,8 @@ __global__ void __launch_bounds__(256, 5) sgd_kernel(float* __restrict__ w, cons
 }
 
 int g_sgd_blocks_per_sm = 4;   // CAFFE_TUNE_SGD_BLOCKS_PER_SM
+int g_sgd_threads = 256;   // CAFFE_TUNE_SGD_THREADS
+
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom, float decay,
                   float gscale, cudaStream_t s) {
     const bool al = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
@@ -1428,9 +1430,10 @@ cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long co
         cudaFuncSetAttribute(sgd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         carve = true;
     }
-    const long long want = (count / 4 + 511) / 512;   // blocks for 2 vectors per thread
+    const int threads = g_sgd_threads;
+    const long long want = (count / 4 + 2 * threads - 1) / (2 * threads);   // blocks for 2 vectors per thread
     const int grid = (int)std::max(1LL, std::min<long long>(148LL * g_sgd_blocks_per_sm, want));
-    sgd_kernel<<<grid, 256, 0, s>>>(w, g, v, (__nv_bfloat16*)w_bf16, count, lr, mom, decay, gscale);
+    sgd_kernel<<<grid, threads, 0, s>>>(w, g, v, (__nv_bfloat16*)w_bf16, count, lr, mom, decay, gscale);
     note_launch();
     return cudaGetLastError();
 }

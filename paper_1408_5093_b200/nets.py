@@ -380,6 +380,7 @@ class Net:
         self.repack_weights()
 
     side_sgd_blocks = 1
+    side_sgd_threads = 256     # (2 x 128-thread blocks per SM measured the same: 1.503 vs 1.507 ms/step)
     # side-stream SGD updates of the layers whose gradients are final may be held back until the
     # backward pass reaches this layer index (None: each layer's update is launched as soon as its
     # gradients are final).  Measured (graph replay, one B200, ms/step): with the weight gradients
@@ -455,6 +456,7 @@ class Net:
                     self._side.wait_event(e)
                 # one 256-thread block per SM: leaves registers / thread slots for the main stream
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_BLOCKS_PER_SM, self.side_sgd_blocks)
+                _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_THREADS, self.side_sgd_threads)
                 with torch.cuda.stream(self._side):
                     for lo, hi in runs:
                         cb.sgd_update(self.params[lo:hi], self.grads[lo:hi], self.mom[lo:hi], lr,
@@ -463,6 +465,7 @@ class Net:
                         if i in self.wsf:
                             self.repack_weights(i)
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_BLOCKS_PER_SM, 0)
+                _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_THREADS, 0)
 
             def done(i):
                 if getattr(self, "skip_update", False):

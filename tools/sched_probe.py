@@ -42,6 +42,7 @@ def main():
                 _abi.call("caffe_set_tuning", int(k[4:]), v)
         net.sgd_flush_layer = p.get("flush", None)
         net.side_sgd_blocks = p.get("blocks", 1)
+        net.side_sgd_threads = p.get("threads", 256)
         net.wgrad_side = bool(p.get("wside", 1))
         net.skip_update = bool(p.get("nosgd", 0))   # probe only: no parameter update (SGD cost)
         net.fuse_ip_sgd = bool(p.get("fuse", 0))
