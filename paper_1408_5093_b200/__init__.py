@@ -78,11 +78,13 @@ def layout_of(t) -> int:
 
 
 def blob(t, shape=None) -> _abi.Blob:
-    """Describe a CUDA tensor as a caffe_blob: contiguous -> NCHW, channels_last -> NHWC."""
+    """Describe a CUDA tensor as a caffe_blob: contiguous -> NCHW, channels_last -> NHWC.  A pinned
+    host tensor is accepted too (the kernels read it through unified addressing over PCIe -- meant
+    for read-only inputs such as an image batch handed to conv_pack_bottom)."""
     if t is None:
         return None
-    if not t.is_cuda:
-        raise ValueError("caffe_b200 blobs must live on a CUDA device")
+    if not t.is_cuda and not t.is_pinned():
+        raise ValueError("caffe_b200 blobs must live on a CUDA device (or in pinned host memory)")
     lay = layout_of(t)
     n, c, h, w = _shape4(t.shape if shape is None else shape)
     return _abi.Blob(ctypes.c_void_p(t.data_ptr()), _abi.Shape4(n, c, h, w), _dtype_code(t), lay)

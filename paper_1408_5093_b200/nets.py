@@ -223,7 +223,7 @@ class Net:
             nxt = a[i + 1] if i + 1 < n - 1 else None
             if L.kind == "conv":
                 pre = i == 0 and self.ws0 is not None
-                if pre:
+                if pre and not self.external_pack:
                     cb.conv_pack_bottom(x, self._wop(i), L.stride, L.pad, L.group, self.math, ws=self.ws0)
                 wpre = i in self.wsf
                 cb.conv_forward(x, self._wop(i), self.B[i], L.stride, L.pad, L.group, self.math, relu=L.relu, out=nxt,
@@ -379,6 +379,9 @@ class Net:
                       w_bf16=self.params_bf16 if self.math == "bf16" else None)
         self.repack_weights()
 
+    # the first layer's packed input (ws0) is written by the caller before the step
+    # (conv_pack_bottom from the host batch, e.g. bench.py's end-to-end input pipeline)
+    external_pack = False
     side_sgd_blocks = 1
     side_sgd_threads = 256     # (2 x 128-thread blocks per SM measured the same: 1.503 vs 1.507 ms/step)
     # side-stream SGD updates of the layers whose gradients are final may be held back until the
