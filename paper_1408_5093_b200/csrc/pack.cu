@@ -311,6 +311,7 @@ cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* d
 __global__ void pack_i8_seg_kernel(const int8_t* __restrict__ src, __nv_bfloat16* __restrict__ dst, PackGeom g,
                                    int total) {
     const int L = g.sw * g.C;
+    const int8_t* src_end = src + (long long)g.N * g.H * g.W * g.C;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
         const int dy = t % g.sh;
         int r = t / g.sh;
@@ -321,18 +322,42 @@ __global__ void pack_i8_seg_kernel(const int8_t* __restrict__ src, __nv_bfloat16
         const int nv = h < g.H ? max(0, min(L, (g.W - X * g.sw) * g.C)) : 0;   // valid elements
         const int8_t* p = src + (((long long)n * g.H + h) * g.W + (long long)X * g.sw) * g.C;
         uint32_t o[8];
+        if (L == 12 && nv == 12 && p + 16 <= src_end) {
+            // whole 12-byte segment: three (or four, when unaligned) word loads + funnel shifts
+            // instead of twelve byte loads
+            const uintptr_t b = reinterpret_cast<uintptr_t>(p);
+            const uint32_t* wp = reinterpret_cast<const uint32_t*>(b & ~uintptr_t(3));
+            const uint32_t sh = (uint32_t)(b & 3) * 8u;
+            const uint32_t w0 = __ldg(wp), w1 = __ldg(wp + 1), w2 = __ldg(wp + 2);
+            const uint32_t w3 = sh ? __ldg(wp + 3) : 0u;
+            const uint32_t x[3] = {__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh)};
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const float a = 2 * i < nv ? (float)__ldg(p + 2 * i) : 0.f;
-            const float b = 2 * i + 1 < nv ? (float)__ldg(p + 2 * i + 1) : 0.f;
-            __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-            o[i] = *reinterpret_cast<uint32_t*>(&v);
+            for (int i = 0; i < 6; i++) {
+                const float a = (float)(int8_t)(x[(2 * i) >> 2] >> (8 * ((2 * i) & 3)));
+                const float c = (float)(int8_t)(x[(2 * i + 1) >> 2] >> (8 * ((2 * i + 1) & 3)));
+                __nv_bfloat162 v = __floats2bfloat162_rn(a, c);
+                o[i] = *reinterpret_cast<uint32_t*>(&v);
+            }
+            o[6] = o[7] = 0u;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const float a = 2 * i < nv ? (float)__ldg(p + 2 * i) : 0.f;
+                const float c = 2 * i + 1 < nv ? (float)__ldg(p + 2 * i + 1) : 0.f;
+                __nv_bfloat162 v = __floats2bfloat162_rn(a, c);
+                o[i] = *reinterpret_cast<uint32_t*>(&v);
+            }
         }
         __nv_bfloat16* q = dst + (((long long)n * g.Hp + Y) * g.Wp + X) * g.Ctot + dy * L;
-        uint32_t* q4 = reinterpret_cast<uint32_t*>(q);   // L even, q 4-byte aligned
+        if (L == 12 && (reinterpret_cast<uintptr_t>(q) & 7) == 0) {
+            uint2* q2 = reinterpret_cast<uint2*>(q);
+            q2[0] = make_uint2(o[0], o[1]); q2[1] = make_uint2(o[2], o[3]); q2[2] = make_uint2(o[4], o[5]);
+        } else {
+            uint32_t* q4 = reinterpret_cast<uint32_t*>(q);   // L even, q 4-byte aligned
 #pragma unroll
-        for (int i = 0; i < 8; i++)
-            if (2 * i < L) q4[i] = o[i];
+            for (int i = 0; i < 8; i++)
+                if (2 * i < L) q4[i] = o[i];
+        }
         if (dy == g.sh - 1) {
             __nv_bfloat16* z = q + L;   // channels [sh*L, Ctot)
             for (int c = 0; c < g.Ctot - g.sh * L; c += 2) *reinterpret_cast<uint32_t*>(z + c) = 0u;

@@ -31,10 +31,10 @@ def main():
     for kv in filter(None, os.environ.get("CAFFE_TUNE", "").split(",")):
         k, v = kv.split("=")
         _abi.call("caffe_set_tuning", int(k), int(v))
-    net = nets.Net(nets.CAFFENET, args.batch, nets.CAFFENET_INPUT, dev, math="bf16", seed=0)
+    net = nets.Net(nets.CAFFENET, args.batch, nets.CAFFENET_INPUT, dev, math="bf16", seed=0, input_i8=True)
     import synth
     net.a[0].copy_(torch.from_numpy(synth.int_pixels((args.batch,) + tuple(nets.CAFFENET_INPUT), 1000))
-                   .to(torch.bfloat16))
+                   .to(net.a[0].dtype))
     net.labels.copy_(torch.from_numpy(synth.labels(args.batch, 1000, 1000)))
     for _ in range(3):
         net.step()
