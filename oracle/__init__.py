@@ -54,6 +54,8 @@ def _L():
         _lib.oracle_col2im_f32.argtypes = [f] + [i] * 10 + [f]
         _lib.oracle_maxpool_forward_f32.argtypes = [f] + [i] * 10 + [f, i32p]
         _lib.oracle_maxpool_backward_f32.argtypes = [f, i32p] + [i] * 10 + [f]
+        _lib.oracle_maxpool_forward_f64.argtypes = [d] + [i] * 10 + [d, i32p]
+        _lib.oracle_maxpool_backward_f64.argtypes = [d, i32p] + [i] * 10 + [d]
         _lib.oracle_avepool_forward.argtypes = [d] + [i] * 10 + [d]
         _lib.oracle_avepool_backward.argtypes = [d] + [i] * 10 + [d]
         _lib.oracle_lrn_forward.argtypes = [d] + [i] * 5 + [dbl] * 3 + [d, d]
@@ -154,27 +156,32 @@ def col2im(col, in_shape, n, ksize, stride=(1, 1), pad=(0, 0), out=None):
 
 
 # ----------------------------------------------------------------------------- pooling
-def maxpool_forward(X, ksize, stride, pad=(0, 0)):
-    """S:163 max with R7 ties/index; float32 in, (Y float32, mask int32)."""
-    X = _f32(X)
+def maxpool_forward(X, ksize, stride, pad=(0, 0), fp64=False):
+    """S:163 max with R7 ties/index; (Y, mask int32).  float32 in/out (the bit-exact GPU parity
+    form) or, with fp64=True, float64 in/out (oracle/net.py): selection does not round, so both
+    pick the same element of the same values."""
+    X = _f64(X) if fp64 else _f32(X)
     N, C, H, Wd = X.shape
     OH = pool_out_dim(H, ksize[0], stride[0], pad[0])
     OW = pool_out_dim(Wd, ksize[1], stride[1], pad[1])
-    Y = np.empty((N, C, OH, OW), np.float32)
+    Y = np.empty((N, C, OH, OW), X.dtype)
     M = np.empty((N, C, OH, OW), np.int32)
-    _L().oracle_maxpool_forward_f32(_pf(X), N, C, H, Wd, ksize[0], ksize[1], stride[0], stride[1],
-                                    pad[0], pad[1], _pf(Y), _pi(M))
+    fn = _L().oracle_maxpool_forward_f64 if fp64 else _L().oracle_maxpool_forward_f32
+    fn(_pd(X) if fp64 else _pf(X), N, C, H, Wd, ksize[0], ksize[1], stride[0], stride[1],
+       pad[0], pad[1], _pd(Y) if fp64 else _pf(Y), _pi(M))
     return Y, M
 
 
-def maxpool_backward(dY, mask, in_shape, ksize, stride, pad=(0, 0)):
-    """S:172 routing by argmax, FP32 gather in ascending (py,px) order (R8)."""
-    dY = _f32(dY)
+def maxpool_backward(dY, mask, in_shape, ksize, stride, pad=(0, 0), fp64=False):
+    """S:172 routing by argmax, gather in ascending (py,px) order (R8): FP32 sums (the bit-exact
+    GPU order) or, with fp64=True, double sums (oracle/net.py)."""
+    dY = _f64(dY) if fp64 else _f32(dY)
     mask = np.ascontiguousarray(mask, dtype=np.int32)
     N, C, H, Wd = in_shape
-    dX = np.empty(in_shape, np.float32)
-    _L().oracle_maxpool_backward_f32(_pf(dY), _pi(mask), N, C, H, Wd, ksize[0], ksize[1],
-                                     stride[0], stride[1], pad[0], pad[1], _pf(dX))
+    dX = np.empty(in_shape, dY.dtype)
+    fn = _L().oracle_maxpool_backward_f64 if fp64 else _L().oracle_maxpool_backward_f32
+    fn(_pd(dY) if fp64 else _pf(dY), _pi(mask), N, C, H, Wd, ksize[0], ksize[1],
+       stride[0], stride[1], pad[0], pad[1], _pd(dX) if fp64 else _pf(dX))
     return dX
 
 

@@ -5,6 +5,12 @@ Chains the oracle layer definitions in the order the paper's nets use them (P:13
 LeNet; CaffeNet = the paper's reference "AlexNet with variations", topology
 from bvlc_reference_caffenet, reading R15: pool before LRN).  Its own layer table (shared with
 nothing in the product package).  Forward, softmax loss, backward (S:154 etc.), SGD.
+Everything is fp64 end to end (max pooling included: `maxpool_forward/backward(fp64=True)`).
+
+Pins (tests/test_oracle_net.py): S:426 zero-parameter loss = ln K; an independent FP64 torch
+autograd chain of the same topology (loss to 1e-12, every gradient to 1e-10 relative)
+whole-LeNet central finite differences; mutations of the layer table (pool/LRN order, ReLU
+placement) must fail the torch check; train_step's update against S:523 written out.
 """
 from __future__ import annotations
 
@@ -53,8 +59,7 @@ def forward_backward(layers, X, params, labels, quant=None, conv_only_first_dgra
             W, b = params[name]
             y = conv_forward(q(x), q(W), b, stride=(P["s"],) * 2, pad=(P["p"],) * 2, group=P["g"], relu=P["relu"])
         elif kind == "pool":
-            y32, m = maxpool_forward(x.astype(np.float32), (P["k"],) * 2, (P["s"],) * 2)
-            y, masks[name] = y32.astype(np.float64), m
+            y, masks[name] = maxpool_forward(x, (P["k"],) * 2, (P["s"],) * 2, fp64=True)
         elif kind == "lrn":
             y = lrn_forward(x, P["n"], P["alpha"], P["beta"], P["kk"])
         else:
@@ -86,8 +91,7 @@ def forward_backward(layers, X, params, labels, quant=None, conv_only_first_dgra
             grads[name] = (dW, db)
             d = dX.reshape(x.shape)
         elif kind == "pool":
-            d = maxpool_backward(d.astype(np.float32), masks[name], x.shape, (P["k"],) * 2,
-                                 (P["s"],) * 2).astype(np.float64)
+            d = maxpool_backward(d, masks[name], x.shape, (P["k"],) * 2, (P["s"],) * 2, fp64=True)
         elif kind == "lrn":
             d = lrn_backward(x, d, P["n"], P["alpha"], P["beta"], P["kk"])
     return loss, grads, acts

@@ -219,55 +219,89 @@ int oracle_pool_out_dim(int in, int k, int s, int p) {
  * clipped at 0; scan h ascending, w ascending; a candidate replaces the
  * current best only if strictly greater; the first in-image element seeds the
  * scan.  mask = h*W + w within the (n,c) plane.  Pure selection -> bit-exact.
+ * Written once for float (_f32: the GPU parity form) and double (_f64: the
+ * fp64 net oracle, oracle/net.py) -- selection does not round, so both give
+ * the same argmax on the same values.
  */
+#define MAXPOOL_FWD_BODY(T)                                                               \
+    int OH = oracle_pool_out_dim(H, kh, sh, ph), OW = oracle_pool_out_dim(W, kw, sw, pw);   \
+    _Pragma("omp parallel for collapse(2) schedule(static)")                              \
+    for (int n = 0; n < N; n++)                                                           \
+        for (int c = 0; c < C; c++)                                                       \
+            for (int py = 0; py < OH; py++)                                               \
+                for (int px = 0; px < OW; px++) {                                         \
+                    int hs = py * sh - ph, ws = px * sw - pw;                             \
+                    int he = hs + kh < H ? hs + kh : H, we = ws + kw < W ? ws + kw : W;   \
+                    if (hs < 0) hs = 0;                                                   \
+                    if (ws < 0) ws = 0;                                                   \
+                    T best = 0;                                                           \
+                    int32_t arg = -1;                                                     \
+                    for (int h = hs; h < he; h++)                                         \
+                        for (int w = ws; w < we; w++) {                                   \
+                            T v = X[IDX4(n, c, h, w, C, H, W)];                           \
+                            if (arg < 0 || v > best) { best = v; arg = h * W + w; }       \
+                        }                                                                 \
+                    Y[IDX4(n, c, py, px, C, OH, OW)] = best;                              \
+                    if (mask) mask[IDX4(n, c, py, px, C, OH, OW)] = arg;                  \
+                }
+
 void oracle_maxpool_forward_f32(const float* X, int N, int C, int H, int W,
                                 int kh, int kw, int sh, int sw, int ph, int pw,
                                 float* Y, int32_t* mask) {
-    int OH = oracle_pool_out_dim(H, kh, sh, ph), OW = oracle_pool_out_dim(W, kw, sw, pw);
-#pragma omp parallel for collapse(2) schedule(static)
-    for (int n = 0; n < N; n++)
-        for (int c = 0; c < C; c++)
-            for (int py = 0; py < OH; py++)
-                for (int px = 0; px < OW; px++) {
-                    int hs = py * sh - ph, ws = px * sw - pw;
-                    int he = hs + kh < H ? hs + kh : H, we = ws + kw < W ? ws + kw : W;
-                    if (hs < 0) hs = 0;
-                    if (ws < 0) ws = 0;
-                    float best = 0.0f;
-                    int32_t arg = -1;
-                    for (int h = hs; h < he; h++)
-                        for (int w = ws; w < we; w++) {
-                            float v = X[IDX4(n, c, h, w, C, H, W)];
-                            if (arg < 0 || v > best) { best = v; arg = h * W + w; }
-                        }
-                    Y[IDX4(n, c, py, px, C, OH, OW)] = best;
-                    if (mask) mask[IDX4(n, c, py, px, C, OH, OW)] = arg;
-                }
+    MAXPOOL_FWD_BODY(float)
+}
+
+void oracle_maxpool_forward_f64(const double* X, int N, int C, int H, int W,
+                                int kh, int kw, int sh, int sw, int ph, int pw,
+                                double* Y, int32_t* mask) {
+    MAXPOOL_FWD_BODY(double)
 }
 
 /*
  * Max pool backward ("routed to its recorded argmax ... accumulating on
- * overlap"), written as a gather with reading R8's fixed FP32 order:
+ * overlap"), written as a gather with reading R8's fixed order:
  *   dX[n,c,h,w] = sum over (py asc, px asc) with mask[n,c,py,px]==h*W+w of dY[n,c,py,px]
- * Only windows that can contain (h,w) are visited; visiting all windows in the
- * same ascending order gives the same FP32 result because the others add nothing.
+ * Only the windows that can contain (h,w) are visited -- rows py with
+ * py*s-p <= h < py*s-p+k, i.e. ceil((h+p-k+1)/s) <= py <= floor((h+p)/s), clipped
+ * to [0,OH) (same for columns) -- in the same ascending order; the windows
+ * skipped cannot hold h*W+w in their mask and would add nothing.
+ * _f32 sums in float (the GPU's bit-exact order), _f64 in double (oracle/net.py).
  */
+static int win_lo(int h, int k, int s, int p) {   /* smallest py with py*s-p+k > h */
+    int t = h + p - k + 1;
+    int q = t <= 0 ? 0 : (t + s - 1) / s;
+    return q;
+}
+static int win_hi(int h, int s, int p, int O) {   /* largest py with py*s-p <= h, clipped */
+    int q = (h + p) / s;
+    return q < O - 1 ? q : O - 1;
+}
+#define MAXPOOL_BWD_BODY(T)                                                               \
+    int OH = oracle_pool_out_dim(H, kh, sh, ph), OW = oracle_pool_out_dim(W, kw, sw, pw);   \
+    _Pragma("omp parallel for collapse(2) schedule(static)")                              \
+    for (int n = 0; n < N; n++)                                                           \
+        for (int c = 0; c < C; c++)                                                       \
+            for (int h = 0; h < H; h++)                                                   \
+                for (int w = 0; w < W; w++) {                                             \
+                    T acc = 0;                                                            \
+                    int y0 = win_lo(h, kh, sh, ph), y1 = win_hi(h, sh, ph, OH);           \
+                    int x0 = win_lo(w, kw, sw, pw), x1 = win_hi(w, sw, pw, OW);           \
+                    for (int py = y0; py <= y1; py++)                                     \
+                        for (int px = x0; px <= x1; px++) {                               \
+                            int64_t t = IDX4(n, c, py, px, C, OH, OW);                    \
+                            if (mask[t] == h * W + w) acc += dY[t];                       \
+                        }                                                                 \
+                    dX[IDX4(n, c, h, w, C, H, W)] = acc;                                  \
+                }
+
 void oracle_maxpool_backward_f32(const float* dY, const int32_t* mask, int N, int C, int H, int W,
                                  int kh, int kw, int sh, int sw, int ph, int pw, float* dX) {
-    int OH = oracle_pool_out_dim(H, kh, sh, ph), OW = oracle_pool_out_dim(W, kw, sw, pw);
-#pragma omp parallel for collapse(2) schedule(static)
-    for (int n = 0; n < N; n++)
-        for (int c = 0; c < C; c++)
-            for (int h = 0; h < H; h++)
-                for (int w = 0; w < W; w++) {
-                    float acc = 0.0f;
-                    for (int py = 0; py < OH; py++)
-                        for (int px = 0; px < OW; px++) {
-                            int64_t t = IDX4(n, c, py, px, C, OH, OW);
-                            if (mask[t] == h * W + w) acc += dY[t];
-                        }
-                    dX[IDX4(n, c, h, w, C, H, W)] = acc;
-                }
+    MAXPOOL_BWD_BODY(float)
+}
+
+void oracle_maxpool_backward_f64(const double* dY, const int32_t* mask, int N, int C, int H, int W,
+                                 int kh, int kw, int sh, int sw, int ph, int pw, double* dX) {
+    MAXPOOL_BWD_BODY(double)
 }
 
 /*
