@@ -281,6 +281,96 @@ def sgd_update(w, g, v, lr, momentum, decay, grad_scale=1.0):
     return w + v2, v2
 
 
+# ----------------------------------------------------------------------------- catalogue layers (NEXT-4)
+def sigmoid_forward(X):
+    """S:199 logistic nonlinearity ("nonlinearities like rectified linear and logistic"):
+    out = 1 / (1 + e^-x); fp64."""
+    X = _f64(X)
+    return 1.0 / (1.0 + np.exp(-X))
+
+
+def sigmoid_backward(Y, dY):
+    """bottom_diff = top_diff * out * (1 - out), from the forward OUTPUT (the
+    in-place sigmoid keeps only its output); fp64."""
+    Y, dY = _f64(Y), _f64(dY)
+    return dY * Y * (1.0 - Y)
+
+
+def eltwise_forward(inputs, op, coeffs=None):
+    """S:235 element-wise operations: sum = sum_i coeff_i x_i (coeffs default 1), prod =
+    prod_i x_i, max = elementwise max; >= 2 inputs of one shape; fp64, inputs
+    combined in list order."""
+    xs = [_f64(x) for x in inputs]
+    if len(xs) < 2:
+        raise ValueError("eltwise needs at least 2 inputs (S:236)")
+    if any(x.shape != xs[0].shape for x in xs):
+        raise ValueError("eltwise inputs must have identical shapes (S:236)")
+    if op == "sum":
+        c = [1.0] * len(xs) if coeffs is None else [float(v) for v in coeffs]
+        out = c[0] * xs[0]
+        for ci, x in zip(c[1:], xs[1:]):
+            out = out + ci * x
+        return out
+    if op == "prod":
+        out = xs[0].copy()
+        for x in xs[1:]:
+            out = out * x
+        return out
+    if op == "max":
+        out = xs[0].copy()
+        for x in xs[1:]:
+            out = np.where(x > out, x, out)
+        return out
+    raise ValueError(f"unknown eltwise op {op}")
+
+
+def eltwise_backward(inputs, dY, op, coeffs=None):
+    """sum: diff_i = coeff_i dY; prod: diff_i = dY * prod_{j != i} x_j (the product of the
+    other inputs, written out -- no division by x_i); max: dY routed to the per-element argmax
+    input, the FIRST one on ties.  Returns a list of fp64 diffs."""
+    xs = [_f64(x) for x in inputs]
+    dY = _f64(dY)
+    n = len(xs)
+    if op == "sum":
+        c = [1.0] * n if coeffs is None else [float(v) for v in coeffs]
+        return [ci * dY for ci in c]
+    if op == "prod":
+        out = []
+        for i in range(n):
+            p = np.ones_like(dY)
+            for j in range(n):
+                if j != i:
+                    p = p * xs[j]
+            out.append(dY * p)
+        return out
+    if op == "max":
+        arg = np.zeros(dY.shape, np.int64)
+        best = xs[0].copy()
+        for i in range(1, n):
+            better = xs[i] > best          # strict: an equal later input never takes the gradient
+            arg = np.where(better, i, arg)
+            best = np.where(better, xs[i], best)
+        return [np.where(arg == i, dY, 0.0) for i in range(n)]
+    raise ValueError(f"unknown eltwise op {op}")
+
+
+def hinge_loss(scores, labels):
+    """S:271 one-vs-all L1 hinge ("losses like softmax and hinge"): y_nk = +1 if k = l_n else
+    -1; loss = (1/N) sum_{n,k} max(0, 1 - y_nk s_nk); diff_nk = -y_nk [1 - y_nk s_nk > 0] / N.
+    Labels outside [0, K) are an error.  Returns (loss, diff) in fp64."""
+    s = _f64(scores).reshape(scores.shape[0], -1)
+    N, K = s.shape
+    lab = np.asarray(labels).astype(np.int64).reshape(-1)
+    if lab.shape[0] != N or np.any(lab < 0) or np.any(lab >= K):
+        raise ValueError("hinge loss: label out of range (S:273)")
+    y = -np.ones_like(s)
+    y[np.arange(N), lab] = 1.0
+    m = 1.0 - y * s
+    loss = float(np.maximum(m, 0.0).sum() / N)
+    diff = np.where(m > 0, -y, 0.0) / N
+    return loss, diff
+
+
 # ----------------------------------------------------------------------------- operand quantizers
 def quant_bf16(x):
     """Round-to-nearest-even FP32 -> BF16 (reading R12/R14), returned as float32 values."""

@@ -119,8 +119,12 @@ def init_params(layers, in_shape, rng_w):
 
 
 def train_step(layers, X, params, moms, labels, lr=0.01, momentum=0.9, decay=5e-4, quant=None):
-    """Full SGD iteration: forward, backward, update.  Returns loss; updates in place."""
+    """Full SGD iteration: forward, backward, update.  Returns loss; updates in place.
+    A non-finite loss raises solver.DivergenceError before any parameter changes."""
     loss, grads, _ = forward_backward(layers, X, params, labels, quant)
+    if not np.isfinite(loss):
+        from .solver import DivergenceError
+        raise DivergenceError(f"non-finite loss {loss}")
     for name, (W, b) in params.items():
         dW, db = grads[name]
         vW, vb = moms[name]
