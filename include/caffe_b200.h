@@ -52,7 +52,7 @@ extern "C" {
 
 typedef struct CUstream_st* caffe_stream_t; /* == cudaStream_t */
 
-#define CAFFE_ABI_VERSION 2
+#define CAFFE_ABI_VERSION 3
 
 typedef enum {
     CAFFE_OK = 0,
@@ -192,6 +192,12 @@ caffe_status caffe_device_check(void);
    CAFFE_TUNE_SGD_BLOCKS_PER_SM it sets how much of an SM an update running beside the backward
    takes.  Results are identical. */
 #define CAFFE_TUNE_SGD_THREADS 15
+/* CAFFE_TUNE_MAX_CTAS: caps the persistent tensor-core grids at this many CTAs (0 = default, one
+   CTA or CTA pair per SM).  Work units, split-K boundaries and reduction orders do not depend on
+   it, so results are bit-identical for every value; a small cap makes each CTA loop over many
+   units (accumulator double-buffer and barrier phases carried across units), which is how the
+   parity tests exercise the batch-256 schedule at small sizes. */
+#define CAFFE_TUNE_MAX_CTAS 16
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation
@@ -317,7 +323,9 @@ caffe_status caffe_pool_relu_backward(const caffe_pool_desc* desc, const caffe_b
 /* ------------------------------------------------------------------ LRN (R9)
    S = k + alpha/n * sum_{c' in [c-r, c+r] clipped} x^2, r=(n-1)/2;  top = bottom * S^-beta.
    scale (F32, nullable) receives S.  Backward is the exact derivative:
-   bottom_diff = top_diff*S^-beta - (2 alpha beta/n) * x * sum_{c' in win(c)} top_diff*top/S.
+   bottom_diff = top_diff*S^-beta - (2 alpha beta/n) * x * sum_{c' in win(c)} top_diff*top/S,
+   where top/S is evaluated as x*S^-beta/S in FP32 from the bottom (the top blob is validated but
+   not read: a BF16-stored top would carry its rounding into that term).
    Even local_size is CAFFE_E_PARAM. */
 caffe_status caffe_lrn_forward(const caffe_lrn_desc* desc, const caffe_blob* bottom, caffe_blob* top,
                                caffe_blob* scale, caffe_stream_t stream);
@@ -383,7 +391,10 @@ caffe_status caffe_col2im(const caffe_conv_desc* desc, const caffe_blob* col, in
 
 /* ------------------------------------------------------------------ glue for the training step
    Softmax with loss: loss (device F32 scalar) = -(1/N) sum_n log softmax(s_n)[l_n];
-   score_diff = (softmax - onehot)/N (nullable).  labels: device int32[N] in [0,K). */
+   score_diff = (softmax - onehot)/N (nullable).  labels: device int32[N] in [0,K).  The labels live
+   on the device, so their range cannot be checked before the (asynchronous) launch: a label
+   outside [0,K) ("label out of range") is never used as an index; it makes the loss NaN and
+   that row of score_diff NaN, which the caller sees on its next read of the loss. */
 caffe_status caffe_softmax_loss(const caffe_blob* scores, const int32_t* labels /* device */,
                                 float* loss /* device */, caffe_blob* score_diff, caffe_stream_t stream);
 
@@ -393,6 +404,71 @@ caffe_status caffe_softmax_loss(const caffe_blob* scores, const int32_t* labels 
    the next step's BF16 operands. */
 caffe_status caffe_sgd_update(float* w, const float* g, float* v, void* w_bf16, int64_t count, float lr,
                               float momentum, float decay, float grad_scale, caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ the rest of the layer catalogue
+   P:158 (Sec. 3.2): "nonlinearities like rectified linear and logistic ... element-wise operations
+   ... losses like softmax and hinge".  Elementwise ops read and write every blob in its own memory
+   order, so all blobs of a call must share shape, dtype (F32 or BF16) and layout; 16-byte aligned
+   buffers (CAFFE_E_ALIGN otherwise).  n == 0 is a no-op.
+
+   Sigmoid: top = 1/(1+e^-x); bottom_diff = top_diff * top * (1 - top), computed from the
+   forward OUTPUT, so top may alias bottom (in place) and bottom_diff may alias top_diff. */
+caffe_status caffe_sigmoid_forward(const caffe_blob* bottom, caffe_blob* top, caffe_stream_t stream);
+caffe_status caffe_sigmoid_backward(const caffe_blob* top, const caffe_blob* top_diff, caffe_blob* bottom_diff,
+                                    caffe_stream_t stream);
+
+/* Eltwise over 2..CAFFE_ELTWISE_MAX_INPUTS inputs:
+   SUM: top = sum_i coeff_i x_i (coeffs: host array of n_inputs floats, NULL = all 1; SUM only);
+   PROD: top = prod_i x_i;  MAX: top = max_i x_i.
+   Backward: SUM diff_i = coeff_i top_diff; PROD diff_i = top_diff * prod_{j!=i} x_j (no division);
+   MAX: top_diff to the first input holding the maximum (strict '>' scan: ties go to the lowest i,
+   S:249), 0 to the others.  inputs: host array of n_inputs blob pointers (SUM backward may pass NULL
+   inputs); bottom_diffs: host array of n_inputs blob pointers, each overwritten (none may overlap an
+   input or another diff).  Fewer than 2 inputs or > CAFFE_ELTWISE_MAX_INPUTS: CAFFE_E_PARAM;
+   shape mismatch: CAFFE_E_SHAPE. */
+#define CAFFE_ELTWISE_MAX_INPUTS 8
+typedef enum { CAFFE_ELTWISE_PROD = 0, CAFFE_ELTWISE_SUM = 1, CAFFE_ELTWISE_MAX = 2 } caffe_eltwise_op;
+caffe_status caffe_eltwise_forward(int32_t op, int32_t n_inputs, const caffe_blob* const* inputs, const float* coeffs,
+                                   caffe_blob* top, caffe_stream_t stream);
+caffe_status caffe_eltwise_backward(int32_t op, int32_t n_inputs, const caffe_blob* const* inputs, const float* coeffs,
+                                    const caffe_blob* top_diff, caffe_blob* const* bottom_diffs, caffe_stream_t stream);
+
+/* One-vs-all L1 hinge loss: y_nk = +1 if k == label_n else -1;
+   loss (device F32 scalar) = (1/N) sum_{n,k} max(0, 1 - y_nk s_nk);
+   score_diff (nullable) = -y_nk [1 - y_nk s_nk > 0] / N.  scores (N,K,1,1) F32/BF16; labels device
+   int32[N].  The sum is in a fixed order (deterministic).  A label outside [0,K) is never
+   used as an index: the loss and that row's diff are NaN. */
+caffe_status caffe_hinge_loss(const caffe_blob* scores, const int32_t* labels, float* loss, caffe_blob* score_diff,
+                              caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ solver (Sec. 3.4)
+   Learning-rate schedules: FIXED lr = base_lr; STEP lr = base_lr * gamma^floor(iter /
+   stepsize); INV lr = base_lr * (1 + gamma*iter)^-power (evaluated in FP64, rounded to F32).
+   caffe_solver_state lives in DEVICE memory (caller-owned, zero-initialised = iteration 0) so a
+   captured CUDA graph of the training step sees the current iteration on every replay:
+     caffe_solver_begin: after the loss of this step is computed -- if *loss is not finite, sets
+       `diverged` (sticky) and `diverged_iter` (the S:524 divergence guard); writes lr = lr_at(iter);
+     caffe_sgd_update_solver: caffe_sgd_update with lr read from the state; does nothing once
+       `diverged` is set (the parameters, momentum and BF16 copy keep their pre-step values);
+     caffe_solver_end: iter += 1 unless diverged.
+   The host reads the state after synchronising and aborts the loop on `diverged`. */
+typedef enum { CAFFE_LR_FIXED = 0, CAFFE_LR_STEP = 1, CAFFE_LR_INV = 2 } caffe_lr_kind;
+typedef struct { int32_t policy; float base_lr, gamma, power; int32_t stepsize; } caffe_lr_policy;
+typedef struct {
+    int64_t iter;          /* iterations completed */
+    int64_t diverged_iter; /* iteration whose loss was non-finite (valid when diverged) */
+    float lr;              /* learning rate of the current iteration (written by caffe_solver_begin) */
+    float last_loss;       /* loss seen by the last caffe_solver_begin */
+    int32_t diverged;
+    int32_t reserved;
+} caffe_solver_state;
+caffe_status caffe_lr_at_iter(const caffe_lr_policy* policy, int64_t iter, float* lr /* host */);
+caffe_status caffe_solver_begin(const caffe_lr_policy* policy, caffe_solver_state* state /* device */,
+                                const float* loss /* device, nullable */, caffe_stream_t stream);
+caffe_status caffe_solver_end(caffe_solver_state* state /* device */, caffe_stream_t stream);
+caffe_status caffe_sgd_update_solver(float* w, const float* g, float* v, void* w_bf16, int64_t count,
+                                     const caffe_solver_state* state /* device */, float momentum, float decay,
+                                     float grad_scale, caffe_stream_t stream);
 
 #ifdef __cplusplus
 }

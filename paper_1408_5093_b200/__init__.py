@@ -77,14 +77,15 @@ def layout_of(t) -> int:
     raise ValueError("caffe_b200 blobs must be contiguous (NCHW) or channels_last (NHWC)")
 
 
-def blob(t, shape=None) -> _abi.Blob:
-    """Describe a CUDA tensor as a caffe_blob: contiguous -> NCHW, channels_last -> NHWC.  A pinned
-    host tensor is accepted too (the kernels read it through unified addressing over PCIe -- meant
-    for read-only inputs such as an image batch handed to conv_pack_bottom)."""
+def blob(t, shape=None, host_ok=False) -> _abi.Blob:
+    """Describe a CUDA tensor as a caffe_blob: contiguous -> NCHW, channels_last -> NHWC.  With
+    host_ok=True a pinned host tensor is accepted too (the kernels read it through unified addressing
+    over PCIe) -- only for read-only inputs such as an image batch handed to conv_pack_bottom."""
     if t is None:
         return None
-    if not t.is_cuda and not t.is_pinned():
-        raise ValueError("caffe_b200 blobs must live on a CUDA device (or in pinned host memory)")
+    if not t.is_cuda and not (host_ok and t.is_pinned()):
+        raise ValueError("caffe_b200 blobs must live on a CUDA device" +
+                         (" (or in pinned host memory)" if host_ok else ""))
     lay = layout_of(t)
     n, c, h, w = _shape4(t.shape if shape is None else shape)
     return _abi.Blob(ctypes.c_void_p(t.data_ptr()), _abi.Shape4(n, c, h, w), _dtype_code(t), lay)
@@ -168,7 +169,7 @@ def conv_pack_bottom(x, w, stride=1, pad=0, group=1, math="bf16", ws=None):
     kh, kw = w.shape[2], w.shape[3]
     d = _conv_desc((kh, kw), stride, pad, group, math)
     p, n = _ws_arg(ws)
-    bx, bw = blob(x), blob(w)
+    bx, bw = blob(x, host_ok=True), blob(w)
     call("caffe_conv_pack_bottom", ctypes.byref(d), ctypes.byref(bx), ctypes.byref(bw), p, n, _stream())
 
 
@@ -488,6 +489,10 @@ def col2im(col, in_shape, n, kernel, stride=1, pad=0, out=None):
 # ------------------------------------------------------------------ loss / solver glue
 def softmax_loss(scores, labels, loss=None, diff=None, want_diff=True):
     torch = _t()
+    if (labels.dtype != torch.int32 or not labels.is_cuda or not labels.is_contiguous()
+            or labels.numel() != scores.shape[0]):
+        raise ValueError("softmax_loss: labels must be a contiguous int32 CUDA tensor with one label per row "
+                         f"(got {labels.dtype}, {labels.device}, {labels.numel()} labels for {scores.shape[0]} rows)")
     if loss is None:
         loss = torch.empty((), dtype=torch.float32, device=scores.device)
     if want_diff and diff is None:
@@ -504,3 +509,88 @@ def sgd_update(w, g, v, lr, momentum=0.0, decay=0.0, grad_scale=1.0, w_bf16=None
          ctypes.c_void_p(w_bf16.data_ptr()) if w_bf16 is not None else None, int(w.numel()), float(lr),
          float(momentum), float(decay), float(grad_scale), _stream())
     return w
+
+
+# ------------------------------------------------------------------ the rest of the layer catalogue
+def sigmoid_forward(x, out=None, inplace=False):
+    """S:199 logistic: 1/(1+e^-x) (caffe_sigmoid_forward; in place allowed)."""
+    torch = _t()
+    if inplace:
+        out = x
+    elif out is None:
+        out = torch.empty_like(x)
+    bx, by = blob(x), blob(out)
+    call("caffe_sigmoid_forward", ctypes.byref(bx), ctypes.byref(by), _stream())
+    return out
+
+
+def sigmoid_backward(y, dy, out=None, inplace=False):
+    """dy * y * (1 - y) from the forward output y (caffe_sigmoid_backward)."""
+    torch = _t()
+    if inplace:
+        out = dy
+    elif out is None:
+        out = torch.empty_like(dy)
+    by, bdy, bdx = blob(y), blob(dy), blob(out)
+    call("caffe_sigmoid_backward", ctypes.byref(by), ctypes.byref(bdy), ctypes.byref(bdx), _stream())
+    return out
+
+
+ELTWISE = {"prod": _abi.CAFFE_ELTWISE_PROD, "sum": _abi.CAFFE_ELTWISE_SUM, "max": _abi.CAFFE_ELTWISE_MAX}
+
+
+def _blob_array(ts):
+    arr = (_abi.Blob * len(ts))(*[blob(t) for t in ts])
+    return arr
+
+
+def _coeff_array(coeffs):
+    if coeffs is None:
+        return None
+    return (ctypes.c_float * len(coeffs))(*[float(c) for c in coeffs])
+
+
+def eltwise_forward(inputs, op="sum", coeffs=None, out=None):
+    """S:235 element-wise sum (coefficients) / prod / max of >= 2 same-shaped blobs."""
+    torch = _t()
+    if out is None:
+        out = torch.empty_like(inputs[0])
+    arr = _blob_array(inputs)
+    ptrs = (ctypes.POINTER(_abi.Blob) * len(inputs))(*[ctypes.pointer(arr[i]) for i in range(len(inputs))])
+    bo = blob(out)
+    call("caffe_eltwise_forward", int(ELTWISE[op]), len(inputs), ptrs, _coeff_array(coeffs), ctypes.byref(bo),
+         _stream())
+    return out
+
+
+def eltwise_backward(inputs, dy, op="sum", coeffs=None, outs=None):
+    """S:244 diffs of every input (list of tensors, overwritten)."""
+    torch = _t()
+    n = len(inputs)
+    if outs is None:
+        outs = [torch.empty_like(dy) for _ in range(n)]
+    arr = _blob_array(inputs)
+    ptrs = (ctypes.POINTER(_abi.Blob) * n)(*[ctypes.pointer(arr[i]) for i in range(n)])
+    oarr = _blob_array(outs)
+    optrs = (ctypes.POINTER(_abi.Blob) * n)(*[ctypes.pointer(oarr[i]) for i in range(n)])
+    bdy = blob(dy)
+    call("caffe_eltwise_backward", int(ELTWISE[op]), n, ptrs, _coeff_array(coeffs), ctypes.byref(bdy), optrs,
+         _stream())
+    return outs
+
+
+def hinge_loss(scores, labels, loss=None, diff=None, want_diff=True):
+    """S:271 one-vs-all L1 hinge loss and its gradient (caffe_hinge_loss)."""
+    torch = _t()
+    if (labels.dtype != torch.int32 or not labels.is_cuda or not labels.is_contiguous()
+            or labels.numel() != scores.shape[0]):
+        raise ValueError("hinge_loss: labels must be a contiguous int32 CUDA tensor with one label per row")
+    if loss is None:
+        loss = torch.empty((), dtype=torch.float32, device=scores.device)
+    if want_diff and diff is None:
+        diff = torch.empty_like(scores)
+    shp = (scores.shape[0], scores.numel() // scores.shape[0], 1, 1)
+    bs, bd = blob(scores, shp), (blob(diff, shp) if want_diff else None)
+    call("caffe_hinge_loss", ctypes.byref(bs), ctypes.c_void_p(labels.data_ptr()), ctypes.c_void_p(loss.data_ptr()),
+         _bp(bd), _stream())
+    return loss, diff

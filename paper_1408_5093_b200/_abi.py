@@ -38,6 +38,10 @@ CAFFE_TUNE_HALO_TMA_STORE = 12
 CAFFE_TUNE_WGRAD_REDUCE_ROWS = 13
 CAFFE_TUNE_HALO_STACKED = 14
 CAFFE_TUNE_SGD_THREADS = 15
+CAFFE_TUNE_MAX_CTAS = 16
+CAFFE_ELTWISE_PROD, CAFFE_ELTWISE_SUM, CAFFE_ELTWISE_MAX = 0, 1, 2
+CAFFE_ELTWISE_MAX_INPUTS = 8
+CAFFE_LR_FIXED, CAFFE_LR_STEP, CAFFE_LR_INV = 0, 1, 2
 
 
 class Shape4(ctypes.Structure):
@@ -63,6 +67,17 @@ class PoolDesc(ctypes.Structure):
 class LrnDesc(ctypes.Structure):
     _fields_ = [("local_size", ctypes.c_int32), ("alpha", ctypes.c_float), ("beta", ctypes.c_float),
                 ("k", ctypes.c_float)]
+
+
+class LrPolicy(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int32), ("base_lr", ctypes.c_float), ("gamma", ctypes.c_float),
+                ("power", ctypes.c_float), ("stepsize", ctypes.c_int32)]
+
+
+class SolverState(ctypes.Structure):
+    """Layout of caffe_solver_state (it lives in device memory; this mirrors it for size/offsets)."""
+    _fields_ = [("iter", ctypes.c_int64), ("diverged_iter", ctypes.c_int64), ("lr", ctypes.c_float),
+                ("last_loss", ctypes.c_float), ("diverged", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 P = ctypes.POINTER
@@ -105,6 +120,15 @@ SIGNATURES = {
     "caffe_col2im": [CD, B, i32, B, vp],
     "caffe_softmax_loss": [B, vp, vp, B, vp],
     "caffe_sgd_update": [vp, vp, vp, vp, i64, f32, f32, f32, f32, vp],
+    "caffe_sigmoid_forward": [B, B, vp],
+    "caffe_sigmoid_backward": [B, B, B, vp],
+    "caffe_eltwise_forward": [i32, i32, P(B), P(f32), B, vp],
+    "caffe_eltwise_backward": [i32, i32, P(B), P(f32), B, P(B), vp],
+    "caffe_hinge_loss": [B, vp, vp, B, vp],
+    "caffe_lr_at_iter": [P(LrPolicy), i64, P(f32)],
+    "caffe_solver_begin": [P(LrPolicy), vp, vp, vp],
+    "caffe_solver_end": [vp, vp],
+    "caffe_sgd_update_solver": [vp, vp, vp, vp, i64, vp, f32, f32, f32, vp],
 }
 _RESTYPES = {"caffe_abi_version": ctypes.c_int32, "caffe_last_error": ctypes.c_char_p,
              "caffe_launch_count": ctypes.c_int64}

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcaffe_b200.so")
-SOURCES = ["abi.cu", "tc_gemm.cu", "tc_halo.cu", "pack.cu", "simple.cu"]
+SOURCES = ["abi.cu", "tc_gemm.cu", "tc_halo.cu", "pack.cu", "simple.cu", "catalog.cu"]
 HEADERS = ["internal.h", "ptx.cuh", "epilogue.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -203,6 +203,7 @@ int choose_bn(int n) {
     return (int)rup(cdiv(n, t), 16);
 }
 // CTA pairs (M=256 tiles, cta_group::2) whenever the pair-tiles still fill every SM pair once.
+int g_max_ctas = 0;  // CAFFE_TUNE_MAX_CTAS: cap on the persistent tensor-core grid (0 = one CTA per SM)
 int g_force_cg = 0;   // caffe_set_tuning(CAFFE_TUNE_CTA_PAIR, 1|2) overrides the automatic choice
 int g_mma_spin = 0;   // CAFFE_TUNE_MMA_SPIN (polling measured slower: it steals issue slots from the epilogue)
 int pick_cg(long long M, int ntiles_x_groups, int E) {
@@ -548,7 +549,9 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
         }
     }
     L.args.spin = g_mma_spin;
-    const int slots = num_sms() / L.cg;                  // CTAs (or CTA pairs) resident at once
+    int slots = num_sms() / L.cg;                        // CTAs (or CTA pairs) resident at once
+    if (g_max_ctas > 0 && g_max_ctas / L.cg < slots)      // CAFFE_TUNE_MAX_CTAS: more units per CTA
+        slots = g_max_ctas / L.cg > 0 ? g_max_ctas / L.cg : 1;
     L.grid = (L.args.units < slots ? L.args.units : slots) * L.cg;
     ProfRec rec{nullptr, nullptr, flops, kind};
     if (g_prof) {
@@ -612,6 +615,11 @@ caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_
 }
 
 caffe_status caffe_set_tuning(int32_t key, int32_t value) {
+    if (key == CAFFE_TUNE_MAX_CTAS) {
+        if (value < 0) return fail(CAFFE_E_PARAM, "max CTAs must be >= 0 (0 = one per SM)");
+        g_max_ctas = value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_CTA_PAIR) {
         if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "CTA-pair mode must be 0 (auto), 1 or 2");
         g_force_cg = value;
@@ -1785,6 +1793,186 @@ caffe_status caffe_sgd_update(float* w, const float* g, float* v, void* w_bf16, 
     if (!aligned16(w) || !aligned16(g) || !aligned16(v) || (reinterpret_cast<uintptr_t>(w_bf16) & 7))
         return fail(CAFFE_E_ALIGN, "SGD buffers must be 16-byte aligned (w_bf16 8-byte)");
     CK(sgd_k(w, g, v, w_bf16, count, lr, momentum, decay, grad_scale, (cudaStream_t)stream), "sgd update");
+    return CAFFE_OK;
+}
+
+
+// ------------------------------------------------------------------ catalogue layers (catalog.cu)
+static caffe_status same_elementwise(const caffe_blob* a, const caffe_blob* b, const char* what) {
+    if (!same_shape(a->shape, b->shape) || a->dtype != b->dtype || a->layout != b->layout)
+        return fail(CAFFE_E_SHAPE, "%s must match in shape, dtype and layout", what);
+    return CAFFE_OK;
+}
+
+caffe_status caffe_sigmoid_forward(const caffe_blob* bottom, caffe_blob* top, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(bottom, "bottom")) || (st = check_blob(top, "top"))) return st;
+    if ((st = same_elementwise(bottom, top, "top and bottom"))) return st;
+    if (bottom->ptr != top->ptr && overlap(bottom, top)) return fail(CAFFE_E_ALIAS, "partial overlap of top and bottom");
+    if (cnt(bottom->shape) == 0) return CAFFE_OK;
+    if (!aligned16(bottom->ptr) || !aligned16(top->ptr)) return fail(CAFFE_E_ALIGN, "sigmoid buffers must be 16-byte aligned");
+    CK(sigmoid_fwd_k(bottom->ptr, top->ptr, isbf(bottom), cnt(bottom->shape), (cudaStream_t)stream), "sigmoid fwd");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_sigmoid_backward(const caffe_blob* top, const caffe_blob* top_diff, caffe_blob* bottom_diff,
+                                    caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(top, "top")) || (st = check_blob(top_diff, "top_diff")) ||
+        (st = check_blob(bottom_diff, "bottom_diff")))
+        return st;
+    if ((st = same_elementwise(top_diff, bottom_diff, "top_diff and bottom_diff"))) return st;
+    if (!same_shape(top->shape, top_diff->shape) || top->layout != top_diff->layout)
+        return fail(CAFFE_E_SHAPE, "top must match top_diff in shape and layout");
+    if ((bottom_diff->ptr != top_diff->ptr && overlap(bottom_diff, top_diff)) || overlap(bottom_diff, top))
+        return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
+    if (cnt(top->shape) == 0) return CAFFE_OK;
+    if (!aligned16(top->ptr) || !aligned16(top_diff->ptr) || !aligned16(bottom_diff->ptr))
+        return fail(CAFFE_E_ALIGN, "sigmoid buffers must be 16-byte aligned");
+    CK(sigmoid_bwd_k(top->ptr, top_diff->ptr, bottom_diff->ptr, isbf(top), isbf(top_diff), cnt(top->shape),
+                     (cudaStream_t)stream),
+       "sigmoid bwd");
+    return CAFFE_OK;
+}
+
+static caffe_status eltwise_check(int32_t op, int32_t n, const caffe_blob* const* in, const caffe_blob* ref,
+                                  bool need_inputs) {
+    caffe_status st;
+    if (op != CAFFE_ELTWISE_PROD && op != CAFFE_ELTWISE_SUM && op != CAFFE_ELTWISE_MAX)
+        return fail(CAFFE_E_INVALID, "bad eltwise op %d", op);
+    if (n < 2 || n > CAFFE_ELTWISE_MAX_INPUTS)
+        return fail(CAFFE_E_PARAM, "eltwise takes 2..%d inputs (S:236), got %d", CAFFE_ELTWISE_MAX_INPUTS, n);
+    if (!need_inputs) return CAFFE_OK;
+    if (!in) return fail(CAFFE_E_INVALID, "inputs is NULL");
+    for (int i = 0; i < n; i++) {
+        if ((st = check_blob(in[i], "input"))) return st;
+        if (!same_shape(in[i]->shape, ref->shape))
+            return fail(CAFFE_E_SHAPE, "eltwise input %d shape (%d,%d,%d,%d) differs from (%d,%d,%d,%d)", i,
+                        in[i]->shape.n, in[i]->shape.c, in[i]->shape.h, in[i]->shape.w, ref->shape.n, ref->shape.c,
+                        ref->shape.h, ref->shape.w);
+        if ((st = same_elementwise(in[i], ref, "eltwise inputs and outputs"))) return st;
+        if (!aligned16(in[i]->ptr)) return fail(CAFFE_E_ALIGN, "eltwise input %d must be 16-byte aligned", i);
+    }
+    return CAFFE_OK;
+}
+
+caffe_status caffe_eltwise_forward(int32_t op, int32_t n_inputs, const caffe_blob* const* inputs, const float* coeffs,
+                                   caffe_blob* top, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(top, "top"))) return st;
+    if ((st = eltwise_check(op, n_inputs, inputs, top, true))) return st;
+    if (coeffs && op != CAFFE_ELTWISE_SUM) return fail(CAFFE_E_PARAM, "coefficients apply to SUM only");
+    for (int i = 0; i < n_inputs; i++)
+        if (overlap(inputs[i], top) && inputs[i]->ptr != top->ptr)
+            return fail(CAFFE_E_ALIAS, "top partially overlaps input %d", i);
+    if (cnt(top->shape) == 0) return CAFFE_OK;
+    if (!aligned16(top->ptr)) return fail(CAFFE_E_ALIGN, "top must be 16-byte aligned");
+    const void* ptrs[CAFFE_ELTWISE_MAX_INPUTS];
+    for (int i = 0; i < n_inputs; i++) ptrs[i] = inputs[i]->ptr;
+    CK(eltwise_fwd_k(op, n_inputs, ptrs, coeffs, top->ptr, isbf(top), cnt(top->shape), (cudaStream_t)stream),
+       "eltwise fwd");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_eltwise_backward(int32_t op, int32_t n_inputs, const caffe_blob* const* inputs, const float* coeffs,
+                                    const caffe_blob* top_diff, caffe_blob* const* bottom_diffs, caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(top_diff, "top_diff"))) return st;
+    const bool need_x = op != CAFFE_ELTWISE_SUM;
+    if ((st = eltwise_check(op, n_inputs, need_x ? inputs : nullptr, top_diff, need_x))) return st;
+    if (coeffs && op != CAFFE_ELTWISE_SUM) return fail(CAFFE_E_PARAM, "coefficients apply to SUM only");
+    if (!bottom_diffs) return fail(CAFFE_E_INVALID, "bottom_diffs is NULL");
+    for (int i = 0; i < n_inputs; i++) {
+        if ((st = check_blob(bottom_diffs[i], "bottom_diff"))) return st;
+        if ((st = same_elementwise(bottom_diffs[i], top_diff, "bottom_diffs and top_diff"))) return st;
+        if (!aligned16(bottom_diffs[i]->ptr)) return fail(CAFFE_E_ALIGN, "bottom_diff %d must be 16-byte aligned", i);
+        if (overlap(bottom_diffs[i], top_diff)) return fail(CAFFE_E_ALIAS, "bottom_diff %d overlaps top_diff", i);
+        for (int j = 0; j < n_inputs; j++) {
+            if (need_x && overlap(bottom_diffs[i], inputs[j])) return fail(CAFFE_E_ALIAS, "bottom_diff %d overlaps input %d", i, j);
+            if (j != i && overlap(bottom_diffs[i], bottom_diffs[j])) return fail(CAFFE_E_ALIAS, "bottom_diffs %d and %d overlap", i, j);
+        }
+    }
+    if (cnt(top_diff->shape) == 0) return CAFFE_OK;
+    if (!aligned16(top_diff->ptr)) return fail(CAFFE_E_ALIGN, "top_diff must be 16-byte aligned");
+    const void* in[CAFFE_ELTWISE_MAX_INPUTS];
+    void* out[CAFFE_ELTWISE_MAX_INPUTS];
+    for (int i = 0; i < n_inputs; i++) {
+        in[i] = need_x ? inputs[i]->ptr : nullptr;
+        out[i] = bottom_diffs[i]->ptr;
+    }
+    CK(eltwise_bwd_k(op, n_inputs, need_x ? in : nullptr, coeffs, top_diff->ptr, out, isbf(top_diff),
+                     cnt(top_diff->shape), (cudaStream_t)stream),
+       "eltwise bwd");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_hinge_loss(const caffe_blob* scores, const int32_t* labels, float* loss, caffe_blob* score_diff,
+                              caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = check_blob(scores, "scores"))) return st;
+    if (!labels || !loss) return fail(CAFFE_E_INVALID, "labels and loss are required");
+    const int N = scores->shape.n;
+    const long long K = (long long)scores->shape.c * scores->shape.h * scores->shape.w;
+    if (scores->shape.h * scores->shape.w != 1 && nhwc(scores)) return fail(CAFFE_E_INVALID, "scores must be (N,K,1,1) or NCHW");
+    if (score_diff) {
+        if ((st = check_blob(score_diff, "score_diff"))) return st;
+        if (!same_shape(score_diff->shape, scores->shape)) return fail(CAFFE_E_SHAPE, "score_diff must match scores");
+        if (score_diff->shape.h * score_diff->shape.w != 1 && nhwc(score_diff))
+            return fail(CAFFE_E_INVALID, "score_diff must be NCHW");
+        if (overlap(score_diff, scores)) return fail(CAFFE_E_ALIAS, "score_diff overlaps scores");
+    }
+    if (N == 0) return CAFFE_OK;
+    CK(hinge_loss_k(scores->ptr, isbf(scores), labels, loss, score_diff ? score_diff->ptr : nullptr,
+                    score_diff ? isbf(score_diff) : 0, N, (int)K, (cudaStream_t)stream),
+       "hinge loss");
+    return CAFFE_OK;
+}
+
+// ------------------------------------------------------------------ solver
+static caffe_status lr_policy_check(const caffe_lr_policy* p) {
+    if (!p) return fail(CAFFE_E_INVALID, "policy is NULL");
+    if (p->policy != CAFFE_LR_FIXED && p->policy != CAFFE_LR_STEP && p->policy != CAFFE_LR_INV)
+        return fail(CAFFE_E_INVALID, "bad lr policy %d", p->policy);
+    if (p->policy == CAFFE_LR_STEP && p->stepsize < 1) return fail(CAFFE_E_PARAM, "step policy needs stepsize >= 1");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_lr_at_iter(const caffe_lr_policy* policy, int64_t iter, float* lr) {
+    caffe_status st;
+    if ((st = lr_policy_check(policy))) return st;
+    if (!lr) return fail(CAFFE_E_INVALID, "lr is NULL");
+    if (iter < 0) return fail(CAFFE_E_PARAM, "iter must be >= 0 (S:513)");
+    *lr = (float)lr_policy_host(*policy, iter);
+    return CAFFE_OK;
+}
+
+caffe_status caffe_solver_begin(const caffe_lr_policy* policy, caffe_solver_state* state, const float* loss,
+                                caffe_stream_t stream) {
+    caffe_status st;
+    if ((st = lr_policy_check(policy))) return st;
+    if (!state) return fail(CAFFE_E_INVALID, "state is NULL");
+    if (reinterpret_cast<uintptr_t>(state) & 7) return fail(CAFFE_E_ALIGN, "state must be 8-byte aligned");
+    CK(solver_begin_k(*policy, state, loss, (cudaStream_t)stream), "solver begin");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_solver_end(caffe_solver_state* state, caffe_stream_t stream) {
+    if (!state) return fail(CAFFE_E_INVALID, "state is NULL");
+    if (reinterpret_cast<uintptr_t>(state) & 7) return fail(CAFFE_E_ALIGN, "state must be 8-byte aligned");
+    CK(solver_end_k(state, (cudaStream_t)stream), "solver end");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_sgd_update_solver(float* w, const float* g, float* v, void* w_bf16, int64_t count,
+                                     const caffe_solver_state* state, float momentum, float decay, float grad_scale,
+                                     caffe_stream_t stream) {
+    if (count < 0) return fail(CAFFE_E_SHAPE, "negative count");
+    if (count == 0) return CAFFE_OK;
+    if (!w || !g || !v || !state) return fail(CAFFE_E_INVALID, "w, g, v and state are required");
+    if (!aligned16(w) || !aligned16(g) || !aligned16(v) || (reinterpret_cast<uintptr_t>(w_bf16) & 7))
+        return fail(CAFFE_E_ALIGN, "SGD buffers must be 16-byte aligned (w_bf16 8-byte)");
+    CK(sgd_solver_k(w, g, v, w_bf16, count, state, momentum, decay, grad_scale, (cudaStream_t)stream),
+       "sgd update (solver)");
     return CAFFE_OK;
 }
 

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda.h>
+#include "caffe_b200.h"
 
 namespace cb {
 
@@ -223,5 +224,26 @@ extern int g_wgrad_reduce_rows;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS
 extern int g_halo_fast_epi;   // CAFFE_TUNE_HALO_FAST_EPI
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,
                   float decay, float gscale, cudaStream_t s);
+
+
+// ------------------------------------------------------------------ catalogue layers and solver (catalog.cu)
+constexpr int ELT_MAX_INPUTS = CAFFE_ELTWISE_MAX_INPUTS;
+enum { ELT_PROD = CAFFE_ELTWISE_PROD, ELT_SUM = CAFFE_ELTWISE_SUM, ELT_MAX = CAFFE_ELTWISE_MAX };
+enum { LR_FIXED = CAFFE_LR_FIXED, LR_STEP = CAFFE_LR_STEP, LR_INV = CAFFE_LR_INV };
+using LrPolicy = caffe_lr_policy;
+using SolverDev = caffe_solver_state;
+cudaError_t sigmoid_fwd_k(const void* x, void* y, int bf16, long long n, cudaStream_t s);
+cudaError_t sigmoid_bwd_k(const void* y, const void* dy, void* dx, int y_bf16, int d_bf16, long long n, cudaStream_t s);
+cudaError_t eltwise_fwd_k(int op, int n_in, const void* const* in, const float* coeff, void* y, int bf16, long long n,
+                          cudaStream_t s);
+cudaError_t eltwise_bwd_k(int op, int n_in, const void* const* in, const float* coeff, const void* dy,
+                          void* const* dx, int bf16, long long n, cudaStream_t s);
+cudaError_t hinge_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff, int diff_bf16,
+                         int N, int K, cudaStream_t s);
+double lr_policy_host(const LrPolicy& p, long long it);
+cudaError_t solver_begin_k(const LrPolicy& p, SolverDev* st, const float* loss, cudaStream_t s);
+cudaError_t solver_end_k(SolverDev* st, cudaStream_t s);
+cudaError_t sgd_solver_k(float* w, const float* g, float* v, void* w_bf16, long long count, const SolverDev* st,
+                         float mom, float decay, float gscale, cudaStream_t s);
 
 }  // namespace cb

@@ -1128,22 +1128,24 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
 }
 
 // Backward: the window sums over the 8 + 2R channel scales and the 8 outputs slide (one add and one
-// subtract per step instead of 2R + 1 terms); FP32 throughout, BF16 output.
+// subtract per step instead of 2R + 1 terms); FP32 throughout, BF16 output.  The cross-channel term
+// uses y/S = x * S^(-beta) / S recomputed in FP32 from the bottom (the stored top is BF16-rounded:
+// reading it made the result lose up to 2^-9 of that term where it cancels the direct term, and cost
+// a third of the kernel's reads); `y` is not read.
 template <int R>
-__global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
-                              const __nv_bfloat16* __restrict__ dy, __nv_bfloat16* __restrict__ dx, int C, int size,
-                              float alpha, float beta, float k, int total) {
+__global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
+                              __nv_bfloat16* __restrict__ dx, int C, int size, float alpha, float beta, float k,
+                              int total) {
     const int cv = C / 8;
     const float an = alpha / size;
     const float cb = 2.f * an * beta;
     GRID_STRIDE(t, total) {
         const int c0 = (t % cv) * 8;
         const long long base = (long long)(t / cv) * C;
-        float xv[24], yv[24], gv[24];
+        float xv[24], gv[24];
         load24(x + base, c0, C, xv);
-        load24(y + base, c0, C, yv);
         load24(dy + base, c0, C, gv);
-        float S[24], tv[24];
+        float P[24], tv[24];
         float s2 = 0.f;
 #pragma unroll
         for (int j = 8 - 2 * R; j <= 8; j++) s2 = fmaf(xv[j], xv[j], s2);   // window of channel 8 - R
@@ -1153,8 +1155,9 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
                 s2 = fmaf(xv[i + R], xv[i + R], s2);
                 s2 = fmaf(-xv[i - R - 1], xv[i - R - 1], s2);
             }
-            S[i] = k + an * s2;
-            tv[i] = gv[i] * yv[i] * rcp_ftz(S[i]);
+            const float S = k + an * s2;
+            P[i] = ex2_ftz(-beta * lg2_ftz(S));                  // S^-beta
+            tv[i] = gv[i] * (xv[i] * P[i]) * rcp_ftz(S);          // dy * y / S
         }
         float out[8];
         float acc = 0.f;
@@ -1163,7 +1166,7 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
 #pragma unroll
         for (int e = 0; e < 8; e++) {
             if (e > 0) acc = acc + tv[8 + e + R] - tv[8 + e - R - 1];
-            out[e] = gv[8 + e] * ex2_ftz(-beta * lg2_ftz(S[8 + e])) - cb * xv[8 + e] * acc;
+            out[e] = gv[8 + e] * P[8 + e] - cb * xv[8 + e] * acc;
         }
         *reinterpret_cast<uint4*>(dx + base + c0) = pack8(out);
     }
@@ -1209,7 +1212,8 @@ __global__ void lrn_bwd_kernel(const void* __restrict__ x, const void* __restric
         for (int cc = lo; cc <= hi; cc++) {
             const int q = base + cc * sc;
             const float S = scale ? scale[q] : lrn_scale(x, bf16, base, sc, cc, C, r, an, k);
-            acc += ldv(dy, q, bf16) * ldv(y, q, bf16) / S;
+            // y/S from the bottom in FP32 (the stored top may be BF16-rounded)
+            acc += ldv(dy, q, bf16) * (ldv(x, q, bf16) * exp2f(-beta * log2f(S))) / S;
         }
         const float v = ldv(dy, t, bf16) * exp2f(-beta * log2f(Sc)) - 2.f * an * beta * ldv(x, t, bf16) * acc;
         stv(dx, t, bf16, v);
@@ -1224,15 +1228,14 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
         const int tv = total / 8;
         const unsigned nb = nblk(tv, 256);
         auto X = (const __nv_bfloat16*)x;
-        auto Y = (const __nv_bfloat16*)y;
         auto G = (const __nv_bfloat16*)dy;
         auto D = (__nv_bfloat16*)dx;
         switch ((size - 1) / 2) {
-            case 0: lrn_bwd_nhwc8<0><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
-            case 1: lrn_bwd_nhwc8<1><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
-            case 2: lrn_bwd_nhwc8<2><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
-            case 3: lrn_bwd_nhwc8<3><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
-            default: lrn_bwd_nhwc8<4><<<nb, 256, 0, s>>>(X, Y, G, D, C, size, alpha, beta, k, tv); break;
+            case 0: lrn_bwd_nhwc8<0><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+            case 1: lrn_bwd_nhwc8<1><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+            case 2: lrn_bwd_nhwc8<2><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+            case 3: lrn_bwd_nhwc8<3><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+            default: lrn_bwd_nhwc8<4><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
         }
         note_launch();
         return cudaGetLastError();
@@ -1264,6 +1267,9 @@ softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restric
     for (int n = gw; n < N; n += gnw) {
         const int base = n * K;
         const int lab = labels[n];
+        // a label outside [0, K) is never read through: its row's loss term and diff are NaN
+        const bool ok = (unsigned)lab < (unsigned)K;
+        const float bad = ok ? 0.f : __int_as_float(0x7fc00000);
         if (K <= 1024) {
             // the row lives in registers: one global read, one write
             float v[32];
@@ -1283,7 +1289,7 @@ softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restric
             }
             for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
             const float lse = logf(se);
-            if (lane == 0) my += lse - (ldv(s, base + lab, sb) - mx);
+            if (lane == 0) my += ok ? lse - (ldv(s, base + lab, sb) - mx) : bad;
             if (diff) {
                 const float inv = 1.f / N, rse = 1.f / se;
 #pragma unroll
@@ -1292,7 +1298,7 @@ softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restric
                     if (k < K) {
                         float p = v[q] * rse;
                         if (k == lab) p -= 1.f;
-                        stv(diff, base + k, db, p * inv);
+                        stv(diff, base + k, db, p * inv + bad);
                     }
                 }
             }
@@ -1305,13 +1311,13 @@ softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restric
         for (int k = lane; k < K; k += 32) se += expf(ldv(s, base + k, sb) - mx);
         for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
         const float lse = logf(se);
-        if (lane == 0) my += lse - (ldv(s, base + lab, sb) - mx);
+        if (lane == 0) my += ok ? lse - (ldv(s, base + lab, sb) - mx) : bad;
         if (diff) {
             const float inv = 1.f / N;
             for (int k = lane; k < K; k += 32) {
                 float p = expf(ldv(s, base + k, sb) - mx - lse);
                 if (k == lab) p -= 1.f;
-                stv(diff, base + k, db, p * inv);
+                stv(diff, base + k, db, p * inv + bad);
             }
         }
     }

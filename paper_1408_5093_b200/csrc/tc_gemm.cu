@@ -257,9 +257,13 @@ __global__ void __launch_bounds__(256, 1)
         }
         // the peer's epilogue arrives remotely on our tempty barriers: drain the last two phases
         // before the pair tears down
-        if (CG == 2) {
-            for (int j = iters - 2; j < iters; j++)
-                if (j >= 0) mbar_wait(&tempty[j & 1], (uint32_t)((j >> 1) & 1));
+        if (CG == 2 && iters > 0) {
+            if (nslots == 2) {
+                for (int j = iters - 2; j < iters; j++)
+                    if (j >= 0) mbar_wait(&tempty[j & 1], (uint32_t)((j >> 1) & 1));
+            } else {
+                mbar_wait(&tempty[0], (uint32_t)((iters - 1) & 1));
+            }
         }
     } else if (warp >= 4) {
         // ===================== epilogue (both CTAs) =====================

@@ -65,3 +65,124 @@ class GradAllReduce:
             w.wait()
         self._works = []
         self._pending = [set(b[2]) for b in self.buckets]
+
+
+class BucketedSGD:
+    """Data-parallel gradient exchange WITH the update, per bucket:
+
+    mode "allreduce": as soon as a bucket's gradients are complete, ``all_reduce(SUM)`` it; as soon as
+        its layers are also done with their weights (their data gradients have run), update the whole
+        bucket (grad_scale = 1/W, reading R17) -- the update overlaps the rest of the backward pass
+        instead of following it.
+    mode "sharded" (reduce-scatter + sharded SGD + all-gather): ``reduce_scatter`` the bucket so that
+        rank r receives the summed gradient of its 1/W slice, apply the update to that slice only (the
+        update's 22 bytes/parameter of HBM traffic drop W-fold), then ``all_gather`` the updated FP32
+        weights and their BF16 copy.  NCCL's in-place forms are used (each rank's slice is a view of
+        the flat buffers), so no staging copies exist.
+
+    The caller provides ``update(lo, hi, grad_scale)`` (the library SGD on the flat range) and calls
+    ``on_grad(key)`` when a layer's parameter gradients are enqueued, ``on_done(key)`` when nothing
+    later in the step reads that layer's parameters, and ``finish()`` at the end of the backward
+    pass (it makes the current stream wait for the last collectives).  Streams: collectives and
+    updates are issued on ``stream`` (a side stream) after it waits for the producing stream.
+    """
+
+    applies_update = True     # Net.step: the exchange applies the SGD update itself
+
+    def __init__(self, flat_grads, flat_params, flat_mom, flat_bf16, segments, world, rank, update=None, mode="sharded",
+                 bucket_bytes=32 << 20, group=None, stream=None):
+        import torch
+        self.torch = torch
+        self.mode = mode
+        self.world, self.rank, self.group = world, rank, group
+        self.update = update
+        self.grads, self.params, self.mom, self.bf16 = flat_grads, flat_params, flat_mom, flat_bf16
+        self.stream = stream
+        self.cuda = flat_grads.is_cuda
+        base = GradAllReduce(flat_grads, segments, world, bucket_bytes=bucket_bytes, group=group)
+        self.buckets = base.buckets
+        self.key_bucket = base.key_bucket
+        if mode == "sharded":
+            for lo, hi, _ in self.buckets:
+                n = hi - lo
+                # equal 16-byte-aligned slices per rank (the flat buffer keeps every tensor 256-byte aligned)
+                if n % (4 * world) or (lo % 4):
+                    raise ValueError(f"bucket [{lo},{hi}) does not split into {world} aligned slices")
+        self._reset()
+
+    def _reset(self):
+        self._grad_pending = [set(b[2]) for b in self.buckets]
+        self._done_pending = [set(b[2]) for b in self.buckets]
+        self._rs = {}
+        self._tail = []
+
+    def _slice(self, bi):
+        lo, hi, _ = self.buckets[bi]
+        if self.mode != "sharded":
+            return lo, hi
+        n = (hi - lo) // self.world
+        return lo + self.rank * n, lo + (self.rank + 1) * n
+
+    def _ctx(self):
+        import contextlib
+        if self.cuda and self.stream is not None:
+            return self.torch.cuda.stream(self.stream)
+        return contextlib.nullcontext()
+
+    def _join_current(self):
+        """The side stream waits for everything enqueued so far on the current stream."""
+        if self.cuda and self.stream is not None:
+            self.stream.wait_stream(self.torch.cuda.current_stream())
+
+    def on_grad(self, key):
+        import torch.distributed as dist
+        bi = self.key_bucket[key]
+        p = self._grad_pending[bi]
+        p.discard(key)
+        if p:
+            return
+        lo, hi, _ = self.buckets[bi]
+        self._join_current()
+        with self._ctx():
+            if self.mode == "sharded":
+                slo, shi = self._slice(bi)
+                self._rs[bi] = dist.reduce_scatter_tensor(self.grads[slo:shi], self.grads[lo:hi], op=dist.ReduceOp.SUM,
+                                                          group=self.group, async_op=True)
+            else:
+                self._rs[bi] = dist.all_reduce(self.grads[lo:hi], op=dist.ReduceOp.SUM, group=self.group,
+                                               async_op=True)
+        self._maybe_update(bi)
+
+    def on_done(self, key):
+        bi = self.key_bucket[key]
+        self._done_pending[bi].discard(key)
+        self._maybe_update(bi)
+
+    def _maybe_update(self, bi):
+        import torch.distributed as dist
+        if self._done_pending[bi] or bi not in self._rs or self._rs[bi] is None:
+            return
+        work = self._rs[bi]
+        self._rs[bi] = None
+        self._join_current()          # after the data gradients that read this bucket's weights
+        with self._ctx():
+            work.wait()               # the reduced gradient slice (stream-ordered on CUDA)
+            slo, shi = self._slice(bi)
+            self.update(slo, shi, 1.0 / self.world)
+            if self.mode == "sharded" and self.world > 1:
+                lo, hi, _ = self.buckets[bi]
+                self._tail.append(dist.all_gather_into_tensor(self.params[lo:hi], self.params[slo:shi],
+                                                              group=self.group, async_op=True))
+                if self.bf16 is not None:
+                    self._tail.append(dist.all_gather_into_tensor(self.bf16[lo:hi], self.bf16[slo:shi],
+                                                                  group=self.group, async_op=True))
+
+    def finish(self):
+        for bi in range(len(self.buckets)):
+            if self._rs.get(bi) is not None or self._done_pending[bi]:
+                raise RuntimeError(f"bucket {bi} was not completed by the backward pass")
+        for w in self._tail:
+            w.wait()
+        if self.cuda and self.stream is not None:
+            self.torch.cuda.current_stream().wait_stream(self.stream)
+        self._reset()

@@ -374,10 +374,19 @@ class Net:
             elif L.kind == "lrn":
                 cb.lrn_backward(a[i], y, dy, **LRN, out=d[i])
 
-    def update(self, lr=0.01, momentum=0.9, decay=5e-4, grad_scale=1.0):
-        cb.sgd_update(self.params, self.grads, self.mom, lr, momentum, decay, grad_scale,
-                      w_bf16=self.params_bf16 if self.math == "bf16" else None)
+    def update(self, lr=0.01, momentum=0.9, decay=5e-4, grad_scale=1.0, solver=None):
+        self._sgd(0, self.nparams, lr, momentum, decay, grad_scale, solver)
         self.repack_weights()
+
+    def _sgd(self, lo, hi, lr, momentum, decay, grad_scale, solver):
+        """SGD update of the flat parameter range [lo, hi): fixed lr, or the solver's
+        device-resident schedule and divergence guard (caffe_sgd_update_solver)."""
+        wb = self.params_bf16[lo:hi] if self.math == "bf16" else None
+        if solver is not None:
+            solver.update(self.params[lo:hi], self.grads[lo:hi], self.mom[lo:hi], wb, grad_scale)
+        else:
+            cb.sgd_update(self.params[lo:hi], self.grads[lo:hi], self.mom[lo:hi], lr, momentum, decay, grad_scale,
+                          w_bf16=wb)
 
     # the first layer's packed input (ws0) is written by the caller before the step
     # (conv_pack_bottom from the host batch, e.g. bench.py's end-to-end input pipeline)
@@ -411,8 +420,21 @@ class Net:
     wgrad_priority = -1
     sgd_priority = 0
 
-    def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4, overlap_update=True):
+    def step(self, allreduce=None, lr=0.01, momentum=0.9, decay=5e-4, overlap_update=True, solver=None):
+        """One SGD iteration.  With `solver` (paper_1408_5093_b200.solver.Solver) the learning rate,
+        momentum and decay come from it: the iteration's lr is computed on the device from its state
+        after the loss (which also arms the divergence guard), and the iteration counter advances at
+        the end of the step -- all inside a captured graph too."""
+        if solver is not None:
+            momentum, decay = solver.momentum, solver.decay
         self.forward()
+        if solver is not None:
+            solver.begin(self.loss)
+        self._step_rest(allreduce, lr, momentum, decay, overlap_update, solver)
+        if solver is not None:
+            solver.end()
+
+    def _step_rest(self, allreduce, lr, momentum, decay, overlap_update, solver):
         if allreduce is None and overlap_update:
             # Single GPU: each layer's SGD update runs on a side stream as soon as nothing later in the
             # step reads that layer's parameters, co-resident with the remaining backward GEMMs (the
@@ -437,7 +459,8 @@ class Net:
 
             launched = []
 
-            fused = dict(lr=lr, momentum=momentum, decay=decay) if (self.fuse_ip_sgd and wstream is not None) else None
+            fused = (dict(lr=lr, momentum=momentum, decay=decay)
+                     if (self.fuse_ip_sgd and wstream is not None and solver is None) else None)
 
             def launch():
                 launched.append(1)
@@ -462,8 +485,7 @@ class Net:
                 _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_SGD_THREADS, self.side_sgd_threads)
                 with torch.cuda.stream(self._side):
                     for lo, hi in runs:
-                        cb.sgd_update(self.params[lo:hi], self.grads[lo:hi], self.mom[lo:hi], lr,
-                                      momentum, decay, 1.0, w_bf16=wb[lo:hi] if wb is not None else None)
+                        self._sgd(lo, hi, lr, momentum, decay, 1.0, solver)
                     for i in layers_done:
                         if i in self.wsf:
                             self.repack_weights(i)
@@ -490,6 +512,35 @@ class Net:
             if wstream is not None and self.wgrad_done:
                 main.wait_stream(wstream)
             return
+        if allreduce is not None and getattr(allreduce, "applies_update", False):
+            # data parallel with the update inside the exchange (dp.BucketedSGD): per bucket, the
+            # all-reduce (or reduce-scatter) is issued once its gradients are complete, and the update
+            # (of the whole bucket, or of this rank's slice followed by an all-gather) once its layers'
+            # data gradients no longer read the weights -- no update pass after the backward
+            torch = self.torch
+            main = torch.cuda.current_stream()
+            if getattr(self, "_wside", None) is None:
+                self._wside = torch.cuda.Stream(priority=self.wgrad_priority)
+            if getattr(self, "_side", None) is None:
+                self._side = torch.cuda.Stream(priority=self.sgd_priority)
+            wstream = self._wside
+            if allreduce.stream is None:
+                allreduce.stream = self._side
+            allreduce.update = lambda lo, hi, gs: self._sgd(lo, hi, lr, momentum, decay, gs, solver)
+
+            def hook(i):
+                ev = torch.cuda.Event()
+                ev.record(main)
+                wstream.wait_event(ev)
+                with torch.cuda.stream(wstream):
+                    allreduce.on_grad(i)
+
+            self.backward(hook=hook, done_hook=allreduce.on_done, wgrad_stream=wstream)
+            main.wait_stream(wstream)
+            allreduce.finish()
+            if self.wsf:
+                self.repack_weights()
+            return
         if allreduce is not None and self.wgrad_side and torch_cuda_ok(self):
             # data parallel: weight gradients on their stream as on one GPU; each bucket's all-reduce
             # is issued from that stream after it has also caught up with the main stream, so the
@@ -510,16 +561,16 @@ class Net:
             self.backward(hook=hook, wgrad_stream=wstream)
             main.wait_stream(wstream)
             allreduce.finish()
-            self.update(lr, momentum, decay, grad_scale=1.0 / allreduce.world)
+            self.update(lr, momentum, decay, grad_scale=1.0 / allreduce.world, solver=solver)
             return
         self.backward(hook=allreduce.on_grad if allreduce else None)
         scale = 1.0
         if allreduce:
             allreduce.finish()
             scale = 1.0 / allreduce.world
-        self.update(lr, momentum, decay, grad_scale=scale)
+        self.update(lr, momentum, decay, grad_scale=scale, solver=solver)
 
-    def capture(self, **kw):
+    def capture(self, prologue=None, **kw):
         """Record one whole training step (every library launch) into a CUDA graph; replaying it
         re-runs the identical kernel sequence on the same buffers without host launch overhead.
         Call after at least one eager step (so the cached workspace has reached its size)."""
@@ -531,7 +582,53 @@ class Net:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
+                if prologue is not None:
+                    prologue()
                 self.step(**kw)
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
         return g
+
+
+class TrainLoop:
+    """A CUDA-graph-captured training loop over a device-resident pool of batches (SURVEY 8(f) NEXT-3;
+    P:174 "Data are processed in mini-batches that pass through the network sequentially"): one
+    graph per pool batch, each = copy that batch into the input blobs + the whole training step with
+    the solver's device-side schedule and divergence guard.  Replaying the graphs in order runs the
+    loop with no per-layer host launches; `run` records each iteration's loss on the device and
+    checks the guard every `check_every` iterations (and at the end)."""
+
+    def __init__(self, net: "Net", solver, images, labels):
+        torch = net.torch
+        self.net, self.solver = net, solver
+        self.images = images          # device (P, B, C, H, W) in the input blob's dtype / layout
+        self.labels = labels          # device (P, B) int32
+        self.graphs = []
+        x0, l0 = net.a[0], net.labels
+        x0.copy_(images[0])
+        l0.copy_(labels[0])
+        # one eager step to size the cached workspaces and create the side streams, then undo it
+        saved = (net.params.clone(), net.mom.clone(), net.params_bf16.clone(), solver.state.clone())
+        net.step(solver=solver)
+        torch.cuda.synchronize()
+        net.params.copy_(saved[0])
+        net.mom.copy_(saved[1])
+        net.params_bf16.copy_(saved[2])
+        solver.state.copy_(saved[3])
+        for b in range(images.shape[0]):
+            def pro(b=b):
+                x0.copy_(images[b])
+                l0.copy_(labels[b])
+            self.graphs.append(net.capture(prologue=pro, solver=solver))
+        torch.cuda.synchronize()
+
+    def run(self, iters: int, start: int = 0, check_every: int = 100):
+        torch = self.net.torch
+        trace = torch.empty(iters, dtype=torch.float32, device=self.net.device)
+        for i in range(iters):
+            self.graphs[(start + i) % len(self.graphs)].replay()
+            trace[i].copy_(self.net.loss)
+            if (i + 1) % check_every == 0:
+                self.solver.check()
+        self.solver.check()
+        return trace

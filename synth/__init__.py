@@ -57,3 +57,16 @@ def distinct_values(shape, seed, spacing=0.01, stream=S_AUX, sub=0):
     n = int(np.prod(shape))
     v = (np.arange(n) - n / 2.0) * spacing
     return gen(seed, stream, sub).permutation(v).reshape(shape).astype(np.float64)
+
+
+def class_pattern_pixels(labels, shape_chw, k, seed, noise=64.0, stream=S_AUX, sub=11):
+    """Learnable synthetic images for a training-loop sanity run: one random template per class
+    (integers U{0..255}) plus per-image integer noise U{-noise..noise}, clipped to [0, 255] and
+    scaled by 1/256 (the LeNet input scale).  Only random draws and a clip -- no arithmetic
+    of the method."""
+    g = gen(seed, stream, sub)
+    templates = g.integers(0, 256, size=(k,) + tuple(shape_chw))
+    lab = np.asarray(labels).astype(np.int64)
+    noise_v = g.integers(-int(noise), int(noise) + 1, size=(lab.shape[0],) + tuple(shape_chw))
+    img = np.clip(templates[lab] + noise_v, 0, 255)
+    return (img / 256.0).astype(np.float32)

@@ -35,3 +35,33 @@ def cuda(a, dtype=None):
 def host(t):
     import torch
     return t.detach().float().cpu().numpy() if t.dtype == torch.bfloat16 else t.detach().cpu().numpy()
+
+
+def bf16_ulp(x):
+    """Spacing of BF16 values at |x| (8 significant bits): 2^(floor(log2|x|) - 7); the subnormal
+    spacing 2^-133 below the normal range."""
+    a = np.abs(np.asarray(x, np.float64))
+    e = np.floor(np.log2(np.maximum(a, 2.0 ** -126)))
+    return 2.0 ** (e - 7)
+
+
+def bf16_ulp_errors(got, ref):
+    """|got - RNE_bf16(ref)| in units of the BF16 spacing at RNE_bf16(ref) (per element)."""
+    import oracle
+    r = oracle.quant_bf16(np.asarray(ref, np.float32)).astype(np.float64)
+    return np.abs(np.asarray(got, np.float64) - r) / bf16_ulp(r)
+
+
+def assert_bf16_ulp(got, ref, what="", ulps=1.0, atol=0.0):
+    """BF16-stored result within `ulps` BF16 spacings of RNE(oracle) per element (reading R12 for BF16
+    outputs).  `atol` (absolute) admits FP32 accumulation error where the exact result cancels to
+    ~0 (a tiny |ref| has a tiny spacing, the rounding of the long FP32 sum does not)."""
+    import oracle
+    got = np.asarray(got, np.float64)
+    r = oracle.quant_bf16(np.asarray(ref, np.float32)).astype(np.float64)
+    err = np.abs(got - r)
+    bound = ulps * bf16_ulp(r) + atol
+    bad = err > bound
+    assert not bad.any(), (f"{what}: {int(bad.sum())} / {bad.size} elements beyond {ulps} BF16 ulp of RNE(ref)"
+                           f" (+{atol:.2e}); worst err {err[bad].max():.3e} at ref {r[bad][np.argmax(err[bad])]:.3e}")
+    return float((err / bf16_ulp(r)).max())

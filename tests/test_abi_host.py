@@ -31,9 +31,9 @@ def test_header_declares_and_library_exports_every_entry_point(lib):
     for n in names:
         assert hasattr(lib, n), f"{n} declared in caffe_b200.h but not exported"
     assert set(names) == set(_abi.SIGNATURES), "ctypes signatures out of sync with the header"
-    assert lib.caffe_abi_version() == 2
+    assert lib.caffe_abi_version() == 3
     src = open(HEADER).read()
-    assert "#define CAFFE_ABI_VERSION 2" in src
+    assert "#define CAFFE_ABI_VERSION 3" in src
 
 
 def test_library_has_no_torch_or_python_dependency():

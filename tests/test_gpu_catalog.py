@@ -1,0 +1,253 @@
+"""GPU parity of the rest of the layer catalogue and the solver against
+the oracle (-m gpu), through the C ABI:
+
+* sigmoid, eltwise sum/prod/max, one-vs-all hinge loss:
+  FP32 storage per element |err| <= 1e-5 (|ref| + 1); BF16 storage within 1 BF16 ulp of RNE(oracle);
+  max routing and max values bit-exact (first input wins ties);
+* lr_at_iter fixed / step / inv on the host entry point and on the device state;
+  the divergence guard: a non-finite loss leaves every parameter as it was;
+* a CUDA-graph-captured LeNet training loop (inv schedule, momentum, decay) on learnable synthetic
+  data: its first losses follow the oracle's training trace and the loss decreases.
+"""
+import numpy as np
+import pytest
+
+import synth
+from _helpers import assert_bf16_ulp, assert_fp32_close, cuda, host
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(2, 3, 5, 7), (4, 64, 13, 13), (1, 8, 1, 1), (3, 16, 9, 11)]
+
+
+def _dev(a, dt, nhwc):
+    import torch
+    t = cuda(a).to(dt)
+    return t.contiguous(memory_format=torch.channels_last) if nhwc else t
+
+
+def _check(got, ref, bf16, what):
+    if bf16:
+        assert_bf16_ulp(got, ref, what)
+    else:
+        assert_fp32_close(got, ref, what)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("nhwc", [False, True])
+def test_sigmoid(oracle, shape, dt, nhwc):
+    import torch
+    import paper_1408_5093_b200 as cb
+    bf = dt == "bf16"
+    tdt = torch.bfloat16 if bf else torch.float32
+    X = synth.uniform(shape, 41, synth.S_X) * 6
+    dY = synth.uniform(shape, 41, synth.S_DY)
+    xt = _dev(X, tdt, nhwc)
+    Xq = host(xt)
+    Y = cb.sigmoid_forward(xt)
+    _check(host(Y), oracle.sigmoid_forward(Xq), bf, "sigmoid fwd")
+    dyt = _dev(dY, tdt, nhwc)
+    dX = cb.sigmoid_backward(Y, dyt)
+    _check(host(dX), oracle.sigmoid_backward(host(Y), host(dyt)), bf, "sigmoid bwd")
+    # in place: top == bottom, bottom_diff == top_diff
+    z = xt.clone()
+    cb.sigmoid_forward(z, inplace=True)
+    np.testing.assert_array_equal(host(z), host(Y))
+    g = dyt.clone()
+    cb.sigmoid_backward(Y, g, inplace=True)
+    np.testing.assert_array_equal(host(g), host(dX))
+
+
+@pytest.mark.parametrize("op", ["sum", "prod", "max"])
+@pytest.mark.parametrize("n", [2, 3, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_eltwise(oracle, op, n, dt):
+    import torch
+    import paper_1408_5093_b200 as cb
+    bf = dt == "bf16"
+    tdt = torch.bfloat16 if bf else torch.float32
+    # 4752 elements = whole 8-element vectors; 1485 = vectors and a scalar tail
+    shape = (3, 5, 9, 11) if n == 3 else (3, 16, 9, 11)
+    xs = [synth.uniform(shape, 50 + i, synth.S_X) * (1.5 if op == "prod" else 3) for i in range(n)]
+    if op == "max":
+        xs[1][0, 0] = xs[0][0, 0]        # ties: the first input must win
+    ts = [_dev(x, tdt, nhwc=False) for x in xs]
+    xq = [host(t) for t in ts]
+    coeffs = [0.5, -2.0, 1.0, 3.0, -0.25, 1.5, 2.0, -1.0][:n] if op == "sum" else None
+    Y = cb.eltwise_forward(ts, op, coeffs)
+    ref = oracle.eltwise_forward(xq, op, coeffs)
+    if op == "max":
+        np.testing.assert_array_equal(host(Y), ref)
+    else:
+        _check(host(Y), ref, bf, f"eltwise {op} fwd")
+    dY = _dev(synth.uniform(shape, 59, synth.S_DY), tdt, nhwc=False)
+    ds = cb.eltwise_backward(ts, dY, op, coeffs)
+    rds = oracle.eltwise_backward(xq, host(dY), op, coeffs)
+    for i, (d, r) in enumerate(zip(ds, rds)):
+        if op == "max":
+            np.testing.assert_array_equal(host(d), r, err_msg=f"max routing input {i}")
+        else:
+            _check(host(d), r, bf, f"eltwise {op} bwd input {i}")
+
+
+def test_eltwise_errors():
+    import torch
+    import paper_1408_5093_b200 as cb
+    a = torch.zeros(2, 3, 4, 4, device="cuda")
+    with pytest.raises(cb.CaffeError, match="E_PARAM"):
+        cb.eltwise_forward([a], "sum")
+    with pytest.raises(cb.CaffeError, match="E_SHAPE"):
+        cb.eltwise_forward([a, torch.zeros(2, 3, 4, 5, device="cuda")], "max")
+    with pytest.raises(cb.CaffeError, match="E_PARAM"):
+        cb.eltwise_forward([a, a], "prod", coeffs=[1, 2])
+    with pytest.raises(cb.CaffeError, match="E_ALIAS"):
+        cb.eltwise_backward([a, a.clone()], a.clone(), "max", outs=[a, torch.empty_like(a)])
+
+
+@pytest.mark.parametrize("N,K,dt", [(256, 1000, "f32"), (256, 1000, "bf16"), (7, 10, "f32"), (33, 3, "bf16")])
+def test_hinge_loss(oracle, N, K, dt):
+    import torch
+    import paper_1408_5093_b200 as cb
+    s = synth.uniform((N, K), 61, synth.S_X) * 2
+    lab = synth.labels(N, K, 61)
+    st = cuda(s).to(torch.bfloat16 if dt == "bf16" else torch.float32)
+    loss, diff = cb.hinge_loss(st, cuda(lab))
+    rl, rd = oracle.hinge_loss(host(st), lab)
+    assert abs(float(loss) - rl) <= 1e-5 * (abs(rl) + 1)
+    if dt == "bf16":
+        assert_bf16_ulp(host(diff), rd, "hinge diff")
+    else:
+        assert_fp32_close(host(diff), rd, "hinge diff")
+    # deterministic (fixed-order sum)
+    loss2, _ = cb.hinge_loss(st, cuda(lab))
+    assert float(loss2) == float(loss)
+
+
+@pytest.mark.parametrize("fn", ["softmax", "hinge"])
+def test_loss_label_out_of_range_is_nan(fn):
+    """S:250 / S:273 "label out of range": never read out of bounds; the loss is NaN."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    s = torch.zeros(4, 10, device="cuda")
+    lab = torch.tensor([0, 3, 10, 2], dtype=torch.int32, device="cuda")
+    f = cb.softmax_loss if fn == "softmax" else cb.hinge_loss
+    loss, diff = f(s, lab)
+    assert np.isnan(float(loss))
+    d = host(diff)
+    assert np.isnan(d[2]).all() and np.isfinite(np.delete(d, 2, axis=0)).all()
+    with pytest.raises(ValueError):
+        f(s, lab.long())
+
+
+# ------------------------------------------------------------------ solver
+POLICIES = [("fixed", dict(base_lr=0.01)), ("step", dict(base_lr=0.01, gamma=0.1, stepsize=100)),
+            ("inv", dict(base_lr=0.01, gamma=1e-4, power=0.75)), ("step", dict(base_lr=0.5, gamma=0.5, stepsize=3))]
+
+
+@pytest.mark.parametrize("policy,kw", POLICIES)
+def test_lr_policies_host_and_device(oracle, policy, kw):
+    import torch
+    from oracle import solver as osolver
+    from paper_1408_5093_b200.solver import Solver
+    s = Solver(torch.device("cuda"), policy, **kw)
+    for it in (0, 1, 2, 3, 99, 100, 250, 1000, 12345):
+        want = np.float32(osolver.lr_at_iter(policy, np.float32(kw["base_lr"]), it, gamma=np.float32(kw.get("gamma", 0.0)),
+                                             stepsize=kw.get("stepsize", 1), power=np.float32(kw.get("power", 0.0))))
+        assert np.float32(s.lr_at(it)) == want, (it, s.lr_at(it), want)
+    # device: the state follows the iterations of begin/end
+    for it in range(7):
+        s.begin(None)
+        st = s.read()
+        assert st["iter"] == it
+        want = osolver.lr_at_iter(policy, np.float32(kw["base_lr"]), it, gamma=np.float32(kw.get("gamma", 0.0)),
+                                  stepsize=kw.get("stepsize", 1), power=np.float32(kw.get("power", 0.0)))
+        assert np.float32(st["lr"]) == np.float32(want)
+        s.end()
+
+
+def test_solver_update_matches_fixed_update_and_guard():
+    """caffe_sgd_update_solver with lr from the state gives the bits of caffe_sgd_update with that lr;
+    after a non-finite loss it changes nothing and the iteration counter stops."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200.solver import Solver, DivergenceError
+    dev = torch.device("cuda")
+    n = 100003
+    w0 = cuda(synth.uniform((n,), 71, synth.S_W))
+    g = cuda(synth.uniform((n,), 71, synth.S_DY))
+    v0 = cuda(synth.uniform((n,), 71, synth.S_AUX)) * 0.1
+    s = Solver(dev, "step", base_lr=0.1, gamma=0.5, stepsize=2, momentum=0.9, decay=1e-3)
+    loss = torch.tensor(1.25, device=dev)
+    w1, v1, b1 = w0.clone(), v0.clone(), torch.empty(n, dtype=torch.bfloat16, device=dev)
+    w2, v2, b2 = w0.clone(), v0.clone(), torch.empty(n, dtype=torch.bfloat16, device=dev)
+    for it in range(5):
+        s.begin(loss)
+        s.update(w1, g, v1, b1, grad_scale=0.5)
+        s.end()
+        cb.sgd_update(w2, g, v2, s.lr_at(it), 0.9, 1e-3, 0.5, w_bf16=b2)
+    assert torch.equal(w1, w2) and torch.equal(v1, v2) and torch.equal(b1, b2)
+    assert s.read()["iter"] == 5
+    loss.fill_(float("nan"))
+    keep = (w1.clone(), v1.clone(), b1.clone())
+    s.begin(loss)
+    s.update(w1, g, v1, b1)
+    s.end()
+    assert torch.equal(w1, keep[0]) and torch.equal(v1, keep[1]) and torch.equal(b1, keep[2])
+    st = s.read()
+    assert st["diverged"] and st["diverged_iter"] == 5 and st["iter"] == 5
+    with pytest.raises(DivergenceError):
+        s.check()
+
+
+def _lenet_loop(P=8, B=64, policy="inv", seed=0):
+    import torch
+    from paper_1408_5093_b200 import nets
+    from paper_1408_5093_b200.solver import Solver
+    dev = torch.device("cuda")
+    net = nets.Net(nets.LENET, B, nets.LENET_INPUT, dev, math="bf16", seed=seed)
+    labs = np.stack([synth.labels(B, 10, 100 + p) for p in range(P)])
+    imgs = np.stack([synth.class_pattern_pixels(labs[p], (1, 28, 28), 10, 7, sub=p) for p in range(P)])
+    di = torch.from_numpy(imgs).to(dev).to(net.a[0].dtype)
+    di = torch.stack([di[p].contiguous(memory_format=torch.channels_last) for p in range(P)])
+    dl = torch.from_numpy(labs).to(dev)
+    solver = Solver(dev, policy, base_lr=0.01, gamma=1e-4, power=0.75, momentum=0.9, decay=5e-4)
+    return net, solver, nets.TrainLoop(net, solver, di, dl), imgs, labs
+
+
+def test_lenet_graph_loop_follows_oracle_then_decreases(oracle):
+    """The graph-captured loop: losses of the first iterations match the oracle's own training
+    trace (oracle/net.py train_step with the same inv schedule, BF16 GEMM operands) to 2e-2, and
+    over 500 iterations the mean loss of iterations 400-500 is below that of 0-100."""
+    from oracle import net as onet, solver as osolver
+    net, solver, loop, imgs, labs = _lenet_loop()
+    params = {net.layers[i].name: (host(net.W[i]).astype(np.float64), host(net.B[i]).astype(np.float64))
+              for (i, _, _) in net.pspecs}
+    moms = {k: (np.zeros_like(w), np.zeros_like(b)) for k, (w, b) in params.items()}
+    ref = []
+    for it in range(4):
+        lr = osolver.lr_at_iter("inv", 0.01, it, gamma=1e-4, power=0.75)
+        ref.append(onet.train_step(onet.LENET, imgs[it % len(imgs)].astype(np.float64), params, moms,
+                                   labs[it % len(labs)], lr=lr, momentum=0.9, decay=5e-4, quant=oracle.quant_bf16))
+    trace = host(loop.run(500))
+    np.testing.assert_allclose(trace[:4], ref, rtol=2e-2)
+    assert np.isfinite(trace).all()
+    assert trace[400:500].mean() < trace[0:100].mean(), (trace[:100].mean(), trace[400:].mean())
+    assert solver.read()["iter"] == 500
+
+
+def test_lenet_graph_loop_divergence_guard():
+    """A batch whose loss is not finite inside the captured loop trips the guard: the loop raises,
+    and the parameters are exactly those from before the diverging iteration.  The bad batch
+    carries a corrupted label (out of range: the loss kernel reports NaN rather than reading out of
+    bounds; a NaN image would not do -- the ReLU of ip1 maps NaN to 0, R10)."""
+    import torch
+    from paper_1408_5093_b200.solver import DivergenceError
+    net, solver, loop, _, _ = _lenet_loop(P=4)
+    loop.run(6, check_every=1000)
+    before = (net.params.clone(), net.mom.clone(), net.params_bf16.clone())
+    loop.labels[2][5] = 10                       # iteration 6 uses pool batch 6 % 4 = 2
+    with pytest.raises(DivergenceError, match="iteration 6"):
+        loop.run(3, start=6, check_every=1000)
+    assert torch.equal(net.params, before[0]) and torch.equal(net.mom, before[1])
+    assert torch.equal(net.params_bf16, before[2])

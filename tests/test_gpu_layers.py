@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import synth
-from _helpers import assert_fp32_close, assert_tc_close, cuda, host
+from _helpers import assert_bf16_ulp, assert_fp32_close, assert_tc_close, cuda, host
 
 pytestmark = pytest.mark.gpu
 
@@ -246,12 +246,15 @@ def test_pool_lrn_nhwc_bf16_vector_paths(oracle, shape):
     for size, a, b, k in ((5, 1e-4, 0.75, 1.0), (3, 0.5, 0.75, 2.0), (9, 2.0, 1.3, 1.0)):
         L, S = cb.lrn_forward(xh, size, a, b, k, want_scale=True)
         rL, rS = oracle.lrn_forward(X, size, a, b, k, want_scale=True)
-        assert_tc_close(host(L), q(rL.astype(np.float32)), f"lrn fwd bf16 nhwc n={size}", tol=2e-3)
+        assert_bf16_ulp(host(L), rL, f"lrn fwd bf16 nhwc n={size}")
         assert_fp32_close(host(S), rS, "lrn scale")
         G = q(synth.uniform(shape, 15, synth.S_DY))
         dL = cb.lrn_backward(xh, L, cuda(G).to(torch.bfloat16).contiguous(memory_format=cl), size, a, b, k)
         rdL = oracle.lrn_backward(X, G, size, a, b, k)
-        assert_tc_close(host(dL), rdL, f"lrn bwd bf16 nhwc n={size}", tol=5e-3)
+        assert_tc_close(host(dL), q(rdL.astype(np.float32)), f"lrn bwd bf16 nhwc n={size}")
+        # the kernel reads the stored BF16 top in the cross-channel term: admit its rounding where the
+        # direct term cancels
+        assert_bf16_ulp(host(dL), rdL, f"lrn bwd bf16 nhwc n={size}", atol=float(np.abs(rdL).max()) * 2.0 ** -16)
 
 
 @pytest.mark.parametrize("shape", [(8, 16, 3, 3, 10), (256, 256, 6, 6, 512)])
@@ -355,10 +358,16 @@ def test_ip_backward_data_relu(oracle, N, K, O, math, act, nhwc):
     cb.relu_backward(top, ref, inplace=True)
     got = cb.ip_backward_data_relu(dY, Wt, top, math=math)
     np.testing.assert_array_equal(host(got), host(ref))
-    want = (host(dY).astype(np.float64) @ host(Wt).astype(np.float64)).reshape(N, -1)
-    mask = host(top).reshape(N, -1) > 0 if not nhwc else (host(top) > 0).reshape(N, -1)
-    g = host(got).reshape(N, -1)
-    assert_tc_close(g, want * mask, "masked ip dgrad", tol=5e-3)
+    qd = oracle.quant_bf16 if math == "bf16" else (lambda a: a)
+    rdX, _, _ = oracle.ip_backward(host(top), host(Wt), qd(host(dY)))
+    want = oracle.relu_backward(host(top), rdX.reshape(top.shape))
+    if act == "bf16":
+        rms = float(np.sqrt(np.mean(np.square(want))))
+        assert_bf16_ulp(host(got), want, "masked ip dgrad (BF16 out)", atol=rms * 2.0 ** -12)
+    elif math == "fp32":
+        assert_fp32_close(host(got), want, "masked ip dgrad fp32")
+    else:
+        assert_tc_close(host(got), want, "masked ip dgrad")
     with pytest.raises(RuntimeError):
         cb.ip_backward_data_relu(dY, Wt, top[:1], math=math)
 
@@ -400,7 +409,9 @@ def test_ip_backward_weight_sgd_fused(oracle, N, bshape, O):
     xr = host(x).astype(np.float64).reshape(N, -1)
     g = host(dy).astype(np.float64).T @ xr
     w_o, v_o = oracle.sgd_update(host(W0).astype(np.float64), g, host(V0).astype(np.float64), lr, mom, decay, gs)
-    assert_tc_close(host(Wf) - host(W0), w_o - host(W0), "fused update step", tol=2e-3)
+    assert_fp32_close(host(Wf), w_o, "fused update: weights")
+    assert_fp32_close(host(Vf), v_o, "fused update: momentum")
+    assert_tc_close(host(Vf), v_o, "fused update: momentum rel-L2")
 
 
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
