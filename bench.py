@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dp-mode", default="sharded", choices=["sharded", "allreduce", "grad_allreduce"],
+                    help="N > 1 exchange: reduce-scatter + sharded SGD + all-gather (default), per-bucket "
+                         "all-reduce + update, or all-reduce then one update")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     return ap.parse_args()
 
@@ -263,8 +266,14 @@ def main():
     lab = synth.labels(B, 1000, 1000 + rank)
     net.a[0].copy_(torch.from_numpy(X).to(net.a[0].dtype))
     net.labels.copy_(torch.from_numpy(lab))
-    from paper_1408_5093_b200.dp import GradAllReduce
-    ar = GradAllReduce(net.grads, net.segments, world) if world > 1 else None
+    from paper_1408_5093_b200.dp import BucketedSGD, GradAllReduce
+    ar = None
+    if world > 1:
+        if args.dp_mode == "grad_allreduce":
+            ar = GradAllReduce(net.grads, net.segments, world)
+        else:   # per-bucket exchange with the update inside it (sharded: reduce-scatter + 1/W SGD + all-gather)
+            ar = BucketedSGD(net.grads, net.params, net.mom, net.params_bf16, net.segments, world, rank,
+                             mode=args.dp_mode)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -276,13 +285,19 @@ def main():
         net.step(ar)
     barrier()
     loss0 = float(net.loss)
-    # CUDA graph of the whole step (N=1): replay removes the host launch overhead of ~30 ABI calls
-    use_graph = world == 1 and not args.no_graph
+    # CUDA graph of the whole step (the NCCL collectives of N > 1 included): replay removes the host
+    # launch overhead of ~30 ABI calls and the per-bucket collective calls
+    use_graph = not args.no_graph
+    graph_note = None
     if use_graph:
-        net.capture(allreduce=None)
-        for _ in range(2):
-            net.graph.replay()
-        barrier()
+        try:
+            net.capture(allreduce=ar)
+            for _ in range(2):
+                net.graph.replay()
+            barrier()
+        except Exception as e:   # e.g. a collective backend that cannot be captured: run eagerly
+            use_graph, graph_note = False, f"capture failed, eager steps: {type(e).__name__}: {str(e)[:120]}"
+            torch.cuda.synchronize()
 
     def run_step():
         if use_graph:
@@ -360,6 +375,8 @@ def main():
                 "measured_in": "instrumented eager pass of the same K steps (events around each GEMM launch)"}
     extra = {
         "graph": use_graph,
+        "graph_note": graph_note,
+        "dp_mode": args.dp_mode if world > 1 else None,
         "eager_ms_per_step": ms_eager / args.steps,
         "conv_gemm_ms_per_step": g_ms.value / args.steps,
         "ip_gemm_ms_per_step": i_ms.value / args.steps,
@@ -387,7 +404,7 @@ def main():
             graphs = [net.graph]
             a0 = net.a[0]
             net.a[0] = dstage[1]
-            graphs.append(net.capture(allreduce=None))
+            graphs.append(net.capture(allreduce=ar))
             net.a[0] = a0
             net.graph = graphs[0]
             barrier()

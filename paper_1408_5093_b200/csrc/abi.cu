@@ -400,7 +400,7 @@ size_t ws_partial(const Plan& p) {
 
 size_t conv_ws(const Plan& p, int pass, caffe_math m) {
     if (pass == CAFFE_PASS_BACKWARD_WEIGHT) {
-        if (m == CAFFE_MATH_FP32 || m == CAFFE_MATH_TF32) return ws_bias(p);
+        if (m == CAFFE_MATH_FP32) return ws_bias(p);
         return ws_x_max(p) + ws_dy_max(p) + ws_partial(p) + ws_bias(p);
     }
     if (m == CAFFE_MATH_FP32) return 0;
@@ -1023,15 +1023,15 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
     if ((st = check_ws(ws, ws_bytes, need))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     char* w8 = (char*)ws;
-    // TF32 weight gradient: CUDA-core FP32 FMA on TF32-rounded operands (the MN-major TF32
-    // tensor-core operand layout is not built); FP32: the same kernel without rounding.
-    if (desc->math == CAFFE_MATH_FP32 || desc->math == CAFFE_MATH_TF32) {
+    // FP32 math: CUDA-core FP32 FMA (blocked reduction, R13).  TF32 runs on the tensor cores below
+    // (tcgen05.mma kind::tf32 with MN-major operands: both packed TF32-RN, as in the other passes).
+    if (desc->math == CAFFE_MATH_FP32) {
         if (bias_diff)
             CK(bias_grad(top_diff->ptr, isbf(top_diff), nhwc(top_diff), (float*)bias_diff->ptr, beta, p.N, p.O,
                          p.OH * p.OW, (float*)w8, s),
                "bias grad");
         CK(fp32_conv_wgrad(bottom->ptr, isbf(bottom), strides(bottom), top_diff->ptr, isbf(top_diff), strides(top_diff),
-                           (float*)weight_diff->ptr, beta, cgeom(p), s, desc->math == CAFFE_MATH_TF32),
+                           (float*)weight_diff->ptr, beta, cgeom(p), s, 0),
            "conv wgrad fp32");
         return CAFFE_OK;
     }
@@ -1350,9 +1350,9 @@ static IpPlan ip_plan_fwd(long long N, long long K, int O, int E) {
     const int BN = choose_bn(O);
     return ip_plan(N, O, K, 128 / E, BN, E, (BN / 2) % 8 == 0);
 }
-static IpPlan ip_plan_dgrad(long long N, long long K, int O) {
-    const int BN = choose_bn((int)(K < 256 ? K : 256));
-    return ip_plan(N, K, O, 64, BN, 2, (BN / 64) % 2 == 0 && BN % 64 == 0);
+static IpPlan ip_plan_dgrad(long long N, long long K, int O, int E) {
+    const int BN = choose_bn((int)(K < 256 ? K : 256)), CH = 128 / E;
+    return ip_plan(N, K, O, CH, BN, E, (BN / CH) % 2 == 0 && BN % CH == 0);
 }
 
 caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32_t O, int32_t pass, size_t* bytes) {
@@ -1364,7 +1364,7 @@ caffe_status caffe_ip_workspace_size(caffe_math math, caffe_shape4 bottom, int32
     const int E = math == CAFFE_MATH_TF32 ? 4 : 2, CHh = 128 / E;
     size_t part = 0;
     if (pass == CAFFE_PASS_FORWARD && N > 0 && O > 0 && K > 0) part = ip_plan_fwd(N, K, O, E).part_bytes;
-    if (pass == CAFFE_PASS_BACKWARD_DATA && N > 0 && O > 0 && K > 0) part = ip_plan_dgrad(N, K, O).part_bytes;
+    if (pass == CAFFE_PASS_BACKWARD_DATA && N > 0 && O > 0 && K > 0) part = ip_plan_dgrad(N, K, O, E).part_bytes;
     // worst case: every operand staged (+ fp32 rows for an NHWC data gradient) + bias partials + split-K partials
     *bytes = align1k((size_t)N * rup(K, CHh) * E) + align1k((size_t)O * rup(K, CHh) * E) +
              align1k((size_t)N * rup(O, CHh) * E) + align1k((size_t)N * K * 4) + bias + part;
@@ -1499,11 +1499,11 @@ static caffe_status ip_bwd_data(caffe_math math, const caffe_blob* top_diff, con
     if (N == 0) return CAFFE_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const caffe_shape4& xs = bottom_diff->shape;
-    if (math == CAFFE_MATH_FP32 || math == CAFFE_MATH_TF32) {   // TF32: CUDA cores on TF32-rounded operands
+    if (math == CAFFE_MATH_FP32) {   // CUDA-core FP32 FMA
         ConvGeom g{N, xs.c, xs.h, xs.w, O, xs.h, xs.w, 1, 1, 0, 0, 1, 1, 1};
         L4 ly{O, 1, 1, 1};
         CK(fp32_conv_dgrad(top_diff->ptr, isbf(top_diff), ly, weight->ptr, isbf(weight), bottom_diff->ptr,
-                           isbf(bottom_diff), nhwc(bottom_diff), beta, g, s, math == CAFFE_MATH_TF32),
+                           isbf(bottom_diff), nhwc(bottom_diff), beta, g, s, 0),
            "ip dgrad fp32");
         if (relu_top)
             CK(relu_bwd(relu_top->ptr, bottom_diff->ptr, bottom_diff->ptr, isbf(relu_top), isbf(bottom_diff),
@@ -1514,14 +1514,15 @@ static caffe_status ip_bwd_data(caffe_math math, const caffe_blob* top_diff, con
     size_t need;
     caffe_ip_workspace_size(math, bottom_diff->shape, O, 1, &need);
     if ((st = check_ws(ws, ws_bytes, need))) return st;
-    const int E = 2;
+    // BF16, or TF32 (tcgen05 kind::tf32; operands staged TF32-RN, the MN-major weight tile too)
+    const int E = math == CAFFE_MATH_TF32 ? 4 : 2, CH = 128 / E;
     char* cur = (char*)ws;
     const void *A, *B;
     long long lda, ldb;
     CK(stage_rows(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
     CK(stage_rows(weight, O, K, E, cur, &B, &ldb, s), "stage weight");
     const bool permute = nhwc(bottom_diff) && xs.h * xs.w > 1 && xs.c > 1;
-    const IpPlan q = ip_plan_dgrad(N, K, O);
+    const IpPlan q = ip_plan_dgrad(N, K, O, E);
     float* part = nullptr;
     if (q.splits > 1) { part = (float*)cur; cur += q.part_bytes; }
     float* rows = permute && !part ? (float*)cur : nullptr;
@@ -1531,10 +1532,10 @@ static caffe_status ip_bwd_data(caffe_math math, const caffe_blob* top_diff, con
     L.cg = q.cg;
     TcArgs& a = L.args;
     a.BN = q.BN;
-    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 128) || !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, 64, 64))
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, CH, 128) || !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, CH, CH))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip dgrad)");
     a.M = N; a.N = (int)K; a.m_tiles = q.m_tiles; a.n_tiles = q.n_tiles; a.groups = 1; a.splits = q.splits;
-    a.kblocks = q.kblocks; a.kb_per_split = q.kb_per; a.b_nchunks = (int)cdiv(a.BN, 64);
+    a.kblocks = q.kblocks; a.kb_per_split = q.kb_per; a.b_nchunks = (int)cdiv(a.BN, CH);
     a.partial = part;
     if (rows) {
         a.out = rows; a.out_bf16 = 0; a.beta = 0.f;
@@ -1549,7 +1550,7 @@ static caffe_status ip_bwd_data(caffe_math math, const caffe_blob* top_diff, con
         a.relu_top = relu_top->ptr; a.relu_top_bf16 = isbf(relu_top);
         masked = true;
     }
-    finish_args(a, a.b_nchunks / q.cg * 64 * 128);
+    finish_args(a, a.b_nchunks / q.cg * CH * 128);
     if (!part && (!masked || (a.out_bf16 && a.relu_top_bf16 && K % 64 == 0)))
         enable_tma_store(L, a.out, a.out_bf16 ? 2 : 4, K, N, K, true);
     if ((st = run_tc(L, s, 2.0 * N * O * (double)K, 1))) return st;
@@ -1608,16 +1609,17 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     float* bpart = (float*)cur;
     cur += align1k((size_t)bias_grad_splits(N, O, 1) * O * 4);
     if (bias_diff) CK(bias_grad(top_diff->ptr, isbf(top_diff), 1, (float*)bias_diff->ptr, beta, N, O, 1, bpart, s), "ip bias grad");
-    if (math == CAFFE_MATH_FP32 || math == CAFFE_MATH_TF32) {   // TF32: CUDA cores on TF32-rounded operands
+    if (math == CAFFE_MATH_FP32) {   // CUDA-core FP32 FMA (blocked reduction, R13)
         const caffe_shape4& b = bottom->shape;
         ConvGeom g{N, b.c, b.h, b.w, O, b.h, b.w, 1, 1, 0, 0, 1, 1, 1};
         L4 ly{O, 1, 1, 1};
         CK(fp32_conv_wgrad(bottom->ptr, isbf(bottom), strides(bottom), top_diff->ptr, isbf(top_diff), ly,
-                           (float*)weight_diff->ptr, beta, g, s, math == CAFFE_MATH_TF32),
+                           (float*)weight_diff->ptr, beta, g, s, 0),
            "ip wgrad fp32");
         return CAFFE_OK;
     }
-    const int E = 2;
+    // BF16, or TF32 (tcgen05 kind::tf32 with both operands MN-major, staged TF32-RN)
+    const int E = math == CAFFE_MATH_TF32 ? 4 : 2, CH = 128 / E;
     const void *A, *B;
     long long lda, ldb;
     CK(stage_rows(top_diff, N, O, E, cur, &A, &lda, s), "stage top_diff");
@@ -1631,14 +1633,14 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     TcArgs& a = L.args;
     a.BN = choose_bn((int)(K < 256 ? K : 256));
     // CTA pairs (M = 256 output rows) stage each bottom tile once for 256 outputs
-    L.cg = (O > 128 && a.BN % 128 == 0 && g_force_cg != 1) ? 2 : 1;
-    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, 64, 64) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, 64, 64))
+    L.cg = (E == 2 && O > 128 && a.BN % 128 == 0 && g_force_cg != 1) ? 2 : 1;
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, CH, CH) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, CH, CH))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip wgrad)");
     a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128 * L.cg); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1;
     a.splits = 1;
-    a.kblocks = (int)cdiv(N, 64); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, 64);
+    a.kblocks = (int)cdiv(N, CH); a.kb_per_split = a.kblocks; a.b_nchunks = (int)cdiv(a.BN, CH);
     a.out = weight_diff->ptr; a.out_bf16 = 0; a.s_n = K; a.s_c = 1; a.s_p = 0; a.P = 1; a.beta = beta;
-    finish_args(a, a.b_nchunks / L.cg * 64 * 128);
+    finish_args(a, a.b_nchunks / L.cg * CH * 128);
     enable_tma_store(L, weight_diff->ptr, 4, K, O, K, true);
     return run_tc(L, s, 2.0 * N * O * (double)K, 1);
 }

@@ -407,6 +407,10 @@ cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s) {
     TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_SGD, 2)
     TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_SGD, 1)
     TC_CASE(4, A_TILED_K, B_TILED_K, EPI_PARTIAL, 1)
+    TC_CASE(4, A_IM2COL_MN, B_TILED_MN, EPI_PARTIAL, 1)
+    TC_CASE(4, A_TILED_K, B_TILED_MN, EPI_STRIDED, 1)
+    TC_CASE(4, A_TILED_K, B_TILED_MN, EPI_PARTIAL, 1)
+    TC_CASE(4, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 1)
     TC_CASE(2, A_TILED_MN, B_TILED_MN, EPI_STRIDED, 1)
     TC_CASE(4, A_IM2COL_K, B_TILED_K, EPI_STRIDED, 1)
     TC_CASE(4, A_TILED_K, B_TILED_K, EPI_STRIDED, 1)
