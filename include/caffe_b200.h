@@ -35,10 +35,11 @@
  *    CAFFE_MATH_BF16 / CAFFE_MATH_TF32 = sm_100a tcgen05 tensor-core
  *    implicit GEMM with FP32 accumulation in TMEM.  Operands are rounded
  *    (RNE) to bf16 / tf32 before the MMA (reading R12).  TF32 with BF16
- *    storage is CAFFE_E_DTYPE.  Exception: the TF32 conv weight gradient and
- *    TF32 inner-product backward passes run the CUDA-core FP32 FMA kernels on
- *    TF32-rounded operands (same rounding, same parity bar; the MN-major TF32
- *    tensor-core operand layout is not built).
+ *    storage is CAFFE_E_DTYPE.  Every TF32 pass runs on the tensor cores
+ *    (tcgen05.mma kind::tf32), including the weight gradients and the
+ *    inner-product data gradient whose operands are MN-major: those are staged
+ *    with the 32-byte-atom 128-byte swizzle, the only shared-memory layout the
+ *    tensor core takes for MN-major TF32.
  */
 #ifndef CAFFE_B200_H_
 #define CAFFE_B200_H_

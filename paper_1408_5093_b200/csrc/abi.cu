@@ -1081,10 +1081,10 @@ caffe_status caffe_conv_backward_weight(const caffe_conv_desc* desc, const caffe
     memset(&L, 0, sizeof L);
     L.esz = p.E; L.amode = A_IM2COL_MN; L.bmode = B_TILED_MN; L.epi = EPI_PARTIAL;
     if (!encode_im2col_4d(&L.mapA, p.E, aptr, A.Ctot, A.W, A.H, p.N, p.pwp, p.php, p.pwp - (p.kwp - 1),
-                          p.php - (p.khp - 1), p.CH, p.CH))
+                          p.php - (p.khp - 1), p.CH, p.CH, p.E == 4))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeIm2col failed (wgrad activation)");
     if (!encode_tiled_2d(&L.mapB, p.E, bptr, (uint64_t)B.Ctot, (uint64_t)p.N * p.OH * p.OW, (uint64_t)B.Ctot * p.E,
-                         p.CH, p.CH))
+                         p.CH, p.CH, p.E == 4))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (wgrad top_diff)");
     TcArgs& a = L.args;
     a.BN = w.BN; a.M = 128 * w.m_tiles; a.N = p.Og;
@@ -1532,7 +1532,8 @@ static caffe_status ip_bwd_data(caffe_math math, const caffe_blob* top_diff, con
     L.cg = q.cg;
     TcArgs& a = L.args;
     a.BN = q.BN;
-    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, CH, 128) || !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, CH, CH))
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, CH, 128) ||
+        !encode_tiled_2d(&L.mapB, E, B, ldb, O, ldb * E, CH, CH, E == 4))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip dgrad)");
     a.M = N; a.N = (int)K; a.m_tiles = q.m_tiles; a.n_tiles = q.n_tiles; a.groups = 1; a.splits = q.splits;
     a.kblocks = q.kblocks; a.kb_per_split = q.kb_per; a.b_nchunks = (int)cdiv(a.BN, CH);
@@ -1634,7 +1635,8 @@ caffe_status caffe_ip_backward_weight(caffe_math math, const caffe_blob* bottom,
     a.BN = choose_bn((int)(K < 256 ? K : 256));
     // CTA pairs (M = 256 output rows) stage each bottom tile once for 256 outputs
     L.cg = (E == 2 && O > 128 && a.BN % 128 == 0 && g_force_cg != 1) ? 2 : 1;
-    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, CH, CH) || !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, CH, CH))
+    if (!encode_tiled_2d(&L.mapA, E, A, lda, N, lda * E, CH, CH, E == 4) ||
+        !encode_tiled_2d(&L.mapB, E, B, ldb, N, ldb * E, CH, CH, E == 4))
         return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (ip wgrad)");
     a.M = O; a.N = (int)K; a.m_tiles = (int)cdiv(O, 128 * L.cg); a.n_tiles = (int)cdiv(K, a.BN); a.groups = 1;
     a.splits = 1;

@@ -110,8 +110,9 @@ extern int g_halo_tma_store;   // CAFFE_TUNE_HALO_TMA_STORE
 int num_sms();
 
 // TMA descriptor encoders (driver entry points resolved at runtime; no -lcuda needed).
+// mn_tf32: the tile feeds a TF32 operand in MN-major form (32-byte-atom 128-byte swizzle, see ptx.cuh)
 bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                     uint32_t box_inner, uint32_t box_outer);
+                     uint32_t box_inner, uint32_t box_outer, bool mn_tf32 = false);
 // row-major output matrix [rows][cols] (row pitch = ld elements) for TMA stores: box (128 B of
 // columns, 32 rows), 128-byte swizzle
 bool encode_store_2d(CUtensorMap* m, int esz, const void* base, uint64_t cols, uint64_t rows, uint64_t ld);
@@ -124,7 +125,7 @@ bool encode_tiled_4d(CUtensorMap* m, int esz, const void* base, int C, int W, in
 bool encode_store_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, long long s_p,
                      long long s_n, uint32_t box_c, uint32_t box_w, uint32_t box_h, int swizzle_bytes);
 bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
-                      int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels);
+                      int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels, bool mn_tf32 = false);
 
 // element strides of a 4-D blob (n, c, h, w) -> n*sn + c*sc + h*sh + w*sw (32-bit: blobs < 2^31)
 struct L4 {

@@ -287,5 +287,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
     return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
+// MN-major TF32 operands: the only layout the tensor core accepts for them is the 128-byte swizzle
+// with 32-byte atoms (descriptor layout type 1, SWIZZLE_128B_BASE32B; TMA CU_TENSOR_MAP_SWIZZLE_
+// 128B_ATOM_32B): the XOR pattern repeats every 4 rows of 128 bytes, so the stride between K groups
+// (SBO) is 512 bytes.
+__device__ __forceinline__ uint64_t smem_desc_sw128_32b(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (1ull << 61);
+}
+// operand descriptor of the GEMM kernels: MN-major TF32 -> 32-byte-atom swizzle, else 128-byte
+template <int ESZ>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t saddr, uint32_t lbo, bool mn) {
+    if (ESZ == 4 && mn) return smem_desc_sw128_32b(saddr, lbo, 512);
+    return smem_desc_sw128(saddr, lbo, 1024);
+}
 
 }  // namespace cb

@@ -230,10 +230,10 @@ __global__ void __launch_bounds__(256, 1)
                 else mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 const uint32_t sa = smem_base + stage * stage_bytes;
-                const uint64_t bd0 = smem_desc_sw128(sa + a_bytes, b_lbo, 1024);
+                const uint64_t bd0 = operand_desc<ESZ>(sa + a_bytes, b_lbo, b_mn);
                 if (elect_one()) {
                     for (int a = 0; a < nacc; a++) {
-                        const uint64_t ad0 = smem_desc_sw128(sa + a * A_STAGE_BYTES, a_lbo, 1024);
+                        const uint64_t ad0 = operand_desc<ESZ>(sa + a * A_STAGE_BYTES, a_lbo, a_mn);
                         const uint32_t dt = d_tmem + a * args.acc_stride;
 #pragma unroll
                         for (int k = 0; k < KSTEPS; k++) {
@@ -445,7 +445,7 @@ static bool resolve() {
 }
 
 bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                     uint32_t box_inner, uint32_t box_outer) {
+                     uint32_t box_inner, uint32_t box_outer, bool mn_tf32) {
     if (!resolve()) return false;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {row_bytes};
@@ -453,7 +453,8 @@ bool encode_tiled_2d(CUtensorMap* m, int esz, const void* base, uint64_t inner, 
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_tiled(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                          const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         mn_tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -516,7 +517,7 @@ bool encode_store_4d(CUtensorMap* m, int esz, const void* base, int C, int W, in
 }
 
 bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, int H, int N, int pad_lo_w,
-                      int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels) {
+                      int pad_lo_h, int up_w, int up_h, uint32_t channels, uint32_t pixels, bool mn_tf32) {
     if (!resolve()) return false;
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)C * esz, (cuuint64_t)C * W * esz, (cuuint64_t)C * W * H * esz};
@@ -525,7 +526,8 @@ bool encode_im2col_4d(CUtensorMap* m, int esz, const void* base, int C, int W, i
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = g_im2col(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           const_cast<void*>(base), dims, strides, lower, upper, channels, pixels, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          mn_tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
