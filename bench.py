@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--math", default="bf16", choices=["bf16", "tf32"],
+                    help="tensor-core operand type of the CaffeNet step (tf32: FP32 activations)")
+    ap.add_argument("--workload", default="caffenet", choices=["caffenet", "lenet_conv1", "lenet", "caffenet_conv1_block"],
+                    help="BASELINE configs: C4/C5 caffenet (default), C1 lenet_conv1, C2 lenet, C3 caffenet_conv1_block")
     ap.add_argument("--dp-mode", default="sharded", choices=["sharded", "allreduce", "grad_allreduce"],
                     help="N > 1 exchange: reduce-scatter + sharded SGD + all-gather (default), per-bucket "
                          "all-reduce + update, or all-reduce then one update")
@@ -205,6 +209,182 @@ def reference_arm(args):
     }))
 
 
+# ------------------------------------------------------------------------------------------ C1-C3
+SMALL = {
+    "lenet_conv1": ("LeNet conv1 (20@5x5 on 1x28x28) fwd + wgrad + dgrad images/sec, batch 64 (BASELINE configs[0])", 64),
+    "lenet": ("LeNet train step (conv1/pool/conv2/pool/ip1+ReLU/ip2/softmax + SGD) images/sec, batch 64 "
+              "(BASELINE configs[1])", 64),
+    "caffenet_conv1_block": ("CaffeNet conv1+ReLU+pool1+norm1 fwd + bwd (wgrad, no data dgrad) images/sec, batch 256 "
+                             "(BASELINE configs[2])", 256),
+}
+
+
+def small_workload(args):
+    """C1 / C2 / C3 on one GPU: the same per-layer C-ABI calls the nets make, captured once in a CUDA
+    graph and replayed; device time with CUDA events; the oracle timed beside it on the same inputs
+    (a bounded sample where the full batch would take too long)."""
+    import ctypes
+    import numpy as np
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi, nets
+    import synth
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    lib = _abi.load()
+    _abi.call("caffe_device_check")
+    metric, B = SMALL[args.workload]
+    cl = torch.channels_last
+    bf = torch.bfloat16
+    flops_step = 0.0
+    net = None
+    if args.workload == "lenet":
+        net = nets.Net(nets.LENET, B, nets.LENET_INPUT, dev, math="bf16", seed=0)
+        X = synth.mnist_pixels((B, 1, 28, 28), 0)
+        lab = synth.labels(B, 10, 0)
+        net.a[0].copy_(torch.from_numpy(X).to(net.a[0].dtype))
+        net.labels.copy_(torch.from_numpy(lab))
+        flops_step = net.conv_flops_step
+
+        def step():
+            net.step()
+    elif args.workload == "lenet_conv1":
+        X = synth.mnist_pixels((B, 1, 28, 28), 0)
+        W = synth.xavier((20, 1, 5, 5), 0)
+        bias = torch.zeros(20, device=dev)
+        x = torch.from_numpy(X).to(dev).to(bf).contiguous(memory_format=cl)
+        w = torch.from_numpy(W).to(dev)
+        dy = torch.from_numpy(synth.uniform((B, 20, 24, 24), 0, synth.S_DY)).to(dev).to(bf).contiguous(memory_format=cl)
+        y = torch.empty((B, 20, 24, 24), device=dev, dtype=bf).contiguous(memory_format=cl)
+        dx = torch.empty_like(x)
+        dw, db = torch.empty_like(w), torch.empty(20, device=dev)
+        wss = [cb.conv_workspace(x.shape, w.shape, 1, 0, 1, "bf16", p, dev) for p in range(3)]
+        flops_step = 3 * 2.0 * B * 20 * 24 * 24 * 25
+
+        def step():
+            cb.conv_forward(x, w, bias, 1, 0, 1, "bf16", out=y, ws=wss[0])
+            cb.conv_backward_weight(x, dy, w.shape, 1, 0, 1, "bf16", beta=0.0, dw=dw, db=db, ws=wss[2])
+            cb.conv_backward_data(dy, w, x.shape, 1, 0, 1, "bf16", out=dx, ws=wss[1])
+    else:   # caffenet_conv1_block: the layers and calls of nets.Net (int8 batch, fused ReLU, U8 mask)
+        X = synth.int_pixels((B, 3, 227, 227), 0)
+        x = torch.from_numpy(X).to(dev).to(torch.int8).contiguous(memory_format=cl)
+        W = synth.gaussian((96, 3, 11, 11), 0.01, 0)
+        wq = torch.from_numpy(W).to(dev).to(bf)
+        bias = torch.zeros(96, device=dev)
+        ws0 = cb.conv_bottom_workspace(x.shape, wq.shape, 4, 0, 1, "bf16", dev)
+        y1 = torch.empty((B, 96, 55, 55), device=dev, dtype=bf).contiguous(memory_format=cl)
+        p1 = torch.empty((B, 96, 27, 27), device=dev, dtype=bf).contiguous(memory_format=cl)
+        m1 = torch.empty((B, 96, 27, 27), device=dev, dtype=torch.uint8).contiguous(memory_format=cl)
+        n1 = torch.empty_like(p1)
+        dn1 = torch.from_numpy(synth.uniform((B, 96, 27, 27), 0, synth.S_DY)).to(dev).to(bf).contiguous(memory_format=cl)
+        dp1, dy1 = torch.empty_like(p1), torch.empty_like(y1)
+        dw, db = torch.empty((96, 3, 11, 11), device=dev), torch.empty(96, device=dev)
+        flops_step = 2 * 2.0 * B * 96 * 55 * 55 * 363
+        L = nets.LRN
+
+        def step():
+            cb.conv_pack_bottom(x, wq, 4, 0, 1, "bf16", ws=ws0)
+            cb.conv_forward(x, wq, bias, 4, 0, 1, "bf16", relu=True, out=y1, ws=ws0, prepacked=True)
+            cb.pool_forward(y1, "max", 3, 2, 0, out=p1, mask=m1)
+            cb.lrn_forward(p1, **L, out=n1)
+            cb.lrn_backward(p1, n1, dn1, **L, out=dp1)
+            cb.pool_relu_backward(p1, dp1, m1, y1.shape, 3, 2, 0, out=dy1)
+            cb.conv_backward_weight(x, dy1, wq.shape, 4, 0, 1, "bf16", beta=0.0, dw=dw, db=db, ws=ws0, prepacked=True)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if net is not None:
+        net.capture()
+        g = net.graph
+    else:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                step()
+        torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    clk = ClockSampler(0)
+    clk.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.stop()
+    # launches per step: count one eager step (graph replays launch the same kernels)
+    n0 = lib.caffe_launch_count()
+    step()
+    torch.cuda.synchronize()
+    per_step_launches = lib.caffe_launch_count() - n0
+    # conv GEMM time of one instrumented eager step (events around each tensor-core launch)
+    lib.caffe_profiler_enable(1)
+    step()
+    torch.cuda.synchronize()
+    lib.caffe_profiler_enable(0)
+    g_ms, g_fl, g_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    _abi.call("caffe_profiler_read", 0, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_n))
+    peaks, src = measured_peaks()
+    peak = float(peaks.get("bf16_tflops"))
+    ach = g_fl.value / (g_ms.value / 1e3) / 1e12 if g_ms.value > 0 else 0.0
+    ms_step = ms / args.steps
+    value = B * args.steps / (ms / 1e3)
+    # the oracle beside it: the same passes on a bounded sample (images scaled to the metric)
+    import oracle
+    oracle.build()
+    from oracle import net as onet
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if args.workload == "lenet":
+        nb = B
+        params = {net.layers[i].name: (net.W[i].float().cpu().numpy().astype(np.float64),
+                                       net.B[i].float().cpu().numpy().astype(np.float64)) for (i, _, _) in net.pspecs}
+        moms = {k: (np.zeros_like(a), np.zeros_like(b)) for k, (a, b) in params.items()}
+        onet.train_step(onet.LENET, X.astype(np.float64), params, moms, lab)
+    elif args.workload == "lenet_conv1":
+        nb = B
+        dyh = dy.float().cpu().numpy()
+        oracle.conv_forward(X, W)
+        oracle.conv_backward_weight(X, dyh, W.shape)
+        oracle.conv_backward_data(dyh, W, X.shape)
+    else:
+        nb = 4
+        Xs = X[:nb].astype(np.float64)
+        Y = oracle.relu_forward(oracle.conv_forward(Xs, W, stride=(4, 4)))
+        P, M = oracle.maxpool_forward(Y, (3, 3), (2, 2), fp64=True)
+        oracle.lrn_forward(P)
+        dP = oracle.lrn_backward(P, dn1[:nb].float().cpu().numpy())
+        dY = oracle.relu_backward(Y, oracle.maxpool_backward(dP, M, Y.shape, (3, 3), (2, 2), fp64=True))
+        oracle.conv_backward_weight(Xs, dY, W.shape, stride=(4, 4))
+    csec = time.perf_counter() - t0
+    out = {
+        "metric": metric, "value": value, "unit": "images/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": args.workload, "batch": B, "graph": True,
+                   "l2": "no flush (a small workload replayed back to back: L2-resident, as in training)"},
+        "roofline": {"bound": "tensor" if args.workload == "caffenet_conv1_block" else "latency",
+                     "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if peak else None,
+                     "traffic": None, "kernel": "tcgen05 conv GEMMs (events around each launch, one eager step)",
+                     "conv_gemm_us_per_step": g_ms.value * 1e3, "conv_gemm_launches": g_n.value,
+                     "conv_tflops_vs_step": flops_step / (ms_step / 1e3) / 1e12,
+                     "peak_source": f"{src} bf16_tflops (burst)"},
+        "cpu_baseline": {"value": nb / csec, "unit": "images/s", "cores": threads, "kind": "oracle",
+                         "sample": f"the same passes on {nb} image(s), fp64 oracle", "cpu_model": cpu_model()},
+        "e2e": None,
+        "gpu_launches": per_step_launches * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(out))
+
+
 # ------------------------------------------------------------------------------------------ GPU arm
 def cpu_model() -> str:
     try:
@@ -239,6 +419,9 @@ def main():
     if args.impl == "reference":
         reference_arm(args)
         return
+    if args.workload != "caffenet":
+        small_workload(args)
+        return
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -261,7 +444,9 @@ def main():
     B = args.batch
     # the image batch travels and is stored as int8 (the synthetic pixels are mean-subtracted
     # integers in [-128, 127]); the first layer's pack converts it exactly to BF16 (CAFFE_I8)
-    net = nets.Net(nets.CAFFENET, B, nets.CAFFENET_INPUT, dev, math="bf16", seed=0, input_i8=True)
+    tf32 = args.math == "tf32"
+    # TF32: FP32 activations (TF32 operands need FP32 storage), the image batch in FP32
+    net = nets.Net(nets.CAFFENET, B, nets.CAFFENET_INPUT, dev, math=args.math, seed=0, input_i8=not tf32)
     X = synth.int_pixels((B, 3, 227, 227), 1000 + rank)
     lab = synth.labels(B, 1000, 1000 + rank)
     net.a[0].copy_(torch.from_numpy(X).to(net.a[0].dtype))
@@ -353,6 +538,8 @@ def main():
     # each GEMM launch is timed alone by an event pair inside an eager pass of ~40 ms at full clocks:
     # the burst regime, so the burst peak is the denominator (sustained and spec fractions beside it)
     peak = float(peaks.get("bf16_tflops"))
+    if tf32:   # TF32 dense peak = the measured BF16 peak x the nominal ratio 1.125 / 2.25
+        peak *= 0.5
     traffic, tensor_pipe = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -365,10 +552,11 @@ def main():
     roofline = {"bound": "tensor", "achieved": conv_tflops, "peak": peak, "unit": "TFLOP/s",
                 "frac": conv_tflops / peak if peak else None, "traffic": traffic,
                 "kernel": "tc_gemm_kernel (tcgen05 implicit-GEMM conv fwd/dgrad/wgrad)",
-                "peak_source": f"{src} bf16_tflops (burst: each GEMM launch timed alone by an event pair)",
+                "peak_source": f"{src} bf16_tflops (burst: each GEMM launch timed alone by an event pair)"
+                               + (" x 0.5 (nominal TF32/BF16 dense ratio)" if tf32 else ""),
                 "frac_of_sustained": conv_tflops / float(peaks.get("bf16_tflops_sustained", peak)),
                 "ncu_tensor_pipe_pct_flop_weighted": tensor_pipe,
-                "frac_of_spec_2250": conv_tflops / 2250.0,
+                "frac_of_spec": conv_tflops / (1125.0 if tf32 else 2250.0),
                 "launches_timed": g_n.value,
                 "avg_launch_ms": g_ms.value / max(1, g_n.value),
                 "algorithmic_gflop_per_launch": g_fl.value / max(1, g_n.value) / 1e9,
@@ -462,11 +650,13 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": args.math, "data": "synthetic",
             "config": {"workload": WORKLOAD, "global_batch": world * B, "per_gpu_batch": B,
                        "image": [3, 227, 227], "parallelism": f"dp{world}",
-                       "math": "bf16 tcgen05 operands, fp32 accumulate; bf16 activations, fp32 master weights",
-                       "input": "int8 mean-subtracted pixels (exact), converted to the packed BF16 operand by conv1's pack",
+                       "math": ("bf16 tcgen05 operands, fp32 accumulate; bf16 activations, fp32 master weights"
+                                if not tf32 else "tf32 tcgen05 operands (RN), fp32 accumulate; fp32 activations"),
+                       "input": ("int8 mean-subtracted pixels (exact), converted to the packed BF16 operand by conv1's pack"
+                                 if not tf32 else "fp32 mean-subtracted integer pixels"),
                        "l2": "no flush: per-step working set ~2 GB of activations/diffs >> 126 MB L2",
                        "paper_context": "~2.5 ms/image (400 img/s) on one K40/Titan, P:20"},
             "roofline": roofline,
