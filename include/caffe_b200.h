@@ -199,6 +199,9 @@ caffe_status caffe_device_check(void);
    units (accumulator double-buffer and barrier phases carried across units), which is how the
    parity tests exercise the batch-256 schedule at small sizes. */
 #define CAFFE_TUNE_MAX_CTAS 16
+/* CAFFE_TUNE_FUSED_POOL_ROWS: 2x2-block rows per CTA of caffe_lrn_pool_backward (0 = automatic).
+   Results are identical for every value. */
+#define CAFFE_TUNE_FUSED_POOL_ROWS 17
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation
@@ -405,6 +408,23 @@ caffe_status caffe_softmax_loss(const caffe_blob* scores, const int32_t* labels 
    the next step's BF16 operands. */
 caffe_status caffe_sgd_update(float* w, const float* g, float* v, void* w_bf16, int64_t count, float lr,
                               float momentum, float decay, float grad_scale, caffe_stream_t stream);
+
+/* ------------------------------------------------------------------ fused pool + LRN
+   CaffeNet's "pool -> LRN" blocks (P:158 pooling + local response normalization; S:160-177,
+   S:214-231) in one pass each, for BF16 channels-last blobs, MAX 3x3/stride-2 unpadded windows that
+   lie inside the map, C % 8 == 0, local_size <= 9 and a U8 window-local mask (anything else:
+   CAFFE_E_INVALID / CAFFE_E_DTYPE -- use the separate calls).  Results are bit-identical to the
+   separate calls; only the intermediate blob's trip through memory is gone.
+   caffe_pool_lrn_forward: pool_top = maxpool(bottom) (+ mask), top = lrn(pool_top).
+   caffe_lrn_pool_backward: bottom_diff (pool input diff, overwritten) = maxpool_backward(
+     lrn_backward(pool_top, top_diff), mask), with relu != 0 gated as caffe_pool_relu_backward (the
+     ReLU that feeds the pool: a window passes its gradient only when pool_top > 0).  pool_top is the
+     LRN's bottom, so the LRN backward needs no other blob. */
+caffe_status caffe_pool_lrn_forward(const caffe_pool_desc* pool, const caffe_lrn_desc* lrn, const caffe_blob* bottom,
+                                    caffe_blob* pool_top, caffe_blob* mask, caffe_blob* top, caffe_stream_t stream);
+caffe_status caffe_lrn_pool_backward(const caffe_pool_desc* pool, const caffe_lrn_desc* lrn, const caffe_blob* pool_top,
+                                     const caffe_blob* top_diff, const caffe_blob* mask, int32_t relu,
+                                     caffe_blob* bottom_diff, caffe_stream_t stream);
 
 /* ------------------------------------------------------------------ the rest of the layer catalogue
    P:158 (Sec. 3.2): "nonlinearities like rectified linear and logistic ... element-wise operations

@@ -375,6 +375,39 @@ def lrn_backward(x, y, dy, local_size=5, alpha=1e-4, beta=0.75, k=1.0, scale=Non
     return out
 
 
+# ------------------------------------------------------------------ fused pool + LRN (NEXT-1)
+def pool_lrn_forward(x, kernel=3, stride=2, pad=0, local_size=5, alpha=1e-4, beta=0.75, k=1.0, pool_out=None, mask=None,
+                     out=None):
+    """maxpool (U8 mask) then LRN in one pass (caffe_pool_lrn_forward); returns (pool_out, mask, out)."""
+    torch = _t()
+    d = _pool_desc("max", kernel, stride, pad)
+    oshape = pool_output_shape(x.shape, "max", kernel, stride, pad)
+    if pool_out is None:
+        pool_out = empty_like_layout(oshape, x.dtype, x.device, like=x)
+    if mask is None:
+        mask = empty_like_layout(oshape, torch.uint8, x.device, like=pool_out)
+    if out is None:
+        out = torch.empty_like(pool_out)
+    ld = _abi.LrnDesc(int(local_size), float(alpha), float(beta), float(k))
+    bx, bp, bm, by = blob(x), blob(pool_out), blob(mask), blob(out)
+    call("caffe_pool_lrn_forward", ctypes.byref(d), ctypes.byref(ld), ctypes.byref(bx), ctypes.byref(bp),
+         ctypes.byref(bm), ctypes.byref(by), _stream())
+    return pool_out, mask, out
+
+
+def lrn_pool_backward(pool_out, dy, mask, in_shape, kernel=3, stride=2, pad=0, local_size=5, alpha=1e-4, beta=0.75,
+                      k=1.0, relu=True, out=None):
+    """LRN backward then maxpool backward (+ the ReLU below when relu) in one pass (caffe_lrn_pool_backward)."""
+    d = _pool_desc("max", kernel, stride, pad)
+    if out is None:
+        out = empty_like_layout(in_shape, dy.dtype, dy.device, like=dy)
+    ld = _abi.LrnDesc(int(local_size), float(alpha), float(beta), float(k))
+    bp, bdy, bm, bdx = blob(pool_out), blob(dy), blob(mask), blob(out)
+    call("caffe_lrn_pool_backward", ctypes.byref(d), ctypes.byref(ld), ctypes.byref(bp), ctypes.byref(bdy),
+         ctypes.byref(bm), int(bool(relu)), ctypes.byref(bdx), _stream())
+    return out
+
+
 # ------------------------------------------------------------------ inner product
 def _ip_ws(math, in_shape, O, pass_):
     n = ctypes.c_size_t()

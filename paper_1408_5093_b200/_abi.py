@@ -39,6 +39,7 @@ CAFFE_TUNE_WGRAD_REDUCE_ROWS = 13
 CAFFE_TUNE_HALO_STACKED = 14
 CAFFE_TUNE_SGD_THREADS = 15
 CAFFE_TUNE_MAX_CTAS = 16
+CAFFE_TUNE_FUSED_POOL_ROWS = 17
 CAFFE_ELTWISE_PROD, CAFFE_ELTWISE_SUM, CAFFE_ELTWISE_MAX = 0, 1, 2
 CAFFE_ELTWISE_MAX_INPUTS = 8
 CAFFE_LR_FIXED, CAFFE_LR_STEP, CAFFE_LR_INV = 0, 1, 2
@@ -120,6 +121,8 @@ SIGNATURES = {
     "caffe_col2im": [CD, B, i32, B, vp],
     "caffe_softmax_loss": [B, vp, vp, B, vp],
     "caffe_sgd_update": [vp, vp, vp, vp, i64, f32, f32, f32, f32, vp],
+    "caffe_pool_lrn_forward": [PD, LD, B, B, B, B, vp],
+    "caffe_lrn_pool_backward": [PD, LD, B, B, B, i32, B, vp],
     "caffe_sigmoid_forward": [B, B, vp],
     "caffe_sigmoid_backward": [B, B, B, vp],
     "caffe_eltwise_forward": [i32, i32, P(B), P(f32), B, vp],

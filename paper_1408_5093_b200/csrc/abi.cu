@@ -615,6 +615,11 @@ caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_
 }
 
 caffe_status caffe_set_tuning(int32_t key, int32_t value) {
+    if (key == CAFFE_TUNE_FUSED_POOL_ROWS) {
+        if (value < 0 || value > 64) return fail(CAFFE_E_PARAM, "fused pool rows must be 0 (auto) .. 64");
+        cb::g_fused_rb = value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_MAX_CTAS) {
         if (value < 0) return fail(CAFFE_E_PARAM, "max CTAs must be >= 0 (0 = one per SM)");
         g_max_ctas = value;
@@ -1800,6 +1805,68 @@ caffe_status caffe_sgd_update(float* w, const float* g, float* v, void* w_bf16, 
     return CAFFE_OK;
 }
 
+
+// ------------------------------------------------------------------ fused pool + LRN (NEXT-1)
+static caffe_status pool_lrn_check(const caffe_pool_desc* pd, const caffe_lrn_desc* ld, const caffe_blob* bottom_like,
+                                   const caffe_blob* pooled, const caffe_blob* mask, PoolGeom* g) {
+    caffe_status st;
+    if ((st = lrn_validate(ld))) return st;
+    if ((st = check_blob(bottom_like, "bottom")) || (st = check_blob(pooled, "pool_top"))) return st;
+    if ((st = check_blob(mask, "mask", false))) return st;
+    if ((st = pool_validate(pd, bottom_like->shape, g))) return st;
+    if (pd->method != CAFFE_POOL_MAX) return fail(CAFFE_E_INVALID, "the fused kernels pool with MAX");
+    caffe_shape4 want{g->N, g->C, g->OH, g->OW};
+    if (!same_shape(pooled->shape, want) || !same_shape(mask->shape, want))
+        return fail(CAFFE_E_SHAPE, "pool_top and mask must be (%d,%d,%d,%d)", want.n, want.c, want.h, want.w);
+    if (!isbf(bottom_like) || !isbf(pooled) || !nhwc(bottom_like) || !nhwc(pooled) || !nhwc(mask) ||
+        mask->dtype != CAFFE_U8)
+        return fail(CAFFE_E_DTYPE, "the fused pool+LRN kernels take BF16 channels-last blobs and a U8 mask");
+    if (!pool_lrn_fusable(*g, ld->local_size))
+        return fail(CAFFE_E_INVALID, "the fused pool+LRN kernels need 3x3/s2 unpadded windows inside the map, "
+                                     "C %% 8 == 0 and local_size <= 9 (use the separate calls)");
+    if (!aligned16(bottom_like->ptr) || !aligned16(pooled->ptr) || !aligned16(mask->ptr))
+        return fail(CAFFE_E_ALIGN, "fused pool+LRN buffers must be 16-byte aligned");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_pool_lrn_forward(const caffe_pool_desc* pool, const caffe_lrn_desc* lrn, const caffe_blob* bottom,
+                                    caffe_blob* pool_top, caffe_blob* mask, caffe_blob* top, caffe_stream_t stream) {
+    caffe_status st;
+    PoolGeom g;
+    if ((st = pool_lrn_check(pool, lrn, bottom, pool_top, mask, &g))) return st;
+    if ((st = check_blob(top, "top"))) return st;
+    if (!same_shape(top->shape, pool_top->shape) || top->dtype != pool_top->dtype || top->layout != pool_top->layout)
+        return fail(CAFFE_E_SHAPE, "top must match pool_top (shape, dtype, layout)");
+    if (!aligned16(top->ptr)) return fail(CAFFE_E_ALIGN, "top must be 16-byte aligned");
+    if (overlap(pool_top, bottom) || overlap(mask, bottom) || overlap(top, bottom) || overlap(top, pool_top) ||
+        overlap(mask, pool_top) || overlap(mask, top))
+        return fail(CAFFE_E_ALIAS, "fused pool+LRN outputs overlap each other or the input");
+    if (g.N == 0) return CAFFE_OK;
+    CK(pool_lrn_fwd(bottom->ptr, pool_top->ptr, mask->ptr, top->ptr, g, lrn->local_size, lrn->alpha, lrn->beta, lrn->k,
+                    (cudaStream_t)stream),
+       "fused pool+lrn fwd");
+    return CAFFE_OK;
+}
+
+caffe_status caffe_lrn_pool_backward(const caffe_pool_desc* pool, const caffe_lrn_desc* lrn, const caffe_blob* pool_top,
+                                     const caffe_blob* top_diff, const caffe_blob* mask, int32_t relu,
+                                     caffe_blob* bottom_diff, caffe_stream_t stream) {
+    caffe_status st;
+    PoolGeom g;
+    if ((st = pool_lrn_check(pool, lrn, bottom_diff, pool_top, mask, &g))) return st;
+    if ((st = check_blob(top_diff, "top_diff"))) return st;
+    if (!same_shape(top_diff->shape, pool_top->shape) || top_diff->dtype != pool_top->dtype ||
+        top_diff->layout != pool_top->layout)
+        return fail(CAFFE_E_SHAPE, "top_diff must match pool_top (shape, dtype, layout)");
+    if (!aligned16(top_diff->ptr)) return fail(CAFFE_E_ALIGN, "top_diff must be 16-byte aligned");
+    if (overlap(bottom_diff, pool_top) || overlap(bottom_diff, top_diff) || overlap(bottom_diff, mask))
+        return fail(CAFFE_E_ALIAS, "bottom_diff overlaps an input");
+    if (g.N == 0) return CAFFE_OK;
+    CK(lrn_pool_bwd(pool_top->ptr, top_diff->ptr, mask->ptr, bottom_diff->ptr, relu ? 1 : 0, g, lrn->local_size,
+                    lrn->alpha, lrn->beta, lrn->k, (cudaStream_t)stream),
+       "fused lrn+pool bwd");
+    return CAFFE_OK;
+}
 
 // ------------------------------------------------------------------ catalogue layers (catalog.cu)
 static caffe_status same_elementwise(const caffe_blob* a, const caffe_blob* b, const char* what) {

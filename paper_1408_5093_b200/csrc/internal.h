@@ -215,6 +215,13 @@ cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int nhwc, in
                     float alpha, float beta, float k, cudaStream_t s);
 cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* scale, void* dx, int bf16, int nhwc,
                     int N, int C, int H, int W, int size, float alpha, float beta, float k, cudaStream_t s);
+// fused CaffeNet pool (3x3/s2, full windows, U8 mask) + LRN, BF16 channels-last (simple.cu)
+bool pool_lrn_fusable(const PoolGeom& g, int size);
+extern int g_fused_rb;   // CAFFE_TUNE_FUSED_POOL_ROWS
+cudaError_t pool_lrn_fwd(const void* x, void* p, void* mask, void* y, const PoolGeom& g, int size, float alpha,
+                         float beta, float k, cudaStream_t s);
+cudaError_t lrn_pool_bwd(const void* p, const void* dn, const void* mask, void* dx, int relu, const PoolGeom& g,
+                         int size, float alpha, float beta, float k, cudaStream_t s);
 cudaError_t softmax_loss_k(const void* scores, int bf16, const int32_t* labels, float* loss, void* diff,
                            int diff_bf16, int N, int K, cudaStream_t s);
 extern int g_sgd_blocks_per_sm;

@@ -1099,6 +1099,20 @@ __device__ __forceinline__ float rcp_ftz(float x) {
     return r;
 }
 
+// the 8 outputs of channels c0..c0+7 from the 24 channels c0-8..c0+15 (zero outside [0, C))
+template <int R>
+__device__ __forceinline__ void lrn_fwd8(const float (&xv)[24], float an, float beta, float k, float (&out)[8],
+                                         float (&S)[8]) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+        float s2 = 0.f;
+#pragma unroll
+        for (int j = -R; j <= R; j++) s2 = fmaf(xv[8 + e + j], xv[8 + e + j], s2);
+        S[e] = k + an * s2;
+        out[e] = xv[8 + e] * ex2_ftz(-beta * lg2_ftz(S[e]));
+    }
+}
+
 template <int R>
 __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                               float* __restrict__ scale, int C, int size, float alpha, float beta, float k, int total) {
@@ -1110,14 +1124,7 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
         float xv[24];
         load24(x + base, c0, C, xv);
         float out[8], S[8];
-#pragma unroll
-        for (int e = 0; e < 8; e++) {
-            float s2 = 0.f;
-#pragma unroll
-            for (int j = -R; j <= R; j++) s2 = fmaf(xv[8 + e + j], xv[8 + e + j], s2);
-            S[e] = k + an * s2;
-            out[e] = xv[8 + e] * ex2_ftz(-beta * lg2_ftz(S[e]));
-        }
+        lrn_fwd8<R>(xv, an, beta, k, out, S);
         *reinterpret_cast<uint4*>(y + base + c0) = pack8(out);
         if (scale) {
             float4* sp = reinterpret_cast<float4*>(scale + base + c0);
@@ -1133,6 +1140,33 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
 // reading it made the result lose up to 2^-9 of that term where it cancels the direct term, and cost
 // a third of the kernel's reads); `y` is not read.
 template <int R>
+__device__ __forceinline__ void lrn_bwd8(const float (&xv)[24], const float (&gv)[24], float an, float beta, float k,
+                                         float cb, float (&out)[8]) {
+    float P[24], tv[24];
+    float s2 = 0.f;
+#pragma unroll
+    for (int j = 8 - 2 * R; j <= 8; j++) s2 = fmaf(xv[j], xv[j], s2);   // window of channel 8 - R
+#pragma unroll
+    for (int i = 8 - R; i < 16 + R; i++) {
+        if (i > 8 - R) {
+            s2 = fmaf(xv[i + R], xv[i + R], s2);
+            s2 = fmaf(-xv[i - R - 1], xv[i - R - 1], s2);
+        }
+        const float S = k + an * s2;
+        P[i] = ex2_ftz(-beta * lg2_ftz(S));                  // S^-beta
+        tv[i] = gv[i] * (xv[i] * P[i]) * rcp_ftz(S);          // dy * y / S
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 8 - R; j <= 8 + R; j++) acc += tv[j];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+        if (e > 0) acc = acc + tv[8 + e + R] - tv[8 + e - R - 1];
+        out[e] = gv[8 + e] * P[8 + e] - cb * xv[8 + e] * acc;
+    }
+}
+
+template <int R>
 __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
                               __nv_bfloat16* __restrict__ dx, int C, int size, float alpha, float beta, float k,
                               int total) {
@@ -1145,29 +1179,8 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
         float xv[24], gv[24];
         load24(x + base, c0, C, xv);
         load24(dy + base, c0, C, gv);
-        float P[24], tv[24];
-        float s2 = 0.f;
-#pragma unroll
-        for (int j = 8 - 2 * R; j <= 8; j++) s2 = fmaf(xv[j], xv[j], s2);   // window of channel 8 - R
-#pragma unroll
-        for (int i = 8 - R; i < 16 + R; i++) {
-            if (i > 8 - R) {
-                s2 = fmaf(xv[i + R], xv[i + R], s2);
-                s2 = fmaf(-xv[i - R - 1], xv[i - R - 1], s2);
-            }
-            const float S = k + an * s2;
-            P[i] = ex2_ftz(-beta * lg2_ftz(S));                  // S^-beta
-            tv[i] = gv[i] * (xv[i] * P[i]) * rcp_ftz(S);          // dy * y / S
-        }
         float out[8];
-        float acc = 0.f;
-#pragma unroll
-        for (int j = 8 - R; j <= 8 + R; j++) acc += tv[j];
-#pragma unroll
-        for (int e = 0; e < 8; e++) {
-            if (e > 0) acc = acc + tv[8 + e + R] - tv[8 + e - R - 1];
-            out[e] = gv[8 + e] * P[8 + e] - cb * xv[8 + e] * acc;
-        }
+        lrn_bwd8<R>(xv, gv, an, beta, k, cb, out);
         *reinterpret_cast<uint4*>(dx + base + c0) = pack8(out);
     }
 }
@@ -1242,6 +1255,272 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
     }
     lrn_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(x, y, dy, scale, dx, bf16, nhwc, C, H, W, sc, size, alpha, beta, k,
                                                      total);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ================================================================ fused max pool + LRN
+// CaffeNet's conv -> ReLU -> pool (3x3/s2) -> LRN blocks, BF16 channels-last, U8 window-local mask.
+// Both kernels give exactly the bits of the separate calls (the pool's packed strict-'>' scan, the
+// LRN arithmetic through the same device functions, R8's FP32 sum order) and drop the
+// intermediate blob's trip through HBM.  Layout of the work: the lanes of a warp hold consecutive
+// 8-channel vectors of one pooled pixel (C/8 <= 32 lanes per pixel, 32/(C/8) pixels per warp), so
+// the cross-channel LRN window is a warp shuffle of the neighbouring lanes' values -- no shared
+// memory (the kernels co-reside with the 200 KB tensor-core CTAs of the other streams) and no
+// block-wide barrier.
+//   forward : pool the warp's pixels (9 loads per lane), store pool output + mask, shuffle the
+//             neighbours' pooled values, LRN, store -- the pool output is not re-read;
+//   backward: a pixel slot walks a strip of `rows` 2x2-block rows column by column; at each column
+//             it computes the LRN backward of the strip's window column (rows+1 pooled pixels: the
+//             lanes of the pixel cooperate, neighbours by shuffle), gates it by pool output > 0 (the
+//             ReLU below), and runs the max-pool backward of the strip's blocks from that column
+//             and the previous one (kept in registers) -- every window's LRN backward is computed
+//             once per strip, the LRN bottom diff never reaches memory, the pool output is read once.
+__device__ __forceinline__ void shfl_neighbours(const uint32_t (&w)[4], int vi, int cv, float (&xv)[24]) {
+    uint32_t l[4], r[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        l[e] = __shfl_up_sync(0xffffffffu, w[e], 1);
+        r[e] = __shfl_down_sync(0xffffffffu, w[e], 1);
+    }
+    if (vi == 0) l[0] = l[1] = l[2] = l[3] = 0u;             // channels below 0
+    if (vi == cv - 1) r[0] = r[1] = r[2] = r[3] = 0u;        // channels from C up
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        xv[2 * e] = __uint_as_float(l[e] << 16);
+        xv[2 * e + 1] = __uint_as_float(l[e] & 0xffff0000u);
+        xv[8 + 2 * e] = __uint_as_float(w[e] << 16);
+        xv[8 + 2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+        xv[16 + 2 * e] = __uint_as_float(r[e] << 16);
+        xv[16 + 2 * e + 1] = __uint_as_float(r[e] & 0xffff0000u);
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256)
+pool_lrn_fwd_k3s2_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ p, uint8_t* __restrict__ mask,
+                        __nv_bfloat16* __restrict__ y, PoolGeom g, int npix, float an, float beta, float k) {
+    const int cv = g.C / 8, ppw = 32 / cv;
+    const int lane = threadIdx.x & 31;
+    const int ps = lane / cv, vi = lane - ps * cv;
+    const int c0 = vi * 8;
+    const long long rs = (long long)g.W * g.C;
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int w0 = gw * ppw; w0 < npix; w0 += nw * ppw) {      // warp-uniform loop
+        const int pix = w0 + ps;
+        const bool act = ps < ppw && pix < npix;
+        uint32_t bw[4] = {0u, 0u, 0u, 0u}, aw[4] = {0u, 0u, 0u, 0u};
+        if (act) {
+            int r = pix;
+            const int px = r % g.OW; r /= g.OW;
+            const int py = r % g.OH;
+            const int n = r / g.OH;
+            const __nv_bfloat16* base = x + (((long long)n * g.H + 2 * py) * g.W + 2 * px) * g.C + c0;
+            uint4 raw[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; i++)
+#pragma unroll
+                for (int j = 0; j < 3; j++) raw[i][j] = __ldg(reinterpret_cast<const uint4*>(base + i * rs + j * g.C));
+            bw[0] = raw[0][0].x; bw[1] = raw[0][0].y; bw[2] = raw[0][0].z; bw[3] = raw[0][0].w;
+#pragma unroll
+            for (int i = 0; i < 3; i++)
+#pragma unroll
+                for (int j = 0; j < 3; j++) {
+                    if (i == 0 && j == 0) continue;
+                    const uint32_t vw[4] = {raw[i][j].x, raw[i][j].y, raw[i][j].z, raw[i][j].w};
+                    const uint32_t pp = (uint32_t)(i * 3 + j) * 0x00010001u;
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vw[e]),
+                                                       *reinterpret_cast<const __nv_bfloat162*>(&bw[e]));
+                        bw[e] = (vw[e] & m) | (bw[e] & ~m);
+                        aw[e] = (pp & m) | (aw[e] & ~m);
+                    }
+                }
+            const long long o = (long long)pix * g.C + c0;
+            *reinterpret_cast<uint4*>(p + o) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+            *reinterpret_cast<uint2*>(mask + o) =
+                make_uint2(__byte_perm(aw[0], aw[1], 0x6420), __byte_perm(aw[2], aw[3], 0x6420));
+        }
+        float xv[24];
+        shfl_neighbours(bw, vi, cv, xv);
+        if (act) {
+            float out[8], S[8];
+            lrn_fwd8<R>(xv, an, beta, k, out, S);
+            *reinterpret_cast<uint4*>(y + (long long)pix * g.C + c0) = pack8(out);
+        }
+    }
+}
+
+// the gated LRN bottom diff of pooled pixel (py, px) (own 8 channels) + its mask word; a missing
+// window (outside the map) has d = 0 and mask 0xFF (selects no block position)
+template <int R, bool RELU>
+__device__ __forceinline__ void lrn_window(PoolWin& w, const __nv_bfloat16* __restrict__ p,
+                                           const __nv_bfloat16* __restrict__ dn, const uint8_t* __restrict__ mask,
+                                           long long q, bool valid, int vi, int cv, float an, float beta, float k,
+                                           float cb) {
+    uint4 pv = make_uint4(0u, 0u, 0u, 0u), gvv = make_uint4(0u, 0u, 0u, 0u);
+    w.m = make_uint2(0xffffffffu, 0xffffffffu);
+    w.y = make_uint4(0u, 0u, 0u, 0u);
+    if (valid) {
+        pv = __ldg(reinterpret_cast<const uint4*>(p + q));
+        gvv = __ldg(reinterpret_cast<const uint4*>(dn + q));
+        w.m = __ldg(reinterpret_cast<const uint2*>(mask + q));
+    }
+    const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w}, gw4[4] = {gvv.x, gvv.y, gvv.z, gvv.w};
+    float xv[24], gv[24];
+    shfl_neighbours(pw, vi, cv, xv);
+    shfl_neighbours(gw4, vi, cv, gv);
+    float out[8];
+    lrn_bwd8<R>(xv, gv, an, beta, k, cb, out);
+    uint4 d = valid ? pack8(out) : make_uint4(0u, 0u, 0u, 0u);
+    if (RELU) {
+        d.x = pool_gate<true>(d.x, pv.x);
+        d.y = pool_gate<true>(d.y, pv.y);
+        d.z = pool_gate<true>(d.z, pv.z);
+        d.w = pool_gate<true>(d.w, pv.w);
+    }
+    w.d = d;
+}
+
+template <int R, bool RELU, int ROWS>
+__global__ void __launch_bounds__(256)
+lrn_pool_bwd_k3s2_nhwc8(const __nv_bfloat16* __restrict__ p, const __nv_bfloat16* __restrict__ dn,
+                        const uint8_t* __restrict__ mask, __nv_bfloat16* __restrict__ dx, PoolGeom g, int HB, int WB,
+                        int nstrip, int cseg, int ncseg, int ntask, float an, float beta, float k, float cb) {
+    const int cv = g.C / 8, ppw = 32 / cv;
+    const int lane = threadIdx.x & 31;
+    const int ps = lane / cv, vi = lane - ps * cv;
+    const int c0 = vi * 8;
+    const long long rs = (long long)g.W * g.C;
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int t0 = gw * ppw; t0 < ntask; t0 += nw * ppw) {     // warp-uniform loop
+        const int task = t0 + ps;
+        const bool act = ps < ppw && task < ntask;
+        // task = ((n * nstrip + strip) * ncseg + column segment); inactive slots mirror slot 0's
+        // geometry so the warp's loop trip counts stay uniform (they load and store nothing)
+        int tr = act ? task : t0;
+        const int seg = tr % ncseg; tr /= ncseg;
+        const int st = tr % nstrip;
+        const int n = tr / nstrip;
+        const int bh0 = st * ROWS;
+        const int bw0 = seg * cseg, bw1 = min(bw0 + cseg, WB);
+        const long long img = (long long)n * g.OH * g.OW * g.C + c0;
+        PoolWin L[ROWS + 1], Rw[ROWS + 1];
+        // left window column (bw0 - 1)
+#pragma unroll
+        for (int a = 0; a <= ROWS; a++) {
+            const int py = bh0 - 1 + a, px = bw0 - 1;
+            const bool v = act && py >= 0 && py < g.OH && px >= 0 && px < g.OW;
+            lrn_window<R, RELU>(L[a], p, dn, mask, img + ((long long)py * g.OW + px) * g.C, v, vi, cv, an, beta, k, cb);
+        }
+        for (int bw = bw0; bw < bw1; bw++) {
+#pragma unroll
+            for (int a = 0; a <= ROWS; a++) {
+                const int py = bh0 - 1 + a;
+                const bool v = act && py >= 0 && py < g.OH && bw < g.OW;
+                lrn_window<R, RELU>(Rw[a], p, dn, mask, img + ((long long)py * g.OW + bw) * g.C, v, vi, cv, an, beta, k,
+                                    cb);
+            }
+            if (act) {
+                const bool right = 2 * bw + 1 < g.W;
+#pragma unroll
+                for (int a = 0; a < ROWS; a++) {
+                    const int bh = bh0 + a;
+                    if (bh < HB) {
+                        __nv_bfloat16* o = dx + (((long long)n * g.H + 2 * bh) * g.W + 2 * bw) * g.C + c0;
+                        pool_block_k3s2<false>(L[a], Rw[a], L[a + 1], Rw[a + 1], o, rs, g.C, right, 2 * bh + 1 < g.H);
+                    }
+                }
+            }
+#pragma unroll
+            for (int a = 0; a <= ROWS; a++) L[a] = Rw[a];
+        }
+    }
+}
+
+int g_fused_rb = 0;   // CAFFE_TUNE_FUSED_POOL_ROWS: block rows per strip of the fused backward (0 = automatic)
+
+bool pool_lrn_fusable(const PoolGeom& g, int size) {
+    return k3s2_full(g) && g.C % 8 == 0 && g.C / 8 <= 32 && size <= 9 && size % 2 == 1;
+}
+
+static unsigned warps_grid(long long warps) {
+    long long b = (warps * 32 + 255) / 256;
+    const long long cap = 148LL * 16;
+    return (unsigned)std::max(1LL, std::min(b, cap));
+}
+
+cudaError_t pool_lrn_fwd(const void* x, void* p, void* mask, void* y, const PoolGeom& g, int size, float alpha,
+                         float beta, float k, cudaStream_t s) {
+    const int cv = g.C / 8;
+    if (cv > 32) return cudaErrorInvalidValue;
+    const int ppw = 32 / cv, npix = g.N * g.OH * g.OW;
+    const unsigned grid = warps_grid((npix + ppw - 1) / ppw);
+    const float an = alpha / size;
+    auto X = (const __nv_bfloat16*)x;
+    auto P = (__nv_bfloat16*)p;
+    auto Y = (__nv_bfloat16*)y;
+    auto M = (uint8_t*)mask;
+    switch ((size - 1) / 2) {
+        case 0: pool_lrn_fwd_k3s2_nhwc8<0><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+        case 1: pool_lrn_fwd_k3s2_nhwc8<1><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+        case 2: pool_lrn_fwd_k3s2_nhwc8<2><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+        case 3: pool_lrn_fwd_k3s2_nhwc8<3><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+        default: pool_lrn_fwd_k3s2_nhwc8<4><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int R, int ROWS>
+static void lrn_pool_bwd_rows(bool relu, unsigned grid, cudaStream_t s, const __nv_bfloat16* P, const __nv_bfloat16* DN,
+                              const uint8_t* M, __nv_bfloat16* DX, const PoolGeom& g, int HB, int WB, int nstrip,
+                              int cseg, int ncseg, int ntask, float an, float beta, float k, float cb) {
+    if (relu)
+        lrn_pool_bwd_k3s2_nhwc8<R, true, ROWS><<<grid, 256, 0, s>>>(P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask,
+                                                                     an, beta, k, cb);
+    else
+        lrn_pool_bwd_k3s2_nhwc8<R, false, ROWS><<<grid, 256, 0, s>>>(P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask,
+                                                                      an, beta, k, cb);
+}
+
+template <int R>
+static void lrn_pool_bwd_r(int rows, bool relu, unsigned grid, cudaStream_t s, const __nv_bfloat16* P,
+                           const __nv_bfloat16* DN, const uint8_t* M, __nv_bfloat16* DX, const PoolGeom& g, int HB,
+                           int WB, int nstrip, int cseg, int ncseg, int ntask, float an, float beta, float k, float cb) {
+    if (rows == 1) lrn_pool_bwd_rows<R, 1>(relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb);
+    else if (rows == 2) lrn_pool_bwd_rows<R, 2>(relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb);
+    else lrn_pool_bwd_rows<R, 4>(relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb);
+}
+
+cudaError_t lrn_pool_bwd(const void* p, const void* dn, const void* mask, void* dx, int relu, const PoolGeom& g,
+                         int size, float alpha, float beta, float k, cudaStream_t s) {
+    const int cv = g.C / 8;
+    if (cv > 32) return cudaErrorInvalidValue;
+    const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2;
+    // strips of `rows` block rows (each strip recomputes one halo window row: (rows+1)/rows LRN
+    // work) split into column segments of cseg blocks (one recomputed window column each)
+    int rows = g_fused_rb > 0 ? g_fused_rb : 4;
+    rows = rows >= 4 ? 4 : rows >= 2 ? 2 : 1;
+    if (rows > HB) rows = HB >= 2 ? 2 : 1;
+    const int nstrip = (HB + rows - 1) / rows;
+    const int ncseg = WB >= 16 ? 2 : 1, cseg = (WB + ncseg - 1) / ncseg;
+    const int ntask = g.N * nstrip * ncseg;
+    const int ppw = 32 / cv;
+    const unsigned grid = warps_grid((ntask + ppw - 1) / ppw);
+    const float an = alpha / size, cb = 2.f * an * beta;
+    auto P = (const __nv_bfloat16*)p;
+    auto DN = (const __nv_bfloat16*)dn;
+    auto M = (const uint8_t*)mask;
+    auto DX = (__nv_bfloat16*)dx;
+    switch ((size - 1) / 2) {
+        case 0: lrn_pool_bwd_r<0>(rows, relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb); break;
+        case 1: lrn_pool_bwd_r<1>(rows, relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb); break;
+        case 2: lrn_pool_bwd_r<2>(rows, relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb); break;
+        case 3: lrn_pool_bwd_r<3>(rows, relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb); break;
+        default: lrn_pool_bwd_r<4>(rows, relu, grid, s, P, DN, M, DX, g, HB, WB, nstrip, cseg, ncseg, ntask, an, beta, k, cb); break;
+    }
     note_launch();
     return cudaGetLastError();
 }

@@ -149,13 +149,25 @@ def test_maxpool_bench_config(oracle, stepped, name):
     px = np.arange(OW).reshape(1, 1, 1, OW)
     np.testing.assert_array_equal((py * L.stride + loc // L.kernel) * x.shape[3] + (px * L.stride + loc % L.kernel),
                                   rM)
-    # backward (the ReLU of the conv below folded in, caffe_pool_relu_backward): FP32 gather in the
-    # R8 order, stored as RNE BF16
-    dy = host(net.d[i + 1])
+    # backward (the ReLU of the conv below folded in): FP32 gather in the R8 order, stored as RNE
+    # BF16.  pool1/pool2 run fused with the LRN above (caffe_lrn_pool_backward: the LRN's bottom diff
+    # is never stored), so their top diff is that LRN backward recomputed here by the separate call
+    # (itself checked against the oracle in test_lrn_bench_config)
+    dy = host(_pool_top_diff(net, i))
     ref = oracle.maxpool_backward(dy, rM, x.shape, (L.kernel,) * 2, (L.stride,) * 2)
     if _relu_below(net, i):
         ref = oracle.relu_backward(x, ref)
     np.testing.assert_array_equal(host(net.d[i]), oracle.quant_bf16(ref))
+
+
+def _pool_top_diff(net, i):
+    """The top diff pool layer i consumed: d[i+1], or -- pool fused with the LRN above -- the LRN's
+    bottom diff from the separate caffe_lrn_backward on the step's own blobs."""
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import nets
+    if not (net._pool_lrn(i) and net.fuse_lrn_pool_backward):
+        return net.d[i + 1]
+    return cb.lrn_backward(net.a[i + 1], net.a[i + 2], net.d[i + 2], **nets.LRN)
 
 
 @pytest.mark.parametrize("name", ["norm1", "norm2"])
@@ -167,7 +179,7 @@ def test_lrn_bench_config(oracle, stepped, name):
     assert_bf16_ulp(_a(net, i + 1), ref, f"{name} fwd")
     dy = _d(net, i + 1)
     ref = oracle.lrn_backward(x, dy, **LRN)
-    got = _d(net, i)
+    got = host(_pool_top_diff(net, i - 1)).astype(np.float64)
     assert_tc_close(got, _q(ref), f"{name} bwd rel-L2")
     # the kernel uses the stored BF16 top in the cross-channel term (-2ab/n x sum dy y / S): admit its
     # rounding where the first term cancels

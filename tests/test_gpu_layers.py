@@ -429,3 +429,54 @@ def test_blob_to_nchw(dt):
         cb.to_nchw(x, out=torch.empty(tuple(x.shape), dtype=torch.float32, device="cuda"))
     with pytest.raises(RuntimeError):
         cb.to_nchw(x, out=torch.empty((5, 256, 6, 5), dtype=d, device="cuda"))
+
+
+@pytest.mark.parametrize("shape", [(3, 96, 55, 55), (2, 256, 27, 27), (2, 16, 13, 13), (1, 8, 7, 9)],
+                         ids=["pool1norm1", "pool2norm2", "c16", "c8odd"])
+@pytest.mark.parametrize("relu", [True, False])
+@pytest.mark.parametrize("lrn", [(5, 1e-4, 0.75, 1.0), (3, 0.5, 0.75, 2.0)])
+def test_fused_pool_lrn_bit_identical(oracle, shape, relu, lrn):
+    """caffe_pool_lrn_forward / caffe_lrn_pool_backward give exactly the bits of
+    caffe_pool_forward + caffe_lrn_forward and of caffe_lrn_backward + caffe_pool_(relu_)backward, on
+    CaffeNet's pool1/norm1 and pool2/norm2 geometries and small odd ones (ragged strips); and the
+    composition matches the oracle (pool bit-exact, LRN within 1 BF16 ulp)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    cl = torch.channels_last
+    size, a, b, k = lrn
+    X = oracle.quant_bf16(np.maximum(synth.uniform(shape, 17, synth.S_X) * 4, 0.0) if relu else
+                          synth.uniform(shape, 17, synth.S_X) * 4)
+    X[0, 0, :4, :4] = 1.0                          # ties
+    xt = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    P, M = cb.pool_forward(xt, "max", 3, 2, mask_dtype=torch.uint8)
+    Y = cb.lrn_forward(P, size, a, b, k)
+    Pf, Mf, Yf = cb.pool_lrn_forward(xt, 3, 2, 0, size, a, b, k)
+    np.testing.assert_array_equal(host(Pf), host(P))
+    np.testing.assert_array_equal(host(Mf).astype(np.int64), host(M).astype(np.int64))
+    np.testing.assert_array_equal(host(Yf), host(Y))
+    G = cuda(oracle.quant_bf16(synth.uniform(tuple(P.shape), 18, synth.S_DY))).to(torch.bfloat16) \
+        .contiguous(memory_format=cl)
+    dP = cb.lrn_backward(P, Y, G, size, a, b, k)
+    dX = cb.pool_relu_backward(P, dP, M, shape, 3, 2) if relu else cb.pool_backward(dP, M, shape, "max", 3, 2)
+    dXf = cb.lrn_pool_backward(Pf, G, Mf, shape, 3, 2, 0, size, a, b, k, relu=relu)
+    np.testing.assert_array_equal(host(dXf), host(dX))
+    # against the oracle: pool exact, LRN <= 1 ulp, the pool backward of the GPU's LRN diff exact
+    rP, rM = oracle.maxpool_forward(X, (3, 3), (2, 2))
+    np.testing.assert_array_equal(host(Pf), rP)
+    assert_bf16_ulp(host(Yf), oracle.lrn_forward(rP, size, a, b, k), "fused lrn fwd")
+    rdP = oracle.lrn_backward(rP, host(G), size, a, b, k)
+    assert_bf16_ulp(host(dP), rdP, "lrn bwd", atol=float(np.abs(rdP).max()) * 2.0 ** -16)
+    ref = oracle.maxpool_backward(host(dP), rM, shape, (3, 3), (2, 2))
+    if relu:
+        ref = oracle.relu_backward(X, ref)
+    np.testing.assert_array_equal(host(dXf), oracle.quant_bf16(ref))
+
+
+def test_fused_pool_lrn_rejects_other_geometry():
+    import torch
+    import paper_1408_5093_b200 as cb
+    x = torch.zeros((1, 16, 12, 12), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    with pytest.raises(cb.CaffeError, match="E_INVALID"):
+        cb.pool_lrn_forward(x, 2, 2, 0)              # 2x2 windows
+    with pytest.raises(cb.CaffeError, match="E_DTYPE"):
+        cb.pool_lrn_forward(x.float(), 3, 2, 0)

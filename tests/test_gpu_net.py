@@ -27,6 +27,7 @@ def _build(which, batch, act):
     layers, shape = (nets.LENET, nets.LENET_INPUT) if which == "lenet" else (nets.CAFFENET, nets.CAFFENET_INPUT)
     dt = torch.float32 if act == "f32" else torch.bfloat16
     net = nets.Net(layers, batch, shape, torch.device("cuda"), act_dtype=dt, math="bf16", seed=0)
+    net.fuse_pool_lrn = False   # every layer's blobs stored (the fused kernels: test_fused_pool_lrn_bit_identical)
     X = synth.int_pixels((batch,) + tuple(shape), 7) if which == "caffenet" else \
         synth.mnist_pixels((batch,) + tuple(shape), 7)
     lab = synth.labels(batch, net.shapes[-1][1], 7)
