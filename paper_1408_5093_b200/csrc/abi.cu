@@ -452,7 +452,7 @@ static bool stacked_geom(const HaloGeom& h) {
 // 67.5/52.2/38.8 (one accumulator per CTA: every weight tile feeds a single 128-pixel tile).
 static bool stacked_applies(int E, const HaloGeom& h, int BN) {
     if (E != 2 || g_halo == 1 || g_halo_stacked == 0 || !stacked_geom(h)) return false;
-    if (g_halo_stacked == 2) return true;
+    if (g_halo_stacked >= 2) return true;
     return !halo_applies(E, h) && BN <= 128;
 }
 // Fills the halo fields of L (A map over the channels-last operand `aptr` [N][Hi][Wi][Ctot]) after
@@ -495,6 +495,12 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     a.a_stages = 2;
     a.macc = 1;
     if (2 * 2 * a.acc_stride <= 512 && a.a_stages * 2 * a.halo_slot <= 140 * 1024) a.macc = 2;
+    // CAFFE_TUNE_HALO_STACKED 3: stacked tiles of up to 256 columns also take two accumulators per
+    // CTA (each weight tile feeds 2 x 128 pixels; the 512 TMEM columns then hold one set, so the
+    // epilogue of a unit does not overlap the next unit's MMAs)
+    if (a.stk && g_halo_stacked >= 3 && a.macc == 1 && a.acc_stride == 256 &&
+        a.a_stages * 2 * a.halo_slot <= 140 * 1024)
+        a.macc = 2;
     // (a deeper A ring for stacked tiles -- 3 or 4 stages -- measured no faster: 2 stages kept)
     a.b_stage_bytes = a.BN / L.cg * 128;
     long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
@@ -650,7 +656,8 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO_STACKED) {
-        if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "stacked halo mode must be 0 (off), 1 (auto), 2 (force)");
+        if (value < 0 || value > 3)
+            return fail(CAFFE_E_PARAM, "stacked halo mode must be 0 (off), 1 (auto), 2 (force), 3 (force, 2 accumulators to 256 columns)");
         g_halo_stacked = value;
         return CAFFE_OK;
     }

@@ -101,6 +101,19 @@ def main():
             n += 1
         res["launch_list_summary"] = {"launches": n, "total_us": round(tot, 1),
                                       "by_kernel_us": {k: round(v, 1) for k, v in sorted(by.items(), key=lambda x: -x[1])}}
+    # conv GEMM aggregates for bench.py's roofline: mean DRAM bytes per launch and the tensor-pipe
+    # activity weighted by each launch's algorithmic FLOPs
+    conv = [r for r in out if r["launch"].startswith("conv")]
+    if conv and all(r.get("dram_read_MB") is not None for r in conv):
+        fl = [CONV_GF[r["launch"].split(" ")[0]] for r in conv]
+        tp = [r.get("tensor_pipe_active_pct") or 0.0 for r in conv]
+        res["conv_gemm_aggregate"] = {
+            "conv_gemm_launches": len(conv),
+            "conv_gemm_dram_bytes_per_launch": sum((r["dram_read_MB"] + r["dram_write_MB"]) * 1e6 for r in conv) / len(conv),
+            "conv_gemm_tensor_pipe_pct_flop_weighted": sum(f * t for f, t in zip(fl, tp)) / sum(fl),
+            "conv_gemm_tensor_pipe_pct_time_weighted": sum((r.get("time_us") or 0) * t for r, t in zip(conv, tp)) /
+            max(1e-9, sum(r.get("time_us") or 0 for r in conv)),
+        }
     s = json.dumps(res, indent=1)
     if args.out:
         open(args.out, "w").write(s + "\n")
