@@ -203,6 +203,10 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_FUSED_POOL_ROWS: 2x2-block rows per CTA of caffe_lrn_pool_backward (0 = automatic).
    Results are identical for every value. */
 #define CAFFE_TUNE_FUSED_POOL_ROWS 17
+/* CAFFE_TUNE_HALO_COALESCE: 1 (default) = the specialised halo epilogue transposes each warp's rows
+   through shared memory so its global stores are coalesced (conv1's 148.7 MB output); 0 = each
+   thread stores its own row.  Bit-identical results. */
+#define CAFFE_TUNE_HALO_COALESCE 18
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -529,6 +529,16 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     // weights resident in shared memory when the whole filter (this CTA's half) fits: staged once
     // per kernel instead of once per unit (the first layer: 9 taps x 6 KB)
     const long long nb = (long long)h.kh * h.kw * a.a_cblocks;
+    // coalesced stores of the specialised epilogue (per-warp transpose through shared memory), when
+    // the staging fits beside resident weights -- the first layer, whose 148.7 MB output bounds it
+    // (conv1 forward 81.7 -> 78.5 us; with a streamed B ring the staging costs B stages instead:
+    // conv2 forward 92.4 -> 96.0 us)
+    a.epi_coal = 0;
+    if (epc > 0 && !a.tma_store && cb::g_halo_coal && a.groups == 1 && a.n_tiles == 1 && nb <= 24 &&
+        nb * a.b_stage_bytes <= budget - (long long)halo_coal_bytes(a) - 1024) {
+        a.epi_coal = 1;
+        budget -= (long long)halo_coal_bytes(a) + 1024;
+    }
     a.b_resident = 0;
     if (a.groups == 1 && a.n_tiles == 1 && nb <= 24 && nb * a.b_stage_bytes <= budget) {
         a.b_resident = 1;
@@ -621,6 +631,10 @@ caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_
 }
 
 caffe_status caffe_set_tuning(int32_t key, int32_t value) {
+    if (key == CAFFE_TUNE_HALO_COALESCE) {
+        cb::g_halo_coal = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_FUSED_POOL_ROWS) {
         if (value < 0 || value > 64) return fail(CAFFE_E_PARAM, "fused pool rows must be 0 (auto) .. 64");
         cb::g_fused_rb = value;

@@ -45,6 +45,66 @@ __device__ __forceinline__ void epi_store_bf16_rowseg(uint32_t taddr, bool row_o
     for (int q = 0; q < EPC / 8; q++) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
 }
 
+// Same arithmetic as epi_store_bf16_rowseg, with the stores coalesced through a per-warp shared-
+// memory transpose: each lane stages its row's EPC/8 16-byte pieces (row stride an odd number of
+// pieces: conflict-free), then the warp writes the 32 rows' pieces in order -- consecutive lanes
+// store consecutive 16-byte pieces of a pixel's channel segment, so a store instruction covers ~6
+// pixel segments instead of 32 scattered 16-byte pieces (the direct form is bound by the L1 store
+// path at one piece per lane per cycle: conv1's 148.7 MB output).  Warp-collective: every lane
+// calls it; rows with row_ok == false store nothing.
+template <int EPC>
+constexpr int coal_warp_bytes() { return 32 * ((EPC / 8) | 1) * 16; }
+
+template <int EPC>
+__device__ __forceinline__ void epi_store_bf16_rowseg_coal(uint32_t taddr, bool row_ok, __nv_bfloat16* dst,
+                                                           uint32_t sbias_addr, bool bias, bool relu, uint32_t wstage,
+                                                           int lane) {
+    constexpr int NCH = EPC / 8;     // 16-byte pieces per row
+    constexpr int STR = NCH | 1;     // staging row stride in pieces (odd)
+    uint32_t v[EPC];
+#pragma unroll
+    for (int c = 0; c < EPC; c += 16) {
+        if (c + 16 <= EPC) tmem_ld16p(taddr + c, v + c);
+        else tmem_ld8p(taddr + c, v + c);
+    }
+    tmem_wait_ld();
+    uint32_t pk[EPC / 2];
+#pragma unroll
+    for (int c = 0; c < EPC; c += 4) {
+        float x0 = __uint_as_float(v[c]), x1 = __uint_as_float(v[c + 1]);
+        float x2 = __uint_as_float(v[c + 2]), x3 = __uint_as_float(v[c + 3]);
+        if (bias) {
+            const float4 b = lds_f4(sbias_addr + 4u * c);
+            x0 += b.x; x1 += b.y; x2 += b.z; x3 += b.w;
+        }
+        if (relu) {
+            x0 = x0 > 0.f ? x0 : 0.f; x1 = x1 > 0.f ? x1 : 0.f;
+            x2 = x2 > 0.f ? x2 : 0.f; x3 = x3 > 0.f ? x3 : 0.f;
+        }
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(x0, x1), h1 = __floats2bfloat162_rn(x2, x3);
+        pk[c / 2] = *reinterpret_cast<uint32_t*>(&h0);
+        pk[c / 2 + 1] = *reinterpret_cast<uint32_t*>(&h1);
+    }
+    __syncwarp();   // the previous call's copy-out has finished reading the staging
+#pragma unroll
+    for (int q = 0; q < NCH; q++)
+        sts_u4(wstage + (uint32_t)((lane * STR + q) * 16), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    __syncwarp();
+    const unsigned ok = __ballot_sync(0xffffffffu, row_ok);
+    const unsigned long long mine = reinterpret_cast<unsigned long long>(dst);
+#pragma unroll
+    for (int it = 0; it < NCH; it++) {
+        const int c = it * 32 + lane;
+        const int p = c / NCH, k = c - p * NCH;
+        const unsigned long long pp = __shfl_sync(0xffffffffu, mine, p);
+        uint32_t a, b, cc, d;
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a), "=r"(b), "=r"(cc), "=r"(d)
+                     : "r"(wstage + (uint32_t)((p * STR + k) * 16)));
+        if ((ok >> p) & 1u) reinterpret_cast<uint4*>(pp)[k] = make_uint4(a, b, cc, d);
+    }
+}
+
 // Same arithmetic as epi_store_bf16_rowseg, but the row's EPC columns (tile columns
 // [col_begin, col_begin + EPC)) go to the shared-memory TMA staging of the tile: chunk q of cw
 // channels holds box row r (= pixel) at q*chunk_bytes + r*cw*2, 16-byte piece k stored at

@@ -67,6 +67,9 @@ struct TcArgs {
     // out_w pixels x halo_th rows (swizzled by the box row width: 128/64/32 B, or none when the
     // row is an odd number of 16-byte pieces) and written by 4-D tensor stores through mapC
     int st_cw, st_chunk_bytes, st_tile_bytes;
+    // A_HALO_K specialised epilogue (EPC > 0, no TMA store): stores coalesced through a per-warp
+    // shared-memory transpose (epi_store_bf16_rowseg_coal)
+    int epi_coal;
     // EPI_STRIDED data gradient through a ReLU (caffe_conv_backward_data_relu): the result of the
     // pass is kept where relu_top (same element strides as out) is > 0 and zeroed elsewhere,
     // before beta*old is added
@@ -105,6 +108,8 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s);
 cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s);
 size_t tc_halo_wgrad_smem_bytes(const TcArgs& a);
 size_t tc_halo_smem_bytes(const TcArgs& a);
+size_t halo_coal_bytes(const TcArgs& a);
+extern int g_halo_coal;   // CAFFE_TUNE_HALO_COALESCE
 int halo_fast_epc(const TcArgs& a, int cg);
 extern int g_halo_tma_store;   // CAFFE_TUNE_HALO_TMA_STORE
 int num_sms();

@@ -28,13 +28,20 @@ namespace cb {
 
 constexpr int HALO_SMEM_ALIGN = 1024;
 int g_halo_fast_epi = 1;   // CAFFE_TUNE_HALO_FAST_EPI
+int g_halo_coal = 1;       // CAFFE_TUNE_HALO_COALESCE
 int g_halo_tma_store = 0;   // CAFFE_TUNE_HALO_TMA_STORE (off: measured no gain for conv1, conv2 fwd 92 -> 106 us)
+
+// per-CTA staging of the coalesced specialised epilogue: 8 epilogue warps
+size_t halo_coal_bytes(const TcArgs& a) {
+    const int epc = a.BN / 2;
+    return (size_t)8 * 32 * ((epc / 8) | 1) * 16;
+}
 
 size_t tc_halo_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
     return (size_t)a.a_stages * macc * a.halo_slot + (size_t)a.stages * a.b_stage_bytes + 512 /*barriers*/ +
            2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN + (a.rows_epi ? 4 * 32 * 17 * 16 : 0) +
-           (a.tma_store ? (size_t)macc * a.st_tile_bytes + 1024 : 0);
+           (a.tma_store ? (size_t)macc * a.st_tile_bytes + 1024 : 0) + (a.epi_coal ? halo_coal_bytes(a) + 1024 : 0);
 }
 
 // KS: 16-channel K steps issued per 64-channel block (4; 3 when the only block holds 48 real
@@ -306,8 +313,13 @@ __global__ void __launch_bounds__(384, 1)
                         continue;
                     }
                     __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + rbase + cbase + cb_;
-                    epi_store_bf16_rowseg<EPC>(taddr + a * args.acc_stride + cb_, row_ok, dst,
-                                               smem_u32(bs + cb_), args.bias != nullptr, args.relu != 0);
+                    if (args.epi_coal)
+                        epi_store_bf16_rowseg_coal<EPC>(taddr + a * args.acc_stride + cb_, row_ok, dst,
+                                                        smem_u32(bs + cb_), args.bias != nullptr, args.relu != 0,
+                                                        stg + (uint32_t)((warp - 4) * coal_warp_bytes<EPC>()), lane);
+                    else
+                        epi_store_bf16_rowseg<EPC>(taddr + a * args.acc_stride + cb_, row_ok, dst,
+                                                   smem_u32(bs + cb_), args.bias != nullptr, args.relu != 0);
                 } else if (cb_ < ce_) {
                     epi_store_strided(args, taddr + a * args.acc_stride, row_ok, rbase, col0, cbase, bs, cb_, ce_);
                 }

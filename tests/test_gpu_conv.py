@@ -412,9 +412,11 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
     _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
     _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 2)
     try:
-        for fast in (0, 1, 2):   # generic; specialised with direct stores; specialised with TMA stores
+        # generic; specialised with per-row stores; with TMA stores; with warp-transposed coalesced stores
+        for fast in (0, 1, 2, 3):
             _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_FAST_EPI, 1 if fast else 0)
             _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_TMA_STORE, 1 if fast == 2 else 0)
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_COALESCE, 1 if fast == 3 else 0)
             y = cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True)
             y0 = cb.conv_forward(Xd, cuda(Wt), None, stride=s, pad=p, group=g, relu=False)
             r = {"y": host(y), "y_nobias": host(y0)}
@@ -431,11 +433,13 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
     finally:
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_FAST_EPI, 1)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_TMA_STORE, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_COALESCE, 1)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
     for kk in outs[0]:
         np.testing.assert_array_equal(outs[0][kk], outs[1][kk], err_msg=kk)
         np.testing.assert_array_equal(outs[0][kk], outs[2][kk], err_msg=kk)
+        np.testing.assert_array_equal(outs[0][kk], outs[3][kk], err_msg=kk)
     # the BF16 outputs are the RNE rounding of the FP32-output pass (R12), which meets the oracle bar
     q = oracle.quant_bf16
     np.testing.assert_array_equal(outs[1]["y"], host(y32.to(torch.bfloat16)))
