@@ -304,7 +304,8 @@ WgradSplit wgrad_split(const Plan& p) {
         }
     }
     if (w.macc > w.m_tiles) w.macc = w.m_tiles;
-    if (p.E != 2) w.macc = 1;
+    // (TF32 takes the same choice: tools/tf32_probe.py, batch 256, conv2-5 weight gradients
+    // 1271/468/389/350 us with one accumulator, 1060/370/312/282 us with 2-4)
     w.m_groups = (int)cdiv(w.m_tiles, w.macc);
     // Split the pixel reduction so that (tiles x splits) work units fill the SMs in whole waves:
     // maximise wave efficiency x split balance x kb/(kb + 2) (per-unit prologue/epilogue cost).

@@ -264,6 +264,15 @@ __global__ void pack_s2d_seg_kernel(const __nv_bfloat16* __restrict__ src, __nv_
     }
 }
 
+// Channels-last FP32 activation whose packed TF32 operand has the same layout (stride 1, no padding,
+// every group's channel count a multiple of 4): a TF32-RN rounding copy in 16-byte vectors.
+__global__ void pack_copy_tf32_kernel(const float4* __restrict__ src, float4* __restrict__ dst, long long n4) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n4; t += (long long)gridDim.x * blockDim.x) {
+        const float4 v = src[t];
+        dst[t] = make_float4(tf32_rn(v.x), tf32_rn(v.y), tf32_rn(v.z), tf32_rn(v.w));
+    }
+}
+
 cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* dst, int dst_esz, const PackGeom& g,
                      cudaStream_t s) {
     const bool plain = g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.Hp == g.H && g.Wp == g.W;
@@ -274,6 +283,16 @@ cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* d
         const int total = g.N * g.Hp * g.Wp * g.sh;
         pack_s2d_seg_kernel<6><<<blocks_for(total, 256), 256, 0, s>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, g,
                                                                        total);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (plain && dst_esz == 4 && !src_bf16 && src_nhwc && ls.sc == 1 && g.cpg == g.Cg && g.G * g.Cg == g.C &&
+        g.Ctot == g.C && g.C % 4 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 &&
+        ls.sw == g.C && ls.sh == (long long)g.W * g.C && ls.sn == (long long)g.H * g.W * g.C) {
+        const long long n4 = (long long)g.N * g.H * g.W * g.C / 4;
+        const long long want = (n4 + 255) / 256;
+        pack_copy_tf32_kernel<<<(unsigned)std::min<long long>(want, 148LL * 16), 256, 0, s>>>(
+            (const float4*)src, (float4*)dst, n4);
         note_launch();
         return cudaGetLastError();
     }

@@ -309,6 +309,24 @@ class Net:
         P = self.layers[i - 1]
         return P.kind in ("conv", "ip") and P.relu
 
+    # cap on the persistent grid of the weight-gradient GEMMs on their side stream (0 = every SM):
+    # leaves SMs to the critical path (data gradients, pool/LRN backward) they run beside
+    wgrad_max_ctas = 0
+
+    def _side_grid(self):
+        import contextlib
+        if not self.wgrad_max_ctas:
+            return contextlib.nullcontext()
+
+        @contextlib.contextmanager
+        def cap():
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_MAX_CTAS, int(self.wgrad_max_ctas))
+            try:
+                yield
+            finally:
+                _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_MAX_CTAS, 0)
+        return cap()
+
     def _sgd_fusable(self, i):
         """caffe_ip_backward_weight_sgd applies: BF16 math, fan-in a multiple of 32 (TMA boxes)."""
         return self.math == "bf16" and self.layers[i].kind == "ip" and self.W[i].shape[1] % 32 == 0
@@ -335,7 +353,7 @@ class Net:
                     ev = torch.cuda.Event()
                     ev.record(torch.cuda.current_stream())
                     wgrad_stream.wait_event(ev)
-                    with torch.cuda.stream(wgrad_stream):
+                    with torch.cuda.stream(wgrad_stream), self._side_grid():
                         cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math,
                                                 beta=0.0, dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
                         self.wgrad_done[i] = torch.cuda.Event()
@@ -380,7 +398,7 @@ class Net:
                     ev = torch.cuda.Event()
                     ev.record(torch.cuda.current_stream())
                     wgrad_stream.wait_event(ev)
-                    with torch.cuda.stream(wgrad_stream):
+                    with torch.cuda.stream(wgrad_stream), self._side_grid():
                         cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
                                               dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
                         self.wgrad_done[i] = torch.cuda.Event()

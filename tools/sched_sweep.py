@@ -1,0 +1,48 @@
+"""Step time (graph replay, CaffeNet batch 256, one B200) under schedule variants of nets.Net:
+    python tools/sched_sweep.py "wgrad_max_ctas=0" "wgrad_max_ctas=96" ...
+Each argument is a comma-separated list of Net attribute assignments."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1408_5093_b200 import nets  # noqa: E402
+
+
+def run(assign):
+    dev = torch.device("cuda")
+    net = nets.Net(nets.CAFFENET, 256, nets.CAFFENET_INPUT, dev, math="bf16", seed=0, input_i8=True)
+    for kv in filter(None, assign.split(",")):
+        k, v = kv.split("=")
+        setattr(net, k, type(getattr(net, k))(eval(v)))
+    net.a[0].copy_(torch.from_numpy(synth.int_pixels((256, 3, 227, 227), 1000)).to(net.a[0].dtype))
+    net.labels.copy_(torch.from_numpy(synth.labels(256, 1000, 1000)))
+    for _ in range(3):
+        net.step()
+    torch.cuda.synchronize()
+    g = net.capture()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            g.replay()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / 10)
+    t = sorted(ts)[2]
+    del net, g
+    torch.cuda.empty_cache()
+    return t
+
+
+if __name__ == "__main__":
+    cfgs = sys.argv[1:] or ["wgrad_max_ctas=0"]
+    for rep in range(2):
+        for c in cfgs:
+            print(f"{c:40s} {run(c) * 1e3:8.1f} us/step", flush=True)

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--math", default="bf16", choices=["bf16", "tf32"])
     args = ap.parse_args()
     dev = torch.device("cuda")
     # CAFFE_TUNE="key=value,..." : library tuning knobs (caffe_set_tuning) for A/B runs
@@ -31,7 +32,8 @@ def main():
     for kv in filter(None, os.environ.get("CAFFE_TUNE", "").split(",")):
         k, v = kv.split("=")
         _abi.call("caffe_set_tuning", int(k), int(v))
-    net = nets.Net(nets.CAFFENET, args.batch, nets.CAFFENET_INPUT, dev, math="bf16", seed=0, input_i8=True)
+    net = nets.Net(nets.CAFFENET, args.batch, nets.CAFFENET_INPUT, dev, math=args.math, seed=0,
+                   input_i8=args.math == "bf16")
     import synth
     net.a[0].copy_(torch.from_numpy(synth.int_pixels((args.batch,) + tuple(nets.CAFFENET_INPUT), 1000))
                    .to(net.a[0].dtype))
