@@ -444,6 +444,8 @@ class Net:
     # the first layer's packed input (ws0) is written by the caller before the step
     # (conv_pack_bottom from the host batch, e.g. bench.py's end-to-end input pipeline)
     external_pack = False
+    # measurement only: leave out the SGD updates of the overlapped step (tools/sched_sweep.py)
+    skip_update = False
     side_sgd_blocks = 1
     side_sgd_threads = 256     # (2 x 128-thread blocks per SM measured the same: 1.503 vs 1.507 ms/step)
     # side-stream SGD updates of the layers whose gradients are final may be held back until the
