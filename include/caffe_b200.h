@@ -207,6 +207,10 @@ caffe_status caffe_device_check(void);
    through shared memory so its global stores are coalesced (conv1's 148.7 MB output); 0 = each
    thread stores its own row.  Bit-identical results. */
 #define CAFFE_TUNE_HALO_COALESCE 18
+/* CAFFE_TUNE_WGRAD_REDUCE_WIDE: 1 = weight-gradient split reductions with >= 64 / >= 96 splits use
+   16 / 32 threads per output (a few partials each); 0 (default, measured faster) = at most 8.
+   Deterministic for either value; the two differ only in the FP32 summation order. */
+#define CAFFE_TUNE_WGRAD_REDUCE_WIDE 19
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -632,6 +632,10 @@ caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_
 }
 
 caffe_status caffe_set_tuning(int32_t key, int32_t value) {
+    if (key == CAFFE_TUNE_WGRAD_REDUCE_WIDE) {
+        cb::g_wgrad_reduce_wide = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_HALO_COALESCE) {
         cb::g_halo_coal = value ? 1 : 0;
         return CAFFE_OK;

@@ -234,6 +234,7 @@ extern int g_sgd_threads;   // CAFFE_TUNE_SGD_THREADS
 extern int g_pool_strip_rows;   // CAFFE_TUNE_POOL_STRIP_ROWS
 extern int g_wgrad_reduce_sg_min;   // CAFFE_TUNE_WGRAD_REDUCE_SG
 extern int g_wgrad_reduce_rows;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS
+extern int g_wgrad_reduce_wide;   // CAFFE_TUNE_WGRAD_REDUCE_WIDE
 extern int g_halo_fast_epi;   // CAFFE_TUNE_HALO_FAST_EPI
 cudaError_t sgd_k(float* w, const float* g, float* v, void* w_bf16, long long count, float lr, float mom,
                   float decay, float gscale, cudaStream_t s);

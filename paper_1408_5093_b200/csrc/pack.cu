@@ -759,6 +759,7 @@ __global__ void wgrad_reduce_rows_kernel(const float* __restrict__ partial, floa
         out[k] = (beta != 0.f ? beta * out[k] : 0.f) + rowbuf[k];
 }
 
+int g_wgrad_reduce_wide = 0;   // CAFFE_TUNE_WGRAD_REDUCE_WIDE (off: conv1 wgrad + reduce 88 -> 121 us with it)
 int g_wgrad_reduce_rows = 0;   // CAFFE_TUNE_WGRAD_REDUCE_ROWS (off: 58.7 vs 52.6 us per step serialised, and its
                                // 1024-thread blocks co-schedule worse beside the side-stream GEMMs)
 
@@ -777,7 +778,14 @@ cudaError_t wgrad_reduce(const float* partial, float* dW, float beta, const WGeo
     if (splits >= g_wgrad_reduce_sg_min) {
         const int nout = total + (db ? g.G * g.Og : 0);
         const unsigned nb = (unsigned)std::min<long long>((nout + 31) / 32, 148LL * 16);
-        if (splits >= 32)
+        // 16/32 threads per output (a few partials each) measured slower than 8 (tools/reduce_probe.py)
+        if (splits >= 96 && g_wgrad_reduce_wide)
+            wgrad_reduce_sg_kernel<32><<<nb, dim3(32, 32), 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
+                                                                  chunk, cblocks, 128 / chunk, total, cbmajor, db);
+        else if (splits >= 64 && g_wgrad_reduce_wide)
+            wgrad_reduce_sg_kernel<16><<<nb, dim3(32, 16), 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
+                                                                  chunk, cblocks, 128 / chunk, total, cbmajor, db);
+        else if (splits >= 32)
             wgrad_reduce_sg_kernel<8><<<nb, dim3(32, 8), 0, s>>>(partial, dW, beta, g, m_tiles, n_tiles, splits, BN,
                                                                 chunk, cblocks, 128 / chunk, total, cbmajor, db);
         else
