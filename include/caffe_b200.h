@@ -211,6 +211,10 @@ caffe_status caffe_device_check(void);
    16 / 32 threads per output (a few partials each); 0 (default, measured faster) = at most 8.
    Deterministic for either value; the two differ only in the FP32 summation order. */
 #define CAFFE_TUNE_WGRAD_REDUCE_WIDE 19
+/* CAFFE_TUNE_HALO_BTAPS: filter taps' weight tiles per B pipeline stage of the halo-tiled forward /
+   data gradient: 0 (default) = 5 where compiled (the 24-column-per-CTA data gradient of 5x5
+   filters, CaffeNet conv2) and >= 4 stages fit, else 1; 1 = always one.  Identical results. */
+#define CAFFE_TUNE_HALO_BTAPS 20
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -459,6 +459,7 @@ static bool stacked_applies(int E, const HaloGeom& h, int BN) {
 // Fills the halo fields of L (A map over the channels-last operand `aptr` [N][Hi][Wi][Ctot]) after
 // the caller has set BN, N, n_tiles, groups, b_row_g, a_cpg, a_cblocks and the epilogue.
 int g_halo_ktrim = 1;   // CAFFE_TUNE_HALO_KTRIM
+int g_halo_btaps = 0;   // CAFFE_TUNE_HALO_BTAPS
 static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Ctot, int N) {
     TcArgs& a = L.args;
     L.amode = A_HALO_K; L.bmode = B_TILED_K; L.epi = EPI_STRIDED; L.esz = 2;
@@ -541,10 +542,20 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
         budget -= (long long)halo_coal_bytes(a) + 1024;
     }
     a.b_resident = 0;
+    a.b_taps = 1;
     if (a.groups == 1 && a.n_tiles == 1 && nb <= 24 && nb * a.b_stage_bytes <= budget) {
         a.b_resident = 1;
         a.stages = (int)nb;
     } else {
+        // CAFFE_TUNE_HALO_BTAPS: weight tiles per B stage (0 = automatic: 2 for tiles of <= 32 rows
+        // per CTA, whose MMAs are short enough for the issue loop to matter)
+        // compiled: 5 taps per stage for the specialised 24-column epilogue instance (conv2's data
+        // gradient, 5x5 filter) when >= 4 stages still fit; 1 elsewhere
+        const int epc_b = halo_fast_epc(a, L.cg);
+        const int want = g_halo_btaps > 0 ? g_halo_btaps : 5;
+        if (want == 5 && epc_b == 24 && a.k_last != 3 && (h.kh * h.kw) % 5 == 0 && budget / (5LL * a.b_stage_bytes) >= 4)
+            a.b_taps = 5;
+        a.b_stage_bytes *= a.b_taps;
         a.stages = (int)std::min<long long>(24, budget / a.b_stage_bytes);
     }
     if (a.stages < 2) return false;
@@ -632,6 +643,11 @@ caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_
 }
 
 caffe_status caffe_set_tuning(int32_t key, int32_t value) {
+    if (key == CAFFE_TUNE_HALO_BTAPS) {
+        if (value < 0 || value > 8) return fail(CAFFE_E_PARAM, "halo B taps per stage must be 0 (auto) .. 8");
+        g_halo_btaps = value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_WGRAD_REDUCE_WIDE) {
         cb::g_wgrad_reduce_wide = value ? 1 : 0;
         return CAFFE_OK;

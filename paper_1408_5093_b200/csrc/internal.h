@@ -57,6 +57,7 @@ struct TcArgs {
     int bias_mma;                       // A_HALO_MN, odd taps: the last pair's spare chunk is all ones, so
                                         // its accumulator rows 64-127 hold sum_pixels dY (bias gradient)
     int a_stages;                       // halo stages in the A ring
+    int b_taps;                         // A_HALO_K: weight tiles (taps) per B stage (1 when resident)
     int b_resident;                     // A_HALO_K: all B tiles (taps x channel blocks) stay in shared
                                         // memory for the whole kernel (one group, one N tile)
     int tma_store;                      // EPI_STRIDED: store tiles with TMA (mapC; row-major output, beta 0)

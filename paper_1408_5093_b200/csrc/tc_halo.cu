@@ -48,7 +48,7 @@ size_t tc_halo_smem_bytes(const TcArgs& a) {
 // channels -- conv1 after space-to-depth, conv2 per group -- so the zero padding is not multiplied)
 // EPC > 0: the specialised channels-last BF16 epilogue (epi_store_bf16_rowseg), each of the two
 // epilogue groups writing EPC = BN/2 columns
-template <int CG, int MACC, int KS, int EPC>
+template <int CG, int MACC, int KS, int EPC, int BT>
 __global__ void __launch_bounds__(384, 1)
     tc_halo_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, const TcArgs args) {
@@ -157,15 +157,19 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 if (++sa == a_stages) { sa = 0; pa ^= 1; }
                 if (args.b_resident) continue;
-                for (int tap = 0; tap < taps; tap++) {
+                // BT weight tiles (taps) per B stage; BT divides the tap count (host)
+                for (int tap = 0; tap < taps; tap += BT) {
                     mbar_wait(&emptyB[sb], pb ^ 1);
                     if (CG == 1 || leader) mbar_arrive_expect_tx(&fullB[sb], txB * CG);
                     else mbar_arrive_cluster(mapa_shared(smem_u32(&fullB[sb]), 0));
-                    const int kb = tap * cblocks + cb;
                     const int row = g * args.b_row_g + n_tile * args.BN + (int)rank * bn_cta;
-                    uint8_t* dst = b_ring + sb * args.b_stage_bytes;
-                    if (CG == 2) tma_load_2d_cg2(dst, &mapB, &fullB[sb], kb * CH, row);
-                    else tma_load_2d(dst, &mapB, &fullB[sb], kb * CH, row);
+#pragma unroll
+                    for (int j = 0; j < BT; j++) {
+                        const int kb = (tap + j) * cblocks + cb;
+                        uint8_t* dst = b_ring + sb * args.b_stage_bytes + j * (args.b_stage_bytes / BT);
+                        if (CG == 2) tma_load_2d_cg2(dst, &mapB, &fullB[sb], kb * CH, row);
+                        else tma_load_2d(dst, &mapB, &fullB[sb], kb * CH, row);
+                    }
                     if (++sb == b_stages) { sb = 0; pb ^= 1; }
                 }
             }
@@ -195,6 +199,46 @@ __global__ void __launch_bounds__(384, 1)
                 uint32_t shift = (uint32_t)args.stk_off * 128u;
                 int tj = 0;
                 const uint32_t row_skip = (uint32_t)(args.halo_wt - args.a_kw + 1) * 128u;
+                if constexpr (BT > 1) {
+                    // BT taps per B stage: one barrier wait and one commit per BT x MACC x KSTEPS MMAs
+                    // (the issue loop's own instructions bound the short-N tiles)
+                    const uint32_t b_tile = (uint32_t)(args.b_stage_bytes / BT);
+                    for (int tap = 0; tap < taps; tap += BT) {
+                        mbar_wait(&fullB[sb], pb);
+                        tc_fence_after();
+                        const uint64_t bs0 = smem_desc_sw128(b_base + (uint32_t)sb * (uint32_t)args.b_stage_bytes, 16, 1024);
+                        if (elect_one()) {
+                            uint32_t sh = shift;
+                            int tjj = tj;
+#pragma unroll
+                            for (int j = 0; j < BT; j++) {
+                                const uint64_t bd0 = bs0 + (uint64_t)((j * b_tile) >> 4);
+#pragma unroll
+                                for (int a = 0; a < MACC; a++) {
+                                    const uint64_t ad0 = smem_desc_sw128(sa_addr + a * slot + sh, 16, 1024);
+                                    const uint32_t dt = d_tmem + a * args.acc_stride;
+#pragma unroll
+                                    for (int k = 0; k < KSTEPS; k++) {
+                                        const uint32_t accum = (cb > 0 || tap + j > 0 || k > 0) ? 1u : 0u;
+                                        if (CG == 2) umma_cg2<2>(dt, ad0 + 2 * k, bd0 + 2 * k, idesc, accum);
+                                        else umma<2>(dt, ad0 + 2 * k, bd0 + 2 * k, idesc, accum);
+                                    }
+                                }
+                                if (++tjj == args.a_kw) { tjj = 0; sh += row_skip; }
+                                else sh += 128u;
+                            }
+                            if (CG == 2) umma_commit_cg2(&emptyB[sb]);
+                            else umma_commit(&emptyB[sb]);
+                        }
+                        __syncwarp();
+                        if (++sb == b_stages) { sb = 0; pb ^= 1; }
+#pragma unroll
+                        for (int j = 0; j < BT; j++) {
+                            if (++tj == args.a_kw) { tj = 0; shift += row_skip; }
+                            else shift += 128u;
+                        }
+                    }
+                } else
                 for (int tap = 0; tap < taps; tap++) {
                     const bool bres = args.b_resident != 0;
                     if (!bres) {
@@ -621,9 +665,9 @@ int halo_fast_epc(const TcArgs& a, int cg) {
     return (epc == 24 || epc == 48 || epc == 64) ? epc : 0;
 }
 
-template <int CG, int MACC, int KS, int EPC = 0>
+template <int CG, int MACC, int KS, int EPC = 0, int BT = 1>
 static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
-    auto kern = tc_halo_kernel<CG, MACC, KS, EPC>;
+    auto kern = tc_halo_kernel<CG, MACC, KS, EPC, BT>;
     const size_t smem = tc_halo_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -660,7 +704,7 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s) {
             if (epc == 48) return halo_launch_one<2, 2, 3, 48>(L, s);
             if (epc == 64) return halo_launch_one<2, 2, 3, 64>(L, s);
         } else {
-            if (epc == 24) return halo_launch_one<2, 2, 4, 24>(L, s);
+            if (epc == 24) return a.b_taps == 5 ? halo_launch_one<2, 2, 4, 24, 5>(L, s) : halo_launch_one<2, 2, 4, 24>(L, s);
             if (epc == 48) return halo_launch_one<2, 2, 4, 48>(L, s);
             if (epc == 64) return halo_launch_one<2, 2, 4, 64>(L, s);
         }

@@ -728,3 +728,45 @@ def test_capped_grid_inner_product(oracle, shape, cap):
     assert_tc_close(outs[1][1].reshape(N, K), rdX, "ip dgrad capped")
     assert_tc_close(outs[1][2], rdW, "ip wgrad capped")
     assert_tc_close(outs[1][3], rdb, "ip bias grad capped")
+
+
+@pytest.mark.parametrize("case", [(2, 96, 27, 27, 256, (5, 5), (1, 1), (2, 2), 2),     # conv2: dgrad N = 48
+                                  (2, 64, 20, 37, 48, (3, 3), (1, 1), (1, 1), 1),      # ragged tiles, 9 taps
+                                  (2, 3, 67, 67, 96, (11, 11), (4, 4), (0, 0), 1)],   # conv1 geometry (s2d)
+                         ids=["conv2geom", "H20W37", "conv1geom"])
+def test_halo_btaps_bit_identical(oracle, case):
+    """CAFFE_TUNE_HALO_BTAPS (5 taps' weight tiles per B pipeline stage in the compiled instance --
+    conv2's 24-column data gradient -- or 1) gives the bits of one tap per stage (the MMA order is
+    unchanged), for the halo forward and data gradient, CTA pairs and single CTAs."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 51)
+    if C == 3:
+        X = synth.int_pixels((N, C, H, W), 51)
+    cl = torch.channels_last
+    Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    outs = {}
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
+    try:
+        for cta in (1, 2):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, cta)
+            for bt in (1, 5):
+                _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_BTAPS, bt)
+                r = {"y": host(cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True))}
+                if s[0] == 1:
+                    dX = torch.empty((N, C, H, W), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl)
+                    cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
+                    r["dx"] = host(dX)
+                outs[(cta, bt)] = r
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_BTAPS, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
+    for (cta, bt), r in outs.items():
+        for kk in r:
+            np.testing.assert_array_equal(r[kk], outs[(cta, 1)][kk], err_msg=f"{kk} cta={cta} btaps={bt}")
+    ry = oracle.conv_forward(host(Xd), oracle.quant_bf16(Wt), b, stride=s, pad=p, group=g, relu=True)
+    assert_bf16_ulp(outs[(2, 5)]["y"], ry, "halo fwd btaps=5", atol=_atol(ry))
