@@ -50,6 +50,19 @@ class GradAllReduce:
         self._pending = [set(b[2]) for b in self.buckets]
         self._works = []
 
+    def reduce_loss(self, loss) -> None:
+        """Replace this rank's loss (a device scalar) by the mean over the ranks, in place -- so a
+        non-finite loss on any rank reaches every rank's divergence guard and all of them
+        skip the same update."""
+        import torch.distributed as dist
+        if self.world <= 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(loss, op=dist.ReduceOp.AVG, group=self.group)
+        else:
+            dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=self.group)
+            loss.div_(self.world)
+
     def on_grad(self, key) -> None:
         bi = self.key_bucket[key]
         p = self._pending[bi]
@@ -109,6 +122,8 @@ class BucketedSGD:
                 if n % (4 * world) or (lo % 4):
                     raise ValueError(f"bucket [{lo},{hi}) does not split into {world} aligned slices")
         self._reset()
+
+    reduce_loss = GradAllReduce.reduce_loss
 
     def _reset(self):
         self._grad_pending = [set(b[2]) for b in self.buckets]

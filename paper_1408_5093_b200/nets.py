@@ -484,6 +484,8 @@ class Net:
             momentum, decay = solver.momentum, solver.decay
         self.forward()
         if solver is not None:
+            if allreduce is not None and hasattr(allreduce, "reduce_loss"):
+                allreduce.reduce_loss(self.loss)   # data parallel: one guard decision for all ranks
             solver.begin(self.loss)
         self._step_rest(allreduce, lr, momentum, decay, overlap_update, solver)
         if solver is not None:

@@ -145,3 +145,58 @@ def test_dp_modes_single_rank_nccl(mode, graph):
         np.testing.assert_array_equal(outs[0][1], outs[1][1])
     finally:
         dist.destroy_process_group()
+
+
+def _guard_worker(rank, world, port, mode, out):
+    import torch
+    import torch.distributed as dist
+    try:
+        torch.cuda.set_device(0)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1408_5093_b200.solver import Solver
+        net = _make_net(B)
+        X, lab = _batch(rank * B, B)
+        net.a[0].copy_(torch.from_numpy(X).to(net.a[0].dtype))
+        net.labels.copy_(torch.from_numpy(lab))
+        sync = _sync(mode, net, world, rank)
+        solver = Solver(torch.device("cuda", 0), "step", base_lr=0.05, gamma=0.5, stepsize=1)
+        net.step(sync, solver=solver)
+        torch.cuda.synchronize()
+        before = net.params.cpu().numpy().copy()
+        if rank == 1:
+            net.labels[3] = 10                      # a corrupted label on ONE rank
+        net.step(sync, solver=solver)
+        torch.cuda.synchronize()
+        st = solver.read()
+        np.save(out + f".{rank}.npy", np.array([float(st["diverged"]), float(st["iter"]),
+                                                 float(np.array_equal(before, net.params.cpu().numpy()))]))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        with open(out + f".{rank}.err", "w") as f:
+            f.write(traceback.format_exc())
+
+
+@pytest.mark.parametrize("mode", ["allreduce", "sharded"])
+def test_dp_divergence_guard_is_global(tmp_path, mode):
+    """With a solver, the data-parallel step averages the loss over the ranks before the guard
+    (S:524): a non-finite loss on one rank makes EVERY rank skip the update (parameters unchanged
+    everywhere, the iteration counter stopped), instead of the healthy ranks updating their slices
+    with gradients that already carry the bad rank's NaNs."""
+    import torch.multiprocessing as mp
+    world = 2
+    out = str(tmp_path / "g")
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_guard_worker, args=(r, world, port, mode, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    for r in range(world):
+        if os.path.exists(out + f".{r}.err"):
+            pytest.fail(open(out + f".{r}.err").read())
+        diverged, it, unchanged = np.load(out + f".{r}.npy")
+        assert diverged == 1.0 and it == 1.0 and unchanged == 1.0, (r, diverged, it, unchanged)
