@@ -150,3 +150,61 @@ def test_ip_validation(lib):
     y = A.Blob(ctypes.c_void_p(0x19000), A.Shape4(4, 5, 1, 1), A.CAFFE_F32)
     assert lib.caffe_ip_forward(A.CAFFE_MATH_BF16, 0, ctypes.byref(x), ctypes.byref(w), None, ctypes.byref(y), None, 0, None) == A.CAFFE_E_SHAPE
     assert b"fan-in" in lib.caffe_last_error()
+
+
+def test_catalogue_and_solver_validation(lib):
+    """NEXT-3 / NEXT-4 entry points: host-side errors before any launch (fake device pointers are
+    never touched), the documented classes; the host LR schedule."""
+    from paper_1408_5093_b200 import _abi as A
+    f = lambda a: ctypes.c_void_p(a)  # noqa: E731
+    x = A.Blob(f(0x10000), A.Shape4(2, 4, 3, 3), A.CAFFE_F32)
+    y_shape = A.Blob(f(0x20000), A.Shape4(2, 4, 3, 4), A.CAFFE_F32)
+    assert lib.caffe_sigmoid_forward(ctypes.byref(x), ctypes.byref(y_shape), None) == A.CAFFE_E_SHAPE
+    y_dtype = A.Blob(f(0x20000), A.Shape4(2, 4, 3, 3), A.CAFFE_BF16)
+    assert lib.caffe_sigmoid_forward(ctypes.byref(x), ctypes.byref(y_dtype), None) == A.CAFFE_E_SHAPE
+    y_part = A.Blob(f(0x10000 + 16), A.Shape4(2, 4, 3, 3), A.CAFFE_F32)
+    assert lib.caffe_sigmoid_forward(ctypes.byref(x), ctypes.byref(y_part), None) == A.CAFFE_E_ALIAS
+    y_mis = A.Blob(f(0x20004), A.Shape4(2, 4, 3, 3), A.CAFFE_F32)
+    assert lib.caffe_sigmoid_forward(ctypes.byref(x), ctypes.byref(y_mis), None) == A.CAFFE_E_ALIGN
+    # eltwise: input count (S:236), op enum, coefficients only for SUM, shapes, aliasing
+    ins = (A.Blob * 3)(x, A.Blob(f(0x30000), A.Shape4(2, 4, 3, 3), A.CAFFE_F32),
+                       A.Blob(f(0x40000), A.Shape4(2, 4, 3, 4), A.CAFFE_F32))
+    ptrs = (ctypes.POINTER(A.Blob) * 3)(*[ctypes.pointer(ins[i]) for i in range(3)])
+    top = A.Blob(f(0x50000), A.Shape4(2, 4, 3, 3), A.CAFFE_F32)
+    assert lib.caffe_eltwise_forward(A.CAFFE_ELTWISE_SUM, 1, ptrs, None, ctypes.byref(top), None) == A.CAFFE_E_PARAM
+    assert lib.caffe_eltwise_forward(A.CAFFE_ELTWISE_SUM, 9, ptrs, None, ctypes.byref(top), None) == A.CAFFE_E_PARAM
+    assert lib.caffe_eltwise_forward(7, 2, ptrs, None, ctypes.byref(top), None) == A.CAFFE_E_INVALID
+    coef = (ctypes.c_float * 2)(1.0, 2.0)
+    assert lib.caffe_eltwise_forward(A.CAFFE_ELTWISE_MAX, 2, ptrs, coef, ctypes.byref(top), None) == A.CAFFE_E_PARAM
+    assert lib.caffe_eltwise_forward(A.CAFFE_ELTWISE_MAX, 3, ptrs, None, ctypes.byref(top), None) == A.CAFFE_E_SHAPE
+    diffs = (A.Blob * 2)(A.Blob(f(0x60000), A.Shape4(2, 4, 3, 3), A.CAFFE_F32), A.Blob(f(0x60000), A.Shape4(2, 4, 3, 3), A.CAFFE_F32))
+    dptr = (ctypes.POINTER(A.Blob) * 2)(*[ctypes.pointer(diffs[i]) for i in range(2)])
+    assert lib.caffe_eltwise_backward(A.CAFFE_ELTWISE_PROD, 2, ptrs, None, ctypes.byref(top), dptr, None) == A.CAFFE_E_ALIAS
+    # hinge: NULL labels
+    sc = A.Blob(f(0x70000), A.Shape4(4, 10, 1, 1), A.CAFFE_F32)
+    assert lib.caffe_hinge_loss(ctypes.byref(sc), None, f(0x80000), None, None) == A.CAFFE_E_INVALID
+    # LR schedules on the host (S:517-519) and their errors
+    lr = ctypes.c_float()
+    pol = A.LrPolicy(A.CAFFE_LR_STEP, 0.01, 0.1, 0.0, 100)
+    assert lib.caffe_lr_at_iter(ctypes.byref(pol), 250, ctypes.byref(lr)) == 0
+    assert abs(lr.value - 1e-4) <= 1e-10
+    pol0 = A.LrPolicy(A.CAFFE_LR_STEP, 0.01, 0.1, 0.0, 0)
+    assert lib.caffe_lr_at_iter(ctypes.byref(pol0), 1, ctypes.byref(lr)) == A.CAFFE_E_PARAM
+    assert lib.caffe_lr_at_iter(ctypes.byref(pol), -1, ctypes.byref(lr)) == A.CAFFE_E_PARAM
+    bad = A.LrPolicy(9, 0.01, 0.1, 0.0, 1)
+    assert lib.caffe_lr_at_iter(ctypes.byref(bad), 1, ctypes.byref(lr)) == A.CAFFE_E_INVALID
+    assert lib.caffe_solver_begin(ctypes.byref(pol), f(0x90004), None, None) == A.CAFFE_E_ALIGN
+    assert lib.caffe_sgd_update_solver(f(0x1000), f(0x2000), f(0x3000), None, 16, None, 0.9, 0.0, 1.0, None) == A.CAFFE_E_INVALID
+    # fused pool + LRN: U8 mask and BF16 channels-last are required
+    p = A.PoolDesc(A.CAFFE_POOL_MAX, 3, 3, 2, 2, 0, 0)
+    l5 = A.LrnDesc(5, 1e-4, 0.75, 1.0)
+    xb = A.Blob(f(0x100000), A.Shape4(2, 16, 13, 13), A.CAFFE_BF16, A.CAFFE_NHWC)
+    pb = A.Blob(f(0x200000), A.Shape4(2, 16, 6, 6), A.CAFFE_BF16, A.CAFFE_NHWC)
+    m32 = A.Blob(f(0x300000), A.Shape4(2, 16, 6, 6), A.CAFFE_I32, A.CAFFE_NHWC)
+    yb = A.Blob(f(0x400000), A.Shape4(2, 16, 6, 6), A.CAFFE_BF16, A.CAFFE_NHWC)
+    assert lib.caffe_pool_lrn_forward(ctypes.byref(p), ctypes.byref(l5), ctypes.byref(xb), ctypes.byref(pb),
+                                      ctypes.byref(m32), ctypes.byref(yb), None) == A.CAFFE_E_DTYPE
+    l4 = A.LrnDesc(4, 1e-4, 0.75, 1.0)
+    m8 = A.Blob(f(0x300000), A.Shape4(2, 16, 6, 6), A.CAFFE_U8, A.CAFFE_NHWC)
+    assert lib.caffe_pool_lrn_forward(ctypes.byref(p), ctypes.byref(l4), ctypes.byref(xb), ctypes.byref(pb),
+                                      ctypes.byref(m8), ctypes.byref(yb), None) == A.CAFFE_E_PARAM
