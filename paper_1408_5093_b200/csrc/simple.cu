@@ -877,6 +877,63 @@ __global__ void maxpool_bwd_k3s2_nhwc8(const __nv_bfloat16* __restrict__ dy, con
     }
 }
 
+// FP32 channels-last 3x3/s2 max-pool backward (the TF32 path's activations): thread = one 2x2 block of
+// input positions x 4 channels; its four windows W11, W10, W01, W00 (ascending (py, px)) are read
+// once and each position sums the windows that selected it in that order from +0 in FP32 -- R8's
+// gather, bit-exact.  RELU: a window passes its gradient only when its max (top) is > 0.
+template <bool RELU>
+__global__ void maxpool_bwd_k3s2_f32(const float* __restrict__ dy, const uint8_t* __restrict__ mask,
+                                     const float* __restrict__ top, float* __restrict__ dx, PoolGeom g, int HB, int WB,
+                                     int total) {
+    const int cv = g.C / 4;
+    GRID_STRIDE(t, total) {
+        const int c0 = (t % cv) * 4;
+        int r = t / cv;
+        const int bw = r % WB; r /= WB;
+        const int bh = r % HB;
+        const int n = r / HB;
+        float4 d[4];
+        uint32_t m[4];
+#pragma unroll
+        for (int w = 0; w < 4; w++) {
+            const int py = bh - 1 + (w >> 1), px = bw - 1 + (w & 1);
+            d[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+            m[w] = 0xffffffffu;
+            if (py >= 0 && py < g.OH && px >= 0 && px < g.OW) {
+                const long long q = (((long long)n * g.OH + py) * g.OW + px) * g.C + c0;
+                d[w] = __ldg(reinterpret_cast<const float4*>(dy + q));
+                m[w] = __ldg(reinterpret_cast<const uint32_t*>(mask + q));
+                if (RELU) {
+                    const float4 y = __ldg(reinterpret_cast<const float4*>(top + q));
+                    if (!(y.x > 0.f)) d[w].x = 0.f;
+                    if (!(y.y > 0.f)) d[w].y = 0.f;
+                    if (!(y.z > 0.f)) d[w].z = 0.f;
+                    if (!(y.w > 0.f)) d[w].w = 0.f;
+                }
+            }
+        }
+        // window-local index of each block position in W11, W10, W01, W00 (-1: not in the window)
+        const int loc[4][4] = {{8, 6, 2, 0}, {-1, 7, -1, 1}, {-1, -1, 5, 3}, {-1, -1, -1, 4}};
+#pragma unroll
+        for (int pos = 0; pos < 4; pos++) {
+            const int h = 2 * bh + (pos >> 1), w_ = 2 * bw + (pos & 1);
+            if (h >= g.H || w_ >= g.W) continue;
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int w = 0; w < 4; w++) {
+                const int l = loc[pos][w];
+                if (l < 0) continue;
+                const float dv[4] = {d[w].x, d[w].y, d[w].z, d[w].w};
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                    if ((int)((m[w] >> (8 * e)) & 0xffu) == l) a[e] += dv[e];
+            }
+            *reinterpret_cast<float4*>(dx + (((long long)n * g.H + h) * g.W + w_) * g.C + c0) =
+                make_float4(a[0], a[1], a[2], a[3]);
+        }
+    }
+}
+
 int g_pool_strip_rows = 0;
 
 static inline bool k3s2_full(const PoolGeom& g) {
@@ -966,6 +1023,16 @@ cudaError_t maxpool_bwd(const void* dy, const void* mask, int mask_u8, const voi
                 maxpool_bwd_nhwc8<1, 1, 0, 0, false><<<nblk(total / 8, 256), 256, 0, s>>>(DY, mask, T, DX, g, g.H, g.W,
                                                                                       total / 8);
         }
+    } else if (!bf16 && xnhwc && ynhwc && mask_u8 && k3s2_full(g) && g.C % 4 == 0 &&
+               ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(top) |
+                 reinterpret_cast<uintptr_t>(mask)) & 15) == 0 && ((reinterpret_cast<uintptr_t>(mask) & 3) == 0)) {
+        const int HB = (g.H + 1) / 2, WB = (g.W + 1) / 2, tb = g.N * HB * WB * (g.C / 4);
+        if (top)
+            maxpool_bwd_k3s2_f32<true><<<nblk(tb, 256), 256, 0, s>>>((const float*)dy, (const uint8_t*)mask,
+                                                                      (const float*)top, (float*)dx, g, HB, WB, tb);
+        else
+            maxpool_bwd_k3s2_f32<false><<<nblk(tb, 256), 256, 0, s>>>((const float*)dy, (const uint8_t*)mask, nullptr,
+                                                                       (float*)dx, g, HB, WB, tb);
     } else {
         maxpool_bwd_kernel<<<nblk(total, 256), 256, 0, s>>>(dy, mask, mask_u8, top, ly, dx, xnhwc, bf16, g, total);
     }
@@ -1062,6 +1129,35 @@ __global__ void lrn_fwd_kernel(const void* __restrict__ x, void* __restrict__ y,
     }
 }
 
+// 8 consecutive channel values as floats / back (BF16: one 16-byte vector; FP32: two)
+__device__ __forceinline__ void ld8v(const __nv_bfloat16* p, float (&f)[8]) { unpack8(*reinterpret_cast<const uint4*>(p), f); }
+__device__ __forceinline__ void ld8v(const float* p, float (&f)[8]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+__device__ __forceinline__ void st8v(__nv_bfloat16* p, const float (&f)[8]) { *reinterpret_cast<uint4*>(p) = pack8(f); }
+__device__ __forceinline__ void st8v(float* p, const float (&f)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(f[0], f[1], f[2], f[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(f[4], f[5], f[6], f[7]);
+}
+// FP32 channels-last LRN (the TF32 path's activations): the same neighbour-vector form
+__device__ __forceinline__ void load24(const float* p, int c0, int C, float (&v)[24]) {
+    float a[8], b[8], c[8];
+    ld8v(p + c0, b);
+    if (c0 >= 8) ld8v(p + c0 - 8, a);
+    else {
+#pragma unroll
+        for (int e = 0; e < 8; e++) a[e] = 0.f;
+    }
+    if (c0 + 8 < C) ld8v(p + c0 + 8, c);
+    else {
+#pragma unroll
+        for (int e = 0; e < 8; e++) c[e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; e++) { v[e] = a[e]; v[8 + e] = b[e]; v[16 + e] = c[e]; }
+}
+
 // channels-last BF16 LRN: a thread owns 8 channels of one pixel and keeps the neighbouring 8-channel
 // vectors (c0-8 .. c0+15) in registers; channels outside [0, C) contribute 0 (clipped window).
 __device__ __forceinline__ void load24(const __nv_bfloat16* p, int c0, int C, float (&v)[24]) {
@@ -1113,8 +1209,8 @@ __device__ __forceinline__ void lrn_fwd8(const float (&xv)[24], float an, float 
     }
 }
 
-template <int R>
-__global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+template <int R, typename T>
+__global__ void lrn_fwd_nhwc8(const T* __restrict__ x, T* __restrict__ y,
                               float* __restrict__ scale, int C, int size, float alpha, float beta, float k, int total) {
     const int cv = C / 8;
     const float an = alpha / size;
@@ -1125,7 +1221,7 @@ __global__ void lrn_fwd_nhwc8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
         load24(x + base, c0, C, xv);
         float out[8], S[8];
         lrn_fwd8<R>(xv, an, beta, k, out, S);
-        *reinterpret_cast<uint4*>(y + base + c0) = pack8(out);
+        st8v(y + base + c0, out);
         if (scale) {
             float4* sp = reinterpret_cast<float4*>(scale + base + c0);
             sp[0] = make_float4(S[0], S[1], S[2], S[3]);
@@ -1166,9 +1262,9 @@ __device__ __forceinline__ void lrn_bwd8(const float (&xv)[24], const float (&gv
     }
 }
 
-template <int R>
-__global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
-                              __nv_bfloat16* __restrict__ dx, int C, int size, float alpha, float beta, float k,
+template <int R, typename T>
+__global__ void lrn_bwd_nhwc8(const T* __restrict__ x, const T* __restrict__ dy,
+                              T* __restrict__ dx, int C, int size, float alpha, float beta, float k,
                               int total) {
     const int cv = C / 8;
     const float an = alpha / size;
@@ -1181,7 +1277,36 @@ __global__ void lrn_bwd_nhwc8(const __nv_bfloat16* __restrict__ x, const __nv_bf
         load24(dy + base, c0, C, gv);
         float out[8];
         lrn_bwd8<R>(xv, gv, an, beta, k, cb, out);
-        *reinterpret_cast<uint4*>(dx + base + c0) = pack8(out);
+        st8v(dx + base + c0, out);
+    }
+}
+
+template <typename T>
+static void lrn_fwd_launch(const void* x, void* y, float* scale, int C, int size, float alpha, float beta, float k,
+                           int tv, unsigned nb, cudaStream_t s) {
+    auto X = (const T*)x;
+    auto Y = (T*)y;
+    switch ((size - 1) / 2) {
+        case 0: lrn_fwd_nhwc8<0, T><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+        case 1: lrn_fwd_nhwc8<1, T><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+        case 2: lrn_fwd_nhwc8<2, T><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+        case 3: lrn_fwd_nhwc8<3, T><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+        default: lrn_fwd_nhwc8<4, T><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
+    }
+}
+
+template <typename T>
+static void lrn_bwd_launch(const void* x, const void* dy, void* dx, int C, int size, float alpha, float beta, float k,
+                           int tv, unsigned nb, cudaStream_t s) {
+    auto X = (const T*)x;
+    auto G = (const T*)dy;
+    auto D = (T*)dx;
+    switch ((size - 1) / 2) {
+        case 0: lrn_bwd_nhwc8<0, T><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+        case 1: lrn_bwd_nhwc8<1, T><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+        case 2: lrn_bwd_nhwc8<2, T><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+        case 3: lrn_bwd_nhwc8<3, T><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
+        default: lrn_bwd_nhwc8<4, T><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
     }
 }
 
@@ -1189,18 +1314,11 @@ cudaError_t lrn_fwd(const void* x, void* y, float* scale, int bf16, int nhwc, in
                     float alpha, float beta, float k, cudaStream_t s) {
     const int total = N * C * H * W;
     const int sc = nhwc ? 1 : H * W;
-    if (bf16 && nhwc && nhwc8_ok(x, y, C) && ((reinterpret_cast<uintptr_t>(scale) & 15) == 0) && size <= 9) {
+    if (nhwc && nhwc8_ok(x, y, C) && ((reinterpret_cast<uintptr_t>(scale) & 15) == 0) && size <= 9) {
         const int tv = total / 8;
         const unsigned nb = nblk(tv, 256);
-        auto X = (const __nv_bfloat16*)x;
-        auto Y = (__nv_bfloat16*)y;
-        switch ((size - 1) / 2) {
-            case 0: lrn_fwd_nhwc8<0><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
-            case 1: lrn_fwd_nhwc8<1><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
-            case 2: lrn_fwd_nhwc8<2><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
-            case 3: lrn_fwd_nhwc8<3><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
-            default: lrn_fwd_nhwc8<4><<<nb, 256, 0, s>>>(X, Y, scale, C, size, alpha, beta, k, tv); break;
-        }
+        if (bf16) lrn_fwd_launch<__nv_bfloat16>(x, y, scale, C, size, alpha, beta, k, tv, nb, s);
+        else lrn_fwd_launch<float>(x, y, scale, C, size, alpha, beta, k, tv, nb, s);
         note_launch();
         return cudaGetLastError();
     }
@@ -1237,19 +1355,11 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
                     int N, int C, int H, int W, int size, float alpha, float beta, float k, cudaStream_t s) {
     const int total = N * C * H * W;
     const int sc = nhwc ? 1 : H * W;
-    if (bf16 && nhwc && nhwc8_ok(x, y, C) && nhwc8_ok(dy, dx, C) && size <= 9) {
+    if (nhwc && nhwc8_ok(x, y, C) && nhwc8_ok(dy, dx, C) && size <= 9) {
         const int tv = total / 8;
         const unsigned nb = nblk(tv, 256);
-        auto X = (const __nv_bfloat16*)x;
-        auto G = (const __nv_bfloat16*)dy;
-        auto D = (__nv_bfloat16*)dx;
-        switch ((size - 1) / 2) {
-            case 0: lrn_bwd_nhwc8<0><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
-            case 1: lrn_bwd_nhwc8<1><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
-            case 2: lrn_bwd_nhwc8<2><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
-            case 3: lrn_bwd_nhwc8<3><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
-            default: lrn_bwd_nhwc8<4><<<nb, 256, 0, s>>>(X, G, D, C, size, alpha, beta, k, tv); break;
-        }
+        if (bf16) lrn_bwd_launch<__nv_bfloat16>(x, dy, dx, C, size, alpha, beta, k, tv, nb, s);
+        else lrn_bwd_launch<float>(x, dy, dx, C, size, alpha, beta, k, tv, nb, s);
         note_launch();
         return cudaGetLastError();
     }

@@ -480,3 +480,32 @@ def test_fused_pool_lrn_rejects_other_geometry():
         cb.pool_lrn_forward(x, 2, 2, 0)              # 2x2 windows
     with pytest.raises(cb.CaffeError, match="E_DTYPE"):
         cb.pool_lrn_forward(x.float(), 3, 2, 0)
+
+
+@pytest.mark.parametrize("shape", [(2, 96, 27, 27), (2, 256, 13, 13), (1, 16, 55, 55)])
+def test_fp32_nhwc_vector_paths(oracle, shape):
+    """FP32 channels-last (the TF32 net's activations): the vector LRN kernels within the FP32 bar of
+    the oracle, and the 3x3/s2 max-pool backward (U8 mask, with and without the ReLU gate)
+    bit-exact (R8's FP32 gather order)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    cl = torch.channels_last
+    X = synth.uniform(shape, 31, synth.S_X) * 3
+    xt = cuda(X).contiguous(memory_format=cl)
+    L = cb.lrn_forward(xt)
+    assert_fp32_close(host(L), oracle.lrn_forward(X), "lrn fwd f32 nhwc")
+    G = synth.uniform(shape, 32, synth.S_DY)
+    dL = cb.lrn_backward(xt, L, cuda(G).contiguous(memory_format=cl))
+    assert_fp32_close(host(dL), oracle.lrn_backward(X, G), "lrn bwd f32 nhwc")
+    Xr = np.maximum(X, 0)
+    Xr[0, 0, :3, :3] = 1.0                           # ties
+    xr = cuda(Xr).contiguous(memory_format=cl)
+    P, M = cb.pool_forward(xr, "max", 3, 2, mask_dtype=torch.uint8)
+    rP, rM = oracle.maxpool_forward(Xr, (3, 3), (2, 2))
+    np.testing.assert_array_equal(host(P), rP)
+    dY = synth.uniform(rP.shape, 33, synth.S_DY)
+    dYt = cuda(dY).contiguous(memory_format=cl)
+    np.testing.assert_array_equal(host(cb.pool_backward(dYt, M, shape, "max", 3, 2)),
+                                  oracle.maxpool_backward(dY, rM, shape, (3, 3), (2, 2)))
+    np.testing.assert_array_equal(host(cb.pool_relu_backward(P, dYt, M, shape, 3, 2)),
+                                  oracle.relu_backward(Xr, oracle.maxpool_backward(dY, rM, shape, (3, 3), (2, 2))))
