@@ -309,6 +309,9 @@ class Net:
         P = self.layers[i - 1]
         return P.kind in ("conv", "ip") and P.relu
 
+    # launch each layer's data gradient (main stream, the critical path) before its weight gradient
+    # (side stream) so the persistent data-gradient GEMM claims the SMs first
+    dgrad_first = False
     # cap on the persistent grid of the weight-gradient GEMMs on their side stream (0 = every SM):
     # leaves SMs to the critical path (data gradients, pool/LRN backward) they run beside
     wgrad_max_ctas = 0
@@ -349,28 +352,42 @@ class Net:
                 cb.relu_backward(y, dy, inplace=True)  # sign of the ReLU output == sign test on its input
             if L.kind == "conv":
                 pre = i == 0 and self.ws0 is not None
-                if wgrad_stream is not None and i > 0:
+                side = wgrad_stream is not None and i > 0
+                if side:
                     ev = torch.cuda.Event()
                     ev.record(torch.cuda.current_stream())
-                    wgrad_stream.wait_event(ev)
-                    with torch.cuda.stream(wgrad_stream), self._side_grid():
+
+                def wgrad():
+                    if side:
+                        wgrad_stream.wait_event(ev)
+                        with torch.cuda.stream(wgrad_stream), self._side_grid():
+                            cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math,
+                                                    beta=0.0, dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
+                            self.wgrad_done[i] = torch.cuda.Event()
+                            self.wgrad_done[i].record(wgrad_stream)
+                    else:
                         cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math,
-                                                beta=0.0, dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
-                        self.wgrad_done[i] = torch.cuda.Event()
-                        self.wgrad_done[i].record(wgrad_stream)
+                                                beta=0.0, dw=self.dW[i], db=self.dB[i], ws=self.ws0 if pre else None,
+                                                prepacked=pre)
+                    if hook:
+                        hook(i)
+
+                def dgrad():
+                    wpre = i in self.wsd
+                    wsd = self.wsd.get(i)
+                    if i > 0 and self._relu_into_dgrad(i):
+                        cb.conv_backward_data_relu(dy, self._wop(i), a[i], L.stride, L.pad, L.group, self.math,
+                                                   out=d[i], ws=wsd, wprepacked=wpre)
+                    elif i > 0:
+                        cb.conv_backward_data(dy, self._wop(i), a[i].shape, L.stride, L.pad, L.group, self.math,
+                                              beta=0.0, out=d[i], ws=wsd, wprepacked=wpre)
+
+                if side and self.dgrad_first:   # the critical path's kernel claims the SMs first
+                    dgrad()
+                    wgrad()
                 else:
-                    cb.conv_backward_weight(a[i], dy, self.W[i].shape, L.stride, L.pad, L.group, self.math, beta=0.0,
-                                            dw=self.dW[i], db=self.dB[i], ws=self.ws0 if pre else None, prepacked=pre)
-                if hook:
-                    hook(i)
-                wpre = i in self.wsd
-                wsd = self.wsd.get(i)
-                if i > 0 and self._relu_into_dgrad(i):
-                    cb.conv_backward_data_relu(dy, self._wop(i), a[i], L.stride, L.pad, L.group, self.math, out=d[i],
-                                               ws=wsd, wprepacked=wpre)
-                elif i > 0:
-                    cb.conv_backward_data(dy, self._wop(i), a[i].shape, L.stride, L.pad, L.group, self.math,
-                                          beta=0.0, out=d[i], ws=wsd, wprepacked=wpre)
+                    wgrad()
+                    dgrad()
                 if done_hook:
                     done_hook(i)
             elif L.kind == "ip" and fused_sgd is not None and wgrad_stream is not None and self._sgd_fusable(i):
@@ -394,24 +411,37 @@ class Net:
                     done_hook(i)
             elif L.kind == "ip":
                 dy2 = dy.view(dy.shape[0], -1)
-                if wgrad_stream is not None:
+                side = wgrad_stream is not None
+                if side:
                     ev = torch.cuda.Event()
                     ev.record(torch.cuda.current_stream())
-                    wgrad_stream.wait_event(ev)
-                    with torch.cuda.stream(wgrad_stream), self._side_grid():
+
+                def wgrad():
+                    if side:
+                        wgrad_stream.wait_event(ev)
+                        with torch.cuda.stream(wgrad_stream), self._side_grid():
+                            cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
+                                                  dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
+                            self.wgrad_done[i] = torch.cuda.Event()
+                            self.wgrad_done[i].record(wgrad_stream)
+                    else:
                         cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
-                                              dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
-                        self.wgrad_done[i] = torch.cuda.Event()
-                        self.wgrad_done[i].record(wgrad_stream)
+                                              dw=self.dW[i], db=self.dB[i])
+                    if hook:
+                        hook(i)
+
+                def dgrad():
+                    if i > 0 and self._relu_into_dgrad(i):
+                        cb.ip_backward_data_relu(dy2, self._wop(i), a[i], self.math, out=d[i])
+                    elif i > 0:
+                        cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
+
+                if side and self.dgrad_first:
+                    dgrad()
+                    wgrad()
                 else:
-                    cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
-                                          dw=self.dW[i], db=self.dB[i])
-                if hook:
-                    hook(i)
-                if i > 0 and self._relu_into_dgrad(i):
-                    cb.ip_backward_data_relu(dy2, self._wop(i), a[i], self.math, out=d[i])
-                elif i > 0:
-                    cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
+                    wgrad()
+                    dgrad()
                 if done_hook:
                     done_hook(i)
             elif L.kind == "pool" and self._pool_lrn(i) and self.fuse_lrn_pool_backward:

@@ -43,6 +43,12 @@ def run(assign):
 
 if __name__ == "__main__":
     cfgs = sys.argv[1:] or ["wgrad_max_ctas=0"]
-    for rep in range(2):
+    reps = int(os.environ.get("REPS", "2"))
+    res = {c: [] for c in cfgs}
+    for rep in range(reps):
         for c in cfgs:
-            print(f"{c:40s} {run(c) * 1e3:8.1f} us/step", flush=True)
+            res[c].append(run(c) * 1e3)
+            print(f"{c:40s} {res[c][-1]:8.1f} us/step", flush=True)
+    for c in cfgs:
+        v = sorted(res[c])
+        print(f"median {c:33s} {v[len(v) // 2]:8.1f} us/step  (min {v[0]:.1f})", flush=True)
