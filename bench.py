@@ -580,6 +580,11 @@ def main():
     # step then moves its batch into the net's input blob with a device copy.
     e2e = None
     if not args.no_e2e:
+        # the same starting state as the device-timed leg (an idle GPU): the instrumented eager pass
+        # just before leaves it hot, and the part's power management slows back-to-back runs by up
+        # to ~10% (1.53 -> 1.65-1.68 ms/step over 100 replays, tools/h2d_probe.py)
+        torch.cuda.synchronize()
+        time.sleep(1.0)
         cl = torch.channels_last
         hX = torch.from_numpy(X).to(net.a[0].dtype).contiguous(memory_format=cl).pin_memory()
         hL = torch.from_numpy(lab).pin_memory()
