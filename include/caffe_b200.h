@@ -188,7 +188,8 @@ caffe_status caffe_device_check(void);
    staged window per 128-pixel tile serving every tap.  0 = off (per-tap im2col tiles), 1 (default)
    = where whole-row halo tiles do not apply and N tiles are <= 128 columns (CaffeNet conv5
    forward), 2 = wherever the geometry allows, 3 = as 2 with two accumulators per CTA for N tiles of
-   up to 256 columns (single-buffered TMEM). */
+   up to 256 columns (single-buffered TMEM), 4 = as 2 with wider N split into tiles of <= 128
+   columns (two double-buffered accumulators). */
 #define CAFFE_TUNE_HALO_STACKED 14
 /* CAFFE_TUNE_SGD_THREADS: threads per block of caffe_sgd_update (0 = default 256; 64, 128): with
    CAFFE_TUNE_SGD_BLOCKS_PER_SM it sets how much of an SM an update running beside the backward

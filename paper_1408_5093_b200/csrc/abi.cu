@@ -456,6 +456,16 @@ static bool stacked_applies(int E, const HaloGeom& h, int BN) {
     if (g_halo_stacked >= 2) return true;
     return !halo_applies(E, h) && BN <= 128;
 }
+// N tile of a halo/stacked pass: CAFFE_TUNE_HALO_STACKED 4 splits the columns of stacked-geometry
+// passes into tiles of <= 128 (two accumulators per CTA, double-buffered: conv3 384 -> 3 x 128,
+// conv4/conv5 data gradient 192 -> 2 x 96)
+static int halo_bn(int n, const HaloGeom& h) {
+    if (g_halo_stacked == 4 && stacked_geom(h) && !halo_applies(2, h) && n > 128) {
+        const int t = (int)cdiv(n, 128);
+        return (int)rup(cdiv(n, t), 16);
+    }
+    return choose_bn(n);
+}
 // Fills the halo fields of L (A map over the channels-last operand `aptr` [N][Hi][Wi][Ctot]) after
 // the caller has set BN, N, n_tiles, groups, b_row_g, a_cpg, a_cblocks and the epilogue.
 int g_halo_ktrim = 1;   // CAFFE_TUNE_HALO_KTRIM
@@ -691,8 +701,9 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO_STACKED) {
-        if (value < 0 || value > 3)
-            return fail(CAFFE_E_PARAM, "stacked halo mode must be 0 (off), 1 (auto), 2 (force), 3 (force, 2 accumulators to 256 columns)");
+        if (value < 0 || value > 4)
+            return fail(CAFFE_E_PARAM, "stacked halo mode must be 0 (off), 1 (auto), 2 (force), 3 (force, 2 accumulators "
+                                       "to 256 columns), 4 (force, N tiles split to <= 128 columns)");
         g_halo_stacked = value;
         return CAFFE_OK;
     }
@@ -878,9 +889,9 @@ caffe_status caffe_conv_forward(const caffe_conv_desc* desc, const caffe_blob* b
     TcLaunch L;
     memset(&L, 0, sizeof L);
     const HaloGeom hg{A.H, A.W, p.OH, p.OW, p.khp, p.kwp, p.php, p.pwp};
-    if (halo_applies(p.E, hg) || stacked_applies(p.E, hg, choose_bn(p.Og))) {
+    if (halo_applies(p.E, hg) || stacked_applies(p.E, hg, halo_bn(p.Og, hg))) {
         TcArgs& a = L.args;
-        a.BN = choose_bn(p.Og); a.N = p.Og;
+        a.BN = halo_bn(p.Og, hg); a.N = p.Og;
         a.n_tiles = (int)cdiv(p.Og, a.BN); a.groups = p.G;
         a.a_cblocks = p.Cgp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Og;
         set_out(a, top);
@@ -989,9 +1000,9 @@ static caffe_status conv_bwd_data(const caffe_conv_desc* desc, const caffe_blob*
     TcLaunch L;
     memset(&L, 0, sizeof L);
     const HaloGeom hg{p.OH, p.OW, Hd, Wd, p.khp, p.kwp, lo_h, lo_w};
-    if (!p.s2d && (halo_applies(p.E, hg) || stacked_applies(p.E, hg, choose_bn(p.Cge)))) {
+    if (!p.s2d && (halo_applies(p.E, hg) || stacked_applies(p.E, hg, halo_bn(p.Cge, hg)))) {
         TcArgs& a = L.args;
-        a.BN = choose_bn(p.Cge); a.N = p.Cge;
+        a.BN = halo_bn(p.Cge, hg); a.N = p.Cge;
         a.n_tiles = (int)cdiv(p.Cge, a.BN); a.groups = p.G;
         a.a_cblocks = p.Ogp / p.CH; a.a_cpg = A.cpg; a.b_row_g = p.Cge;
         set_out(a, bottom_diff);

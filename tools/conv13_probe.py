@@ -15,7 +15,7 @@ from paper_1408_5093_b200 import _abi  # noqa: E402
 from gemm_probe import timeit  # noqa: E402
 
 LAYERS = [("conv3", 256, 384, 1, 76.55), ("conv4", 384, 384, 2, 57.42), ("conv5", 384, 256, 2, 38.28)]
-MODES = [("im2col", 0), ("stacked auto", 1), ("stacked force", 2), ("stacked 2acc", 3)]
+MODES = [("im2col", 0), ("stacked auto", 1), ("stacked force", 2), ("stacked 2acc", 3), ("stacked bn<=128", 4)]
 
 
 def main():
