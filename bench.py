@@ -420,6 +420,10 @@ def main():
         reference_arm(args)
         return
     if args.workload != "caffenet":
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            if int(os.environ.get("RANK", "0")) == 0:
+                print(json.dumps({"workload": args.workload, "unavailable": "C1-C3 are single-GPU configurations"}))
+            return
         small_workload(args)
         return
     import numpy as np
