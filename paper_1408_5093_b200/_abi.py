@@ -8,7 +8,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcaffe_b200.so")
+# CAFFE_B200_LIB: load another in-tree build of the same library (A/B experiments of compile options)
+LIB_PATH = os.environ.get("CAFFE_B200_LIB") or os.path.join(HERE, "libcaffe_b200.so")
 
 # enums (include/caffe_b200.h)
 CAFFE_OK, CAFFE_E_INVALID, CAFFE_E_SHAPE, CAFFE_E_PARAM, CAFFE_E_DTYPE = 0, 1, 2, 3, 4

@@ -1,6 +1,7 @@
 """Step time (graph replay, CaffeNet batch 256, one B200) under schedule variants of nets.Net:
     python tools/sched_sweep.py "wgrad_max_ctas=0" "wgrad_max_ctas=96" ...
-Each argument is a comma-separated list of Net attribute assignments."""
+Each argument is a comma-separated list of Net attribute assignments; "tuneK=V" entries set library
+tuning knob K (caffe_set_tuning) instead, and each such configuration runs in a fresh process."""
 import os
 import sys
 
@@ -12,11 +13,20 @@ from paper_1408_5093_b200 import nets  # noqa: E402
 
 
 def run(assign):
+    if "tune" in assign and os.environ.get("SCHED_SWEEP_CHILD") != "1":
+        import subprocess
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), assign], capture_output=True, text=True,
+                             env=dict(os.environ, SCHED_SWEEP_CHILD="1", REPS="1"), timeout=600).stdout
+        return float(out.strip().splitlines()[-1].split()[-4]) / 1e3
+    from paper_1408_5093_b200 import _abi
     dev = torch.device("cuda")
     net = nets.Net(nets.CAFFENET, 256, nets.CAFFENET_INPUT, dev, math="bf16", seed=0, input_i8=True)
     for kv in filter(None, assign.split(",")):
         k, v = kv.split("=")
-        setattr(net, k, type(getattr(net, k))(eval(v)))
+        if k.startswith("tune"):
+            _abi.call("caffe_set_tuning", int(k[4:]), int(eval(v)))
+        else:
+            setattr(net, k, type(getattr(net, k))(eval(v)))
     net.a[0].copy_(torch.from_numpy(synth.int_pixels((256, 3, 227, 227), 1000)).to(net.a[0].dtype))
     net.labels.copy_(torch.from_numpy(synth.labels(256, 1000, 1000)))
     for _ in range(3):

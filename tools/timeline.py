@@ -14,6 +14,14 @@ from paper_1408_5093_b200 import nets  # noqa: E402
 def main():
     B = 256
     net = nets.Net(nets.CAFFENET, B, nets.CAFFENET_INPUT, torch.device("cuda"), math="bf16", seed=0, input_i8=True)
+    from paper_1408_5093_b200 import _abi
+    for kv in filter(None, os.environ.get("CAFFE_TUNE", "").split(",")):   # library knobs "key=value,..."
+        k, v = kv.split("=")
+        _abi.call("caffe_set_tuning", int(k), int(v))
+    # NET_ATTRS="attr=value,...": Net attribute overrides (as tools/sched_sweep.py)
+    for kv in filter(None, os.environ.get("NET_ATTRS", "").split(",")):
+        k, v = kv.split("=")
+        setattr(net, k, type(getattr(net, k))(eval(v)))
     net.a[0].copy_(torch.from_numpy(synth.int_pixels((B,) + tuple(nets.CAFFENET_INPUT), 1000)).to(net.a[0].dtype))
     net.labels.copy_(torch.from_numpy(synth.labels(B, 1000, 1000)))
     for _ in range(3):
