@@ -216,6 +216,11 @@ caffe_status caffe_device_check(void);
    data gradient: 0 (default) = 5 where compiled (the 24-column-per-CTA data gradient of 5x5
    filters, CaffeNet conv2) and >= 4 stages fit, else 1; 1 = always one.  Identical results. */
 #define CAFFE_TUNE_HALO_BTAPS 20
+/* CAFFE_TUNE_HALO_EPI_GROUPS: epilogue warp groups of the halo-tiled forward with 96 output columns
+   and one 48-channel block (the space-to-depth first layer): 0 (default) = 3, 2 = two groups of 48
+   columns (384 threads), 3 = three groups of 32 (512 threads; conv1 forward 78.4 -> 71.8 us at batch
+   256), 4 = four groups of 24 (640 threads).  Identical results. */
+#define CAFFE_TUNE_HALO_EPI_GROUPS 21
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

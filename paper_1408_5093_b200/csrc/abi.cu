@@ -519,8 +519,12 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     // TMA tensor-store epilogue (specialised-epilogue launches): the unit's tiles are staged in
     // shared memory as boxes of cw channels x Wo pixels x halo_th rows and leave through mapC
     a.tma_store = 0;
+    // CAFFE_TUNE_HALO_EPI_GROUPS: the first layer's 96 output columns as three epilogue groups of 32
+    // (default 3: conv1 forward 78.4 -> 71.8 us; 4 groups 73.8 us)
+    a.epi_groups = (g_halo_epi_groups != 2 && a.BN == 96 && a.k_last == 3 && a.a_cblocks == 1)
+                       ? (g_halo_epi_groups == 0 ? 3 : g_halo_epi_groups) : 2;
     const int epc = halo_fast_epc(a, L.cg);
-    if (epc > 0 && cb::g_halo_tma_store && !a.stk) {
+    if (epc > 0 && cb::g_halo_tma_store && !a.stk && a.epi_groups == 2) {
         const int cwl = epc % 64 == 0 ? 6 : epc % 32 == 0 ? 5 : epc % 16 == 0 ? 4 : 0;
         const int cw = cwl ? 1 << cwl : epc;
         const int align = cwl ? 16 * cw : 128;   // the swizzle pattern repeats every 8 rows
@@ -591,6 +595,13 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     if (g_max_ctas > 0 && g_max_ctas / L.cg < slots)      // CAFFE_TUNE_MAX_CTAS: more units per CTA
         slots = g_max_ctas / L.cg > 0 ? g_max_ctas / L.cg : 1;
     L.grid = (L.args.units < slots ? L.args.units : slots) * L.cg;
+    static const bool dbg = getenv("CAFFE_DEBUG_TC") != nullptr;   // launch-plan trace (development aid)
+    if (dbg)
+        fprintf(stderr, "tc amode %d bmode %d epi %d cg %d units %d grid %d BN %d macc %d stages %d kblocks %d "
+                        "kb/split %d splits %d M %d N %d waves %.2f\n",
+                L.amode, L.bmode, L.epi, L.cg, L.args.units, L.grid, L.args.BN, L.args.macc, L.args.stages,
+                L.args.kblocks, L.args.kb_per_split, L.args.splits, L.args.M, L.args.N,
+                (double)L.args.units / (L.grid / L.cg));
     ProfRec rec{nullptr, nullptr, flops, kind};
     if (g_prof) {
         std::lock_guard<std::mutex> lk(g_pmu);
@@ -653,6 +664,11 @@ caffe_status caffe_profiler_read(int32_t kind, double* ms, double* flops, int64_
 }
 
 caffe_status caffe_set_tuning(int32_t key, int32_t value) {
+    if (key == CAFFE_TUNE_HALO_EPI_GROUPS) {
+        if (value != 0 && (value < 2 || value > 4)) return fail(CAFFE_E_PARAM, "halo epilogue groups must be 0 (auto), 2, 3 or 4");
+        g_halo_epi_groups = value;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_HALO_BTAPS) {
         if (value < 0 || value > 8) return fail(CAFFE_E_PARAM, "halo B taps per stage must be 0 (auto) .. 8");
         g_halo_btaps = value;

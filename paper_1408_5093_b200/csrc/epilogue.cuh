@@ -92,17 +92,24 @@ __device__ __forceinline__ void epi_store_bf16_rowseg_coal(uint32_t taddr, bool 
     __syncwarp();
     const unsigned ok = __ballot_sync(0xffffffffu, row_ok);
     const unsigned long long mine = reinterpret_cast<unsigned long long>(dst);
+    // every piece read back from the staging before the first global store: the stores then issue
+    // back to back instead of each waiting on its own shared-memory load
+    uint4 piece[NCH];
+    unsigned long long addr[NCH];
+    bool st_ok[NCH];
 #pragma unroll
     for (int it = 0; it < NCH; it++) {
         const int c = it * 32 + lane;
         const int p = c / NCH, k = c - p * NCH;
-        const unsigned long long pp = __shfl_sync(0xffffffffu, mine, p);
-        uint32_t a, b, cc, d;
+        addr[it] = __shfl_sync(0xffffffffu, mine, p) + 16ull * (unsigned long long)k;
+        st_ok[it] = (ok >> p) & 1u;
         asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(a), "=r"(b), "=r"(cc), "=r"(d)
+                     : "=r"(piece[it].x), "=r"(piece[it].y), "=r"(piece[it].z), "=r"(piece[it].w)
                      : "r"(wstage + (uint32_t)((p * STR + k) * 16)));
-        if ((ok >> p) & 1u) reinterpret_cast<uint4*>(pp)[k] = make_uint4(a, b, cc, d);
     }
+#pragma unroll
+    for (int it = 0; it < NCH; it++)
+        if (st_ok[it]) *reinterpret_cast<uint4*>(addr[it]) = piece[it];
 }
 
 // Same arithmetic as epi_store_bf16_rowseg, but the row's EPC columns (tile columns

@@ -71,6 +71,9 @@ struct TcArgs {
     // A_HALO_K specialised epilogue (EPC > 0, no TMA store): stores coalesced through a per-warp
     // shared-memory transpose (epi_store_bf16_rowseg_coal)
     int epi_coal;
+    // A_HALO_K specialised epilogue: epilogue warp groups (2 = default; 3 = conv1's 96 columns as
+    // 3 x 32, 512 threads per CTA)
+    int epi_groups;
     // EPI_STRIDED data gradient through a ReLU (caffe_conv_backward_data_relu): the result of the
     // pass is kept where relu_top (same element strides as out) is > 0 and zeroed elsewhere,
     // before beta*old is added
@@ -111,6 +114,7 @@ size_t tc_halo_wgrad_smem_bytes(const TcArgs& a);
 size_t tc_halo_smem_bytes(const TcArgs& a);
 size_t halo_coal_bytes(const TcArgs& a);
 extern int g_halo_coal;   // CAFFE_TUNE_HALO_COALESCE
+extern int g_halo_epi_groups;   // CAFFE_TUNE_HALO_EPI_GROUPS
 int halo_fast_epc(const TcArgs& a, int cg);
 extern int g_halo_tma_store;   // CAFFE_TUNE_HALO_TMA_STORE
 int num_sms();

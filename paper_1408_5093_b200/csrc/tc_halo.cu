@@ -31,10 +31,13 @@ int g_halo_fast_epi = 1;   // CAFFE_TUNE_HALO_FAST_EPI
 int g_halo_coal = 1;       // CAFFE_TUNE_HALO_COALESCE
 int g_halo_tma_store = 0;   // CAFFE_TUNE_HALO_TMA_STORE (off: measured no gain for conv1, conv2 fwd 92 -> 106 us)
 
-// per-CTA staging of the coalesced specialised epilogue: 8 epilogue warps
+int g_halo_epi_groups = 0;   // CAFFE_TUNE_HALO_EPI_GROUPS (0 = automatic)
+
+// per-CTA staging of the coalesced specialised epilogue: 4 warps per epilogue group
 size_t halo_coal_bytes(const TcArgs& a) {
-    const int epc = a.BN / 2;
-    return (size_t)8 * 32 * ((epc / 8) | 1) * 16;
+    const int ng = a.epi_groups >= 3 ? a.epi_groups : 2;
+    const int epc = a.BN / ng;
+    return (size_t)4 * ng * 32 * ((epc / 8) | 1) * 16;
 }
 
 size_t tc_halo_smem_bytes(const TcArgs& a) {
@@ -46,10 +49,10 @@ size_t tc_halo_smem_bytes(const TcArgs& a) {
 
 // KS: 16-channel K steps issued per 64-channel block (4; 3 when the only block holds 48 real
 // channels -- conv1 after space-to-depth, conv2 per group -- so the zero padding is not multiplied)
-// EPC > 0: the specialised channels-last BF16 epilogue (epi_store_bf16_rowseg), each of the two
-// epilogue groups writing EPC = BN/2 columns
-template <int CG, int MACC, int KS, int EPC, int BT>
-__global__ void __launch_bounds__(384, 1)
+// EPC > 0: the specialised channels-last BF16 epilogue (epi_store_bf16_rowseg), each of the NEG
+// epilogue groups (4 warps each) writing EPC = BN/NEG columns
+template <int CG, int MACC, int KS, int EPC, int BT, int NEG = 2>
+__global__ void __launch_bounds__(128 + 128 * NEG, 1)
     tc_halo_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, const TcArgs args) {
     constexpr int CH = 64;                 // bf16 channels per 128-byte row
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch(&mapB);
         for (int i = 0; i < a_stages; i++) { mbar_init(&fullA[i], CG); mbar_init(&emptyA[i], 1); }
         for (int i = 0; i < b_stages; i++) { mbar_init(&fullB[i], CG); mbar_init(&emptyB[i], 1); }
-        for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 256 * CG); }
+        for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * NEG * CG); }
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -292,16 +295,17 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp >= 4) {
-        // ===================== epilogue (both CTAs): two groups of 4 warps =====================
-        // Group e (warps 4-7, 8-11) writes columns [e*half, ...) of the tiles; both groups read the
-        // same TMEM lanes (warp % 4 selects the lane quadrant).  Two warps per SM sub-partition hide
-        // the TMEM-load and store latency of the epilogue, which bounds the wide-output layers.
+        // ===================== epilogue (both CTAs): NEG groups of 4 warps =====================
+        // Group e (warps 4-7, 8-11, ...) writes columns [e*half, ...) of the tiles; every group reads
+        // the same TMEM lanes (warp % 4 selects the lane quadrant).  Several warps per SM
+        // sub-partition hide the TMEM-load and store latency of the epilogue, which bounds the
+        // wide-output layers (conv1 forward: three groups).
         const int q = warp & 3;
         const int eg = (warp - 4) >> 2;
         const int row = q * 32 + lane;
         const int yy = row / args.halo_wt, xx = row - yy * args.halo_wt;
         const int half = EPC > 0 ? EPC : ((args.BN / 2) + 15) & ~15;
-        const int cb_ = eg == 0 ? 0 : half, ce_ = eg == 0 ? half : args.BN;
+        const int cb_ = eg * half, ce_ = eg == NEG - 1 ? args.BN : cb_ + half;
         int acc = 0;
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(384, 1)
             const int g = t / tgroups;
             if (tstore) {   // the previous unit's tensor stores must have finished reading the staging
                 if (issuer) tma_store_wait_read0();
-                asm volatile("bar.sync 3, 256;" ::: "memory");
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + NEG), "r"(128 * NEG) : "memory");
             }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -326,8 +330,7 @@ __global__ void __launch_bounds__(384, 1)
             float* bs = sbias + acc * 256;
             if (args.bias) {
                 for (int c = cb_ + row; c < ce_; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
-                if (eg == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
-                else asm volatile("bar.sync 2, 128;" ::: "memory");
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");
             }
             for (int a = 0; a < macc; a++) {
                 const int tile = tg * tiles_per_unit + a * CG + (int)rank;
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(384, 1)
             if (++acc == nslots) { acc = 0; acc_phase ^= 1; }
             if (tstore) {   // staged tiles -> global: one 4-D tensor store per channel chunk
                 fence_proxy_async_smem();
-                asm volatile("bar.sync 3, 256;" ::: "memory");
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + NEG), "r"(128 * NEG) : "memory");
                 if (issuer) {
                     const int cw = args.st_cw > 0 ? (1 << args.st_cw) : EPC;
                     const int nch = args.BN / cw;
@@ -660,23 +663,26 @@ int halo_fast_epc(const TcArgs& a, int cg) {
     if (!(a.out_bf16 && a.s_c == 1 && a.beta == 0.f && a.N % a.BN == 0 && (a.BN / 2) % 8 == 0 && a.s_n % 8 == 0 &&
           a.s_p % 8 == 0 && a.col_g % 8 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0))
         return 0;
+    if (a.epi_groups >= 3)   // three / four epilogue groups: compiled for the 96-column first layer only
+        return (a.k_last == 3 && a.a_cblocks == 1 && a.BN == 96 && !a.tma_store) ? 96 / a.epi_groups : 0;
     const int epc = a.BN / 2;
     if (a.k_last == 3 && a.a_cblocks == 1) return (epc == 48 || epc == 64) ? epc : 0;
     return (epc == 24 || epc == 48 || epc == 64) ? epc : 0;
 }
 
-template <int CG, int MACC, int KS, int EPC = 0, int BT = 1>
+template <int CG, int MACC, int KS, int EPC = 0, int BT = 1, int NEG = 2>
 static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
-    auto kern = tc_halo_kernel<CG, MACC, KS, EPC, BT>;
+    auto kern = tc_halo_kernel<CG, MACC, KS, EPC, BT, NEG>;
+    constexpr int threads = 128 + 128 * NEG;
     const size_t smem = tc_halo_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (CG == 1) {
-        kern<<<L.grid, 384, smem, s>>>(L.mapA, L.mapB, L.mapC, L.args);
+        kern<<<L.grid, threads, smem, s>>>(L.mapA, L.mapB, L.mapC, L.args);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(L.grid);
-        cfg.blockDim = dim3(384);
+        cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -701,6 +707,8 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s) {
     const int epc = halo_fast_epc(a, L.cg);
     if (epc > 0) {
         if (a.k_last == 3 && a.a_cblocks == 1) {
+            if (epc == 32 && a.epi_groups == 3) return halo_launch_one<2, 2, 3, 32, 1, 3>(L, s);
+            if (epc == 24 && a.epi_groups == 4) return halo_launch_one<2, 2, 3, 24, 1, 4>(L, s);
             if (epc == 48) return halo_launch_one<2, 2, 3, 48>(L, s);
             if (epc == 64) return halo_launch_one<2, 2, 3, 64>(L, s);
         } else {

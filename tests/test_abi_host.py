@@ -208,3 +208,19 @@ def test_catalogue_and_solver_validation(lib):
     m8 = A.Blob(f(0x300000), A.Shape4(2, 16, 6, 6), A.CAFFE_U8, A.CAFFE_NHWC)
     assert lib.caffe_pool_lrn_forward(ctypes.byref(p), ctypes.byref(l4), ctypes.byref(xb), ctypes.byref(pb),
                                       ctypes.byref(m8), ctypes.byref(yb), None) == A.CAFFE_E_PARAM
+
+
+def test_tuning_knob_ranges(lib):
+    """caffe_set_tuning validates every ranged knob on the host (no device needed) and accepts the
+    documented values; knobs are restored to their defaults."""
+    from paper_1408_5093_b200 import _abi as A
+    bad = [(A.CAFFE_TUNE_HALO_EPI_GROUPS, 1), (A.CAFFE_TUNE_HALO_EPI_GROUPS, 5), (A.CAFFE_TUNE_HALO_BTAPS, 9),
+           (A.CAFFE_TUNE_MAX_CTAS, -1), (A.CAFFE_TUNE_SGD_THREADS, 96), (A.CAFFE_TUNE_SGD_BLOCKS_PER_SM, 9),
+           (A.CAFFE_TUNE_CTA_PAIR, 3), (A.CAFFE_TUNE_FUSED_POOL_ROWS, 65)]
+    for key, value in bad:
+        assert lib.caffe_set_tuning(key, value) == A.CAFFE_E_PARAM, (key, value)
+    for key, value in [(A.CAFFE_TUNE_HALO_EPI_GROUPS, 2), (A.CAFFE_TUNE_HALO_EPI_GROUPS, 3),
+                       (A.CAFFE_TUNE_HALO_BTAPS, 5), (A.CAFFE_TUNE_MAX_CTAS, 16)]:
+        assert lib.caffe_set_tuning(key, value) == 0, (key, value)
+    for key in (A.CAFFE_TUNE_HALO_EPI_GROUPS, A.CAFFE_TUNE_HALO_BTAPS, A.CAFFE_TUNE_MAX_CTAS):
+        assert lib.caffe_set_tuning(key, 0) == 0
