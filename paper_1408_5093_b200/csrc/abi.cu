@@ -520,9 +520,12 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     // shared memory as boxes of cw channels x Wo pixels x halo_th rows and leave through mapC
     a.tma_store = 0;
     // CAFFE_TUNE_HALO_EPI_GROUPS: the first layer's 96 output columns as three epilogue groups of 32
-    // (default 3: conv1 forward 78.4 -> 71.8 us; 4 groups 73.8 us)
-    a.epi_groups = (g_halo_epi_groups != 2 && a.BN == 96 && a.k_last == 3 && a.a_cblocks == 1)
-                       ? (g_halo_epi_groups == 0 ? 3 : g_halo_epi_groups) : 2;
+    // (first layer, 96 columns: default 3 -- conv1 forward 78.4 -> 71.8 us, 4 groups 73.8 us; the
+    // 128-column passes of conv2 / conv5 forward measured slower with 4 groups of 32: 93.7 -> 94.9,
+    // 40.5 -> 42.4 us -- their MMAs, not the epilogue, bound them)
+    a.epi_groups = 2;
+    if (a.BN == 96 && a.k_last == 3 && a.a_cblocks == 1)
+        a.epi_groups = g_halo_epi_groups == 0 ? 3 : g_halo_epi_groups;
     const int epc = halo_fast_epc(a, L.cg);
     if (epc > 0 && cb::g_halo_tma_store && !a.stk && a.epi_groups == 2) {
         const int cwl = epc % 64 == 0 ? 6 : epc % 32 == 0 ? 5 : epc % 16 == 0 ? 4 : 0;
