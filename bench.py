@@ -597,16 +597,22 @@ def main():
         # next batch lands directly in the blob the next replay reads -- no device-side copy
         graphs = None
         if use_graph:
+            # each graph has its own input blob, labels and loss: the copy stream fills the other
+            # graph's inputs and reads this graph's loss while the compute stream only replays
             dstage = [net.a[0], torch.empty_like(net.a[0])]
+            dlab = [net.labels, torch.empty_like(net.labels)]
+            dloss = [net.loss, torch.empty_like(net.loss)]
             graphs = [net.graph]
-            a0 = net.a[0]
-            net.a[0] = dstage[1]
+            saved = (net.a[0], net.labels, net.loss)
+            net.a[0], net.labels, net.loss = dstage[1], dlab[1], dloss[1]
             graphs.append(net.capture(allreduce=ar))
-            net.a[0] = a0
+            net.a[0], net.labels, net.loss = saved
             net.graph = graphs[0]
             barrier()
         else:   # eager steps read net.a[0]: stage in two buffers and copy the batch in on the compute stream
             dstage = [torch.empty_like(net.a[0]) for _ in range(2)]
+            dlab = [torch.empty_like(net.labels) for _ in range(2)]
+            dloss = [net.loss, net.loss]
         copy_stream = torch.cuda.Stream()
         copied = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
@@ -619,23 +625,31 @@ def main():
             copy_stream.wait_stream(stream) if i < 2 else copy_stream.wait_event(consumed[k])
             with torch.cuda.stream(copy_stream):
                 dstage[k].copy_(hX, non_blocking=True)
+                dlab[k].copy_(hL, non_blocking=True)
                 copied[k].record(copy_stream)
 
         prefetch(0)
+        done = [torch.cuda.Event() for _ in range(2)]
         for i in range(args.steps):
-            if i + 1 < args.steps:
-                prefetch(i + 1)
             k = i % 2
             stream.wait_event(copied[k])
-            net.labels.copy_(hL, non_blocking=True)
             if graphs is not None:
                 graphs[k].replay()
                 consumed[k].record(stream)
             else:
                 net.a[0].copy_(dstage[k], non_blocking=True)
+                net.labels.copy_(dlab[k], non_blocking=True)
                 consumed[k].record(stream)
                 run_step()
-            hloss.copy_(net.loss, non_blocking=True)
+            done[k].record(stream)
+            if i + 1 < args.steps:   # the next batch into the other buffers, beside this step
+                prefetch(i + 1)
+            # this step's loss to the host on the copy stream once the step is done (the compute
+            # stream never waits on a device->host copy)
+            copy_stream.wait_event(done[k])
+            with torch.cuda.stream(copy_stream):
+                hloss.copy_(dloss[k], non_blocking=True)
+        stream.wait_stream(copy_stream)
         e1.record(stream)
         barrier()
         ems = e0.elapsed_time(e1)

@@ -589,6 +589,22 @@ cudaError_t repack_w_dgrad(const void* w, int w_bf16, void* dst, int dst_esz, co
     return cudaGetLastError();
 }
 
+// sum_{sp = s0 .. s1-1} pp[sp * stride], added in ascending order (the fixed split order every
+// reduction of this file uses); eight loads in flight before the eight adds
+__device__ __forceinline__ float sum_splits_asc(const float* __restrict__ pp, long long stride, int s0, int s1) {
+    float acc = 0.f;
+    int sp = s0;
+    for (; sp + 8 <= s1; sp += 8) {
+        float a[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) a[k] = pp[(long long)(sp + k) * stride];
+#pragma unroll
+        for (int k = 0; k < 8; k++) acc += a[k];
+    }
+    for (; sp < s1; sp++) acc += pp[(long long)sp * stride];
+    return acc;
+}
+
 // ---------------------------------------------------------------- wgrad split reduction
 // Thread = one partial row/column (g, o, chunk q, row-in-chunk rr), rr fastest so the partial
 // reads are coalesced.  Sums the splits in ascending order (deterministic), then maps the
@@ -629,14 +645,7 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ partial, float* __
         // fixed ascending-split order; loads batched 4 at a time so they are in flight together
         const long long sstride = (long long)g.G * m_tiles * n_tiles * BN * 128;
         const float* pp = partial + ((((long long)grp * m_tiles + m_tile) * n_tiles + n_tile) * BN + col) * 128 + row;
-        float acc = 0.f;
-        int sp = 0;
-        for (; sp + 4 <= splits; sp += 4) {
-            const float a0 = pp[sp * sstride], a1 = pp[(sp + 1) * sstride], a2 = pp[(sp + 2) * sstride],
-                        a3 = pp[(sp + 3) * sstride];
-            acc += a0; acc += a1; acc += a2; acc += a3;
-        }
-        for (; sp < splits; sp++) acc += pp[sp * sstride];
+        const float acc = sum_splits_asc(pp, sstride, 0, splits);
         float* p = dW + (((long long)(grp * g.Og + o) * g.Cg + c) * g.kh + i) * g.kw + j;
         *p = (beta != 0.f ? beta * *p : 0.f) + acc;
     }
@@ -692,16 +701,7 @@ __global__ void wgrad_reduce_sg_kernel(const float* __restrict__ partial, float*
             pp = partial + ((((long long)grp * m_tiles + (pairs - 1)) * n_tiles + n_tile) * BN + col) * 128 + 64;
             dst = db + u;
         }
-        float acc = 0.f;
-        if (pp) {
-            int sp = sp0;
-            for (; sp + 4 <= sp1; sp += 4) {
-                const float a0 = pp[sp * sstride], a1 = pp[(sp + 1) * sstride], a2 = pp[(sp + 2) * sstride],
-                            a3 = pp[(sp + 3) * sstride];
-                acc += a0; acc += a1; acc += a2; acc += a3;
-            }
-            for (; sp < sp1; sp++) acc += pp[sp * sstride];
-        }
+        const float acc = pp ? sum_splits_asc(pp, sstride, sp0, sp1) : 0.f;
         part[threadIdx.y][threadIdx.x] = acc;
         __syncthreads();
         if (threadIdx.y == 0 && dst) {

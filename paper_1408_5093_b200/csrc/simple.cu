@@ -1189,11 +1189,6 @@ __device__ __forceinline__ float ex2_ftz(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ float rcp_ftz(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
 
 // the 8 outputs of channels c0..c0+7 from the 24 channels c0-8..c0+15 (zero outside [0, C))
 template <int R>
@@ -1230,15 +1225,18 @@ __global__ void lrn_fwd_nhwc8(const T* __restrict__ x, T* __restrict__ y,
     }
 }
 
-// Backward: the window sums over the 8 + 2R channel scales and the 8 outputs slide (one add and one
-// subtract per step instead of 2R + 1 terms); FP32 throughout, BF16 output.  The cross-channel term
-// uses y/S = x * S^(-beta) / S recomputed in FP32 from the bottom (the stored top is BF16-rounded:
-// reading it made the result lose up to 2^-9 of that term where it cancels the direct term, and cost
-// a third of the kernel's reads); `y` is not read.
+// Backward: the window sums over the 8 + 2R channel positions slide (one add and one subtract per
+// step); each position takes Q = S^(-beta-1) = 2^((-beta-1) lg2 S) and S^-beta = Q * S: two MUFU
+// operations (lg2, ex2) instead of three (no reciprocal; the kernel is issue-bound).  The
+// cross-channel term uses y/S = x * Q recomputed in FP32 from the bottom (the stored top is
+// BF16-rounded: reading it made the result lose up to 2^-9 of that term where it cancels the direct
+// term, and cost a third of the kernel's reads); `y` is not read.  The 8 outputs' window sums of
+// dy*y/S slide (one add and one subtract per step); FP32 throughout, BF16 or FP32 output.
 template <int R>
 __device__ __forceinline__ void lrn_bwd8(const float (&xv)[24], const float (&gv)[24], float an, float beta, float k,
                                          float cb, float (&out)[8]) {
     float P[24], tv[24];
+    const float nb1 = -beta - 1.f;
     float s2 = 0.f;
 #pragma unroll
     for (int j = 8 - 2 * R; j <= 8; j++) s2 = fmaf(xv[j], xv[j], s2);   // window of channel 8 - R
@@ -1249,8 +1247,9 @@ __device__ __forceinline__ void lrn_bwd8(const float (&xv)[24], const float (&gv
             s2 = fmaf(-xv[i - R - 1], xv[i - R - 1], s2);
         }
         const float S = k + an * s2;
-        P[i] = ex2_ftz(-beta * lg2_ftz(S));                  // S^-beta
-        tv[i] = gv[i] * (xv[i] * P[i]) * rcp_ftz(S);          // dy * y / S
+        const float Q = ex2_ftz(nb1 * lg2_ftz(S));           // S^(-beta-1)
+        P[i] = Q * S;                                          // S^-beta
+        tv[i] = gv[i] * (xv[i] * Q);                           // dy * y / S
     }
     float acc = 0.f;
 #pragma unroll
