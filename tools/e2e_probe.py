@@ -41,7 +41,10 @@ def main():
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
 
-    def run(h2d, small):
+    dX = torch.empty_like(net.a[0])
+    dX.copy_(hX)
+
+    def run(h2d, small, src=None):
         torch.cuda.synchronize()
         time.sleep(0.5)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -51,7 +54,7 @@ def main():
             k = i % 2
             cs.wait_stream(stream) if i < 2 else cs.wait_event(consumed[k])
             with torch.cuda.stream(cs):
-                dstage[k].copy_(hX, non_blocking=True)
+                dstage[k].copy_(hX if src is None else src, non_blocking=True)
                 copied[k].record(cs)
         if h2d:
             prefetch(0)
@@ -71,7 +74,8 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / K
 
-    cfgs = [("bench", (1, 1)), ("h2d_only", (1, 0)), ("small_only", (0, 1)), ("replay_only", (0, 0))]
+    cfgs = [("bench", (1, 1)), ("h2d_only", (1, 0)), ("d2d_only", (1, 0, dX)), ("small_only", (0, 1)),
+            ("replay_only", (0, 0))]
     res = {n: [] for n, _ in cfgs}
     for _ in range(4):
         for name, cfg in cfgs:
