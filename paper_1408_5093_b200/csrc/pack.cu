@@ -853,7 +853,19 @@ __global__ void gemm_partial_reduce8_kernel(const float* __restrict__ part, int 
         float acc[8];
 #pragma unroll
         for (int e = 0; e < 8; e++) acc[e] = 0.f;
-        for (int sp = 0; sp < splits; sp++) {   // ascending split order
+        int sp = 0;
+        for (; sp + 4 <= splits; sp += 4) {   // ascending split order; 32 loads in flight
+            float v[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int e = 0; e < 8; e++) v[q][e] = pp[(sp + q) * sstride + (long long)e * TM];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[e] += v[q][e];
+        }
+        for (; sp < splits; sp++) {
             float v[8];
 #pragma unroll
             for (int e = 0; e < 8; e++) v[e] = pp[sp * sstride + (long long)e * TM];
@@ -934,7 +946,19 @@ __global__ void gemm_partial_reduce_nhwc8_kernel(const float* __restrict__ part,
             const int n = (c0 + e) * pHW + hw, nt = n / BN, nc = n - nt * BN;
             pp[e] = part + (((long long)mt * n_tiles + nt) * BN + nc) * TM + mr;
         }
-        for (int sp = 0; sp < splits; sp++) {   // ascending split order
+        int sp = 0;
+        for (; sp + 4 <= splits; sp += 4) {   // ascending split order; 32 loads in flight
+            float v[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int e = 0; e < 8; e++) v[q][e] = pp[e][(sp + q) * sstride];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int e = 0; e < 8; e++) acc[e] += v[q][e];
+        }
+        for (; sp < splits; sp++) {
             float v[8];
 #pragma unroll
             for (int e = 0; e < 8; e++) v[e] = pp[e][sp * sstride];
