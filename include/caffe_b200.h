@@ -221,6 +221,11 @@ caffe_status caffe_device_check(void);
    columns (384 threads), 3 = three groups of 32 (512 threads; conv1 forward 78.4 -> 71.8 us at batch
    256), 4 = four groups of 24 (640 threads).  Identical results. */
 #define CAFFE_TUNE_HALO_EPI_GROUPS 21
+/* CAFFE_TUNE_HALO_JN: 1 (default) = stride-1 data gradients of compiled shapes (5x5 filters, 48
+   channels per group: CaffeNet conv2) run the kernel that puts the kw taps of a filter row in the
+   MMA's N (kw x 48 = 240 columns per MMA instead of 48) and sums the taps' shifted accumulator rows
+   in the epilogue; 0 = one MMA per tap.  Same result up to FP32 summation order. */
+#define CAFFE_TUNE_HALO_JN 22
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

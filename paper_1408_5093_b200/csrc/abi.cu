@@ -584,6 +584,37 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
     return true;
 }
 
+// Data gradient with a filter row's taps in the MMA's N (tc_halo_jn_kernel, A_HALO_JN): after
+// halo_setup, for whole-row halo tiles of compiled (kh, kw, channels per group) shapes with 64-channel
+// blocks of output channels, BF16 channels-last output, beta 0 and no ReLU gate (CaffeNet conv2).
+// CAFFE_TUNE_HALO_JN: 1 (default) where it applies, 0 = the per-tap halo kernel.
+int g_halo_jn = 1;
+static bool jn_setup(TcLaunch& L, const Plan& p, const caffe_blob* bottom_diff, const caffe_blob* relu_top, float beta,
+                     const void* WD) {
+    TcArgs& a = L.args;
+    if (!g_halo_jn || a.stk || relu_top || beta != 0.f || !isbf(bottom_diff) || !nhwc(bottom_diff) || p.s2d) return false;
+    if (!tc_halo_jn_compiled(p.khp, p.kwp, p.Cge) || p.Cge != p.Cg || p.Og % 64 != 0 || p.Ogp != p.Og) return false;
+    if (a.s_p % 8 || a.s_n % 8 || a.col_g % 8 || (reinterpret_cast<uintptr_t>(a.out) & 15)) return false;
+    if (num_sms() / 2 < p.G) return false;
+    TcArgs t = a;
+    t.a_stages = 2;
+    if (tc_halo_jn_smem_bytes(t, p.khp, p.kwp, p.Cge) > 232448) return false;
+    CUtensorMap mb;
+    // WD [G*Cge rows][taps][Ogp] as a 4-D tensor (o, tap, row, 1): one box = 64 o x kw taps x Cge/2 rows
+    if (!encode_tiled_4d(&mb, 2, WD, p.Ogp, p.taps, p.G * p.Cge, 1, 64, (uint32_t)p.kwp, (uint32_t)(p.Cge / 2)))
+        return false;
+    L.mapB = mb;
+    L.amode = A_HALO_JN;
+    L.cg = 2;
+    a.a_stages = 2;
+    a.macc = 1;
+    a.acc_stride = 256;
+    a.tmem_cols = 512;
+    a.units = a.groups * (int)cdiv(a.total_tiles, 2);
+    a.BN = p.kwp * p.Cge;
+    return true;
+}
+
 caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     if (L.cg < 1) L.cg = 1;
     if (L.epi == EPI_STRIDED && L.amode != A_HALO_MN) {
@@ -598,6 +629,13 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     if (g_max_ctas > 0 && g_max_ctas / L.cg < slots)      // CAFFE_TUNE_MAX_CTAS: more units per CTA
         slots = g_max_ctas / L.cg > 0 ? g_max_ctas / L.cg : 1;
     L.grid = (L.args.units < slots ? L.args.units : slots) * L.cg;
+    if (L.amode == A_HALO_JN) {   // each CTA pair serves one group: a multiple of `groups` pairs
+        const int G = L.args.groups;
+        int pairs = L.grid / 2;
+        if (pairs < G) pairs = G;
+        pairs -= pairs % G;
+        L.grid = pairs * 2;
+    }
     static const bool dbg = getenv("CAFFE_DEBUG_TC") != nullptr;   // launch-plan trace (development aid)
     if (dbg)
         fprintf(stderr, "tc amode %d bmode %d epi %d cg %d units %d grid %d BN %d macc %d stages %d kblocks %d "
@@ -614,6 +652,7 @@ caffe_status run_tc(TcLaunch& L, cudaStream_t s, double flops, int kind) {
     }
     cudaError_t e = L.amode == A_HALO_K    ? tc_halo_launch(L, s)
                     : L.amode == A_HALO_MN ? tc_halo_wgrad_launch(L, s)
+                    : L.amode == A_HALO_JN ? tc_halo_jn_launch(L, s)
                                            : tc_launch(L, s);
     if (g_prof) {
         cudaEventRecord(rec.b, s);
@@ -670,6 +709,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     if (key == CAFFE_TUNE_HALO_EPI_GROUPS) {
         if (value != 0 && (value < 2 || value > 4)) return fail(CAFFE_E_PARAM, "halo epilogue groups must be 0 (auto), 2, 3 or 4");
         g_halo_epi_groups = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_HALO_JN) {
+        g_halo_jn = value ? 1 : 0;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO_BTAPS) {
@@ -1029,6 +1072,7 @@ static caffe_status conv_bwd_data(const caffe_conv_desc* desc, const caffe_blob*
         if (relu_top) { a.relu_top = relu_top->ptr; a.relu_top_bf16 = isbf(relu_top); }
         a.k_last = g_halo_ktrim ? (int)cdiv(p.Og - p.CH * (a.a_cblocks - 1), 16) : 0;
         if (!halo_setup(L, hg, aptr, A.Ctot, p.N)) return fail(CAFFE_E_CUDA, "halo tile setup failed (top_diff)");
+        if (jn_setup(L, p, bottom_diff, relu_top, beta, WD)) return run_tc(L, s, conv_flops(p), 0);
         if (!encode_tiled_2d(&L.mapB, p.E, WD, (uint64_t)p.taps * p.Ogp, (uint64_t)p.G * p.Cge,
                              (uint64_t)p.taps * p.Ogp * p.E, p.CH, a.BN / L.cg))
             return fail(CAFFE_E_CUDA, "cuTensorMapEncodeTiled failed (dgrad weights)");

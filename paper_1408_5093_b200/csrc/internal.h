@@ -11,7 +11,8 @@ namespace cb {
 // ------------------------------------------------------------------ tensor-core GEMM (tc_gemm.cu)
 // D[m, n] = sum_k A[m, k] * B[n, k], A/B staged by TMA in 128-byte-swizzled shared memory,
 // tcgen05.mma (M=128, N=BN, K=16 bf16 / 8 tf32) accumulating FP32 in TMEM.
-enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3, A_HALO_K = 4, A_HALO_MN = 5 };
+enum AMode { A_TILED_K = 0, A_IM2COL_K = 1, A_IM2COL_MN = 2, A_TILED_MN = 3, A_HALO_K = 4, A_HALO_MN = 5,
+             A_HALO_JN = 6 /* data gradient, a filter row's taps in N (tc_halo_jn_kernel) */ };
 enum BMode { B_TILED_K = 0, B_TILED_MN = 1 };
 enum EpiMode { EPI_STRIDED = 0, EPI_PARTIAL = 1, EPI_SGD = 2 /* fused inner-product update (its own instance) */ };
 
@@ -112,6 +113,10 @@ cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s);
 cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s);
 size_t tc_halo_wgrad_smem_bytes(const TcArgs& a);
 size_t tc_halo_smem_bytes(const TcArgs& a);
+// A_HALO_JN (tc_halo.cu): compiled (kh, kw, channels per group) instances and their shared memory
+bool tc_halo_jn_compiled(int kh, int kw, int cpg);
+size_t tc_halo_jn_smem_bytes(const TcArgs& a, int kh, int kw, int cpg);
+cudaError_t tc_halo_jn_launch(const TcLaunch& L, cudaStream_t s);
 size_t halo_coal_bytes(const TcArgs& a);
 extern int g_halo_coal;   // CAFFE_TUNE_HALO_COALESCE
 extern int g_halo_epi_groups;   // CAFFE_TUNE_HALO_EPI_GROUPS

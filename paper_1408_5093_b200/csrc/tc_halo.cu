@@ -406,6 +406,242 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
     }
 }
 
+// ------------------------------------------------------------------ data gradient, column taps in N
+// The halo kernel above issues one MMA per filter tap with N = the group's channels: CaffeNet
+// conv2's data gradient has 48 per group, 24 per CTA of a pair, so each MMA reads a 4 KB A tile
+// for ~24 cycles of tensor work and the pass is bound by shared-memory operand reads (~49% tensor
+// pipe).  Here the KW taps of one filter row share an MMA:
+//   P[m][(c, j)] = sum_i sum_o A[m + i*wt][o] * Wf[o][c][i][j]   (N = CPG*KW; A shifted by i*wt rows)
+//   dX[m][c]     = sum_{j=0..KW-1} P[m + j][(c, j)]               (epilogue)
+// (A = dY padded by k-1-p, Wf the flipped filter, S:154 / P:156).  The MMAs are KW times wider and
+// the A tile is read KH instead of KH*KW times per 64-channel block.  Accumulator row m + j is TMEM
+// lane m + j: the epilogue takes it from lane + j of its warp by a shuffle and, for the last KW-1
+// lanes, from the next warp's first lanes through shared memory.  A valid output (x < OW) only
+// reads rows of its own padded output row (x + j < wt), so a tile never needs another tile's rows.
+// B = the CPG/2 channels x KW taps of this CTA's half, per (filter row i, 64-channel block), stays
+// resident in shared memory; each CTA pair serves one group (pair index mod groups).  Row order of
+// a B tile (and so the accumulator column of (c, j)) is c*KW + j: the tile is one 4-D TMA box
+// (64 o, KW taps, CPG/2 channels) of the flipped, transposed filter WD[G*Cge][taps][Ogp].
+__device__ __forceinline__ uint4 jn_pack8(const float (&f)[8]) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; e++) h[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+    return u;
+}
+
+template <int KH, int KW, int CPG>
+__global__ void __launch_bounds__(384, 1)
+    tc_halo_jn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                      const TcArgs args) {
+    constexpr int CH = 64;
+    constexpr int NCOL = KW * CPG;              // MMA N over the pair
+    constexpr int B_TILE = NCOL / 2 * 128;      // this CTA's rows of one (i, channel block) tile
+    constexpr int CE = CPG / 2;                 // channels per epilogue group
+    constexpr int NSUB = CE / 8;                // 8-channel sub-chunks per group
+    constexpr int XW = (KW - 1) * 8 * (KW - 1); // floats a warp publishes per sub-chunk
+    static_assert(NCOL <= 256 && NCOL % 16 == 0 && (NCOL / 2) % 8 == 0 && CE % 8 == 0, "tile shape");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + HALO_SMEM_ALIGN - 1) &
+                                               ~uintptr_t(HALO_SMEM_ALIGN - 1));
+    const int cblocks = args.a_cblocks;
+    const int a_stages = args.a_stages;
+    const int slot = args.halo_slot;
+    uint8_t* b_res = smem;                                   // KH * cblocks tiles
+    uint8_t* a_ring = b_res + KH * cblocks * B_TILE;
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(a_ring + a_stages * slot);
+    uint64_t* emptyA = fullA + 4;
+    uint64_t* fullB = emptyA + 4;
+    uint64_t* tfull = fullB + 1;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* xbuf = reinterpret_cast<float*>(fullA + 16);      // [2][8 warps][XW]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+    const int G = args.groups;
+    const int g = cid % G, npg = ncl / G;                   // host: ncl is a multiple of G
+    const int tgroups = (args.total_tiles + 1) / 2;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&mapA);
+        tma_prefetch(&mapB);
+        for (int i = 0; i < a_stages; i++) { mbar_init(&fullA[i], 2); mbar_init(&emptyA[i], 1); }
+        mbar_init(fullB, 2);
+        for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * 2 * 2); }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_cg2(tmem_holder, 512);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0 && lane == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (leader) mbar_arrive_expect_tx(fullB, (uint32_t)B_TILE * 2u * (uint32_t)(KH * cblocks));
+        else mbar_arrive_cluster(mapa_shared(smem_u32(fullB), 0));
+        for (int i = 0; i < KH; i++)
+            for (int cb = 0; cb < cblocks; cb++)
+                tma_load_4d_cg2(b_res + (i * cblocks + cb) * B_TILE, &mapB, fullB, cb * CH, i * KW,
+                                g * args.b_row_g + (int)rank * CE, 0);
+        const uint32_t txA = (uint32_t)(args.halo_rows * args.halo_wt * 128);
+        int sa = 0;
+        uint32_t pa = 0;
+        for (int tg = cid / G; tg < tgroups; tg += npg) {
+            int tile = tg * 2 + (int)rank;
+            if (tile >= args.total_tiles) tile = args.total_tiles - 1;   // rows discarded
+            const int n = tile / args.tiles_per_img;
+            const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;
+            for (int cb = 0; cb < cblocks; cb++) {
+                mbar_wait(&emptyA[sa], pa ^ 1);
+                if (leader) mbar_arrive_expect_tx(&fullA[sa], txA * 2u);
+                else mbar_arrive_cluster(mapa_shared(smem_u32(&fullA[sa]), 0));
+                tma_load_4d_cg2(a_ring + sa * slot, &mapA, &fullA[sa], g * args.a_cpg + cb * CH, -args.a_pad_w,
+                                y0 - args.a_pad_h, n);
+                if (++sa == a_stages) { sa = 0; pa ^= 1; }
+            }
+        }
+    } else if (warp == 1 && leader) {
+        // ===================== MMA issuer (leader CTA, whole warp) =====================
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);
+        const uint32_t a_base = smem_u32(a_ring), b_base = smem_u32(b_res);
+        const uint32_t rowsh = (uint32_t)args.halo_wt * 128u;
+        mbar_wait(fullB, 0);
+        tc_fence_after();
+        int sa = 0, acc = 0, iters = 0;
+        uint32_t pa = 0, acc_phase = 0;
+        for (int tg = cid / G; tg < tgroups; tg += npg, iters++) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem_base + (uint32_t)acc * 256u;
+            for (int cb = 0; cb < cblocks; cb++) {
+                mbar_wait(&fullA[sa], pa);
+                tc_fence_after();
+                const uint32_t sa_addr = a_base + (uint32_t)(sa * slot);
+                if (elect_one()) {
+#pragma unroll
+                    for (int i = 0; i < KH; i++) {
+                        const uint64_t ad = smem_desc_sw128(sa_addr + (uint32_t)i * rowsh, 16, 1024);
+                        const uint64_t bd = smem_desc_sw128(b_base + (uint32_t)((i * cblocks + cb) * B_TILE), 16, 1024);
+#pragma unroll
+                        for (int k = 0; k < 4; k++)
+                            umma_cg2<2>(d, ad + 2 * k, bd + 2 * k, idesc, (cb > 0 || i > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit_cg2(&emptyA[sa]);
+                }
+                __syncwarp();
+                if (++sa == a_stages) { sa = 0; pa ^= 1; }
+            }
+            if (elect_one()) umma_commit_cg2(&tfull[acc]);
+            __syncwarp();
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        // the peer's epilogue arrives remotely on our tempty barriers: drain before teardown
+        for (int j = iters - 2; j < iters; j++)
+            if (j >= 0) mbar_wait(&tempty[j & 1], (uint32_t)((j >> 1) & 1));
+    } else if (warp >= 4) {
+        // ===================== epilogue (both CTAs): 2 groups x 4 warps =====================
+        const int q = warp & 3;
+        const int eg = (warp - 4) >> 2;
+        const int ws = warp - 4;
+        const int row = q * 32 + lane;
+        const int yy = row / args.halo_wt, xx = row - yy * args.halo_wt;
+        const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+        int acc = 0, xs = 0;
+        uint32_t acc_phase = 0;
+        for (int tg = cid / G; tg < tgroups; tg += npg) {
+            const int tile = tg * 2 + (int)rank;
+            const int n = tile / args.tiles_per_img;
+            const int y = (tile - n * args.tiles_per_img) * args.halo_th + yy;
+            const bool row_ok = tile < args.total_tiles && yy < args.halo_th && y < args.out_h && xx < args.out_w;
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + (long long)n * args.s_n +
+                                 (long long)(y * args.out_w + xx) * args.s_p + g * args.col_g + eg * CE;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)acc * 256u + (uint32_t)(eg * CE * KW);
+#pragma unroll 1
+            for (int s = 0; s < NSUB; s++) {
+                uint32_t v[8 * KW];
+                const uint32_t ta = taddr + (uint32_t)(s * 8 * KW);
+#pragma unroll
+                for (int c = 0; c + 16 <= 8 * KW; c += 16) tmem_ld16p(ta + c, v + c);
+                if constexpr ((8 * KW) % 16 == 8) tmem_ld8p(ta + 8 * KW - 8, v + 8 * KW - 8);
+                tmem_wait_ld();
+                // publish this warp's first KW-1 lanes for the warp below (rows 32q-KW+1 .. 32q-1 need them)
+                float* xw = xbuf + (xs * 8 + ws) * XW;
+                if (lane < KW - 1) {
+#pragma unroll
+                    for (int cc = 0; cc < 8; cc++)
+#pragma unroll
+                        for (int j = 1; j < KW; j++) xw[(lane * 8 + cc) * (KW - 1) + j - 1] = __uint_as_float(v[cc * KW + j]);
+                }
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");
+                const float* xn = xbuf + (xs * 8 + ws + 1) * XW;   // next warp of the group (q < 3)
+                float o[8];
+#pragma unroll
+                for (int cc = 0; cc < 8; cc++) {
+                    float sum = __uint_as_float(v[cc * KW]);
+#pragma unroll
+                    for (int j = 1; j < KW; j++) {
+                        float t = __shfl_down_sync(0xffffffffu, __uint_as_float(v[cc * KW + j]), j);
+                        if (lane + j >= 32) t = q < 3 ? xn[((lane + j - 32) * 8 + cc) * (KW - 1) + j - 1] : 0.f;
+                        sum += t;
+                    }
+                    o[cc] = sum;
+                }
+                if (row_ok) *reinterpret_cast<uint4*>(dst + s * 8) = jn_pack8(o);
+                xs ^= 1;
+            }
+            tc_fence_before();
+            mbar_arrive_cluster(tempty_leader + (uint32_t)acc * 8u);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_cg2(tmem_base, 512);
+    }
+}
+
+size_t tc_halo_jn_smem_bytes(const TcArgs& a, int kh, int kw, int cpg) {
+    const int xw = (kw - 1) * 8 * (kw - 1);
+    return (size_t)kh * a.a_cblocks * (kw * cpg / 2 * 128) + (size_t)a.a_stages * a.halo_slot + 128 /*barriers*/ +
+           2 * 8 * xw * 4 + HALO_SMEM_ALIGN;
+}
+
+bool tc_halo_jn_compiled(int kh, int kw, int cpg) { return kh == 5 && kw == 5 && cpg == 48; }
+
+cudaError_t tc_halo_jn_launch(const TcLaunch& L, cudaStream_t s) {
+    const TcArgs& a = L.args;
+    if (!tc_halo_jn_compiled(a.halo_kh, a.a_kw, a.N)) return cudaErrorInvalidValue;
+    auto kern = tc_halo_jn_kernel<5, 5, 48>;
+    const size_t smem = tc_halo_jn_smem_bytes(a, 5, 5, 48);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.grid);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.args);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ weight gradient (halo along K)
 // dW[(tap, c)][o] = sum_pixels X[pixel + shift(tap)][c] * dY[pixel][o]: the reduction index is the
 // pixel, so a K block is one output tile -- halo_th rows x halo_wt columns (columns >= OW are

@@ -411,6 +411,7 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
     outs = {}
     _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
     _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 2)
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_JN, 0)   # the per-tap kernel's epilogues
     try:
         # generic; specialised with per-row stores; with TMA stores; with warp-transposed coalesced
         # stores; three epilogue groups (the 96-column first layer) coalesced / per-row; four, coalesced
@@ -439,6 +440,7 @@ def test_halo_fast_epilogue_bit_identical(oracle, case):
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_EPI_GROUPS, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_JN, 1)
     for kk in outs[0]:
         for f in range(1, 7):
             np.testing.assert_array_equal(outs[0][kk], outs[f][kk], err_msg=f"{kk} mode {f}")
@@ -752,6 +754,7 @@ def test_halo_btaps_bit_identical(oracle, case):
     dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
     outs = {}
     _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_JN, 0)   # the per-tap kernel's B stages
     try:
         for cta in (1, 2):
             _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, cta)
@@ -767,8 +770,51 @@ def test_halo_btaps_bit_identical(oracle, case):
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_BTAPS, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_JN, 1)
     for (cta, bt), r in outs.items():
         for kk in r:
             np.testing.assert_array_equal(r[kk], outs[(cta, 1)][kk], err_msg=f"{kk} cta={cta} btaps={bt}")
     ry = oracle.conv_forward(host(Xd), oracle.quant_bf16(Wt), b, stride=s, pad=p, group=g, relu=True)
     assert_bf16_ulp(outs[(2, 5)]["y"], ry, "halo fwd btaps=5", atol=_atol(ry))
+
+
+# data gradients of the column-taps-in-N kernel (A_HALO_JN): 5x5 filters with 48 channels per group
+JN_CASES = [(2, 96, 27, 27, 256, (5, 5), (1, 1), (2, 2), 2),   # CaffeNet conv2: 240-column MMAs, 2 channel blocks
+            (3, 96, 27, 27, 128, (5, 5), (1, 1), (2, 2), 2),   # one channel block, odd tile count
+            (2, 48, 19, 27, 64, (5, 5), (1, 1), (2, 2), 1)]    # one group, ragged last tile (3 of 4 rows)
+JN_IDS = ["conv2", "Og64", "g1H19"]
+
+
+@pytest.mark.parametrize("max_ctas", [0, 4])
+@pytest.mark.parametrize("case", JN_CASES, ids=JN_IDS)
+def test_conv_dgrad_taps_in_n(oracle, case, max_ctas):
+    """Data gradient with a filter row's taps in the MMA's N (CAFFE_TUNE_HALO_JN, the default for these
+    shapes): BF16 channels-last result within 1 BF16 ulp of RNE(oracle) per element (R28) and rel-L2
+    <= 1e-3; with the grid capped at 4 CTAs (2 pairs, one per group) every pair runs many tiles, so
+    the accumulator double buffer, the A ring phases and the epilogue's cross-warp exchange buffers
+    carry across units.  The per-tap kernel (CAFFE_TUNE_HALO_JN=0) agrees to FP32 summation order."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 21)
+    cl = torch.channels_last
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    ref = oracle.conv_backward_data(host(dYd), oracle.quant_bf16(Wt), X.shape, stride=s, pad=p, group=g)
+    outs = {}
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_MAX_CTAS, max_ctas)
+    try:
+        for jn in (1, 0):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_JN, jn)
+            dX = torch.full((N, C, H, W), float("nan"), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl)
+            cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
+            outs[jn] = host(dX.float())
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_JN, 1)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_MAX_CTAS, 0)
+    for jn, got in outs.items():
+        assert np.isfinite(got).all(), f"jn={jn}: unwritten outputs"
+        assert_bf16_ulp(got, ref, f"dgrad jn={jn} max_ctas={max_ctas}", atol=_atol(ref))
+        assert_tc_close(got, oracle.quant_bf16(ref), f"dgrad jn={jn} max_ctas={max_ctas}")
+    # different FP32 summation order: the two kernels really ran (not bit-identical)
+    assert (outs[1] != outs[0]).any()
