@@ -439,7 +439,8 @@ __global__ void __launch_bounds__(384, 1)
     constexpr int B_TILE = NCOL / 2 * 128;      // this CTA's rows of one (i, channel block) tile
     constexpr int CE = CPG / 2;                 // channels per epilogue group
     constexpr int NSUB = CE / 8;                // 8-channel sub-chunks per group
-    constexpr int XW = (KW - 1) * 8 * (KW - 1); // floats a warp publishes per sub-chunk
+    constexpr int XROW = (KW - 1) * 32 + 16;    // bytes one publishing lane writes per sub-chunk (+ pad)
+    constexpr int XWB = (KW - 1) * XROW;        // bytes per warp per sub-chunk
     static_assert(NCOL <= 256 && NCOL % 16 == 0 && (NCOL / 2) % 8 == 0 && CE % 8 == 0, "tile shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + HALO_SMEM_ALIGN - 1) &
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* tfull = fullB + 1;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* xbuf = reinterpret_cast<float*>(fullA + 16);      // [2][8 warps][XW]
+    const uint32_t xbase = smem_u32(fullA + 16);             // [2][8 warps][XWB bytes] exchange rows
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -571,26 +572,44 @@ __global__ void __launch_bounds__(384, 1)
                 for (int c = 0; c + 16 <= 8 * KW; c += 16) tmem_ld16p(ta + c, v + c);
                 if constexpr ((8 * KW) % 16 == 8) tmem_ld8p(ta + 8 * KW - 8, v + 8 * KW - 8);
                 tmem_wait_ld();
-                // publish this warp's first KW-1 lanes for the warp below (rows 32q-KW+1 .. 32q-1 need them)
-                float* xw = xbuf + (xs * 8 + ws) * XW;
+                // publish this warp's first KW-1 lanes for the warp below (rows 32q-KW+1 .. 32q-1 need
+                // them): per lane XROW bytes = (j, 8 channels) float rows, 16-byte vector stores; the
+                // 16-byte pad per lane puts the lanes of one vector access in distinct banks
+                const uint32_t xw = xbase + (uint32_t)((xs * 8 + ws) * XWB);
                 if (lane < KW - 1) {
 #pragma unroll
-                    for (int cc = 0; cc < 8; cc++)
-#pragma unroll
-                        for (int j = 1; j < KW; j++) xw[(lane * 8 + cc) * (KW - 1) + j - 1] = __uint_as_float(v[cc * KW + j]);
+                    for (int j = 1; j < KW; j++) {
+                        const uint32_t a = xw + (uint32_t)(lane * XROW + (j - 1) * 32);
+                        sts_u4(a, v[0 * KW + j], v[1 * KW + j], v[2 * KW + j], v[3 * KW + j]);
+                        sts_u4(a + 16, v[4 * KW + j], v[5 * KW + j], v[6 * KW + j], v[7 * KW + j]);
+                    }
                 }
+                float sh[KW - 1][8];   // accumulator row lane + j of this warp
+#pragma unroll
+                for (int j = 1; j < KW; j++)
+#pragma unroll
+                    for (int cc = 0; cc < 8; cc++) sh[j - 1][cc] = __shfl_down_sync(0xffffffffu, __uint_as_float(v[cc * KW + j]), j);
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");
-                const float* xn = xbuf + (xs * 8 + ws + 1) * XW;   // next warp of the group (q < 3)
+                // rows past this warp's lanes come from the next warp of the group; in the last quadrant
+                // they would be rows >= 128, which no valid output reads (x + j < wt)
+                if (q < 3 && lane >= 32 - (KW - 1)) {
+                    const uint32_t xn = xw + (uint32_t)XWB;
+#pragma unroll
+                    for (int j = 1; j < KW; j++) {
+                        if (lane + j >= 32) {
+                            const uint32_t a = xn + (uint32_t)((lane + j - 32) * XROW + (j - 1) * 32);
+                            const float4 x0 = lds_f4(a), x1 = lds_f4(a + 16);
+                            sh[j - 1][0] = x0.x; sh[j - 1][1] = x0.y; sh[j - 1][2] = x0.z; sh[j - 1][3] = x0.w;
+                            sh[j - 1][4] = x1.x; sh[j - 1][5] = x1.y; sh[j - 1][6] = x1.z; sh[j - 1][7] = x1.w;
+                        }
+                    }
+                }
                 float o[8];
 #pragma unroll
                 for (int cc = 0; cc < 8; cc++) {
                     float sum = __uint_as_float(v[cc * KW]);
 #pragma unroll
-                    for (int j = 1; j < KW; j++) {
-                        float t = __shfl_down_sync(0xffffffffu, __uint_as_float(v[cc * KW + j]), j);
-                        if (lane + j >= 32) t = q < 3 ? xn[((lane + j - 32) * 8 + cc) * (KW - 1) + j - 1] : 0.f;
-                        sum += t;
-                    }
+                    for (int j = 1; j < KW; j++) sum += sh[j - 1][cc];
                     o[cc] = sum;
                 }
                 if (row_ok) *reinterpret_cast<uint4*>(dst + s * 8) = jn_pack8(o);
@@ -610,9 +629,9 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 size_t tc_halo_jn_smem_bytes(const TcArgs& a, int kh, int kw, int cpg) {
-    const int xw = (kw - 1) * 8 * (kw - 1);
+    const int xwb = (kw - 1) * ((kw - 1) * 32 + 16);
     return (size_t)kh * a.a_cblocks * (kw * cpg / 2 * 128) + (size_t)a.a_stages * a.halo_slot + 128 /*barriers*/ +
-           2 * 8 * xw * 4 + HALO_SMEM_ALIGN;
+           2 * 8 * xwb + HALO_SMEM_ALIGN;
 }
 
 bool tc_halo_jn_compiled(int kh, int kw, int cpg) { return kh == 5 && kw == 5 && cpg == 48; }
