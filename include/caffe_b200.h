@@ -226,6 +226,11 @@ caffe_status caffe_device_check(void);
    MMA's N (kw x 48 = 240 columns per MMA instead of 48) and sums the taps' shifted accumulator rows
    in the epilogue; 0 = one MMA per tap.  Same result up to FP32 summation order. */
 #define CAFFE_TUNE_HALO_JN 22
+/* CAFFE_TUNE_WGRAD_BN: output-channel (N) tile of the halo-tiled weight gradients: 0 (default) =
+   automatic (several channel blocks: <= 96 columns, five accumulators per unit), 1 = the widest of
+   192/128/96/64 dividing the outputs (faster alone, slower in the three-stream training step),
+   else a multiple of 16 up to 256.  Same result up to FP32 summation order. */
+#define CAFFE_TUNE_WGRAD_BN 23
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -337,6 +337,7 @@ struct WgHalo {
     int Wt, TH, rows, tpi, total, ksteps, cblocks;  // tile geometry (output tile = TH rows x Wt columns)
     int BN, n_tiles, nch, acc_stride, macc, pairs, mgroups, splits, kb_per, slot, bchunk, stages;
 };
+int g_wgrad_bn = 0;   // CAFFE_TUNE_WGRAD_BN: N tile of the halo weight gradient (0 = automatic)
 WgHalo wgrad_halo_plan(const Plan& p) {
     WgHalo h;
     memset(&h, 0, sizeof h);
@@ -364,10 +365,23 @@ WgHalo wgrad_halo_plan(const Plan& p) {
     h.total = p.N * h.tpi;
     h.cblocks = p.Cgp / 64;
     h.BN = choose_bn(p.Og);
-    if (h.cblocks > 1) {   // every tap of a channel block in one unit: 5 accumulators of <= 96 columns
+    // several channel blocks (the 13x13 layers): every tap of a channel block in one unit -- 5
+    // accumulators of <= 96 columns -- so the staged window serves all taps.  CAFFE_TUNE_WGRAD_BN 1
+    // takes the widest N tile of <= 192 columns instead (an MMA reads a 4 KB A tile per K step, so
+    // narrow N is shared-memory bound; wider tiles fit fewer taps per unit and restage the window):
+    // faster alone (tools/wgrad_probe.py, batch 256, us: conv3 92.4 -> 86.9, conv4 72.8 -> 66.7,
+    // conv5 59.6 -> 51.7) but slower in the three-stream step (tools/sched_sweep.py, same box:
+    // 1.51-1.54 -> 1.57-1.62 ms/step), so off by default
+    if (h.cblocks > 1 && g_wgrad_bn != 1) {
         if (p.Og % 96 == 0) h.BN = 96;
         else if (p.Og % 64 == 0) h.BN = 64;
+    } else if (h.cblocks > 1) {
+        if (p.Og % 192 == 0) h.BN = 192;
+        else if (p.Og % 128 == 0) h.BN = 128;
+        else if (p.Og % 96 == 0) h.BN = 96;
+        else if (p.Og % 64 == 0) h.BN = 64;
     }
+    if (g_wgrad_bn > 0 && g_wgrad_bn % 16 == 0 && g_wgrad_bn <= 256) h.BN = std::min(g_wgrad_bn, (int)rup(p.Og, 16));
     if (h.BN > 256) return h;
     h.n_tiles = (int)cdiv(p.Og, h.BN);
     h.nch = (int)cdiv(h.BN, 64);
@@ -709,6 +723,12 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     if (key == CAFFE_TUNE_HALO_EPI_GROUPS) {
         if (value != 0 && (value < 2 || value > 4)) return fail(CAFFE_E_PARAM, "halo epilogue groups must be 0 (auto), 2, 3 or 4");
         g_halo_epi_groups = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_WGRAD_BN) {
+        if (value < 0 || value > 256 || (value % 16 && value != 1))
+            return fail(CAFFE_E_PARAM, "weight-gradient N tile must be 0 (auto), 1 (widest <= 192) or a multiple of 16 <= 256");
+        g_wgrad_bn = value;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO_JN) {
