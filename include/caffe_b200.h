@@ -231,6 +231,11 @@ caffe_status caffe_device_check(void);
    192/128/96/64 dividing the outputs (faster alone, slower in the three-stream training step),
    else a multiple of 16 up to 256.  Same result up to FP32 summation order. */
 #define CAFFE_TUNE_WGRAD_BN 23
+/* CAFFE_TUNE_HALO_MERGE: 1 = halo-tiled forward / data-gradient CTAs with two accumulators take two
+   consecutive row blocks of one image and stage one shared input window for both, three stages deep
+   (where an image has an even number of tiles, e.g. the first layer); 0 (default) = one window per
+   tile (measured as fast).  Identical results. */
+#define CAFFE_TUNE_HALO_MERGE 24
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

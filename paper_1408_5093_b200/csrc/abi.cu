@@ -483,6 +483,8 @@ static int halo_bn(int n, const HaloGeom& h) {
 // Fills the halo fields of L (A map over the channels-last operand `aptr` [N][Hi][Wi][Ctot]) after
 // the caller has set BN, N, n_tiles, groups, b_row_g, a_cpg, a_cblocks and the epilogue.
 int g_halo_ktrim = 1;   // CAFFE_TUNE_HALO_KTRIM
+int g_halo_merge = 0;   // CAFFE_TUNE_HALO_MERGE (bit-identical; measured no faster: conv1 forward 110.8 vs
+                        // 110.7 us with its pack, tools/merge_probe.py; step 1.50-1.52 vs 1.52-1.53 ms)
 int g_halo_btaps = 0;   // CAFFE_TUNE_HALO_BTAPS
 static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Ctot, int N) {
     TcArgs& a = L.args;
@@ -528,8 +530,26 @@ static bool halo_setup(TcLaunch& L, const HaloGeom& h, const void* aptr, int Cto
         a.a_stages * 2 * a.halo_slot <= 140 * 1024)
         a.macc = 2;
     // (a deeper A ring for stacked tiles -- 3 or 4 stages -- measured no faster: 2 stages kept)
+    // CAFFE_TUNE_HALO_MERGE: with two accumulators per CTA on whole-row tiles, the CTA takes two
+    // consecutive row blocks of one image and stages ONE window of 2*halo_th + kh - 1 rows for both
+    // (conv1: 6 instead of 2 x 4 input rows per stage), three stages deep where they fit; off by
+    // default -- conv1's forward is bound by its output stores, not by the staging of its windows
+    a.a_merge = 0;
+    if (g_halo_merge && a.macc == 2 && !a.stk && a.tiles_per_img % 2 == 0) {
+        const int mrows = 2 * a.halo_th + h.kh - 1;
+        const int need = std::max(mrows * a.halo_wt, (h.kh - 1 + a.halo_th) * a.halo_wt + (h.kw - 1) + 128);
+        const int mslot = (int)rup((long long)need * 128, 1024);
+        const int st = 3LL * mslot <= 140 * 1024 ? 3 : 2;
+        if ((long long)st * mslot <= 140 * 1024 &&
+            encode_tiled_4d(&L.mapA, 2, aptr, Ctot, h.Wi, h.Hi, N, 64, (uint32_t)a.halo_wt, (uint32_t)mrows)) {
+            a.a_merge = 1;
+            a.halo_rows = mrows;
+            a.halo_slot = mslot;
+            a.a_stages = st;
+        }
+    }
     a.b_stage_bytes = a.BN / L.cg * 128;
-    long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * a.macc * a.halo_slot;
+    long long budget = 232448 - 512 - 2048 - 1024 - (long long)a.a_stages * (a.a_merge ? 1 : a.macc) * a.halo_slot;
     // TMA tensor-store epilogue (specialised-epilogue launches): the unit's tiles are staged in
     // shared memory as boxes of cw channels x Wo pixels x halo_th rows and leave through mapC
     a.tma_store = 0;
@@ -606,7 +626,7 @@ int g_halo_jn = 1;
 static bool jn_setup(TcLaunch& L, const Plan& p, const caffe_blob* bottom_diff, const caffe_blob* relu_top, float beta,
                      const void* WD) {
     TcArgs& a = L.args;
-    if (!g_halo_jn || a.stk || relu_top || beta != 0.f || !isbf(bottom_diff) || !nhwc(bottom_diff) || p.s2d) return false;
+    if (!g_halo_jn || a.stk || a.a_merge || relu_top || beta != 0.f || !isbf(bottom_diff) || !nhwc(bottom_diff) || p.s2d) return false;
     if (!tc_halo_jn_compiled(p.khp, p.kwp, p.Cge) || p.Cge != p.Cg || p.Og % 64 != 0 || p.Ogp != p.Og) return false;
     if (a.s_p % 8 || a.s_n % 8 || a.col_g % 8 || (reinterpret_cast<uintptr_t>(a.out) & 15)) return false;
     if (num_sms() / 2 < p.G) return false;
@@ -723,6 +743,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     if (key == CAFFE_TUNE_HALO_EPI_GROUPS) {
         if (value != 0 && (value < 2 || value > 4)) return fail(CAFFE_E_PARAM, "halo epilogue groups must be 0 (auto), 2, 3 or 4");
         g_halo_epi_groups = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_HALO_MERGE) {
+        g_halo_merge = value ? 1 : 0;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_WGRAD_BN) {

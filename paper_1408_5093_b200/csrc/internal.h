@@ -87,6 +87,10 @@ struct TcArgs {
     // regardless of image boundaries.  A tile's window is staged as stk_nb one-row TMA boxes placed
     // so that the tile's first pixel lands at shared-memory row stk_off in every CTA.
     int stk, stk_wt, stk_hs, stk_nimg, stk_nb, stk_off;
+    // A_HALO_K, macc > 1: the macc tiles of a CTA are consecutive row blocks of one image staged as
+    // ONE window of halo_rows = macc*halo_th + kh - 1 rows (accumulator a reads it shifted by
+    // a*halo_th*halo_wt rows); halo_slot is then the whole window's stage
+    int a_merge;
     // EPI_STRIDED + tma_store, inner-product weight gradient with the SGD update fused in
     // (caffe_ip_backward_weight_sgd): out = the FP32 master weights W (read and rewritten),
     // sgd_v = momentum (same layout), mapC / mapV / mapWb store W, v and the BF16 copy

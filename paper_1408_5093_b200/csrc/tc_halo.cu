@@ -42,7 +42,7 @@ size_t halo_coal_bytes(const TcArgs& a) {
 
 size_t tc_halo_smem_bytes(const TcArgs& a) {
     const int macc = a.macc > 1 ? a.macc : 1;
-    return (size_t)a.a_stages * macc * a.halo_slot + (size_t)a.stages * a.b_stage_bytes + 512 /*barriers*/ +
+    return (size_t)a.a_stages * (a.a_merge ? 1 : macc) * a.halo_slot + (size_t)a.stages * a.b_stage_bytes + 512 /*barriers*/ +
            2 * 256 * 4 /*bias*/ + HALO_SMEM_ALIGN + (a.rows_epi ? 4 * 32 * 17 * 16 : 0) +
            (a.tma_store ? (size_t)macc * a.st_tile_bytes + 1024 : 0) + (a.epi_coal ? halo_coal_bytes(a) + 1024 : 0);
 }
@@ -64,7 +64,11 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
     constexpr int macc = MACC;             // accumulators (tiles) per CTA per unit
     const int a_stages = args.a_stages, b_stages = args.stages;
     const int slot = args.halo_slot;
-    const int a_stage_bytes = macc * slot;
+    // a_merge: the MACC tiles of a CTA are consecutive row blocks of one image and share ONE staged
+    // window (accumulator a reads it shifted by a*halo_th*halo_wt rows)
+    const bool merge = args.a_merge != 0;
+    const int a_stage_bytes = merge ? slot : macc * slot;
+    const uint32_t acc_rows_b = (uint32_t)(args.halo_th * args.halo_wt * 128);
     uint8_t* a_ring = smem;
     uint8_t* b_ring = smem + a_stages * a_stage_bytes;
     uint64_t* fullA = reinterpret_cast<uint64_t*>(b_ring + b_stages * args.b_stage_bytes);
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
     if (warp == 0 && lane == 0) {
         // ===================== TMA producer (both CTAs) =====================
         const uint32_t txA = args.stk ? (uint32_t)(macc * args.stk_nb * args.stk_wt * 128)
-                                      : (uint32_t)(macc * args.halo_rows * args.halo_wt * 128);
+                                      : (uint32_t)((merge ? 1 : macc) * args.halo_rows * args.halo_wt * 128);
         const uint32_t txB = (uint32_t)args.b_stage_bytes;
         const int bn_cta = args.BN / CG;
         int sa = 0, sb = 0;
@@ -133,8 +137,8 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
                 mbar_wait(&emptyA[sa], pa ^ 1);
                 if (CG == 1 || leader) mbar_arrive_expect_tx(&fullA[sa], txA * CG);
                 else mbar_arrive_cluster(mapa_shared(smem_u32(&fullA[sa]), 0));
-                for (int a = 0; a < macc; a++) {
-                    int tile = tg * tiles_per_unit + a * CG + (int)rank;
+                for (int a = 0; a < (merge ? 1 : macc); a++) {
+                    int tile = tg * tiles_per_unit + (merge ? (int)rank * macc : a * CG + (int)rank);
                     if (tile >= args.total_tiles) tile = args.total_tiles - 1;   // rows discarded
                     uint8_t* dst = a_ring + sa * a_stage_bytes + a * slot;
                     const int c = g * args.a_cpg + cb * CH;
@@ -218,7 +222,8 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
                                 const uint64_t bd0 = bs0 + (uint64_t)((j * b_tile) >> 4);
 #pragma unroll
                                 for (int a = 0; a < MACC; a++) {
-                                    const uint64_t ad0 = smem_desc_sw128(sa_addr + a * slot + sh, 16, 1024);
+                                    const uint64_t ad0 =
+                                        smem_desc_sw128(sa_addr + (merge ? a * acc_rows_b : a * slot) + sh, 16, 1024);
                                     const uint32_t dt = d_tmem + a * args.acc_stride;
 #pragma unroll
                                     for (int k = 0; k < KSTEPS; k++) {
@@ -253,7 +258,8 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
                     if (elect_one()) {
 #pragma unroll
                         for (int a = 0; a < MACC; a++) {
-                            const uint64_t ad0 = smem_desc_sw128(sa_addr + a * slot + shift, 16, 1024);
+                            const uint64_t ad0 =
+                                smem_desc_sw128(sa_addr + (merge ? a * acc_rows_b : a * slot) + shift, 16, 1024);
                             const uint32_t dt = d_tmem + a * args.acc_stride;
 #pragma unroll
                             for (int k = 0; k < KSTEPS; k++) {
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");
             }
             for (int a = 0; a < macc; a++) {
-                const int tile = tg * tiles_per_unit + a * CG + (int)rank;
+                const int tile = tg * tiles_per_unit + (merge ? (int)rank * macc + a : a * CG + (int)rank);
                 int n, y, x;
                 bool row_ok;
                 if (args.stk) {   // stacked pixel m = n*(hs*wt) + y*wt + x
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
                     const int cw = args.st_cw > 0 ? (1 << args.st_cw) : EPC;
                     const int nch = args.BN / cw;
                     for (int a = 0; a < macc; a++) {
-                        const int tile = tg * tiles_per_unit + a * CG + (int)rank;
+                        const int tile = tg * tiles_per_unit + (merge ? (int)rank * macc + a : a * CG + (int)rank);
                         if (tile >= args.total_tiles) continue;
                         const int n = tile / args.tiles_per_img;
                         const int y0 = (tile - n * args.tiles_per_img) * args.halo_th;

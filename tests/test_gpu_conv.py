@@ -818,3 +818,50 @@ def test_conv_dgrad_taps_in_n(oracle, case, max_ctas):
         assert_tc_close(got, oracle.quant_bf16(ref), f"dgrad jn={jn} max_ctas={max_ctas}")
     # different FP32 summation order: the two kernels really ran (not bit-identical)
     assert (outs[1] != outs[0]).any()
+
+
+@pytest.mark.parametrize("case", [(2, 3, 227, 227, 96, (11, 11), (4, 4), (0, 0), 1),   # conv1: 28 tiles per image
+                                  (2, 64, 24, 30, 96, (3, 3), (1, 1), (1, 1), 1),      # 6 tiles of 4 rows
+                                  (3, 32, 16, 60, 64, (5, 5), (1, 1), (2, 2), 2)],     # 64-wide rows, 2 groups
+                         ids=["conv1", "H24W30", "W60g2"])
+@pytest.mark.parametrize("cta,max_ctas", [(2, 0), (2, 4), (1, 3)])
+def test_halo_merged_window_bit_identical(oracle, case, cta, max_ctas):
+    """CAFFE_TUNE_HALO_MERGE (off by default: a CTA's two accumulators take consecutive row blocks of
+    one image and share one staged window, three stages deep) writes exactly the bits of one window per tile, for
+    the halo forward (bias + ReLU, BF16 channels-last) and the stride-1 data gradient, CTA pairs and
+    single CTAs, full and capped grids (many units per CTA); the result meets the oracle bar."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W, O, k, s, p, g = case
+    X, Wt, b, dY = _inputs(case, 61)
+    if C == 3:
+        X = synth.int_pixels((N, C, H, W), 61)
+    cl = torch.channels_last
+    Xd = cuda(X).to(torch.bfloat16).contiguous(memory_format=cl)
+    dYd = cuda(dY).to(torch.bfloat16).contiguous(memory_format=cl)
+    outs = {}
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 2)
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, cta)
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_MAX_CTAS, max_ctas)
+    try:
+        for merge in (1, 0):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_MERGE, merge)
+            r = {"y": host(cb.conv_forward(Xd, cuda(Wt), cuda(b), stride=s, pad=p, group=g, relu=True))}
+            if s[0] == 1:
+                dX = torch.empty((N, C, H, W), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl)
+                cb.conv_backward_data(dYd, cuda(Wt), X.shape, stride=s, pad=p, group=g, out=dX)
+                r["dx"] = host(dX)
+            outs[merge] = r
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO_MERGE, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_MAX_CTAS, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_CTA_PAIR, 0)
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_HALO, 0)
+    for kk in outs[0]:
+        np.testing.assert_array_equal(outs[1][kk], outs[0][kk], err_msg=f"{kk} merged vs per-tile windows")
+    ry = oracle.conv_forward(host(Xd), oracle.quant_bf16(Wt), b, stride=s, pad=p, group=g, relu=True)
+    assert_bf16_ulp(outs[1]["y"], ry, "halo fwd merged", atol=_atol(ry))
+    if "dx" in outs[1]:
+        rd = oracle.conv_backward_data(host(dYd), oracle.quant_bf16(Wt), X.shape, stride=s, pad=p, group=g)
+        assert_bf16_ulp(outs[1]["dx"], rd, "halo dgrad merged", atol=_atol(rd))
