@@ -216,11 +216,15 @@ def test_tuning_knob_ranges(lib):
     from paper_1408_5093_b200 import _abi as A
     bad = [(A.CAFFE_TUNE_HALO_EPI_GROUPS, 1), (A.CAFFE_TUNE_HALO_EPI_GROUPS, 5), (A.CAFFE_TUNE_HALO_BTAPS, 9),
            (A.CAFFE_TUNE_MAX_CTAS, -1), (A.CAFFE_TUNE_SGD_THREADS, 96), (A.CAFFE_TUNE_SGD_BLOCKS_PER_SM, 9),
-           (A.CAFFE_TUNE_CTA_PAIR, 3), (A.CAFFE_TUNE_FUSED_POOL_ROWS, 65)]
+           (A.CAFFE_TUNE_CTA_PAIR, 3), (A.CAFFE_TUNE_FUSED_POOL_ROWS, 65), (A.CAFFE_TUNE_WGRAD_BN, 17),
+           (A.CAFFE_TUNE_WGRAD_BN, 272), (A.CAFFE_TUNE_WGRAD_BN, -16)]
     for key, value in bad:
         assert lib.caffe_set_tuning(key, value) == A.CAFFE_E_PARAM, (key, value)
     for key, value in [(A.CAFFE_TUNE_HALO_EPI_GROUPS, 2), (A.CAFFE_TUNE_HALO_EPI_GROUPS, 3),
-                       (A.CAFFE_TUNE_HALO_BTAPS, 5), (A.CAFFE_TUNE_MAX_CTAS, 16)]:
+                       (A.CAFFE_TUNE_HALO_BTAPS, 5), (A.CAFFE_TUNE_MAX_CTAS, 16), (A.CAFFE_TUNE_WGRAD_BN, 1),
+                       (A.CAFFE_TUNE_WGRAD_BN, 192), (A.CAFFE_TUNE_HALO_JN, 0), (A.CAFFE_TUNE_HALO_MERGE, 1)]:
         assert lib.caffe_set_tuning(key, value) == 0, (key, value)
-    for key in (A.CAFFE_TUNE_HALO_EPI_GROUPS, A.CAFFE_TUNE_HALO_BTAPS, A.CAFFE_TUNE_MAX_CTAS):
+    for key in (A.CAFFE_TUNE_HALO_EPI_GROUPS, A.CAFFE_TUNE_HALO_BTAPS, A.CAFFE_TUNE_MAX_CTAS, A.CAFFE_TUNE_WGRAD_BN,
+                A.CAFFE_TUNE_HALO_MERGE):
         assert lib.caffe_set_tuning(key, 0) == 0
+    assert lib.caffe_set_tuning(A.CAFFE_TUNE_HALO_JN, 1) == 0   # defaults restored

@@ -14,6 +14,10 @@ from paper_1408_5093_b200 import _abi  # noqa: E402
 from gemm_probe import timeit  # noqa: E402
 
 
+# library defaults of the knobs the probe sets (restored after each configuration)
+DEFAULTS = {5: 1, 10: 1, 11: 1, 12: 0, 18: 1, 22: 1}
+
+
 def main():
     dev = torch.device("cuda")
     B = 256
@@ -42,7 +46,7 @@ def main():
         print(f"{cfg:20s} conv1 fwd {t1 * 1e3:7.1f} us   conv2 fwd {t2 * 1e3:7.1f} us   conv2 dgrad {t3 * 1e3:7.1f} us",
               flush=True)
         for k, v in kv:
-            _abi.call("caffe_set_tuning", k, 1 if k in (5, 10, 11, 12) else 0)
+            _abi.call("caffe_set_tuning", k, DEFAULTS.get(k, 0))
 
 
 if __name__ == "__main__":
