@@ -497,7 +497,7 @@ def main():
         else:
             net.step(ar)
 
-    def timed(nsteps, instrument=False):
+    def timed(nsteps, instrument=False, eager=False, serial=False):
         if instrument:
             lib.caffe_profiler_enable(1)
         n0 = lib.caffe_launch_count()
@@ -505,7 +505,10 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(nsteps):
-            (net.step(ar) if instrument else run_step())
+            if instrument or eager:
+                net.step(ar, overlap_update=not serial)
+            else:
+                run_step()
         e1.record(stream)
         barrier()
         nl = lib.caffe_launch_count() - n0
@@ -528,13 +531,17 @@ def main():
     value = world * B * args.steps / (ms / 1000.0)
     # ---------------- instrumented eager pass: the same kernels with a CUDA-event pair around every
     # tcgen05 GEMM launch (library profiler, on the launching stream) -> roofline of the dominant kernel
-    # (weight gradients serialised with the data gradients here, so each event pair times one kernel
-    # alone rather than two time-sharing the SMs)
+    # (weight gradients serialised with the data gradients and, on one GPU, the SGD update after the
+    # backward, so each event pair times one kernel alone rather than several time-sharing the SMs --
+    # the regime of ncu's serialised launch list)
     wside = net.wgrad_side
     net.wgrad_side = False
-    ms_eager, nl_eager = timed(args.steps, instrument=True)
+    ms_eager, _ = timed(args.steps, instrument=True, serial=(world == 1))
     net.wgrad_side = wside
-    launches = nl_eager  # graph replays launch exactly the eager kernel sequence
+    # kernels per step: one eager pass of the benchmarked schedule (graph replays launch exactly the
+    # eager kernel sequence)
+    _, nl_eager = timed(args.steps, eager=True)
+    launches = nl_eager
     import ctypes
     g_ms, g_fl, g_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
     _abi.call("caffe_profiler_read", 0, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_n))
@@ -567,7 +574,8 @@ def main():
                 "launches_timed": g_n.value,
                 "avg_launch_ms": g_ms.value / max(1, g_n.value),
                 "algorithmic_gflop_per_launch": g_fl.value / max(1, g_n.value) / 1e9,
-                "measured_in": "instrumented eager pass of the same K steps (events around each GEMM launch)"}
+                "measured_in": "instrumented eager pass of the same K steps (events around each GEMM launch; "
+                               "weight gradients and the SGD update serialised, so each launch runs alone)"}
     extra = {
         "graph": use_graph,
         "graph_note": graph_note,
