@@ -229,7 +229,8 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_WGRAD_BN: output-channel (N) tile of the halo-tiled weight gradients: 0 (default) =
    automatic (several channel blocks: <= 96 columns, five accumulators per unit), 1 = the widest of
    192/128/96/64 dividing the outputs (faster alone, slower in the three-stream training step),
-   else a multiple of 16 up to 256.  Same result up to FP32 summation order. */
+   2 = <= 96 columns but 128 instead of 64 (measured no faster in the step), else a multiple of 16
+   up to 256.  Same result up to FP32 summation order. */
 #define CAFFE_TUNE_WGRAD_BN 23
 /* CAFFE_TUNE_HALO_MERGE: 1 = halo-tiled forward / data-gradient CTAs with two accumulators take two
    consecutive row blocks of one image and stage one shared input window for both, three stages deep

@@ -372,7 +372,11 @@ WgHalo wgrad_halo_plan(const Plan& p) {
     // faster alone (tools/wgrad_probe.py, batch 256, us: conv3 92.4 -> 86.9, conv4 72.8 -> 66.7,
     // conv5 59.6 -> 51.7) but slower in the three-stream step (tools/sched_sweep.py, same box:
     // 1.51-1.54 -> 1.57-1.62 ms/step), so off by default
-    if (h.cblocks > 1 && g_wgrad_bn != 1) {
+    if (h.cblocks > 1 && g_wgrad_bn == 2) {   // <= 96 columns, but 128 rather than 64
+        if (p.Og % 96 == 0) h.BN = 96;
+        else if (p.Og % 128 == 0) h.BN = 128;
+        else if (p.Og % 64 == 0) h.BN = 64;
+    } else if (h.cblocks > 1 && g_wgrad_bn != 1) {
         if (p.Og % 96 == 0) h.BN = 96;
         else if (p.Og % 64 == 0) h.BN = 64;
     } else if (h.cblocks > 1) {
@@ -381,7 +385,7 @@ WgHalo wgrad_halo_plan(const Plan& p) {
         else if (p.Og % 96 == 0) h.BN = 96;
         else if (p.Og % 64 == 0) h.BN = 64;
     }
-    if (g_wgrad_bn > 0 && g_wgrad_bn % 16 == 0 && g_wgrad_bn <= 256) h.BN = std::min(g_wgrad_bn, (int)rup(p.Og, 16));
+    if (g_wgrad_bn > 2 && g_wgrad_bn % 16 == 0 && g_wgrad_bn <= 256) h.BN = std::min(g_wgrad_bn, (int)rup(p.Og, 16));
     if (h.BN > 256) return h;
     h.n_tiles = (int)cdiv(p.Og, h.BN);
     h.nch = (int)cdiv(h.BN, 64);
@@ -750,7 +754,7 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_WGRAD_BN) {
-        if (value < 0 || value > 256 || (value % 16 && value != 1))
+        if (value < 0 || value > 256 || (value % 16 && value != 1 && value != 2))
             return fail(CAFFE_E_PARAM, "weight-gradient N tile must be 0 (auto), 1 (widest <= 192) or a multiple of 16 <= 256");
         g_wgrad_bn = value;
         return CAFFE_OK;
