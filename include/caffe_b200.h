@@ -237,6 +237,9 @@ caffe_status caffe_device_check(void);
    (where an image has an even number of tiles, e.g. the first layer); 0 (default) = one window per
    tile (measured as fast).  Identical results. */
 #define CAFFE_TUNE_HALO_MERGE 24
+/* CAFFE_TUNE_IP_MAX_SPLITS: cap on the split-K factor of the inner-product forward / data gradient
+   (0 = none: splits fill the CTA pairs).  Same result up to FP32 summation order. */
+#define CAFFE_TUNE_IP_MAX_SPLITS 25
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

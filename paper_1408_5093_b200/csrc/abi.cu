@@ -337,6 +337,7 @@ struct WgHalo {
     int Wt, TH, rows, tpi, total, ksteps, cblocks;  // tile geometry (output tile = TH rows x Wt columns)
     int BN, n_tiles, nch, acc_stride, macc, pairs, mgroups, splits, kb_per, slot, bchunk, stages;
 };
+int g_ip_max_splits = 0;   // CAFFE_TUNE_IP_MAX_SPLITS: cap on the inner-product split-K factor (0 = none)
 int g_wgrad_bn = 0;   // CAFFE_TUNE_WGRAD_BN: N tile of the halo weight gradient (0 = automatic)
 WgHalo wgrad_halo_plan(const Plan& p) {
     WgHalo h;
@@ -747,6 +748,11 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     if (key == CAFFE_TUNE_HALO_EPI_GROUPS) {
         if (value != 0 && (value < 2 || value > 4)) return fail(CAFFE_E_PARAM, "halo epilogue groups must be 0 (auto), 2, 3 or 4");
         g_halo_epi_groups = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_IP_MAX_SPLITS) {
+        if (value < 0 || value > 64) return fail(CAFFE_E_PARAM, "inner-product split cap must be 0 (none) .. 64");
+        g_ip_max_splits = value;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_HALO_MERGE) {
@@ -1507,6 +1513,7 @@ static IpPlan ip_plan(long long M, long long Ncols, long long Kred, int kchunk, 
     if (tiles < slots / 2) {
         int sp = (int)(slots / tiles);
         if (sp > q.kblocks / 4) sp = q.kblocks / 4;
+        if (g_ip_max_splits > 0 && sp > g_ip_max_splits) sp = g_ip_max_splits;
         if (sp > 1) {
             q.kb_per = (int)cdiv(q.kblocks, sp);
             q.splits = (int)cdiv(q.kblocks, q.kb_per);
