@@ -347,7 +347,7 @@ def small_workload(args):
     t0 = time.perf_counter()
     if args.workload == "lenet":
         nb = B
-        params = {net.layers[i].name: (net.W[i].float().cpu().numpy().astype(np.float64),
+        params = {net.layers[i].name: (net.canonical(i, net.W[i].float().cpu().numpy()).astype(np.float64),
                                        net.B[i].float().cpu().numpy().astype(np.float64)) for (i, _, _) in net.pspecs}
         moms = {k: (np.zeros_like(a), np.zeros_like(b)) for k, (a, b) in params.items()}
         onet.train_step(onet.LENET, X.astype(np.float64), params, moms, lab)

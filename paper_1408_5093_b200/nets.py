@@ -98,6 +98,7 @@ class Net:
         self.shapes = []            # input shape of each layer
         shape = (batch,) + tuple(input_shape)
         pspecs = []                 # (layer idx, w_shape, b_shape)
+        self.hwc = {}               # inner products whose weight columns are stored in (h, w, c) order
         self.conv_flops_fwd = 0
         self.conv_flops_step = 0    # fwd + wgrad + dgrad (no dgrad for the first layer)
         for i, L in enumerate(layers):
@@ -113,6 +114,8 @@ class Net:
             elif L.kind == "ip":
                 K = int(np.prod(shape[1:]))
                 pspecs.append((i, (L.num_output, K), (L.num_output,)))
+                if self.fc_hwc and len(shape) == 4 and shape[2] * shape[3] > 1:
+                    self.hwc[i] = (shape[1], shape[2], shape[3])
                 shape = (batch, L.num_output)
             elif L.kind == "lrn":
                 pass
@@ -135,6 +138,9 @@ class Net:
         for k, ((i, ws, bs), (ow, nw, ob, nb)) in enumerate(zip(pspecs, offs)):
             L = layers[i]
             w = synth.gaussian(ws, L.w_std, seed, synth.S_W, k) if L.w_std > 0 else synth.xavier(ws, seed, synth.S_W, k)
+            if i in self.hwc:   # the same weights, columns permuted from (c, h, w) to (h, w, c)
+                C, H, Wd = self.hwc[i]
+                w = w.reshape(ws[0], C, H, Wd).transpose(0, 2, 3, 1)
             host[ow:ow + nw] = w.ravel()
             host[ob:ob + nb] = L.b_init
             self.W[i] = self.params[ow:ow + nw].view(ws)
@@ -213,6 +219,31 @@ class Net:
             cb.conv_pack_weights(self._wop(j), self.shapes[j], L.stride, L.pad, L.group, self.math, 1, ws=self.wsd[j])
 
     # --------------------------------------------------------------- one training iteration
+    # fc6 (an inner product over a channels-last 4-D activation) keeps its weight columns in the
+    # (h, w, c) order of the activation's memory, so its input, its data gradient and its weight
+    # gradient's input are the channels-last buffers read as rows: no (c, h, w) staging transpose in
+    # the forward or the weight gradient, no channels-last scatter in the data gradient's split-K
+    # reduce.  The same linear map (S:130's (c, h, w) flatten with the columns permuted once);
+    # canonical(i, t) returns a weight-shaped tensor in the (c, h, w) column order.
+    fc_hwc = False
+
+    def _ip_rows(self, i, t):
+        """Layer i's (N, C, H, W) channels-last input (or its diff) as (N, H*W*C) rows."""
+        if i not in self.hwc:
+            return t
+        r = t.permute(0, 2, 3, 1).reshape(t.shape[0], -1)
+        assert r.data_ptr() == t.data_ptr(), "fc_hwc needs a channels-last activation"
+        return r
+
+    def canonical(self, i, t):
+        """A weight-shaped (O, K) tensor / array of layer i in the (c, h, w) column order of S:130."""
+        if i not in self.hwc:
+            return t
+        C, H, Wd = self.hwc[i]
+        if isinstance(t, np.ndarray):
+            return np.ascontiguousarray(t.reshape(t.shape[0], H, Wd, C).transpose(0, 3, 1, 2)).reshape(t.shape[0], -1)
+        return t.reshape(t.shape[0], H, Wd, C).permute(0, 3, 1, 2).reshape(t.shape[0], -1)
+
     def _wop(self, i):
         return self.Wq[i] if self.math == "bf16" else self.W[i]
 
@@ -266,6 +297,7 @@ class Net:
                 out = nxt if nxt is not None else self.scores
                 if i in self.rows:
                     x = cb.to_nchw(x, out=self.rows[i])
+                x = self._ip_rows(i, x)
                 cb.ip_forward(x, self._wop(i), self.B[i], self.math, relu=L.relu, out=out.view(out.shape[0], -1))
             elif L.kind == "loss":
                 cb.softmax_loss(self.scores, self.labels, loss=self.loss, diff=self.dscores)
@@ -312,6 +344,9 @@ class Net:
     # launch each layer's data gradient (main stream, the critical path) before its weight gradient
     # (side stream) so the persistent data-gradient GEMM claims the SMs first
     dgrad_first = False
+    # conv layers (names, space-separated) whose weight gradient starts only after their data
+    # gradient has completed
+    wgrad_after_dgrad = ""
     # cap on the persistent grid of the weight-gradient GEMMs on their side stream (0 = every SM):
     # leaves SMs to the critical path (data gradients, pool/LRN backward) they run beside
     wgrad_max_ctas = 0
@@ -382,7 +417,14 @@ class Net:
                         cb.conv_backward_data(dy, self._wop(i), a[i].shape, L.stride, L.pad, L.group, self.math,
                                               beta=0.0, out=d[i], ws=wsd, wprepacked=wpre)
 
-                if side and self.dgrad_first:   # the critical path's kernel claims the SMs first
+                if side and L.name in self.wgrad_after_dgrad.split():
+                    # this layer's weight gradient waits for its data gradient (the critical path's
+                    # GEMM runs alone, then the weight gradient overlaps the bandwidth-bound passes)
+                    dgrad()
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream())
+                    wgrad()
+                elif side and self.dgrad_first:   # the critical path's kernel claims the SMs first
                     dgrad()
                     wgrad()
                 else:
@@ -394,15 +436,16 @@ class Net:
                 # one GPU: the weight update is fused into the weight-gradient GEMM; it rewrites the
                 # BF16 weights, so it follows this layer's data gradient
                 dy2 = dy.view(dy.shape[0], -1)
+                xi, di = self._ip_rows(i, a[i]), self._ip_rows(i, d[i])
                 if i > 0 and self._relu_into_dgrad(i):
-                    cb.ip_backward_data_relu(dy2, self._wop(i), a[i], self.math, out=d[i])
+                    cb.ip_backward_data_relu(dy2, self._wop(i), xi, self.math, out=di)
                 elif i > 0:
-                    cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
+                    cb.ip_backward_data(dy2, self._wop(i), xi.shape, self.math, beta=0.0, out=di)
                 ev = torch.cuda.Event()
                 ev.record(torch.cuda.current_stream())
                 wgrad_stream.wait_event(ev)
                 with torch.cuda.stream(wgrad_stream):
-                    cb.ip_backward_weight_sgd(self.rows.get(i, a[i]), dy2, self.W[i], self.Mw[i], self.Wq[i], fused_sgd["lr"],
+                    cb.ip_backward_weight_sgd(self.rows.get(i, xi), dy2, self.W[i], self.Mw[i], self.Wq[i], fused_sgd["lr"],
                                               fused_sgd["momentum"], fused_sgd["decay"], 1.0, db=self.dB[i],
                                               ws=self._wgrad_workspace())
                     self.wgrad_done[i] = torch.cuda.Event()
@@ -411,6 +454,7 @@ class Net:
                     done_hook(i)
             elif L.kind == "ip":
                 dy2 = dy.view(dy.shape[0], -1)
+                xi, di = self._ip_rows(i, a[i]), self._ip_rows(i, d[i])
                 side = wgrad_stream is not None
                 if side:
                     ev = torch.cuda.Event()
@@ -420,21 +464,21 @@ class Net:
                     if side:
                         wgrad_stream.wait_event(ev)
                         with torch.cuda.stream(wgrad_stream), self._side_grid():
-                            cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
+                            cb.ip_backward_weight(self.rows.get(i, xi), dy2, self.W[i].shape, self.math, beta=0.0,
                                                   dw=self.dW[i], db=self.dB[i], ws=self._wgrad_workspace())
                             self.wgrad_done[i] = torch.cuda.Event()
                             self.wgrad_done[i].record(wgrad_stream)
                     else:
-                        cb.ip_backward_weight(self.rows.get(i, a[i]), dy2, self.W[i].shape, self.math, beta=0.0,
+                        cb.ip_backward_weight(self.rows.get(i, xi), dy2, self.W[i].shape, self.math, beta=0.0,
                                               dw=self.dW[i], db=self.dB[i])
                     if hook:
                         hook(i)
 
                 def dgrad():
                     if i > 0 and self._relu_into_dgrad(i):
-                        cb.ip_backward_data_relu(dy2, self._wop(i), a[i], self.math, out=d[i])
+                        cb.ip_backward_data_relu(dy2, self._wop(i), xi, self.math, out=di)
                     elif i > 0:
-                        cb.ip_backward_data(dy2, self._wop(i), a[i].shape, self.math, beta=0.0, out=d[i])
+                        cb.ip_backward_data(dy2, self._wop(i), xi.shape, self.math, beta=0.0, out=di)
 
                 if side and self.dgrad_first:
                     dgrad()

@@ -59,8 +59,8 @@ def stepped():
     net.graph.replay()
     torch.cuda.synchronize()
     # weights the step read (the step updates them in place at its end)
-    W = {i: snap["wq"][net.W[i].storage_offset() - net.params.storage_offset():][:net.W[i].numel()]
-         .view(net.W[i].shape).float().cpu().numpy().astype(np.float64) for (i, _, _) in net.pspecs}
+    W = {i: net.canonical(i, snap["wq"][net.W[i].storage_offset() - net.params.storage_offset():][:net.W[i].numel()]
+                          .view(net.W[i].shape).float().cpu().numpy().astype(np.float64)) for (i, _, _) in net.pspecs}
     Bs = {i: snap["params"][net.B[i].storage_offset() - net.params.storage_offset():][:net.B[i].numel()]
           .cpu().numpy().astype(np.float64) for (i, _, _) in net.pspecs}
     return net, snap, W, Bs, lab
@@ -205,7 +205,7 @@ def test_inner_product_bench_config(oracle, stepped, name):
         assert_bf16_ulp(got, ref, f"{name} fwd", atol=_conv_atol(ref))
     dy = _d(net, i + 1).reshape(B, -1)
     rdX, rdW, rdb = oracle.ip_backward(x, W[i], dy)
-    gW, gb = host(net.dW[i]).astype(np.float64), host(net.dB[i]).astype(np.float64)
+    gW, gb = net.canonical(i, host(net.dW[i])).astype(np.float64), host(net.dB[i]).astype(np.float64)
     assert_tc_close(gW, rdW, f"{name} dW")
     assert_tc_close(gb, rdb, f"{name} db")
     assert np.abs(gW - rdW).max() <= 1e-3 * np.abs(rdW).max()

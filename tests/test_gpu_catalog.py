@@ -221,7 +221,7 @@ def test_lenet_graph_loop_follows_oracle_then_decreases(oracle):
     over 500 iterations the mean loss of iterations 400-500 is below that of 0-100."""
     from oracle import net as onet, solver as osolver
     net, solver, loop, imgs, labs = _lenet_loop()
-    params = {net.layers[i].name: (host(net.W[i]).astype(np.float64), host(net.B[i]).astype(np.float64))
+    params = {net.layers[i].name: (net.canonical(i, host(net.W[i])).astype(np.float64), host(net.B[i]).astype(np.float64))
               for (i, _, _) in net.pspecs}
     moms = {k: (np.zeros_like(w), np.zeros_like(b)) for k, (w, b) in params.items()}
     ref = []

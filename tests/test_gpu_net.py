@@ -21,12 +21,18 @@ pytestmark = pytest.mark.gpu
 LRN = dict(size=5, alpha=1e-4, beta=0.75, k=1.0)
 
 
-def _build(which, batch, act):
+def _build(which, batch, act, fc_hwc=False):
     import torch
     from paper_1408_5093_b200 import nets
     layers, shape = (nets.LENET, nets.LENET_INPUT) if which == "lenet" else (nets.CAFFENET, nets.CAFFENET_INPUT)
     dt = torch.float32 if act == "f32" else torch.bfloat16
-    net = nets.Net(layers, batch, shape, torch.device("cuda"), act_dtype=dt, math="bf16", seed=0)
+    saved = nets.Net.fc_hwc
+    nets.Net.fc_hwc = fc_hwc   # read at construction (weight layout of the first inner product)
+    try:
+        net = nets.Net(layers, batch, shape, torch.device("cuda"), act_dtype=dt, math="bf16", seed=0)
+    finally:
+        nets.Net.fc_hwc = saved
+    assert bool(net.hwc) == fc_hwc
     net.fuse_pool_lrn = False   # every layer's blobs stored (the fused kernels: test_fused_pool_lrn_bit_identical)
     X = synth.int_pixels((batch,) + tuple(shape), 7) if which == "caffenet" else \
         synth.mnist_pixels((batch,) + tuple(shape), 7)
@@ -50,16 +56,19 @@ def _stored(net, ref, i_out):
     return ref
 
 
-@pytest.mark.parametrize("which,batch,act", [("lenet", 16, "f32"), ("lenet", 16, "bf16"),
-                                             ("caffenet", 2, "f32"), ("caffenet", 2, "bf16")])
-def test_net_teacher_forced(oracle, which, batch, act):
+@pytest.mark.parametrize("which,batch,act,hwc", [("lenet", 16, "f32", False), ("lenet", 16, "bf16", False),
+                                                 ("caffenet", 2, "f32", False), ("caffenet", 2, "bf16", False),
+                                                 ("lenet", 16, "bf16", True), ("caffenet", 2, "bf16", True)])
+def test_net_teacher_forced(oracle, which, batch, act, hwc):
+    """(hwc: the first inner product's weight columns stored in the (h, w, c) order of its channels-last
+    input, Net.fc_hwc -- compared through Net.canonical in the (c, h, w) order of S:130.)"""
     from oracle import net as onet
-    net, X, lab = _build(which, batch, act)
+    net, X, lab = _build(which, batch, act, fc_hwc=hwc)
     q = oracle.quant_bf16
     n = len(net.layers)
     # ---------------- end-to-end loss vs the oracle's own forward (BF16 GEMM operands)
     olayers = onet.LENET if which == "lenet" else onet.CAFFENET
-    params = {net.layers[i].name: (host(net.W[i]).astype(np.float64), host(net.B[i]).astype(np.float64))
+    params = {net.layers[i].name: (net.canonical(i, host(net.W[i])).astype(np.float64), host(net.B[i]).astype(np.float64))
               for (i, _, _) in net.pspecs}
     oloss, _, _ = onet.forward_backward(olayers, X, params, lab, quant=q)
     assert abs(float(net.loss) - oloss) <= 1e-3 * abs(oloss), (float(net.loss), oloss)
@@ -68,7 +77,7 @@ def test_net_teacher_forced(oracle, which, batch, act):
         x = host(net.a[i]).astype(np.float64)
         last = i + 1 == n - 1
         y = host(net.scores if last else net.a[i + 1])
-        W = host(net.W[i]) if i in net.W else None
+        W = net.canonical(i, host(net.W[i])) if i in net.W else None
         if L.kind == "conv":
             ref = oracle.conv_forward(q(x), q(W), host(net.B[i]), stride=(L.stride,) * 2, pad=(L.pad,) * 2,
                                       group=L.group, relu=L.relu)
@@ -106,9 +115,9 @@ def test_net_teacher_forced(oracle, which, batch, act):
             ref = oracle.conv_backward_data(q(dy), q(W), x.shape, stride=(L.stride,) * 2, pad=(L.pad,) * 2,
                                             group=L.group)
         elif L.kind == "ip":
-            W = host(net.W[i])
+            W = net.canonical(i, host(net.W[i]))
             dX, dW, _ = oracle.ip_backward(q(x), q(W), q(dy.reshape(dy.shape[0], -1)))
-            assert_tc_close(host(net.dW[i]), dW, f"{which} {L.name} dW")
+            assert_tc_close(net.canonical(i, host(net.dW[i])), dW, f"{which} {L.name} dW")
             assert_tc_close(host(net.dB[i]), dy.reshape(dy.shape[0], -1).sum(0), f"{which} {L.name} db")
             ref = dX.reshape(x.shape)
         elif L.kind == "pool":

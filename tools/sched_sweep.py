@@ -13,16 +13,22 @@ from paper_1408_5093_b200 import nets  # noqa: E402
 
 
 def run(assign):
-    if "tune" in assign and os.environ.get("SCHED_SWEEP_CHILD") != "1":
+    if ("tune" in assign or "cls." in assign) and os.environ.get("SCHED_SWEEP_CHILD") != "1":
         import subprocess
         out = subprocess.run([sys.executable, os.path.abspath(__file__), assign], capture_output=True, text=True,
                              env=dict(os.environ, SCHED_SWEEP_CHILD="1", REPS="1"), timeout=600).stdout
         return float(out.strip().splitlines()[-1].split()[-4]) / 1e3
     from paper_1408_5093_b200 import _abi
     dev = torch.device("cuda")
+    for kv in filter(None, assign.split(",")):   # "cls.X=V": a Net class attribute read at construction
+        k, v = kv.split("=")
+        if k.startswith("cls."):
+            setattr(nets.Net, k[4:], type(getattr(nets.Net, k[4:]))(eval(v)))
     net = nets.Net(nets.CAFFENET, 256, nets.CAFFENET_INPUT, dev, math="bf16", seed=0, input_i8=True)
     for kv in filter(None, assign.split(",")):
         k, v = kv.split("=")
+        if k.startswith("cls."):
+            continue
         if k.startswith("tune"):
             _abi.call("caffe_set_tuning", int(k[4:]), int(eval(v)))
         else:
