@@ -32,7 +32,8 @@ def run(assign):
         if k.startswith("tune"):
             _abi.call("caffe_set_tuning", int(k[4:]), int(eval(v)))
         else:
-            setattr(net, k, type(getattr(net, k))(eval(v)))
+            cur = getattr(net, k)
+            setattr(net, k, eval(v) if cur is None else type(cur)(eval(v)))
     net.a[0].copy_(torch.from_numpy(synth.int_pixels((256, 3, 227, 227), 1000)).to(net.a[0].dtype))
     net.labels.copy_(torch.from_numpy(synth.labels(256, 1000, 1000)))
     for _ in range(3):
