@@ -271,9 +271,51 @@ class Net:
         # C = 96 a quarter of the lanes idle and the separate kernels are faster (48.5 vs 52 us)
         return ok and (self.fuse_lrn_pool_backward or 32 % (x.shape[1] // 8) == 0)
 
+    # conv weight operands packed at the start of each step on a side stream (1: the forward
+    # operands, 2: forward and data-gradient operands) into dedicated workspaces; the passes then
+    # skip their per-call repack (CAFFE_WEIGHTS_PREPACKED) and only wait for their layer's pack --
+    # the five forward repacks (2.4-4 us each) leave the serial forward.  Measured (same box,
+    # tools/sched_sweep.py, 6 alternations): 1 -> 1.490-1.515 ms/step (mean 1.500), 0 -> 1.492-1.533
+    # (mean 1.513); 2 (the data-gradient packs too) was not better than 1.  Bit-identical.
+    pack_side = 1
+
+    def _pack_side_begin(self):
+        torch = self.torch
+        if getattr(self, "_psf", None) is None:
+            self._psf, self._psd = {}, {}
+            for i, L in enumerate(self.layers):
+                if L.kind != "conv":
+                    continue
+                wsh = tuple(self.W[i].shape)
+                self._psf[i] = (self.ws0 if (i == 0 and self.ws0 is not None) else
+                                cb.conv_workspace(self.shapes[i], wsh, L.stride, L.pad, L.group, self.math, 0, self.device))
+                if i > 0:
+                    self._psd[i] = cb.conv_workspace(self.shapes[i], wsh, L.stride, L.pad, L.group, self.math, 1,
+                                                     self.device)
+            self._pstream = torch.cuda.Stream(priority=self.wgrad_priority)
+        main = torch.cuda.current_stream()
+        self._pstream.wait_stream(main)   # the previous step's updates are complete on main
+        self._pev_f, self._pev_d = {}, {}
+        with torch.cuda.stream(self._pstream):
+            for i in self._psf:
+                L = self.layers[i]
+                cb.conv_pack_weights(self._wop(i), self.shapes[i], L.stride, L.pad, L.group, self.math, 0, ws=self._psf[i])
+                self._pev_f[i] = torch.cuda.Event()
+                self._pev_f[i].record(self._pstream)
+            if self.pack_side >= 2:
+                for i in self._psd:
+                    L = self.layers[i]
+                    cb.conv_pack_weights(self._wop(i), self.shapes[i], L.stride, L.pad, L.group, self.math, 1,
+                                         ws=self._psd[i])
+                    self._pev_d[i] = torch.cuda.Event()
+                    self._pev_d[i].record(self._pstream)
+
     def forward(self):
         a, n = self.a, len(self.layers)
         skip = set()
+        side_pack = bool(self.pack_side) and self.math != "fp32" and not self.wsf
+        if side_pack:
+            self._pack_side_begin()
         for i, L in enumerate(self.layers):
             if i in skip:
                 continue
@@ -284,8 +326,12 @@ class Net:
                 if pre and not self.external_pack:
                     cb.conv_pack_bottom(x, self._wop(i), L.stride, L.pad, L.group, self.math, ws=self.ws0)
                 wpre = i in self.wsf
+                wsf = self.wsf.get(i)
+                if side_pack:
+                    self.torch.cuda.current_stream().wait_event(self._pev_f[i])
+                    wpre, wsf = True, self._psf[i]
                 cb.conv_forward(x, self._wop(i), self.B[i], L.stride, L.pad, L.group, self.math, relu=L.relu, out=nxt,
-                                ws=self.wsf[i] if wpre else (self.ws0 if pre else None), prepacked=pre, wprepacked=wpre)
+                                ws=wsf if wpre else (self.ws0 if pre else None), prepacked=pre, wprepacked=wpre)
             elif L.kind == "pool" and self._pool_lrn(i):
                 cb.pool_lrn_forward(x, L.kernel, L.stride, L.pad, **LRN, pool_out=nxt, mask=self.mask[i], out=a[i + 2])
                 skip.add(i + 1)
@@ -301,6 +347,8 @@ class Net:
                 cb.ip_forward(x, self._wop(i), self.B[i], self.math, relu=L.relu, out=out.view(out.shape[0], -1))
             elif L.kind == "loss":
                 cb.softmax_loss(self.scores, self.labels, loss=self.loss, diff=self.dscores)
+        if side_pack:   # rejoin (the data-gradient packs finished long before)
+            self.torch.cuda.current_stream().wait_stream(self._pstream)
 
     def _relu_fused(self, i):
         """True when layer i's ReLU backward is folded into the MAX-pool backward of layer i+1."""
@@ -410,6 +458,9 @@ class Net:
                 def dgrad():
                     wpre = i in self.wsd
                     wsd = self.wsd.get(i)
+                    if getattr(self, "_pev_d", None) and i in self._pev_d:
+                        torch.cuda.current_stream().wait_event(self._pev_d[i])
+                        wpre, wsd = True, self._psd[i]
                     if i > 0 and self._relu_into_dgrad(i):
                         cb.conv_backward_data_relu(dy, self._wop(i), a[i], L.stride, L.pad, L.group, self.math,
                                                    out=d[i], ws=wsd, wprepacked=wpre)

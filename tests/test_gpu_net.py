@@ -242,3 +242,25 @@ def test_dp_path_single_rank_nccl():
         np.testing.assert_array_equal(outs[0], outs[1])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_side_stream_weight_packs_bit_identical(mode):
+    """Net.pack_side (conv weight operands packed at the start of the step on a side stream into
+    dedicated workspaces; 1: forward, 2: forward + data gradient) gives exactly the bits of the
+    per-call repacks: loss, every parameter gradient and the updated parameters after two steps."""
+    import torch
+    from paper_1408_5093_b200 import nets
+    outs = []
+    for ps in (0, mode):
+        net = nets.Net(nets.CAFFENET, 4, nets.CAFFENET_INPUT, torch.device("cuda"), math="bf16", seed=0)
+        net.pack_side = ps
+        net.a[0].copy_(torch.from_numpy(synth.int_pixels((4,) + tuple(nets.CAFFENET_INPUT), 5)))
+        net.labels.copy_(torch.from_numpy(synth.labels(4, 1000, 5)))
+        for _ in range(2):
+            net.step()
+        torch.cuda.synchronize()
+        outs.append((float(net.loss), net.grads.cpu().numpy().copy(), net.params.cpu().numpy().copy()))
+    assert outs[0][0] == outs[1][0]
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[0][2], outs[1][2])
