@@ -392,6 +392,8 @@ class Net:
     # launch each layer's data gradient (main stream, the critical path) before its weight gradient
     # (side stream) so the persistent data-gradient GEMM claims the SMs first
     dgrad_first = False
+    # the inner-product weight gradients on the weight-gradient stream (False: on the main stream)
+    ip_wgrad_side = True
     # conv layers (names, space-separated) whose weight gradient starts only after their data
     # gradient has completed
     wgrad_after_dgrad = ""
@@ -506,7 +508,7 @@ class Net:
             elif L.kind == "ip":
                 dy2 = dy.view(dy.shape[0], -1)
                 xi, di = self._ip_rows(i, a[i]), self._ip_rows(i, d[i])
-                side = wgrad_stream is not None
+                side = wgrad_stream is not None and self.ip_wgrad_side
                 if side:
                     ev = torch.cuda.Event()
                     ev.record(torch.cuda.current_stream())
