@@ -240,6 +240,10 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_IP_MAX_SPLITS: cap on the split-K factor of the inner-product forward / data gradient
    (0 = none: splits fill the CTA pairs).  Same result up to FP32 summation order. */
 #define CAFFE_TUNE_IP_MAX_SPLITS 25
+/* CAFFE_TUNE_I8_ROWS: 1 (default) = the int8 image pack of a 4x4 space-to-depth of 3 channels (the
+   CaffeNet first layer) runs one thread per packed pixel (four 12-byte segments in flight, six
+   16-byte stores); 0 = one thread per 12-byte source segment.  Identical results. */
+#define CAFFE_TUNE_I8_ROWS 26
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

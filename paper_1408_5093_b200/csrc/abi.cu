@@ -750,6 +750,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_halo_epi_groups = value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_I8_ROWS) {
+        cb::g_i8_rows = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_IP_MAX_SPLITS) {
         if (value < 0 || value > 64) return fail(CAFFE_E_PARAM, "inner-product split cap must be 0 (none) .. 64");
         g_ip_max_splits = value;

@@ -403,8 +403,68 @@ __global__ void pack_i8_generic_kernel(const int8_t* __restrict__ src, __nv_bflo
     }
 }
 
+// Pixel form: one thread per packed pixel (n, Y, X) of a 4x4 space-to-depth of 3 channels (CaffeNet's
+// first layer: 48 channels, no padding): its four 12-byte source segments are read as word loads +
+// funnel shifts, all in flight together, and the 96-byte packed pixel leaves as six 16-byte stores
+// (the segment kernel writes 8-byte pieces at a 24-byte stride, one dy row per thread).
+__device__ __forceinline__ void i8_seg12(const int8_t* p, bool whole, int nv, uint32_t (&x)[3]) {
+    if (whole) {
+        const uintptr_t b = reinterpret_cast<uintptr_t>(p);
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(b & ~uintptr_t(3));
+        const uint32_t sh = (uint32_t)(b & 3) * 8u;
+        const uint32_t w0 = __ldg(wp), w1 = __ldg(wp + 1), w2 = __ldg(wp + 2);
+        const uint32_t w3 = sh ? __ldg(wp + 3) : 0u;
+        x[0] = __funnelshift_r(w0, w1, sh);
+        x[1] = __funnelshift_r(w1, w2, sh);
+        x[2] = __funnelshift_r(w2, w3, sh);
+    } else {
+        x[0] = x[1] = x[2] = 0u;
+        for (int i = 0; i < nv; i++) x[i >> 2] |= (uint32_t)(uint8_t)__ldg(p + i) << (8 * (i & 3));
+    }
+}
+__global__ void pack_i8_px_kernel(const int8_t* __restrict__ src, __nv_bfloat16* __restrict__ dst, PackGeom g,
+                                  int total) {
+    // (a thread per 16-byte chunk, chunks fastest, measured 76 us: runtime-indexed segment words spill)
+    const int8_t* src_end = src + (long long)g.N * g.H * g.W * 3;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        int r = t;
+        const int X = r % g.Wp; r /= g.Wp;
+        const int Y = r % g.Hp;
+        const int n = r / g.Hp;
+        const int nv = max(0, min(12, (g.W - X * 4) * 3));
+        uint32_t x[4][3];
+#pragma unroll
+        for (int dy = 0; dy < 4; dy++) {
+            const int h = Y * 4 + dy;
+            const int8_t* p = src + (((long long)n * g.H + h) * g.W + (long long)X * 4) * 3;
+            const int v = h < g.H ? nv : 0;
+            i8_seg12(p, v == 12 && p + 16 <= src_end, v, x[dy]);
+        }
+        uint32_t o[24];
+#pragma unroll
+        for (int k = 0; k < 24; k++) {   // channels 2k, 2k+1 = bytes of segment (2k)/12
+            const int k0 = 2 * k, k1 = k0 + 1;
+            const float a = (float)(int8_t)(x[k0 / 12][(k0 % 12) >> 2] >> (8 * ((k0 % 12) & 3)));
+            const float c = (float)(int8_t)(x[k1 / 12][(k1 % 12) >> 2] >> (8 * ((k1 % 12) & 3)));
+            __nv_bfloat162 bv = __floats2bfloat162_rn(a, c);
+            o[k] = *reinterpret_cast<uint32_t*>(&bv);
+        }
+        uint4* q = reinterpret_cast<uint4*>(dst + (long long)t * 48);
+#pragma unroll
+        for (int j = 0; j < 6; j++) q[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+    }
+}
+int g_i8_rows = 1;   // CAFFE_TUNE_I8_ROWS
+
 cudaError_t pack_act_i8(const void* src, void* dst, const PackGeom& g, cudaStream_t s) {
     const int L = g.sw * g.C;
+    if (g_i8_rows && g.G == 1 && g.ph == 0 && g.pw == 0 && g.C == 3 && g.sh == 4 && g.sw == 4 && g.Ctot == 48 &&
+        g.cpg == 48 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        const int total = g.N * g.Hp * g.Wp;
+        pack_i8_px_kernel<<<blocks_for(total, 256), 256, 0, s>>>((const int8_t*)src, (__nv_bfloat16*)dst, g, total);
+        note_launch();
+        return cudaGetLastError();
+    }
     if (g.G == 1 && g.ph == 0 && g.pw == 0 && L <= 16 && L % 2 == 0 && g.cpg == g.Ctot && g.Ctot >= g.sh * L &&
         (g.Ctot - g.sh * L) % 2 == 0 && g.Ctot % 2 == 0) {
         const int total = g.N * g.Hp * g.Wp * g.sh;

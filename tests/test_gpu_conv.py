@@ -581,10 +581,23 @@ def test_conv_stacked_halo(oracle, case, cta):
 @pytest.mark.parametrize("case", [CASES[3], (2, 3, 67, 67, 96, (11, 11), (4, 4), (0, 0), 1),
                                   (2, 4, 9, 9, 8, (3, 3), (1, 1), (1, 1), 1)],
                          ids=["conv1like", "conv1geom", "plain3x3"])
-def test_conv_i8_bottom(oracle, case):
+@pytest.mark.parametrize("rows", [1, 0])
+def test_conv_i8_bottom(oracle, case, rows):
     """An int8 channels-last image batch (CAFFE_I8) packed by caffe_conv_pack_bottom gives the same
     bits as the same integers stored in BF16, for the prepacked forward and weight gradient
-    (space-to-depth segment kernel and the element-form pack)."""
+    (space-to-depth: the row-staged pack, CAFFE_TUNE_I8_ROWS=1, or the segment kernel; the
+    element-form pack otherwise)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_I8_ROWS, rows)
+    try:
+        _i8_bottom(oracle, case)
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_I8_ROWS, 1)
+
+
+def _i8_bottom(oracle, case):
     import torch
     import paper_1408_5093_b200 as cb
     N, C, H, W, O, k, s, p, g = case
