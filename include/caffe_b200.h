@@ -244,6 +244,10 @@ caffe_status caffe_device_check(void);
    CaffeNet first layer) runs one thread per packed pixel (four 12-byte segments in flight, six
    16-byte stores); 0 = one thread per 12-byte source segment.  Identical results. */
 #define CAFFE_TUNE_I8_ROWS 26
+/* CAFFE_TUNE_ROWS_CB: 1 (default) = a BF16 channels-last inner-product input is staged as (c,h,w)
+   rows by one block per (64-channel block, image) with paired 4-byte stores; 0 = one block per image
+   (scalar stores).  Identical results. */
+#define CAFFE_TUNE_ROWS_CB 27
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

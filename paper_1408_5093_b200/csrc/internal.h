@@ -166,6 +166,7 @@ cudaError_t pack_act(const void* src, int src_bf16, L4 ls, int src_nhwc, void* d
 // Channels-last int8 image batch -> packed BF16 operand (same layout as pack_act; exact).
 cudaError_t pack_act_i8(const void* src, void* dst, const PackGeom& g, cudaStream_t s);
 extern int g_i8_rows;   // CAFFE_TUNE_I8_ROWS
+extern int g_rows_cb;   // CAFFE_TUNE_ROWS_CB
 // Inverse for the s2d data gradient into a blob of either layout, with beta.
 cudaError_t unpack_s2d_grad(const float* T, void* dX, int dx_bf16, int xnhwc, float beta, const PackGeom& g,
                             cudaStream_t s);

@@ -1115,6 +1115,35 @@ __global__ void nhwc_to_rows_kernel(const void* __restrict__ src, int src_bf16, 
     }
 }
 
+// BF16 -> BF16 rows, one block per (64-channel block, image): the block's HW x 64 channels are read
+// as 16-byte vectors into shared memory (pitch 65) and leave as bf16x2 stores -- a warp writes 128
+// contiguous bytes of the (c,h,w) row (the one-block-per-image form stores scalar 2-byte elements
+// from 256 blocks: latency-bound, ~10 us for fc6's 4.7 MB input)
+int g_rows_cb = 1;   // CAFFE_TUNE_ROWS_CB
+__global__ void __launch_bounds__(256) nhwc_to_rows_cb_kernel(const __nv_bfloat16* __restrict__ src,
+                                                              __nv_bfloat16* __restrict__ dst, int C, int HW) {
+    extern __shared__ float tr_cb[];   // [HW][65]
+    const int n = blockIdx.y, c0 = blockIdx.x * 64;
+    const __nv_bfloat16* sp = src + (long long)n * C * HW + c0;
+    for (int i = threadIdx.x; i < HW * 8; i += blockDim.x) {
+        const int p = i >> 3, v = i & 7;
+        const uint4 u = *reinterpret_cast<const uint4*>(sp + (long long)p * C + v * 8);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const float2 f = __bfloat1622float2(h[q]);
+            tr_cb[p * 65 + v * 8 + 2 * q] = f.x;
+            tr_cb[p * 65 + v * 8 + 2 * q + 1] = f.y;
+        }
+    }
+    __syncthreads();
+    __nv_bfloat162* dp = reinterpret_cast<__nv_bfloat162*>(dst + ((long long)n * C + c0) * HW);
+    for (int k2 = threadIdx.x; k2 < 32 * HW; k2 += blockDim.x) {   // element pairs (k, k+1) of the block's rows
+        const int k = 2 * k2, c = k / HW, p = k - c * HW;          // HW even: a pair never straddles channels
+        dp[k2] = __floats2bfloat162_rn(tr_cb[p * 65 + c], tr_cb[(p + 1) * 65 + c]);
+    }
+}
+
 // One block per image: the (HW x C) channels-last image is read coalesced into shared memory
 // (padded pitch C+1) and written as the (c,h,w)-ordered row, coalesced; 32-bit index math.
 __global__ void nhwc_to_rows_tiled_kernel(const void* __restrict__ src, int src_bf16, void* __restrict__ dst, int esz,
@@ -1160,6 +1189,14 @@ __global__ void nhwc_to_rows_tiled_kernel(const void* __restrict__ src, int src_
 
 cudaError_t nhwc_to_rows(const void* src, int src_bf16, void* dst, int dst_esz, int N, int C, int HW, long long ld,
                          cudaStream_t s) {
+    if (g_rows_cb && src_bf16 && dst_esz == 2 && C % 64 == 0 && HW % 2 == 0 && ld == (long long)C * HW &&
+        HW * 65 * 4 <= 48 * 1024 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) & 3) == 0 && ld < (1LL << 31)) {
+        const size_t tile = (size_t)HW * 65 * sizeof(float);
+        nhwc_to_rows_cb_kernel<<<dim3(C / 64, N), 256, tile, s>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, C, HW);
+        note_launch();
+        return cudaGetLastError();
+    }
     const size_t tile = (size_t)HW * (C + 1) * sizeof(float);
     if (tile <= 48 * 1024 && ld < (1LL << 31)) {
         nhwc_to_rows_tiled_kernel<<<N, 256, tile, s>>>(src, src_bf16, dst, dst_esz, C, HW, (int)ld);

@@ -509,3 +509,33 @@ def test_fp32_nhwc_vector_paths(oracle, shape):
                                   oracle.maxpool_backward(dY, rM, shape, (3, 3), (2, 2)))
     np.testing.assert_array_equal(host(cb.pool_relu_backward(P, dYt, M, shape, 3, 2)),
                                   oracle.relu_backward(Xr, oracle.maxpool_backward(dY, rM, shape, (3, 3), (2, 2))))
+
+
+@pytest.mark.parametrize("shape", [(5, 256, 6, 6), (3, 64, 4, 6)], ids=["pool5", "C64HW24"])
+def test_ip_nhwc_rows_staging_bit_identical(oracle, shape):
+    """The (c,h,w) row staging of a channels-last BF16 inner-product input (CAFFE_TUNE_ROWS_CB: one
+    block per 64-channel block and image, or one per image) gives the same bits for the forward and
+    the weight gradient, and the forward meets the oracle bar (flatten order S:130)."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    N, C, H, W = shape
+    K, O = C * H * W, 96
+    x = synth.uniform(shape, 3, synth.S_X)
+    w = synth.xavier((O, K), 3)
+    dy = synth.uniform((N, O), 3, synth.S_DY)
+    xd = cuda(x).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    wd = cuda(w).to(torch.bfloat16)
+    outs = []
+    try:
+        for v in (1, 0):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_ROWS_CB, v)
+            y = cb.ip_forward(xd, wd, None, "bf16", out_dtype=torch.float32)
+            dw, _ = cb.ip_backward_weight(xd, cuda(dy).to(torch.bfloat16), (O, K), "bf16")
+            outs.append((host(y), host(dw)))
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_ROWS_CB, 1)
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    q = oracle.quant_bf16
+    assert_tc_close(outs[0][0], oracle.ip_forward(q(x.reshape(N, -1)), q(w)), "ip fwd nhwc rows")
