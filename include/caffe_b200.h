@@ -248,6 +248,11 @@ caffe_status caffe_device_check(void);
    rows by one block per (64-channel block, image) with paired 4-byte stores; 0 = one block per image
    (scalar stores).  Identical results. */
 #define CAFFE_TUNE_ROWS_CB 27
+/* CAFFE_TUNE_BIAS_ROWS: 1 = an inner product's bias gradient (<= 8192 rows) in one pass (8 row
+   groups per column block, fixed order); 0 (default) = split partials + a final pass (the one-pass
+   form measured slower in the training step).  Deterministic either way; the FP32 summation order
+   differs. */
+#define CAFFE_TUNE_BIAS_ROWS 28
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -750,6 +750,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_halo_epi_groups = value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_BIAS_ROWS) {
+        cb::g_bias_rows = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_ROWS_CB) {
         cb::g_rows_cb = value ? 1 : 0;
         return CAFFE_OK;

@@ -539,3 +539,31 @@ def test_ip_nhwc_rows_staging_bit_identical(oracle, shape):
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
     q = oracle.quant_bf16
     assert_tc_close(outs[0][0], oracle.ip_forward(q(x.reshape(N, -1)), q(w)), "ip fwd nhwc rows")
+
+
+@pytest.mark.parametrize("N,O", [(256, 4096), (37, 1000), (3, 20)], ids=["fc6", "fc8odd", "tiny"])
+def test_ip_bias_grad_one_pass(oracle, N, O):
+    """Inner-product bias gradient db = beta*db + sum_n dY in one pass (CAFFE_TUNE_BIAS_ROWS=1)
+    and as split partials + final (=0): each meets the FP32 bar against the oracle, both with beta=1
+    accumulation, and each is deterministic run to run."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    K = 64
+    x = synth.uniform((N, K), 4, synth.S_X)
+    dy = synth.uniform((N, O), 4, synth.S_DY)
+    prev = synth.uniform((O,), 4, synth.S_AUX)
+    ref = dy.astype(np.float64).sum(0) + prev
+    try:
+        for v in (1, 0):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_BIAS_ROWS, v)
+            got = []
+            for _ in range(2):
+                db = cuda(prev.copy())
+                cb.ip_backward_weight(cuda(x), cuda(dy), (O, K), "bf16", beta=1.0, dw=torch.zeros(O, K, device="cuda"),
+                                      db=db)
+                got.append(host(db))
+            np.testing.assert_array_equal(got[0], got[1])
+            assert_fp32_close(got[0], ref, f"ip db bias_rows={v}")
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_BIAS_ROWS, 0)
