@@ -394,8 +394,8 @@ class Net:
     dgrad_first = False
     # the inner-product weight gradients on the weight-gradient stream (False: on the main stream)
     ip_wgrad_side = True
-    # conv layers (names, space-separated) whose weight gradient starts only after their data
-    # gradient has completed
+    # conv / inner-product layers (names, space-separated) whose weight gradient starts only after
+    # their data gradient has completed (measured: conv2 / conv2-5 no better, fc6 or fc8 +70-90 us)
     wgrad_after_dgrad = ""
     # cap on the persistent grid of the weight-gradient GEMMs on their side stream (0 = every SM):
     # leaves SMs to the critical path (data gradients, pool/LRN backward) they run beside
@@ -533,7 +533,12 @@ class Net:
                     elif i > 0:
                         cb.ip_backward_data(dy2, self._wop(i), xi.shape, self.math, beta=0.0, out=di)
 
-                if side and self.dgrad_first:
+                if side and L.name in self.wgrad_after_dgrad.split():
+                    dgrad()
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream())
+                    wgrad()
+                elif side and self.dgrad_first:
                     dgrad()
                     wgrad()
                 else:
