@@ -253,6 +253,9 @@ caffe_status caffe_device_check(void);
    form measured slower in the training step).  Deterministic either way; the FP32 summation order
    differs. */
 #define CAFFE_TUNE_BIAS_ROWS 28
+/* CAFFE_TUNE_BIAS_SPLIT_ROWS: rows (pixels x images) per split of the two-pass bias gradient, 8 ..
+   1024 (default 64).  Deterministic; the FP32 summation order follows the split. */
+#define CAFFE_TUNE_BIAS_SPLIT_ROWS 29
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -216,6 +216,7 @@ cudaError_t fp32_conv_wgrad(const void* x, int x_bf16, L4 lx, const void* dy, in
                             float beta, const ConvGeom& g, cudaStream_t s, int tf32 = 0);
 int bias_grad_splits(int N, int O, int P);
 extern int g_bias_rows;   // CAFFE_TUNE_BIAS_ROWS
+extern int g_bias_split_rows;   // CAFFE_TUNE_BIAS_SPLIT_ROWS
 cudaError_t bias_grad(const void* dy, int dy_bf16, int nhwc, float* db, float beta, int N, int O, int P, float* part,
                       cudaStream_t s);
 cudaError_t im2col_k(const float* x, int n, const ConvGeom& g, float* col, cudaStream_t s);

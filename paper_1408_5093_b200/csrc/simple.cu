@@ -263,9 +263,10 @@ __global__ void bias_final(const float* __restrict__ part, int S, int O, float* 
 }
 
 // splits of the pixel range: ~8 blocks per SM, >= 64 rows each
+int g_bias_split_rows = 64;   // CAFFE_TUNE_BIAS_SPLIT_ROWS: rows per bias-gradient split (8 .. 1024)
 int bias_grad_splits(int N, int O, int P) {
     const long long M = (long long)N * P;
-    long long S = (M + 63) / 64;
+    long long S = (M + g_bias_split_rows - 1) / g_bias_split_rows;
     if (S > BG_SPLITS_MAX) S = BG_SPLITS_MAX;
     return S < 1 ? 1 : (int)S;
 }
