@@ -109,7 +109,10 @@ __device__ __forceinline__ void epi_store_bf16_rowseg_coal(uint32_t taddr, bool 
     }
 #pragma unroll
     for (int it = 0; it < NCH; it++)
-        if (st_ok[it]) *reinterpret_cast<uint4*>(addr[it]) = piece[it];
+        if (st_ok[it])   // global-space store (a pointer rebuilt from an integer would be a generic ST)
+            asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(addr[it]), "r"(piece[it].x), "r"(piece[it].y),
+                         "r"(piece[it].z), "r"(piece[it].w)
+                         : "memory");
 }
 
 // Same arithmetic as epi_store_bf16_rowseg, but the row's EPC columns (tile columns
