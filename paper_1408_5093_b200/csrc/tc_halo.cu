@@ -319,6 +319,17 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
         const bool tstore = EPC > 0 && args.tma_store != 0;
         const uint32_t stg = (smem_u32(sbias + 2 * 256) + 1023u) & ~1023u;
         const bool issuer = warp == 4 && lane == 0;
+        // one group and one N tile (the first layer): every unit has the same bias columns -- stage
+        // both accumulator slots' copies once instead of once per unit behind a group barrier
+        const bool bias_const = args.bias && args.n_tiles == 1 && args.groups == 1;
+        if (bias_const) {
+            for (int c = cb_ + row; c < ce_; c += 128) {
+                const float b = c < args.N ? args.bias[c] : 0.f;
+                sbias[c] = b;
+                sbias[256 + c] = b;
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");
+        }
         for (int u = cid; u < units; u += ncl) {
             int t = u;
             const int n_tile = t % args.n_tiles; t /= args.n_tiles;
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
             const int col0 = n_tile * args.BN;
             const int cbase = g * args.col_g + col0;
             float* bs = sbias + acc * 256;
-            if (args.bias) {
+            if (args.bias && !bias_const) {
                 for (int c = cb_ + row; c < ce_; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");
             }
