@@ -273,6 +273,15 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
         int tbuf = 0;
+        // the whole bias vector (groups x N <= 512 columns, whole N tiles) staged once per kernel
+        // instead of each unit's columns behind a barrier; a unit reads its columns at offset cbase
+        const int nbias = args.groups * args.N;
+        const bool bias_const = args.bias && EPI != EPI_SGD && nbias <= 512 && args.N % args.BN == 0 &&
+                                args.col_g == args.N;
+        if (bias_const) {
+            for (int c = row; c < nbias; c += 128) sbias[c] = args.bias[c];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         for (int u = cid; u < args.units; u += ncl) {
             int t = u;
             const int n_tile = t % args.n_tiles; t /= args.n_tiles;
@@ -312,8 +321,8 @@ __global__ void __launch_bounds__(256, 1)
                 const int cbase = g * args.col_g + col0;   // output channel of tile column 0
                 // stage this tile's bias once (double-buffered by accumulator: a warp can be at most
                 // one tile ahead of the slowest epilogue warp)
-                float* bs = sbias + acc * 256;
-                if (args.bias) {
+                float* bs = bias_const ? sbias + cbase : sbias + acc * 256;
+                if (args.bias && !bias_const) {
                     for (int c = row; c < args.BN; c += 128) bs[c] = (col0 + c < args.N) ? args.bias[cbase + c] : 0.f;
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
