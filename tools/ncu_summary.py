@@ -15,9 +15,12 @@ import json
 # algorithmic GFLOP per pass at batch 256 (2 * MACs)
 CONV_GF = {"conv1": 53.97, "conv2": 114.66, "conv3": 76.55, "conv4": 57.42, "conv5": 38.28}
 FC_GF = {"fc6": 2 * 256 * 9216 * 4096 / 1e9, "fc7": 2 * 256 * 4096 * 4096 / 1e9, "fc8": 2 * 256 * 4096 * 1000 / 1e9}
+# backward launch order per layer: data gradient first (nets.Net.dgrad_first, the default since
+# round 2's end; --wgrad-first for captures of the earlier schedule)
+_P = ("wgrad", "dgrad") if "--wgrad-first" in __import__("sys").argv else ("dgrad", "wgrad")
 ORDER = ([f"conv{i} fwd" for i in range(1, 6)] + ["fc6 fwd", "fc7 fwd", "fc8 fwd"] +
-         [f"{l} {p}" for l in ("fc8", "fc7", "fc6") for p in ("wgrad", "dgrad")] +
-         [f"conv{i} {p}" for i in (5, 4, 3, 2) for p in ("wgrad", "dgrad")] + ["conv1 wgrad"])
+         [f"{l} {p}" for l in ("fc8", "fc7", "fc6") for p in _P] +
+         [f"conv{i} {p}" for i in (5, 4, 3, 2) for p in _P] + ["conv1 wgrad"])
 
 COLS = {
     "time_us": ("gpu__time_duration.sum", 1e-3),
@@ -47,6 +50,7 @@ def main():
     ap.add_argument("raw")
     ap.add_argument("--launches", default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--wgrad-first", action="store_true", help="capture of the weight-gradient-first schedule")
     args = ap.parse_args()
     rows = list(csv.reader(open(args.raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
