@@ -256,6 +256,11 @@ caffe_status caffe_device_check(void);
 /* CAFFE_TUNE_BIAS_SPLIT_ROWS: rows (pixels x images) per split of the two-pass bias gradient, 8 ..
    1024 (default 64).  Deterministic; the FP32 summation order follows the split. */
 #define CAFFE_TUNE_BIAS_SPLIT_ROWS 29
+/* CAFFE_TUNE_PDL: 1 = the tensor-core GEMMs are launched with programmatic stream serialization, so
+   their prologue (barrier init, TMEM allocation, cluster sync) overlaps the end of the kernel before
+   them on the stream; they wait for it (griddepcontrol.wait) before touching global memory.
+   0 (default) = ordinary stream order.  Identical results. */
+#define CAFFE_TUNE_PDL 30
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

@@ -750,6 +750,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_halo_epi_groups = value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_PDL) {
+        cb::g_pdl = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_BIAS_SPLIT_ROWS) {
         if (value < 8 || value > 1024) return fail(CAFFE_E_PARAM, "bias split rows must be 8 .. 1024");
         cb::g_bias_split_rows = value;

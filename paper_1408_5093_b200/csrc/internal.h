@@ -112,6 +112,36 @@ struct TcLaunch {
 size_t tc_smem_bytes(const TcArgs& a);
 // instrumentation (abi.cu): every kernel launch of the library is counted.
 void note_launch();
+// CAFFE_TUNE_PDL: tensor-core GEMMs launched with programmatic stream serialization (their prologue --
+// barrier init, TMEM allocation, cluster sync -- overlaps the tail of the kernel before them; the
+// kernels wait on griddepcontrol.wait before touching global memory)
+extern int g_pdl;
+template <typename K, typename... Args>
+cudaError_t launch_tc(K kern, unsigned grid, unsigned threads, size_t smem, cudaStream_t s, int cluster,
+                      Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    unsigned na = 0;
+    if (cluster > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)cluster;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        na++;
+    }
+    if (g_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        na++;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 cudaError_t tc_launch(const TcLaunch& L, cudaStream_t s);
 cudaError_t tc_halo_launch(const TcLaunch& L, cudaStream_t s);
 cudaError_t tc_halo_wgrad_launch(const TcLaunch& L, cudaStream_t s);

@@ -271,6 +271,13 @@ __device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
         : "memory");
 }
 
+// Programmatic dependent launch: wait for the preceding kernel's completion (a no-op when this
+// kernel was launched without the attribute), then let the next kernel start its prologue.
+__device__ __forceinline__ void pdl_wait_and_trigger() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // One lane of the (converged) warp returns true.
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;

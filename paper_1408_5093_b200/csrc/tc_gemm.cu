@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(256, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    pdl_wait_and_trigger();
 
     if (warp == 0 && lane == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -369,30 +370,16 @@ int num_sms() {
     return n;
 }
 
+int g_pdl = 0;   // CAFFE_TUNE_PDL
+
 template <int ESZ, int AM, int BMd, int EP, int CG>
 static cudaError_t launch_one(const TcLaunch& L, cudaStream_t s) {
     auto kern = tc_gemm_kernel<ESZ, AM, BMd, EP, CG>;
     const size_t smem = tc_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (CG == 1) {
-        kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.mapC, L.mapV, L.mapWb, L.args);
-    } else {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(L.grid);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CG;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.mapC, L.mapV, L.mapWb, L.args);
-        if (e != cudaSuccess) return e;
-    }
+    e = launch_tc(kern, L.grid, 256, smem, s, CG, L.mapA, L.mapB, L.mapC, L.mapV, L.mapWb, L.args);
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
 }

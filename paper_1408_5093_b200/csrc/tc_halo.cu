@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(128 + 128 * NEG, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    pdl_wait_and_trigger();
 
     if (warp == 0 && lane == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(384, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    pdl_wait_and_trigger();
 
     if (warp == 0 && lane == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -659,19 +661,7 @@ cudaError_t tc_halo_jn_launch(const TcLaunch& L, cudaStream_t s) {
     const size_t smem = tc_halo_jn_smem_bytes(a, 5, 5, 48);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(L.grid);
-    cfg.blockDim = dim3(384);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.args);
+    e = launch_tc(kern, L.grid, 384, smem, s, 2, L.mapA, L.mapB, L.args);
     if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
@@ -739,6 +729,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    pdl_wait_and_trigger();
 
     auto decode = [&](int u, int& n_tile, int& mg, int& cb, int& g, int& t0, int& t1) {
         int t = u;
@@ -898,7 +889,8 @@ static cudaError_t halo_wgrad_launch_one(const TcLaunch& L, cudaStream_t s) {
     const size_t smem = tc_halo_wgrad_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<L.grid, 256, smem, s>>>(L.mapA, L.mapB, L.args);
+    e = launch_tc(kern, L.grid, 256, smem, s, 1, L.mapA, L.mapB, L.args);
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
 }
@@ -948,24 +940,8 @@ static cudaError_t halo_launch_one(const TcLaunch& L, cudaStream_t s) {
     const size_t smem = tc_halo_smem_bytes(L.args);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (CG == 1) {
-        kern<<<L.grid, threads, smem, s>>>(L.mapA, L.mapB, L.mapC, L.args);
-    } else {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(L.grid);
-        cfg.blockDim = dim3(threads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CG;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, L.mapA, L.mapB, L.mapC, L.args);
-        if (e != cudaSuccess) return e;
-    }
+    e = launch_tc(kern, L.grid, threads, smem, s, CG, L.mapA, L.mapB, L.mapC, L.args);
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
 }

@@ -264,3 +264,31 @@ def test_side_stream_weight_packs_bit_identical(mode):
     assert outs[0][0] == outs[1][0]
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
     np.testing.assert_array_equal(outs[0][2], outs[1][2])
+
+
+def test_pdl_launches_bit_identical():
+    """CAFFE_TUNE_PDL (tensor-core GEMMs launched with programmatic stream serialization; each waits
+    on griddepcontrol.wait before touching global memory) gives exactly the bits of ordinary stream
+    order: two eager steps and two graph replays of the CaffeNet step (batch 4, three streams)."""
+    import torch
+    from paper_1408_5093_b200 import _abi, nets
+    outs = []
+    try:
+        for pdl in (0, 1):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_PDL, pdl)
+            net = nets.Net(nets.CAFFENET, 4, nets.CAFFENET_INPUT, torch.device("cuda"), math="bf16", seed=0,
+                           input_i8=True)
+            net.a[0].copy_(torch.from_numpy(synth.int_pixels((4,) + tuple(nets.CAFFENET_INPUT), 9)).to(torch.int8))
+            net.labels.copy_(torch.from_numpy(synth.labels(4, 1000, 9)))
+            for _ in range(2):
+                net.step()
+            g = net.capture()
+            for _ in range(2):
+                g.replay()
+            torch.cuda.synchronize()
+            outs.append((float(net.loss), net.grads.cpu().numpy().copy(), net.params.cpu().numpy().copy()))
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_PDL, 0)
+    assert outs[0][0] == outs[1][0]
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[0][2], outs[1][2])
