@@ -261,6 +261,10 @@ caffe_status caffe_device_check(void);
    them on the stream; they wait for it (griddepcontrol.wait) before touching global memory.
    0 (default) = ordinary stream order.  Identical results. */
 #define CAFFE_TUNE_PDL 30
+/* CAFFE_TUNE_IP_FWD_SMALL_BN: N tile (64 or 128, default 128) of inner-product forwards with <= 1024
+   outputs (fc8: fewer split-K partials to reduce); 0 = the general rule.  Same result up to FP32
+   summation order. */
+#define CAFFE_TUNE_IP_FWD_SMALL_BN 31
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

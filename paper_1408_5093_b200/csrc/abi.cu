@@ -337,6 +337,11 @@ struct WgHalo {
     int Wt, TH, rows, tpi, total, ksteps, cblocks;  // tile geometry (output tile = TH rows x Wt columns)
     int BN, n_tiles, nch, acc_stride, macc, pairs, mgroups, splits, kb_per, slot, bchunk, stages;
 };
+// CAFFE_TUNE_IP_FWD_SMALL_BN: N tile of inner-product forwards with <= 1024 outputs (fc8: 8 N tiles x
+// 9 splits instead of 4 x 16 -- 9.4 instead of 16.8 MB of partials; GEMM + reduce 16.2 -> 12.4-12.8 us
+// alone, tools/fc8_probe.py; the forward runs alone on the GPU, so this is step time; the 4-run step
+// A/B was within its noise)
+int g_ip_fwd_small_bn = 128;
 int g_ip_max_splits = 0;   // CAFFE_TUNE_IP_MAX_SPLITS: cap on the inner-product split-K factor (0 = none)
 int g_wgrad_bn = 0;   // CAFFE_TUNE_WGRAD_BN: N tile of the halo weight gradient (0 = automatic)
 WgHalo wgrad_halo_plan(const Plan& p) {
@@ -748,6 +753,11 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
     if (key == CAFFE_TUNE_HALO_EPI_GROUPS) {
         if (value != 0 && (value < 2 || value > 4)) return fail(CAFFE_E_PARAM, "halo epilogue groups must be 0 (auto), 2, 3 or 4");
         g_halo_epi_groups = value;
+        return CAFFE_OK;
+    }
+    if (key == CAFFE_TUNE_IP_FWD_SMALL_BN) {
+        if (value != 0 && value != 64 && value != 128) return fail(CAFFE_E_PARAM, "small-output inner-product N tile must be 0, 64 or 128");
+        g_ip_fwd_small_bn = value;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_PDL) {
@@ -1544,7 +1554,7 @@ static IpPlan ip_plan(long long M, long long Ncols, long long Kred, int kchunk, 
     return q;
 }
 static IpPlan ip_plan_fwd(long long N, long long K, int O, int E) {
-    const int BN = choose_bn(O);
+    const int BN = (g_ip_fwd_small_bn > 0 && O <= 1024) ? g_ip_fwd_small_bn : choose_bn(O);
     return ip_plan(N, O, K, 128 / E, BN, E, (BN / 2) % 8 == 0);
 }
 static IpPlan ip_plan_dgrad(long long N, long long K, int O, int E) {
