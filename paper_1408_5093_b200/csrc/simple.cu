@@ -1695,6 +1695,51 @@ softmax_loss_kernel(const void* __restrict__ s, int sb, const int32_t* __restric
         // a label outside [0, K) is never read through: its row's loss term and diff are NaN
         const bool ok = (unsigned)lab < (unsigned)K;
         const float bad = ok ? 0.f : __int_as_float(0x7fc00000);
+        if (K <= 1024 && (K & 3) == 0 && !sb && db && ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(diff)) & 15) == 0) {
+            // FP32 scores, BF16 diff: lane l holds columns 4(l + 32q) .. +3 -- 16-byte loads, 8-byte
+            // stores; the same arithmetic per element as below
+            float v[32];
+            float mx = -INFINITY;
+            const float4* s4 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(s) + base);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int k4 = lane + 32 * q;
+                float4 f = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                if (4 * k4 < K) f = __ldg(s4 + k4);
+                v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+                mx = fmaxf(mx, fmaxf(fmaxf(f.x, f.y), fmaxf(f.z, f.w)));
+            }
+            for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            float se = 0.f;
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+                v[q] = (4 * (lane + 32 * (q >> 2)) + (q & 3) < K) ? expf(v[q] - mx) : 0.f;
+                se += v[q];
+            }
+            for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+            const float lse = logf(se);
+            if (lane == 0) my += ok ? lse - (reinterpret_cast<const float*>(s)[base + lab] - mx) : bad;
+            if (diff) {
+                const float inv = 1.f / N, rse = 1.f / se;
+                uint2* d2 = reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(diff) + base);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int k4 = lane + 32 * q;
+                    if (4 * k4 < K) {
+                        float p[4];
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            p[e] = v[4 * q + e] * rse;
+                            if (4 * k4 + e == lab) p[e] -= 1.f;
+                            p[e] = p[e] * inv + bad;
+                        }
+                        __nv_bfloat162 h0 = __floats2bfloat162_rn(p[0], p[1]), h1 = __floats2bfloat162_rn(p[2], p[3]);
+                        d2[k4] = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+                    }
+                }
+            }
+            continue;
+        }
         if (K <= 1024) {
             // the row lives in registers: one global read, one write
             float v[32];
