@@ -265,6 +265,10 @@ caffe_status caffe_device_check(void);
    outputs (fc8: fewer split-K partials to reduce); 0 = the general rule.  Same result up to FP32
    summation order. */
 #define CAFFE_TUNE_IP_FWD_SMALL_BN 31
+/* CAFFE_TUNE_POOL_LRN_C16: 1 (default) = caffe_pool_lrn_forward with C % 16 == 0 where C/8 does not
+   divide 32 (CaffeNet's 96-channel pool1/norm1) and an LRN window of <= 5 runs 16 channels per lane;
+   0 = 8 channels per lane.  Identical results. */
+#define CAFFE_TUNE_POOL_LRN_C16 32
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

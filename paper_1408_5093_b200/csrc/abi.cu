@@ -755,6 +755,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_halo_epi_groups = value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_POOL_LRN_C16) {
+        cb::g_pool_lrn_c16 = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_IP_FWD_SMALL_BN) {
         if (value != 0 && value != 64 && value != 128) return fail(CAFFE_E_PARAM, "small-output inner-product N tile must be 0, 64 or 128");
         g_ip_fwd_small_bn = value;

@@ -271,6 +271,7 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
 // fused CaffeNet pool (3x3/s2, full windows, U8 mask) + LRN, BF16 channels-last (simple.cu)
 bool pool_lrn_fusable(const PoolGeom& g, int size);
 extern int g_fused_rb;   // CAFFE_TUNE_FUSED_POOL_ROWS
+extern int g_pool_lrn_c16;   // CAFFE_TUNE_POOL_LRN_C16
 cudaError_t pool_lrn_fwd(const void* x, void* p, void* mask, void* y, const PoolGeom& g, int size, float alpha,
                          float beta, float k, cudaStream_t s);
 cudaError_t lrn_pool_bwd(const void* p, const void* dn, const void* mask, void* dx, int relu, const PoolGeom& g,

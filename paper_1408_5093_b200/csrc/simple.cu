@@ -1597,8 +1597,125 @@ static unsigned warps_grid(long long warps) {
     return (unsigned)std::max(1LL, std::min(b, cap));
 }
 
+// 16 channels per lane (C % 16 == 0, LRN window radius <= 2): C/16 lanes per pooled pixel (6 for
+// CaffeNet's 96-channel norm1: 5 pixels = 30 active lanes per warp, where the 8-channel form idles a
+// quarter of them), 18 window loads in flight per lane; the LRN window needs 2 channels from each
+// neighbouring lane (one bf16x2 word by shuffle).  Pool scan and LRN arithmetic as in the 8-channel
+// kernel (and the separate calls), so the bits are the same.
+__device__ __forceinline__ void pool9_scan8(const __nv_bfloat16* base, long long rs, int C, uint32_t (&bw)[4],
+                                            uint32_t (&aw)[4]) {
+    uint4 raw[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) raw[i][j] = __ldg(reinterpret_cast<const uint4*>(base + i * rs + j * C));
+    bw[0] = raw[0][0].x; bw[1] = raw[0][0].y; bw[2] = raw[0][0].z; bw[3] = raw[0][0].w;
+    aw[0] = aw[1] = aw[2] = aw[3] = 0u;
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            if (i == 0 && j == 0) continue;
+            const uint32_t vw[4] = {raw[i][j].x, raw[i][j].y, raw[i][j].z, raw[i][j].w};
+            const uint32_t pp = (uint32_t)(i * 3 + j) * 0x00010001u;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vw[e]),
+                                               *reinterpret_cast<const __nv_bfloat162*>(&bw[e]));
+                bw[e] = (vw[e] & m) | (bw[e] & ~m);
+                aw[e] = (pp & m) | (aw[e] & ~m);
+            }
+        }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256)
+pool_lrn_fwd_k3s2_c16(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ p, uint8_t* __restrict__ mask,
+                      __nv_bfloat16* __restrict__ y, PoolGeom g, int npix, float an, float beta, float k) {
+    static_assert(R <= 2, "two channels from each neighbouring lane");
+    const int cv = g.C / 16, ppw = 32 / cv;
+    const int lane = threadIdx.x & 31;
+    const int ps = lane / cv, vi = lane - ps * cv;
+    const int c0 = vi * 16;
+    const long long rs = (long long)g.W * g.C;
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int w0 = gw * ppw; w0 < npix; w0 += nw * ppw) {      // warp-uniform loop
+        const int pix = w0 + ps;
+        const bool act = ps < ppw && pix < npix;
+        uint32_t bw[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, aw[8];
+        if (act) {
+            int r = pix;
+            const int px = r % g.OW; r /= g.OW;
+            const int py = r % g.OH;
+            const int n = r / g.OH;
+            const __nv_bfloat16* base = x + (((long long)n * g.H + 2 * py) * g.W + 2 * px) * g.C + c0;
+            uint32_t b0[4], a0[4], b1[4], a1[4];
+            pool9_scan8(base, rs, g.C, b0, a0);
+            pool9_scan8(base + 8, rs, g.C, b1, a1);
+#pragma unroll
+            for (int e = 0; e < 4; e++) { bw[e] = b0[e]; bw[4 + e] = b1[e]; aw[e] = a0[e]; aw[4 + e] = a1[e]; }
+            const long long o = (long long)pix * g.C + c0;
+            uint4* po = reinterpret_cast<uint4*>(p + o);
+            po[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+            po[1] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
+            uint2* mo = reinterpret_cast<uint2*>(mask + o);
+            mo[0] = make_uint2(__byte_perm(aw[0], aw[1], 0x6420), __byte_perm(aw[2], aw[3], 0x6420));
+            mo[1] = make_uint2(__byte_perm(aw[4], aw[5], 0x6420), __byte_perm(aw[6], aw[7], 0x6420));
+        }
+        // channels c0-2, c0-1 (left lane's last word) and c0+16, c0+17 (right lane's first word)
+        uint32_t lw = __shfl_up_sync(0xffffffffu, bw[7], 1);
+        uint32_t rw = __shfl_down_sync(0xffffffffu, bw[0], 1);
+        if (vi == 0) lw = 0u;
+        if (vi == cv - 1) rw = 0u;
+        if (act) {
+            float xv[20];   // channels c0-2 .. c0+17
+            xv[0] = __uint_as_float(lw << 16);
+            xv[1] = __uint_as_float(lw & 0xffff0000u);
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                xv[2 + 2 * e] = __uint_as_float(bw[e] << 16);
+                xv[3 + 2 * e] = __uint_as_float(bw[e] & 0xffff0000u);
+            }
+            xv[18] = __uint_as_float(rw << 16);
+            xv[19] = __uint_as_float(rw & 0xffff0000u);
+            float out[16];
+#pragma unroll
+            for (int e = 0; e < 16; e++) {   // lrn_fwd8's arithmetic, element by element
+                float s2 = 0.f;
+#pragma unroll
+                for (int j = -R; j <= R; j++) s2 = fmaf(xv[2 + e + j], xv[2 + e + j], s2);
+                const float S = k + an * s2;
+                out[e] = xv[2 + e] * ex2_ftz(-beta * lg2_ftz(S));
+            }
+            float o8a[8], o8b[8];
+#pragma unroll
+            for (int e = 0; e < 8; e++) { o8a[e] = out[e]; o8b[e] = out[8 + e]; }
+            uint4* yo = reinterpret_cast<uint4*>(y + (long long)pix * g.C + c0);
+            yo[0] = pack8(o8a);
+            yo[1] = pack8(o8b);
+        }
+    }
+}
+int g_pool_lrn_c16 = 1;   // CAFFE_TUNE_POOL_LRN_C16
+
 cudaError_t pool_lrn_fwd(const void* x, void* p, void* mask, void* y, const PoolGeom& g, int size, float alpha,
                          float beta, float k, cudaStream_t s) {
+    if (g_pool_lrn_c16 && g.C % 16 == 0 && g.C / 16 <= 32 && 32 % (g.C / 8) != 0 && size <= 5) {
+        const int cv = g.C / 16, ppw = 32 / cv, npix = g.N * g.OH * g.OW;
+        const unsigned grid = warps_grid((npix + ppw - 1) / ppw);
+        const float an = alpha / size;
+        auto X = (const __nv_bfloat16*)x;
+        auto P = (__nv_bfloat16*)p;
+        auto Y = (__nv_bfloat16*)y;
+        auto M = (uint8_t*)mask;
+        switch ((size - 1) / 2) {
+            case 0: pool_lrn_fwd_k3s2_c16<0><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+            case 1: pool_lrn_fwd_k3s2_c16<1><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+            default: pool_lrn_fwd_k3s2_c16<2><<<grid, 256, 0, s>>>(X, P, M, Y, g, npix, an, beta, k); break;
+        }
+        note_launch();
+        return cudaGetLastError();
+    }
     const int cv = g.C / 8;
     if (cv > 32) return cudaErrorInvalidValue;
     const int ppw = 32 / cv, npix = g.N * g.OH * g.OW;

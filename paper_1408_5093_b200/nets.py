@@ -255,6 +255,7 @@ class Net:
     # (norm1 83 vs 134 us, norm2 57 vs 69 us) -- the fused kernel's per-lane LRN work per window
     # column needs ~120 registers, which caps it at 16 warps per SM, too few to hide its loads.
     fuse_pool_lrn = True
+    fuse_pool_lrn_c16 = True   # pool1/norm1 too, through the 16-channel-lane kernel
     fuse_lrn_pool_backward = False
 
     def _pool_lrn(self, i):
@@ -267,9 +268,10 @@ class Net:
         x = self.a[i]
         ok = (x.dtype == self.torch.bfloat16 and self.nhwc[i] and x.shape[1] % 8 == 0
               and 2 * (self.shapes[i + 1][2] - 1) + 3 <= x.shape[2] and x.shape[2] <= 2 * self.shapes[i + 1][2] + 1)
-        # the fused forward keeps every lane busy only when C/8 divides 32 (pool2/norm2, C = 256); with
-        # C = 96 a quarter of the lanes idle and the separate kernels are faster (48.5 vs 52 us)
-        return ok and (self.fuse_lrn_pool_backward or 32 % (x.shape[1] // 8) == 0)
+        # the 8-channel-lane fused forward keeps every lane busy only when C/8 divides 32 (pool2/norm2,
+        # C = 256); C = 96 (pool1/norm1) runs the 16-channel-lane form (CAFFE_TUNE_POOL_LRN_C16)
+        C = x.shape[1]
+        return ok and (self.fuse_lrn_pool_backward or 32 % (C // 8) == 0 or (self.fuse_pool_lrn_c16 and C % 16 == 0))
 
     # conv weight operands packed at the start of each step on a side stream (1: the forward
     # operands, 2: forward and data-gradient operands) into dedicated workspaces; the passes then

@@ -431,8 +431,8 @@ def test_blob_to_nchw(dt):
         cb.to_nchw(x, out=torch.empty((5, 256, 6, 5), dtype=d, device="cuda"))
 
 
-@pytest.mark.parametrize("shape", [(3, 96, 55, 55), (2, 256, 27, 27), (2, 16, 13, 13), (1, 8, 7, 9)],
-                         ids=["pool1norm1", "pool2norm2", "c16", "c8odd"])
+@pytest.mark.parametrize("shape", [(3, 96, 55, 55), (2, 256, 27, 27), (2, 16, 13, 13), (1, 8, 7, 9), (2, 160, 13, 15)],
+                         ids=["pool1norm1", "pool2norm2", "c16", "c8odd", "c160"])
 @pytest.mark.parametrize("relu", [True, False])
 @pytest.mark.parametrize("lrn", [(5, 1e-4, 0.75, 1.0), (3, 0.5, 0.75, 2.0)])
 def test_fused_pool_lrn_bit_identical(oracle, shape, relu, lrn):
