@@ -782,7 +782,8 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_I8_ROWS) {
-        cb::g_i8_rows = value ? 1 : 0;
+        if (value < 0 || value > 2) return fail(CAFFE_E_PARAM, "I8 pack form must be 0, 1 or 2");
+        cb::g_i8_rows = value;
         return CAFFE_OK;
     }
     if (key == CAFFE_TUNE_IP_MAX_SPLITS) {

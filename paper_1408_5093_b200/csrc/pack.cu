@@ -422,36 +422,62 @@ __device__ __forceinline__ void i8_seg12(const int8_t* p, bool whole, int nv, ui
         for (int i = 0; i < nv; i++) x[i >> 2] |= (uint32_t)(uint8_t)__ldg(p + i) << (8 * (i & 3));
     }
 }
-__global__ void pack_i8_px_kernel(const int8_t* __restrict__ src, __nv_bfloat16* __restrict__ dst, PackGeom g,
-                                  int total) {
+template <bool COAL>
+__global__ void __launch_bounds__(256) pack_i8_px_kernel(const int8_t* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                         PackGeom g, int total) {
     // (a thread per 16-byte chunk, chunks fastest, measured 76 us: runtime-indexed segment words spill)
+    // COAL: the warp's 32 packed pixels (3 KB, contiguous in the output) leave through a per-warp
+    // shared-memory transpose as lane-contiguous 16-byte stores; warp-uniform loop
+    __shared__ uint4 stg[COAL ? 8 : 1][COAL ? 32 * 6 + 1 : 1];
     const int8_t* src_end = src + (long long)g.N * g.H * g.W * 3;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        int r = t;
-        const int X = r % g.Wp; r /= g.Wp;
-        const int Y = r % g.Hp;
-        const int n = r / g.Hp;
-        const int nv = max(0, min(12, (g.W - X * 4) * 3));
-        uint32_t x[4][3];
-#pragma unroll
-        for (int dy = 0; dy < 4; dy++) {
-            const int h = Y * 4 + dy;
-            const int8_t* p = src + (((long long)n * g.H + h) * g.W + (long long)X * 4) * 3;
-            const int v = h < g.H ? nv : 0;
-            i8_seg12(p, v == 12 && p + 16 <= src_end, v, x[dy]);
-        }
+    const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int stride = gridDim.x * blockDim.x;
+    for (int tw = blockIdx.x * blockDim.x + (threadIdx.x & ~31); tw < total; tw += stride) {
+        const int t = tw + ln;
+        const bool act = t < total;
         uint32_t o[24];
 #pragma unroll
-        for (int k = 0; k < 24; k++) {   // channels 2k, 2k+1 = bytes of segment (2k)/12
-            const int k0 = 2 * k, k1 = k0 + 1;
-            const float a = (float)(int8_t)(x[k0 / 12][(k0 % 12) >> 2] >> (8 * ((k0 % 12) & 3)));
-            const float c = (float)(int8_t)(x[k1 / 12][(k1 % 12) >> 2] >> (8 * ((k1 % 12) & 3)));
-            __nv_bfloat162 bv = __floats2bfloat162_rn(a, c);
-            o[k] = *reinterpret_cast<uint32_t*>(&bv);
-        }
-        uint4* q = reinterpret_cast<uint4*>(dst + (long long)t * 48);
+        for (int k = 0; k < 24; k++) o[k] = 0u;
+        if (act) {
+            int r = t;
+            const int X = r % g.Wp; r /= g.Wp;
+            const int Y = r % g.Hp;
+            const int n = r / g.Hp;
+            const int nv = max(0, min(12, (g.W - X * 4) * 3));
+            uint32_t x[4][3];
 #pragma unroll
-        for (int j = 0; j < 6; j++) q[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            for (int dy = 0; dy < 4; dy++) {
+                const int h = Y * 4 + dy;
+                const int8_t* p = src + (((long long)n * g.H + h) * g.W + (long long)X * 4) * 3;
+                const int v = h < g.H ? nv : 0;
+                i8_seg12(p, v == 12 && p + 16 <= src_end, v, x[dy]);
+            }
+#pragma unroll
+            for (int k = 0; k < 24; k++) {   // channels 2k, 2k+1 = bytes of segment (2k)/12
+                const int k0 = 2 * k, k1 = k0 + 1;
+                const float a = (float)(int8_t)(x[k0 / 12][(k0 % 12) >> 2] >> (8 * ((k0 % 12) & 3)));
+                const float c = (float)(int8_t)(x[k1 / 12][(k1 % 12) >> 2] >> (8 * ((k1 % 12) & 3)));
+                __nv_bfloat162 bv = __floats2bfloat162_rn(a, c);
+                o[k] = *reinterpret_cast<uint32_t*>(&bv);
+            }
+        }
+        if constexpr (COAL) {
+#pragma unroll
+            for (int j = 0; j < 6; j++) stg[w][ln * 6 + j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            __syncwarp();
+            const int nval = min(32, total - tw);
+            uint4* q = reinterpret_cast<uint4*>(dst + (long long)tw * 48);
+#pragma unroll
+            for (int j = 0; j < 6; j++) {
+                const int c = j * 32 + ln;
+                if (c < nval * 6) q[c] = stg[w][c];
+            }
+            __syncwarp();
+        } else if (act) {
+            uint4* q = reinterpret_cast<uint4*>(dst + (long long)t * 48);
+#pragma unroll
+            for (int j = 0; j < 6; j++) q[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        }
     }
 }
 int g_i8_rows = 1;   // CAFFE_TUNE_I8_ROWS
@@ -461,7 +487,10 @@ cudaError_t pack_act_i8(const void* src, void* dst, const PackGeom& g, cudaStrea
     if (g_i8_rows && g.G == 1 && g.ph == 0 && g.pw == 0 && g.C == 3 && g.sh == 4 && g.sw == 4 && g.Ctot == 48 &&
         g.cpg == 48 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
         const int total = g.N * g.Hp * g.Wp;
-        pack_i8_px_kernel<<<blocks_for(total, 256), 256, 0, s>>>((const int8_t*)src, (__nv_bfloat16*)dst, g, total);
+        if (g_i8_rows == 2)
+            pack_i8_px_kernel<false><<<blocks_for(total, 256), 256, 0, s>>>((const int8_t*)src, (__nv_bfloat16*)dst, g, total);
+        else
+            pack_i8_px_kernel<true><<<blocks_for(total, 256), 256, 0, s>>>((const int8_t*)src, (__nv_bfloat16*)dst, g, total);
         note_launch();
         return cudaGetLastError();
     }

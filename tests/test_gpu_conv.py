@@ -581,7 +581,7 @@ def test_conv_stacked_halo(oracle, case, cta):
 @pytest.mark.parametrize("case", [CASES[3], (2, 3, 67, 67, 96, (11, 11), (4, 4), (0, 0), 1),
                                   (2, 4, 9, 9, 8, (3, 3), (1, 1), (1, 1), 1)],
                          ids=["conv1like", "conv1geom", "plain3x3"])
-@pytest.mark.parametrize("rows", [1, 0])
+@pytest.mark.parametrize("rows", [1, 2, 0])
 def test_conv_i8_bottom(oracle, case, rows):
     """An int8 channels-last image batch (CAFFE_I8) packed by caffe_conv_pack_bottom gives the same
     bits as the same integers stored in BF16, for the prepacked forward and weight gradient

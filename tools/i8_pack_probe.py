@@ -22,7 +22,7 @@ def main():
     ws = cb.conv_bottom_workspace(x.shape, w.shape, 4, 0, 1, "bf16", dev)
     mb = (x.numel() + 256 * 57 * 57 * 48 * 2) / 1e6
     res = {}
-    for r in (0, 1, 0, 1):
+    for r in (0, 1, 2, 0, 1, 2):
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_I8_ROWS, r)
         t = timeit(lambda: cb.conv_pack_bottom(x, w, 4, 0, 1, "bf16", ws=ws))
         torch.cuda.synchronize()
