@@ -269,6 +269,10 @@ caffe_status caffe_device_check(void);
    divide 32 (CaffeNet's 96-channel pool1/norm1) and an LRN window of <= 5 runs 16 channels per lane;
    0 = 8 channels per lane.  Identical results. */
 #define CAFFE_TUNE_POOL_LRN_C16 32
+/* CAFFE_TUNE_LRN_BWD_C16: 1 (default) = the BF16 channels-last LRN backward with C % 16 == 0 runs 16
+   channels per lane (own channels loaded once, neighbours by shuffle); 0 = 8 channels per thread
+   with the neighbouring vectors loaded.  Identical results. */
+#define CAFFE_TUNE_LRN_BWD_C16 33
 caffe_status caffe_set_tuning(int32_t key, int32_t value);
 
 /* ------------------------------------------------------------------ instrumentation

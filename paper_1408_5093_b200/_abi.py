@@ -56,6 +56,7 @@ CAFFE_TUNE_BIAS_SPLIT_ROWS = 29
 CAFFE_TUNE_PDL = 30
 CAFFE_TUNE_IP_FWD_SMALL_BN = 31
 CAFFE_TUNE_POOL_LRN_C16 = 32
+CAFFE_TUNE_LRN_BWD_C16 = 33
 CAFFE_ELTWISE_PROD, CAFFE_ELTWISE_SUM, CAFFE_ELTWISE_MAX = 0, 1, 2
 CAFFE_ELTWISE_MAX_INPUTS = 8
 CAFFE_LR_FIXED, CAFFE_LR_STEP, CAFFE_LR_INV = 0, 1, 2

@@ -755,6 +755,10 @@ caffe_status caffe_set_tuning(int32_t key, int32_t value) {
         g_halo_epi_groups = value;
         return CAFFE_OK;
     }
+    if (key == CAFFE_TUNE_LRN_BWD_C16) {
+        cb::g_lrn_bwd_c16 = value ? 1 : 0;
+        return CAFFE_OK;
+    }
     if (key == CAFFE_TUNE_POOL_LRN_C16) {
         cb::g_pool_lrn_c16 = value ? 1 : 0;
         return CAFFE_OK;

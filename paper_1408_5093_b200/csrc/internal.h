@@ -272,6 +272,7 @@ cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* s
 bool pool_lrn_fusable(const PoolGeom& g, int size);
 extern int g_fused_rb;   // CAFFE_TUNE_FUSED_POOL_ROWS
 extern int g_pool_lrn_c16;   // CAFFE_TUNE_POOL_LRN_C16
+extern int g_lrn_bwd_c16;   // CAFFE_TUNE_LRN_BWD_C16
 cudaError_t pool_lrn_fwd(const void* x, void* p, void* mask, void* y, const PoolGeom& g, int size, float alpha,
                          float beta, float k, cudaStream_t s);
 cudaError_t lrn_pool_bwd(const void* p, const void* dn, const void* mask, void* dx, int relu, const PoolGeom& g,

@@ -1387,10 +1387,89 @@ __global__ void lrn_bwd_kernel(const void* __restrict__ x, const void* __restric
     }
 }
 
+// BF16 channels-last LRN backward with 16 channels per lane (C % 16 == 0, C/16 <= 32): a lane loads
+// only its own 16 channels of x and dy (the 8-channel kernel loads 24 of each, neighbours included)
+// and takes the neighbouring 8-channel vectors from the adjacent lanes of the same pixel by shuffle;
+// each 8-channel half then goes through lrn_bwd8 with exactly the 24 channels the 8-channel kernel
+// would have loaded (zero outside [0, C)) -- the same bits.
+__device__ __forceinline__ void unpack_words8(const uint32_t* w, float* f) {
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        f[2 * e] = __uint_as_float(w[e] << 16);
+        f[2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+    }
+}
+template <int R>
+__global__ void __launch_bounds__(256) lrn_bwd_c16(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
+                                                   __nv_bfloat16* __restrict__ dx, int C, int npix, float an, float beta,
+                                                   float k, float cb) {
+    const int cv = C / 16, ppw = 32 / cv;
+    const int lane = threadIdx.x & 31;
+    const int ps = lane / cv, vi = lane - ps * cv;
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int w0 = gw * ppw; w0 < npix; w0 += nw * ppw) {      // warp-uniform loop
+        const int pix = w0 + ps;
+        const bool act = ps < ppw && pix < npix;
+        uint32_t xw[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, gw8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        const long long o = (long long)pix * C + vi * 16;
+        if (act) {
+            const uint4* xp = reinterpret_cast<const uint4*>(x + o);
+            const uint4* gp = reinterpret_cast<const uint4*>(dy + o);
+            const uint4 x0 = __ldg(xp), x1 = __ldg(xp + 1), g0 = __ldg(gp), g1 = __ldg(gp + 1);
+            xw[0] = x0.x; xw[1] = x0.y; xw[2] = x0.z; xw[3] = x0.w; xw[4] = x1.x; xw[5] = x1.y; xw[6] = x1.z; xw[7] = x1.w;
+            gw8[0] = g0.x; gw8[1] = g0.y; gw8[2] = g0.z; gw8[3] = g0.w; gw8[4] = g1.x; gw8[5] = g1.y; gw8[6] = g1.z; gw8[7] = g1.w;
+        }
+        uint32_t xl[4], xr[4], gl[4], gr[4];   // the left lane's upper 8 channels, the right lane's lower 8
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            xl[e] = __shfl_up_sync(0xffffffffu, xw[4 + e], 1);
+            gl[e] = __shfl_up_sync(0xffffffffu, gw8[4 + e], 1);
+            xr[e] = __shfl_down_sync(0xffffffffu, xw[e], 1);
+            gr[e] = __shfl_down_sync(0xffffffffu, gw8[e], 1);
+        }
+        if (vi == 0) { xl[0] = xl[1] = xl[2] = xl[3] = 0u; gl[0] = gl[1] = gl[2] = gl[3] = 0u; }
+        if (vi == cv - 1) { xr[0] = xr[1] = xr[2] = xr[3] = 0u; gr[0] = gr[1] = gr[2] = gr[3] = 0u; }
+        if (act) {
+            float xv[24], gv[24], out[8];
+            // half 0: channels c0-8 .. c0+15
+            unpack_words8(xl, xv); unpack_words8(xw, xv + 8); unpack_words8(xw + 4, xv + 16);
+            unpack_words8(gl, gv); unpack_words8(gw8, gv + 8); unpack_words8(gw8 + 4, gv + 16);
+            lrn_bwd8<R>(xv, gv, an, beta, k, cb, out);
+            uint4* d = reinterpret_cast<uint4*>(dx + o);
+            d[0] = pack8(out);
+            // half 1: channels c0 .. c0+23
+            unpack_words8(xw, xv); unpack_words8(xw + 4, xv + 8); unpack_words8(xr, xv + 16);
+            unpack_words8(gw8, gv); unpack_words8(gw8 + 4, gv + 8); unpack_words8(gr, gv + 16);
+            lrn_bwd8<R>(xv, gv, an, beta, k, cb, out);
+            d[1] = pack8(out);
+        }
+    }
+}
+int g_lrn_bwd_c16 = 1;   // CAFFE_TUNE_LRN_BWD_C16
+
 cudaError_t lrn_bwd(const void* x, const void* y, const void* dy, const float* scale, void* dx, int bf16, int nhwc,
                     int N, int C, int H, int W, int size, float alpha, float beta, float k, cudaStream_t s) {
     const int total = N * C * H * W;
     const int sc = nhwc ? 1 : H * W;
+    if (g_lrn_bwd_c16 && nhwc && bf16 && C % 16 == 0 && C / 16 <= 32 && size <= 9 && nhwc8_ok(x, y, C) &&
+        nhwc8_ok(dy, dx, C)) {
+        const int cv = C / 16, ppw = 32 / cv, npix = N * H * W;
+        const long long warps = (npix + ppw - 1) / ppw;
+        const unsigned grid = (unsigned)std::max(1LL, std::min((warps * 32 + 255) / 256, 148LL * 16));
+        const float an = alpha / size, cbv = 2.f * an * beta;
+        auto X = (const __nv_bfloat16*)x;
+        auto G = (const __nv_bfloat16*)dy;
+        auto D = (__nv_bfloat16*)dx;
+        switch ((size - 1) / 2) {
+            case 0: lrn_bwd_c16<0><<<grid, 256, 0, s>>>(X, G, D, C, npix, an, beta, k, cbv); break;
+            case 1: lrn_bwd_c16<1><<<grid, 256, 0, s>>>(X, G, D, C, npix, an, beta, k, cbv); break;
+            case 2: lrn_bwd_c16<2><<<grid, 256, 0, s>>>(X, G, D, C, npix, an, beta, k, cbv); break;
+            case 3: lrn_bwd_c16<3><<<grid, 256, 0, s>>>(X, G, D, C, npix, an, beta, k, cbv); break;
+            default: lrn_bwd_c16<4><<<grid, 256, 0, s>>>(X, G, D, C, npix, an, beta, k, cbv); break;
+        }
+        note_launch();
+        return cudaGetLastError();
+    }
     if (nhwc && nhwc8_ok(x, y, C) && nhwc8_ok(dy, dx, C) && size <= 9) {
         const int tv = total / 8;
         const unsigned nb = nblk(tv, 256);

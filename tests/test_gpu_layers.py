@@ -567,3 +567,29 @@ def test_ip_bias_grad_one_pass(oracle, N, O):
             assert_fp32_close(got[0], ref, f"ip db bias_rows={v}")
     finally:
         _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_BIAS_ROWS, 0)
+
+
+@pytest.mark.parametrize("shape", [(2, 96, 27, 27), (2, 256, 13, 13), (3, 16, 5, 7), (1, 160, 6, 6)])
+@pytest.mark.parametrize("size", [5, 3, 9])
+def test_lrn_backward_c16_bit_identical(oracle, shape, size):
+    """The 16-channel-lane BF16 LRN backward (CAFFE_TUNE_LRN_BWD_C16, neighbours by shuffle) writes
+    exactly the bits of the 8-channel kernel, and meets the BF16 bar against the oracle."""
+    import torch
+    import paper_1408_5093_b200 as cb
+    from paper_1408_5093_b200 import _abi
+    cl = torch.channels_last
+    x = oracle.quant_bf16(synth.uniform(shape, 23, synth.S_X) * 3)
+    g = oracle.quant_bf16(synth.uniform(shape, 23, synth.S_DY))
+    xd = cuda(x).to(torch.bfloat16).contiguous(memory_format=cl)
+    gd = cuda(g).to(torch.bfloat16).contiguous(memory_format=cl)
+    y = cb.lrn_forward(xd, local_size=size)
+    outs = []
+    try:
+        for v in (1, 0):
+            _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_LRN_BWD_C16, v)
+            outs.append(host(cb.lrn_backward(xd, y, gd, local_size=size).float()))
+    finally:
+        _abi.call("caffe_set_tuning", _abi.CAFFE_TUNE_LRN_BWD_C16, 1)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    ref = oracle.lrn_backward(x.astype(np.float64), g.astype(np.float64), size=size, alpha=1e-4, beta=0.75, k=1.0)
+    assert_bf16_ulp(outs[0], ref, f"lrn bwd c16 size={size}", atol=float(np.abs(ref).max()) * 2.0 ** -16)
